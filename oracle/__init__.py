@@ -1,0 +1,296 @@
+"""ctypes loader for the CPU oracle (oracle/ader_oracle.c).
+
+TEST INFRASTRUCTURE ONLY: only tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / --impl reference legs may import this package.  The product
+path (paper_1212_3585_b200/) never imports it.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB = None
+
+EULER, MHD = 0, 1
+PERIODIC, TRANSMISSIVE = 0, 1
+
+IC_FN = C.CFUNCTYPE(None, C.POINTER(C.c_double), C.c_int64, C.POINTER(C.c_double), C.c_void_p)
+
+
+class OrcConfig(C.Structure):
+    _fields_ = [
+        ("dim", C.c_int32), ("system", C.c_int32), ("degree", C.c_int32),
+        ("n", C.c_int32 * 3), ("lo", C.c_double * 3), ("hi", C.c_double * 3),
+        ("bc", C.c_int32 * 6),
+        ("gamma", C.c_double), ("ch", C.c_double), ("cfl", C.c_double),
+        ("pred_tol", C.c_double), ("pred_max_sweeps", C.c_int32),
+        ("ic_quad", C.c_int32),
+        ("refine_factor", C.c_int32), ("lmax", C.c_int32),
+        ("chi_ref", C.c_double), ("chi_rec", C.c_double), ("chi_eps", C.c_double),
+    ]
+
+
+class OrcReport(C.Structure):
+    _fields_ = [
+        ("t", C.c_double), ("dt", C.c_double),
+        ("steps", C.c_int64), ("cell_updates", C.c_int64), ("sweeps_total", C.c_int64),
+        ("sweeps_max", C.c_int32), ("updates_per_level", C.c_int64 * 8),
+    ]
+
+
+def build():
+    src = os.path.join(_HERE, "ader_oracle.c")
+    so = os.path.join(_HERE, "liboracle.so")
+    if (not os.path.exists(so)) or os.path.getmtime(so) < max(
+            os.path.getmtime(src), os.path.getmtime(os.path.join(_HERE, "ader_oracle.h"))):
+        subprocess.check_call(["make", "-s", "-C", _HERE, "liboracle.so"])
+    return so
+
+
+def lib():
+    global _LIB
+    if _LIB is None:
+        _LIB = C.CDLL(build())
+        L = _LIB
+        dp = C.POINTER(C.c_double)
+        ip = C.POINTER(C.c_int)
+        L.orc_create.restype = C.c_void_p
+        L.orc_create.argtypes = [C.POINTER(OrcConfig)]
+        L.orc_destroy.argtypes = [C.c_void_p]
+        L.orc_last_error.restype = C.c_char_p
+        L.orc_last_error.argtypes = [C.c_void_p]
+        L.orc_set_initial.argtypes = [C.c_void_p, IC_FN, C.c_void_p]
+        L.orc_set_cells.argtypes = [C.c_void_p, dp]
+        L.orc_get_cells.argtypes = [C.c_void_p, dp]
+        L.orc_time.restype = C.c_double
+        L.orc_time.argtypes = [C.c_void_p]
+        L.orc_num_cells.restype = C.c_int64
+        L.orc_num_cells.argtypes = [C.c_void_p]
+        L.orc_compute_dt.restype = C.c_double
+        L.orc_compute_dt.argtypes = [C.c_void_p]
+        L.orc_step.argtypes = [C.c_void_p, C.c_double, C.c_int64, C.POINTER(OrcReport)]
+        L.orc_advance_box.argtypes = [C.c_void_p, C.c_double, C.POINTER(C.c_int32),
+                                      C.POINTER(C.c_int32), dp, C.POINTER(OrcReport)]
+        L.orc_dump_recon.argtypes = [C.c_void_p, dp]
+        L.orc_dump_pred.argtypes = [C.c_void_p, C.c_double, dp]
+        L.orc_dump_flux.argtypes = [C.c_void_p, C.c_double, dp]
+        L.orc_nvar.argtypes = [C.c_int, C.c_int]
+        L.orc_basis_tables.argtypes = [C.c_int] + [dp] * 5 + [dp, ip, ip, dp] + [dp] * 3
+        L.orc_predictor_matrices.argtypes = [C.c_int, C.c_int, dp, dp, dp]
+        L.orc_weno_1d.argtypes = [C.c_int, dp, dp]
+        L.orc_reconstruct_box.argtypes = [C.c_int, C.c_int, C.c_int, dp, dp]
+        L.orc_predict_cell.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
+                                       dp, dp, C.c_double, C.c_int, dp, ip]
+        L.orc_face_flux.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
+                                    C.c_int, dp, dp, dp]
+        L.orc_phys_flux.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, dp, C.c_int, dp]
+        L.orc_max_speed.restype = C.c_double
+        L.orc_max_speed.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, dp, C.c_int]
+        L.orc_rusanov.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, dp, dp, C.c_int, dp]
+        L.orc_prim_to_cons.argtypes = [C.c_int, C.c_int, C.c_double, dp, dp]
+    return _LIB
+
+
+def _p(a):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def nvar(system, dim):
+    return lib().orc_nvar(system, dim)
+
+
+def tables(M):
+    N = M + 1
+    lam, w, p0, p1 = (np.zeros(N) for _ in range(4))
+    Sig = np.zeros((N, N))
+    rec = np.zeros((4, N, N))
+    L = np.zeros(4, dtype=np.int32)
+    R = np.zeros(4, dtype=np.int32)
+    lin = np.zeros(4)
+    M1, Kx1, K1t = (np.zeros((N, N)) for _ in range(3))
+    ip = C.POINTER(C.c_int)
+    nS = lib().orc_basis_tables(M, _p(lam), _p(w), _p(p0), _p(p1), _p(Sig), _p(rec),
+                                L.ctypes.data_as(ip), R.ctypes.data_as(ip), _p(lin),
+                                _p(M1), _p(Kx1), _p(K1t))
+    return dict(lam=lam, w=w, psi0=p0, psi1=p1, Sigma=Sig, rec=rec[:nS], L=L[:nS], R=R[:nS],
+                lin=lin[:nS], M1=M1, Kx1=Kx1, K1t=K1t, nS=nS)
+
+
+def predictor_matrices(d, M):
+    N = M + 1
+    NS, NST = N ** d, N ** (d + 1)
+    K1 = np.zeros((NST, NST))
+    Kd = np.zeros((d, NST, NST))
+    F0 = np.zeros((NST, NS))
+    lib().orc_predictor_matrices(d, M, _p(K1), _p(Kd), _p(F0))
+    return K1, Kd, F0
+
+
+def weno_1d(M, win):
+    win = np.ascontiguousarray(win, dtype=np.float64)
+    out = np.zeros(M + 1)
+    lib().orc_weno_1d(M, _p(win), _p(out))
+    return out
+
+
+def reconstruct_box(d, M, nv, ubox):
+    ubox = np.ascontiguousarray(ubox, dtype=np.float64)
+    w = np.zeros((nv, (M + 1) ** d))
+    rc = lib().orc_reconstruct_box(d, M, nv, _p(ubox), _p(w))
+    assert rc == 0
+    return w
+
+
+def predict_cell(d, M, system, gamma, ch, w, dtdx, tol=1e-13, max_sweeps=32):
+    w = np.ascontiguousarray(w, dtype=np.float64)
+    nv = w.shape[0]
+    q = np.zeros((nv, (M + 1) ** (d + 1)))
+    dtdx = np.ascontiguousarray(dtdx, dtype=np.float64)
+    sw = C.c_int(0)
+    rc = lib().orc_predict_cell(d, M, system, gamma, ch, _p(w), _p(dtdx), tol, max_sweeps,
+                                _p(q), C.byref(sw))
+    return rc, q, sw.value
+
+
+def face_flux(d, M, system, gamma, ch, direction, qL, qR):
+    qL = np.ascontiguousarray(qL, dtype=np.float64)
+    qR = np.ascontiguousarray(qR, dtype=np.float64)
+    F = np.zeros(qL.shape[0])
+    rc = lib().orc_face_flux(d, M, system, gamma, ch, direction, _p(qL), _p(qR), _p(F))
+    assert rc == 0
+    return F
+
+
+def phys_flux(system, dim, gamma, ch, u, direction):
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    f = np.zeros(len(u))
+    rc = lib().orc_phys_flux(system, dim, gamma, ch, _p(u), direction, _p(f))
+    assert rc == 0
+    return f
+
+
+def max_speed(system, dim, gamma, ch, u, direction):
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    return lib().orc_max_speed(system, dim, gamma, ch, _p(u), direction)
+
+
+def rusanov(system, dim, gamma, ch, uL, uR, direction):
+    uL = np.ascontiguousarray(uL, dtype=np.float64)
+    uR = np.ascontiguousarray(uR, dtype=np.float64)
+    f = np.zeros(len(uL))
+    rc = lib().orc_rusanov(system, dim, gamma, ch, _p(uL), _p(uR), direction, _p(f))
+    assert rc == 0
+    return f
+
+
+def prim_to_cons(system, dim, gamma, prim):
+    prim = np.zeros(9) + np.asarray(list(prim) + [0.0] * (9 - len(prim)), dtype=np.float64)
+    u = np.zeros(nvar(system, dim))
+    lib().orc_prim_to_cons(system, dim, gamma, _p(prim), _p(u))
+    return u
+
+
+class Oracle:
+    """Uniform-grid oracle run (level 0 only)."""
+
+    def __init__(self, *, dim, system=EULER, degree, n, lo, hi, bc, gamma=1.4, ch=0.0,
+                 cfl=0.9, pred_tol=1e-13, pred_max_sweeps=32, ic_quad=0):
+        cfg = OrcConfig()
+        cfg.dim, cfg.system, cfg.degree = dim, system, degree
+        n = list(n) + [1] * (3 - len(n))
+        lo = list(lo) + [0.0] * (3 - len(lo))
+        hi = list(hi) + [1.0] * (3 - len(hi))
+        for k in range(3):
+            cfg.n[k], cfg.lo[k], cfg.hi[k] = n[k], lo[k], hi[k]
+        bc = list(bc) + [0] * (6 - len(bc))
+        for k in range(6):
+            cfg.bc[k] = bc[k]
+        cfg.gamma, cfg.ch, cfg.cfl = gamma, ch, cfl
+        cfg.pred_tol, cfg.pred_max_sweeps, cfg.ic_quad = pred_tol, pred_max_sweeps, ic_quad
+        self.cfg = cfg
+        self.dim, self.degree, self.system = dim, degree, system
+        self.n = n[:dim]
+        self.nv = nvar(system, dim)
+        self.ptr = lib().orc_create(C.byref(cfg))
+        if not self.ptr:
+            raise ValueError("orc_create rejected the configuration")
+
+    def __del__(self):
+        if getattr(self, "ptr", None):
+            lib().orc_destroy(self.ptr)
+            self.ptr = None
+
+    @property
+    def ncells(self):
+        return int(np.prod(self.n))
+
+    def error(self):
+        return lib().orc_last_error(self.ptr).decode()
+
+    def set_initial(self, ic):
+        """ic(x[n,3]) -> prim[n,9] (numpy)."""
+        def cb(xp, n, pp, user):
+            x = np.ctypeslib.as_array(xp, shape=(n, 3))
+            p = np.ctypeslib.as_array(pp, shape=(n, 9))
+            p[:] = ic(x)
+        self._cb = IC_FN(cb)
+        rc = lib().orc_set_initial(self.ptr, self._cb, None)
+        assert rc == 0
+
+    def set_cells(self, u):
+        u = np.ascontiguousarray(u, dtype=np.float64).reshape(self.ncells, self.nv)
+        lib().orc_set_cells(self.ptr, _p(u))
+
+    def get_cells(self):
+        u = np.zeros((self.ncells, self.nv))
+        lib().orc_get_cells(self.ptr, _p(u))
+        return u
+
+    @property
+    def t(self):
+        return lib().orc_time(self.ptr)
+
+    def compute_dt(self):
+        return lib().orc_compute_dt(self.ptr)
+
+    def step(self, t_end=1e300, max_steps=1):
+        rep = OrcReport()
+        rc = lib().orc_step(self.ptr, t_end, max_steps, C.byref(rep))
+        if rc:
+            raise RuntimeError(f"oracle step failed ({rc}): {self.error()}")
+        return rep
+
+    def advance_box(self, dt, blo, bhi):
+        blo = (list(blo) + [0, 0, 0])[:3]
+        bhi = (list(bhi) + [1, 1, 1])[:3]
+        a = (C.c_int32 * 3)(*blo)
+        b = (C.c_int32 * 3)(*bhi)
+        nb = int(np.prod([bhi[k] - blo[k] for k in range(self.dim)]))
+        out = np.zeros((nb, self.nv))
+        rep = OrcReport()
+        rc = lib().orc_advance_box(self.ptr, dt, a, b, _p(out), C.byref(rep))
+        if rc:
+            raise RuntimeError(f"oracle advance_box failed: {self.error()}")
+        return out, rep
+
+    def dump_recon(self):
+        w = np.zeros((self.ncells, self.nv, (self.degree + 1) ** self.dim))
+        lib().orc_dump_recon(self.ptr, _p(w))
+        return w
+
+    def dump_pred(self, dt):
+        q = np.zeros((self.ncells, self.nv, (self.degree + 1) ** (self.dim + 1)))
+        rc = lib().orc_dump_pred(self.ptr, dt, _p(q))
+        assert rc == 0, self.error()
+        return q
+
+    def dump_flux(self, dt):
+        e = [k + 1 for k in self.n] + ([1] if self.dim == 2 else [])
+        F = np.zeros((self.dim, int(np.prod(e)), self.nv))
+        rc = lib().orc_dump_flux(self.ptr, dt, _p(F))
+        assert rc == 0, self.error()
+        return F

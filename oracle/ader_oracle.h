@@ -1,0 +1,116 @@
+/*
+ * ader_oracle.h — CPU ORACLE of the ADER-WENO hot path (arXiv:1212.3585).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load, call or link
+ * anything under oracle/.  The product path (paper_1212_3585_b200/) never
+ * does, and shares no code, header, table or helper with this file.
+ *
+ * Citation format: "P:a-b" = lines a..b of PAPER.md (the LaTeX source of the
+ * paper), with the section / equation label they fall in.
+ *
+ * All arithmetic is IEEE FP64, single threaded, compiled with
+ * -O2 -ffp-contract=off (no FMA contraction, no fast-math).
+ */
+#ifndef ADER_ORACLE_H
+#define ADER_ORACLE_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ORC_MAXN 5            /* nodes per axis, N = M+1 <= 5                */
+#define ORC_MAXV 9            /* conserved variables (MHD-GLM)               */
+
+enum { ORC_EULER = 0, ORC_MHD = 1 };
+enum { ORC_BC_PERIODIC = 0, ORC_BC_TRANSMISSIVE = 1 };
+
+typedef struct {
+  int32_t dim, system, degree;       /* d in {2,3}; M in {2,3}              */
+  int32_t n[3];                      /* level-0 cells per axis (n[2]=1, d=2) */
+  double lo[3], hi[3];
+  int32_t bc[6];                     /* -x,+x,-y,+y,-z,+z                   */
+  double gamma, ch, cfl;
+  double pred_tol; int32_t pred_max_sweeps;
+  int32_t ic_quad;                   /* GL points per axis for IC averages   */
+  /* AMR (used by the AMR oracle; lmax = 0 means uniform grid) */
+  int32_t refine_factor, lmax;
+  double chi_ref, chi_rec, chi_eps;
+} orc_config;
+
+/* Batched initial-condition callback: x[n][3] -> prim[n][9]
+ * prim = (rho, vx, vy, vz, p, Bx, By, Bz, psi); Euler reads the first 5. */
+typedef void (*orc_ic_fn)(const double* x, int64_t n, double* prim, void* user);
+
+typedef struct orc_ctx orc_ctx;
+
+typedef struct {
+  double t, dt;
+  int64_t steps, cell_updates, sweeps_total;
+  int32_t sweeps_max;
+  int64_t updates_per_level[8];
+} orc_report;
+
+/* ---- tables / pure per-cell numerics (for pins) ---------------------- */
+int  orc_nvar(int system, int dim);
+/* Basis tables for degree M.  Any pointer may be NULL.
+ * lam,w [N]; psi0,psi1 [N]; Sigma [N*N]; rec [nS*N*N] (rec[s][p][o]);
+ * stencil L,R,lin [nS]; M1,Kx1,K1t [N*N] row-major [test][trial]; returns nS. */
+int  orc_basis_tables(int M, double* lam, double* w, double* psi0, double* psi1,
+                      double* Sigma, double* rec, int* L, int* R, double* lin,
+                      double* M1, double* Kx1, double* K1t);
+/* Dense predictor operators (eqn.pde.weak4 @ P:451-459) for (d, M):
+ * NST = N^(d+1), NS = N^d.  K1 [NST*NST], Kdir [d][NST*NST], F0 [NST*NS]. */
+int  orc_predictor_matrices(int d, int M, double* K1, double* Kdir, double* F0);
+void orc_weno_1d(int M, const double* win, double* out);
+/* Dimension-by-dimension WENO of one cell from its (2M+1)^d box of cell
+ * averages ubox[box][nv] (x fastest) -> w[nv][N^d] (x fastest). */
+int  orc_reconstruct_box(int d, int M, int nv, const double* ubox, double* w);
+/* Space-time predictor (eqn.stdg.final @ P:463-474): w[nv][N^d] ->
+ * q[nv][N^(d+1)] (space fastest, time slowest).  dtdx[d] = dt/dx_dir.
+ * Returns 0 on success, 3 on non-convergence or inadmissible state. */
+int  orc_predict_cell(int d, int M, int system, double gamma, double ch,
+                      const double* w, const double* dtdx, double tol, int max_sweeps,
+                      double* q, int* sweeps);
+/* Space-time Rusanov face flux (flux:F/G/H @ P:158-172, eqn.rusanov @ P:181-185)
+ * between the left (lower) cell qL and right (upper) cell qR along dir. */
+int  orc_face_flux(int d, int M, int system, double gamma, double ch, int dir,
+                   const double* qL, const double* qR, double* F);
+int  orc_phys_flux(int system, int dim, double gamma, double ch, const double* u, int dir, double* f);
+double orc_max_speed(int system, int dim, double gamma, double ch, const double* u, int dir);
+int  orc_rusanov(int system, int dim, double gamma, double ch, const double* uL,
+                 const double* uR, int dir, double* f);
+void orc_prim_to_cons(int system, int dim, double gamma, const double* prim, double* u);
+
+/* ---- uniform-grid driver --------------------------------------------- */
+orc_ctx* orc_create(const orc_config* cfg);
+void     orc_destroy(orc_ctx* c);
+const char* orc_last_error(const orc_ctx* c);
+int  orc_set_initial(orc_ctx* c, orc_ic_fn ic, void* user);
+/* Interior cell averages, u[cell][nv], cells x fastest then y then z. */
+int  orc_set_cells(orc_ctx* c, const double* u);
+int  orc_get_cells(const orc_ctx* c, double* u);
+double orc_time(const orc_ctx* c);
+int64_t orc_num_cells(const orc_ctx* c);
+/* CFL time step of the current state (O2), before clipping. */
+double orc_compute_dt(orc_ctx* c);
+/* Whole steps until t_end or max_steps. */
+int  orc_step(orc_ctx* c, double t_end, int64_t max_steps, orc_report* rep);
+/* One step of size dt computed only for the interior box [blo,bhi) (cell
+ * indices); writes the new averages of the box to out[box cells][nv]
+ * (x fastest) and leaves the state untouched.  Used for sampled parity. */
+int  orc_advance_box(orc_ctx* c, double dt, const int32_t* blo, const int32_t* bhi,
+                     double* out, orc_report* rep);
+/* Debug: reconstruction / predictor of the interior cells with the current
+ * state and step dt.  w[cell][nv][N^d], q[cell][nv][N^(d+1)]. */
+int  orc_dump_recon(orc_ctx* c, double* w);
+int  orc_dump_pred(orc_ctx* c, double dt, double* q);
+/* Debug: face fluxes F[dir][cell][nv] on the lower face of every interior
+ * cell, plus the upper boundary faces at index n[dir] (array sized
+ * d * (n0+1)(n1+1)(n2+1) * nv, cell index over the (n+1) extended box). */
+int  orc_dump_flux(orc_ctx* c, double dt, double* F);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

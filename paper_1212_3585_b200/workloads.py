@@ -1,0 +1,203 @@
+"""Seeded, synthetic inputs shared by the CUDA path and the oracle.
+
+This module holds ONLY input specifications: the paper's initial conditions as
+point functions x -> primitive state, and the workload configurations of
+BASELINE.json.  It holds none of the method's arithmetic (no reconstruction,
+predictor, flux, update, quadrature or basis table); both the CUDA library and
+the oracle call these point functions through their own IC callbacks and do
+their own cell averaging.
+
+Primitive layout of every IC: (rho, vx, vy, vz, p, Bx, By, Bz, psi).
+
+Citations: P:n = PAPER.md line n.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+SEEDS = (1212, 3585)
+
+
+# --------------------------------------------------------------------------
+# Initial conditions
+# --------------------------------------------------------------------------
+
+def isentropic_vortex(eps=5.0, gamma=1.4, center=(5.0, 5.0)):
+    """2D isentropic vortex, eq:pert @ P:875-896 (eps = 5, gamma = 1.4)."""
+    def ic(x):
+        x = np.asarray(x, dtype=np.float64)
+        dx = x[:, 0] - center[0]
+        dy = x[:, 1] - center[1]
+        r2 = dx * dx + dy * dy
+        dT = -(eps * eps * (gamma - 1.0)) / (8.0 * gamma * math.pi ** 2) * np.exp(1.0 - r2)
+        e = eps / (2.0 * math.pi) * np.exp(0.5 * (1.0 - r2))
+        out = np.zeros((x.shape[0], 9))
+        out[:, 0] = (1.0 + dT) ** (1.0 / (gamma - 1.0))
+        out[:, 1] = 1.0 - dy * e
+        out[:, 2] = 1.0 + dx * e
+        out[:, 4] = (1.0 + dT) ** (gamma / (gamma - 1.0))
+        return out
+    return ic
+
+
+def vortex_exact(t, eps=5.0, gamma=1.4, period=10.0):
+    """Exact solution of the vortex at time t: advection by (1,1) on the periodic [0,10]^2."""
+    base = isentropic_vortex(eps, gamma)
+
+    def ic(x):
+        y = np.array(x, dtype=np.float64, copy=True)
+        y[:, 0] = np.mod(y[:, 0] - t, period)
+        y[:, 1] = np.mod(y[:, 1] - t, period)
+        return base(y)
+    return ic
+
+
+def explosion(dim, radius=0.5, inner=(1.0, 1.0), outer=(0.125, 0.1)):
+    """Cylindrical/spherical explosion, P:995-1024 and Table tab.3d.explos.ic
+    (rho, p) = (1, 1) inside r <= R, (0.125, 0.1) outside, zero velocity.
+    BASELINE.json uses R = 0.5 (the paper's R = 0.4 is reading D2)."""
+    def ic(x):
+        x = np.asarray(x, dtype=np.float64)
+        r2 = np.zeros(x.shape[0])
+        for k in range(dim):
+            r2 += x[:, k] * x[:, k]
+        inside = r2 <= radius * radius
+        out = np.zeros((x.shape[0], 9))
+        out[:, 0] = np.where(inside, inner[0], outer[0])
+        out[:, 4] = np.where(inside, inner[1], outer[1])
+        return out
+    return ic
+
+
+def orszag_tang(gamma=5.0 / 3.0):
+    """Orszag-Tang vortex, B scaled by sqrt(4 pi) (Gaussian units)."""
+    s = math.sqrt(4.0 * math.pi)
+
+    def ic(x):
+        x = np.asarray(x, dtype=np.float64)
+        out = np.zeros((x.shape[0], 9))
+        out[:, 0] = gamma * gamma
+        out[:, 1] = -np.sin(x[:, 1])
+        out[:, 2] = np.sin(x[:, 0])
+        out[:, 4] = gamma
+        out[:, 5] = -s * np.sin(x[:, 1])
+        out[:, 6] = s * np.sin(2.0 * x[:, 0])
+        return out
+    return ic
+
+
+def shock_tube(axis=0, x0=0.5, left=(1.0, 0.0, 1.0), right=(0.125, 0.0, 0.1)):
+    """Sod-type Riemann problem along one axis (rho, v_n, p) (test-only workload)."""
+    def ic(x):
+        x = np.asarray(x, dtype=np.float64)
+        lft = x[:, axis] < x0
+        out = np.zeros((x.shape[0], 9))
+        out[:, 0] = np.where(lft, left[0], right[0])
+        out[:, 1 + axis] = np.where(lft, left[1], right[1])
+        out[:, 4] = np.where(lft, left[2], right[2])
+        return out
+    return ic
+
+
+def constant_state(rho=1.0, v=(0.3, -0.2, 0.1), p=0.7, B=(0.0, 0.0, 0.0)):
+    def ic(x):
+        out = np.zeros((np.asarray(x).shape[0], 9))
+        out[:, 0] = rho
+        out[:, 1:4] = v
+        out[:, 4] = p
+        out[:, 5:8] = B
+        return out
+    return ic
+
+
+def entropy_wave(dim, amp=0.2, v=(1.0, 0.5, 0.25), p=1.0, L=1.0):
+    """Density wave advected by a constant velocity at constant pressure."""
+    def ic(x):
+        x = np.asarray(x, dtype=np.float64)
+        ph = np.zeros(x.shape[0])
+        for k in range(dim):
+            ph += 2.0 * math.pi * x[:, k] / L
+        out = np.zeros((x.shape[0], 9))
+        out[:, 0] = 1.0 + amp * np.sin(ph)
+        out[:, 1:1 + dim] = v[:dim]
+        out[:, 4] = p
+        return out
+    return ic
+
+
+def random_smooth(dim, seed=SEEDS[0], modes=3, amp=0.05, system=0):
+    """Seeded smooth random admissible state (sum of a few Fourier modes)."""
+    rng = np.random.default_rng(seed)
+    coef = rng.uniform(-1.0, 1.0, size=(9, modes, dim))
+    phase = rng.uniform(0.0, 2 * math.pi, size=(9, modes))
+    base = np.array([1.0, 0.2, -0.1, 0.05, 1.0, 0.3, 0.2, -0.1, 0.0])
+
+    def ic(x):
+        x = np.asarray(x, dtype=np.float64)
+        out = np.tile(base, (x.shape[0], 1))
+        for v in range(9):
+            for m in range(modes):
+                arg = phase[v, m] + 2.0 * math.pi * (x[:, :dim] @ np.round(coef[v, m] * 2.0))
+                out[:, v] += amp * np.sin(arg)
+        if system == 0:
+            out[:, 5:] = 0.0
+        if dim == 2:
+            out[:, 3] = 0.0
+        return out
+    return ic
+
+
+# --------------------------------------------------------------------------
+# BASELINE.json configurations
+# --------------------------------------------------------------------------
+
+@dataclass
+class Workload:
+    name: str
+    dim: int
+    system: int            # 0 Euler, 1 MHD-GLM
+    degree: int            # M
+    n: tuple
+    lo: tuple
+    hi: tuple
+    bc: tuple              # 6 ints, 0 periodic, 1 transmissive
+    gamma: float
+    cfl: float
+    t_end: float
+    steps: int = 0         # fixed step count (0: run to t_end)
+    ic: object = None
+    ch: float = 0.0
+    refine_factor: int = 3
+    lmax: int = 0
+    note: str = ""
+    extra: dict = field(default_factory=dict)
+
+
+def config(name: str, n=None) -> Workload:
+    """Named workloads.  c1..c5 follow BASELINE.json configs[0..4]."""
+    P, T = 0, 1
+    if name == "c1":
+        nn = n or 32
+        return Workload("c1_vortex2d_o3", 2, 0, 2, (nn, nn), (0.0, 0.0), (10.0, 10.0),
+                        (P,) * 6, 1.4, 0.9, 1.0, ic=isentropic_vortex())
+    if name == "c2":
+        nn = n or 512
+        return Workload(f"c2_vortex2d_o4_{nn}", 2, 0, 3, (nn, nn), (0.0, 0.0), (10.0, 10.0),
+                        (P,) * 6, 1.4, 0.9, 10.0, ic=isentropic_vortex())
+    if name == "c3":
+        nn = n or 100
+        return Workload("c3_explosion2d_amr", 2, 0, 2, (nn, nn), (-1.0, -1.0), (1.0, 1.0),
+                        (T,) * 6, 1.4, 0.9, 0.25, ic=explosion(2), refine_factor=3, lmax=2)
+    if name == "c4":
+        nn = n or 256
+        return Workload(f"c4_explosion3d_o3_{nn}", 3, 0, 2, (nn, nn, nn), (-1.0,) * 3, (1.0,) * 3,
+                        (T,) * 6, 1.4, 0.9, 1e300, steps=50, ic=explosion(3))
+    if name == "c5":
+        nn = n or 120
+        return Workload("c5_orszag_tang_mhd", 2, 1, 3, (nn, nn), (0.0, 0.0),
+                        (2 * math.pi, 2 * math.pi), (P,) * 6, 5.0 / 3.0, 0.9, 0.5,
+                        ic=orszag_tang(), ch=2.0, refine_factor=3, lmax=3)
+    raise KeyError(name)
