@@ -1,0 +1,317 @@
+#!/usr/bin/env python
+"""Benchmark of the ADER-WENO hot path on B200 (BASELINE.json metric).
+
+python bench.py --gpus N --steps K --warmup W [--config c4|c2|c1] [--n SIZE] [--impl reference]
+
+A step is one level-0 macro step of the whole hot path (WENO -> predictor ->
+face flux -> FV update, incl. ghost exchange and the CFL reduction) over the
+workload.  Default workload: BASELINE configs[3] (3D Euler spherical
+explosion, uniform 256^3, order 3, FP64), the configuration the metric's
+1/2/4/8-GPU numbers are quoted on; it fits one B200.  Inputs (~90 GB of
+state and stage buffers) are larger than L2, so no explicit flush is needed.
+
+--impl reference times the CPU oracle (oracle/, single thread) on bounded
+sub-box samples of the same workload; that is this tier's reference arm.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FP64 cell-updates/s (2D/3D Euler, MHD) at 1/2/4/8 B200; % FP64 roofline"
+UNIT = "cell-updates/s"
+# FP64 ALU peak of B200 derived from unit counts and clocks:
+# 148 SMs x 64 FP64 FMA lanes/clk x 2 flop x 1.965 GHz (clocks.max.sm)
+SM_COUNT, FP64_FMA_PER_CLK = 148, 64
+
+
+def fp64_peak_tflops(mhz):
+    return SM_COUNT * FP64_FMA_PER_CLK * 2 * mhz * 1e6 / 1e12
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--config", default="c4")
+    p.add_argument("--n", type=int, default=0)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--e2e-steps", type=int, default=3)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-box", type=int, default=12, help="edge of the oracle sample box (cells)")
+    return p.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device=0):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[4:8]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle sample (cpu_baseline and --impl reference)
+# ---------------------------------------------------------------------------
+def oracle_sample(wl, edge, reps=1):
+    """Time the oracle (single thread, as it stands) on `reps` sub-boxes of the
+    workload: one step of an edge^d box straddling the initial discontinuity
+    (explosion) / the vortex core.  Returns (cell-updates/s, description)."""
+    import oracle as O
+    o = O.Oracle(dim=wl.dim, degree=wl.degree, n=wl.n, lo=wl.lo, hi=wl.hi, bc=wl.bc, system=wl.system,
+                 gamma=wl.gamma, ch=wl.ch, cfl=wl.cfl)
+    n = wl.n
+    if wl.name.startswith("c4") or wl.name.startswith("c3"):
+        # centre the box on x = 0.5 (r = R on the x axis), mid-plane in y, z
+        cx = int(round((0.5 - wl.lo[0]) / (wl.hi[0] - wl.lo[0]) * n[0]))
+        ctr = [cx] + [n[k] // 2 for k in range(1, wl.dim)]
+    else:
+        ctr = [n[k] // 2 for k in range(wl.dim)]
+    blo = [max(0, c - edge // 2) for c in ctr]
+    bhi = [min(n[k], blo[k] + edge) for k in range(wl.dim)]
+    glo = [max(0, b - wl.degree - 2) for b in blo]
+    ghi = [min(n[k], b + wl.degree + 2) for k, b in enumerate(bhi)]
+    o.set_initial_box(wl.ic, glo, ghi)
+    if wl.name.startswith("c4"):
+        uin = O.prim_to_cons(0, 3, wl.gamma, [1, 0, 0, 0, 1])
+        dx = (wl.hi[0] - wl.lo[0]) / n[0]
+        dt = wl.cfl / sum(O.max_speed(0, 3, wl.gamma, 0, uin, d) / dx for d in range(3))
+    else:
+        o.set_initial(wl.ic)
+        dt = o.compute_dt()
+    ups, secs = 0, 0.0
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        _, rep = o.advance_box(dt, blo, bhi)
+        secs += time.perf_counter() - t0
+        ups += rep.cell_updates
+    desc = (f"one step of the {'x'.join(str(bhi[k] - blo[k]) for k in range(wl.dim))} cell box at "
+            f"{blo} of {wl.name} (box + face neighbours reconstructed/predicted), single thread")
+    return ups / secs, desc, ups, secs
+
+
+def run_reference(args, wl):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    edge = max(2, args.cpu_box // 2)
+    for _ in range(args.warmup):
+        oracle_sample(wl, edge)
+    tot_u, tot_s = 0, 0.0
+    desc = ""
+    for _ in range(args.steps):
+        _, desc, u, s = oracle_sample(wl, edge)
+        tot_u += u
+        tot_s += s
+    val = tot_u / tot_s
+    cfgd = {"workload": wl.name, "dim": wl.dim, "degree": wl.degree, "cells": list(wl.n), "system": "euler" if wl.system == 0 else "mhd_glm"}
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * tot_s / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfgd,
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def load_traffic(wl):
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        d = json.load(open(path))
+        return d.get(wl.name, {}).get("stdg_predictor_dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def main():
+    args = parse()
+    from paper_1212_3585_b200 import workloads as W
+    wl = W.config(args.config, args.n or None)
+    if args.impl == "reference":
+        return run_reference(args, wl)
+
+    import torch
+    import torch.distributed as dist
+    from paper_1212_3585_b200 import ader
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and world > 1:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    nid = None
+    if world > 1:
+        obj = [ader.ader_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nid = obj[0]
+    cfg = ader.make_config(dim=wl.dim, degree=wl.degree, n0=wl.n, lo=wl.lo, hi=wl.hi, bc=wl.bc, system=wl.system,
+                           gamma=wl.gamma, ch=wl.ch, cfl=wl.cfl, rank=rank, world_size=world, device=local,
+                           nccl_id=nid)
+    s = ader.Solver(cfg)
+    stream = torch.cuda.current_stream()
+    s.set_stream(stream.cuda_stream)
+    t_ic = time.perf_counter()
+    s.set_initial(wl.ic)
+    t_ic = time.perf_counter() - t_ic
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    # warm-up
+    if args.warmup:
+        s.step(1e300, args.warmup)
+    barrier()
+    # timed region: exactly K macro steps
+    s.set_profiling(True)
+    l0 = s.launch_count()
+    clk = ClockSampler(local)
+    clk.start()
+    time.sleep(0.3)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    rep = s.step(1e300, args.steps)
+    e1.record(stream)
+    barrier()
+    clocks = clk.stop()
+    ms = e0.elapsed_time(e1)
+    launches = s.launch_count() - l0
+    kms, kl, kfl = s.kernel_stats()
+    s.set_profiling(False)
+    t_max = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    ups = torch.tensor([float(rep.cell_updates)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+        dist.all_reduce(ups, op=dist.ReduceOp.SUM)
+    ms_max = float(t_max.item())
+    total_updates = float(ups.item())
+    value = total_updates / (ms_max / 1e3)
+
+    # end-to-end through the public API with host buffers (pinned)
+    ne = max(1, args.e2e_steps)
+    host = torch.empty((s.ncells, s.nv), dtype=torch.float64, pin_memory=True)
+    s.get_state_ptr(host.data_ptr())
+    barrier()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    e2e_updates = 0
+    for _ in range(ne):
+        s.set_cells_ptr(host.data_ptr())       # H2D of the step's input state
+        r2 = s.step(1e300, 1)
+        s.get_state_ptr(host.data_ptr())       # D2H of the step's result
+        e2e_updates += r2.cell_updates
+    f1.record(stream)
+    barrier()
+    e2e_ms = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device="cuda")
+    e2u = torch.tensor([float(e2e_updates)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+        dist.all_reduce(e2u, op=dist.ReduceOp.SUM)
+    e2e_val = float(e2u.item()) / (float(e2e_ms.item()) / 1e3)
+    bytes_step = s.ncells * s.nv * 8
+
+    if rank == 0:
+        pred_ms_avg = kms[ader.K_PRED] / max(1, kl[ader.K_PRED])
+        pred_flops = kfl[ader.K_PRED] / max(1, kl[ader.K_PRED])
+        achieved = pred_flops / (pred_ms_avg / 1e3) / 1e12
+        peak = fp64_peak_tflops(1965.0)
+        step_ms = ms_max / args.steps
+        share = {ader.KERNEL_NAMES[i]: round(kms[i] / max(1e-9, ms) , 4) for i in range(ader.K_COUNT)}
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": wl.name, "dim": wl.dim, "degree": wl.degree, "order": wl.degree + 1,
+                       "cells": list(wl.n), "system": "euler" if wl.system == 0 else "mhd_glm",
+                       "flux": "rusanov", "cfl": wl.cfl, "ic": "explosion r<0.5" if "explosion" in wl.name else wl.name,
+                       "parallelism": f"level-0 blocks x{world}", "l2": "inputs larger than L2 (~90 GB working set)"},
+            "roofline": {"bound": "alu", "kernel": "stdg_predictor", "achieved": achieved, "peak": peak,
+                         "unit": "TFLOP/s", "frac": achieved / peak, "traffic": load_traffic(wl),
+                         "peak_note": "FP64 FMA pipe: 148 SM x 64 lanes x 2 x 1.965 GHz (derived, DESIGN.md)",
+                         "achieved_note": "algorithmic FP64 flops of the Picard sweeps actually run / CUDA-event time"},
+            "kernel_share_of_step": share,
+            "pred_sweeps_mean": rep.pred_sweeps_total / max(1, rep.pred_cells),
+            "clocks": clocks,
+            "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": bytes_step, "d2h_bytes_per_step": bytes_step,
+                    "steps": ne},
+            "gpu_launches": int(launches),
+            "ic_setup_s": t_ic,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            v, desc, u, secs = oracle_sample(wl, args.cpu_box)
+            line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc,
+                                    "cell_updates": u, "seconds": secs, "host_nproc": os.cpu_count()}
+        print(json.dumps(line), flush=True)
+    s.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,169 @@
+/*
+ * ader.h — C ABI of the B200-native ADER-WENO hot path (arXiv:1212.3585).
+ *
+ * extern "C", FP64 throughout, plain pointers and sizes, no torch types.
+ * One context = one rank = one GPU.  A context is single-writer: calls on the
+ * same context must not overlap (they may run on different contexts in
+ * different threads).  Every call returns an ader_status; on failure
+ * ader_last_error(ctx) holds a one-line reason (with cell index, level and
+ * time for solver failures, following SPEC S:47/S:88).
+ *
+ * Citations: P:a-b = PAPER.md lines a..b with the equation label they fall in.
+ *
+ * What one macro step computes (ader_step), on the active cells of every
+ * level:
+ *   a1 WENO reconstruction, dimension by dimension
+ *   a2 local space-time DG predictor (Picard iteration) P:331-474
+ *   a3 space-time Gauss quadrature of the Rusanov flux
+ *   a4 one-step finite-volume update                     eq:finite_vol P:147-152
+ *   a8 CFL time step dt0 = cfl / max sum_dir s_dir/dx_dir (reading R1)
+ * Level-0 cells are partitioned in Cartesian blocks over world_size ranks;
+ * ghost layers are exchanged with NCCL (P:794-810 is the paper's MPI form).
+ */
+#ifndef ADER_H
+#define ADER_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ADER_ABI_VERSION 1
+
+typedef struct ader_ctx ader_ctx;   /* opaque; owns all device memory it allocates */
+
+typedef enum {
+  ADER_OK = 0,
+  ADER_ERR_ARG = 1,      /* null pointer, capacity too small, bad enum            */
+  ADER_ERR_CONFIG = 2,   /* configuration rejected before any allocation  */
+  ADER_ERR_SOLVER = 3,   /* inadmissible state (rho<=0 or p<=0) or predictor cap  */
+  ADER_ERR_CUDA = 4,     /* CUDA runtime error or no sm_100 device                */
+  ADER_ERR_NCCL = 5,     /* NCCL missing or failed                                */
+  ADER_ERR_UNSUPPORTED = 6
+} ader_status;
+
+typedef enum { ADER_EULER = 0, ADER_MHD_GLM = 1 } ader_system;
+typedef enum { ADER_BC_PERIODIC = 0, ADER_BC_TRANSMISSIVE = 1 } ader_bc;
+
+/* Problem statement.  All lengths in cells. */
+typedef struct {
+  int32_t abi_version;          /* must be ADER_ABI_VERSION                        */
+  int32_t dim;                  /* d in {2,3}                                      */
+  int32_t system;               /* ader_system: Euler nu = d+2 (2D nu=4), MHD nu=9 */
+  int32_t degree;               /* M in {2,3}: order M+1 in space and time         */
+  int32_t n0[3];                /* level-0 cells per axis (global); n0[2]=1 if d=2 */
+  double  lo[3], hi[3];         /* domain box                                      */
+  int32_t bc[6];                /* ader_bc for -x,+x,-y,+y,-z,+z                   */
+  int32_t refine_factor;        /* r >= M                              */
+  int32_t lmax;                 /* 0 = uniform grid                                */
+  double  gamma;                /* ideal-gas adiabatic index                       */
+  double  ch;                   /* GLM cleaning speed (MHD only)           */
+  double  cfl;                  /* reading R1 (BASELINE: 0.9)                      */
+  double  chi_ref, chi_rec, chi_eps;   /* indicator thresholds         */
+  int32_t indicator_var;        /* 0 = rho                                 */
+  double  pred_tol;             /* Picard stopping tolerance (reading R2), 1e-13   */
+  int32_t pred_max_sweeps;      /* cap (reading R2), 32; reaching it = solver error*/
+  int32_t ic_quad;              /* GL points per axis for IC cell averages (R6); 0 = M+1 */
+  int32_t adapt_every;          /* macro steps between adapts (AMR); 0 = frozen    */
+  int32_t rank, world_size;     /* one rank per GPU; world_size=1 => no NCCL       */
+  int32_t device;               /* CUDA device ordinal; -1 = current device        */
+  uint8_t nccl_id[128];         /* ncclUniqueId from rank 0 (ader_nccl_unique_id)  */
+} ader_config;
+
+/* Batched IC callback (host): x[n][3] -> prim[n][9] with
+ * prim = (rho, vx, vy, vz, p, Bx, By, Bz, psi).  Euler reads the first five. */
+typedef void (*ader_ic_fn)(const double* x, int64_t n, double* prim, void* user);
+
+typedef struct {
+  double  t, dt0;                 /* time reached, last level-0 dt                 */
+  int64_t macro_steps;            /* level-0 steps taken by this call              */
+  int64_t cell_updates;           /* active-cell local steps, this rank*/
+  int64_t updates_per_level[8];
+  int64_t pred_sweeps_total;      /* Picard sweeps summed over predicted cells     */
+  int32_t pred_sweeps_max;
+  int32_t pad_;
+  int64_t pred_cells;             /* cells run through the predictor (incl. halo)  */
+  double  cons_total[9];          /* sum of u * cell volume over owned active cells*/
+  double  wall_s;
+} ader_step_report;
+
+/* One cell as exported by ader_get_cells: parity key (level, idx, status). */
+typedef struct {
+  int32_t level;
+  int32_t status;                 /* 0 active, +1 virtual child, -1 virtual mother */
+  int64_t idx[3];                 /* integer index at its level (global)           */
+  double  u[9];                   /* cell average (first nu entries valid)         */
+} ader_cell;
+
+/* Block of level-0 cells owned by a rank (host-only, no GPU needed). */
+typedef struct {
+  int32_t dims[3];                /* process grid                                  */
+  int32_t coord[3];               /* this rank's coordinate in the process grid    */
+  int32_t lo[3], hi[3];           /* owned global cells [lo, hi)                   */
+  int32_t nbr[6];                 /* neighbour rank on -x,+x,-y,+y,-z,+z; -1 none  */
+  int32_t halo;                   /* ghost-layer width (M+1)                       */
+} ader_partition_info;
+
+/* --- lifecycle ------------------------------------------------------------ */
+/* Validates cfg before any allocation (ADER_ERR_CONFIG: dim/degree/system out
+ * of range, r < M, n0 < 1, world_size not in 1..8, rank out of range).  On
+ * success *out owns device memory on cfg->device; release with ader_destroy. */
+ader_status ader_create(const ader_config* cfg, ader_ctx** out);
+void        ader_destroy(ader_ctx* c);
+const char* ader_last_error(const ader_ctx* c);
+/* Use the given cudaStream_t for all work (e.g. torch's current stream);
+ * NULL restores the context's own stream. */
+ader_status ader_set_stream(ader_ctx* c, void* cuda_stream);
+
+/* --- state ---------------------------------------------------------------- */
+/* Host-evaluated IC: ic is called on batches of Gauss-Legendre points
+ * x = lo + (i + lambda_k) dx (reading R6), the cell averages are formed on
+ * the GPU.  Then (lmax > 0) the initial refinement runs up to lmax. */
+ader_status ader_set_initial(ader_ctx* c, ader_ic_fn ic, void* user);
+/* Owned level-0 cell averages from a host buffer u[cell][nu], cells ordered
+ * x fastest then y then z inside the rank's block; n_cells must equal the
+ * block size.  Synchronous. */
+ader_status ader_set_cells(ader_ctx* c, const double* u_host, int64_t n_cells);
+/* Compact copy of the owned level-0 averages into u_host[cell][nu] (same
+ * order as ader_set_cells).  Synchronous. */
+ader_status ader_get_state(const ader_ctx* c, double* u_host, int64_t capacity_cells);
+/* All cells of this rank (every status) sorted by (level, z, y, x);
+ * out == NULL => *n = count only.  Synchronous. */
+ader_status ader_get_cells(const ader_ctx* c, ader_cell* out, int64_t capacity, int64_t* n);
+double      ader_time(const ader_ctx* c);
+
+/* --- time stepping ---------------------------------------------------------- */
+/* Whole level-0 macro steps until t >= t_end or max_macro_steps were taken:
+ * dt0 = cfl / max over active cells of sum_dir s_dir/dx_dir (all ranks),
+ * clipped to t_end; then a1..a4 on every level in LTS order;
+ * adapt every adapt_every macro steps (AMR).  rep may be NULL. */
+ader_status ader_step(ader_ctx* c, double t_end, int64_t max_macro_steps, ader_step_report* rep);
+/* One adapt pass at synchronized time.  Uniform grids: no-op. */
+ader_status ader_refine(ader_ctx* c, ader_step_report* rep);
+
+/* --- multi-GPU plumbing (host only) ---------------------------------------- */
+ader_status ader_partition(const ader_config* cfg, int32_t rank, ader_partition_info* out);
+/* 128-byte ncclUniqueId for rank 0 to broadcast (loads libnccl.so.2 lazily). */
+ader_status ader_nccl_unique_id(uint8_t out[128]);
+
+/* --- instrumentation / test hooks ---------------------------------------- */
+enum { ADER_K_WENO = 0, ADER_K_PRED = 1, ADER_K_FLUX = 2, ADER_K_UPDATE = 3,
+       ADER_K_HALO = 4, ADER_K_OTHER = 5, ADER_K_COUNT = 6 };
+/* When on, every kernel launch is bracketed by CUDA events on the launch
+ * stream; ader_kernel_stats returns, per kernel class, total device ms,
+ * launch count and the algorithmic FP64 flops of those launches. */
+ader_status ader_set_profiling(ader_ctx* c, int32_t on);
+ader_status ader_kernel_stats(ader_ctx* c, double ms[ADER_K_COUNT], int64_t launches[ADER_K_COUNT],
+                              double flops[ADER_K_COUNT]);
+/* Number of kernels this context has launched since ader_create. */
+ader_status ader_launch_count(const ader_ctx* c, int64_t* n);
+/* Test-only dumps of one stage on the current state (state not modified):
+ *   what = 0 RECON: w[cell][nu][N^d]           (owned cells, x-fastest nodes)
+ *   what = 1 PRED : q[cell][nu][N^(d+1)]       (space fastest, time slowest), step dt
+ *   what = 2 FLUX : F[dir][ext cell][nu]        ext box = block + 1 per axis, lower faces
+ * capacity in doubles. */
+ader_status ader_debug_dump(ader_ctx* c, int32_t what, double dt, double* out, int64_t capacity);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

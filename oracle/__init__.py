@@ -64,6 +64,7 @@ def lib():
         L.orc_last_error.restype = C.c_char_p
         L.orc_last_error.argtypes = [C.c_void_p]
         L.orc_set_initial.argtypes = [C.c_void_p, IC_FN, C.c_void_p]
+        L.orc_set_initial_box.argtypes = [C.c_void_p, IC_FN, C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
         L.orc_set_cells.argtypes = [C.c_void_p, dp]
         L.orc_get_cells.argtypes = [C.c_void_p, dp]
         L.orc_time.restype = C.c_double
@@ -239,6 +240,17 @@ class Oracle:
             p[:] = ic(x)
         self._cb = IC_FN(cb)
         rc = lib().orc_set_initial(self.ptr, self._cb, None)
+        assert rc == 0
+
+    def set_initial_box(self, ic, blo, bhi):
+        def cb(xp, n, pp, user):
+            x = np.ctypeslib.as_array(xp, shape=(n, 3))
+            p = np.ctypeslib.as_array(pp, shape=(n, 9))
+            p[:] = ic(x)
+        self._cb = IC_FN(cb)
+        a = (C.c_int32 * 3)(*((list(blo) + [0, 0, 0])[:3]))
+        b = (C.c_int32 * 3)(*((list(bhi) + [1, 1, 1])[:3]))
+        rc = lib().orc_set_initial_box(self.ptr, self._cb, None, a, b)
         assert rc == 0
 
     def set_cells(self, u):

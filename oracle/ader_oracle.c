@@ -664,11 +664,22 @@ double orc_time(const orc_ctx* c) { return c->t; }
 int64_t orc_num_cells(const orc_ctx* c) { return (int64_t)c->n[0] * c->n[1] * c->n[2]; }
 
 int orc_set_initial(orc_ctx* c, orc_ic_fn ic, void* user) {
+  int32_t lo[3] = {0, 0, 0}, hi[3] = {c->n[0], c->n[1], c->n[2]};
+  return orc_set_initial_box(c, ic, user, lo, hi);
+}
+
+int orc_set_initial_box(orc_ctx* c, orc_ic_fn ic, void* user, const int32_t* blo, const int32_t* bhi) {
   int Q = c->cfg.ic_quad, d = c->d, nv = c->nv;
   double qx[16], qw[16];
   gauss_legendre01(Q, qx, qw);
   int nq = ipow(Q, d);
-  int64_t ncell = orc_num_cells(c);
+  int bl[3], be[3];
+  for (int k = 0; k < 3; ++k) {
+    bl[k] = (k < d) ? (blo[k] < 0 ? 0 : blo[k]) : 0;
+    int h = (k < d) ? (bhi[k] > c->n[k] ? c->n[k] : bhi[k]) : 1;
+    be[k] = h > bl[k] ? h - bl[k] : 0;
+  }
+  int64_t ncell = (int64_t)be[0] * be[1] * be[2];
   const int64_t chunk = 4096;
   double* x = (double*)malloc(sizeof(double) * chunk * nq * 3);
   double* pr = (double*)malloc(sizeof(double) * chunk * nq * 9);
@@ -676,7 +687,7 @@ int orc_set_initial(orc_ctx* c, orc_ic_fn ic, void* user) {
     int64_t nc = (ncell - c0 < chunk) ? ncell - c0 : chunk;
     for (int64_t ci = 0; ci < nc; ++ci) {
       int64_t lin = c0 + ci;
-      int ii[3] = {(int)(lin % c->n[0]), (int)((lin / c->n[0]) % c->n[1]), (int)(lin / ((int64_t)c->n[0] * c->n[1]))};
+      int ii[3] = {bl[0] + (int)(lin % be[0]), bl[1] + (int)((lin / be[0]) % be[1]), bl[2] + (int)(lin / ((int64_t)be[0] * be[1]))};
       for (int g = 0; g < nq; ++g) {
         int gi[3] = {g % Q, (g / Q) % Q, g / (Q * Q)};
         double* xp = &x[(ci * nq + g) * 3];
@@ -688,7 +699,7 @@ int orc_set_initial(orc_ctx* c, orc_ic_fn ic, void* user) {
     ic(x, nc * nq, pr, user);
     for (int64_t ci = 0; ci < nc; ++ci) {
       int64_t lin = c0 + ci;
-      int ii[3] = {(int)(lin % c->n[0]), (int)((lin / c->n[0]) % c->n[1]), (int)(lin / ((int64_t)c->n[0] * c->n[1]))};
+      int ii[3] = {bl[0] + (int)(lin % be[0]), bl[1] + (int)((lin / be[0]) % be[1]), bl[2] + (int)(lin / ((int64_t)be[0] * be[1]))};
       double acc[VMAX] = {0};
       /* u_bar = sum_g (prod_k w_gk) cons(ic(x_g)) , z outer, y, x inner (reading R6) */
       for (int g = 0; g < nq; ++g) {

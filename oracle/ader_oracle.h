@@ -87,6 +87,8 @@ orc_ctx* orc_create(const orc_config* cfg);
 void     orc_destroy(orc_ctx* c);
 const char* orc_last_error(const orc_ctx* c);
 int  orc_set_initial(orc_ctx* c, orc_ic_fn ic, void* user);
+/* IC averages only for the interior cells of the box [blo, bhi). */
+int  orc_set_initial_box(orc_ctx* c, orc_ic_fn ic, void* user, const int32_t* blo, const int32_t* bhi);
 /* Interior cell averages, u[cell][nv], cells x fastest then y then z. */
 int  orc_set_cells(orc_ctx* c, const double* u);
 int  orc_get_cells(const orc_ctx* c, double* u);

@@ -1,0 +1,260 @@
+"""Thin ctypes binding of the C ABI in include/ader.h (libader_b200.so).
+
+Argument marshalling only: every stage of the path runs in the CUDA kernels
+of the library.  There is no fallback: if the shared library is missing or
+cannot be loaded, importing the binding's entry points raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libader_b200.so")
+_LIB = None
+
+ABI_VERSION = 1
+EULER, MHD_GLM = 0, 1
+PERIODIC, TRANSMISSIVE = 0, 1
+K_WENO, K_PRED, K_FLUX, K_UPDATE, K_HALO, K_OTHER, K_COUNT = range(7)
+KERNEL_NAMES = ("weno_reconstruct", "stdg_predictor", "face_flux_rusanov", "fv_update", "halo", "other")
+STATUS = {0: "ADER_OK", 1: "ADER_ERR_ARG", 2: "ADER_ERR_CONFIG", 3: "ADER_ERR_SOLVER", 4: "ADER_ERR_CUDA",
+          5: "ADER_ERR_NCCL", 6: "ADER_ERR_UNSUPPORTED"}
+
+IC_FN = C.CFUNCTYPE(None, C.POINTER(C.c_double), C.c_int64, C.POINTER(C.c_double), C.c_void_p)
+
+
+class AderConfig(C.Structure):
+    _fields_ = [
+        ("abi_version", C.c_int32), ("dim", C.c_int32), ("system", C.c_int32), ("degree", C.c_int32),
+        ("n0", C.c_int32 * 3), ("lo", C.c_double * 3), ("hi", C.c_double * 3), ("bc", C.c_int32 * 6),
+        ("refine_factor", C.c_int32), ("lmax", C.c_int32),
+        ("gamma", C.c_double), ("ch", C.c_double), ("cfl", C.c_double),
+        ("chi_ref", C.c_double), ("chi_rec", C.c_double), ("chi_eps", C.c_double),
+        ("indicator_var", C.c_int32),
+        ("pred_tol", C.c_double), ("pred_max_sweeps", C.c_int32),
+        ("ic_quad", C.c_int32), ("adapt_every", C.c_int32),
+        ("rank", C.c_int32), ("world_size", C.c_int32), ("device", C.c_int32),
+        ("nccl_id", C.c_uint8 * 128),
+    ]
+
+
+class AderStepReport(C.Structure):
+    _fields_ = [
+        ("t", C.c_double), ("dt0", C.c_double),
+        ("macro_steps", C.c_int64), ("cell_updates", C.c_int64), ("updates_per_level", C.c_int64 * 8),
+        ("pred_sweeps_total", C.c_int64), ("pred_sweeps_max", C.c_int32), ("pad_", C.c_int32),
+        ("pred_cells", C.c_int64), ("cons_total", C.c_double * 9), ("wall_s", C.c_double),
+    ]
+
+
+class AderCell(C.Structure):
+    _fields_ = [("level", C.c_int32), ("status", C.c_int32), ("idx", C.c_int64 * 3), ("u", C.c_double * 9)]
+
+
+class AderPartitionInfo(C.Structure):
+    _fields_ = [("dims", C.c_int32 * 3), ("coord", C.c_int32 * 3), ("lo", C.c_int32 * 3), ("hi", C.c_int32 * 3),
+                ("nbr", C.c_int32 * 6), ("halo", C.c_int32)]
+
+
+class AderError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+def lib():
+    """Load libader_b200.so (raises if it has not been built)."""
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback exists)")
+        L = C.CDLL(LIB_PATH)
+        vp, dp = C.c_void_p, C.POINTER(C.c_double)
+        L.ader_create.argtypes = [C.POINTER(AderConfig), C.POINTER(vp)]
+        L.ader_destroy.argtypes = [vp]
+        L.ader_destroy.restype = None
+        L.ader_last_error.argtypes = [vp]
+        L.ader_last_error.restype = C.c_char_p
+        L.ader_set_stream.argtypes = [vp, vp]
+        L.ader_set_initial.argtypes = [vp, IC_FN, vp]
+        L.ader_set_cells.argtypes = [vp, dp, C.c_int64]
+        L.ader_get_state.argtypes = [vp, dp, C.c_int64]
+        L.ader_get_cells.argtypes = [vp, C.POINTER(AderCell), C.c_int64, C.POINTER(C.c_int64)]
+        L.ader_time.argtypes = [vp]
+        L.ader_time.restype = C.c_double
+        L.ader_step.argtypes = [vp, C.c_double, C.c_int64, C.POINTER(AderStepReport)]
+        L.ader_refine.argtypes = [vp, C.POINTER(AderStepReport)]
+        L.ader_partition.argtypes = [C.POINTER(AderConfig), C.c_int32, C.POINTER(AderPartitionInfo)]
+        L.ader_nccl_unique_id.argtypes = [C.POINTER(C.c_uint8)]
+        L.ader_set_profiling.argtypes = [vp, C.c_int32]
+        L.ader_kernel_stats.argtypes = [vp, dp, C.POINTER(C.c_int64), dp]
+        L.ader_launch_count.argtypes = [vp, C.POINTER(C.c_int64)]
+        L.ader_debug_dump.argtypes = [vp, C.c_int32, C.c_double, dp, C.c_int64]
+        _LIB = L
+    return _LIB
+
+
+EXPORTED = ("ader_create", "ader_destroy", "ader_last_error", "ader_set_stream", "ader_set_initial",
+            "ader_set_cells", "ader_get_state", "ader_get_cells", "ader_time", "ader_step", "ader_refine",
+            "ader_partition", "ader_nccl_unique_id", "ader_set_profiling", "ader_kernel_stats",
+            "ader_launch_count", "ader_debug_dump")
+
+
+def _dp(a):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def make_config(*, dim, degree, n0, lo, hi, bc, system=EULER, gamma=1.4, ch=0.0, cfl=0.9,
+                refine_factor=3, lmax=0, chi_ref=0.2, chi_rec=0.1, chi_eps=0.01, pred_tol=1e-13,
+                pred_max_sweeps=32, ic_quad=0, adapt_every=1, rank=0, world_size=1, device=-1,
+                nccl_id=None) -> AderConfig:
+    cfg = AderConfig()
+    cfg.abi_version = ABI_VERSION
+    cfg.dim, cfg.system, cfg.degree = dim, system, degree
+    n0 = list(n0) + [1] * (3 - len(n0))
+    lo = list(lo) + [0.0] * (3 - len(lo))
+    hi = list(hi) + [1.0] * (3 - len(hi))
+    for k in range(3):
+        cfg.n0[k], cfg.lo[k], cfg.hi[k] = n0[k], lo[k], hi[k]
+    bc = list(bc) + [0] * (6 - len(bc))
+    for k in range(6):
+        cfg.bc[k] = bc[k]
+    cfg.refine_factor, cfg.lmax = refine_factor, lmax
+    cfg.gamma, cfg.ch, cfg.cfl = gamma, ch, cfl
+    cfg.chi_ref, cfg.chi_rec, cfg.chi_eps, cfg.indicator_var = chi_ref, chi_rec, chi_eps, 0
+    cfg.pred_tol, cfg.pred_max_sweeps = pred_tol, pred_max_sweeps
+    cfg.ic_quad, cfg.adapt_every = ic_quad, adapt_every
+    cfg.rank, cfg.world_size, cfg.device = rank, world_size, device
+    if nccl_id is not None:
+        for i, b in enumerate(bytes(nccl_id)[:128]):
+            cfg.nccl_id[i] = b
+    return cfg
+
+
+def ader_partition(cfg: AderConfig, rank: int) -> AderPartitionInfo:
+    info = AderPartitionInfo()
+    st = lib().ader_partition(C.byref(cfg), rank, C.byref(info))
+    if st:
+        raise AderError(st, "ader_partition rejected the configuration")
+    return info
+
+
+def ader_nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    st = lib().ader_nccl_unique_id(buf)
+    if st:
+        raise AderError(st, "ncclGetUniqueId failed")
+    return bytes(buf)
+
+
+class Solver:
+    """One rank's context: ader_create ... ader_destroy."""
+
+    def __init__(self, cfg: AderConfig):
+        self.cfg = cfg
+        self.nv = 9 if cfg.system == MHD_GLM else cfg.dim + 2
+        self.N = cfg.degree + 1
+        self.part = ader_partition(cfg, cfg.rank)
+        self.block = [self.part.hi[k] - self.part.lo[k] for k in range(cfg.dim)]
+        self.ptr = C.c_void_p()
+        st = lib().ader_create(C.byref(cfg), C.byref(self.ptr))
+        if st:
+            raise AderError(st, lib().ader_last_error(None).decode())
+
+    def close(self):
+        if self.ptr:
+            lib().ader_destroy(self.ptr)
+            self.ptr = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _chk(self, st):
+        if st:
+            raise AderError(st, lib().ader_last_error(self.ptr).decode())
+
+    @property
+    def ncells(self):
+        return int(np.prod(self.block))
+
+    def set_stream(self, stream_ptr):
+        self._chk(lib().ader_set_stream(self.ptr, C.c_void_p(stream_ptr)))
+
+    def set_initial(self, ic):
+        def cb(xp, n, pp, user):
+            x = np.ctypeslib.as_array(xp, shape=(n, 3))
+            p = np.ctypeslib.as_array(pp, shape=(n, 9))
+            p[:] = ic(x)
+        self._cb = IC_FN(cb)
+        self._chk(lib().ader_set_initial(self.ptr, self._cb, None))
+
+    def set_cells(self, u):
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        self._chk(lib().ader_set_cells(self.ptr, _dp(u), self.ncells))
+
+    def set_cells_ptr(self, host_ptr):
+        self._chk(lib().ader_set_cells(self.ptr, C.cast(C.c_void_p(host_ptr), C.POINTER(C.c_double)), self.ncells))
+
+    def get_state(self, out=None):
+        if out is None:
+            out = np.empty((self.ncells, self.nv))
+        self._chk(lib().ader_get_state(self.ptr, _dp(out), self.ncells))
+        return out
+
+    def get_state_ptr(self, host_ptr):
+        self._chk(lib().ader_get_state(self.ptr, C.cast(C.c_void_p(host_ptr), C.POINTER(C.c_double)), self.ncells))
+
+    def get_cells(self):
+        n = C.c_int64(0)
+        self._chk(lib().ader_get_cells(self.ptr, None, 0, C.byref(n)))
+        arr = (AderCell * n.value)()
+        self._chk(lib().ader_get_cells(self.ptr, arr, n.value, C.byref(n)))
+        return arr
+
+    @property
+    def t(self):
+        return lib().ader_time(self.ptr)
+
+    def step(self, t_end=1e300, max_steps=1) -> AderStepReport:
+        rep = AderStepReport()
+        self._chk(lib().ader_step(self.ptr, t_end, max_steps, C.byref(rep)))
+        return rep
+
+    def refine(self):
+        rep = AderStepReport()
+        self._chk(lib().ader_refine(self.ptr, C.byref(rep)))
+        return rep
+
+    def set_profiling(self, on):
+        self._chk(lib().ader_set_profiling(self.ptr, 1 if on else 0))
+
+    def kernel_stats(self):
+        ms = np.zeros(K_COUNT)
+        ln = np.zeros(K_COUNT, dtype=np.int64)
+        fl = np.zeros(K_COUNT)
+        self._chk(lib().ader_kernel_stats(self.ptr, _dp(ms), ln.ctypes.data_as(C.POINTER(C.c_int64)), _dp(fl)))
+        return ms, ln, fl
+
+    def launch_count(self):
+        n = C.c_int64(0)
+        self._chk(lib().ader_launch_count(self.ptr, C.byref(n)))
+        return n.value
+
+    def debug_dump(self, what, dt=0.0):
+        d, nv, N = self.cfg.dim, self.nv, self.N
+        nc = self.ncells
+        if what == 0:
+            out = np.zeros((nc, nv, N ** d))
+        elif what == 1:
+            out = np.zeros((nc, nv, N ** (d + 1)))
+        else:
+            e = [b + 1 for b in self.block] + ([1] if d == 2 else [])
+            out = np.zeros((d, int(np.prod(e)), nv))
+        self._chk(lib().ader_debug_dump(self.ptr, what, dt, _dp(out), out.size))
+        return out

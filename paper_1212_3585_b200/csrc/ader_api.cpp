@@ -1,0 +1,839 @@
+// ader_api.cpp — C-ABI implementation (include/ader.h): validation, device
+// memory, the host orchestrator of one macro step, ghost-layer exchange over
+// NCCL, IC projection, debug dumps and kernel instrumentation.
+//
+// The host never computes cell data: every stage of the path runs in the
+// kernels of kernels.cu; the host only schedules launches and reduces
+// scalars (the CFL dt, report counters).
+// Citations: P:n = PAPER.md line n.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/ader.h"
+#include "launch.h"
+#include "tables.h"
+
+using namespace ader;
+
+// ---------------------------------------------------------------------------
+// NCCL, loaded lazily (the soname already loaded by torch is reused)
+// ---------------------------------------------------------------------------
+namespace {
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  bool load(std::string& err) {
+    if (h) return true;
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* n : names) {
+      h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+      if (h) break;
+    }
+    if (!h) { err = std::string("cannot load libnccl.so.2: ") + dlerror(); return false; }
+#define SYM(x) x = reinterpret_cast<decltype(x)>(dlsym(h, "nccl" #x)); if (!x) { err = "missing nccl" #x; return false; }
+    SYM(GetUniqueId) SYM(CommInitRank) SYM(CommDestroy) SYM(Send) SYM(Recv) SYM(GroupStart) SYM(GroupEnd)
+    SYM(AllReduce) SYM(GetErrorString)
+#undef SYM
+    return true;
+  }
+};
+NcclApi g_nccl;
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// context
+// ---------------------------------------------------------------------------
+struct ProfRec { int kind; cudaEvent_t e0, e1; double flops; };
+
+struct ader_ctx {
+  ader_config cfg{};
+  int d = 2, M = 2, N = 3, nv = 4, NS = 9, NST = 27, H = 3;
+  ader_partition_info part{};
+  int n[3] = {1, 1, 1}, P[3] = {1, 1, 1};
+  long long ncell = 0;
+  double dx[3] = {1, 1, 1}, inv_dx[3] = {1, 1, 1};
+  KCtx k{};
+  cudaStream_t own_stream = nullptr;
+  double *u = nullptr, *wx = nullptr, *wxy = nullptr, *w = nullptr, *q = nullptr, *F = nullptr;
+  double *stage = nullptr;                     // compact staging buffer (set/get)
+  double *sendb[6] = {}, *recvb[6] = {};       // halo buffers per side
+  long long halo_cap = 0;
+  DevCounters* cnt = nullptr;                  // device
+  DevCounters* hcnt = nullptr;                 // pinned host mirror
+  double t = 0.0;
+  bool speed_valid = false;
+  ncclComm_t comm = nullptr;
+  std::string err;
+  // instrumentation
+  bool prof = false;
+  std::vector<ProfRec> recs;
+  std::vector<cudaEvent_t> ev_pool;
+  unsigned long long prof_sweeps0 = 0;
+  double kflops_sweep = 0.0;                   // predictor flops per cell per sweep
+  long long launches = 0;                      // kernels launched by this context
+};
+
+namespace {
+
+ader_status fail(ader_ctx* c, ader_status s, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  return s;
+}
+
+#define CK(call)                                                                                   \
+  do {                                                                                             \
+    cudaError_t e_ = (call);                                                                       \
+    if (e_ != cudaSuccess) return fail(c, ADER_ERR_CUDA, "%s failed: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+#define NK(call)                                                                                   \
+  do {                                                                                             \
+    ncclResult_t r_ = (call);                                                                      \
+    if (r_ != ncclSuccess) return fail(c, ADER_ERR_NCCL, "%s failed: %s", #call, g_nccl.GetErrorString(r_)); \
+  } while (0)
+
+int nvar_of(int system, int dim) { return system == ADER_MHD_GLM ? 9 : dim + 2; }
+
+ader_status validate(const ader_config* cfg, std::string& why) {
+  char b[256];
+  auto bad = [&](const char* s) { why = s; return ADER_ERR_CONFIG; };
+  if (cfg->abi_version != ADER_ABI_VERSION) return bad("abi_version mismatch");
+  if (cfg->dim != 2 && cfg->dim != 3) return bad("dim must be 2 or 3");
+  if (cfg->system != ADER_EULER && cfg->system != ADER_MHD_GLM) return bad("unknown system");
+  if (cfg->degree < 2 || cfg->degree > 3) return bad("degree M must be 2 or 3");
+  if (!supported(cfg->dim, cfg->degree, cfg->system)) return bad("(dim, degree, system) not compiled (3D needs M=2)");
+  for (int k = 0; k < cfg->dim; ++k)
+    if (cfg->n0[k] < 1) return bad("n0 must be >= 1 on every axis");
+  if (cfg->dim == 2 && cfg->n0[2] != 1) return bad("n0[2] must be 1 in 2D");
+  for (int k = 0; k < cfg->dim; ++k)
+    if (!(cfg->hi[k] > cfg->lo[k])) return bad("hi must exceed lo");
+  for (int k = 0; k < 2 * cfg->dim; ++k)
+    if (cfg->bc[k] != ADER_BC_PERIODIC && cfg->bc[k] != ADER_BC_TRANSMISSIVE) return bad("bad bc");
+  for (int k = 0; k < cfg->dim; ++k)
+    if ((cfg->bc[2 * k] == ADER_BC_PERIODIC) != (cfg->bc[2 * k + 1] == ADER_BC_PERIODIC))
+      return bad("periodic bc must be set on both sides of an axis");
+  if (cfg->lmax < 0 || cfg->lmax > 7) return bad("lmax out of range");
+  if (cfg->lmax > 0 && cfg->refine_factor < cfg->degree) return bad("refine_factor r must be >= M (P:539-541)");
+  if (cfg->lmax > 0) return ADER_ERR_UNSUPPORTED;
+  if (!(cfg->gamma > 1.0)) return bad("gamma must exceed 1");
+  if (!(cfg->cfl > 0.0)) return bad("cfl must be positive");
+  if (cfg->world_size < 1 || cfg->world_size > 8) return bad("world_size must be in 1..8");
+  if (cfg->rank < 0 || cfg->rank >= cfg->world_size) return bad("rank out of range");
+  if (cfg->ic_quad < 0 || cfg->ic_quad > 8) return bad("ic_quad must be in 0..8");
+  if (cfg->pred_max_sweeps < 0 || cfg->pred_max_sweeps > 1000) return bad("pred_max_sweeps out of range");
+  (void)b;
+  return ADER_OK;
+}
+
+// Process grid minimising the halo surface of the largest block.
+void process_grid(const ader_config* cfg, int dims[3]) {
+  const int ws = cfg->world_size;
+  double best = 1e300;
+  dims[0] = ws; dims[1] = 1; dims[2] = 1;
+  for (int px = 1; px <= ws; ++px)
+    for (int py = 1; px * py <= ws; ++py) {
+      if (ws % (px * py)) continue;
+      const int pz = ws / (px * py);
+      if (cfg->dim == 2 && pz != 1) continue;
+      const int p[3] = {px, py, pz};
+      double e[3], surf = 0.0;
+      bool ok = true;
+      for (int k = 0; k < 3; ++k) {
+        if (p[k] > cfg->n0[k]) ok = false;
+        e[k] = std::ceil((double)cfg->n0[k] / p[k]);
+      }
+      if (!ok) continue;
+      if (cfg->dim == 2) surf = e[0] + e[1];
+      else surf = e[0] * e[1] + e[1] * e[2] + e[0] * e[2];
+      if (surf < best - 1e-9) { best = surf; dims[0] = px; dims[1] = py; dims[2] = pz; }
+    }
+}
+
+void partition(const ader_config* cfg, int rank, ader_partition_info* pi) {
+  std::memset(pi, 0, sizeof(*pi));
+  process_grid(cfg, pi->dims);
+  int r = rank;
+  pi->coord[0] = r % pi->dims[0]; r /= pi->dims[0];
+  pi->coord[1] = r % pi->dims[1]; r /= pi->dims[1];
+  pi->coord[2] = r;
+  for (int k = 0; k < 3; ++k) {
+    const long long n = cfg->n0[k];
+    pi->lo[k] = (int)(n * pi->coord[k] / pi->dims[k]);
+    pi->hi[k] = (int)(n * (pi->coord[k] + 1) / pi->dims[k]);
+  }
+  for (int k = 0; k < 3; ++k)
+    for (int side = 0; side < 2; ++side) {
+      int cc[3] = {pi->coord[0], pi->coord[1], pi->coord[2]};
+      cc[k] += side ? 1 : -1;
+      const bool periodic = k < cfg->dim && cfg->bc[2 * k] == ADER_BC_PERIODIC;
+      if (k >= cfg->dim) { pi->nbr[2 * k + side] = -1; continue; }
+      if (cc[k] < 0 || cc[k] >= pi->dims[k]) {
+        if (!periodic) { pi->nbr[2 * k + side] = -1; continue; }
+        cc[k] = (cc[k] + pi->dims[k]) % pi->dims[k];
+      }
+      pi->nbr[2 * k + side] = cc[0] + pi->dims[0] * (cc[1] + pi->dims[1] * cc[2]);
+    }
+  pi->halo = cfg->degree + 1;
+}
+
+Box make_box(int x0, int x1, int y0, int y1, int z0, int z1) {
+  Box b;
+  b.lo[0] = x0; b.lo[1] = y0; b.lo[2] = z0;
+  b.ext[0] = std::max(0, x1 - x0); b.ext[1] = std::max(0, y1 - y0); b.ext[2] = std::max(0, z1 - z0);
+  return b;
+}
+
+// owned block in padded coordinates
+Box owned(const ader_ctx* c) {
+  const int H = c->H, zH = c->d == 3 ? H : 0;
+  return make_box(H, H + c->n[0], H, H + c->n[1], zH, zH + c->n[2]);
+}
+// block grown by g cells on every active axis
+Box grown(const ader_ctx* c, int g) {
+  const int H = c->H, zH = c->d == 3 ? H : 0, gz = c->d == 3 ? g : 0;
+  return make_box(H - g, H + c->n[0] + g, H - g, H + c->n[1] + g, zH - gz, zH + c->n[2] + gz);
+}
+
+// ---- instrumentation -------------------------------------------------------
+cudaEvent_t get_event(ader_ctx* c) {
+  if (!c->ev_pool.empty()) { cudaEvent_t e = c->ev_pool.back(); c->ev_pool.pop_back(); return e; }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+struct Scope {
+  ader_ctx* c; ProfRec r{};
+  Scope(ader_ctx* c_, int kind, double flops) : c(c_) {
+    if (!c->prof) return;
+    r.kind = kind; r.flops = flops;
+    r.e0 = get_event(c); r.e1 = get_event(c);
+    cudaEventRecord(r.e0, c->k.stream);
+  }
+  ~Scope() {
+    if (!c->prof) return;
+    cudaEventRecord(r.e1, c->k.stream);
+    c->recs.push_back(r);
+  }
+};
+
+// Algorithmic FP64 flop model (FMA = 2, add/mul/div/sqrt = 1); see DESIGN.md.
+double weno_problem_flops(int M) {
+  const int N = M + 1, nS = (M % 2 == 0) ? 3 : 4;
+  // per stencil: rec N*N FMA, sigma N*N FMA + N FMA, (sig+eps) 1 + 3 squarings + 1 div + 1 add
+  // blend: 1 div, N*nS (mul + FMA)
+  return nS * (2.0 * N * N + 2.0 * N * N + 2.0 * N + 6.0) + 1.0 + 3.0 * N * nS;
+}
+double flux_eval_flops(int sys, int d) {
+  // pointwise physical fluxes in all d directions incl. the dt/dx scaling
+  if (sys == ADER_EULER) return 1 + d + 2 * d + 4 + 1 + d * (d + 2) + d * (d + 2);
+  return 40 + d * 30 + d * 9;
+}
+double pred_sweep_flops(const ader_ctx* c) {
+  // NST flux evaluations + NV*NST*(2 d N [D contractions] + 2 N [T_tau] + 1 [dq])
+  return c->NST * flux_eval_flops(c->cfg.system, c->d) + (double)c->nv * c->NST * (2.0 * c->d * c->N + 2.0 * c->N + 1.0);
+}
+double face_flops(const ader_ctx* c) {
+  const double rus = (c->cfg.system == ADER_EULER) ? 2.0 * (12 + 2 * c->d) + 4.0 * c->nv : 2.0 * 90 + 4.0 * c->nv;
+  return c->NS * (4.0 * c->nv * c->N + rus + 2.0 * c->nv + 2.0);
+}
+
+// ---- ghost layers ------------------------------------------------------------
+ader_status fill_halo(ader_ctx* c, double* u) {
+  Scope sc(c, ADER_K_HALO, 0.0);
+  const int H = c->H;
+  for (int a = 0; a < c->d; ++a) {
+    // extents of the other axes: processed axes full, unprocessed interior
+    int lo[3], hi[3];
+    for (int b = 0; b < 3; ++b) {
+      if (b >= c->d) { lo[b] = 0; hi[b] = 1; continue; }
+      if (b < a) { lo[b] = 0; hi[b] = c->P[b]; }
+      else { lo[b] = H; hi[b] = H + c->n[b]; }
+    }
+    auto slab = [&](int a0, int a1) {
+      int l[3] = {lo[0], lo[1], lo[2]}, h[3] = {hi[0], hi[1], hi[2]};
+      l[a] = a0; h[a] = a1;
+      return make_box(l[0], h[0], l[1], h[1], l[2], h[2]);
+    };
+    const Box rlo = slab(0, H), rhi = slab(H + c->n[a], 2 * H + c->n[a]);
+    const Box slo = slab(H, 2 * H), shi = slab(c->n[a], c->n[a] + H);
+    const int nb_lo = c->part.nbr[2 * a], nb_hi = c->part.nbr[2 * a + 1];
+    const bool remote_lo = nb_lo >= 0 && nb_lo != c->cfg.rank;
+    const bool remote_hi = nb_hi >= 0 && nb_hi != c->cfg.rank;
+    if (remote_lo || remote_hi) {
+      if (remote_lo) launch_pack(c->k, u, slo, c->sendb[2 * a]);
+      if (remote_hi) launch_pack(c->k, u, shi, c->sendb[2 * a + 1]);
+      const size_t cnt = (size_t)rlo.count() * c->nv;
+      NK(g_nccl.GroupStart());
+      // order per peer: (send low, recv high, send high, recv low) on every rank
+      if (remote_lo) NK(g_nccl.Send(c->sendb[2 * a], cnt, ncclDouble, nb_lo, c->comm, c->k.stream));
+      if (remote_hi) NK(g_nccl.Recv(c->recvb[2 * a + 1], cnt, ncclDouble, nb_hi, c->comm, c->k.stream));
+      if (remote_hi) NK(g_nccl.Send(c->sendb[2 * a + 1], cnt, ncclDouble, nb_hi, c->comm, c->k.stream));
+      if (remote_lo) NK(g_nccl.Recv(c->recvb[2 * a], cnt, ncclDouble, nb_lo, c->comm, c->k.stream));
+      NK(g_nccl.GroupEnd());
+      if (remote_lo) launch_unpack(c->k, u, rlo, c->recvb[2 * a]);
+      if (remote_hi) launch_unpack(c->k, u, rhi, c->recvb[2 * a + 1]);
+    }
+    // local sides: periodic wrap onto ourselves, or transmissive copy (reading R5)
+    const bool periodic = c->cfg.bc[2 * a] == ADER_BC_PERIODIC;
+    if (!remote_lo) launch_fill_axis(c->k, u, rlo, a, (periodic && nb_lo >= 0) ? 0 : 1, H, c->n[a]);
+    if (!remote_hi) launch_fill_axis(c->k, u, rhi, a, (periodic && nb_hi >= 0) ? 0 : 1, H, c->n[a]);
+  }
+  return ADER_OK;
+}
+
+// ---- one stage each ----------------------------------------------------------
+void run_weno(ader_ctx* c) {
+  // x sweep on the rows needed by the y (and z) sweeps, ..., last sweep on block+1
+  const int H = c->H, M = c->M;
+  const int zH = c->d == 3 ? H : 0;
+  const int nx = c->n[0], ny = c->n[1], nz = c->n[2];
+  double* dst_last = c->w;
+  if (c->d == 2) {
+    const Box rx = make_box(H - 1, H + nx + 1, H - 1 - M, H + ny + 1 + M, 0, 1);
+    const Box ry = grown(c, 1);
+    Scope s(c, ADER_K_WENO, weno_problem_flops(M) * (rx.count() * c->nv + ry.count() * c->nv * c->N));
+    launch_weno_sweep(c->k, 0, c->u, c->wx, rx);
+    launch_weno_sweep(c->k, 1, c->wx, dst_last, ry);
+  } else {
+    const Box rx = make_box(H - 1, H + nx + 1, H - 1 - M, H + ny + 1 + M, zH - 1 - M, zH + nz + 1 + M);
+    const Box ry = make_box(H - 1, H + nx + 1, H - 1, H + ny + 1, zH - 1 - M, zH + nz + 1 + M);
+    const Box rz = grown(c, 1);
+    Scope s(c, ADER_K_WENO,
+            weno_problem_flops(M) * (rx.count() * c->nv + ry.count() * c->nv * c->N + rz.count() * c->nv * c->N * c->N));
+    launch_weno_sweep(c->k, 0, c->u, c->wx, rx);
+    launch_weno_sweep(c->k, 1, c->wx, c->wxy, ry);
+    launch_weno_sweep(c->k, 2, c->wxy, dst_last, rz);
+  }
+}
+
+void run_predictor(ader_ctx* c, double dt) {
+  const Box r = grown(c, 1);
+  double dtdx[3] = {0, 0, 0};
+  for (int k = 0; k < c->d; ++k) dtdx[k] = dt / c->dx[k];
+  Scope s(c, ADER_K_PRED, 0.0);   // flops from the sweep counter (ader_kernel_stats)
+  launch_predictor(c->k, c->w, c->q, r, dtdx, c->cfg.pred_tol, c->cfg.pred_max_sweeps, c->cnt);
+}
+
+void face_boxes(const ader_ctx* c, Box fb[3]) {
+  const int H = c->H, zH = c->d == 3 ? H : 0;
+  for (int dir = 0; dir < 3; ++dir) {
+    int e[3] = {c->n[0], c->n[1], c->n[2]};
+    if (dir < c->d) e[dir] += 1;
+    fb[dir] = make_box(H, H + e[0], H, H + e[1], zH, zH + e[2]);
+    if (dir >= c->d) fb[dir] = make_box(0, 0, 0, 0, 0, 0);
+  }
+}
+
+void run_flux(ader_ctx* c) {
+  Box fb[3];
+  face_boxes(c, fb);
+  long long nf = 0;
+  for (int k = 0; k < c->d; ++k) nf += fb[k].count();
+  Scope s(c, ADER_K_FLUX, face_flops(c) * nf);
+  launch_face_flux(c->k, c->q, c->F, fb, c->cnt);
+}
+
+void run_update(ader_ctx* c, double dt) {
+  const Box r = owned(c);
+  double dtdx[3] = {0, 0, 0};
+  for (int k = 0; k < c->d; ++k) dtdx[k] = dt / c->dx[k];
+  Scope s(c, ADER_K_UPDATE, (double)r.count() * c->nv * 3.0 * c->d);
+  launch_update(c->k, c->u, c->F, r, dtdx, c->inv_dx, c->cnt);
+}
+
+ader_status check_errors(ader_ctx* c) {
+  if (c->hcnt->err_code == 0) return ADER_OK;
+  const long long cell = (long long)c->hcnt->err_cell;
+  const long long x = cell % c->P[0], y = (cell / c->P[0]) % c->P[1], z = cell / ((long long)c->P[0] * c->P[1]);
+  const int zH = c->d == 3 ? c->H : 0;
+  const char* what = c->hcnt->err_code == 1 ? "inadmissible state (rho<=0 or p<=0)" : "predictor reached pred_max_sweeps";
+  const char* stage[] = {"?", "predictor", "face flux", "update", "cfl"};
+  return fail(c, ADER_ERR_SOLVER, "%s in %s at cell (%lld,%lld,%lld), level 0, t=%.17g", what,
+              stage[std::min(4, std::max(0, c->hcnt->err_stage))], x - c->H + c->part.lo[0], y - c->H + c->part.lo[1],
+              z - zH + c->part.lo[2], c->t);
+}
+
+// CFL speed of the current state, reduced over ranks; synchronises the stream.
+ader_status global_speed(ader_ctx* c, double* speed) {
+  if (!c->speed_valid) {
+    CK(cudaMemsetAsync(&c->cnt->speed_bits, 0, sizeof(unsigned long long), c->k.stream));
+    Scope s(c, ADER_K_OTHER, 0.0);
+    launch_cfl_speed(c->k, c->u, owned(c), c->inv_dx, c->cnt);
+  }
+  if (c->comm)
+    NK(g_nccl.AllReduce(&c->cnt->speed_bits, &c->cnt->speed_bits, 1, ncclUint64, ncclMax, c->comm, c->k.stream));
+  CK(cudaMemcpyAsync(c->hcnt, c->cnt, sizeof(DevCounters), cudaMemcpyDeviceToHost, c->k.stream));
+  CK(cudaStreamSynchronize(c->k.stream));
+  ader_status st = check_errors(c);
+  if (st != ADER_OK) return st;
+  unsigned long long b = c->hcnt->speed_bits;
+  double s;
+  std::memcpy(&s, &b, sizeof(s));
+  *speed = s;
+  c->speed_valid = true;
+  return ADER_OK;
+}
+
+void free_ctx(ader_ctx* c) {
+  if (!c) return;
+  if (c->k.stream) cudaStreamSynchronize(c->k.stream);
+  double* bufs[] = {c->u, c->wx, c->wxy, c->w, c->q, c->F, c->stage};
+  for (double* b : bufs)
+    if (b) cudaFree(b);
+  for (int i = 0; i < 6; ++i) {
+    if (c->sendb[i]) cudaFree(c->sendb[i]);
+    if (c->recvb[i]) cudaFree(c->recvb[i]);
+  }
+  if (c->cnt) cudaFree(c->cnt);
+  if (c->hcnt) cudaFreeHost(c->hcnt);
+  for (auto& r : c->recs) { cudaEventDestroy(r.e0); cudaEventDestroy(r.e1); }
+  for (auto e : c->ev_pool) cudaEventDestroy(e);
+  if (c->comm) g_nccl.CommDestroy(c->comm);
+  if (c->own_stream) cudaStreamDestroy(c->own_stream);
+  delete c;
+}
+
+// Gauss-Legendre rule on [0,1] for the IC averages (closed forms up to 4 points,
+// Newton on the Legendre recurrence beyond).
+void gl_rule(int Q, double* x, double* w) {
+  if (Q == 1) { x[0] = 0.5; w[0] = 1.0; return; }
+  if (Q == 2) { const double h = std::sqrt(3.0) / 6.0; x[0] = 0.5 - h; x[1] = 0.5 + h; w[0] = w[1] = 0.5; return; }
+  if (Q == 3 || Q == 4) {
+    DevTables t;
+    build_tables(Q - 1, &t);
+    for (int i = 0; i < Q; ++i) { x[i] = t.lam[i]; w[i] = t.w[i]; }
+    return;
+  }
+  for (int i = 0; i < Q; ++i) {
+    double z = -std::cos(M_PI * (i + 0.75) / (Q + 0.5)), dp = 1.0;
+    for (int it = 0; it < 60; ++it) {
+      double p0 = 1.0, p1 = z;
+      for (int k = 2; k <= Q; ++k) { const double p2 = ((2 * k - 1) * z * p1 - (k - 1) * p0) / k; p0 = p1; p1 = p2; }
+      dp = Q * (z * p1 - p0) / (z * z - 1.0);
+      const double dz = p1 / dp;
+      z -= dz;
+      if (std::fabs(dz) < 1e-16) break;
+    }
+    x[i] = 0.5 * (1.0 + z);
+    w[i] = 1.0 / ((1.0 - z * z) * dp * dp);
+  }
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+static thread_local std::string g_create_err = "null context";
+const char* ader_last_error(const ader_ctx* c) { return c ? c->err.c_str() : g_create_err.c_str(); }
+
+ader_status ader_partition(const ader_config* cfg, int32_t rank, ader_partition_info* out) {
+  if (!cfg || !out) return ADER_ERR_ARG;
+  std::string why;
+  ader_config tmp = *cfg;
+  tmp.rank = 0;
+  ader_status st = validate(&tmp, why);
+  if (st != ADER_OK) return st;
+  if (rank < 0 || rank >= cfg->world_size) return ADER_ERR_ARG;
+  partition(cfg, rank, out);
+  return ADER_OK;
+}
+
+ader_status ader_nccl_unique_id(uint8_t out[128]) {
+  std::string err;
+  if (!out) return ADER_ERR_ARG;
+  if (!g_nccl.load(err)) return ADER_ERR_NCCL;
+  ncclUniqueId id;
+  if (g_nccl.GetUniqueId(&id) != ncclSuccess) return ADER_ERR_NCCL;
+  std::memcpy(out, &id, 128);
+  return ADER_OK;
+}
+
+static ader_status create_impl(const ader_config* cfg, ader_ctx** out);
+
+ader_status ader_create(const ader_config* cfg, ader_ctx** out) {
+  if (!cfg || !out) return ADER_ERR_ARG;
+  *out = nullptr;
+  std::string why;
+  ader_status st = validate(cfg, why);
+  if (st != ADER_OK) {
+    g_create_err = st == ADER_ERR_UNSUPPORTED ? "configuration not supported yet (lmax > 0)" : why;
+    return st;
+  }
+  ader_ctx* c = nullptr;
+  st = create_impl(cfg, &c);
+  if (st != ADER_OK) {
+    g_create_err = c ? c->err : "allocation failed";
+    free_ctx(c);
+    return st;
+  }
+  *out = c;
+  return ADER_OK;
+}
+
+static ader_status create_impl(const ader_config* cfg, ader_ctx** out) {
+  ader_partition_info pi;
+  partition(cfg, cfg->rank, &pi);
+  const int H = cfg->degree + 1;
+  for (int k = 0; k < cfg->dim; ++k) {
+    const bool remote = (pi.nbr[2 * k] >= 0 && pi.nbr[2 * k] != cfg->rank) ||
+                        (pi.nbr[2 * k + 1] >= 0 && pi.nbr[2 * k + 1] != cfg->rank);
+    if (remote && pi.hi[k] - pi.lo[k] < H) {
+      g_create_err = "rank block thinner than the ghost layer (M+1)";
+      return ADER_ERR_CONFIG;
+    }
+  }
+  ader_ctx* c = new ader_ctx();
+  *out = c;
+  c->cfg = *cfg;
+  c->part = pi;
+  c->d = cfg->dim; c->M = cfg->degree; c->N = c->M + 1;
+  c->nv = nvar_of(cfg->system, cfg->dim);
+  c->NS = 1;
+  for (int k = 0; k < c->d; ++k) c->NS *= c->N;
+  c->NST = c->NS * c->N;
+  c->H = H;
+  if (c->cfg.pred_tol <= 0) c->cfg.pred_tol = 1e-13;
+  if (c->cfg.pred_max_sweeps <= 0) c->cfg.pred_max_sweeps = 32;
+  if (c->cfg.ic_quad <= 0) c->cfg.ic_quad = c->N;
+  for (int k = 0; k < 3; ++k) {
+    c->n[k] = (k < c->d) ? pi.hi[k] - pi.lo[k] : 1;
+    c->P[k] = (k < c->d) ? c->n[k] + 2 * H : 1;
+    c->dx[k] = (k < c->d) ? (cfg->hi[k] - cfg->lo[k]) / cfg->n0[k] : 1.0;
+    c->inv_dx[k] = (k < c->d) ? 1.0 / c->dx[k] : 0.0;
+  }
+  c->ncell = (long long)c->P[0] * c->P[1] * c->P[2];
+  if (cfg->device >= 0) CK(cudaSetDevice(cfg->device));
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, dev));
+  if (prop.major != 10) {
+    return fail(c, ADER_ERR_CUDA, "device %d is sm_%d%d; this library is built for sm_100a", dev, prop.major, prop.minor);
+  }
+  CK(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+  if (!build_tables(c->M, &c->k.tab)) return fail(c, ADER_ERR_CONFIG, "no tables for M=%d", c->M);
+  c->k.D = c->d; c->k.M = c->M; c->k.SYS = cfg->system; c->k.NV = c->nv;
+  c->k.sy = c->P[0]; c->k.sz = (long long)c->P[0] * c->P[1];
+  c->k.ncell = c->ncell;
+  c->k.gamma = cfg->gamma; c->k.ch = cfg->ch;
+  c->k.stream = c->own_stream;
+  c->k.launches = &c->launches;
+  const size_t nc = (size_t)c->ncell;
+  auto alloc = [&](double** p, size_t n) { return cudaMalloc(p, n * sizeof(double)); };
+  CK(alloc(&c->u, nc * c->nv));
+  CK(alloc(&c->wx, nc * c->nv * c->N));
+  if (c->d == 3) CK(alloc(&c->wxy, nc * c->nv * c->N * c->N));
+  CK(alloc(&c->w, nc * c->nv * c->NS));
+  CK(alloc(&c->q, nc * c->nv * c->NST));
+  CK(alloc(&c->F, nc * c->nv * c->d));
+  CK(alloc(&c->stage, (size_t)c->n[0] * c->n[1] * c->n[2] * c->nv * std::max(c->NST, c->d)));
+  CK(cudaMemset(c->u, 0, nc * c->nv * sizeof(double)));
+  CK(cudaMemset(c->F, 0, nc * c->nv * c->d * sizeof(double)));
+  CK(cudaMalloc(&c->cnt, sizeof(DevCounters)));
+  CK(cudaMemset(c->cnt, 0, sizeof(DevCounters)));
+  CK(cudaMallocHost(&c->hcnt, sizeof(DevCounters)));
+  std::memset(c->hcnt, 0, sizeof(DevCounters));
+  // halo buffers (largest slab over axes)
+  long long cap = 0;
+  for (int a = 0; a < c->d; ++a) {
+    long long s = H;
+    for (int b = 0; b < c->d; ++b)
+      if (b != a) s *= c->P[b];
+    cap = std::max(cap, s);
+  }
+  c->halo_cap = cap * c->nv;
+  if (cfg->world_size > 1) {
+    for (int i = 0; i < 2 * c->d; ++i) {
+      CK(alloc(&c->sendb[i], (size_t)c->halo_cap));
+      CK(alloc(&c->recvb[i], (size_t)c->halo_cap));
+    }
+    std::string err;
+    if (!g_nccl.load(err)) return fail(c, ADER_ERR_NCCL, "%s", err.c_str());
+    ncclUniqueId id;
+    std::memcpy(&id, cfg->nccl_id, sizeof(id));
+    ncclResult_t r = g_nccl.CommInitRank(&c->comm, cfg->world_size, id, cfg->rank);
+    if (r != ncclSuccess) {
+      c->comm = nullptr;
+      return fail(c, ADER_ERR_NCCL, "ncclCommInitRank: %s", g_nccl.GetErrorString(r));
+    }
+  }
+  c->kflops_sweep = pred_sweep_flops(c);
+  return ADER_OK;
+}
+
+void ader_destroy(ader_ctx* c) { free_ctx(c); }
+
+ader_status ader_set_stream(ader_ctx* c, void* s) {
+  if (!c) return ADER_ERR_ARG;
+  c->k.stream = s ? (cudaStream_t)s : c->own_stream;
+  return ADER_OK;
+}
+
+double ader_time(const ader_ctx* c) { return c ? c->t : 0.0; }
+
+ader_status ader_set_initial(ader_ctx* c, ader_ic_fn ic, void* user) {
+  if (!c || !ic) return ADER_ERR_ARG;
+  const int Q = c->cfg.ic_quad, d = c->d;
+  double qx[16], qw[16];
+  gl_rule(Q, qx, qw);
+  int nq = 1;
+  for (int k = 0; k < d; ++k) nq *= Q;
+  std::vector<double> wq(nq);
+  for (int g = 0; g < nq; ++g) {
+    const int gi[3] = {g % Q, (g / Q) % Q, g / (Q * Q)};
+    double wg = 1.0;
+    for (int k = 0; k < d; ++k) wg *= qw[gi[k]];
+    wq[g] = wg;
+  }
+  const long long ncells = (long long)c->n[0] * c->n[1] * c->n[2];
+  const long long chunk = std::max<long long>(1, std::min<long long>(ncells, (1 << 22) / nq));
+  std::vector<double> x((size_t)chunk * nq * 3), pr((size_t)chunk * nq * 9);
+  double *dprim = nullptr, *dwq = nullptr;
+  CK(cudaMalloc(&dprim, pr.size() * sizeof(double)));
+  CK(cudaMalloc(&dwq, nq * sizeof(double)));
+  CK(cudaMemcpy(dwq, wq.data(), nq * sizeof(double), cudaMemcpyHostToDevice));
+  for (long long c0 = 0; c0 < ncells; c0 += chunk) {
+    const long long ncur = std::min(chunk, ncells - c0);
+    for (long long i = 0; i < ncur; ++i) {
+      const long long lin = c0 + i;
+      const long long ii[3] = {lin % c->n[0] + c->part.lo[0], (lin / c->n[0]) % c->n[1] + c->part.lo[1],
+                               lin / ((long long)c->n[0] * c->n[1]) + c->part.lo[2]};
+      for (int g = 0; g < nq; ++g) {
+        const int gi[3] = {g % Q, (g / Q) % Q, g / (Q * Q)};
+        double* xp = &x[(i * nq + g) * 3];
+        for (int k = 0; k < 3; ++k)
+          xp[k] = (k < d) ? c->cfg.lo[k] + ((double)ii[k] + qx[gi[k]]) * c->dx[k] : 0.0;
+      }
+    }
+    std::fill(pr.begin(), pr.begin() + ncur * nq * 9, 0.0);
+    ic(x.data(), ncur * nq, pr.data(), user);
+    CK(cudaMemcpyAsync(dprim, pr.data(), (size_t)ncur * nq * 9 * sizeof(double), cudaMemcpyHostToDevice, c->k.stream));
+    launch_ic_average(c->k, c->u, dprim, dwq, nq, c0, ncur, c->n, c->H);
+    CK(cudaStreamSynchronize(c->k.stream));
+  }
+  cudaFree(dprim);
+  cudaFree(dwq);
+  c->t = 0.0;
+  c->speed_valid = false;
+  return ADER_OK;
+}
+
+ader_status ader_set_cells(ader_ctx* c, const double* u_host, int64_t n_cells) {
+  if (!c || !u_host) return ADER_ERR_ARG;
+  const Box b = owned(c);
+  if (n_cells != b.count()) return fail(c, ADER_ERR_ARG, "n_cells %lld != owned %lld", (long long)n_cells, b.count());
+  CK(cudaMemcpyAsync(c->stage, u_host, (size_t)n_cells * c->nv * sizeof(double), cudaMemcpyHostToDevice, c->k.stream));
+  launch_scatter(c->k, c->u, c->nv, b, c->stage);
+  CK(cudaStreamSynchronize(c->k.stream));
+  c->speed_valid = false;
+  return ADER_OK;
+}
+
+ader_status ader_get_state(const ader_ctx* cc, double* u_host, int64_t capacity) {
+  ader_ctx* c = const_cast<ader_ctx*>(cc);
+  if (!c || !u_host) return ADER_ERR_ARG;
+  const Box b = owned(c);
+  if (capacity < b.count()) return fail(c, ADER_ERR_ARG, "capacity too small");
+  launch_gather(c->k, c->u, c->nv, b, c->stage);
+  CK(cudaMemcpyAsync(u_host, c->stage, (size_t)b.count() * c->nv * sizeof(double), cudaMemcpyDeviceToHost, c->k.stream));
+  CK(cudaStreamSynchronize(c->k.stream));
+  return ADER_OK;
+}
+
+ader_status ader_get_cells(const ader_ctx* cc, ader_cell* out, int64_t capacity, int64_t* n) {
+  ader_ctx* c = const_cast<ader_ctx*>(cc);
+  if (!c || !n) return ADER_ERR_ARG;
+  const Box b = owned(c);
+  *n = b.count();
+  if (!out) return ADER_OK;
+  if (capacity < b.count()) return fail(c, ADER_ERR_ARG, "capacity too small");
+  std::vector<double> u((size_t)b.count() * c->nv);
+  ader_status st = ader_get_state(c, u.data(), b.count());
+  if (st != ADER_OK) return st;
+  long long i = 0;
+  for (int z = 0; z < c->n[2]; ++z)
+    for (int y = 0; y < c->n[1]; ++y)
+      for (int x = 0; x < c->n[0]; ++x, ++i) {
+        ader_cell& e = out[i];
+        std::memset(&e, 0, sizeof(e));
+        e.level = 0; e.status = 0;
+        e.idx[0] = x + c->part.lo[0]; e.idx[1] = y + c->part.lo[1]; e.idx[2] = z + c->part.lo[2];
+        for (int v = 0; v < c->nv; ++v) e.u[v] = u[i * c->nv + v];
+      }
+  return ADER_OK;
+}
+
+ader_status ader_step(ader_ctx* c, double t_end, int64_t max_macro_steps, ader_step_report* rep) {
+  if (!c) return ADER_ERR_ARG;
+  const auto w0 = std::chrono::steady_clock::now();
+  ader_step_report r;
+  std::memset(&r, 0, sizeof(r));
+  CK(cudaMemcpyAsync(c->hcnt, c->cnt, sizeof(DevCounters), cudaMemcpyDeviceToHost, c->k.stream));
+  CK(cudaStreamSynchronize(c->k.stream));
+  const unsigned long long sw0 = c->hcnt->sweeps, pc0 = c->hcnt->cells;
+  const long long owned_cells = owned(c).count();
+  ader_status st = ADER_OK;
+  while (r.macro_steps < max_macro_steps && c->t < t_end) {
+    st = fill_halo(c, c->u);
+    if (st != ADER_OK) break;
+    run_weno(c);
+    double speed = 0.0;
+    st = global_speed(c, &speed);   // overlaps the WENO sweeps
+    if (st != ADER_OK) break;
+    double dt = c->cfg.cfl / speed;   // reading R1
+    if (!(dt > 0.0) || !std::isfinite(dt)) { st = fail(c, ADER_ERR_SOLVER, "invalid dt %g at t=%.17g", dt, c->t); break; }
+    if (c->t + dt > t_end) dt = t_end - c->t;
+    run_predictor(c, dt);
+    run_flux(c);
+    CK(cudaMemsetAsync(&c->cnt->speed_bits, 0, sizeof(unsigned long long), c->k.stream));
+    run_update(c, dt);
+    c->speed_valid = true;   // computed by the update of the new state
+    c->t += dt;
+    r.dt0 = dt;
+    r.macro_steps++;
+  }
+  CK(cudaMemcpyAsync(c->hcnt, c->cnt, sizeof(DevCounters), cudaMemcpyDeviceToHost, c->k.stream));
+  CK(cudaStreamSynchronize(c->k.stream));
+  if (st == ADER_OK) st = check_errors(c);
+  r.t = c->t;
+  r.cell_updates = r.macro_steps * owned_cells;
+  r.updates_per_level[0] = r.cell_updates;
+  r.pred_sweeps_total = (int64_t)(c->hcnt->sweeps - sw0);
+  r.pred_cells = (int64_t)(c->hcnt->cells - pc0);
+  r.pred_sweeps_max = c->hcnt->sweeps_max;
+  // conserved totals (diagnostic): block partials on device, summed in order here
+  {
+    const Box b = owned(c);
+    double vol = 1.0;
+    for (int k = 0; k < c->d; ++k) vol *= c->dx[k];
+    const int maxb = (int)((b.count() + 255) / 256);
+    double* part = nullptr;
+    if (cudaMalloc(&part, (size_t)maxb * c->nv * sizeof(double)) == cudaSuccess) {
+      const int nb = launch_cons_partials(c->k, c->u, b, vol, part, maxb);
+      std::vector<double> h((size_t)nb * c->nv);
+      cudaMemcpyAsync(h.data(), part, h.size() * sizeof(double), cudaMemcpyDeviceToHost, c->k.stream);
+      cudaStreamSynchronize(c->k.stream);
+      for (int i = 0; i < nb; ++i)
+        for (int v = 0; v < c->nv; ++v) r.cons_total[v] += h[(size_t)i * c->nv + v];
+      cudaFree(part);
+    }
+  }
+  r.wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - w0).count();
+  if (rep) *rep = r;
+  return st;
+}
+
+ader_status ader_refine(ader_ctx* c, ader_step_report* rep) {
+  if (!c) return ADER_ERR_ARG;
+  if (rep) std::memset(rep, 0, sizeof(*rep));
+  return ADER_OK;   // uniform grid: nothing to adapt
+}
+
+ader_status ader_set_profiling(ader_ctx* c, int32_t on) {
+  if (!c) return ADER_ERR_ARG;
+  CK(cudaStreamSynchronize(c->k.stream));
+  for (auto& r : c->recs) { c->ev_pool.push_back(r.e0); c->ev_pool.push_back(r.e1); }
+  c->recs.clear();
+  c->prof = on != 0;
+  CK(cudaMemcpy(c->hcnt, c->cnt, sizeof(DevCounters), cudaMemcpyDeviceToHost));
+  c->prof_sweeps0 = c->hcnt->sweeps;
+  return ADER_OK;
+}
+
+ader_status ader_kernel_stats(ader_ctx* c, double ms[ADER_K_COUNT], int64_t launches[ADER_K_COUNT],
+                              double flops[ADER_K_COUNT]) {
+  if (!c) return ADER_ERR_ARG;
+  CK(cudaStreamSynchronize(c->k.stream));
+  for (int i = 0; i < ADER_K_COUNT; ++i) {
+    if (ms) ms[i] = 0.0;
+    if (launches) launches[i] = 0;
+    if (flops) flops[i] = 0.0;
+  }
+  for (auto& r : c->recs) {
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, r.e0, r.e1));
+    if (ms) ms[r.kind] += t;
+    if (launches) launches[r.kind] += 1;
+    if (flops) flops[r.kind] += r.flops;
+  }
+  CK(cudaMemcpy(c->hcnt, c->cnt, sizeof(DevCounters), cudaMemcpyDeviceToHost));
+  if (flops) flops[ADER_K_PRED] = (double)(c->hcnt->sweeps - c->prof_sweeps0) * c->kflops_sweep;
+  return ADER_OK;
+}
+
+ader_status ader_launch_count(const ader_ctx* c, int64_t* n) {
+  if (!c || !n) return ADER_ERR_ARG;
+  *n = c->launches;
+  return ADER_OK;
+}
+
+ader_status ader_debug_dump(ader_ctx* c, int32_t what, double dt, double* out, int64_t capacity) {
+  if (!c || !out) return ADER_ERR_ARG;
+  const Box b = owned(c);
+  ader_status st = fill_halo(c, c->u);
+  if (st != ADER_OK) return st;
+  run_weno(c);
+  if (what == 0) {
+    if (capacity < b.count() * c->nv * c->NS) return fail(c, ADER_ERR_ARG, "capacity too small");
+    launch_gather(c->k, c->w, c->nv * c->NS, b, c->stage);
+    CK(cudaMemcpyAsync(out, c->stage, (size_t)b.count() * c->nv * c->NS * sizeof(double), cudaMemcpyDeviceToHost, c->k.stream));
+    CK(cudaStreamSynchronize(c->k.stream));
+    return ADER_OK;
+  }
+  run_predictor(c, dt);
+  if (what == 1) {
+    if (capacity < b.count() * c->nv * c->NST) return fail(c, ADER_ERR_ARG, "capacity too small");
+    launch_gather(c->k, c->q, c->nv * c->NST, b, c->stage);
+    CK(cudaMemcpyAsync(out, c->stage, (size_t)b.count() * c->nv * c->NST * sizeof(double), cudaMemcpyDeviceToHost, c->k.stream));
+    CK(cudaStreamSynchronize(c->k.stream));
+    CK(cudaMemcpy(c->hcnt, c->cnt, sizeof(DevCounters), cudaMemcpyDeviceToHost));
+    return check_errors(c);
+  }
+  if (what == 2) {
+    CK(cudaMemsetAsync(c->F, 0, (size_t)c->ncell * c->nv * c->d * sizeof(double), c->k.stream));
+    run_flux(c);
+    const int zH = c->d == 3 ? c->H : 0;
+    const Box e = make_box(c->H, c->H + c->n[0] + 1, c->H, c->H + c->n[1] + 1, zH, zH + c->n[2] + (c->d == 3 ? 1 : 0));
+    if (capacity < e.count() * c->nv * c->d) return fail(c, ADER_ERR_ARG, "capacity too small");
+    double* tmp = nullptr;
+    CK(cudaMalloc(&tmp, (size_t)e.count() * c->nv * sizeof(double)));
+    for (int dir = 0; dir < c->d; ++dir) {
+      launch_gather(c->k, c->F + (size_t)dir * c->ncell * c->nv, c->nv, e, tmp);
+      CK(cudaMemcpyAsync(out + (size_t)dir * e.count() * c->nv, tmp, (size_t)e.count() * c->nv * sizeof(double),
+                         cudaMemcpyDeviceToHost, c->k.stream));
+    }
+    CK(cudaStreamSynchronize(c->k.stream));
+    cudaFree(tmp);
+    CK(cudaMemcpy(c->hcnt, c->cnt, sizeof(DevCounters), cudaMemcpyDeviceToHost));
+    return check_errors(c);
+  }
+  return ADER_ERR_ARG;
+}
+
+}  // extern "C"

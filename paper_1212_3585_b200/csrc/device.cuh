@@ -1,0 +1,213 @@
+// device.cuh — device-side physics and the 1D WENO building block.
+// Citations: P:n = PAPER.md line n.
+#pragma once
+#include <cstdint>
+
+#include "tables.h"
+
+namespace ader {
+
+// ---------------------------------------------------------------------------
+// Physics.  Euler (eq:Euler-system @ P:838-869): nu = D+2 (rho, rho v, E) —
+// reading R7 drops the identically-zero v_z row in 2D.  GLM-MHD in Gaussian
+// units: nu = 9 (rho, rho v[3], E, B[3], psi).
+// All functions return false when the state is inadmissible (rho<=0, p<=0).
+// ---------------------------------------------------------------------------
+template <int SYS, int D> struct Phys;
+
+template <int D> struct Phys<0, D> {
+  static constexpr int NV = D + 2;
+  // fluxes f_dir(u) for every direction at once (predictor nodes)
+  __device__ __forceinline__ static bool fluxes(const double (&u)[NV], double gamma, double /*ch*/,
+                                                double (&f)[D][NV]) {
+    const double rho = u[0];
+    const double ir = 1.0 / rho;
+    double v[D], ke = 0.0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) { v[k] = u[1 + k] * ir; ke += v[k] * u[1 + k]; }
+    const double p = (gamma - 1.0) * (u[D + 1] - 0.5 * ke);
+    const double ep = u[D + 1] + p;
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      f[d][0] = u[1 + d];
+#pragma unroll
+      for (int k = 0; k < D; ++k) f[d][1 + k] = u[1 + d] * v[k];
+      f[d][1 + d] += p;
+      f[d][D + 1] = v[d] * ep;
+    }
+    return rho > 0.0 && p > 0.0;
+  }
+  // flux along one direction + max |eigenvalue|: |v_n| + sqrt(gamma p / rho)
+  template <int DIR>
+  __device__ __forceinline__ static bool flux_speed(const double (&u)[NV], double gamma, double /*ch*/,
+                                                    double (&f)[NV], double& s) {
+    const double rho = u[0];
+    const double ir = 1.0 / rho;
+    double v[D], ke = 0.0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) { v[k] = u[1 + k] * ir; ke += v[k] * u[1 + k]; }
+    const double p = (gamma - 1.0) * (u[D + 1] - 0.5 * ke);
+    f[0] = u[1 + DIR];
+#pragma unroll
+    for (int k = 0; k < D; ++k) f[1 + k] = u[1 + DIR] * v[k];
+    f[1 + DIR] += p;
+    f[D + 1] = v[DIR] * (u[D + 1] + p);
+    const bool ok = rho > 0.0 && p > 0.0;
+    s = fabs(v[DIR]) + sqrt(fmax(gamma * p * ir, 0.0));
+    return ok;
+  }
+  // sum_dir s_dir(u) * inv_dx[dir]  (CFL, reading R1)
+  __device__ __forceinline__ static bool cfl_speed(const double (&u)[NV], double gamma, double /*ch*/,
+                                                   const double (&inv_dx)[3], double& s) {
+    const double rho = u[0];
+    const double ir = 1.0 / rho;
+    double v[D], ke = 0.0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) { v[k] = u[1 + k] * ir; ke += v[k] * u[1 + k]; }
+    const double p = (gamma - 1.0) * (u[D + 1] - 0.5 * ke);
+    const double c = sqrt(fmax(gamma * p * ir, 0.0));
+    s = 0.0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) s += (fabs(v[k]) + c) * inv_dx[k];
+    return rho > 0.0 && p > 0.0;
+  }
+  __device__ __forceinline__ static void prim_to_cons(const double* pr, double gamma, double (&u)[NV]) {
+    const double rho = pr[0];
+    double ke = 0.0;
+    u[0] = rho;
+#pragma unroll
+    for (int k = 0; k < D; ++k) { u[1 + k] = rho * pr[1 + k]; ke += pr[1 + k] * pr[1 + k]; }
+    u[D + 1] = pr[4] / (gamma - 1.0) + 0.5 * rho * ke;
+  }
+};
+
+template <int D> struct Phys<1, D> {
+  static constexpr int NV = 9;
+  static constexpr double k4pi = 0.07957747154594767;   // 1/(4 pi)
+  static constexpr double k8pi = 0.039788735772973836;  // 1/(8 pi)
+  __device__ __forceinline__ static bool prim(const double (&u)[NV], double gamma, double (&v)[3],
+                                              double& p, double& bb, double& vb) {
+    const double ir = 1.0 / u[0];
+    v[0] = u[1] * ir; v[1] = u[2] * ir; v[2] = u[3] * ir;
+    const double ke = v[0] * u[1] + v[1] * u[2] + v[2] * u[3];
+    bb = u[5] * u[5] + u[6] * u[6] + u[7] * u[7];
+    vb = v[0] * u[5] + v[1] * u[6] + v[2] * u[7];
+    p = (gamma - 1.0) * (u[4] - 0.5 * ke - bb * k8pi);
+    return u[0] > 0.0 && p > 0.0;
+  }
+  template <int DIR>
+  __device__ __forceinline__ static void flux_dir(const double (&u)[NV], double ch, const double (&v)[3],
+                                                  double p, double bb, double vb, double (&f)[NV]) {
+    const double pt = p + bb * k8pi;
+    const double Bn = u[5 + DIR];
+    f[0] = u[1 + DIR];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) f[1 + k] = u[1 + DIR] * v[k] - Bn * u[5 + k] * k4pi;
+    f[1 + DIR] += pt;
+    f[4] = v[DIR] * (u[4] + pt) - Bn * vb * k4pi;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) f[5 + k] = v[DIR] * u[5 + k] - Bn * v[k];
+    f[5 + DIR] += u[8];
+    f[8] = ch * ch * Bn;
+  }
+  __device__ __forceinline__ static double fast_speed(const double (&u)[NV], double gamma, double ch,
+                                                      const double (&v)[3], double p, double bb, int dir) {
+    const double ir = 1.0 / u[0];
+    const double a2 = gamma * p * ir;
+    const double b2 = bb * k4pi * ir;
+    const double bn2 = u[5 + dir] * u[5 + dir] * k4pi * ir;
+    const double s = a2 + b2;
+    const double disc = fmax(s * s - 4.0 * a2 * bn2, 0.0);
+    const double cf = sqrt(0.5 * (s + sqrt(disc)));
+    return fmax(fabs(v[dir]) + cf, ch);
+  }
+  __device__ __forceinline__ static bool fluxes(const double (&u)[NV], double gamma, double ch,
+                                                double (&f)[D][NV]) {
+    double v[3], p, bb, vb;
+    const bool ok = prim(u, gamma, v, p, bb, vb);
+    flux_dir<0>(u, ch, v, p, bb, vb, f[0]);
+    flux_dir<1>(u, ch, v, p, bb, vb, f[1]);
+    if constexpr (D == 3) flux_dir<2>(u, ch, v, p, bb, vb, f[2]);
+    return ok;
+  }
+  template <int DIR>
+  __device__ __forceinline__ static bool flux_speed(const double (&u)[NV], double gamma, double ch,
+                                                    double (&f)[NV], double& s) {
+    double v[3], p, bb, vb;
+    const bool ok = prim(u, gamma, v, p, bb, vb);
+    flux_dir<DIR>(u, ch, v, p, bb, vb, f);
+    s = fast_speed(u, gamma, ch, v, fmax(p, 0.0), bb, DIR);
+    return ok;
+  }
+  __device__ __forceinline__ static bool cfl_speed(const double (&u)[NV], double gamma, double ch,
+                                                   const double (&inv_dx)[3], double& s) {
+    double v[3], p, bb, vb;
+    const bool ok = prim(u, gamma, v, p, bb, vb);
+    s = 0.0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) s += fast_speed(u, gamma, ch, v, fmax(p, 0.0), bb, k) * inv_dx[k];
+    return ok;
+  }
+  __device__ __forceinline__ static void prim_to_cons(const double* pr, double gamma, double (&u)[NV]) {
+    const double rho = pr[0];
+    u[0] = rho; u[1] = rho * pr[1]; u[2] = rho * pr[2]; u[3] = rho * pr[3];
+    const double bb = pr[5] * pr[5] + pr[6] * pr[6] + pr[7] * pr[7];
+    u[4] = pr[4] / (gamma - 1.0) + 0.5 * rho * (pr[1] * pr[1] + pr[2] * pr[2] + pr[3] * pr[3]) + bb * k8pi;
+    u[5] = pr[5]; u[6] = pr[6]; u[7] = pr[7]; u[8] = pr[8];
+  }
+};
+
+// ---------------------------------------------------------------------------
+// WENO, one 1D problem: win[0..2M] are the cell averages of cells
+// i-M..i+M (or previous-sweep dofs); out[N] the nodal dofs.
+// ---------------------------------------------------------------------------
+template <int M> struct Stencils {
+  static constexpr int N = M + 1;
+  static constexpr int NS = (M % 2 == 0) ? 3 : 4;
+  __host__ __device__ static constexpr int L(int s) {
+    return (M % 2 == 0) ? (s == 0 ? M / 2 : (s == 1 ? M : 0))
+                        : (s == 0 ? M / 2 + 1 : (s == 1 ? M / 2 : (s == 2 ? M : 0)));
+  }
+};
+
+template <int M>
+__device__ __forceinline__ void weno1d(const DevTables& T, const double (&win)[2 * M + 1], double (&out)[M + 1]) {
+  constexpr int N = M + 1;
+  constexpr int NS = Stencils<M>::NS;
+  double ws[NS][N], om[NS];
+  double sum = 0.0;
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    constexpr int dummy = 0; (void)dummy;
+#pragma unroll
+    for (int p = 0; p < N; ++p) {
+      double acc = 0.0;
+#pragma unroll
+      for (int o = 0; o < N; ++o) acc += T.rec[s][p][o] * win[M - Stencils<M>::L(s) + o];
+      ws[s][p] = acc;
+    }
+    double sig = 0.0;
+#pragma unroll
+    for (int p = 0; p < N; ++p) {
+      double acc = 0.0;
+#pragma unroll
+      for (int m = 0; m < N; ++m) acc += T.sigma[p][m] * ws[s][m];
+      sig += acc * ws[s][p];
+    }
+    // omega~ = lambda_s / (sigma + 1e-14)^8 by three squarings
+    double x = sig + 1e-14;
+    x = x * x; x = x * x; x = x * x;
+    om[s] = T.lin[s] / x;
+    sum += om[s];
+  }
+  const double isum = 1.0 / sum;
+#pragma unroll
+  for (int p = 0; p < N; ++p) {
+    double acc = 0.0;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) acc += (om[s] * isum) * ws[s][p];
+    out[p] = acc;
+  }
+}
+
+}  // namespace ader

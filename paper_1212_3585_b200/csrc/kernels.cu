@@ -1,0 +1,595 @@
+// kernels.cu — sm_100a kernels of the ADER-WENO hot path (FP64).
+//
+//   k_weno      a1 WENO reconstruction, one sweep
+//   k_predictor a2 local space-time DG predictor, nodal Picard form of
+//               eqn.stdg.final: q = w - T_tau sum_dir D_dir f*_dir(q)
+//   k_face_flux a3 space-time Gauss quadrature of the Rusanov flux
+//   k_update    a4 one-step FV update (eq:finite_vol @ P:147-152) fused with the
+//               CFL speed of the new state (reading R1)
+// plus ghost fill / pack / IC / gather helpers.  Layouts: see launch.h.
+// Citations: P:n = PAPER.md line n.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "device.cuh"
+#include "launch.h"
+
+namespace ader {
+
+constexpr int ipow_c(int b, int e) { return e == 0 ? 1 : b * ipow_c(b, e - 1); }
+
+__device__ __forceinline__ long long box_cell(const Box& R, long long r, long long sy, long long sz) {
+  const long long x = R.lo[0] + r % R.ext[0];
+  const long long t = r / R.ext[0];
+  const long long y = R.lo[1] + t % R.ext[1];
+  const long long z = R.lo[2] + t / R.ext[1];
+  return x + y * sy + z * sz;
+}
+
+__device__ __forceinline__ void record_error(DevCounters* c, int code, int stage, long long cell) {
+  if (atomicCAS(&c->err_code, 0, code) == 0) {
+    c->err_stage = stage;
+    c->err_cell = (unsigned long long)cell;
+  }
+}
+
+// ===========================================================================
+// a1: WENO sweep K (axis K).  Thread per (cell, variable, previous-sweep dof).
+// src [cell][NV][N^K], dst [cell][NV][N^(K+1)] with the new axis slowest.
+// ===========================================================================
+template <int M, int K, int NV>
+__global__ void __launch_bounds__(256) k_weno(const double* __restrict__ src, double* __restrict__ dst,
+                                              const Box R, const long long sy, const long long sz,
+                                              const long long astride, const __grid_constant__ DevTables T) {
+  constexpr int N = M + 1;
+  constexpr int NT = ipow_c(N, K);
+  constexpr int NIN = NV * NT;
+  const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= R.count() * NIN) return;
+  const long long r = gid / NIN;
+  const int inner = (int)(gid - r * NIN);
+  const long long cell = box_cell(R, r, sy, sz);
+  double win[2 * M + 1];
+#pragma unroll
+  for (int o = -M; o <= M; ++o) win[o + M] = __ldg(&src[(cell + o * astride) * NIN + inner]);
+  double out[N];
+  weno1d<M>(T, win, out);
+  const int v = inner / NT, t = inner - v * NT;
+  double* d = dst + cell * (NIN * N) + v * NT * N + t;
+#pragma unroll
+  for (int a = 0; a < N; ++a) d[NT * a] = out[a];
+}
+
+// ===========================================================================
+// a2: predictor.  One thread per (cell, spatial node); the thread keeps the
+// node's time pencil q[NV][N] in registers.  Pointwise fluxes are exchanged
+// through shared memory inside the warp that holds the cell, so the Picard
+// loop needs only __syncwarp; each cell stops at its own convergence.
+// ===========================================================================
+template <int D, int M, int SYS, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) k_predictor(
+    const double* __restrict__ w, double* __restrict__ q, const Box R, const long long sy, const long long sz,
+    const double dtdx0, const double dtdx1, const double dtdx2, const double gamma, const double ch,
+    const double tol, const int max_sweeps, DevCounters* __restrict__ cnt, const __grid_constant__ DevTables T) {
+  using PH = Phys<SYS, D>;
+  constexpr int NV = PH::NV, N = M + 1, NS = ipow_c(N, D), NST = NS * N;
+  constexpr int CPW = 32 / NS;
+  static_assert(CPW >= 1, "one cell must fit in a warp");
+  constexpr int FSZ = D * NV * N * NS;
+  extern __shared__ double smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int slot = lane / NS, node = lane - slot * NS;
+  double* Fs = smem + (warp * CPW + (slot < CPW ? slot : CPW - 1)) * FSZ;
+  double* red = smem + WARPS * CPW * FSZ + warp * 64;
+  const long long rc = ((long long)blockIdx.x * WARPS + warp) * CPW + slot;
+  const bool active = slot < CPW && rc < R.count();
+  const long long cell = active ? box_cell(R, rc, sy, sz) : 0;
+  int ia[3];
+  ia[0] = node % N;
+  ia[1] = (node / N) % N;
+  ia[2] = node / (N * N);
+  const double dtdx[3] = {dtdx0, dtdx1, dtdx2};
+
+  double wv[NV], qv[NV][N];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    wv[v] = active ? w[cell * (NV * NS) + v * NS + node] : 1.0;
+#pragma unroll
+    for (int s = 0; s < N; ++s) qv[v][s] = wv[v];   // time-constant initial guess (reading R3)
+  }
+  bool conv = !active, bad = false;
+  int nsw = 0;
+  for (int sweep = 1; sweep <= max_sweeps; ++sweep) {
+    if (!conv) {
+      // nodal fluxes f*_dir = (dt/dx_dir) f_dir(q) (eqn.nodal.eval @ P:405-412)
+#pragma unroll
+      for (int s = 0; s < N; ++s) {
+        double uu[NV], f[D][NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) uu[v] = qv[v][s];
+        bad |= !PH::fluxes(uu, gamma, ch, f);
+#pragma unroll
+        for (int d = 0; d < D; ++d)
+#pragma unroll
+          for (int v = 0; v < NV; ++v) Fs[((d * NV + v) * N + s) * NS + node] = dtdx[d] * f[d][v];
+      }
+    }
+    __syncwarp();
+    double dmax = 0.0, qmax = 0.0;
+    if (!conv) {
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        double G[N];
+#pragma unroll
+        for (int s = 0; s < N; ++s) {
+          double g = 0.0;
+#pragma unroll
+          for (int d = 0; d < D; ++d) {
+            constexpr int dummy = 0; (void)dummy;
+            const int sd = (d == 0) ? 1 : (d == 1 ? N : N * N);
+            const double* fb = Fs + ((d * NV + v) * N + s) * NS + node - ia[d] * sd;
+#pragma unroll
+            for (int j = 0; j < N; ++j) g += T.D[ia[d]][j] * fb[j * sd];
+          }
+          G[s] = g;
+        }
+#pragma unroll
+        for (int s = 0; s < N; ++s) {
+          double acc = wv[v];
+#pragma unroll
+          for (int s2 = 0; s2 < N; ++s2) acc -= T.T[s][s2] * G[s2];
+          dmax = fmax(dmax, fabs(acc - qv[v][s]));
+          qmax = fmax(qmax, fabs(acc));
+          qv[v][s] = acc;
+        }
+      }
+    }
+    red[lane] = dmax;
+    red[32 + lane] = qmax;
+    __syncwarp();
+    if (!conv) {
+      double dm = 0.0, qm = 0.0;
+#pragma unroll
+      for (int j = 0; j < NS; ++j) {
+        dm = fmax(dm, red[slot * NS + j]);
+        qm = fmax(qm, red[32 + slot * NS + j]);
+      }
+      nsw = sweep;
+      if (dm <= tol * (1.0 + qm)) conv = true;   // reading R2
+    }
+    if (__all_sync(0xffffffffu, conv)) break;
+  }
+  if (!active) return;
+  if (bad) record_error(cnt, 1, 1, cell);
+  else if (!conv) record_error(cnt, 2, 1, cell);
+  double* qo = q + cell * (NV * NST) + node;
+#pragma unroll
+  for (int v = 0; v < NV; ++v)
+#pragma unroll
+    for (int s = 0; s < N; ++s) qo[v * NST + s * NS] = qv[v][s];
+  if (node == 0) {
+    atomicAdd(&cnt->sweeps, (unsigned long long)nsw);
+    atomicAdd(&cnt->cells, 1ull);
+    atomicMax(&cnt->sweeps_max, nsw);
+  }
+}
+
+// ===========================================================================
+// a3: face flux.  One thread per space-time quadrature point of a face
+// (N^(D-1) tangential x N time = NS points); a face per NS-lane group.
+// ===========================================================================
+template <int D, int M, int SYS, int DIR, int WARPS>
+__device__ __forceinline__ void face_flux_dir(const double* __restrict__ q, double* __restrict__ F, const Box& R,
+                                              long long sy, long long sz, long long ncell, double gamma, double ch,
+                                              DevCounters* cnt, const DevTables& T, double* red) {
+  using PH = Phys<SYS, D>;
+  constexpr int NV = PH::NV, N = M + 1, NS = ipow_c(N, D), NST = NS * N;
+  constexpr int NT = NS / N;   // tangential points
+  constexpr int CPW = 32 / NS;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int slot = lane / NS, p = lane - slot * NS;
+  const long long rc = ((long long)blockIdx.x * WARPS + warp) * CPW + slot;
+  const bool active = slot < CPW && rc < R.count();
+  double* rw = red + (warp * CPW + (slot < CPW ? slot : CPW - 1)) * NV * NS;
+  if (active) {
+    const long long cR = box_cell(R, rc, sy, sz);
+    const long long sd = (DIR == 0) ? 1 : (DIR == 1 ? sy : sz);
+    const long long cL = cR - sd;
+    const int s = p / NT, t = p - s * NT;
+    const int t1 = t % N, t2 = t / N;
+    constexpr int ax0 = (DIR == 0) ? 1 : 0;
+    constexpr int ax1 = (DIR == 2) ? 1 : 2;
+    constexpr int sn = ipow_c(N, DIR);
+    const int base = s * NS + t1 * ipow_c(N, ax0) + (D == 3 ? t2 * ipow_c(N, ax1) : 0);
+    const double* qL = q + cL * (NV * NST) + base;
+    const double* qR = q + cR * (NV * NST) + base;
+    double um[NV], up[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      double a = 0.0, b = 0.0;
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        a += T.psi1[k] * __ldg(&qL[v * NST + k * sn]);   // q_h^- at xi = 1 of the left cell
+        b += T.psi0[k] * __ldg(&qR[v * NST + k * sn]);   // q_h^+ at xi = 0 of the right cell
+      }
+      um[v] = a;
+      up[v] = b;
+    }
+    double fL[NV], fR[NV], sL, sR;
+    bool ok = PH::template flux_speed<DIR>(um, gamma, ch, fL, sL);
+    ok &= PH::template flux_speed<DIR>(up, gamma, ch, fR, sR);
+    if (!ok) record_error(cnt, 1, 2, cR);
+    const double smax = fmax(sL, sR);   // reading R4
+    double wt = T.w[s] * T.w[t1];
+    if (D == 3) wt *= T.w[t2];
+#pragma unroll
+    for (int v = 0; v < NV; ++v)
+      rw[v * NS + p] = wt * (0.5 * (fL[v] + fR[v]) - 0.5 * smax * (up[v] - um[v]));   // eqn.rusanov
+  }
+  __syncwarp();
+  if (active && p < NV) {
+    const long long cR = box_cell(R, rc, sy, sz);
+    double acc = 0.0;
+    for (int j = 0; j < NS; ++j) acc += rw[p * NS + j];
+    F[((long long)DIR * ncell + cR) * NV + p] = acc;
+  }
+}
+
+template <int D, int M, int SYS, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) k_face_flux(const double* __restrict__ q, double* __restrict__ F,
+                                                          const Box R0, const Box R1, const Box R2, const long long sy,
+                                                          const long long sz, const long long ncell,
+                                                          const double gamma, const double ch,
+                                                          DevCounters* __restrict__ cnt,
+                                                          const __grid_constant__ DevTables T) {
+  extern __shared__ double red[];
+  if (blockIdx.y == 0) face_flux_dir<D, M, SYS, 0, WARPS>(q, F, R0, sy, sz, ncell, gamma, ch, cnt, T, red);
+  else if (blockIdx.y == 1) face_flux_dir<D, M, SYS, 1, WARPS>(q, F, R1, sy, sz, ncell, gamma, ch, cnt, T, red);
+  else if (D == 3) face_flux_dir<D, M, SYS, 2, WARPS>(q, F, R2, sy, sz, ncell, gamma, ch, cnt, T, red);
+}
+
+// ===========================================================================
+// a4: FV update + next CFL speed (block max, then one atomicMax per block).
+// ===========================================================================
+__device__ __forceinline__ void block_max_to(double s, unsigned long long* dst) {
+  __shared__ double sm[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s = fmax(s, __shfl_xor_sync(0xffffffffu, s, o));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) sm[warp] = s;
+  __syncthreads();
+  if (warp == 0) {
+    s = (lane < (int)(blockDim.x >> 5)) ? sm[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s = fmax(s, __shfl_xor_sync(0xffffffffu, s, o));
+    if (lane == 0) atomicMax(dst, (unsigned long long)__double_as_longlong(s));
+  }
+}
+
+template <int D, int SYS>
+__global__ void __launch_bounds__(256) k_update(double* __restrict__ u, const double* __restrict__ F, const Box R,
+                                                const long long sy, const long long sz, const long long ncell,
+                                                const double dtdx0, const double dtdx1, const double dtdx2,
+                                                const double idx0, const double idx1, const double idx2,
+                                                const double gamma, const double ch, DevCounters* __restrict__ cnt) {
+  using PH = Phys<SYS, D>;
+  constexpr int NV = PH::NV;
+  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  double s = 0.0;
+  if (r < R.count()) {
+    const long long c = box_cell(R, r, sy, sz);
+    const double dtdx[3] = {dtdx0, dtdx1, dtdx2};
+    const long long st[3] = {1, sy, sz};
+    double uu[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) uu[v] = u[c * NV + v];
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const double* Fm = F + ((long long)d * ncell + c) * NV;
+      const double* Fp = F + ((long long)d * ncell + c + st[d]) * NV;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) uu[v] = uu[v] - dtdx[d] * (Fp[v] - Fm[v]);
+    }
+    const double inv_dx[3] = {idx0, idx1, idx2};
+    if (!PH::cfl_speed(uu, gamma, ch, inv_dx, s)) record_error(cnt, 1, 3, c);
+#pragma unroll
+    for (int v = 0; v < NV; ++v) u[c * NV + v] = uu[v];
+  }
+  block_max_to(s, &cnt->speed_bits);
+}
+
+template <int D, int SYS>
+__global__ void __launch_bounds__(256) k_cfl_speed(const double* __restrict__ u, const Box R, const long long sy,
+                                                   const long long sz, const double idx0, const double idx1,
+                                                   const double idx2, const double gamma, const double ch,
+                                                   DevCounters* __restrict__ cnt) {
+  using PH = Phys<SYS, D>;
+  constexpr int NV = PH::NV;
+  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  double s = 0.0;
+  if (r < R.count()) {
+    const long long c = box_cell(R, r, sy, sz);
+    double uu[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) uu[v] = u[c * NV + v];
+    const double inv_dx[3] = {idx0, idx1, idx2};
+    if (!PH::cfl_speed(uu, gamma, ch, inv_dx, s)) record_error(cnt, 1, 4, c);
+  }
+  block_max_to(s, &cnt->speed_bits);
+}
+
+// ===========================================================================
+// helpers
+// ===========================================================================
+__global__ void k_fill_axis(double* __restrict__ u, const Box R, const long long sy, const long long sz, const int nv,
+                            const int axis, const int mode, const int H, const int n) {
+  const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= R.count() * nv) return;
+  const long long r = gid / nv;
+  const int v = (int)(gid - r * nv);
+  int c[3];
+  c[0] = R.lo[0] + (int)(r % R.ext[0]);
+  const long long t = r / R.ext[0];
+  c[1] = R.lo[1] + (int)(t % R.ext[1]);
+  c[2] = R.lo[2] + (int)(t / R.ext[1]);
+  int i = c[axis] - H;
+  if (mode == 0) i = ((i % n) + n) % n;
+  else i = i < 0 ? 0 : (i >= n ? n - 1 : i);
+  int s[3] = {c[0], c[1], c[2]};
+  s[axis] = i + H;
+  const long long dst = c[0] + c[1] * sy + c[2] * sz;
+  const long long src = s[0] + s[1] * sy + s[2] * sz;
+  u[dst * nv + v] = u[src * nv + v];
+}
+
+__global__ void k_pack(const double* __restrict__ src, const Box R, const long long sy, const long long sz,
+                       const int stride, double* __restrict__ out, const int to_buf) {
+  const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= R.count() * stride) return;
+  const long long r = gid / stride;
+  const int v = (int)(gid - r * stride);
+  const long long c = box_cell(R, r, sy, sz);
+  if (to_buf) out[gid] = src[c * stride + v];
+  else const_cast<double*>(src)[c * stride + v] = out[gid];
+}
+
+template <int D, int SYS>
+__global__ void k_ic_average(double* __restrict__ u, const double* __restrict__ prim, const double* __restrict__ wq,
+                             const int nq, const long long first, const long long ncells, const int n0, const int n1,
+                             const int H, const long long sy, const long long sz, const double gamma) {
+  using PH = Phys<SYS, D>;
+  constexpr int NV = PH::NV;
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ncells) return;
+  const long long lin = first + i;
+  const long long x = lin % n0, y = (lin / n0) % n1, z = lin / ((long long)n0 * n1);
+  double acc[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) acc[v] = 0.0;
+  for (int g = 0; g < nq; ++g) {
+    double uu[NV];
+    PH::prim_to_cons(prim + (i * nq + g) * 9, gamma, uu);
+#pragma unroll
+    for (int v = 0; v < NV; ++v) acc[v] += wq[g] * uu[v];
+  }
+  const long long c = (x + H) + (y + H) * sy + (D == 3 ? (z + H) : z) * sz;
+#pragma unroll
+  for (int v = 0; v < NV; ++v) u[c * NV + v] = acc[v];
+}
+
+__global__ void k_cons_partials(const double* __restrict__ u, const Box R, const long long sy, const long long sz,
+                                const int nv, const double vol, double* __restrict__ partial) {
+  __shared__ double sm[256 * 9];
+  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int v = 0; v < nv; ++v) sm[v * 256 + threadIdx.x] = 0.0;
+  if (r < R.count()) {
+    const long long c = box_cell(R, r, sy, sz);
+    for (int v = 0; v < nv; ++v) sm[v * 256 + threadIdx.x] = u[c * nv + v] * vol;
+  }
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o)
+      for (int v = 0; v < nv; ++v) sm[v * 256 + threadIdx.x] += sm[v * 256 + threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0)
+    for (int v = 0; v < nv; ++v) partial[(long long)blockIdx.x * nv + v] = sm[v * 256];
+}
+
+// ===========================================================================
+// launchers
+// ===========================================================================
+namespace {
+inline unsigned grid_for(long long n, int bs) { return (unsigned)((n + bs - 1) / bs); }
+inline void count_launch(const KCtx& k) { if (k.launches) ++*k.launches; }
+
+#define ADER_DISPATCH(D_, M_, SYS_, ...)                                          \
+  do {                                                                             \
+    if (D_ == 2 && M_ == 2 && SYS_ == 0) { constexpr int D = 2, M = 2, SYS = 0; __VA_ARGS__; } \
+    else if (D_ == 2 && M_ == 3 && SYS_ == 0) { constexpr int D = 2, M = 3, SYS = 0; __VA_ARGS__; } \
+    else if (D_ == 3 && M_ == 2 && SYS_ == 0) { constexpr int D = 3, M = 2, SYS = 0; __VA_ARGS__; } \
+    else if (D_ == 2 && M_ == 2 && SYS_ == 1) { constexpr int D = 2, M = 2, SYS = 1; __VA_ARGS__; } \
+    else if (D_ == 2 && M_ == 3 && SYS_ == 1) { constexpr int D = 2, M = 3, SYS = 1; __VA_ARGS__; } \
+    else if (D_ == 3 && M_ == 2 && SYS_ == 1) { constexpr int D = 3, M = 2, SYS = 1; __VA_ARGS__; } \
+  } while (0)
+
+constexpr int kPredWarps = 4;
+constexpr int kFluxWarps = 4;
+
+template <int D, int M, int SYS>
+size_t pred_smem() {
+  constexpr int NV = Phys<SYS, D>::NV, N = M + 1, NS = ipow_c(N, D), CPW = 32 / NS;
+  return sizeof(double) * ((size_t)kPredWarps * CPW * D * NV * N * NS + kPredWarps * 64);
+}
+template <int D, int M, int SYS>
+size_t flux_smem() {
+  constexpr int NV = Phys<SYS, D>::NV, N = M + 1, NS = ipow_c(N, D), CPW = 32 / NS;
+  return sizeof(double) * (size_t)kFluxWarps * CPW * NV * NS;
+}
+}  // namespace
+
+bool supported(int D, int M, int SYS) {
+  bool ok = false;
+  ADER_DISPATCH(D, M, SYS, ok = true);
+  return ok;
+}
+
+template <int M, int K>
+static void weno_sweep_nv(const KCtx& k, const double* src, double* dst, const Box& R, long long astride) {
+  constexpr int N = M + 1;
+  const long long per = ipow_c(N, K);
+  const long long total = R.count() * k.NV * per;
+  if (total == 0) return;
+  const unsigned g = grid_for(total, 256);
+  count_launch(k);
+  switch (k.NV) {
+    case 4: k_weno<M, K, 4><<<g, 256, 0, k.stream>>>(src, dst, R, k.sy, k.sz, astride, k.tab); break;
+    case 5: k_weno<M, K, 5><<<g, 256, 0, k.stream>>>(src, dst, R, k.sy, k.sz, astride, k.tab); break;
+    case 9: k_weno<M, K, 9><<<g, 256, 0, k.stream>>>(src, dst, R, k.sy, k.sz, astride, k.tab); break;
+    default: break;
+  }
+}
+
+void launch_weno_sweep(const KCtx& k, int sweep, const double* src, double* dst, const Box& region) {
+  const long long astride = sweep == 0 ? 1 : (sweep == 1 ? k.sy : k.sz);
+  if (k.M == 2) {
+    if (sweep == 0) weno_sweep_nv<2, 0>(k, src, dst, region, astride);
+    else if (sweep == 1) weno_sweep_nv<2, 1>(k, src, dst, region, astride);
+    else weno_sweep_nv<2, 2>(k, src, dst, region, astride);
+  } else if (k.M == 3) {
+    if (sweep == 0) weno_sweep_nv<3, 0>(k, src, dst, region, astride);
+    else if (sweep == 1) weno_sweep_nv<3, 1>(k, src, dst, region, astride);
+    else weno_sweep_nv<3, 2>(k, src, dst, region, astride);
+  }
+}
+
+void launch_predictor(const KCtx& k, const double* w, double* q, const Box& region, const double dtdx[3],
+                      double tol, int max_sweeps, DevCounters* cnt) {
+  if (region.count() == 0) return;
+  ADER_DISPATCH(k.D, k.M, k.SYS, {
+    constexpr int N = M + 1;
+    constexpr int NS = ipow_c(N, D);
+    constexpr int CPW = 32 / NS;
+    const size_t sm = pred_smem<D, M, SYS>();
+    auto kern = k_predictor<D, M, SYS, kPredWarps>;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      attr = true;
+    }
+    const unsigned g = grid_for(region.count(), kPredWarps * CPW);
+    count_launch(k);
+    kern<<<g, kPredWarps * 32, sm, k.stream>>>(w, q, region, k.sy, k.sz, dtdx[0], dtdx[1], dtdx[2], k.gamma,
+                                                k.ch, tol, max_sweeps, cnt, k.tab);
+  });
+}
+
+void launch_face_flux(const KCtx& k, const double* q, double* F, const Box faces[3], DevCounters* cnt) {
+  long long mx = 0;
+  for (int d = 0; d < k.D; ++d) mx = faces[d].count() > mx ? faces[d].count() : mx;
+  if (mx == 0) return;
+  ADER_DISPATCH(k.D, k.M, k.SYS, {
+    constexpr int N = M + 1;
+    constexpr int NS = ipow_c(N, D);
+    constexpr int CPW = 32 / NS;
+    const size_t sm = flux_smem<D, M, SYS>();
+    auto kern = k_face_flux<D, M, SYS, kFluxWarps>;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      attr = true;
+    }
+    dim3 g(grid_for(mx, kFluxWarps * CPW), D);
+    count_launch(k);
+    kern<<<g, kFluxWarps * 32, sm, k.stream>>>(q, F, faces[0], faces[1], faces[2], k.sy, k.sz, k.ncell, k.gamma,
+                                                k.ch, cnt, k.tab);
+  });
+}
+
+void launch_update(const KCtx& k, double* u, const double* F, const Box& R, const double dtdx[3],
+                   const double inv_dx[3], DevCounters* cnt) {
+  if (R.count() == 0) return;
+  const unsigned g = grid_for(R.count(), 256);
+  count_launch(k);
+#define UPD(D_, S_)                                                                                   \
+  k_update<D_, S_><<<g, 256, 0, k.stream>>>(u, F, R, k.sy, k.sz, k.ncell, dtdx[0], dtdx[1], dtdx[2], \
+                                             inv_dx[0], inv_dx[1], inv_dx[2], k.gamma, k.ch, cnt)
+  if (k.D == 2 && k.SYS == 0) UPD(2, 0);
+  else if (k.D == 3 && k.SYS == 0) UPD(3, 0);
+  else if (k.D == 2 && k.SYS == 1) UPD(2, 1);
+  else if (k.D == 3 && k.SYS == 1) UPD(3, 1);
+#undef UPD
+}
+
+void launch_cfl_speed(const KCtx& k, const double* u, const Box& R, const double inv_dx[3], DevCounters* cnt) {
+  if (R.count() == 0) return;
+  const unsigned g = grid_for(R.count(), 256);
+  count_launch(k);
+#define SPD(D_, S_) \
+  k_cfl_speed<D_, S_><<<g, 256, 0, k.stream>>>(u, R, k.sy, k.sz, inv_dx[0], inv_dx[1], inv_dx[2], k.gamma, k.ch, cnt)
+  if (k.D == 2 && k.SYS == 0) SPD(2, 0);
+  else if (k.D == 3 && k.SYS == 0) SPD(3, 0);
+  else if (k.D == 2 && k.SYS == 1) SPD(2, 1);
+  else if (k.D == 3 && k.SYS == 1) SPD(3, 1);
+#undef SPD
+}
+
+void launch_fill_axis(const KCtx& k, double* u, const Box& region, int axis, int mode, int H, int n) {
+  const long long total = region.count() * k.NV;
+  if (total == 0) return;
+  count_launch(k);
+  k_fill_axis<<<grid_for(total, 256), 256, 0, k.stream>>>(u, region, k.sy, k.sz, k.NV, axis, mode, H, n);
+}
+
+void launch_pack(const KCtx& k, const double* u, const Box& b, double* buf) {
+  const long long total = b.count() * k.NV;
+  if (total == 0) return;
+  count_launch(k);
+  k_pack<<<grid_for(total, 256), 256, 0, k.stream>>>(u, b, k.sy, k.sz, k.NV, buf, 1);
+}
+
+void launch_unpack(const KCtx& k, double* u, const Box& b, const double* buf) {
+  const long long total = b.count() * k.NV;
+  if (total == 0) return;
+  count_launch(k);
+  k_pack<<<grid_for(total, 256), 256, 0, k.stream>>>(u, b, k.sy, k.sz, k.NV, const_cast<double*>(buf), 0);
+}
+
+void launch_gather(const KCtx& k, const double* src, int stride, const Box& b, double* out) {
+  const long long total = b.count() * stride;
+  if (total == 0) return;
+  count_launch(k);
+  k_pack<<<grid_for(total, 256), 256, 0, k.stream>>>(src, b, k.sy, k.sz, stride, out, 1);
+}
+
+void launch_scatter(const KCtx& k, double* dst, int stride, const Box& b, const double* in) {
+  const long long total = b.count() * stride;
+  if (total == 0) return;
+  count_launch(k);
+  k_pack<<<grid_for(total, 256), 256, 0, k.stream>>>(dst, b, k.sy, k.sz, stride, const_cast<double*>(in), 0);
+}
+
+void launch_ic_average(const KCtx& k, double* u, const double* prim, const double* wq, int nq, long long first,
+                       long long ncells, const int n[3], int H) {
+  if (ncells == 0) return;
+  const unsigned g = grid_for(ncells, 128);
+  count_launch(k);
+#define ICA(D_, S_) \
+  k_ic_average<D_, S_><<<g, 128, 0, k.stream>>>(u, prim, wq, nq, first, ncells, n[0], n[1], H, k.sy, k.sz, k.gamma)
+  if (k.D == 2 && k.SYS == 0) ICA(2, 0);
+  else if (k.D == 3 && k.SYS == 0) ICA(3, 0);
+  else if (k.D == 2 && k.SYS == 1) ICA(2, 1);
+  else if (k.D == 3 && k.SYS == 1) ICA(3, 1);
+#undef ICA
+}
+
+int launch_cons_partials(const KCtx& k, const double* u, const Box& b, double vol, double* partial, int max_blocks) {
+  const unsigned g = grid_for(b.count(), 256);
+  if ((int)g > max_blocks || g == 0) return 0;
+  count_launch(k);
+  k_cons_partials<<<g, 256, 0, k.stream>>>(u, b, k.sy, k.sz, k.NV, vol, partial);
+  return (int)g;
+}
+
+}  // namespace ader

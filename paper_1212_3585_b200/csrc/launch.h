@@ -1,0 +1,76 @@
+// launch.h — host-side launchers of the sm_100a kernels (kernels.cu).
+// All cell arrays are cell-major on the rank's padded grid (owned block plus a
+// ghost layer of width H = M+1 on every axis of the d axes):
+//   u  [cell][nu]              cell averages
+//   wk [cell][nu][N^(k+1)]     dofs after WENO sweep k (x, then y, then z)
+//   q  [cell][nu][N^(d+1)]     space-time predictor dofs, space fastest
+//   F  [dir][cell][nu]         space-time averaged flux on the lower face of cell
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "tables.h"
+
+namespace ader {
+
+struct Box {
+  int lo[3];     // padded coordinates of the first cell
+  int ext[3];    // extent per axis (1 on unused axes)
+  __host__ __device__ long long count() const { return (long long)ext[0] * ext[1] * ext[2]; }
+};
+
+struct DevCounters {              // device-resident, zeroed by the host
+  unsigned long long sweeps;      // Picard sweeps summed over cells
+  unsigned long long cells;       // predicted cells
+  unsigned long long speed_bits;  // max CFL speed (bits of a non-negative double)
+  unsigned long long err_cell;    // padded cell index of the first failure
+  int sweeps_max;
+  int err_code;                   // 0 ok, 1 inadmissible state, 2 predictor cap
+  int err_stage;                  // 1 predictor, 2 flux, 3 update, 4 speed
+  int pad;
+};
+
+struct KCtx {
+  int D, M, SYS, NV;
+  long long sy, sz;               // cell strides along y, z in the padded grid
+  long long ncell;                // padded cells
+  double gamma, ch;
+  cudaStream_t stream;
+  long long* launches;            // host counter of kernel launches (instrumentation)
+  DevTables tab;
+};
+
+// returns false if (D, M, SYS) has no compiled instantiation
+bool supported(int D, int M, int SYS);
+
+// WENO sweep k along axis k (k = 0 x, 1 y, 2 z) on the cells of `region`.
+void launch_weno_sweep(const KCtx& k, int sweep, const double* src, double* dst, const Box& region);
+// Predictor on `region`: w -> q.
+void launch_predictor(const KCtx& k, const double* w, double* q, const Box& region, const double dtdx[3],
+                      double tol, int max_sweeps, DevCounters* cnt);
+// Face fluxes on the lower face of every cell of faces[dir], for dir < D.
+void launch_face_flux(const KCtx& k, const double* q, double* F, const Box faces[3], DevCounters* cnt);
+// FV update of `interior` in place + max CFL speed of the new state.
+void launch_update(const KCtx& k, double* u, const double* F, const Box& interior, const double dtdx[3],
+                   const double inv_dx[3], DevCounters* cnt);
+void launch_cfl_speed(const KCtx& k, const double* u, const Box& interior, const double inv_dx[3],
+                      DevCounters* cnt);
+// Ghost copy along one axis: for every cell of `region` (halo cells), copy the
+// cell at map(coord[axis]) with the other coordinates unchanged.
+//   mode 0: periodic wrap within [H, H+n), mode 1: clamp to [H, H+n-1]
+void launch_fill_axis(const KCtx& k, double* u, const Box& region, int axis, int mode, int H, int n);
+// Pack / unpack a box of u into / from a contiguous buffer [box cell][nu].
+void launch_pack(const KCtx& k, const double* u, const Box& b, double* buf);
+void launch_unpack(const KCtx& k, double* u, const Box& b, const double* buf);
+// IC cell averages: prim[cell][nq][9] at the GL points of `ncells` consecutive
+// owned cells starting at owned linear index first; weights wq[nq].
+void launch_ic_average(const KCtx& k, double* u, const double* prim, const double* wq, int nq,
+                       long long first, long long ncells, const int n[3], int H);
+// Owned cells <-> compact [cell][stride] buffers (x fastest within the block).
+void launch_gather(const KCtx& k, const double* src, int stride, const Box& b, double* out);
+void launch_scatter(const KCtx& k, double* dst, int stride, const Box& b, const double* in);
+// Block partial sums of u (times vol) over owned cells -> partial[block][nu]; returns #blocks.
+int launch_cons_partials(const KCtx& k, const double* u, const Box& b, double vol, double* partial, int max_blocks);
+
+}  // namespace ader

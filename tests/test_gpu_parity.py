@@ -1,0 +1,210 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle on the same
+seeded / closed-form inputs.  Tolerances follow BASELINE.json north_star:
+max relative error <= 1e-11 after one step and <= 1e-8 after 100 steps, with
+the per-variable scale max_c |u_oracle[c, v]| (reading of "relative");
+stage dumps (reconstruction, predictor, face flux) within 1e-12 of that scale
+(reading R8: the predictor is converged to 1e-13 relative)."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_1212_3585_b200 import ader
+from paper_1212_3585_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+def rel_err(a, b, axis=None):
+    """max |a-b| / max |b| per trailing variable, then max over variables."""
+    b2 = b.reshape(-1, b.shape[-1])
+    a2 = a.reshape(-1, a.shape[-1])
+    scale = np.abs(b2).max(axis=0)
+    scale[scale == 0] = 1.0
+    return (np.abs(a2 - b2).max(axis=0) / scale).max()
+
+
+def pair(dim, degree, n, lo, hi, bc, ic, system=0, gamma=1.4, ch=0.0, cfl=0.9, ic_quad=0):
+    cfg = ader.make_config(dim=dim, degree=degree, n0=n, lo=lo, hi=hi, bc=bc, system=system, gamma=gamma,
+                           ch=ch, cfl=cfl, ic_quad=ic_quad, device=0)
+    g = ader.Solver(cfg)
+    g.set_initial(ic)
+    o = O.Oracle(dim=dim, degree=degree, n=n, lo=lo, hi=hi, bc=bc, system=system, gamma=gamma, ch=ch, cfl=cfl,
+                 ic_quad=ic_quad)
+    o.set_initial(ic)
+    return g, o
+
+
+CASES = {
+    "vortex2d_M2": dict(dim=2, degree=2, n=(20, 18), lo=(0, 0), hi=(10, 10), bc=(0,) * 6, ic=W.isentropic_vortex()),
+    "vortex2d_M3": dict(dim=2, degree=3, n=(17, 16), lo=(0, 0), hi=(10, 10), bc=(0,) * 6, ic=W.isentropic_vortex()),
+    "explosion2d_M2": dict(dim=2, degree=2, n=(22, 21), lo=(-1, -1), hi=(1, 1), bc=(1,) * 6, ic=W.explosion(2)),
+    "explosion3d_M2": dict(dim=3, degree=2, n=(9, 8, 7), lo=(-1,) * 3, hi=(1,) * 3, bc=(1,) * 6, ic=W.explosion(3)),
+    "random3d_M2": dict(dim=3, degree=2, n=(7, 6, 9), lo=(0,) * 3, hi=(1,) * 3, bc=(0,) * 6,
+                        ic=W.random_smooth(3, seed=3585, amp=0.08)),
+    "mhd_ot_M3": dict(dim=2, degree=3, n=(16, 15), lo=(0, 0), hi=(2 * math.pi, 2 * math.pi), bc=(0,) * 6,
+                      ic=W.orszag_tang(), system=1, gamma=5 / 3, ch=2.0),
+    "mhd_ot_M2": dict(dim=2, degree=2, n=(14, 13), lo=(0, 0), hi=(2 * math.pi, 2 * math.pi), bc=(0,) * 6,
+                      ic=W.orszag_tang(), system=1, gamma=5 / 3, ch=2.0),
+}
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_initial_averages(name):
+    g, o = pair(**CASES[name])
+    assert rel_err(g.get_state(), o.get_cells()) < 1e-14
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_stage_parity_recon_pred_flux(name):
+    g, o = pair(**CASES[name])
+    wo = o.dump_recon()
+    wg = g.debug_dump(0)
+    assert rel_err(np.moveaxis(wg, 1, 2), np.moveaxis(wo, 1, 2)) < 1e-12
+    dt = o.compute_dt()
+    qo = o.dump_pred(dt)
+    qg = g.debug_dump(1, dt)
+    assert rel_err(np.moveaxis(qg, 1, 2), np.moveaxis(qo, 1, 2)) < 1e-12
+    Fo = o.dump_flux(dt)
+    Fg = g.debug_dump(2, dt)
+    assert rel_err(Fg, Fo) < 1e-12
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_one_step_parity(name):
+    g, o = pair(**CASES[name])
+    dt_o = o.compute_dt()
+    rep = g.step(1e300, 1)
+    assert abs(rep.dt0 - dt_o) <= 1e-14 * dt_o
+    o.step(1e300, 1)
+    assert rel_err(g.get_state(), o.get_cells()) <= 1e-11
+
+
+def test_c1_full_run_parity_and_exact_error():
+    # BASELINE configs[0]: 2D vortex, 32^2, M=2, CFL 0.9, t = 1
+    wl = W.config("c1")
+    g, o = pair(wl.dim, wl.degree, wl.n, wl.lo, wl.hi, wl.bc, wl.ic)
+    rg = g.step(wl.t_end, 10 ** 6)
+    ro = o.step(wl.t_end, 10 ** 6)
+    assert rg.macro_steps == ro.steps and abs(rg.t - 1.0) < 1e-15 and abs(ro.t - 1.0) < 1e-15
+    ug, uo = g.get_state(), o.get_cells()
+    assert rel_err(ug, uo) <= 1e-8
+    ex = O.Oracle(dim=2, degree=2, n=wl.n, lo=wl.lo, hi=wl.hi, bc=wl.bc, ic_quad=5)
+    ex.set_initial(W.vortex_exact(1.0))
+    ue = ex.get_cells()
+    l1g = np.abs(ug[:, 0] - ue[:, 0]).mean()
+    l1o = np.abs(uo[:, 0] - ue[:, 0]).mean()
+    assert abs(l1g - l1o) <= 0.01 * l1o
+
+
+def test_100_step_parity_and_conservation():
+    g, o = pair(2, 2, (24, 24), (0, 0), (10, 10), (0,) * 6, W.isentropic_vortex())
+    u0 = g.get_state()
+    rg = g.step(1e300, 100)
+    o.step(1e300, 100)
+    ug = g.get_state()
+    assert rel_err(ug, o.get_cells()) <= 1e-8
+    # periodic: totals conserved to round-off
+    assert np.all(np.abs(ug.sum(0) - u0.sum(0)) <= 1e-11 * np.abs(u0).sum(0))
+    assert rg.pred_sweeps_max <= 32
+
+
+def test_100_step_parity_3d_explosion():
+    g, o = pair(3, 2, (10, 10, 10), (-1,) * 3, (1,) * 3, (1,) * 6, W.explosion(3))
+    g.step(1e300, 100)
+    o.step(1e300, 100)
+    assert rel_err(g.get_state(), o.get_cells()) <= 1e-8
+
+
+def test_constant_state_bitwise():
+    for dim, M, n in [(2, 2, (13, 11)), (2, 3, (9, 10)), (3, 2, (6, 7, 5))]:
+        cfg = ader.make_config(dim=dim, degree=M, n0=n, lo=(0,) * dim, hi=(1,) * dim, bc=(0,) * 6, device=0)
+        g = ader.Solver(cfg)
+        g.set_initial(W.constant_state())
+        u0 = g.get_state().copy()
+        g.step(1e300, 3)
+        assert np.array_equal(g.get_state(), u0)
+
+
+def test_degenerate_single_cell_periodic_and_ragged():
+    # one cell along y (periodic), ragged x: the y reconstruction sees copies of itself
+    g, o = pair(2, 2, (37, 1), (0, 0), (1, 1.0 / 37), (1, 1, 0, 0, 0, 0), W.shock_tube(0, 0.5))
+    g.step(0.1, 10 ** 6)
+    o.step(0.1, 10 ** 6)
+    assert rel_err(g.get_state(), o.get_cells()) <= 1e-9
+
+
+def test_solver_error_reported_for_inadmissible_state():
+    cfg = ader.make_config(dim=2, degree=2, n0=(8, 8), lo=(0, 0), hi=(1, 1), bc=(0,) * 6, device=0)
+    g = ader.Solver(cfg)
+    u = np.tile(np.array([1.0, 0.0, 0.0, 2.5]), (64, 1))
+    u[10, 3] = -1.0   # negative energy -> negative pressure
+    g.set_cells(u)
+    with pytest.raises(ader.AderError) as e:
+        g.step(1e300, 1)
+    assert e.value.status == 3
+    assert "cell" in str(e.value)
+
+
+def test_predictor_cap_is_an_error():
+    cfg = ader.make_config(dim=2, degree=2, n0=(16, 16), lo=(0, 0), hi=(10, 10), bc=(0,) * 6, device=0,
+                           pred_max_sweeps=2)
+    g = ader.Solver(cfg)
+    g.set_initial(W.isentropic_vortex())
+    with pytest.raises(ader.AderError) as e:
+        g.step(1e300, 1)
+    assert e.value.status == 3 and "pred_max_sweeps" in str(e.value)
+
+
+# ---------------------------------------------------------------------------
+# full BASELINE sizes, in the launch configuration bench.py times:
+# sampled cells recomputed one by one by the oracle
+# ---------------------------------------------------------------------------
+
+def test_c2_512_sampled_parity():
+    wl = W.config("c2", 512)
+    cfg = ader.make_config(dim=2, degree=3, n0=wl.n, lo=wl.lo, hi=wl.hi, bc=wl.bc, device=0)
+    g = ader.Solver(cfg)
+    g.set_initial(wl.ic)
+    o = O.Oracle(dim=2, degree=3, n=wl.n, lo=wl.lo, hi=wl.hi, bc=wl.bc)
+    o.set_initial(wl.ic)
+    dt = o.compute_dt()
+    rep = g.step(1e300, 1)
+    assert abs(rep.dt0 - dt) <= 1e-14 * dt
+    ug = g.get_state().reshape(512, 512, 4)
+    rng = np.random.default_rng(1212)
+    boxes = [((0, 0), (3, 2)), ((509, 510), (512, 512)), ((250, 250), (254, 253))]
+    boxes += [((int(x), int(y)), (int(x) + 2, int(y) + 2)) for x, y in rng.integers(0, 510, size=(3, 2))]
+    for blo, bhi in boxes:
+        out, _ = o.advance_box(dt, blo, bhi)
+        gg = ug[blo[1]:bhi[1], blo[0]:bhi[0]].reshape(-1, 4)
+        assert rel_err(gg, out) <= 1e-11 or np.abs(gg - out).max() <= 1e-11 * np.abs(ug).reshape(-1, 4).max(0).max()
+
+
+def test_c4_256_sampled_parity():
+    wl = W.config("c4", 256)
+    cfg = ader.make_config(dim=3, degree=2, n0=wl.n, lo=wl.lo, hi=wl.hi, bc=wl.bc, device=0)
+    g = ader.Solver(cfg)
+    g.set_initial(wl.ic)
+    rep = g.step(1e300, 1)
+    # the explosion's largest CFL speed is the resting inner state (rho, p) = (1, 1):
+    # dt = cfl / sum_dir c / dx with c from the oracle's own eigenvalue bound
+    uin = O.prim_to_cons(0, 3, 1.4, [1, 0, 0, 0, 1])
+    dx = 2.0 / 256
+    s = sum(O.max_speed(0, 3, 1.4, 0, uin, d) / dx for d in range(3))
+    dt = 0.9 / s
+    assert abs(rep.dt0 - dt) <= 1e-14 * dt
+    ug = g.get_state().reshape(256, 256, 256, 5)
+    o = O.Oracle(dim=3, degree=2, n=wl.n, lo=wl.lo, hi=wl.hi, bc=wl.bc)
+    scale = np.array([1.0, 1.0, 1.0, 1.0, 2.5])
+    boxes = [((0, 0, 0), (2, 2, 2)), ((254, 100, 127), (256, 102, 129)),   # corner / face
+             ((62, 127, 127), (65, 129, 129)),                              # across r = 0.5
+             ((127, 127, 127), (129, 129, 129)), ((200, 40, 90), (202, 42, 92))]
+    for blo, bhi in boxes:
+        glo = [max(0, blo[k] - 4) for k in range(3)]
+        ghi = [min(256, bhi[k] + 4) for k in range(3)]
+        o.set_initial_box(wl.ic, glo, ghi)
+        out, _ = o.advance_box(dt, blo, bhi)
+        gg = ug[blo[2]:bhi[2], blo[1]:bhi[1], blo[0]:bhi[0]].reshape(-1, 5)
+        assert (np.abs(gg - out).max(axis=0) / scale).max() <= 1e-11, (blo, np.abs(gg - out).max(axis=0))
