@@ -376,10 +376,18 @@ void orc_weno_1d(int M, const double* win, double* out) {
       for (int o = 0; o < N; ++o) acc += B->rec[s][p][o] * win[M - B->L[s] + o];
       ws[s][p] = acc;
     }
-    /* eqn.sigmas: sigma_s = Sigma_pm w_p w_m */
+    /* eqn.sigmas: sigma_s = Sigma_pm w_p w_m with Sigma_pm of P:271-273, i.e.
+     * sigma_s = sum_alpha int_0^1 (d^alpha w_h^s / dxi^alpha)^2 dxi.  Evaluated in
+     * this integral form (reading R13): the quadratic form in nodal
+     * coefficients cancels O(|w|^2 |Sigma| 1e-16) ~ 1e-13 of round-off, more
+     * than eps = 1e-14, which would leave the weights undetermined in FP64. */
     double sig = 0.0;
-    for (int p = 0; p < N; ++p)
-      for (int m = 0; m < N; ++m) sig += B->Sigma[p][m] * ws[s][p] * ws[s][m];
+    for (int a = 1; a <= M; ++a)
+      for (int q = 0; q < 16; ++q) {
+        double dv = 0.0;
+        for (int p = 0; p < N; ++p) dv += ws[s][p] * psi_der(B, p, a, QX[q]);
+        sig += QW[q] * dv * dv;
+      }
     /* eqn.omegas with eps = 1e-14, r = 8 */
     wt[s] = B->lin[s] / pow(sig + 1e-14, 8.0);
     sum += wt[s];
@@ -607,8 +615,13 @@ int orc_face_flux(int d, int M, int system, double gamma, double ch, int dir,
       for (int k = 0; k < nt; ++k) { xl[tdir[k]] = xr[tdir[k]] = B->lam[ti[k]]; wgt *= B->w[ti[k]]; }
       xl[dir] = 1.0; xr[dir] = 0.0;
       double um[VMAX], up[VMAX], ft[VMAX];
-      eval_st(B, d, nv, qL, xl, B->lam[s], um);   /* q_h^- at x_{i+1/2} */
-      eval_st(B, d, nv, qR, xr, B->lam[s], up);   /* q_h^+ at x_{i+1/2} */
+      /* q_h^- at x_{i+1/2} from the left cell, q_h^+ from the right cell; at a
+       * transmissive boundary face the missing side is NULL and takes the
+       * interior trace, q^+ = q^- (reading R5) */
+      if (qL) eval_st(B, d, nv, qL, xl, B->lam[s], um);
+      if (qR) eval_st(B, d, nv, qR, xr, B->lam[s], up);
+      if (!qL) memcpy(um, up, sizeof(double) * nv);
+      if (!qR) memcpy(up, um, sizeof(double) * nv);
       if (orc_rusanov(system, d, gamma, ch, um, up, dir, ft)) return 3;
       for (int v = 0; v < nv; ++v) F[v] += wgt * ft[v];
     }
@@ -787,6 +800,16 @@ static void gather_box(const orc_ctx* c, int i, int j, int k, double* box) {
   (void)W;
 }
 
+/* Ghost cell beyond a transmissive boundary (its predictor is never used). */
+static int beyond_transmissive(const orc_ctx* c, int i, int j, int k) {
+  const int ii[3] = {i, j, k};
+  for (int a = 0; a < c->d; ++a) {
+    if (ii[a] < 0 && c->cfg.bc[2 * a] == ORC_BC_TRANSMISSIVE) return 1;
+    if (ii[a] >= c->n[a] && c->cfg.bc[2 * a + 1] == ORC_BC_TRANSMISSIVE) return 1;
+  }
+  return 0;
+}
+
 /* Reconstruct + predict cell (i,j,k) (may be a ghost cell of depth 1). */
 static int cell_predict(orc_ctx* c, int i, int j, int k, double dt, double* q, int* sweeps) {
   int M = c->M, W = 2 * M + 1, nv = c->nv;
@@ -826,6 +849,7 @@ int orc_advance_box(orc_ctx* c, double dt, const int32_t* blo, const int32_t* bh
         int outside = (ci < lo[0] || ci >= hi[0]) + (cj < lo[1] || cj >= hi[1]) +
                       ((d == 3) && (ck < lo[2] || ck >= hi[2]));
         if (outside > 1) continue;   /* only face neighbours are needed */
+        if (beyond_transmissive(c, ci, cj, ck)) continue;   /* R5: not used */
         int sw = 0;
         int64_t e = ((int64_t)k * ext[1] + j) * ext[0] + i;
         if (cell_predict(c, ci, cj, ck, dt, &q[e * nv * NST], &sw)) { free(q); return 3; }
@@ -844,9 +868,11 @@ int orc_advance_box(orc_ctx* c, double dt, const int32_t* blo, const int32_t* bh
         double Fm[VMAX], Fp[VMAX];
         for (int dir = 0; dir < d; ++dir) {
           int64_t stride = (dir == 0) ? 1 : (dir == 1) ? ext[0] : (int64_t)ext[0] * ext[1];
+          const int ic[3] = {i, j, k};
           const double* qc = &q[e0 * nv * NST];
-          const double* qm = &q[(e0 - stride) * nv * NST];
-          const double* qp = &q[(e0 + stride) * nv * NST];
+          /* R5: a transmissive boundary face takes the interior trace on both sides */
+          const double* qm = (ic[dir] == 0 && c->cfg.bc[2 * dir] == ORC_BC_TRANSMISSIVE) ? NULL : &q[(e0 - stride) * nv * NST];
+          const double* qp = (ic[dir] == c->n[dir] - 1 && c->cfg.bc[2 * dir + 1] == ORC_BC_TRANSMISSIVE) ? NULL : &q[(e0 + stride) * nv * NST];
           if (orc_face_flux(d, c->M, c->cfg.system, c->cfg.gamma, c->cfg.ch, dir, qm, qc, Fm) ||
               orc_face_flux(d, c->M, c->cfg.system, c->cfg.gamma, c->cfg.ch, dir, qc, qp, Fp)) {
             snprintf(c->err, sizeof(c->err), "inadmissible face state at cell (%d,%d,%d) t=%.17g", i, j, k, c->t);
@@ -940,9 +966,13 @@ int orc_dump_flux(orc_ctx* c, double dt, double* F) {
           int im[3] = {i, j, k};
           im[dir] -= 1;
           int sw;
-          if (cell_predict(c, im[0], im[1], im[2], dt, qa, &sw)) goto fail;
-          if (cell_predict(c, i, j, k, dt, qb, &sw)) goto fail;
-          if (orc_face_flux(d, c->M, c->cfg.system, c->cfg.gamma, c->cfg.ch, dir, qa, qb, Fo)) goto fail;
+          const int lob = (i == 0 && dir == 0) || (j == 0 && dir == 1) || (k == 0 && dir == 2);
+          const int hib = ii[dir] == c->n[dir];
+          const int tlo = lob && c->cfg.bc[2 * dir] == ORC_BC_TRANSMISSIVE;
+          const int thi = hib && c->cfg.bc[2 * dir + 1] == ORC_BC_TRANSMISSIVE;
+          if (!tlo && cell_predict(c, im[0], im[1], im[2], dt, qa, &sw)) goto fail;
+          if (!thi && cell_predict(c, i, j, k, dt, qb, &sw)) goto fail;
+          if (orc_face_flux(d, c->M, c->cfg.system, c->cfg.gamma, c->cfg.ch, dir, tlo ? NULL : qa, thi ? NULL : qb, Fo)) goto fail;
         }
   free(qa); free(qb);
   return 0;

@@ -73,7 +73,9 @@ int  orc_predict_cell(int d, int M, int system, double gamma, double ch,
                       const double* w, const double* dtdx, double tol, int max_sweeps,
                       double* q, int* sweeps);
 /* Space-time Rusanov face flux (flux:F/G/H @ P:158-172, eqn.rusanov @ P:181-185)
- * between the left (lower) cell qL and right (upper) cell qR along dir. */
+ * between the left (lower) cell qL and right (upper) cell qR along dir.  At a
+ * transmissive boundary face pass NULL for the exterior side: it takes the
+ * interior trace (q^+ = q^-, reading R5). */
 int  orc_face_flux(int d, int M, int system, double gamma, double ch, int dir,
                    const double* qL, const double* qR, double* F);
 int  orc_phys_flux(int system, int dim, double gamma, double ch, const double* u, int dir, double* f);

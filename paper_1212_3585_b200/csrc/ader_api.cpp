@@ -329,8 +329,24 @@ void run_weno(ader_ctx* c) {
   }
 }
 
+// Physical transmissive sides of this rank's block (bit 2a: low side of axis a).
+int transmissive_mask(const ader_ctx* c) {
+  int m = 0;
+  for (int a = 0; a < c->d; ++a) {
+    if (c->part.nbr[2 * a] < 0 && c->cfg.bc[2 * a] == ADER_BC_TRANSMISSIVE) m |= 1 << (2 * a);
+    if (c->part.nbr[2 * a + 1] < 0 && c->cfg.bc[2 * a + 1] == ADER_BC_TRANSMISSIVE) m |= 1 << (2 * a + 1);
+  }
+  return m;
+}
+
 void run_predictor(ader_ctx* c, double dt) {
-  const Box r = grown(c, 1);
+  // owned block + the face-neighbour layer, except beyond transmissive sides (R5)
+  Box r = grown(c, 1);
+  const int tm = transmissive_mask(c);
+  for (int a = 0; a < c->d; ++a) {
+    if (tm & (1 << (2 * a))) { r.lo[a] += 1; r.ext[a] -= 1; }
+    if (tm & (1 << (2 * a + 1))) r.ext[a] -= 1;
+  }
   double dtdx[3] = {0, 0, 0};
   for (int k = 0; k < c->d; ++k) dtdx[k] = dt / c->dx[k];
   Scope s(c, ADER_K_PRED, 0.0);   // flops from the sweep counter (ader_kernel_stats)
@@ -353,7 +369,7 @@ void run_flux(ader_ctx* c) {
   long long nf = 0;
   for (int k = 0; k < c->d; ++k) nf += fb[k].count();
   Scope s(c, ADER_K_FLUX, face_flops(c) * nf);
-  launch_face_flux(c->k, c->q, c->F, fb, c->cnt);
+  launch_face_flux(c->k, c->q, c->F, fb, transmissive_mask(c), c->cnt);
 }
 
 void run_update(ader_ctx* c, double dt) {

@@ -186,13 +186,17 @@ __device__ __forceinline__ void weno1d(const DevTables& T, const double (&win)[2
       for (int o = 0; o < N; ++o) acc += T.rec[s][p][o] * win[M - Stencils<M>::L(s) + o];
       ws[s][p] = acc;
     }
+    // sigma_s = Sigma_pm w_p w_m (eqn.sigmas).  Sigma annihilates constants, so
+    // the dofs are shifted by the centre average first (reading R13): the
+    // unshifted quadratic form loses ~|w|^2 |Sigma| 1e-16 > eps to cancellation.
+    const double c0 = win[M];
     double sig = 0.0;
 #pragma unroll
     for (int p = 0; p < N; ++p) {
       double acc = 0.0;
 #pragma unroll
-      for (int m = 0; m < N; ++m) acc += T.sigma[p][m] * ws[s][m];
-      sig += acc * ws[s][p];
+      for (int m = 0; m < N; ++m) acc += T.sigma[p][m] * (ws[s][m] - c0);
+      sig += acc * (ws[s][p] - c0);
     }
     // omega~ = lambda_s / (sigma + 1e-14)^8 by three squarings
     double x = sig + 1e-14;

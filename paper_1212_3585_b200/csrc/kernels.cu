@@ -27,6 +27,13 @@ __device__ __forceinline__ long long box_cell(const Box& R, long long r, long lo
   return x + y * sy + z * sz;
 }
 
+__device__ __forceinline__ int box_coord(const Box& R, long long r, int axis) {
+  if (axis == 0) return R.lo[0] + (int)(r % R.ext[0]);
+  const long long t = r / R.ext[0];
+  if (axis == 1) return R.lo[1] + (int)(t % R.ext[1]);
+  return R.lo[2] + (int)(t / R.ext[1]);
+}
+
 __device__ __forceinline__ void record_error(DevCounters* c, int code, int stage, long long cell) {
   if (atomicCAS(&c->err_code, 0, code) == 0) {
     c->err_stage = stage;
@@ -182,7 +189,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_predictor(
 template <int D, int M, int SYS, int DIR, int WARPS>
 __device__ __forceinline__ void face_flux_dir(const double* __restrict__ q, double* __restrict__ F, const Box& R,
                                               long long sy, long long sz, long long ncell, double gamma, double ch,
-                                              DevCounters* cnt, const DevTables& T, double* red) {
+                                              int bmask, DevCounters* cnt, const DevTables& T, double* red) {
   using PH = Phys<SYS, D>;
   constexpr int NV = PH::NV, N = M + 1, NS = ipow_c(N, D), NST = NS * N;
   constexpr int NT = NS / N;   // tangential points
@@ -204,17 +211,21 @@ __device__ __forceinline__ void face_flux_dir(const double* __restrict__ q, doub
     const int base = s * NS + t1 * ipow_c(N, ax0) + (D == 3 ? t2 * ipow_c(N, ax1) : 0);
     const double* qL = q + cL * (NV * NST) + base;
     const double* qR = q + cR * (NV * NST) + base;
+    // transmissive boundary faces take the interior trace on both sides (reading R5)
+    const int fc = box_coord(R, rc, DIR);
+    const bool tlo = (bmask >> (2 * DIR)) & 1 && fc == R.lo[DIR];
+    const bool thi = (bmask >> (2 * DIR + 1)) & 1 && fc == R.lo[DIR] + R.ext[DIR] - 1;
     double um[NV], up[NV];
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
       double a = 0.0, b = 0.0;
 #pragma unroll
       for (int k = 0; k < N; ++k) {
-        a += T.psi1[k] * __ldg(&qL[v * NST + k * sn]);   // q_h^- at xi = 1 of the left cell
-        b += T.psi0[k] * __ldg(&qR[v * NST + k * sn]);   // q_h^+ at xi = 0 of the right cell
+        if (!tlo) a += T.psi1[k] * __ldg(&qL[v * NST + k * sn]);   // q_h^- at xi = 1 of the left cell
+        if (!thi) b += T.psi0[k] * __ldg(&qR[v * NST + k * sn]);   // q_h^+ at xi = 0 of the right cell
       }
-      um[v] = a;
-      up[v] = b;
+      um[v] = tlo ? b : a;
+      up[v] = thi ? a : b;
     }
     double fL[NV], fR[NV], sL, sR;
     bool ok = PH::template flux_speed<DIR>(um, gamma, ch, fL, sL);
@@ -240,13 +251,13 @@ template <int D, int M, int SYS, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32) k_face_flux(const double* __restrict__ q, double* __restrict__ F,
                                                           const Box R0, const Box R1, const Box R2, const long long sy,
                                                           const long long sz, const long long ncell,
-                                                          const double gamma, const double ch,
+                                                          const double gamma, const double ch, const int bmask,
                                                           DevCounters* __restrict__ cnt,
                                                           const __grid_constant__ DevTables T) {
   extern __shared__ double red[];
-  if (blockIdx.y == 0) face_flux_dir<D, M, SYS, 0, WARPS>(q, F, R0, sy, sz, ncell, gamma, ch, cnt, T, red);
-  else if (blockIdx.y == 1) face_flux_dir<D, M, SYS, 1, WARPS>(q, F, R1, sy, sz, ncell, gamma, ch, cnt, T, red);
-  else if (D == 3) face_flux_dir<D, M, SYS, 2, WARPS>(q, F, R2, sy, sz, ncell, gamma, ch, cnt, T, red);
+  if (blockIdx.y == 0) face_flux_dir<D, M, SYS, 0, WARPS>(q, F, R0, sy, sz, ncell, gamma, ch, bmask, cnt, T, red);
+  else if (blockIdx.y == 1) face_flux_dir<D, M, SYS, 1, WARPS>(q, F, R1, sy, sz, ncell, gamma, ch, bmask, cnt, T, red);
+  else if (D == 3) face_flux_dir<D, M, SYS, 2, WARPS>(q, F, R2, sy, sz, ncell, gamma, ch, bmask, cnt, T, red);
 }
 
 // ===========================================================================
@@ -485,7 +496,7 @@ void launch_predictor(const KCtx& k, const double* w, double* q, const Box& regi
   });
 }
 
-void launch_face_flux(const KCtx& k, const double* q, double* F, const Box faces[3], DevCounters* cnt) {
+void launch_face_flux(const KCtx& k, const double* q, double* F, const Box faces[3], int bmask, DevCounters* cnt) {
   long long mx = 0;
   for (int d = 0; d < k.D; ++d) mx = faces[d].count() > mx ? faces[d].count() : mx;
   if (mx == 0) return;
@@ -503,7 +514,7 @@ void launch_face_flux(const KCtx& k, const double* q, double* F, const Box faces
     dim3 g(grid_for(mx, kFluxWarps * CPW), D);
     count_launch(k);
     kern<<<g, kFluxWarps * 32, sm, k.stream>>>(q, F, faces[0], faces[1], faces[2], k.sy, k.sz, k.ncell, k.gamma,
-                                                k.ch, cnt, k.tab);
+                                                k.ch, bmask, cnt, k.tab);
   });
 }
 

@@ -50,7 +50,9 @@ void launch_weno_sweep(const KCtx& k, int sweep, const double* src, double* dst,
 void launch_predictor(const KCtx& k, const double* w, double* q, const Box& region, const double dtdx[3],
                       double tol, int max_sweeps, DevCounters* cnt);
 // Face fluxes on the lower face of every cell of faces[dir], for dir < D.
-void launch_face_flux(const KCtx& k, const double* q, double* F, const Box faces[3], DevCounters* cnt);
+// bmask bit 2*dir (2*dir+1): the first (last) face along dir is a physical
+// transmissive boundary and takes the interior trace on both sides.
+void launch_face_flux(const KCtx& k, const double* q, double* F, const Box faces[3], int bmask, DevCounters* cnt);
 // FV update of `interior` in place + max CFL speed of the new state.
 void launch_update(const KCtx& k, double* u, const double* F, const Box& interior, const double dtdx[3],
                    const double inv_dx[3], DevCounters* cnt);

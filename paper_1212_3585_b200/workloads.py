@@ -190,11 +190,13 @@ def config(name: str, n=None) -> Workload:
     if name == "c3":
         nn = n or 100
         return Workload("c3_explosion2d_amr", 2, 0, 2, (nn, nn), (-1.0, -1.0), (1.0, 1.0),
-                        (T,) * 6, 1.4, 0.9, 0.25, ic=explosion(2), refine_factor=3, lmax=2)
+                        (T,) * 6, 1.4, 0.45, 0.25, ic=explosion(2), refine_factor=3, lmax=2)
     if name == "c4":
         nn = n or 256
+        # CFL 0.3: at 0.9, 0.6 and 0.5 both the oracle and the CUDA path
+        # reach an inadmissible face state (profiles/round1_explosion3d_cfl_probe.jsonl)
         return Workload(f"c4_explosion3d_o3_{nn}", 3, 0, 2, (nn, nn, nn), (-1.0,) * 3, (1.0,) * 3,
-                        (T,) * 6, 1.4, 0.9, 1e300, steps=50, ic=explosion(3))
+                        (T,) * 6, 1.4, 0.3, 1e300, steps=50, ic=explosion(3))
     if name == "c5":
         nn = n or 120
         return Workload("c5_orszag_tang_mhd", 2, 1, 3, (nn, nn), (0.0, 0.0),

@@ -17,11 +17,13 @@ pytestmark = pytest.mark.gpu
 
 
 def rel_err(a, b, axis=None):
-    """max |a-b| / max |b| per trailing variable, then max over variables."""
+    """Reading R8: max |a-b| / scale_v per trailing variable v, then max over v,
+    with scale_v = max(max_c |b_v|, max_c |b_0|): a variable that is zero in
+    exact arithmetic (v_y of a 1D tube, psi of Orszag-Tang at t=0) is measured
+    against the density scale."""
     b2 = b.reshape(-1, b.shape[-1])
     a2 = a.reshape(-1, a.shape[-1])
-    scale = np.abs(b2).max(axis=0)
-    scale[scale == 0] = 1.0
+    scale = np.maximum(np.abs(b2).max(axis=0), np.abs(b2[:, 0]).max())
     return (np.abs(a2 - b2).max(axis=0) / scale).max()
 
 
@@ -110,10 +112,12 @@ def test_100_step_parity_and_conservation():
     assert rg.pred_sweeps_max <= 32
 
 
-def test_100_step_parity_3d_explosion():
-    g, o = pair(3, 2, (10, 10, 10), (-1,) * 3, (1,) * 3, (1,) * 6, W.explosion(3))
-    g.step(1e300, 100)
-    o.step(1e300, 100)
+def test_3d_explosion_to_paper_final_time():
+    # P:1018 Table tab.3d.explos.ic: t_e = 0.25
+    g, o = pair(3, 2, (12, 12, 12), (-1,) * 3, (1,) * 3, (1,) * 6, W.explosion(3))
+    rg = g.step(0.25, 10 ** 6)
+    ro = o.step(0.25, 10 ** 6)
+    assert rg.macro_steps == ro.steps
     assert rel_err(g.get_state(), o.get_cells()) <= 1e-8
 
 
@@ -179,12 +183,13 @@ def test_c2_512_sampled_parity():
     for blo, bhi in boxes:
         out, _ = o.advance_box(dt, blo, bhi)
         gg = ug[blo[1]:bhi[1], blo[0]:bhi[0]].reshape(-1, 4)
-        assert rel_err(gg, out) <= 1e-11 or np.abs(gg - out).max() <= 1e-11 * np.abs(ug).reshape(-1, 4).max(0).max()
+        scale = np.maximum(np.abs(ug).reshape(-1, 4).max(0), 1.0)
+        assert (np.abs(gg - out).max(axis=0) / scale).max() <= 1e-11, (blo, np.abs(gg - out).max(axis=0))
 
 
 def test_c4_256_sampled_parity():
     wl = W.config("c4", 256)
-    cfg = ader.make_config(dim=3, degree=2, n0=wl.n, lo=wl.lo, hi=wl.hi, bc=wl.bc, device=0)
+    cfg = ader.make_config(dim=3, degree=2, n0=wl.n, lo=wl.lo, hi=wl.hi, bc=wl.bc, cfl=wl.cfl, device=0)
     g = ader.Solver(cfg)
     g.set_initial(wl.ic)
     rep = g.step(1e300, 1)
@@ -193,10 +198,10 @@ def test_c4_256_sampled_parity():
     uin = O.prim_to_cons(0, 3, 1.4, [1, 0, 0, 0, 1])
     dx = 2.0 / 256
     s = sum(O.max_speed(0, 3, 1.4, 0, uin, d) / dx for d in range(3))
-    dt = 0.9 / s
+    dt = wl.cfl / s
     assert abs(rep.dt0 - dt) <= 1e-14 * dt
     ug = g.get_state().reshape(256, 256, 256, 5)
-    o = O.Oracle(dim=3, degree=2, n=wl.n, lo=wl.lo, hi=wl.hi, bc=wl.bc)
+    o = O.Oracle(dim=3, degree=2, n=wl.n, lo=wl.lo, hi=wl.hi, bc=wl.bc, cfl=wl.cfl)
     scale = np.array([1.0, 1.0, 1.0, 1.0, 2.5])
     boxes = [((0, 0, 0), (2, 2, 2)), ((254, 100, 127), (256, 102, 129)),   # corner / face
              ((62, 127, 127), (65, 129, 129)),                              # across r = 0.5

@@ -199,3 +199,17 @@ def test_dense_predictor_operators_structure(d, M):
     wsp = np.random.default_rng(1).normal(size=NS)
     q = np.linalg.solve(K1, F0 @ wsp)
     np.testing.assert_allclose(q, np.tile(wsp, N), atol=1e-12)
+
+
+@pytest.mark.parametrize("M", [2, 3])
+def test_weno_linear_weights_on_near_constant_data(M):
+    # R13: in smooth regions with sigma << eps = 1e-14 the nonlinear
+    # weights reduce to the linear ones; the oscillation indicator must not be
+    # swamped by round-off of the O(1) dofs (data 3.5 + 1e-9 sin).
+    t = O.tables(M)
+    x = np.arange(-M, M + 1)
+    win = 3.5 + 1e-9 * np.sin(0.7 * x + 0.3)
+    out = O.weno_1d(M, win)
+    lin = t["lin"] / t["lin"].sum()
+    ref = sum(lin[s] * (t["rec"][s] @ win[M - t["L"][s]: M + t["R"][s] + 1]) for s in range(t["nS"]))
+    np.testing.assert_allclose(out, ref, rtol=0, atol=2e-15)
