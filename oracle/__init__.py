@@ -306,3 +306,121 @@ class Oracle:
         rc = lib().orc_dump_flux(self.ptr, dt, _p(F))
         assert rc == 0, self.error()
         return F
+
+
+class AmrCell(C.Structure):
+    _fields_ = [("level", C.c_int32), ("status", C.c_int32), ("idx", C.c_int64 * 3), ("u", C.c_double * 9)]
+
+
+def indicator(d, phi, eps=0.01):
+    phi = np.ascontiguousarray(phi, dtype=np.float64).reshape(-1)
+    L = lib()
+    L.orc_indicator.restype = C.c_double
+    L.orc_indicator.argtypes = [C.c_int, C.POINTER(C.c_double), C.c_double]
+    return L.orc_indicator(d, _p(phi), eps)
+
+
+class AmrOracle:
+    """Cell-by-cell AMR + LTS oracle (oracle/ader_oracle_amr.c)."""
+
+    def __init__(self, *, dim, degree, n, lo, hi, bc, system=EULER, gamma=1.4, ch=0.0, cfl=0.45,
+                 refine_factor=3, lmax=1, chi_ref=0.2, chi_rec=0.1, chi_eps=0.01, pred_tol=1e-13,
+                 pred_max_sweeps=32, ic_quad=0):
+        L = lib()
+        vp = C.c_void_p
+        L.orc_amr_create.restype = vp
+        L.orc_amr_create.argtypes = [C.POINTER(OrcConfig)]
+        L.orc_amr_destroy.argtypes = [vp]
+        L.orc_amr_last_error.restype = C.c_char_p
+        L.orc_amr_last_error.argtypes = [vp]
+        L.orc_amr_time.restype = C.c_double
+        L.orc_amr_time.argtypes = [vp]
+        L.orc_amr_set_initial.argtypes = [vp, IC_FN, vp]
+        L.orc_amr_compute_dt.restype = C.c_double
+        L.orc_amr_compute_dt.argtypes = [vp]
+        L.orc_amr_step.argtypes = [vp, C.c_double, C.c_int64, C.c_int, C.POINTER(OrcReport)]
+        L.orc_amr_adapt.argtypes = [vp]
+        L.orc_amr_get_cells.restype = C.c_int64
+        L.orc_amr_get_cells.argtypes = [vp, C.POINTER(AmrCell)]
+        L.orc_amr_check.argtypes = [vp, C.c_char_p, C.c_int]
+        L.orc_amr_refine_cell.argtypes = [vp, C.c_int, C.POINTER(C.c_int64)]
+        L.orc_amr_schedule.argtypes = [C.POINTER(C.c_int), C.c_int]
+        cfg = OrcConfig()
+        cfg.dim, cfg.system, cfg.degree = dim, system, degree
+        n = list(n) + [1] * (3 - len(n))
+        lo = list(lo) + [0.0] * (3 - len(lo))
+        hi = list(hi) + [1.0] * (3 - len(hi))
+        for k in range(3):
+            cfg.n[k], cfg.lo[k], cfg.hi[k] = n[k], lo[k], hi[k]
+        bc = list(bc) + [0] * (6 - len(bc))
+        for k in range(6):
+            cfg.bc[k] = bc[k]
+        cfg.gamma, cfg.ch, cfg.cfl = gamma, ch, cfl
+        cfg.pred_tol, cfg.pred_max_sweeps, cfg.ic_quad = pred_tol, pred_max_sweeps, ic_quad
+        cfg.refine_factor, cfg.lmax = refine_factor, lmax
+        cfg.chi_ref, cfg.chi_rec, cfg.chi_eps = chi_ref, chi_rec, chi_eps
+        self.cfg, self.dim, self.nv = cfg, dim, nvar(system, dim)
+        self.ptr = L.orc_amr_create(C.byref(cfg))
+        if not self.ptr:
+            raise ValueError("orc_amr_create rejected the configuration")
+
+    def __del__(self):
+        if getattr(self, "ptr", None):
+            lib().orc_amr_destroy(self.ptr)
+            self.ptr = None
+
+    def error(self):
+        return lib().orc_amr_last_error(self.ptr).decode()
+
+    def set_initial(self, ic):
+        def cb(xp, n, pp, user):
+            x = np.ctypeslib.as_array(xp, shape=(n, 3))
+            p = np.ctypeslib.as_array(pp, shape=(n, 9))
+            p[:] = ic(x)
+        self._cb = IC_FN(cb)
+        rc = lib().orc_amr_set_initial(self.ptr, self._cb, None)
+        if rc:
+            raise RuntimeError(self.error())
+
+    @property
+    def t(self):
+        return lib().orc_amr_time(self.ptr)
+
+    def compute_dt(self):
+        return lib().orc_amr_compute_dt(self.ptr)
+
+    def step(self, t_end=1e300, max_steps=1, adapt_every=1):
+        rep = OrcReport()
+        rc = lib().orc_amr_step(self.ptr, t_end, max_steps, adapt_every, C.byref(rep))
+        if rc:
+            raise RuntimeError(f"AMR oracle step failed: {self.error()}")
+        return rep
+
+    def adapt(self):
+        assert lib().orc_amr_adapt(self.ptr) == 0, self.error()
+
+    def cells(self):
+        """structured array: level, status, idx[3], u[9] sorted by (level, z, y, x)"""
+        n = lib().orc_amr_get_cells(self.ptr, None)
+        arr = (AmrCell * n)()
+        lib().orc_amr_get_cells(self.ptr, arr)
+        lv = np.array([c.level for c in arr], dtype=np.int32)
+        st = np.array([c.status for c in arr], dtype=np.int32)
+        ix = np.array([list(c.idx) for c in arr], dtype=np.int64).reshape(-1, 3)
+        u = np.array([list(c.u)[:self.nv] for c in arr]).reshape(-1, self.nv)
+        return lv, st, ix, u
+
+    def check(self):
+        buf = C.create_string_buffer(256)
+        rc = lib().orc_amr_check(self.ptr, buf, 256)
+        return rc, buf.value.decode()
+
+    def refine_cell(self, level, idx):
+        a = (C.c_int64 * 3)(*((list(idx) + [0, 0, 0])[:3]))
+        return lib().orc_amr_refine_cell(self.ptr, level, a)
+
+    @staticmethod
+    def schedule():
+        buf = (C.c_int * 4096)()
+        n = lib().orc_amr_schedule(buf, 4096)
+        return list(buf[:min(n, 4096)])

@@ -83,6 +83,26 @@ double orc_max_speed(int system, int dim, double gamma, double ch, const double*
 int  orc_rusanov(int system, int dim, double gamma, double ch, const double* uL,
                  const double* uR, int dir, double* f);
 void orc_prim_to_cons(int system, int dim, double gamma, const double* prim, double* u);
+/* q_h(xi, tau) = theta_p(xi, tau) q_p (eqn.st.q @ P:391-394), q[nv][N^(d+1)]. */
+void orc_eval_st(int d, int M, int nv, const double* q, const double* xi, double tau, double* out);
+/* w_h(xi) = psi_p(xi) w_p (eqn.weno.z @ P:314-317), w[nv][N^d]. */
+void orc_eval_w(int d, int M, int nv, const double* w, const double* xi, double* out);
+/* n-point Gauss-Legendre rule on [0,1]. */
+void orc_gauss_legendre(int n, double* x, double* w);
+/* Space-time Rusanov flux along dir integrated over the face sub-box of the
+ * left cell qL and right cell qR: the face points are given in each cell's
+ * reference coordinates by affine maps xi = a + b * eta (eta the fine face /
+ * time GL nodes), i.e. for cell X: xi_k = offX[k] + sclX * eta_k on the
+ * tangential axes, xi_dir = posX, tau = toffX + tsclX * eta_t.  NULL side =
+ * transmissive boundary (interior trace on both sides).  Used by the AMR
+ * oracle for same-level and coarse-fine faces. */
+int  orc_face_flux_mapped(int d, int M, int system, double gamma, double ch, int dir,
+                          const double* qL, const double* offL, double sclL, double toffL, double tsclL,
+                          const double* qR, const double* offR, double sclR, double toffR, double tsclR,
+                          double* F);
+/* Loehner-type indicator chi of eqn.indicator in the discretised
+ * reading R14 from the 3^d same-level box of Phi (x fastest). */
+double orc_indicator(int d, const double* phi, double eps);
 
 /* ---- uniform-grid driver --------------------------------------------- */
 orc_ctx* orc_create(const orc_config* cfg);
