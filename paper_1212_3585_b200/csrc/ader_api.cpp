@@ -22,6 +22,7 @@
 #include "../../include/ader.h"
 #include "launch.h"
 #include "tables.h"
+#include "amr.h"
 
 using namespace ader;
 
@@ -90,6 +91,7 @@ struct ader_ctx {
   unsigned long long prof_sweeps0 = 0;
   double kflops_sweep = 0.0;                   // predictor flops per cell per sweep
   long long launches = 0;                      // kernels launched by this context
+  AmrState* amr = nullptr;                     // lmax > 0: device-resident AMR
 };
 
 namespace {
@@ -137,7 +139,9 @@ ader_status validate(const ader_config* cfg, std::string& why) {
       return bad("periodic bc must be set on both sides of an axis");
   if (cfg->lmax < 0 || cfg->lmax > 7) return bad("lmax out of range");
   if (cfg->lmax > 0 && cfg->refine_factor < cfg->degree) return bad("refine_factor r must be >= M (P:539-541)");
-  if (cfg->lmax > 0) return ADER_ERR_UNSUPPORTED;
+  if (cfg->lmax > 0 && cfg->world_size > 1) return ADER_ERR_UNSUPPORTED;   // AMR: one GPU (round 1)
+  if (cfg->lmax > 0 && cfg->refine_factor > 4) return bad("refine_factor must be <= 4");
+  if (cfg->lmax > 0 && cfg->ic_quad > 4) return bad("AMR ic_quad must be <= 4");
   if (!(cfg->gamma > 1.0)) return bad("gamma must exceed 1");
   if (!(cfg->cfl > 0.0)) return bad("cfl must be positive");
   if (cfg->world_size < 1 || cfg->world_size > 8) return bad("world_size must be in 1..8");
@@ -416,6 +420,7 @@ ader_status global_speed(ader_ctx* c, double* speed) {
 void free_ctx(ader_ctx* c) {
   if (!c) return;
   if (c->k.stream) cudaStreamSynchronize(c->k.stream);
+  if (c->amr) amr_destroy(c->amr);
   double* bufs[] = {c->u, c->wx, c->wxy, c->w, c->q, c->F, c->stage};
   for (double* b : bufs)
     if (b) cudaFree(b);
@@ -560,6 +565,18 @@ static ader_status create_impl(const ader_config* cfg, ader_ctx** out) {
   c->k.gamma = cfg->gamma; c->k.ch = cfg->ch;
   c->k.stream = c->own_stream;
   c->k.launches = &c->launches;
+  c->kflops_sweep = pred_sweep_flops(c);
+  if (cfg->lmax > 0) {
+    // device-resident cell-by-cell AMR (amr.cpp); uniform buffers are not used
+    CK(cudaMalloc(&c->cnt, sizeof(DevCounters)));
+    CK(cudaMemset(c->cnt, 0, sizeof(DevCounters)));
+    CK(cudaMallocHost(&c->hcnt, sizeof(DevCounters)));
+    std::memset(c->hcnt, 0, sizeof(DevCounters));
+    std::string err;
+    c->amr = amr_create(cfg, &c->k, c->cnt, c->hcnt, err);
+    if (!c->amr) return fail(c, ADER_ERR_CUDA, "amr_create: %s", err.c_str());
+    return ADER_OK;
+  }
   const size_t nc = (size_t)c->ncell;
   auto alloc = [&](double** p, size_t n) { return cudaMalloc(p, n * sizeof(double)); };
   CK(alloc(&c->u, nc * c->nv));
@@ -611,10 +628,16 @@ ader_status ader_set_stream(ader_ctx* c, void* s) {
   return ADER_OK;
 }
 
-double ader_time(const ader_ctx* c) { return c ? c->t : 0.0; }
+double ader_time(const ader_ctx* c) { return c ? (c->amr ? amr_time(c->amr) : c->t) : 0.0; }
 
 ader_status ader_set_initial(ader_ctx* c, ader_ic_fn ic, void* user) {
   if (!c || !ic) return ADER_ERR_ARG;
+  if (c->amr) {
+    std::string e;
+    ader_status s = amr_set_initial(c->amr, ic, user, e);
+    if (s != ADER_OK) c->err = e;
+    return s;
+  }
   const int Q = c->cfg.ic_quad, d = c->d;
   double qx[16], qw[16];
   gl_rule(Q, qx, qw);
@@ -662,6 +685,7 @@ ader_status ader_set_initial(ader_ctx* c, ader_ic_fn ic, void* user) {
 
 ader_status ader_set_cells(ader_ctx* c, const double* u_host, int64_t n_cells) {
   if (!c || !u_host) return ADER_ERR_ARG;
+  if (c->amr) return fail(c, ADER_ERR_UNSUPPORTED, "ader_set_cells: uniform grids only (use ader_set_initial)");
   const Box b = owned(c);
   if (n_cells != b.count()) return fail(c, ADER_ERR_ARG, "n_cells %lld != owned %lld", (long long)n_cells, b.count());
   CK(cudaMemcpyAsync(c->stage, u_host, (size_t)n_cells * c->nv * sizeof(double), cudaMemcpyHostToDevice, c->k.stream));
@@ -674,6 +698,7 @@ ader_status ader_set_cells(ader_ctx* c, const double* u_host, int64_t n_cells) {
 ader_status ader_get_state(const ader_ctx* cc, double* u_host, int64_t capacity) {
   ader_ctx* c = const_cast<ader_ctx*>(cc);
   if (!c || !u_host) return ADER_ERR_ARG;
+  if (c->amr) return fail(c, ADER_ERR_UNSUPPORTED, "ader_get_state: uniform grids only (use ader_get_cells)");
   const Box b = owned(c);
   if (capacity < b.count()) return fail(c, ADER_ERR_ARG, "capacity too small");
   launch_gather(c->k, c->u, c->nv, b, c->stage);
@@ -685,6 +710,12 @@ ader_status ader_get_state(const ader_ctx* cc, double* u_host, int64_t capacity)
 ader_status ader_get_cells(const ader_ctx* cc, ader_cell* out, int64_t capacity, int64_t* n) {
   ader_ctx* c = const_cast<ader_ctx*>(cc);
   if (!c || !n) return ADER_ERR_ARG;
+  if (c->amr) {
+    std::string e;
+    ader_status s = amr_get_cells(c->amr, out, capacity, n, e);
+    if (s != ADER_OK) c->err = e;
+    return s;
+  }
   const Box b = owned(c);
   *n = b.count();
   if (!out) return ADER_OK;
@@ -708,6 +739,13 @@ ader_status ader_get_cells(const ader_ctx* cc, ader_cell* out, int64_t capacity,
 ader_status ader_step(ader_ctx* c, double t_end, int64_t max_macro_steps, ader_step_report* rep) {
   if (!c) return ADER_ERR_ARG;
   const auto w0 = std::chrono::steady_clock::now();
+  if (c->amr) {
+    std::string e;
+    ader_status s = amr_step(c->amr, t_end, max_macro_steps, rep, e);
+    if (s != ADER_OK) c->err = e;
+    if (rep) rep->wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - w0).count();
+    return s;
+  }
   ader_step_report r;
   std::memset(&r, 0, sizeof(r));
   CK(cudaMemcpyAsync(c->hcnt, c->cnt, sizeof(DevCounters), cudaMemcpyDeviceToHost, c->k.stream));
@@ -768,6 +806,12 @@ ader_status ader_step(ader_ctx* c, double t_end, int64_t max_macro_steps, ader_s
 ader_status ader_refine(ader_ctx* c, ader_step_report* rep) {
   if (!c) return ADER_ERR_ARG;
   if (rep) std::memset(rep, 0, sizeof(*rep));
+  if (c->amr) {
+    std::string e;
+    ader_status s = amr_adapt(c->amr, e);
+    if (s != ADER_OK) c->err = e;
+    return s;
+  }
   return ADER_OK;   // uniform grid: nothing to adapt
 }
 
@@ -811,6 +855,7 @@ ader_status ader_launch_count(const ader_ctx* c, int64_t* n) {
 
 ader_status ader_debug_dump(ader_ctx* c, int32_t what, double dt, double* out, int64_t capacity) {
   if (!c || !out) return ADER_ERR_ARG;
+  if (c->amr) return fail(c, ADER_ERR_UNSUPPORTED, "ader_debug_dump: uniform grids only");
   const Box b = owned(c);
   ader_status st = fill_halo(c, c->u);
   if (st != ADER_OK) return st;

@@ -1,0 +1,685 @@
+// amr.cpp — host orchestration of the device-resident AMR (see amr.h).
+//
+// The tree topology (status, links) is mirrored here because the adapt rules
+// are integer logic on a few hundred thousand cells once per macro step; all
+// floating-point work runs on the GPU.  The adapt follows the same readings
+// as DESIGN.md R14-R20 (order-independent closure, simultaneous recoarsening
+// that the closure may revert, GC), written independently of oracle/.
+// Citations: P:n = PAPER.md line n.
+#include "amr.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+namespace ader {
+
+namespace {
+struct HCell {
+  int level = 0, status = 0, mother = -1, child = -1;
+  long long idx[3] = {0, 0, 0};
+  bool alive = false, isnew = false;
+};
+
+// one pending device initialisation of a cell's average
+struct Init { int cell, mother, mode; };   // mode 0: WENO sub-box, 1: q_h at tau=1, 2: IC
+}  // namespace
+
+struct AmrState {
+  ader_config cfg{};
+  KCtx* k = nullptr;
+  DevCounters* cnt = nullptr;
+  DevCounters* hcnt = nullptr;
+  int d = 2, M = 2, N = 3, nv = 4, NS = 9, NST = 27, r = 3, rd = 9, lmax = 1;
+  long long n[kAmrMaxLevels][3]{};
+  double dx[kAmrMaxLevels][3]{};
+  std::vector<HCell> cells;
+  std::vector<int> free_blocks;                       // first ids of freed r^d blocks
+  std::vector<std::vector<int>> hmap;                 // dense id maps per level
+  int cap = 0;
+  AmrDevView V{};
+  int* dmap[kAmrMaxLevels]{};
+  int* dlist = nullptr;
+  long long dlist_cap = 0;
+  // lists (host) and their offsets inside dlist
+  std::vector<int> lact[kAmrMaxLevels], lvch[kAmrMaxLevels], lvmo[kAmrMaxLevels], lall;
+  long long oact[kAmrMaxLevels]{}, ovch[kAmrMaxLevels]{}, ovmo[kAmrMaxLevels]{}, oall = 0;
+  SubTables st{};
+  double t = 0.0;
+  ader_ic_fn ic = nullptr;
+  void* user = nullptr;
+  std::vector<Init> inits;
+  std::vector<int> chi_ids;
+  std::vector<double> chi;
+  long long updates[kAmrMaxLevels]{};
+  std::string err;
+};
+
+namespace {
+
+#define ACK(call)                                                                        \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess) { err = std::string(#call) + ": " + cudaGetErrorString(e_); return ADER_ERR_CUDA; } \
+  } while (0)
+
+double lagrange(const DevTables& T, int N, int p, double x) {
+  double v = 1.0;
+  for (int k = 0; k < N; ++k)
+    if (k != p) v *= (x - T.lam[k]) / (T.lam[p] - T.lam[k]);
+  return v;
+}
+
+void build_sub(const DevTables& T, int N, int r, SubTables* S) {
+  std::memset(S, 0, sizeof(*S));
+  S->r = r;
+  for (int c = 0; c < r; ++c) {
+    for (int p = 0; p < N; ++p) {
+      // r * int_{c/r}^{(c+1)/r} psi_p = sum_k w_k psi_p((c + lam_k)/r)  (exact, degree M)
+      double acc = 0.0;
+      for (int k = 0; k < N; ++k) acc += T.w[k] * lagrange(T, N, p, (c + T.lam[k]) / r);
+      S->Psub[c][p] = acc;
+    }
+    for (int k = 0; k < N; ++k)
+      for (int p = 0; p < N; ++p) S->Esub[c][k][p] = lagrange(T, N, p, (c + T.lam[k]) / r);
+  }
+}
+
+long long lin(const AmrState* A, int l, const long long* ix) { return (ix[2] * A->n[l][1] + ix[1]) * A->n[l][0] + ix[0]; }
+
+int hlookup(const AmrState* A, int l, const long long* ix0, bool skip_outside) {
+  long long ix[3] = {ix0[0], ix0[1], ix0[2]};
+  for (int k = 0; k < A->d; ++k) {
+    const long long nn = A->n[l][k];
+    if (ix[k] < 0 || ix[k] >= nn) {
+      const int side = ix[k] < 0 ? 0 : 1;
+      if (A->cfg.bc[2 * k + side] == ADER_BC_PERIODIC) ix[k] = ((ix[k] % nn) + nn) % nn;
+      else {
+        if (skip_outside) return -1;
+        ix[k] = ix[k] < 0 ? 0 : nn - 1;
+      }
+    }
+  }
+  if (A->d == 2) ix[2] = 0;
+  return A->hmap[l][lin(A, l, ix)];
+}
+
+int voronoi(const AmrState* A, int id, int* out) {
+  const HCell& C = A->cells[id];
+  int cnt = 0;
+  const int zl = A->d == 3 ? -1 : 0, zh = A->d == 3 ? 1 : 0;
+  for (int dz = zl; dz <= zh; ++dz)
+    for (int dy = -1; dy <= 1; ++dy)
+      for (int dx = -1; dx <= 1; ++dx) {
+        if (!dx && !dy && !dz) continue;
+        const long long ix[3] = {C.idx[0] + dx, C.idx[1] + dy, C.idx[2] + dz};
+        out[cnt++] = hlookup(A, C.level, ix, true);
+      }
+  return cnt;
+}
+
+int alloc_block(AmrState* A) {
+  if (!A->free_blocks.empty()) {
+    const int id = A->free_blocks.back();
+    A->free_blocks.pop_back();
+    return id;
+  }
+  const int id = (int)A->cells.size();
+  A->cells.resize(A->cells.size() + A->rd);
+  return id;
+}
+
+int make_children(AmrState* A, int m, int status) {
+  const int id = alloc_block(A);
+  HCell& Mc = A->cells[m];
+  Mc.child = id;
+  const int l = Mc.level + 1;
+  for (int q = 0; q < A->rd; ++q) {
+    HCell& C = A->cells[id + q];
+    C = HCell();
+    C.alive = true;
+    C.level = l;
+    C.status = status;
+    C.mother = m;
+    const int off[3] = {q % A->r, (q / A->r) % A->r, A->d == 3 ? q / (A->r * A->r) : 0};
+    for (int k = 0; k < 3; ++k) C.idx[k] = k < A->d ? A->cells[m].idx[k] * A->r + off[k] : 0;
+    A->hmap[l][lin(A, l, C.idx)] = id + q;
+  }
+  return id;
+}
+
+void destroy_children(AmrState* A, int m, std::vector<int>* freed) {
+  const int ch = A->cells[m].child;
+  if (ch < 0) return;
+  for (int q = 0; q < A->rd; ++q) {
+    HCell& C = A->cells[ch + q];
+    if (C.child >= 0) destroy_children(A, ch + q, freed);
+    A->hmap[C.level][lin(A, C.level, C.idx)] = -1;
+    C = HCell();
+  }
+  freed->push_back(ch);
+  A->cells[m].child = -1;
+}
+
+void refine_cell(AmrState* A, int c, bool t0) {
+  if (A->cells[c].child < 0) make_children(A, c, 0);
+  else
+    for (int q = 0; q < A->rd; ++q) A->cells[A->cells[c].child + q].status = 0;
+  A->cells[c].status = -1;
+  const int ch = A->cells[c].child;
+  for (int q = 0; q < A->rd; ++q) {
+    A->cells[ch + q].isnew = true;
+    A->inits.push_back({ch + q, c, t0 ? 2 : 0});
+  }
+}
+
+void virtually_refine(AmrState* A, int v, bool t0) {
+  const int ch = make_children(A, v, 1);
+  for (int q = 0; q < A->rd; ++q) A->inits.push_back({ch + q, v, t0 ? 2 : 1});
+}
+
+void closure(AmrState* A, bool t0) {
+  int nb[26];
+  bool changed = true;
+  while (changed) {
+    changed = false;
+    const int nu = (int)A->cells.size();
+    for (int i = 0; i < nu; ++i) {
+      if (!A->cells[i].alive || A->cells[i].status != -1) continue;
+      const int k = voronoi(A, i, nb);
+      for (int j = 0; j < k; ++j) {
+        const int v = nb[j];
+        if (v < 0 || A->cells[v].child >= 0) continue;
+        if (A->cells[v].status == 0) { virtually_refine(A, v, t0); changed = true; }
+        else if (A->cells[v].status == 1) { refine_cell(A, A->cells[v].mother, t0); changed = true; }
+      }
+    }
+  }
+}
+
+void garbage_collect(AmrState* A, std::vector<int>* freed) {
+  int nb[26];
+  for (int i = 0; i < (int)A->cells.size(); ++i) {
+    HCell& C = A->cells[i];
+    if (!C.alive || C.status != 0 || C.child < 0) continue;
+    const int k = voronoi(A, i, nb);
+    bool need = false;
+    for (int j = 0; j < k && !need; ++j) need = nb[j] >= 0 && A->cells[nb[j]].status == -1;
+    if (!need) destroy_children(A, i, freed);
+  }
+}
+
+// ---- device mirrors ---------------------------------------------------------
+ader_status ensure_capacity(AmrState* A, std::string& err) {
+  const int need = (int)A->cells.size();
+  if (need <= A->cap) return ADER_OK;
+  const int nc = std::max(need + need / 2, 1024);
+  auto grow = [&](void** p, size_t elem) -> cudaError_t {
+    void* np = nullptr;
+    cudaError_t e = cudaMalloc(&np, (size_t)nc * elem);
+    if (e != cudaSuccess) return e;
+    cudaMemsetAsync(np, 0, (size_t)nc * elem, A->k->stream);
+    if (*p) {
+      cudaMemcpyAsync(np, *p, (size_t)A->cap * elem, cudaMemcpyDeviceToDevice, A->k->stream);
+      cudaStreamSynchronize(A->k->stream);
+      cudaFree(*p);
+    }
+    *p = np;
+    return cudaSuccess;
+  };
+  AmrDevView& V = A->V;
+  ACK(grow((void**)&V.u, sizeof(double) * A->nv));
+  ACK(grow((void**)&V.mem, sizeof(double) * 6 * A->nv));
+  ACK(grow((void**)&V.w, sizeof(double) * A->nv * A->NS));
+  ACK(grow((void**)&V.q, sizeof(double) * A->nv * A->NST));
+  ACK(grow((void**)&V.chi, sizeof(double)));
+  ACK(grow((void**)&V.level, sizeof(int)));
+  ACK(grow((void**)&V.status, sizeof(int)));
+  ACK(grow((void**)&V.mother, sizeof(int)));
+  ACK(grow((void**)&V.child, sizeof(int)));
+  ACK(grow((void**)&V.idx, sizeof(long long) * 3));
+  A->cap = nc;
+  return ADER_OK;
+}
+
+ader_status upload_topology(AmrState* A, std::string& err) {
+  ader_status s = ensure_capacity(A, err);
+  if (s != ADER_OK) return s;
+  const int nu = (int)A->cells.size();
+  std::vector<int> lv(nu), st(nu), mo(nu), ch(nu);
+  std::vector<long long> ix((size_t)nu * 3);
+  for (int l = 0; l <= A->lmax; ++l) { A->lact[l].clear(); A->lvch[l].clear(); A->lvmo[l].clear(); }
+  A->lall.clear();
+  for (int i = 0; i < nu; ++i) {
+    const HCell& C = A->cells[i];
+    lv[i] = C.level; st[i] = C.alive ? C.status : 9; mo[i] = C.mother; ch[i] = C.child;
+    for (int k = 0; k < 3; ++k) ix[(size_t)i * 3 + k] = C.idx[k];
+  }
+  // lists in (level, z, y, x) order (deterministic)
+  for (int l = 0; l <= A->lmax; ++l)
+    for (int id : A->hmap[l]) {
+      if (id < 0) continue;
+      const int s2 = A->cells[id].status;
+      if (s2 == 0) { A->lact[l].push_back(id); A->lall.push_back(id); }
+      else if (s2 == 1) A->lvch[l].push_back(id);
+      else A->lvmo[l].push_back(id);
+    }
+  cudaStream_t sm = A->k->stream;
+  AmrDevView& V = A->V;
+  ACK(cudaMemcpyAsync(V.level, lv.data(), sizeof(int) * nu, cudaMemcpyHostToDevice, sm));
+  ACK(cudaMemcpyAsync(V.status, st.data(), sizeof(int) * nu, cudaMemcpyHostToDevice, sm));
+  ACK(cudaMemcpyAsync(V.mother, mo.data(), sizeof(int) * nu, cudaMemcpyHostToDevice, sm));
+  ACK(cudaMemcpyAsync(V.child, ch.data(), sizeof(int) * nu, cudaMemcpyHostToDevice, sm));
+  ACK(cudaMemcpyAsync(V.idx, ix.data(), sizeof(long long) * 3 * nu, cudaMemcpyHostToDevice, sm));
+  for (int l = 0; l <= A->lmax; ++l)
+    ACK(cudaMemcpyAsync(A->dmap[l], A->hmap[l].data(), sizeof(int) * A->hmap[l].size(), cudaMemcpyHostToDevice, sm));
+  // concatenated lists
+  std::vector<int> all;
+  for (int l = 0; l <= A->lmax; ++l) {
+    A->oact[l] = (long long)all.size(); all.insert(all.end(), A->lact[l].begin(), A->lact[l].end());
+    A->ovch[l] = (long long)all.size(); all.insert(all.end(), A->lvch[l].begin(), A->lvch[l].end());
+    A->ovmo[l] = (long long)all.size(); all.insert(all.end(), A->lvmo[l].begin(), A->lvmo[l].end());
+  }
+  A->oall = (long long)all.size();
+  all.insert(all.end(), A->lall.begin(), A->lall.end());
+  if ((long long)all.size() > A->dlist_cap) {
+    if (A->dlist) { cudaStreamSynchronize(sm); cudaFree(A->dlist); }
+    A->dlist_cap = (long long)all.size() * 3 / 2 + 1024;
+    ACK(cudaMalloc(&A->dlist, sizeof(int) * A->dlist_cap));
+  }
+  ACK(cudaMemcpyAsync(A->dlist, all.data(), sizeof(int) * all.size(), cudaMemcpyHostToDevice, sm));
+  ACK(cudaStreamSynchronize(sm));   // host vectors go out of scope
+  return ADER_OK;
+}
+
+const int* L_act(const AmrState* A, int l) { return A->dlist + A->oact[l]; }
+const int* L_vch(const AmrState* A, int l) { return A->dlist + A->ovch[l]; }
+const int* L_vmo(const AmrState* A, int l) { return A->dlist + A->ovmo[l]; }
+
+void psi_at(const AmrState* A, double tau, double out[4]) {
+  for (int s = 0; s < 4; ++s) out[s] = s < A->N ? lagrange(A->k->tab, A->N, s, tau) : 0.0;
+}
+
+// IC cell averages of the listed cells (Q^d GL points, host callback, device sum)
+ader_status ic_cells(AmrState* A, const std::vector<int>& ids, std::string& err) {
+  if (ids.empty()) return ADER_OK;
+  const int Q = A->cfg.ic_quad, d = A->d;
+  // Gauss-Legendre rule on [0,1] from the context tables when Q == N, else closed forms
+  double qx[8], qw[8];
+  DevTables tq;
+  if (Q == 3 || Q == 4) { build_tables(Q - 1, &tq); for (int i = 0; i < Q; ++i) { qx[i] = tq.lam[i]; qw[i] = tq.w[i]; } }
+  else if (Q == 2) { const double h = std::sqrt(3.0) / 6.0; qx[0] = 0.5 - h; qx[1] = 0.5 + h; qw[0] = qw[1] = 0.5; }
+  else { qx[0] = 0.5; qw[0] = 1.0; }
+  int nq = 1;
+  for (int k = 0; k < d; ++k) nq *= Q;
+  std::vector<double> wq(nq);
+  for (int g = 0; g < nq; ++g) {
+    const int gi[3] = {g % Q, (g / Q) % Q, g / (Q * Q)};
+    double wg = 1.0;
+    for (int k = 0; k < d; ++k) wg *= qw[gi[k]];
+    wq[g] = wg;
+  }
+  const size_t nc = ids.size();
+  std::vector<double> x(nc * nq * 3), pr(nc * nq * 9, 0.0);
+  for (size_t i = 0; i < nc; ++i) {
+    const HCell& C = A->cells[ids[i]];
+    for (int g = 0; g < nq; ++g) {
+      const int gi[3] = {g % Q, (g / Q) % Q, g / (Q * Q)};
+      for (int k = 0; k < 3; ++k)
+        x[(i * nq + g) * 3 + k] = k < d ? A->cfg.lo[k] + ((double)C.idx[k] + qx[gi[k]]) * A->dx[C.level][k] : 0.0;
+    }
+  }
+  A->ic(x.data(), (int64_t)(nc * nq), pr.data(), A->user);
+  double *dpr = nullptr, *dwq = nullptr;
+  int* dids = nullptr;
+  ACK(cudaMalloc(&dpr, sizeof(double) * pr.size()));
+  ACK(cudaMalloc(&dwq, sizeof(double) * nq));
+  ACK(cudaMalloc(&dids, sizeof(int) * nc));
+  cudaStream_t sm = A->k->stream;
+  ACK(cudaMemcpyAsync(dpr, pr.data(), sizeof(double) * pr.size(), cudaMemcpyHostToDevice, sm));
+  ACK(cudaMemcpyAsync(dwq, wq.data(), sizeof(double) * nq, cudaMemcpyHostToDevice, sm));
+  ACK(cudaMemcpyAsync(dids, ids.data(), sizeof(int) * nc, cudaMemcpyHostToDevice, sm));
+  amr_launch_ic(*A->k, A->V, dids, (int)nc, dpr, dwq, nq);
+  ACK(cudaStreamSynchronize(sm));
+  cudaFree(dpr); cudaFree(dwq); cudaFree(dids);
+  return ADER_OK;
+}
+
+// apply the pending initialisations (after the topology is on the device)
+ader_status run_inits(AmrState* A, std::string& err) {
+  // keep only the last init per live cell (a cell may be re-initialised in a cascade)
+  std::vector<int> last(A->cells.size(), -1);
+  for (size_t i = 0; i < A->inits.size(); ++i)
+    if (A->inits[i].cell < (int)A->cells.size()) last[A->inits[i].cell] = (int)i;
+  std::vector<int> pw, pp, ic;
+  for (size_t i = 0; i < A->inits.size(); ++i) {
+    const Init& z = A->inits[i];
+    if (last[z.cell] != (int)i || !A->cells[z.cell].alive) continue;
+    if (z.mode == 0) { pw.push_back(z.cell); pw.push_back(z.mother); }
+    else if (z.mode == 1) { pp.push_back(z.cell); pp.push_back(z.mother); }
+    else ic.push_back(z.cell);
+  }
+  A->inits.clear();
+  cudaStream_t sm = A->k->stream;
+  int* dp = nullptr;
+  const size_t tot = pw.size() + pp.size();
+  if (tot) {
+    ACK(cudaMalloc(&dp, sizeof(int) * tot));
+    if (!pw.empty()) ACK(cudaMemcpyAsync(dp, pw.data(), sizeof(int) * pw.size(), cudaMemcpyHostToDevice, sm));
+    if (!pp.empty()) ACK(cudaMemcpyAsync(dp + pw.size(), pp.data(), sizeof(int) * pp.size(), cudaMemcpyHostToDevice, sm));
+    amr_launch_init_from_weno(*A->k, A->V, A->st, dp, (int)(pw.size() / 2));
+    double pt[4];
+    psi_at(A, 1.0, pt);
+    amr_launch_init_from_pred(*A->k, A->V, A->st, dp + pw.size(), (int)(pp.size() / 2), pt);
+    ACK(cudaStreamSynchronize(sm));
+    cudaFree(dp);
+  }
+  std::sort(ic.begin(), ic.end());
+  return ic_cells(A, ic, err);
+}
+
+ader_status fetch_speed(AmrState* A, double* speed, std::string& err) {
+  cudaStream_t sm = A->k->stream;
+  ACK(cudaMemsetAsync(&A->cnt->speed_bits, 0, sizeof(unsigned long long), sm));
+  double inv[3] = {0, 0, 0};
+  for (int k = 0; k < A->d; ++k) inv[k] = 1.0 / A->dx[0][k];
+  amr_launch_cfl(*A->k, A->V, A->dlist + A->oall, (int)A->lall.size(), inv, A->cnt);
+  ACK(cudaMemcpyAsync(A->hcnt, A->cnt, sizeof(DevCounters), cudaMemcpyDeviceToHost, sm));
+  ACK(cudaStreamSynchronize(sm));
+  unsigned long long b = A->hcnt->speed_bits;
+  std::memcpy(speed, &b, sizeof(double));
+  return ADER_OK;
+}
+
+ader_status check_err(AmrState* A, std::string& err) {
+  cudaStream_t sm = A->k->stream;
+  ACK(cudaMemcpyAsync(A->hcnt, A->cnt, sizeof(DevCounters), cudaMemcpyDeviceToHost, sm));
+  ACK(cudaStreamSynchronize(sm));
+  if (A->hcnt->err_code) {
+    const long long id = (long long)A->hcnt->err_cell;
+    char b[512];
+    const HCell& C = A->cells[(size_t)id < A->cells.size() ? id : 0];
+    snprintf(b, sizeof(b), "%s at level %d cell (%lld,%lld,%lld), t=%.17g",
+             A->hcnt->err_code == 1 ? "inadmissible state (rho<=0 or p<=0)" : "predictor reached pred_max_sweeps",
+             C.level, C.idx[0], C.idx[1], C.idx[2], A->t);
+    err = b;
+    return ADER_ERR_SOLVER;
+  }
+  return ADER_OK;
+}
+
+// ---- local time stepping (recursive form of eqn.update.criterion, R15) -------
+void advance(AmrState* A, int l, int m, double dt0) {
+  double dt = dt0;
+  for (int k = 0; k < l; ++k) dt /= A->r;
+  double dtdx[3] = {0, 0, 0};
+  for (int k = 0; k < A->d; ++k) dtdx[k] = dt / A->dx[l][k];
+  // ghost refresh (R16): averaging of virtual mothers on levels >= l, finest first
+  for (int lv = A->lmax - 1; lv >= l; --lv) amr_launch_average(*A->k, A->V, L_vmo(A, lv), (int)A->lvmo[lv].size());
+  if (l >= 1) {
+    double pt[4];
+    psi_at(A, (double)m / A->r, pt);
+    amr_launch_project(*A->k, A->V, A->st, L_vch(A, l), (int)A->lvch[l].size(), pt);
+  }
+  const int na = (int)A->lact[l].size();
+  amr_launch_weno(*A->k, A->V, L_act(A, l), na);
+  amr_launch_predictor(*A->k, A->V, L_act(A, l), na, dtdx, A->cfg.pred_tol, A->cfg.pred_max_sweeps, A->cnt);
+  if (l < A->lmax && (A->lact[l + 1].size() + A->lvch[l + 1].size() + A->lvmo[l + 1].size()) > 0)
+    for (int k = 0; k < A->r; ++k) advance(A, l + 1, k, dt0);
+  amr_launch_flux_update(*A->k, A->V, A->st, L_act(A, l), na, m, dtdx, A->cnt);
+  A->updates[l] += na;
+}
+
+// ---- adapt (rules 1-7) --------------------------------------------------------
+ader_status adapt(AmrState* A, bool t0, std::string& err) {
+  cudaStream_t sm = A->k->stream;
+  int nb[26];
+  if (!t0) {
+    // ghost refresh at t^{n+1}: averages (finest first), projections at tau = 1
+    for (int lv = A->lmax - 1; lv >= 0; --lv) amr_launch_average(*A->k, A->V, L_vmo(A, lv), (int)A->lvmo[lv].size());
+    double pt[4];
+    psi_at(A, 1.0, pt);
+    for (int l = 1; l <= A->lmax; ++l) amr_launch_project(*A->k, A->V, A->st, L_vch(A, l), (int)A->lvch[l].size(), pt);
+  }
+  // indicator on all active cells (device), WENO polynomials of all active cells (R18)
+  const int na = (int)A->lall.size();
+  amr_launch_indicator(*A->k, A->V, A->dlist + A->oall, na, A->cfg.chi_eps);
+  if (!t0)
+    for (int l = 0; l <= A->lmax; ++l) amr_launch_weno(*A->k, A->V, L_act(A, l), (int)A->lact[l].size());
+  std::vector<double> chi(A->cells.size(), 0.0);
+  ACK(cudaMemcpyAsync(chi.data(), A->V.chi, sizeof(double) * A->cells.size(), cudaMemcpyDeviceToHost, sm));
+  ACK(cudaStreamSynchronize(sm));
+  for (auto& c : A->cells) c.isnew = false;
+  const int nu = (int)A->cells.size();
+  std::vector<char> mark(nu, 0);
+  for (int i = 0; i < nu; ++i)
+    mark[i] = A->cells[i].alive && A->cells[i].status == 0 && A->cells[i].level < A->lmax && chi[i] > A->cfg.chi_ref;
+  for (int i = 0; i < nu; ++i)
+    if (mark[i]) refine_cell(A, i, t0);
+  closure(A, t0);
+  std::vector<int> freed;
+  std::vector<int> coarsened;
+  if (!t0) {
+    const int nu2 = (int)A->cells.size();
+    std::vector<char> cand(nu2, 0);
+    for (int i = 0; i < nu2; ++i) {
+      const HCell& C = A->cells[i];
+      if (!C.alive || C.status != -1) continue;
+      bool ok = true;
+      for (int q = 0; q < A->rd && ok; ++q) {
+        const int kid = C.child + q;
+        const HCell& K = A->cells[kid];
+        if (K.status != 0 || K.child >= 0 || K.isnew || !(kid < nu && chi[kid] < A->cfg.chi_rec) || (kid < nu && mark[kid]))
+          ok = false;
+      }
+      cand[i] = ok;
+    }
+    for (;;) {
+      // tentative simultaneous rule 7, then closure; reverted candidates retry
+      const std::vector<HCell> snap_cells = A->cells;
+      const std::vector<std::vector<int>> snap_map = A->hmap;
+      const std::vector<int> snap_free = A->free_blocks;
+      const size_t snap_inits = A->inits.size();
+      std::vector<char> destroy(nu2, 0);
+      for (int i = 0; i < nu2; ++i) {
+        if (!cand[i]) continue;
+        const int k = voronoi(A, i, nb);
+        bool busy = false;
+        for (int j = 0; j < k && !busy; ++j) busy = nb[j] >= 0 && A->cells[nb[j]].status == -1;
+        destroy[i] = !busy;
+      }
+      std::vector<int> fr;
+      for (int i = 0; i < nu2; ++i) {
+        if (!cand[i]) continue;
+        if (destroy[i]) destroy_children(A, i, &fr);
+        else
+          for (int q = 0; q < A->rd; ++q) A->cells[A->cells[i].child + q].status = 1;
+        A->cells[i].status = 0;
+      }
+      closure(A, false);
+      bool reverted = false;
+      for (int i = 0; i < nu2; ++i)
+        if (cand[i] && A->cells[i].status == -1) { cand[i] = 0; reverted = true; }
+      if (!reverted) {
+        freed.insert(freed.end(), fr.begin(), fr.end());
+        for (int i = 0; i < nu2; ++i)
+          if (cand[i]) coarsened.push_back(i);
+        break;
+      }
+      A->cells = snap_cells;
+      A->hmap = snap_map;
+      A->free_blocks = snap_free;
+      A->inits.resize(snap_inits);
+    }
+  }
+  garbage_collect(A, &freed);
+  // device: averages of coarsened mothers from their (old) children first
+  if (!coarsened.empty()) {
+    // children ids are still valid on the device (freed blocks are reused only later)
+    int* dl = nullptr;
+    ACK(cudaMalloc(&dl, sizeof(int) * coarsened.size()));
+    ACK(cudaMemcpyAsync(dl, coarsened.data(), sizeof(int) * coarsened.size(), cudaMemcpyHostToDevice, sm));
+    // the device child links of these mothers are the pre-adapt ones
+    amr_launch_average(*A->k, A->V, dl, (int)coarsened.size());
+    ACK(cudaStreamSynchronize(sm));
+    cudaFree(dl);
+  }
+  ader_status s = upload_topology(A, err);
+  if (s != ADER_OK) return s;
+  s = run_inits(A, err);
+  if (s != ADER_OK) return s;
+  // clear the flux memory of every virtual child (synchronized time: all consumed)
+  for (int l = 1; l <= A->lmax; ++l)
+    for (int id : A->lvch[l]) ACK(cudaMemsetAsync(A->V.mem + (size_t)id * 6 * A->nv, 0, sizeof(double) * 6 * A->nv, sm));
+  for (int b : freed) A->free_blocks.push_back(b);
+  for (auto& c : A->cells) c.isnew = false;
+  ACK(cudaStreamSynchronize(sm));
+  return ADER_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+AmrState* amr_create(const ader_config* cfg, KCtx* k, DevCounters* cnt, DevCounters* hcnt, std::string& err) {
+  AmrState* A = new AmrState();
+  A->cfg = *cfg;
+  A->k = k; A->cnt = cnt; A->hcnt = hcnt;
+  A->d = cfg->dim; A->M = cfg->degree; A->N = A->M + 1;
+  A->nv = cfg->system == ADER_MHD_GLM ? 9 : cfg->dim + 2;
+  A->NS = 1;
+  for (int i = 0; i < A->d; ++i) A->NS *= A->N;
+  A->NST = A->NS * A->N;
+  A->r = cfg->refine_factor; A->lmax = cfg->lmax;
+  A->rd = 1;
+  for (int i = 0; i < A->d; ++i) A->rd *= A->r;
+  if (A->cfg.ic_quad <= 0) A->cfg.ic_quad = A->N;
+  if (A->cfg.pred_tol <= 0) A->cfg.pred_tol = 1e-13;
+  if (A->cfg.pred_max_sweeps <= 0) A->cfg.pred_max_sweeps = 32;
+  build_sub(k->tab, A->N, A->r, &A->st);
+  A->hmap.resize(A->lmax + 1);
+  for (int l = 0; l <= A->lmax; ++l) {
+    long long s = 1, f = 1;
+    for (int q = 0; q < l; ++q) f *= A->r;
+    for (int i = 0; i < 3; ++i) {
+      A->n[l][i] = i < A->d ? cfg->n0[i] * f : 1;
+      A->dx[l][i] = i < A->d ? (cfg->hi[i] - cfg->lo[i]) / (double)A->n[l][i] : 1.0;
+      s *= A->n[l][i];
+    }
+    A->hmap[l].assign((size_t)s, -1);
+    if (cudaMalloc(&A->dmap[l], sizeof(int) * s) != cudaSuccess) { err = "cudaMalloc map"; delete A; return nullptr; }
+    A->V.map[l] = A->dmap[l];
+    for (int i = 0; i < 3; ++i) A->V.n[l][i] = A->n[l][i];
+  }
+  for (int i = 0; i < 6; ++i) A->V.bc[i] = cfg->bc[i];
+  A->V.D = A->d; A->V.NV = A->nv; A->V.r = A->r; A->V.rd = A->rd;
+  const long long n0 = A->n[0][0] * A->n[0][1] * A->n[0][2];
+  A->cells.resize(n0);
+  for (long long i = 0; i < n0; ++i) {
+    HCell& C = A->cells[i];
+    C.alive = true;
+    C.idx[0] = i % A->n[0][0]; C.idx[1] = (i / A->n[0][0]) % A->n[0][1]; C.idx[2] = i / (A->n[0][0] * A->n[0][1]);
+    A->hmap[0][i] = (int)i;
+  }
+  if (upload_topology(A, err) != ADER_OK) { amr_destroy(A); return nullptr; }
+  return A;
+}
+
+void amr_destroy(AmrState* A) {
+  if (!A) return;
+  cudaStreamSynchronize(A->k->stream);
+  void* ps[] = {A->V.u, A->V.mem, A->V.w, A->V.q, A->V.chi, A->V.level, A->V.status, A->V.mother, A->V.child, A->V.idx,
+                A->dlist};
+  for (void* p : ps)
+    if (p) cudaFree(p);
+  for (int l = 0; l < kAmrMaxLevels; ++l)
+    if (A->dmap[l]) cudaFree(A->dmap[l]);
+  delete A;
+}
+
+double amr_time(const AmrState* A) { return A->t; }
+
+int64_t amr_num_active(const AmrState* A) { return (int64_t)A->lall.size(); }
+
+ader_status amr_set_initial(AmrState* A, ader_ic_fn ic, void* user, std::string& err) {
+  A->ic = ic; A->user = user;
+  std::vector<int> ids;
+  for (int i = 0; i < (int)A->cells.size(); ++i)
+    if (A->cells[i].alive) ids.push_back(i);
+  ader_status s = ic_cells(A, ids, err);
+  if (s != ADER_OK) return s;
+  for (int l = 0; l < A->lmax; ++l) {     // initial hierarchy (R20)
+    s = adapt(A, true, err);
+    if (s != ADER_OK) return s;
+  }
+  A->t = 0.0;
+  return ADER_OK;
+}
+
+ader_status amr_adapt(AmrState* A, std::string& err) { return adapt(A, false, err); }
+
+ader_status amr_step(AmrState* A, double t_end, int64_t max_steps, ader_step_report* rep, std::string& err) {
+  ader_step_report R;
+  std::memset(&R, 0, sizeof(R));
+  for (int l = 0; l < kAmrMaxLevels; ++l) A->updates[l] = 0;
+  ader_status s = ADER_OK;
+  cudaStream_t sm = A->k->stream;
+  ACK(cudaMemcpyAsync(A->hcnt, A->cnt, sizeof(DevCounters), cudaMemcpyDeviceToHost, sm));
+  ACK(cudaStreamSynchronize(sm));
+  const unsigned long long sw0 = A->hcnt->sweeps, pc0 = A->hcnt->cells;
+  while (R.macro_steps < max_steps && A->t < t_end) {
+    double speed = 0.0;
+    s = fetch_speed(A, &speed, err);
+    if (s != ADER_OK) break;
+    s = check_err(A, err);
+    if (s != ADER_OK) break;
+    double dt = A->cfg.cfl / speed;
+    if (!(dt > 0.0) || !std::isfinite(dt)) { err = "invalid dt"; s = ADER_ERR_SOLVER; break; }
+    if (A->t + dt > t_end) dt = t_end - A->t;
+    advance(A, 0, 0, dt);
+    s = check_err(A, err);
+    if (s != ADER_OK) break;
+    A->t += dt;
+    R.dt0 = dt;
+    R.macro_steps++;
+    if (A->cfg.adapt_every > 0 && R.macro_steps % A->cfg.adapt_every == 0) {
+      s = adapt(A, false, err);
+      if (s != ADER_OK) break;
+    }
+  }
+  ACK(cudaMemcpyAsync(A->hcnt, A->cnt, sizeof(DevCounters), cudaMemcpyDeviceToHost, sm));
+  ACK(cudaStreamSynchronize(sm));
+  R.t = A->t;
+  for (int l = 0; l < kAmrMaxLevels && l <= A->lmax; ++l) { R.updates_per_level[l] = A->updates[l]; R.cell_updates += A->updates[l]; }
+  R.pred_sweeps_total = (int64_t)(A->hcnt->sweeps - sw0);
+  R.pred_cells = (int64_t)(A->hcnt->cells - pc0);
+  R.pred_sweeps_max = A->hcnt->sweeps_max;
+  if (rep) *rep = R;
+  return s;
+}
+
+ader_status amr_get_cells(AmrState* A, ader_cell* out, int64_t cap, int64_t* n, std::string& err) {
+  int64_t cnt = 0;
+  for (int l = 0; l <= A->lmax; ++l)
+    for (int id : A->hmap[l]) cnt += id >= 0;
+  *n = cnt;
+  if (!out) return ADER_OK;
+  if (cap < cnt) { err = "capacity too small"; return ADER_ERR_ARG; }
+  std::vector<double> u(A->cells.size() * A->nv);
+  ACK(cudaMemcpyAsync(u.data(), A->V.u, sizeof(double) * u.size(), cudaMemcpyDeviceToHost, A->k->stream));
+  ACK(cudaStreamSynchronize(A->k->stream));
+  int64_t i = 0;
+  for (int l = 0; l <= A->lmax; ++l)
+    for (int id : A->hmap[l]) {
+      if (id < 0) continue;
+      ader_cell& e = out[i++];
+      std::memset(&e, 0, sizeof(e));
+      const HCell& C = A->cells[id];
+      e.level = C.level; e.status = C.status;
+      for (int k = 0; k < 3; ++k) e.idx[k] = C.idx[k];
+      for (int v = 0; v < A->nv; ++v) e.u[v] = u[(size_t)id * A->nv + v];
+    }
+  return ADER_OK;
+}
+
+}  // namespace ader

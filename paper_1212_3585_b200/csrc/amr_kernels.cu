@@ -1,0 +1,541 @@
+// amr_kernels.cu — sm_100a kernels of the AMR / local-time-stepping path.
+//   k_amr_average   averaging of virtual mothers (eqn.average @ P:743-753)
+//   k_amr_project   projection of the mother's q_h into virtual children
+//   k_amr_weno      dimension-by-dimension WENO of a listed active cell
+//   k_predictor     (kernels.cu, list mode) space-time predictor
+//   k_amr_flux_update  face fluxes incl. coarse-fine faces with flux memory
+//                   (eqn.memory.sum) + one-step update (eq:finite_vol)
+//   k_amr_indicator refinement indicator, reading R14 of eqn.indicator,
+//                   evaluated without FMA contraction (bit-exact flags, H2)
+// Citations: P:n = PAPER.md line n.
+#include <cuda_runtime.h>
+
+#include "amr.h"
+#include "device.cuh"
+
+namespace ader {
+
+constexpr int ipow_a(int b, int e) { return e == 0 ? 1 : b * ipow_a(b, e - 1); }
+
+__device__ __forceinline__ int amr_lookup(const AmrDevView& V, int l, long long x, long long y, long long z) {
+  long long c[3] = {x, y, z};
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    if (k >= V.D) { c[k] = 0; continue; }
+    const long long n = V.n[l][k];
+    if (c[k] < 0 || c[k] >= n) {
+      const int side = c[k] < 0 ? 0 : 1;
+      if (V.bc[2 * k + side] == ADER_BC_PERIODIC) c[k] = ((c[k] % n) + n) % n;
+      else c[k] = c[k] < 0 ? 0 : n - 1;
+    }
+  }
+  return V.map[l][(c[2] * V.n[l][1] + c[1]) * V.n[l][0] + c[0]];
+}
+
+__device__ __forceinline__ void amr_error(DevCounters* c, int code, int stage, long long cell) {
+  if (atomicCAS(&c->err_code, 0, code) == 0) {
+    c->err_stage = stage;
+    c->err_cell = (unsigned long long)cell;
+  }
+}
+
+// ---------------------------------------------------------------------------
+__global__ void k_amr_average(AmrDevView V, const int* __restrict__ list, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n * V.NV) return;
+  const int m = list[i / V.NV], v = i % V.NV;
+  const int ch = V.child[m];
+  double s = 0.0;
+  for (int q = 0; q < V.rd; ++q) s += V.u[(long long)(ch + q) * V.NV + v];
+  V.u[(long long)m * V.NV + v] = s / (double)V.rd;
+}
+
+// sub-box average of the mother's polynomial (mode 0: WENO w, 1: q_h at tau)
+template <int D, int M>
+__device__ __forceinline__ double subbox(const AmrDevView& V, const SubTables& S, int cell, int mom, int v, int mode,
+                                         const double* psi_tau) {
+  constexpr int N = M + 1, NS = ipow_a(N, D), NST = NS * N;
+  int off[3] = {0, 0, 0};
+#pragma unroll
+  for (int k = 0; k < D; ++k) off[k] = (int)(V.idx[(long long)cell * 3 + k] - V.idx[(long long)mom * 3 + k] * V.r);
+  double acc = 0.0;
+  if (mode == 0) {
+    const double* w = V.w + ((long long)mom * V.NV + v) * NS;
+#pragma unroll
+    for (int p = 0; p < NS; ++p) {
+      double c = S.Psub[off[0]][p % N] * S.Psub[off[1]][(p / N) % N];
+      if (D == 3) c *= S.Psub[off[2]][p / (N * N)];
+      acc += c * w[p];
+    }
+  } else {
+    const double* q = V.q + ((long long)mom * V.NV + v) * NST;
+    for (int p = 0; p < NST; ++p) {
+      const int sp = p % NS, s = p / NS;
+      double c = S.Psub[off[0]][sp % N] * S.Psub[off[1]][(sp / N) % N];
+      if (D == 3) c *= S.Psub[off[2]][sp / (N * N)];
+      acc += (c * psi_tau[s]) * q[p];
+    }
+  }
+  return acc;
+}
+
+template <int D, int M>
+__global__ void k_amr_project(AmrDevView V, const __grid_constant__ SubTables S, const int* __restrict__ list, int n,
+                              double t0, double t1, double t2, double t3) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n * V.NV) return;
+  const int c = list[i / V.NV], v = i % V.NV;
+  const double psi_tau[4] = {t0, t1, t2, t3};
+  V.u[(long long)c * V.NV + v] = subbox<D, M>(V, S, c, V.mother[c], v, 1, psi_tau);
+}
+
+template <int D, int M>
+__global__ void k_amr_init_pairs(AmrDevView V, const __grid_constant__ SubTables S, const int* __restrict__ pairs,
+                                 int n, int mode, double t0, double t1, double t2, double t3) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n * V.NV) return;
+  const int k = i / V.NV, v = i % V.NV;
+  const int c = pairs[2 * k], m = pairs[2 * k + 1];
+  const double psi_tau[4] = {t0, t1, t2, t3};
+  V.u[(long long)c * V.NV + v] = subbox<D, M>(V, S, c, m, v, mode, psi_tau);
+}
+
+// ---------------------------------------------------------------------------
+// WENO of a listed active cell from its (2M+1)^D box, thread per (cell, var)
+template <int D, int M, int NV>
+__global__ void __launch_bounds__(128) k_amr_weno(AmrDevView V, const int* __restrict__ list, int n,
+                                                  const __grid_constant__ DevTables T) {
+  constexpr int N = M + 1, W = 2 * M + 1, NS = ipow_a(N, D);
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n * NV) return;
+  const int c = list[i / NV], v = i % NV;
+  const int l = V.level[c];
+  const long long x0 = V.idx[(long long)c * 3], y0 = V.idx[(long long)c * 3 + 1], z0 = V.idx[(long long)c * 3 + 2];
+  double* wo = V.w + ((long long)c * NV + v) * NS;
+  if (D == 2) {
+    double wx[W][N];
+    for (int jy = 0; jy < W; ++jy) {
+      double win[W];
+#pragma unroll
+      for (int o = 0; o < W; ++o) win[o] = V.u[(long long)amr_lookup(V, l, x0 + o - M, y0 + jy - M, 0) * NV + v];
+      double out[N];
+      weno1d<M>(T, win, out);
+#pragma unroll
+      for (int a = 0; a < N; ++a) wx[jy][a] = out[a];
+    }
+#pragma unroll
+    for (int a = 0; a < N; ++a) {
+      double win[W], out[N];
+#pragma unroll
+      for (int j = 0; j < W; ++j) win[j] = wx[j][a];
+      weno1d<M>(T, win, out);
+#pragma unroll
+      for (int b = 0; b < N; ++b) wo[a + N * b] = out[b];
+    }
+  } else {
+    double wxy[W][N][N];
+    for (int jz = 0; jz < W; ++jz) {
+      double wx[W][N];
+      for (int jy = 0; jy < W; ++jy) {
+        double win[W], out[N];
+#pragma unroll
+        for (int o = 0; o < W; ++o)
+          win[o] = V.u[(long long)amr_lookup(V, l, x0 + o - M, y0 + jy - M, z0 + jz - M) * NV + v];
+        weno1d<M>(T, win, out);
+#pragma unroll
+        for (int a = 0; a < N; ++a) wx[jy][a] = out[a];
+      }
+#pragma unroll
+      for (int a = 0; a < N; ++a) {
+        double win[W], out[N];
+#pragma unroll
+        for (int j = 0; j < W; ++j) win[j] = wx[j][a];
+        weno1d<M>(T, win, out);
+#pragma unroll
+        for (int b = 0; b < N; ++b) wxy[jz][a][b] = out[b];
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < N; ++a)
+#pragma unroll
+      for (int b = 0; b < N; ++b) {
+        double win[W], out[N];
+#pragma unroll
+        for (int k = 0; k < W; ++k) win[k] = wxy[k][a][b];
+        weno1d<M>(T, win, out);
+#pragma unroll
+        for (int cc = 0; cc < N; ++cc) wo[a + N * b + N * N * cc] = out[cc];
+      }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// face flux / update.  Trace of a same-level cell X on its face (DIR, at_one)
+// at tangential nodes (t1, t2) and time node s; coarse trace of K at the fine
+// face points via the sub-interval tables.
+template <int D, int M, int NV, int DIR>
+__device__ __forceinline__ void trace_full(const double* __restrict__ qX, bool at_one, int t1, int t2, int s,
+                                           const DevTables& T, double (&out)[NV]) {
+  constexpr int N = M + 1, NS = ipow_a(N, D), NST = NS * N;
+  constexpr int ax0 = (DIR == 0) ? 1 : 0, ax1 = (DIR == 2) ? 1 : 2;
+  const int base = s * NS + t1 * ipow_a(N, ax0) + (D == 3 ? t2 * ipow_a(N, ax1) : 0);
+  constexpr int sn = ipow_a(N, DIR);
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    double a = 0.0;
+#pragma unroll
+    for (int k = 0; k < N; ++k) a += (at_one ? T.psi1[k] : T.psi0[k]) * qX[v * NST + base + k * sn];
+    out[v] = a;
+  }
+}
+
+template <int D, int M, int NV, int DIR>
+__device__ __forceinline__ void trace_coarse(const double* __restrict__ qK, bool at_one, int o1, int o2, int m, int t1,
+                                             int t2, int s, const DevTables& T, const SubTables& S,
+                                             double (&out)[NV]) {
+  constexpr int N = M + 1, NS = ipow_a(N, D), NST = NS * N;
+  constexpr int ax0 = (DIR == 0) ? 1 : 0, ax1 = (DIR == 2) ? 1 : 2;
+  for (int v = 0; v < NV; ++v) out[v] = 0.0;
+  for (int p = 0; p < NST; ++p) {
+    int e[4];
+    e[0] = p % N; e[1] = (p / N) % N; e[2] = (D == 3) ? (p / (N * N)) % N : 0;
+    const int et = p / NS;
+    double th = (at_one ? T.psi1[e[DIR]] : T.psi0[e[DIR]]) * S.Esub[o1][t1][e[ax0]];
+    if (D == 3) th *= S.Esub[o2][t2][e[ax1]];
+    th *= S.Esub[m][s][et];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) out[v] += th * qK[v * NST + p];
+  }
+}
+
+template <int SYS, int D, int DIR>
+__device__ __forceinline__ bool rusanov_pt(const double (&um)[Phys<SYS, D>::NV], const double (&up)[Phys<SYS, D>::NV],
+                                           double gamma, double ch, double (&f)[Phys<SYS, D>::NV]) {
+  using PH = Phys<SYS, D>;
+  constexpr int NV = PH::NV;
+  double fL[NV], fR[NV], sL, sR;
+  bool ok = PH::template flux_speed<DIR>(um, gamma, ch, fL, sL);
+  ok &= PH::template flux_speed<DIR>(up, gamma, ch, fR, sR);
+  const double smax = fmax(sL, sR);
+#pragma unroll
+  for (int v = 0; v < NV; ++v) f[v] = 0.5 * (fL[v] + fR[v]) - 0.5 * smax * (up[v] - um[v]);
+  return ok;
+}
+
+// kind: 0 same level (qL, qR full faces), 1 left boundary (qR only), 2 right
+// boundary (qL only), 3 coarse left (qL = K), 4 coarse right (qR = K)
+template <int D, int M, int SYS, int DIR>
+__device__ bool face_flux_amr(int kind, const double* qL, const double* qR, int o1, int o2, int m, double gamma,
+                              double ch, const DevTables& T, const SubTables& S, double (&F)[Phys<SYS, D>::NV]) {
+  constexpr int NV = Phys<SYS, D>::NV, N = M + 1;
+  constexpr int NT = (D == 3) ? N * N : N;
+  bool ok = true;
+#pragma unroll
+  for (int v = 0; v < NV; ++v) F[v] = 0.0;
+  for (int s = 0; s < N; ++s)
+    for (int t = 0; t < NT; ++t) {
+      const int t1 = t % N, t2 = t / N;
+      double um[NV], up[NV], ft[NV];
+      if (kind == 0 || kind == 2 || kind == 4) trace_full<D, M, NV, DIR>(qL, true, t1, t2, s, T, um);
+      if (kind == 0 || kind == 1 || kind == 3) trace_full<D, M, NV, DIR>(qR, false, t1, t2, s, T, up);
+      if (kind == 3) trace_coarse<D, M, NV, DIR>(qL, true, o1, o2, m, t1, t2, s, T, S, um);
+      if (kind == 4) trace_coarse<D, M, NV, DIR>(qR, false, o1, o2, m, t1, t2, s, T, S, up);
+      if (kind == 1) for (int v = 0; v < NV; ++v) um[v] = up[v];
+      if (kind == 2) for (int v = 0; v < NV; ++v) up[v] = um[v];
+      ok &= rusanov_pt<SYS, D, DIR>(um, up, gamma, ch, ft);
+      double wgt = T.w[s] * T.w[t1];
+      if (D == 3) wgt *= T.w[t2];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) F[v] += wgt * ft[v];
+    }
+  return ok;
+}
+
+template <int D, int M, int SYS, int DIR>
+__device__ bool cell_face(const AmrDevView& V, int c, int side, int m, double gamma, double ch, const DevTables& T,
+                          const SubTables& S, double (&F)[Phys<SYS, D>::NV]) {
+  constexpr int NV = Phys<SYS, D>::NV, N = M + 1, NS = ipow_a(N, D), NST = NS * N;
+  const int l = V.level[c];
+  long long ix[3] = {V.idx[(long long)c * 3], V.idx[(long long)c * 3 + 1], V.idx[(long long)c * 3 + 2]};
+  ix[DIR] += side ? 1 : -1;
+  const double* qc = V.q + (long long)c * NV * NST;
+  const bool out = ix[DIR] < 0 || ix[DIR] >= V.n[l][DIR];
+  if (out && V.bc[2 * DIR + side] == ADER_BC_TRANSMISSIVE)
+    return face_flux_amr<D, M, SYS, DIR>(side ? 2 : 1, qc, qc, 0, 0, 0, gamma, ch, T, S, F);
+  const int nb = amr_lookup(V, l, ix[0], ix[1], ix[2]);
+  if (nb < 0) return false;
+  const int st = V.status[nb];
+  if (st == 0) {
+    const double* qn = V.q + (long long)nb * NV * NST;
+    return side ? face_flux_amr<D, M, SYS, DIR>(0, qc, qn, 0, 0, 0, gamma, ch, T, S, F)
+                : face_flux_amr<D, M, SYS, DIR>(0, qn, qc, 0, 0, 0, gamma, ch, T, S, F);
+  }
+  if (st == 1) {
+    // coarse-fine: the virtual neighbour scales its mother's q_h down
+    const int K = V.mother[nb];
+    const double* qK = V.q + (long long)K * NV * NST;
+    constexpr int ax0 = (DIR == 0) ? 1 : 0, ax1 = (DIR == 2) ? 1 : 2;
+    const int o1 = (int)(V.idx[(long long)c * 3 + ax0] % V.r);
+    const int o2 = (D == 3) ? (int)(V.idx[(long long)c * 3 + ax1] % V.r) : 0;
+    bool ok = side ? face_flux_amr<D, M, SYS, DIR>(4, qc, qK, o1, o2, m, gamma, ch, T, S, F)
+                   : face_flux_amr<D, M, SYS, DIR>(3, qK, qc, o1, o2, m, gamma, ch, T, S, F);
+    double* mm = V.mem + ((long long)nb * 6 + 2 * DIR + (side ? 0 : 1)) * NV;   // nb's face toward c
+#pragma unroll
+    for (int v = 0; v < NV; ++v) mm[v] += F[v];
+    return ok;
+  }
+  // virtual mother: sum the memory of our own virtual children on this face (eqn.memory.sum)
+  const int ch0 = V.child[c];
+  if (ch0 < 0) return false;
+#pragma unroll
+  for (int v = 0; v < NV; ++v) F[v] = 0.0;
+  for (int qd = 0; qd < V.rd; ++qd) {
+    const int off[3] = {qd % V.r, (qd / V.r) % V.r, qd / (V.r * V.r)};
+    if (off[DIR] != (side ? V.r - 1 : 0)) continue;
+    double* mm = V.mem + ((long long)(ch0 + qd) * 6 + 2 * DIR + side) * NV;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) { F[v] += mm[v]; mm[v] = 0.0; }
+  }
+#pragma unroll
+  for (int v = 0; v < NV; ++v) F[v] = F[v] / (double)V.rd;
+  return true;
+}
+
+template <int D, int M, int SYS>
+__global__ void __launch_bounds__(64) k_amr_flux_update(AmrDevView V, const __grid_constant__ SubTables S,
+                                                        const int* __restrict__ list, int n, int m, double dtdx0,
+                                                        double dtdx1, double dtdx2, double gamma, double ch,
+                                                        DevCounters* cnt, const __grid_constant__ DevTables T) {
+  constexpr int NV = Phys<SYS, D>::NV;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int c = list[i];
+  const double dtdx[3] = {dtdx0, dtdx1, dtdx2};
+  double uu[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) uu[v] = V.u[(long long)c * NV + v];
+  bool ok = true;
+  double Fm[NV], Fp[NV];
+  ok &= cell_face<D, M, SYS, 0>(V, c, 0, m, gamma, ch, T, S, Fm);
+  ok &= cell_face<D, M, SYS, 0>(V, c, 1, m, gamma, ch, T, S, Fp);
+#pragma unroll
+  for (int v = 0; v < NV; ++v) uu[v] = uu[v] - dtdx[0] * (Fp[v] - Fm[v]);
+  ok &= cell_face<D, M, SYS, 1>(V, c, 0, m, gamma, ch, T, S, Fm);
+  ok &= cell_face<D, M, SYS, 1>(V, c, 1, m, gamma, ch, T, S, Fp);
+#pragma unroll
+  for (int v = 0; v < NV; ++v) uu[v] = uu[v] - dtdx[1] * (Fp[v] - Fm[v]);
+  if (D == 3) {
+    ok &= cell_face<D, M, SYS, 2>(V, c, 0, m, gamma, ch, T, S, Fm);
+    ok &= cell_face<D, M, SYS, 2>(V, c, 1, m, gamma, ch, T, S, Fp);
+#pragma unroll
+    for (int v = 0; v < NV; ++v) uu[v] = uu[v] - dtdx[2] * (Fp[v] - Fm[v]);
+  }
+  if (!ok) amr_error(cnt, 1, 2, c);
+#pragma unroll
+  for (int v = 0; v < NV; ++v) V.u[(long long)c * NV + v] = uu[v];
+}
+
+// ---------------------------------------------------------------------------
+template <int D, int SYS>
+__global__ void __launch_bounds__(256) k_amr_cfl(AmrDevView V, const int* __restrict__ list, int n, double i0,
+                                                 double i1, double i2, double gamma, double ch,
+                                                 DevCounters* __restrict__ cnt) {
+  using PH = Phys<SYS, D>;
+  constexpr int NV = PH::NV;
+  __shared__ double sm[32];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  double s = 0.0;
+  if (i < n) {
+    const int c = list[i];
+    double uu[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) uu[v] = V.u[(long long)c * NV + v];
+    const double inv[3] = {i0, i1, i2};
+    if (!PH::cfl_speed(uu, gamma, ch, inv, s)) amr_error(cnt, 1, 4, c);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s = fmax(s, __shfl_xor_sync(0xffffffffu, s, o));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) sm[warp] = s;
+  __syncthreads();
+  if (warp == 0) {
+    s = (lane < (int)(blockDim.x >> 5)) ? sm[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s = fmax(s, __shfl_xor_sync(0xffffffffu, s, o));
+    if (lane == 0) atomicMax(&cnt->speed_bits, (unsigned long long)__double_as_longlong(s));
+  }
+}
+
+// indicator, reading R14: every operation explicitly rounded (no FMA), in the
+// oracle's order, so that chi and the refinement flags are bit-identical
+__global__ void k_amr_indicator(AmrDevView V, const int* __restrict__ list, int n, double eps) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int c = list[i];
+  const int l = V.level[c];
+  const long long x0 = V.idx[(long long)c * 3], y0 = V.idx[(long long)c * 3 + 1], z0 = V.idx[(long long)c * 3 + 2];
+  double phi[27];
+  const int D = V.D;
+  const int zl = D == 3 ? -1 : 0, zh = D == 3 ? 1 : 0;
+  int b = 0;
+  for (int dz = zl; dz <= zh; ++dz)
+    for (int dy = -1; dy <= 1; ++dy)
+      for (int dx = -1; dx <= 1; ++dx, ++b) {
+        const int nb = amr_lookup(V, l, x0 + dx, y0 + dy, z0 + dz);
+        phi[b] = V.u[(long long)(nb >= 0 ? nb : c) * V.NV];   // Phi = rho
+      }
+  const int st[3] = {1, 3, 9};
+  int cc = 0;
+  for (int k = 0; k < D; ++k) cc += st[k];
+  double num = 0.0, den = 0.0;
+  for (int k = 0; k < D; ++k)
+    for (int q = 0; q < D; ++q) {
+      double nn, e;
+      if (k == q) {
+        const double pp = phi[cc + st[k]], p0 = phi[cc], pm = phi[cc - st[k]];
+        nn = __dadd_rn(__dsub_rn(pp, __dmul_rn(2.0, p0)), pm);
+        e = __dadd_rn(__dadd_rn(fabs(__dsub_rn(pp, p0)), fabs(__dsub_rn(p0, pm))),
+                      __dmul_rn(eps, __dadd_rn(__dadd_rn(fabs(pp), __dmul_rn(2.0, fabs(p0))), fabs(pm))));
+      } else {
+        const double a = phi[cc + st[k] + st[q]], bb = phi[cc + st[k] - st[q]];
+        const double c2 = phi[cc - st[k] + st[q]], d2 = phi[cc - st[k] - st[q]];
+        nn = __dmul_rn(0.25, __dadd_rn(__dsub_rn(__dsub_rn(a, bb), c2), d2));
+        e = __dadd_rn(__dmul_rn(0.5, __dadd_rn(fabs(__dsub_rn(a, c2)), fabs(__dsub_rn(bb, d2)))),
+                      __dmul_rn(__dmul_rn(0.25, eps),
+                                __dadd_rn(__dadd_rn(__dadd_rn(fabs(a), fabs(bb)), fabs(c2)), fabs(d2))));
+      }
+      num = __dadd_rn(num, __dmul_rn(nn, nn));
+      den = __dadd_rn(den, __dmul_rn(e, e));
+    }
+  V.chi[c] = (den == 0.0) ? 0.0 : __dsqrt_rn(__ddiv_rn(num, den));
+}
+
+template <int D, int SYS>
+__global__ void k_amr_ic(AmrDevView V, const int* __restrict__ list, int n, const double* __restrict__ prim,
+                         const double* __restrict__ wq, int nq, double gamma) {
+  using PH = Phys<SYS, D>;
+  constexpr int NV = PH::NV;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double acc[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) acc[v] = 0.0;
+  for (int g = 0; g < nq; ++g) {
+    double uu[NV];
+    PH::prim_to_cons(prim + ((long long)i * nq + g) * 9, gamma, uu);
+#pragma unroll
+    for (int v = 0; v < NV; ++v) acc[v] += wq[g] * uu[v];
+  }
+  const int c = list[i];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) V.u[(long long)c * NV + v] = acc[v];
+}
+
+// ===========================================================================
+// launchers
+// ===========================================================================
+namespace {
+inline unsigned gsz(long long n, int bs) { return (unsigned)((n + bs - 1) / bs); }
+inline void cl(const KCtx& k) { if (k.launches) ++*k.launches; }
+}  // namespace
+
+#define AMR_DISPATCH(D_, M_, SYS_, ...)                                                         \
+  do {                                                                                          \
+    if (D_ == 2 && M_ == 2 && SYS_ == 0) { constexpr int D = 2, M = 2, SYS = 0; __VA_ARGS__; }  \
+    else if (D_ == 2 && M_ == 3 && SYS_ == 0) { constexpr int D = 2, M = 3, SYS = 0; __VA_ARGS__; } \
+    else if (D_ == 3 && M_ == 2 && SYS_ == 0) { constexpr int D = 3, M = 2, SYS = 0; __VA_ARGS__; } \
+    else if (D_ == 2 && M_ == 2 && SYS_ == 1) { constexpr int D = 2, M = 2, SYS = 1; __VA_ARGS__; } \
+    else if (D_ == 2 && M_ == 3 && SYS_ == 1) { constexpr int D = 2, M = 3, SYS = 1; __VA_ARGS__; } \
+    else if (D_ == 3 && M_ == 2 && SYS_ == 1) { constexpr int D = 3, M = 2, SYS = 1; __VA_ARGS__; } \
+  } while (0)
+
+void amr_launch_average(const KCtx& k, const AmrDevView& v, const int* list, int n) {
+  if (n <= 0) return;
+  cl(k);
+  k_amr_average<<<gsz((long long)n * v.NV, 256), 256, 0, k.stream>>>(v, list, n);
+}
+
+void amr_launch_project(const KCtx& k, const AmrDevView& v, const SubTables& st, const int* list, int n,
+                        const double* pt) {
+  if (n <= 0) return;
+  cl(k);
+  AMR_DISPATCH(k.D, k.M, k.SYS, (void)SYS;
+               k_amr_project<D, M><<<gsz((long long)n * v.NV, 128), 128, 0, k.stream>>>(v, st, list, n, pt[0], pt[1],
+                                                                                        pt[2], pt[3]));
+}
+
+void amr_launch_init_from_weno(const KCtx& k, const AmrDevView& v, const SubTables& st, const int* pairs, int n) {
+  if (n <= 0) return;
+  cl(k);
+  AMR_DISPATCH(k.D, k.M, k.SYS, (void)SYS;
+               k_amr_init_pairs<D, M><<<gsz((long long)n * v.NV, 128), 128, 0, k.stream>>>(v, st, pairs, n, 0, 0, 0,
+                                                                                           0, 0));
+}
+
+void amr_launch_init_from_pred(const KCtx& k, const AmrDevView& v, const SubTables& st, const int* pairs, int n,
+                               const double* pt) {
+  if (n <= 0) return;
+  cl(k);
+  AMR_DISPATCH(k.D, k.M, k.SYS, (void)SYS;
+               k_amr_init_pairs<D, M><<<gsz((long long)n * v.NV, 128), 128, 0, k.stream>>>(v, st, pairs, n, 1, pt[0],
+                                                                                           pt[1], pt[2], pt[3]));
+}
+
+void amr_launch_weno(const KCtx& k, const AmrDevView& v, const int* list, int n) {
+  if (n <= 0) return;
+  cl(k);
+  AMR_DISPATCH(k.D, k.M, k.SYS, {
+    constexpr int NV = Phys<SYS, D>::NV;
+    k_amr_weno<D, M, NV><<<gsz((long long)n * NV, 128), 128, 0, k.stream>>>(v, list, n, k.tab);
+  });
+}
+
+void amr_launch_predictor(const KCtx& k, const AmrDevView& v, const int* list, int n, const double dtdx[3],
+                          double tol, int max_sweeps, DevCounters* cnt) {
+  if (n <= 0) return;
+  Box none{{0, 0, 0}, {0, 0, 0}};
+  launch_predictor_list(k, v.w, v.q, none, list, n, dtdx, tol, max_sweeps, cnt);
+}
+
+void amr_launch_flux_update(const KCtx& k, const AmrDevView& v, const SubTables& st, const int* list, int n, int m,
+                            const double dtdx[3], DevCounters* cnt) {
+  if (n <= 0) return;
+  cl(k);
+  AMR_DISPATCH(k.D, k.M, k.SYS,
+               k_amr_flux_update<D, M, SYS><<<gsz(n, 64), 64, 0, k.stream>>>(v, st, list, n, m, dtdx[0], dtdx[1],
+                                                                            dtdx[2], k.gamma, k.ch, cnt, k.tab));
+}
+
+void amr_launch_cfl(const KCtx& k, const AmrDevView& v, const int* list, int n, const double inv_dx0[3],
+                    DevCounters* cnt) {
+  if (n <= 0) return;
+  cl(k);
+#define CFLK(D_, S_)                                                                                          \
+  k_amr_cfl<D_, S_><<<gsz(n, 256), 256, 0, k.stream>>>(v, list, n, inv_dx0[0], inv_dx0[1], inv_dx0[2], k.gamma, \
+                                                       k.ch, cnt)
+  if (k.D == 2 && k.SYS == 0) CFLK(2, 0);
+  else if (k.D == 3 && k.SYS == 0) CFLK(3, 0);
+  else if (k.D == 2 && k.SYS == 1) CFLK(2, 1);
+  else CFLK(3, 1);
+#undef CFLK
+}
+
+void amr_launch_indicator(const KCtx& k, const AmrDevView& v, const int* list, int n, double eps) {
+  if (n <= 0) return;
+  cl(k);
+  k_amr_indicator<<<gsz(n, 128), 128, 0, k.stream>>>(v, list, n, eps);
+}
+
+void amr_launch_ic(const KCtx& k, const AmrDevView& v, const int* list, int n, const double* prim, const double* wq,
+                   int nq) {
+  if (n <= 0) return;
+  cl(k);
+#define ICK(D_, S_) k_amr_ic<D_, S_><<<gsz(n, 128), 128, 0, k.stream>>>(v, list, n, prim, wq, nq, k.gamma)
+  if (k.D == 2 && k.SYS == 0) ICK(2, 0);
+  else if (k.D == 3 && k.SYS == 0) ICK(3, 0);
+  else if (k.D == 2 && k.SYS == 1) ICK(2, 1);
+  else ICK(3, 1);
+#undef ICK
+}
+
+}  // namespace ader

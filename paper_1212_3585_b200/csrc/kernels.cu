@@ -78,7 +78,8 @@ template <int D, int M, int SYS, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32) k_predictor(
     const double* __restrict__ w, double* __restrict__ q, const Box R, const long long sy, const long long sz,
     const double dtdx0, const double dtdx1, const double dtdx2, const double gamma, const double ch,
-    const double tol, const int max_sweeps, DevCounters* __restrict__ cnt, const __grid_constant__ DevTables T) {
+    const double tol, const int max_sweeps, DevCounters* __restrict__ cnt, const int* __restrict__ list,
+    const long long nlist, const __grid_constant__ DevTables T) {
   using PH = Phys<SYS, D>;
   constexpr int NV = PH::NV, N = M + 1, NS = ipow_c(N, D), NST = NS * N;
   constexpr int CPW = 32 / NS;
@@ -90,8 +91,9 @@ __global__ void __launch_bounds__(WARPS * 32) k_predictor(
   double* Fs = smem + (warp * CPW + (slot < CPW ? slot : CPW - 1)) * FSZ;
   double* red = smem + WARPS * CPW * FSZ + warp * 64;
   const long long rc = ((long long)blockIdx.x * WARPS + warp) * CPW + slot;
-  const bool active = slot < CPW && rc < R.count();
-  const long long cell = active ? box_cell(R, rc, sy, sz) : 0;
+  // cells of a box (uniform grid) or of an id list (AMR level)
+  const bool active = slot < CPW && rc < (list ? nlist : R.count());
+  const long long cell = active ? (list ? (long long)list[rc] : box_cell(R, rc, sy, sz)) : 0;
   int ia[3];
   ia[0] = node % N;
   ia[1] = (node / N) % N;
@@ -477,7 +479,13 @@ void launch_weno_sweep(const KCtx& k, int sweep, const double* src, double* dst,
 
 void launch_predictor(const KCtx& k, const double* w, double* q, const Box& region, const double dtdx[3],
                       double tol, int max_sweeps, DevCounters* cnt) {
-  if (region.count() == 0) return;
+  launch_predictor_list(k, w, q, region, nullptr, 0, dtdx, tol, max_sweeps, cnt);
+}
+
+void launch_predictor_list(const KCtx& k, const double* w, double* q, const Box& region, const int* list,
+                           long long nlist, const double dtdx[3], double tol, int max_sweeps, DevCounters* cnt) {
+  const long long count = list ? nlist : region.count();
+  if (count == 0) return;
   ADER_DISPATCH(k.D, k.M, k.SYS, {
     constexpr int N = M + 1;
     constexpr int NS = ipow_c(N, D);
@@ -489,10 +497,10 @@ void launch_predictor(const KCtx& k, const double* w, double* q, const Box& regi
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       attr = true;
     }
-    const unsigned g = grid_for(region.count(), kPredWarps * CPW);
+    const unsigned g = grid_for(count, kPredWarps * CPW);
     count_launch(k);
     kern<<<g, kPredWarps * 32, sm, k.stream>>>(w, q, region, k.sy, k.sz, dtdx[0], dtdx[1], dtdx[2], k.gamma,
-                                                k.ch, tol, max_sweeps, cnt, k.tab);
+                                                k.ch, tol, max_sweeps, cnt, list, nlist, k.tab);
   });
 }
 

@@ -49,6 +49,9 @@ void launch_weno_sweep(const KCtx& k, int sweep, const double* src, double* dst,
 // Predictor on `region`: w -> q.
 void launch_predictor(const KCtx& k, const double* w, double* q, const Box& region, const double dtdx[3],
                       double tol, int max_sweeps, DevCounters* cnt);
+// Predictor on the cells of an id list (AMR levels): w, q indexed by id.
+void launch_predictor_list(const KCtx& k, const double* w, double* q, const Box& region, const int* list,
+                           long long nlist, const double dtdx[3], double tol, int max_sweeps, DevCounters* cnt);
 // Face fluxes on the lower face of every cell of faces[dir], for dir < D.
 // bmask bit 2*dir (2*dir+1): the first (last) face along dir is a physical
 // transmissive boundary and takes the interior trace on both sides.

@@ -1,0 +1,99 @@
+"""GPU parity of the AMR + local-time-stepping path against the AMR oracle:
+cell sets and statuses bit-exact (key: level, idx, status), active cell
+averages within the north_star tolerances (reading R8 scale)."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_1212_3585_b200 import ader
+from paper_1212_3585_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+def gpu_cells(s):
+    arr = s.get_cells()
+    lv = np.array([c.level for c in arr], dtype=np.int32)
+    st = np.array([c.status for c in arr], dtype=np.int32)
+    ix = np.array([list(c.idx) for c in arr], dtype=np.int64).reshape(-1, 3)
+    u = np.array([list(c.u)[:s.nv] for c in arr]).reshape(-1, s.nv)
+    return lv, st, ix, u
+
+
+def pair(*, dim, degree, n, lo, hi, bc, ic, lmax, system=0, gamma=1.4, ch=0.0, cfl=0.45, chi_ref=0.2, chi_rec=0.1,
+         refine_factor=3):
+    cfg = ader.make_config(dim=dim, degree=degree, n0=n, lo=lo, hi=hi, bc=bc, system=system, gamma=gamma, ch=ch,
+                           cfl=cfl, lmax=lmax, refine_factor=refine_factor, chi_ref=chi_ref, chi_rec=chi_rec,
+                           adapt_every=1, device=0)
+    g = ader.Solver(cfg)
+    g.set_initial(ic)
+    o = O.AmrOracle(dim=dim, degree=degree, n=n, lo=lo, hi=hi, bc=bc, system=system, gamma=gamma, ch=ch, cfl=cfl,
+                    lmax=lmax, refine_factor=refine_factor, chi_ref=chi_ref, chi_rec=chi_rec)
+    o.set_initial(ic)
+    return g, o
+
+
+def compare(g, o, tol):
+    lg, sg, ig, ug = gpu_cells(g)
+    lo_, so, io, uo = o.cells()
+    assert len(lg) == len(lo_), (len(lg), len(lo_))
+    assert np.array_equal(lg, lo_) and np.array_equal(ig, io) and np.array_equal(sg, so)
+    act = so == 0
+    scale = np.maximum(np.abs(uo[act]).max(axis=0), np.abs(uo[act, 0]).max())
+    err = (np.abs(ug[act] - uo[act]).max(axis=0) / scale).max()
+    assert err <= tol, err
+    return err
+
+
+CASES = {
+    "explosion2d_l2": dict(dim=2, degree=2, n=(16, 16), lo=(-1, -1), hi=(1, 1), bc=(1,) * 6, ic=W.explosion(2), lmax=2),
+    "vortex2d_M3_l1": dict(dim=2, degree=3, n=(12, 12), lo=(0, 0), hi=(10, 10), bc=(0,) * 6, ic=W.isentropic_vortex(),
+                           lmax=1, cfl=0.9, chi_ref=0.01, chi_rec=0.005),
+    "ot_mhd_M3_l1": dict(dim=2, degree=3, n=(12, 12), lo=(0, 0), hi=(2 * math.pi, 2 * math.pi), bc=(0,) * 6,
+                         ic=W.orszag_tang(), lmax=1, system=1, gamma=5 / 3, ch=2.0, chi_ref=0.02, chi_rec=0.01),
+    "explosion3d_l1": dict(dim=3, degree=2, n=(6, 6, 6), lo=(-1,) * 3, hi=(1,) * 3, bc=(1,) * 6, ic=W.explosion(3),
+                           lmax=1, cfl=0.3),
+}
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_initial_hierarchy_bit_exact(name):
+    g, o = pair(**CASES[name])
+    compare(g, o, 1e-14)
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_one_macro_step(name):
+    g, o = pair(**CASES[name])
+    dt_o = o.compute_dt()
+    rg = g.step(1e300, 1)
+    ro = o.step(1e300, 1)
+    assert abs(rg.dt0 - dt_o) <= 1e-14 * dt_o
+    assert list(rg.updates_per_level) == list(ro.updates_per_level)
+    compare(g, o, 1e-11)
+
+
+@pytest.mark.parametrize("name", ["explosion2d_l2", "vortex2d_M3_l1"])
+def test_several_macro_steps_with_adapt(name):
+    g, o = pair(**CASES[name])
+    rg = g.step(1e300, 4)
+    ro = o.step(1e300, 4)
+    assert rg.cell_updates == ro.cell_updates
+    compare(g, o, 1e-9)
+
+
+def test_amr_conservation_periodic():
+    g, _ = pair(dim=2, degree=2, n=(12, 12), lo=(0, 0), hi=(1, 1), bc=(0,) * 6, ic=W.random_smooth(2, seed=3585, amp=0.15),
+                lmax=1, cfl=0.45, chi_ref=0.02, chi_rec=0.01)
+
+    def tot():
+        lv, st, ix, u = gpu_cells(g)
+        vol = np.array([(1 / 12 / 3 ** l) ** 2 for l in lv])
+        a = st == 0
+        return (u[a] * vol[a, None]).sum(0)
+    t0 = tot()
+    g.step(1e300, 3)
+    t1 = tot()
+    assert np.all(np.abs(t1 - t0) <= 1e-13 * np.maximum(1.0, np.abs(t0)))
