@@ -373,7 +373,9 @@ void run_flux(ader_ctx* c) {
   long long nf = 0;
   for (int k = 0; k < c->d; ++k) nf += fb[k].count();
   Scope s(c, ADER_K_FLUX, face_flops(c) * nf);
-  launch_face_flux(c->k, c->q, c->F, fb, transmissive_mask(c), c->cnt);
+  const int H = c->H, zH = c->d == 3 ? H : 0;
+  const Box ext = make_box(H, H + c->n[0] + 1, H, H + c->n[1] + 1, zH, zH + c->n[2] + (c->d == 3 ? 1 : 0));
+  launch_face_flux_cells(c->k, c->q, c->F, ext, H, c->n, transmissive_mask(c), c->cnt);
 }
 
 void run_update(ader_ctx* c, double dt) {

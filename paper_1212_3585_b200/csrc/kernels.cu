@@ -69,10 +69,13 @@ __global__ void __launch_bounds__(256) k_weno(const double* __restrict__ src, do
 }
 
 // ===========================================================================
-// a2: predictor.  One thread per (cell, spatial node); the thread keeps the
-// node's time pencil q[NV][N] in registers.  Pointwise fluxes are exchanged
-// through shared memory inside the warp that holds the cell, so the Picard
-// loop needs only __syncwarp; each cell stops at its own convergence.
+// a2: predictor.  One lane per (cell, spatial node); the lane keeps the node's
+// time pencil q[NV][N] in registers.  A cell owns a power-of-two lane group
+// (G >= N^D) inside one warp, so the Picard loop needs only __syncwarp and
+// segmented shuffles; each cell stops at its own convergence (R2), which makes
+// the result independent of how cells are grouped into CTAs.
+// Sweep 1 starts from the time-constant guess q^0 = w (R3): all N time levels
+// carry the same flux, so it is evaluated once and q^1_s = w - (sum_s' T_ss') G.
 // ===========================================================================
 template <int D, int M, int SYS, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32) k_predictor(
@@ -82,92 +85,104 @@ __global__ void __launch_bounds__(WARPS * 32) k_predictor(
     const long long nlist, const __grid_constant__ DevTables T) {
   using PH = Phys<SYS, D>;
   constexpr int NV = PH::NV, N = M + 1, NS = ipow_c(N, D), NST = NS * N;
-  constexpr int CPW = 32 / NS;
-  static_assert(CPW >= 1, "one cell must fit in a warp");
-  constexpr int FSZ = D * NV * N * NS;
+  constexpr int G = (NS <= 8) ? 8 : (NS <= 16 ? 16 : 32);   // lanes per cell
+  constexpr int CPW = 32 / G;
+  static_assert(NS <= 32, "one cell must fit in a warp");
+  constexpr int FSZ = D * NV * N * NS + 8;                   // +8: bank offset between cells
   extern __shared__ double smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int slot = lane / NS, node = lane - slot * NS;
-  double* Fs = smem + (warp * CPW + (slot < CPW ? slot : CPW - 1)) * FSZ;
-  double* red = smem + WARPS * CPW * FSZ + warp * 64;
+  const int slot = lane / G, node0 = lane - slot * G;
+  const bool lane_ok = node0 < NS;
+  const int node = lane_ok ? node0 : NS - 1;
+  double* Fs = smem + (warp * CPW + slot) * FSZ;
   const long long rc = ((long long)blockIdx.x * WARPS + warp) * CPW + slot;
   // cells of a box (uniform grid) or of an id list (AMR level)
-  const bool active = slot < CPW && rc < (list ? nlist : R.count());
-  const long long cell = active ? (list ? (long long)list[rc] : box_cell(R, rc, sy, sz)) : 0;
+  const bool cell_ok = rc < (list ? nlist : R.count());
+  const bool active = cell_ok && lane_ok;
+  const long long cell = cell_ok ? (list ? (long long)list[rc] : box_cell(R, rc, sy, sz)) : 0;
   int ia[3];
   ia[0] = node % N;
   ia[1] = (node / N) % N;
   ia[2] = node / (N * N);
   const double dtdx[3] = {dtdx0, dtdx1, dtdx2};
+  double Drow[D][N];                                          // D[ia_d][j] (lane-dependent rows)
+#pragma unroll
+  for (int d = 0; d < D; ++d)
+#pragma unroll
+    for (int j = 0; j < N; ++j) Drow[d][j] = T.D[ia[d]][j];
 
   double wv[NV], qv[NV][N];
 #pragma unroll
-  for (int v = 0; v < NV; ++v) {
-    wv[v] = active ? w[cell * (NV * NS) + v * NS + node] : 1.0;
-#pragma unroll
-    for (int s = 0; s < N; ++s) qv[v][s] = wv[v];   // time-constant initial guess (reading R3)
-  }
-  bool conv = !active, bad = false;
+  for (int v = 0; v < NV; ++v) wv[v] = cell_ok ? w[cell * (NV * NS) + v * NS + node] : 1.0;
+  bool conv = !cell_ok, bad = false;
   int nsw = 0;
   for (int sweep = 1; sweep <= max_sweeps; ++sweep) {
+    const int NT = (sweep == 1) ? 1 : N;                      // distinct time levels of the iterate
     if (!conv) {
       // nodal fluxes f*_dir = (dt/dx_dir) f_dir(q) (eqn.nodal.eval @ P:405-412)
 #pragma unroll
       for (int s = 0; s < N; ++s) {
+        if (s >= NT) break;
         double uu[NV], f[D][NV];
 #pragma unroll
-        for (int v = 0; v < NV; ++v) uu[v] = qv[v][s];
-        bad |= !PH::fluxes(uu, gamma, ch, f);
+        for (int v = 0; v < NV; ++v) uu[v] = (sweep == 1) ? wv[v] : qv[v][s];
+        bad |= lane_ok && !PH::fluxes(uu, gamma, ch, f);
+        if (lane_ok) {
 #pragma unroll
-        for (int d = 0; d < D; ++d)
+          for (int d = 0; d < D; ++d)
 #pragma unroll
-          for (int v = 0; v < NV; ++v) Fs[((d * NV + v) * N + s) * NS + node] = dtdx[d] * f[d][v];
+            for (int v = 0; v < NV; ++v) Fs[((d * NV + v) * N + s) * NS + node] = dtdx[d] * f[d][v];
+        }
       }
     }
     __syncwarp();
     double dmax = 0.0, qmax = 0.0;
-    if (!conv) {
+    if (!conv && lane_ok) {
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
-        double G[N];
+        double Gs[N];
 #pragma unroll
         for (int s = 0; s < N; ++s) {
+          if (s >= NT) break;
           double g = 0.0;
 #pragma unroll
           for (int d = 0; d < D; ++d) {
-            constexpr int dummy = 0; (void)dummy;
             const int sd = (d == 0) ? 1 : (d == 1 ? N : N * N);
             const double* fb = Fs + ((d * NV + v) * N + s) * NS + node - ia[d] * sd;
 #pragma unroll
-            for (int j = 0; j < N; ++j) g += T.D[ia[d]][j] * fb[j * sd];
+            for (int j = 0; j < N; ++j) g += Drow[d][j] * fb[j * sd];
           }
-          G[s] = g;
+          Gs[s] = g;
         }
 #pragma unroll
         for (int s = 0; s < N; ++s) {
-          double acc = wv[v];
+          double acc;
+          if (sweep == 1) {
+            acc = wv[v] - T.Tsum[s] * Gs[0];
+          } else {
+            acc = wv[v];
 #pragma unroll
-          for (int s2 = 0; s2 < N; ++s2) acc -= T.T[s][s2] * G[s2];
-          dmax = fmax(dmax, fabs(acc - qv[v][s]));
+            for (int s2 = 0; s2 < N; ++s2) acc -= T.T[s][s2] * Gs[s2];
+          }
+          const double prev = (sweep == 1) ? wv[v] : qv[v][s];
+          dmax = fmax(dmax, fabs(acc - prev));
           qmax = fmax(qmax, fabs(acc));
           qv[v][s] = acc;
         }
       }
     }
-    red[lane] = dmax;
-    red[32 + lane] = qmax;
-    __syncwarp();
-    if (!conv) {
-      double dm = 0.0, qm = 0.0;
+    // per-cell max over the lane group (segmented butterfly)
 #pragma unroll
-      for (int j = 0; j < NS; ++j) {
-        dm = fmax(dm, red[slot * NS + j]);
-        qm = fmax(qm, red[32 + slot * NS + j]);
-      }
+    for (int o = G / 2; o > 0; o >>= 1) {
+      dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o, G));
+      qmax = fmax(qmax, __shfl_xor_sync(0xffffffffu, qmax, o, G));
+    }
+    if (!conv) {
       nsw = sweep;
-      if (dm <= tol * (1.0 + qm)) conv = true;   // reading R2
+      if (dmax <= tol * (1.0 + qmax)) conv = true;   // reading R2
     }
     if (__all_sync(0xffffffffu, conv)) break;
+    __syncwarp();
   }
   if (!active) return;
   if (bad) record_error(cnt, 1, 1, cell);
@@ -260,6 +275,102 @@ __global__ void __launch_bounds__(WARPS * 32) k_face_flux(const double* __restri
   if (blockIdx.y == 0) face_flux_dir<D, M, SYS, 0, WARPS>(q, F, R0, sy, sz, ncell, gamma, ch, bmask, cnt, T, red);
   else if (blockIdx.y == 1) face_flux_dir<D, M, SYS, 1, WARPS>(q, F, R1, sy, sz, ncell, gamma, ch, bmask, cnt, T, red);
   else if (D == 3) face_flux_dir<D, M, SYS, 2, WARPS>(q, F, R2, sy, sz, ncell, gamma, ch, bmask, cnt, T, red);
+}
+
+// ---------------------------------------------------------------------------
+// a3 (cell-grouped): one lane group (power of two >= N^D lanes, a lane per
+// space-time quadrature point) computes ALL lower faces of one cell, reading the
+// cell's q once for the D faces.  Cells are visited x fastest, then y inside
+// chunks of YC rows, then z, then the y chunk, so that the -y and -z
+// neighbours' q (read for the same cell) were touched a few MB earlier and are
+// still in L2 (the plain x-y-z order re-reads the -z neighbour from HBM).
+// The per-face sum over quadrature points is a fixed butterfly (deterministic).
+// ---------------------------------------------------------------------------
+template <int D, int M, int SYS, int DIR, int G>
+__device__ __forceinline__ void cell_face(const double* __restrict__ q, double* __restrict__ F, long long cR,
+                                          int fc, bool fok, int lo_face, int hi_face, long long sd, long long ncell,
+                                          double gamma, double ch, int bmask, DevCounters* cnt, const DevTables& T) {
+  using PH = Phys<SYS, D>;
+  constexpr int NV = PH::NV, N = M + 1, NS = ipow_c(N, D), NST = NS * N;
+  constexpr int NT = NS / N;
+  const int p = threadIdx.x & (G - 1);
+  double val[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) val[v] = 0.0;
+  if (fok && p < NS) {
+    const long long cL = cR - sd;
+    const int s = p / NT, t = p - s * NT;
+    const int t1 = t % N, t2 = t / N;
+    constexpr int ax0 = (DIR == 0) ? 1 : 0;
+    constexpr int ax1 = (DIR == 2) ? 1 : 2;
+    constexpr int sn = ipow_c(N, DIR);
+    const int base = s * NS + t1 * ipow_c(N, ax0) + (D == 3 ? t2 * ipow_c(N, ax1) : 0);
+    const double* qL = q + cL * (NV * NST) + base;
+    const double* qR = q + cR * (NV * NST) + base;
+    const bool tlo = ((bmask >> (2 * DIR)) & 1) && fc == lo_face;
+    const bool thi = ((bmask >> (2 * DIR + 1)) & 1) && fc == hi_face;
+    double um[NV], up[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      double a = 0.0, b = 0.0;
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        if (!tlo) a += T.psi1[k] * __ldg(&qL[v * NST + k * sn]);   // q_h^- (xi = 1 of the left cell)
+        if (!thi) b += T.psi0[k] * __ldg(&qR[v * NST + k * sn]);   // q_h^+ (xi = 0 of the right cell)
+      }
+      um[v] = tlo ? b : a;   // transmissive boundary: interior trace on both sides (R5)
+      up[v] = thi ? a : b;
+    }
+    double fL[NV], fR[NV], sL, sR;
+    bool ok = PH::template flux_speed<DIR>(um, gamma, ch, fL, sL);
+    ok &= PH::template flux_speed<DIR>(up, gamma, ch, fR, sR);
+    if (!ok) record_error(cnt, 1, 2, cR);
+    const double smax = fmax(sL, sR);   // reading R4
+    double wt = T.w[s] * T.w[t1];
+    if (D == 3) wt *= T.w[t2];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) val[v] = wt * (0.5 * (fL[v] + fR[v]) - 0.5 * smax * (up[v] - um[v]));   // eqn.rusanov
+  }
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1)
+#pragma unroll
+    for (int v = 0; v < NV; ++v) val[v] += __shfl_xor_sync(0xffffffffu, val[v], o, G);
+  if (fok && p == 0) {
+    double* out = F + ((long long)DIR * ncell + cR) * NV;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) out[v] = val[v];
+  }
+}
+
+template <int D, int M, int SYS, int WARPS, int YC>
+__global__ void __launch_bounds__(WARPS * 32) k_face_flux_cells(const double* __restrict__ q, double* __restrict__ F,
+                                                                const Box E, const int H, const int n0, const int n1,
+                                                                const int n2, const long long sy, const long long sz,
+                                                                const long long ncell, const double gamma,
+                                                                const double ch, const int bmask,
+                                                                DevCounters* __restrict__ cnt,
+                                                                const __grid_constant__ DevTables T) {
+  constexpr int NS = ipow_c(M + 1, D);
+  constexpr int G = (NS <= 8) ? 8 : (NS <= 16 ? 16 : 32);
+  constexpr int CPW = 32 / G;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long r = ((long long)blockIdx.x * WARPS + warp) * CPW + lane / G;
+  const int ex = E.ext[0], ez = E.ext[2];
+  const long long t = r / ex;
+  const int x = (int)(r - t * ex);
+  const int yi = (int)(t % YC);
+  const long long t2 = t / YC;
+  const int z = (int)(t2 % ez);
+  const long long yb = t2 / ez;
+  const int y = (int)(yb * YC + yi);
+  const bool ok = y < E.ext[1] && yb * YC < E.ext[1];
+  const int cx = E.lo[0] + x, cy = E.lo[1] + y, cz = E.lo[2] + z;
+  const long long cR = ok ? cx + cy * sy + cz * sz : 0;
+  const int zH = (D == 3) ? H : 0;
+  const bool inx = cx < H + n0, iny = cy < H + n1, inz = (D == 2) || cz < zH + n2;
+  cell_face<D, M, SYS, 0, G>(q, F, cR, cx, ok && iny && inz, H, H + n0, 1, ncell, gamma, ch, bmask, cnt, T);
+  cell_face<D, M, SYS, 1, G>(q, F, cR, cy, ok && inx && inz, H, H + n1, sy, ncell, gamma, ch, bmask, cnt, T);
+  if (D == 3) cell_face<D, M, SYS, 2, G>(q, F, cR, cz, ok && inx && iny, zH, zH + n2, sz, ncell, gamma, ch, bmask, cnt, T);
 }
 
 // ===========================================================================
@@ -432,8 +543,9 @@ constexpr int kFluxWarps = 4;
 
 template <int D, int M, int SYS>
 size_t pred_smem() {
-  constexpr int NV = Phys<SYS, D>::NV, N = M + 1, NS = ipow_c(N, D), CPW = 32 / NS;
-  return sizeof(double) * ((size_t)kPredWarps * CPW * D * NV * N * NS + kPredWarps * 64);
+  constexpr int NV = Phys<SYS, D>::NV, N = M + 1, NS = ipow_c(N, D);
+  constexpr int G = (NS <= 8) ? 8 : (NS <= 16 ? 16 : 32), CPW = 32 / G;
+  return sizeof(double) * ((size_t)kPredWarps * CPW * (D * NV * N * NS + 8));
 }
 template <int D, int M, int SYS>
 size_t flux_smem() {
@@ -489,7 +601,7 @@ void launch_predictor_list(const KCtx& k, const double* w, double* q, const Box&
   ADER_DISPATCH(k.D, k.M, k.SYS, {
     constexpr int N = M + 1;
     constexpr int NS = ipow_c(N, D);
-    constexpr int CPW = 32 / NS;
+    constexpr int CPW = 32 / ((NS <= 8) ? 8 : (NS <= 16 ? 16 : 32));
     const size_t sm = pred_smem<D, M, SYS>();
     auto kern = k_predictor<D, M, SYS, kPredWarps>;
     static bool attr = false;
@@ -501,6 +613,21 @@ void launch_predictor_list(const KCtx& k, const double* w, double* q, const Box&
     count_launch(k);
     kern<<<g, kPredWarps * 32, sm, k.stream>>>(w, q, region, k.sy, k.sz, dtdx[0], dtdx[1], dtdx[2], k.gamma,
                                                 k.ch, tol, max_sweeps, cnt, list, nlist, k.tab);
+  });
+}
+
+void launch_face_flux_cells(const KCtx& k, const double* q, double* F, const Box& ext, int H, const int n[3],
+                            int bmask, DevCounters* cnt) {
+  if (ext.count() == 0) return;
+  constexpr int YC = 16;
+  ADER_DISPATCH(k.D, k.M, k.SYS, {
+    constexpr int NS = ipow_c(M + 1, D);
+    constexpr int CPW = 32 / ((NS <= 8) ? 8 : (NS <= 16 ? 16 : 32));
+    const long long ych = (ext.ext[1] + YC - 1) / YC;
+    const long long groups = (long long)ext.ext[0] * ych * YC * ext.ext[2];
+    count_launch(k);
+    k_face_flux_cells<D, M, SYS, kFluxWarps, YC><<<grid_for(groups, kFluxWarps * CPW), kFluxWarps * 32, 0, k.stream>>>(
+        q, F, ext, H, n[0], n[1], n[2], k.sy, k.sz, k.ncell, k.gamma, k.ch, bmask, cnt, k.tab);
   });
 }
 

@@ -56,6 +56,10 @@ void launch_predictor_list(const KCtx& k, const double* w, double* q, const Box&
 // bmask bit 2*dir (2*dir+1): the first (last) face along dir is a physical
 // transmissive boundary and takes the interior trace on both sides.
 void launch_face_flux(const KCtx& k, const double* q, double* F, const Box faces[3], int bmask, DevCounters* cnt);
+// Same fluxes, one lane group per cell of `ext` (owned block + 1 on each active
+// axis) computing all lower faces of that cell (L2-friendly traversal).
+void launch_face_flux_cells(const KCtx& k, const double* q, double* F, const Box& ext, int H, const int n[3],
+                            int bmask, DevCounters* cnt);
 // FV update of `interior` in place + max CFL speed of the new state.
 void launch_update(const KCtx& k, double* u, const double* F, const Box& interior, const double dtdx[3],
                    const double inv_dx[3], DevCounters* cnt);

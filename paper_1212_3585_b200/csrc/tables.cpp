@@ -111,8 +111,11 @@ bool build_tables(int M, DevTables* t) {
         B[a * N + b] = (a == b) ? t->w[a] : 0.0;
       }
     if (!solve(N, N, K, B)) return false;
-    for (int a = 0; a < N; ++a)
-      for (int b = 0; b < N; ++b) t->T[a][b] = B[a * N + b];
+    for (int a = 0; a < N; ++a) {
+      double rs = 0.0;
+      for (int b = 0; b < N; ++b) { t->T[a][b] = B[a * N + b]; rs += B[a * N + b]; }
+      t->Tsum[a] = rs;
+    }
   }
   // WENO stencils (eqn.stencildef @ P:220-224): offsets -L..R
   int nS, Ls[4];

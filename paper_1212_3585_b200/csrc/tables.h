@@ -19,7 +19,7 @@ struct DevTables {
   double rec[4][kMaxN][kMaxN];    // rec[s][p][o]: stencil inverse (eqn.rec.x)
   double sigma[kMaxN][kMaxN];     // oscillation indicator matrix
   double lin[4];                  // linear weights lambda_s
-  double P[9][kMaxN][kMaxN];      // projection onto r sub-intervals (AMR; unused uniform)
+  double Tsum[kMaxN];             // row sums of T_tau (first Picard sweep, time-constant guess)
 };
 
 // Fills t for degree M (2 or 3).  Returns false for an unsupported degree.
