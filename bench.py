@@ -116,6 +116,22 @@ def oracle_sample(wl, edge, reps=1):
     workload: one step of an edge^d box straddling the initial discontinuity
     (explosion) / the vortex core.  Returns (cell-updates/s, description)."""
     import oracle as O
+    if wl.lmax > 0:
+        # AMR workload: one macro step of the AMR oracle on a level-0 grid of
+        # edge^d cells of the same problem (full LTS hierarchy, adapt included)
+        n = tuple([edge] * wl.dim)
+        a = O.AmrOracle(dim=wl.dim, degree=wl.degree, n=n, lo=wl.lo, hi=wl.hi, bc=wl.bc, system=wl.system,
+                        gamma=wl.gamma, ch=wl.ch, cfl=wl.cfl, lmax=wl.lmax, refine_factor=wl.refine_factor)
+        a.set_initial(wl.ic)
+        ups, secs = 0, 0.0
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            rep = a.step(1e300, 1, adapt_every=1)
+            secs += time.perf_counter() - t0
+            ups += rep.cell_updates
+        desc = (f"one macro step (all levels, adapt) of {wl.name} on a {'x'.join(map(str, n))} level-0 grid, "
+                f"AMR oracle, single thread")
+        return ups / secs, desc, ups, secs
     o = O.Oracle(dim=wl.dim, degree=wl.degree, n=wl.n, lo=wl.lo, hi=wl.hi, bc=wl.bc, system=wl.system,
                  gamma=wl.gamma, ch=wl.ch, cfl=wl.cfl)
     n = wl.n
@@ -209,7 +225,7 @@ def main():
         nid = obj[0]
     cfg = ader.make_config(dim=wl.dim, degree=wl.degree, n0=wl.n, lo=wl.lo, hi=wl.hi, bc=wl.bc, system=wl.system,
                            gamma=wl.gamma, ch=wl.ch, cfl=wl.cfl, rank=rank, world_size=world, device=local,
-                           nccl_id=nid)
+                           nccl_id=nid, lmax=wl.lmax, refine_factor=wl.refine_factor, adapt_every=1)
     s = ader.Solver(cfg)
     stream = torch.cuda.current_stream()
     s.set_stream(stream.cuda_stream)
@@ -255,26 +271,44 @@ def main():
 
     # end-to-end through the public API with host buffers (pinned)
     ne = max(1, args.e2e_steps)
-    host = torch.empty((s.ncells, s.nv), dtype=torch.float64, pin_memory=True)
-    s.get_state_ptr(host.data_ptr())
-    barrier()
-    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    f0.record(stream)
-    e2e_updates = 0
-    for _ in range(ne):
-        s.set_cells_ptr(host.data_ptr())       # H2D of the step's input state
-        r2 = s.step(1e300, 1)
-        s.get_state_ptr(host.data_ptr())       # D2H of the step's result
-        e2e_updates += r2.cell_updates
-    f1.record(stream)
-    barrier()
-    e2e_ms = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device="cuda")
-    e2u = torch.tensor([float(e2e_updates)], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
-        dist.all_reduce(e2u, op=dist.ReduceOp.SUM)
-    e2e_val = float(e2u.item()) / (float(e2e_ms.item()) / 1e3)
-    bytes_step = s.ncells * s.nv * 8
+    e2e = None
+    if wl.lmax == 0:
+        host = torch.empty((s.ncells, s.nv), dtype=torch.float64, pin_memory=True)
+        s.get_state_ptr(host.data_ptr())
+        barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        e2e_updates = 0
+        for _ in range(ne):
+            s.set_cells_ptr(host.data_ptr())       # H2D of the step's input state
+            r2 = s.step(1e300, 1)
+            s.get_state_ptr(host.data_ptr())       # D2H of the step's result
+            e2e_updates += r2.cell_updates
+        f1.record(stream)
+        barrier()
+        e2e_ms = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device="cuda")
+        e2u = torch.tensor([float(e2e_updates)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+            dist.all_reduce(e2u, op=dist.ReduceOp.SUM)
+        bytes_step = s.ncells * s.nv * 8
+        e2e = {"value": float(e2u.item()) / (float(e2e_ms.item()) / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": bytes_step, "d2h_bytes_per_step": bytes_step, "steps": ne}
+    else:
+        # AMR: the state lives in the device tree; a step's host output is the
+        # full cell list (ader_get_cells), read back every step
+        barrier()
+        w0 = time.perf_counter()
+        e2e_updates, nbytes = 0, 0
+        for _ in range(ne):
+            r2 = s.step(1e300, 1)
+            cells = s.get_cells()
+            e2e_updates += r2.cell_updates
+            nbytes = len(cells) * 96
+        barrier()
+        e2e = {"value": e2e_updates / (time.perf_counter() - w0), "unit": UNIT, "h2d_bytes_per_step": 0,
+               "d2h_bytes_per_step": nbytes, "steps": ne,
+               "note": "AMR: no per-step host input; wall clock incl. ader_get_cells readback"}
 
     if rank == 0:
         pred_ms_avg = kms[ader.K_PRED] / max(1, kl[ader.K_PRED])
@@ -298,8 +332,7 @@ def main():
             "kernel_share_of_step": share,
             "pred_sweeps_mean": rep.pred_sweeps_total / max(1, rep.pred_cells),
             "clocks": clocks,
-            "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": bytes_step, "d2h_bytes_per_step": bytes_step,
-                    "steps": ne},
+            "e2e": e2e,
             "gpu_launches": int(launches),
             "ic_setup_s": t_ic,
         }

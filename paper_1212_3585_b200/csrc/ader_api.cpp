@@ -92,6 +92,7 @@ struct ader_ctx {
   double kflops_sweep = 0.0;                   // predictor flops per cell per sweep
   long long launches = 0;                      // kernels launched by this context
   AmrState* amr = nullptr;                     // lmax > 0: device-resident AMR
+  ProfHook hook;
 };
 
 namespace {
@@ -242,6 +243,27 @@ struct Scope {
     c->recs.push_back(r);
   }
 };
+
+// hook used by the AMR orchestrator (amr.cpp): same records as Scope
+void hook_begin(void* p, int kind) {
+  ader_ctx* c = (ader_ctx*)p;
+  if (!c->prof) return;
+  ProfRec r{};
+  r.kind = kind;
+  r.e0 = get_event(c);
+  r.e1 = nullptr;
+  cudaEventRecord(r.e0, c->k.stream);
+  c->recs.push_back(r);
+}
+void hook_end(void* p, int kind, double flops) {
+  ader_ctx* c = (ader_ctx*)p;
+  if (!c->prof || c->recs.empty() || c->recs.back().e1) return;
+  ProfRec& r = c->recs.back();
+  r.e1 = get_event(c);
+  r.flops = flops;
+  (void)kind;
+  cudaEventRecord(r.e1, c->k.stream);
+}
 
 // Algorithmic FP64 flop model (FMA = 2, add/mul/div/sqrt = 1); see DESIGN.md.
 double weno_problem_flops(int M) {
@@ -432,7 +454,7 @@ void free_ctx(ader_ctx* c) {
   }
   if (c->cnt) cudaFree(c->cnt);
   if (c->hcnt) cudaFreeHost(c->hcnt);
-  for (auto& r : c->recs) { cudaEventDestroy(r.e0); cudaEventDestroy(r.e1); }
+  for (auto& r : c->recs) { if (r.e0) cudaEventDestroy(r.e0); if (r.e1) cudaEventDestroy(r.e1); }
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   if (c->comm) g_nccl.CommDestroy(c->comm);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
@@ -567,6 +589,10 @@ static ader_status create_impl(const ader_config* cfg, ader_ctx** out) {
   c->k.gamma = cfg->gamma; c->k.ch = cfg->ch;
   c->k.stream = c->own_stream;
   c->k.launches = &c->launches;
+  c->hook.ctx = c;
+  c->hook.begin = hook_begin;
+  c->hook.end = hook_end;
+  c->k.hook = &c->hook;
   c->kflops_sweep = pred_sweep_flops(c);
   if (cfg->lmax > 0) {
     // device-resident cell-by-cell AMR (amr.cpp); uniform buffers are not used
@@ -820,7 +846,7 @@ ader_status ader_refine(ader_ctx* c, ader_step_report* rep) {
 ader_status ader_set_profiling(ader_ctx* c, int32_t on) {
   if (!c) return ADER_ERR_ARG;
   CK(cudaStreamSynchronize(c->k.stream));
-  for (auto& r : c->recs) { c->ev_pool.push_back(r.e0); c->ev_pool.push_back(r.e1); }
+  for (auto& r : c->recs) { if (r.e0) c->ev_pool.push_back(r.e0); if (r.e1) c->ev_pool.push_back(r.e1); }
   c->recs.clear();
   c->prof = on != 0;
   CK(cudaMemcpy(c->hcnt, c->cnt, sizeof(DevCounters), cudaMemcpyDeviceToHost));
@@ -839,6 +865,7 @@ ader_status ader_kernel_stats(ader_ctx* c, double ms[ADER_K_COUNT], int64_t laun
   }
   for (auto& r : c->recs) {
     float t = 0.f;
+    if (!r.e1) continue;
     CK(cudaEventElapsedTime(&t, r.e0, r.e1));
     if (ms) ms[r.kind] += t;
     if (launches) launches[r.kind] += 1;

@@ -86,6 +86,17 @@ void build_sub(const DevTables& T, int N, int r, SubTables* S) {
   }
 }
 
+// CUDA-event scope through the context's instrumentation hook
+struct AScope {
+  const AmrState* A; int kind; double fl;
+  AScope(const AmrState* a, int k, double f) : A(a), kind(k), fl(f) {
+    if (A->k->hook && A->k->hook->begin) A->k->hook->begin(A->k->hook->ctx, kind);
+  }
+  ~AScope() {
+    if (A->k->hook && A->k->hook->end) A->k->hook->end(A->k->hook->ctx, kind, fl);
+  }
+};
+
 long long lin(const AmrState* A, int l, const long long* ix) { return (ix[2] * A->n[l][1] + ix[1]) * A->n[l][0] + ix[0]; }
 
 int hlookup(const AmrState* A, int l, const long long* ix0, bool skip_outside) {
@@ -416,18 +427,30 @@ void advance(AmrState* A, int l, int m, double dt0) {
   double dtdx[3] = {0, 0, 0};
   for (int k = 0; k < A->d; ++k) dtdx[k] = dt / A->dx[l][k];
   // ghost refresh (R16): averaging of virtual mothers on levels >= l, finest first
-  for (int lv = A->lmax - 1; lv >= l; --lv) amr_launch_average(*A->k, A->V, L_vmo(A, lv), (int)A->lvmo[lv].size());
-  if (l >= 1) {
-    double pt[4];
-    psi_at(A, (double)m / A->r, pt);
-    amr_launch_project(*A->k, A->V, A->st, L_vch(A, l), (int)A->lvch[l].size(), pt);
+  {
+    AScope sc(A, ADER_K_HALO, 0.0);
+    for (int lv = A->lmax - 1; lv >= l; --lv) amr_launch_average(*A->k, A->V, L_vmo(A, lv), (int)A->lvmo[lv].size());
+    if (l >= 1) {
+      double pt[4];
+      psi_at(A, (double)m / A->r, pt);
+      amr_launch_project(*A->k, A->V, A->st, L_vch(A, l), (int)A->lvch[l].size(), pt);
+    }
   }
   const int na = (int)A->lact[l].size();
-  amr_launch_weno(*A->k, A->V, L_act(A, l), na);
-  amr_launch_predictor(*A->k, A->V, L_act(A, l), na, dtdx, A->cfg.pred_tol, A->cfg.pred_max_sweeps, A->cnt);
+  const int W = 2 * A->M + 1;
+  double wfl = 0.0;   // 1D WENO problems of the per-cell box reconstruction
+  {
+    double per = 0.0, rows = 1.0;
+    for (int k = 0; k < A->d; ++k) { per += rows * (A->d - k == 1 ? 1.0 : std::pow((double)W, A->d - 1 - k)); rows *= A->N; }
+    const int N = A->N, nS = (A->M % 2 == 0) ? 3 : 4;
+    wfl = (double)na * A->nv * per * (nS * (4.0 * N * N + 2.0 * N + 6.0) + 1.0 + 3.0 * N * nS);
+  }
+  { AScope sc(A, ADER_K_WENO, wfl); amr_launch_weno(*A->k, A->V, L_act(A, l), na); }
+  { AScope sc(A, ADER_K_PRED, 0.0);
+    amr_launch_predictor(*A->k, A->V, L_act(A, l), na, dtdx, A->cfg.pred_tol, A->cfg.pred_max_sweeps, A->cnt); }
   if (l < A->lmax && (A->lact[l + 1].size() + A->lvch[l + 1].size() + A->lvmo[l + 1].size()) > 0)
     for (int k = 0; k < A->r; ++k) advance(A, l + 1, k, dt0);
-  amr_launch_flux_update(*A->k, A->V, A->st, L_act(A, l), na, m, dtdx, A->cnt);
+  { AScope sc(A, ADER_K_FLUX, 0.0); amr_launch_flux_update(*A->k, A->V, A->st, L_act(A, l), na, m, dtdx, A->cnt); }
   A->updates[l] += na;
 }
 

@@ -31,7 +31,15 @@ struct DevCounters {              // device-resident, zeroed by the host
   int pad;
 };
 
+// Instrumentation hook (CUDA events around launches, set by ader_api.cpp).
+struct ProfHook {
+  void* ctx = nullptr;
+  void (*begin)(void* ctx, int kind) = nullptr;
+  void (*end)(void* ctx, int kind, double flops) = nullptr;
+};
+
 struct KCtx {
+  ProfHook* hook;
   int D, M, SYS, NV;
   long long sy, sz;               // cell strides along y, z in the padded grid
   long long ncell;                // padded cells

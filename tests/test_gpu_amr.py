@@ -84,6 +84,32 @@ def test_several_macro_steps_with_adapt(name):
     compare(g, o, 1e-9)
 
 
+def test_c3_full_size_first_macro_steps():
+    # BASELINE configs[2]: 2D explosion, 100^2 level 0, r=3, lmax=2, O3 (full size;
+    # the oracle's full run to t=0.25 takes hours, so parity covers 2 macro steps)
+    wl = W.config("c3")
+    g, o = pair(dim=2, degree=2, n=wl.n, lo=wl.lo, hi=wl.hi, bc=wl.bc, ic=wl.ic, lmax=wl.lmax, cfl=wl.cfl,
+                refine_factor=wl.refine_factor)
+    compare(g, o, 1e-14)
+    for _ in range(2):
+        rg = g.step(1e300, 1)
+        ro = o.step(1e300, 1)
+        assert list(rg.updates_per_level) == list(ro.updates_per_level)
+        compare(g, o, 1e-10)
+
+
+def test_c5_full_size_first_macro_step():
+    # BASELINE configs[4]: Orszag-Tang, 120^2 level 0, r=3, lmax=3, M=3, c_h=2
+    wl = W.config("c5")
+    g, o = pair(dim=2, degree=3, n=wl.n, lo=wl.lo, hi=wl.hi, bc=wl.bc, ic=wl.ic, lmax=wl.lmax, system=1,
+                gamma=wl.gamma, ch=wl.ch, cfl=wl.cfl, refine_factor=wl.refine_factor)
+    compare(g, o, 1e-14)
+    rg = g.step(1e300, 1)
+    ro = o.step(1e300, 1)
+    assert list(rg.updates_per_level) == list(ro.updates_per_level)
+    compare(g, o, 1e-11)
+
+
 def test_amr_conservation_periodic():
     g, _ = pair(dim=2, degree=2, n=(12, 12), lo=(0, 0), hi=(1, 1), bc=(0,) * 6, ic=W.random_smooth(2, seed=3585, amp=0.15),
                 lmax=1, cfl=0.45, chi_ref=0.02, chi_rec=0.01)
