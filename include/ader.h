@@ -142,6 +142,20 @@ ader_status ader_refine(ader_ctx* c, ader_step_report* rep);
 
 /* --- multi-GPU plumbing (host only) ---------------------------------------- */
 ader_status ader_partition(const ader_config* cfg, int32_t rank, ader_partition_info* out);
+/* Ghost-layer plan of one side of one axis for a rank (host only).  Boxes are
+ * in the rank's padded coordinates (owned cells start at H = M+1 on every active
+ * axis).  Axes are filled in order x, y, z; for axis a, the extent on axes < a
+ * covers the full padded range (so edges and corners propagate), on axes > a
+ * the owned range.  kind: 0 axis unused, 1 exchange with `peer` (send
+ * send_lo..send_hi, receive into recv_lo..recv_hi; NCCL order per peer: send
+ * low, recv high, send high, recv low), 2 periodic wrap onto itself, 3
+ * transmissive copy of the nearest owned cell (reading R5). */
+typedef struct {
+  int32_t kind, peer;
+  int32_t send_lo[3], send_hi[3];
+  int32_t recv_lo[3], recv_hi[3];
+} ader_halo_desc;
+ader_status ader_halo_plan(const ader_config* cfg, int32_t rank, int32_t axis, int32_t side, ader_halo_desc* out);
 /* 128-byte ncclUniqueId for rank 0 to broadcast (loads libnccl.so.2 lazily). */
 ader_status ader_nccl_unique_id(uint8_t out[128]);
 

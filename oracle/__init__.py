@@ -289,6 +289,31 @@ class Oracle:
             raise RuntimeError(f"oracle advance_box failed: {self.error()}")
         return out, rep
 
+    # distributed emulation: padded grid with caller-provided ghost cells
+    def padded_shape(self):
+        g = self.degree + 1
+        p = [k + 2 * g for k in self.n] + ([1] if self.dim == 2 else [])
+        return (p[2], p[1], p[0], self.nv)
+
+    def get_padded(self):
+        L = lib()
+        L.orc_get_padded.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
+        u = np.zeros(self.padded_shape())
+        L.orc_get_padded(self.ptr, _p(u))
+        return u
+
+    def set_padded(self, u):
+        L = lib()
+        L.orc_set_padded.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        assert u.shape == self.padded_shape()
+        L.orc_set_padded(self.ptr, _p(u))
+
+    def set_external_ghosts(self, on=True):
+        L = lib()
+        L.orc_set_external_ghosts.argtypes = [C.c_void_p, C.c_int]
+        L.orc_set_external_ghosts(self.ptr, 1 if on else 0)
+
     def dump_recon(self):
         w = np.zeros((self.ncells, self.nv, (self.degree + 1) ** self.dim))
         lib().orc_dump_recon(self.ptr, _p(w))

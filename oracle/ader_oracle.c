@@ -726,6 +726,7 @@ struct orc_ctx {
   double dx[3];
   double* u;          /* padded grid [pad cell][nv], ghosts of width G */
   double t;
+  int ext_ghosts;
   char err[512];
 };
 
@@ -846,7 +847,13 @@ static int ghost_src(const orc_ctx* c, int axis, int i) {
   return (i < 0) ? 0 : n - 1;
 }
 
+int64_t orc_num_padded(const orc_ctx* c) { return c->npad; }
+int orc_get_padded(const orc_ctx* c, double* u) { memcpy(u, c->u, sizeof(double) * c->npad * c->nv); return 0; }
+int orc_set_padded(orc_ctx* c, const double* u) { memcpy(c->u, u, sizeof(double) * c->npad * c->nv); return 0; }
+void orc_set_external_ghosts(orc_ctx* c, int on) { c->ext_ghosts = on; }
+
 static void fill_ghosts(orc_ctx* c) {
+  if (c->ext_ghosts) return;   /* ghost cells provided by the caller (distributed emulation) */
   int G = c->G;
   int lo[3], hi[3];
   for (int k = 0; k < 3; ++k) { lo[k] = (k < c->d) ? -G : 0; hi[k] = (k < c->d) ? c->n[k] + G : 1; }

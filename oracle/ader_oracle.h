@@ -125,6 +125,13 @@ int  orc_step(orc_ctx* c, double t_end, int64_t max_steps, orc_report* rep);
  * (x fastest) and leaves the state untouched.  Used for sampled parity. */
 int  orc_advance_box(orc_ctx* c, double dt, const int32_t* blo, const int32_t* bhi,
                      double* out, orc_report* rep);
+/* Distributed emulation (tests of the multi-rank host logic): the padded
+ * grid [pad cell][nv] with ghost width M+1 (x fastest), and a switch that
+ * makes the driver use the ghost cells as given instead of filling them. */
+int64_t orc_num_padded(const orc_ctx* c);
+int  orc_get_padded(const orc_ctx* c, double* u);
+int  orc_set_padded(orc_ctx* c, const double* u);
+void orc_set_external_ghosts(orc_ctx* c, int on);
 /* Debug: reconstruction / predictor of the interior cells with the current
  * state and step dt.  w[cell][nv][N^d], q[cell][nv][N^(d+1)]. */
 int  orc_dump_recon(orc_ctx* c, double* w);

@@ -59,6 +59,11 @@ class AderPartitionInfo(C.Structure):
                 ("nbr", C.c_int32 * 6), ("halo", C.c_int32)]
 
 
+class AderHaloDesc(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("peer", C.c_int32), ("send_lo", C.c_int32 * 3), ("send_hi", C.c_int32 * 3),
+                ("recv_lo", C.c_int32 * 3), ("recv_hi", C.c_int32 * 3)]
+
+
 class AderError(RuntimeError):
     def __init__(self, status, msg):
         super().__init__(f"{STATUS.get(status, status)}: {msg}")
@@ -89,6 +94,7 @@ def lib():
         L.ader_refine.argtypes = [vp, C.POINTER(AderStepReport)]
         L.ader_partition.argtypes = [C.POINTER(AderConfig), C.c_int32, C.POINTER(AderPartitionInfo)]
         L.ader_nccl_unique_id.argtypes = [C.POINTER(C.c_uint8)]
+        L.ader_halo_plan.argtypes = [C.POINTER(AderConfig), C.c_int32, C.c_int32, C.c_int32, C.POINTER(AderHaloDesc)]
         L.ader_set_profiling.argtypes = [vp, C.c_int32]
         L.ader_kernel_stats.argtypes = [vp, dp, C.POINTER(C.c_int64), dp]
         L.ader_launch_count.argtypes = [vp, C.POINTER(C.c_int64)]
@@ -99,7 +105,7 @@ def lib():
 
 EXPORTED = ("ader_create", "ader_destroy", "ader_last_error", "ader_set_stream", "ader_set_initial",
             "ader_set_cells", "ader_get_state", "ader_get_cells", "ader_time", "ader_step", "ader_refine",
-            "ader_partition", "ader_nccl_unique_id", "ader_set_profiling", "ader_kernel_stats",
+            "ader_partition", "ader_halo_plan", "ader_nccl_unique_id", "ader_set_profiling", "ader_kernel_stats",
             "ader_launch_count", "ader_debug_dump")
 
 
@@ -140,6 +146,14 @@ def ader_partition(cfg: AderConfig, rank: int) -> AderPartitionInfo:
     if st:
         raise AderError(st, "ader_partition rejected the configuration")
     return info
+
+
+def ader_halo_plan(cfg: AderConfig, rank: int, axis: int, side: int) -> AderHaloDesc:
+    d = AderHaloDesc()
+    st = lib().ader_halo_plan(C.byref(cfg), rank, axis, side, C.byref(d))
+    if st:
+        raise AderError(st, "ader_halo_plan rejected the arguments")
+    return d
 
 
 def ader_nccl_unique_id() -> bytes:

@@ -287,45 +287,56 @@ double face_flops(const ader_ctx* c) {
 }
 
 // ---- ghost layers ------------------------------------------------------------
+// Ghost-layer plan of (axis, side) for a rank's block (ader_halo_desc, ader.h).
+void halo_plan(int d, int H, const int n[3], const int P[3], const ader_partition_info& part, int rank,
+               const int32_t* bc, int a, int side, ader_halo_desc* o) {
+  std::memset(o, 0, sizeof(*o));
+  o->peer = -1;
+  if (a >= d) return;
+  int lo[3], hi[3];
+  for (int b = 0; b < 3; ++b) {
+    if (b >= d) { lo[b] = 0; hi[b] = 1; continue; }
+    if (b < a) { lo[b] = 0; hi[b] = P[b]; }      // processed axes: full padded extent
+    else { lo[b] = H; hi[b] = H + n[b]; }        // unprocessed axes: owned extent
+  }
+  for (int b = 0; b < 3; ++b) { o->send_lo[b] = o->recv_lo[b] = lo[b]; o->send_hi[b] = o->recv_hi[b] = hi[b]; }
+  if (side == 0) { o->recv_lo[a] = 0; o->recv_hi[a] = H; o->send_lo[a] = H; o->send_hi[a] = 2 * H; }
+  else { o->recv_lo[a] = H + n[a]; o->recv_hi[a] = 2 * H + n[a]; o->send_lo[a] = n[a]; o->send_hi[a] = n[a] + H; }
+  const int nb = part.nbr[2 * a + side];
+  if (nb >= 0 && nb != rank) { o->kind = 1; o->peer = nb; }
+  else if (nb >= 0 && bc[2 * a + side] == ADER_BC_PERIODIC) o->kind = 2;
+  else o->kind = 3;
+}
+
+Box desc_box(const int32_t* lo, const int32_t* hi) { return make_box(lo[0], hi[0], lo[1], hi[1], lo[2], hi[2]); }
+
 ader_status fill_halo(ader_ctx* c, double* u) {
   Scope sc(c, ADER_K_HALO, 0.0);
   const int H = c->H;
   for (int a = 0; a < c->d; ++a) {
-    // extents of the other axes: processed axes full, unprocessed interior
-    int lo[3], hi[3];
-    for (int b = 0; b < 3; ++b) {
-      if (b >= c->d) { lo[b] = 0; hi[b] = 1; continue; }
-      if (b < a) { lo[b] = 0; hi[b] = c->P[b]; }
-      else { lo[b] = H; hi[b] = H + c->n[b]; }
-    }
-    auto slab = [&](int a0, int a1) {
-      int l[3] = {lo[0], lo[1], lo[2]}, h[3] = {hi[0], hi[1], hi[2]};
-      l[a] = a0; h[a] = a1;
-      return make_box(l[0], h[0], l[1], h[1], l[2], h[2]);
-    };
-    const Box rlo = slab(0, H), rhi = slab(H + c->n[a], 2 * H + c->n[a]);
-    const Box slo = slab(H, 2 * H), shi = slab(c->n[a], c->n[a] + H);
-    const int nb_lo = c->part.nbr[2 * a], nb_hi = c->part.nbr[2 * a + 1];
-    const bool remote_lo = nb_lo >= 0 && nb_lo != c->cfg.rank;
-    const bool remote_hi = nb_hi >= 0 && nb_hi != c->cfg.rank;
+    ader_halo_desc dl, dh;
+    halo_plan(c->d, H, c->n, c->P, c->part, c->cfg.rank, c->cfg.bc, a, 0, &dl);
+    halo_plan(c->d, H, c->n, c->P, c->part, c->cfg.rank, c->cfg.bc, a, 1, &dh);
+    const bool remote_lo = dl.kind == 1, remote_hi = dh.kind == 1;
+    const Box rlo = desc_box(dl.recv_lo, dl.recv_hi), rhi = desc_box(dh.recv_lo, dh.recv_hi);
+    const Box slo = desc_box(dl.send_lo, dl.send_hi), shi = desc_box(dh.send_lo, dh.send_hi);
     if (remote_lo || remote_hi) {
       if (remote_lo) launch_pack(c->k, u, slo, c->sendb[2 * a]);
       if (remote_hi) launch_pack(c->k, u, shi, c->sendb[2 * a + 1]);
       const size_t cnt = (size_t)rlo.count() * c->nv;
       NK(g_nccl.GroupStart());
       // order per peer: (send low, recv high, send high, recv low) on every rank
-      if (remote_lo) NK(g_nccl.Send(c->sendb[2 * a], cnt, ncclDouble, nb_lo, c->comm, c->k.stream));
-      if (remote_hi) NK(g_nccl.Recv(c->recvb[2 * a + 1], cnt, ncclDouble, nb_hi, c->comm, c->k.stream));
-      if (remote_hi) NK(g_nccl.Send(c->sendb[2 * a + 1], cnt, ncclDouble, nb_hi, c->comm, c->k.stream));
-      if (remote_lo) NK(g_nccl.Recv(c->recvb[2 * a], cnt, ncclDouble, nb_lo, c->comm, c->k.stream));
+      if (remote_lo) NK(g_nccl.Send(c->sendb[2 * a], cnt, ncclDouble, dl.peer, c->comm, c->k.stream));
+      if (remote_hi) NK(g_nccl.Recv(c->recvb[2 * a + 1], cnt, ncclDouble, dh.peer, c->comm, c->k.stream));
+      if (remote_hi) NK(g_nccl.Send(c->sendb[2 * a + 1], cnt, ncclDouble, dh.peer, c->comm, c->k.stream));
+      if (remote_lo) NK(g_nccl.Recv(c->recvb[2 * a], cnt, ncclDouble, dl.peer, c->comm, c->k.stream));
       NK(g_nccl.GroupEnd());
       if (remote_lo) launch_unpack(c->k, u, rlo, c->recvb[2 * a]);
       if (remote_hi) launch_unpack(c->k, u, rhi, c->recvb[2 * a + 1]);
     }
     // local sides: periodic wrap onto ourselves, or transmissive copy (reading R5)
-    const bool periodic = c->cfg.bc[2 * a] == ADER_BC_PERIODIC;
-    if (!remote_lo) launch_fill_axis(c->k, u, rlo, a, (periodic && nb_lo >= 0) ? 0 : 1, H, c->n[a]);
-    if (!remote_hi) launch_fill_axis(c->k, u, rhi, a, (periodic && nb_hi >= 0) ? 0 : 1, H, c->n[a]);
+    if (!remote_lo) launch_fill_axis(c->k, u, rlo, a, dl.kind == 2 ? 0 : 1, H, c->n[a]);
+    if (!remote_hi) launch_fill_axis(c->k, u, rhi, a, dh.kind == 2 ? 0 : 1, H, c->n[a]);
   }
   return ADER_OK;
 }
@@ -506,6 +517,21 @@ ader_status ader_partition(const ader_config* cfg, int32_t rank, ader_partition_
   if (st != ADER_OK) return st;
   if (rank < 0 || rank >= cfg->world_size) return ADER_ERR_ARG;
   partition(cfg, rank, out);
+  return ADER_OK;
+}
+
+ader_status ader_halo_plan(const ader_config* cfg, int32_t rank, int32_t axis, int32_t side, ader_halo_desc* out) {
+  if (!cfg || !out || axis < 0 || axis > 2 || side < 0 || side > 1) return ADER_ERR_ARG;
+  ader_partition_info pi;
+  ader_status st = ader_partition(cfg, rank, &pi);
+  if (st != ADER_OK) return st;
+  const int H = cfg->degree + 1;
+  int n[3], P[3];
+  for (int k = 0; k < 3; ++k) {
+    n[k] = k < cfg->dim ? pi.hi[k] - pi.lo[k] : 1;
+    P[k] = k < cfg->dim ? n[k] + 2 * H : 1;
+  }
+  halo_plan(cfg->dim, H, n, P, pi, rank, cfg->bc, axis, side, out);
   return ADER_OK;
 }
 
