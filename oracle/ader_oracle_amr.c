@@ -353,7 +353,13 @@ static int advance(amr_t* A, int l, int m, double dt0) {
     for (int v = 0; v < nv; ++v) unew[(size_t)i * nv + v] = C->u[v];
     for (int dir = 0; dir < A->d; ++dir) {
       double Fm[VMAX], Fp[VMAX];
-      if (cell_face_flux(A, i, dir, 0, m, Fm) || cell_face_flux(A, i, dir, 1, m, Fp)) { free(unew); return 3; }
+      if (cell_face_flux(A, i, dir, 0, m, Fm) || cell_face_flux(A, i, dir, 1, m, Fp)) {
+        if (!A->err[0])
+          snprintf(A->err, sizeof(A->err), "inadmissible face state at level %d cell (%lld,%lld,%lld) t=%.17g", l,
+                   (long long)C->idx[0], (long long)C->idx[1], (long long)C->idx[2], A->t);
+        free(unew);
+        return 3;
+      }
       for (int v = 0; v < nv; ++v) unew[(size_t)i * nv + v] = unew[(size_t)i * nv + v] - dt / A->dx[l][dir] * (Fp[v] - Fm[v]);
     }
     A->updates[l]++;

@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "device.cuh"
 #include "launch.h"
@@ -78,7 +79,7 @@ __global__ void __launch_bounds__(256) k_weno(const double* __restrict__ src, do
 // carry the same flux, so it is evaluated once and q^1_s = w - (sum_s' T_ss') G.
 // ===========================================================================
 template <int D, int M, int SYS, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32) k_predictor(
+__global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? 4 : 2) k_predictor(
     const double* __restrict__ w, double* __restrict__ q, const Box R, const long long sy, const long long sz,
     const double dtdx0, const double dtdx1, const double dtdx2, const double gamma, const double ch,
     const double tol, const int max_sweeps, DevCounters* __restrict__ cnt, const int* __restrict__ list,
@@ -95,11 +96,9 @@ __global__ void __launch_bounds__(WARPS * 32) k_predictor(
   const bool lane_ok = node0 < NS;
   const int node = lane_ok ? node0 : NS - 1;
   double* Fs = smem + (warp * CPW + slot) * FSZ;
-  const long long rc = ((long long)blockIdx.x * WARPS + warp) * CPW + slot;
   // cells of a box (uniform grid) or of an id list (AMR level)
-  const bool cell_ok = rc < (list ? nlist : R.count());
-  const bool active = cell_ok && lane_ok;
-  const long long cell = cell_ok ? (list ? (long long)list[rc] : box_cell(R, rc, sy, sz)) : 0;
+  const long long count = list ? nlist : R.count();
+  auto cell_of = [&](long long r) -> long long { return list ? (long long)list[r] : box_cell(R, r, sy, sz); };
   int ia[3];
   ia[0] = node % N;
   ia[1] = (node / N) % N;
@@ -111,39 +110,63 @@ __global__ void __launch_bounds__(WARPS * 32) k_predictor(
 #pragma unroll
     for (int j = 0; j < N; ++j) Drow[d][j] = T.D[ia[d]][j];
 
+  // persistent warps: the warp walks cell groups with a stride of the whole
+  // grid and prefetches the next group's w while it iterates on the current one
+  const long long wstride = (long long)gridDim.x * WARPS;
+  long long wb = (long long)blockIdx.x * WARPS + warp;        // warp-uniform iteration index
+  double wn[NV];
+  {
+    const long long r0 = wb * CPW + slot;
+    const long long c0 = r0 < count ? cell_of(r0) : 0;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) wn[v] = r0 < count ? __ldg(&w[c0 * (NV * NS) + v * NS + node]) : 1.0;
+  }
+  unsigned long long acc_sweeps = 0, acc_cells = 0;
+  int acc_max = 0;
+  for (; wb * CPW < count; wb += wstride) {
+  const long long rc = wb * CPW + slot;
+  const bool cell_ok = rc < count;
+  const bool active = cell_ok && lane_ok;
+  const long long cell = cell_ok ? cell_of(rc) : 0;
   double wv[NV], qv[NV][N];
 #pragma unroll
-  for (int v = 0; v < NV; ++v) wv[v] = cell_ok ? w[cell * (NV * NS) + v * NS + node] : 1.0;
+  for (int v = 0; v < NV; ++v) wv[v] = wn[v];
+  {
+    const long long rn = (wb + wstride) * CPW + slot;
+    const long long cn = rn < count ? cell_of(rn) : 0;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) wn[v] = rn < count ? __ldg(&w[cn * (NV * NS) + v * NS + node]) : 1.0;
+  }
   bool conv = !cell_ok, bad = false;
   int nsw = 0;
-  for (int sweep = 1; sweep <= max_sweeps; ++sweep) {
-    const int NT = (sweep == 1) ? 1 : N;                      // distinct time levels of the iterate
-    if (!conv) {
+  // one Picard sweep; FIRST: the iterate is the time-constant guess (one flux level)
+  auto sweep_once = [&](auto first_tag) {
+    constexpr bool FIRST = decltype(first_tag)::value;
+    constexpr int NT = FIRST ? 1 : N;                          // distinct time levels of the iterate
+    if (!conv && lane_ok) {
       // nodal fluxes f*_dir = (dt/dx_dir) f_dir(q) (eqn.nodal.eval @ P:405-412)
 #pragma unroll
-      for (int s = 0; s < N; ++s) {
-        if (s >= NT) break;
+      for (int s = 0; s < NT; ++s) {
         double uu[NV], f[D][NV];
 #pragma unroll
-        for (int v = 0; v < NV; ++v) uu[v] = (sweep == 1) ? wv[v] : qv[v][s];
-        bad |= lane_ok && !PH::fluxes(uu, gamma, ch, f);
-        if (lane_ok) {
+        for (int v = 0; v < NV; ++v) uu[v] = FIRST ? wv[v] : qv[v][s];
+        bad |= !PH::fluxes(uu, gamma, ch, f);
 #pragma unroll
-          for (int d = 0; d < D; ++d)
+        for (int d = 0; d < D; ++d)
 #pragma unroll
-            for (int v = 0; v < NV; ++v) Fs[((d * NV + v) * N + s) * NS + node] = dtdx[d] * f[d][v];
-        }
+          for (int v = 0; v < NV; ++v) Fs[((d * NV + v) * N + s) * NS + node] = dtdx[d] * f[d][v];
       }
     }
     __syncwarp();
-    double dmax = 0.0, qmax = 0.0;
+    // convergence bookkeeping in FP32 with directed rounding: |dq| rounded up,
+    // |q| rounded down, so a passed test implies the exact FP64 test (R2)
+    float dmax = 0.f, qmax = 0.f;
     if (!conv && lane_ok) {
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
-        double Gs[N];
+        double Gs[NT];
 #pragma unroll
-        for (int s = 0; s < N; ++s) {
-          if (s >= NT) break;
+        for (int s = 0; s < NT; ++s) {
           double g = 0.0;
 #pragma unroll
           for (int d = 0; d < D; ++d) {
@@ -157,16 +180,16 @@ __global__ void __launch_bounds__(WARPS * 32) k_predictor(
 #pragma unroll
         for (int s = 0; s < N; ++s) {
           double acc;
-          if (sweep == 1) {
+          if (FIRST) {
             acc = wv[v] - T.Tsum[s] * Gs[0];
           } else {
             acc = wv[v];
 #pragma unroll
-            for (int s2 = 0; s2 < N; ++s2) acc -= T.T[s][s2] * Gs[s2];
+            for (int s2 = 0; s2 < NT; ++s2) acc -= T.T[s][s2] * Gs[s2];
           }
-          const double prev = (sweep == 1) ? wv[v] : qv[v][s];
-          dmax = fmax(dmax, fabs(acc - prev));
-          qmax = fmax(qmax, fabs(acc));
+          const double prev = FIRST ? wv[v] : qv[v][s];
+          dmax = fmaxf(dmax, __double2float_ru(fabs(acc - prev)));
+          qmax = fmaxf(qmax, __double2float_rd(fabs(acc)));
           qv[v][s] = acc;
         }
       }
@@ -174,28 +197,46 @@ __global__ void __launch_bounds__(WARPS * 32) k_predictor(
     // per-cell max over the lane group (segmented butterfly)
 #pragma unroll
     for (int o = G / 2; o > 0; o >>= 1) {
-      dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o, G));
-      qmax = fmax(qmax, __shfl_xor_sync(0xffffffffu, qmax, o, G));
+      dmax = fmaxf(dmax, __shfl_xor_sync(0xffffffffu, dmax, o, G));
+      qmax = fmaxf(qmax, __shfl_xor_sync(0xffffffffu, qmax, o, G));
     }
     if (!conv) {
-      nsw = sweep;
-      if (dmax <= tol * (1.0 + qmax)) conv = true;   // reading R2
+      ++nsw;
+      if ((double)dmax <= tol * (1.0 + (double)qmax)) conv = true;   // reading R2
     }
-    if (__all_sync(0xffffffffu, conv)) break;
+  };
+  if (max_sweeps >= 1) sweep_once(std::integral_constant<bool, true>());
+  while (nsw < max_sweeps && !__all_sync(0xffffffffu, conv)) {
     __syncwarp();
+    sweep_once(std::integral_constant<bool, false>());
   }
-  if (!active) return;
-  if (bad) record_error(cnt, 1, 1, cell);
-  else if (!conv) record_error(cnt, 2, 1, cell);
-  double* qo = q + cell * (NV * NST) + node;
+  if (active) {
+    if (bad) record_error(cnt, 1, 1, cell);
+    else if (!conv) record_error(cnt, 2, 1, cell);
+    double* qo = q + cell * (NV * NST) + node;
 #pragma unroll
-  for (int v = 0; v < NV; ++v)
+    for (int v = 0; v < NV; ++v)
 #pragma unroll
-    for (int s = 0; s < N; ++s) qo[v * NST + s * NS] = qv[v][s];
-  if (node == 0) {
-    atomicAdd(&cnt->sweeps, (unsigned long long)nsw);
-    atomicAdd(&cnt->cells, 1ull);
-    atomicMax(&cnt->sweeps_max, nsw);
+      for (int s = 0; s < N; ++s) qo[v * NST + s * NS] = qv[v][s];
+    if (node == 0) {
+      acc_sweeps += (unsigned long long)nsw;
+      acc_cells += 1ull;
+      acc_max = nsw > acc_max ? nsw : acc_max;
+    }
+  }
+  __syncwarp();
+  }
+  // one set of counter atomics per warp (same-address atomics per cell serialise in L2)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    acc_sweeps += __shfl_xor_sync(0xffffffffu, acc_sweeps, o);
+    acc_cells += __shfl_xor_sync(0xffffffffu, acc_cells, o);
+    acc_max = max(acc_max, __shfl_xor_sync(0xffffffffu, acc_max, o));
+  }
+  if (lane == 0 && acc_cells) {
+    atomicAdd(&cnt->sweeps, acc_sweeps);
+    atomicAdd(&cnt->cells, acc_cells);
+    atomicMax(&cnt->sweeps_max, acc_max);
   }
 }
 
@@ -609,7 +650,9 @@ void launch_predictor_list(const KCtx& k, const double* w, double* q, const Box&
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       attr = true;
     }
-    const unsigned g = grid_for(count, kPredWarps * CPW);
+    // persistent grid: enough CTAs for every SM at full occupancy, a few times over
+    const unsigned need = grid_for(count, kPredWarps * CPW);
+    const unsigned g = need < 148u * 16u ? need : 148u * 16u;
     count_launch(k);
     kern<<<g, kPredWarps * 32, sm, k.stream>>>(w, q, region, k.sy, k.sz, dtdx[0], dtdx[1], dtdx[2], k.gamma,
                                                 k.ch, tol, max_sweeps, cnt, list, nlist, k.tab);
