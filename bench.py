@@ -121,7 +121,8 @@ def oracle_sample(wl, edge, reps=1):
         # edge^d cells of the same problem (full LTS hierarchy, adapt included)
         n = tuple([edge] * wl.dim)
         a = O.AmrOracle(dim=wl.dim, degree=wl.degree, n=n, lo=wl.lo, hi=wl.hi, bc=wl.bc, system=wl.system,
-                        gamma=wl.gamma, ch=wl.ch, cfl=wl.cfl, lmax=wl.lmax, refine_factor=wl.refine_factor)
+                        gamma=wl.gamma, ch=wl.ch, cfl=wl.cfl, lmax=wl.lmax, refine_factor=wl.refine_factor,
+                        chi_ref=wl.chi_ref, chi_rec=wl.chi_rec)
         a.set_initial(wl.ic)
         ups, secs = 0, 0.0
         for _ in range(reps):
@@ -225,7 +226,8 @@ def main():
         nid = obj[0]
     cfg = ader.make_config(dim=wl.dim, degree=wl.degree, n0=wl.n, lo=wl.lo, hi=wl.hi, bc=wl.bc, system=wl.system,
                            gamma=wl.gamma, ch=wl.ch, cfl=wl.cfl, rank=rank, world_size=world, device=local,
-                           nccl_id=nid, lmax=wl.lmax, refine_factor=wl.refine_factor, adapt_every=1)
+                           nccl_id=nid, lmax=wl.lmax, refine_factor=wl.refine_factor, adapt_every=1,
+                           chi_ref=wl.chi_ref, chi_rec=wl.chi_rec)
     s = ader.Solver(cfg)
     stream = torch.cuda.current_stream()
     s.set_stream(stream.cuda_stream)

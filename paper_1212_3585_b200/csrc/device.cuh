@@ -7,6 +7,35 @@
 
 namespace ader {
 
+// Reciprocal and square root from the MUFU approximations refined by Newton
+// steps to ~1 ulp: the IEEE-exact div/sqrt sequences (slow-path branches
+// included) dominated the pointwise flux evaluations.  Inputs here are
+// positive, normal numbers (densities, squared sound speeds); the
+// admissibility checks run on the unmodified values.
+__device__ __forceinline__ double fast_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
+__device__ __forceinline__ double fast_sqrt(double a) {
+  if (!(a > 0.0)) return 0.0;
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
+  // Newton on 1/sqrt(a): y <- y (3 - a y^2) / 2, twice; then s = a y with one correction
+  double h = 0.5 * a;
+  y = y * fma(-h * y, y, 1.5);
+  y = y * fma(-h * y, y, 1.5);
+  double s = a * y;
+  const double r = fma(-s, s, a);
+  return fma(0.5 * y, r, s);
+}
+
 // ---------------------------------------------------------------------------
 // Physics.  Euler (eq:Euler-system @ P:838-869): nu = D+2 (rho, rho v, E) —
 // reading R7 drops the identically-zero v_z row in 2D.  GLM-MHD in Gaussian
@@ -21,7 +50,7 @@ template <int D> struct Phys<0, D> {
   __device__ __forceinline__ static bool fluxes(const double (&u)[NV], double gamma, double /*ch*/,
                                                 double (&f)[D][NV]) {
     const double rho = u[0];
-    const double ir = 1.0 / rho;
+    const double ir = fast_rcp(rho);
     double v[D], ke = 0.0;
 #pragma unroll
     for (int k = 0; k < D; ++k) { v[k] = u[1 + k] * ir; ke += v[k] * u[1 + k]; }
@@ -42,7 +71,7 @@ template <int D> struct Phys<0, D> {
   __device__ __forceinline__ static bool flux_speed(const double (&u)[NV], double gamma, double /*ch*/,
                                                     double (&f)[NV], double& s) {
     const double rho = u[0];
-    const double ir = 1.0 / rho;
+    const double ir = fast_rcp(rho);
     double v[D], ke = 0.0;
 #pragma unroll
     for (int k = 0; k < D; ++k) { v[k] = u[1 + k] * ir; ke += v[k] * u[1 + k]; }
@@ -53,19 +82,19 @@ template <int D> struct Phys<0, D> {
     f[1 + DIR] += p;
     f[D + 1] = v[DIR] * (u[D + 1] + p);
     const bool ok = rho > 0.0 && p > 0.0;
-    s = fabs(v[DIR]) + sqrt(fmax(gamma * p * ir, 0.0));
+    s = fabs(v[DIR]) + fast_sqrt(gamma * p * ir);
     return ok;
   }
   // sum_dir s_dir(u) * inv_dx[dir]  (CFL, reading R1)
   __device__ __forceinline__ static bool cfl_speed(const double (&u)[NV], double gamma, double /*ch*/,
                                                    const double (&inv_dx)[3], double& s) {
     const double rho = u[0];
-    const double ir = 1.0 / rho;
+    const double ir = fast_rcp(rho);
     double v[D], ke = 0.0;
 #pragma unroll
     for (int k = 0; k < D; ++k) { v[k] = u[1 + k] * ir; ke += v[k] * u[1 + k]; }
     const double p = (gamma - 1.0) * (u[D + 1] - 0.5 * ke);
-    const double c = sqrt(fmax(gamma * p * ir, 0.0));
+    const double c = fast_sqrt(gamma * p * ir);
     s = 0.0;
 #pragma unroll
     for (int k = 0; k < D; ++k) s += (fabs(v[k]) + c) * inv_dx[k];
@@ -87,7 +116,7 @@ template <int D> struct Phys<1, D> {
   static constexpr double k8pi = 0.039788735772973836;  // 1/(8 pi)
   __device__ __forceinline__ static bool prim(const double (&u)[NV], double gamma, double (&v)[3],
                                               double& p, double& bb, double& vb) {
-    const double ir = 1.0 / u[0];
+    const double ir = fast_rcp(u[0]);
     v[0] = u[1] * ir; v[1] = u[2] * ir; v[2] = u[3] * ir;
     const double ke = v[0] * u[1] + v[1] * u[2] + v[2] * u[3];
     bb = u[5] * u[5] + u[6] * u[6] + u[7] * u[7];
@@ -112,13 +141,13 @@ template <int D> struct Phys<1, D> {
   }
   __device__ __forceinline__ static double fast_speed(const double (&u)[NV], double gamma, double ch,
                                                       const double (&v)[3], double p, double bb, int dir) {
-    const double ir = 1.0 / u[0];
+    const double ir = fast_rcp(u[0]);
     const double a2 = gamma * p * ir;
     const double b2 = bb * k4pi * ir;
     const double bn2 = u[5 + dir] * u[5 + dir] * k4pi * ir;
     const double s = a2 + b2;
     const double disc = fmax(s * s - 4.0 * a2 * bn2, 0.0);
-    const double cf = sqrt(0.5 * (s + sqrt(disc)));
+    const double cf = fast_sqrt(0.5 * (s + fast_sqrt(disc)));
     return fmax(fabs(v[dir]) + cf, ch);
   }
   __device__ __forceinline__ static bool fluxes(const double (&u)[NV], double gamma, double ch,
@@ -201,10 +230,10 @@ __device__ __forceinline__ void weno1d(const DevTables& T, const double (&win)[2
     // omega~ = lambda_s / (sigma + 1e-14)^8 by three squarings
     double x = sig + 1e-14;
     x = x * x; x = x * x; x = x * x;
-    om[s] = T.lin[s] / x;
+    om[s] = T.lin[s] * fast_rcp(x);
     sum += om[s];
   }
-  const double isum = 1.0 / sum;
+  const double isum = fast_rcp(sum);
 #pragma unroll
   for (int p = 0; p < N; ++p) {
     double acc = 0.0;

@@ -325,63 +325,76 @@ __global__ void __launch_bounds__(WARPS * 32) k_face_flux(const double* __restri
 // chunks of YC rows, then z, then the y chunk, so that the -y and -z
 // neighbours' q (read for the same cell) were touched a few MB earlier and are
 // still in L2 (the plain x-y-z order re-reads the -z neighbour from HBM).
-// The per-face sum over quadrature points is a fixed butterfly (deterministic).
+// The D faces are evaluated together (independent dependency chains) and the
+// D*NV point sums are formed by one transpose-reduction over the lane group
+// (fixed butterfly, deterministic).
 // ---------------------------------------------------------------------------
-template <int D, int M, int SYS, int DIR, int G>
-__device__ __forceinline__ void cell_face(const double* __restrict__ q, double* __restrict__ F, long long cR,
-                                          int fc, bool fok, int lo_face, int hi_face, long long sd, long long ncell,
-                                          double gamma, double ch, int bmask, DevCounters* cnt, const DevTables& T) {
+template <int D, int M, int SYS, int DIR>
+__device__ __forceinline__ bool point_flux(const double* __restrict__ q, long long cR, long long sd, int p, bool fok,
+                                           bool tlo, bool thi, double wt, double gamma, double ch,
+                                           const DevTables& T, double* val) {
   using PH = Phys<SYS, D>;
   constexpr int NV = PH::NV, N = M + 1, NS = ipow_c(N, D), NST = NS * N;
   constexpr int NT = NS / N;
-  const int p = threadIdx.x & (G - 1);
-  double val[NV];
 #pragma unroll
   for (int v = 0; v < NV; ++v) val[v] = 0.0;
-  if (fok && p < NS) {
-    const long long cL = cR - sd;
-    const int s = p / NT, t = p - s * NT;
-    const int t1 = t % N, t2 = t / N;
-    constexpr int ax0 = (DIR == 0) ? 1 : 0;
-    constexpr int ax1 = (DIR == 2) ? 1 : 2;
-    constexpr int sn = ipow_c(N, DIR);
-    const int base = s * NS + t1 * ipow_c(N, ax0) + (D == 3 ? t2 * ipow_c(N, ax1) : 0);
-    const double* qL = q + cL * (NV * NST) + base;
-    const double* qR = q + cR * (NV * NST) + base;
-    const bool tlo = ((bmask >> (2 * DIR)) & 1) && fc == lo_face;
-    const bool thi = ((bmask >> (2 * DIR + 1)) & 1) && fc == hi_face;
-    double um[NV], up[NV];
+  if (!fok) return true;
+  const long long cL = cR - sd;
+  const int s = p / NT, t = p - s * NT;
+  const int t1 = t % N, t2 = t / N;
+  constexpr int ax0 = (DIR == 0) ? 1 : 0;
+  constexpr int ax1 = (DIR == 2) ? 1 : 2;
+  constexpr int sn = ipow_c(N, DIR);
+  const int base = s * NS + t1 * ipow_c(N, ax0) + (D == 3 ? t2 * ipow_c(N, ax1) : 0);
+  const double* qL = q + cL * (NV * NST) + base;
+  const double* qR = q + cR * (NV * NST) + base;
+  double um[NV], up[NV];
 #pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      double a = 0.0, b = 0.0;
+  for (int v = 0; v < NV; ++v) {
+    double a = 0.0, b = 0.0;
 #pragma unroll
-      for (int k = 0; k < N; ++k) {
-        if (!tlo) a += T.psi1[k] * __ldg(&qL[v * NST + k * sn]);   // q_h^- (xi = 1 of the left cell)
-        if (!thi) b += T.psi0[k] * __ldg(&qR[v * NST + k * sn]);   // q_h^+ (xi = 0 of the right cell)
-      }
-      um[v] = tlo ? b : a;   // transmissive boundary: interior trace on both sides (R5)
-      up[v] = thi ? a : b;
+    for (int k = 0; k < N; ++k) {
+      if (!tlo) a += T.psi1[k] * __ldg(&qL[v * NST + k * sn]);   // q_h^- (xi = 1 of the left cell)
+      if (!thi) b += T.psi0[k] * __ldg(&qR[v * NST + k * sn]);   // q_h^+ (xi = 0 of the right cell)
     }
-    double fL[NV], fR[NV], sL, sR;
-    bool ok = PH::template flux_speed<DIR>(um, gamma, ch, fL, sL);
-    ok &= PH::template flux_speed<DIR>(up, gamma, ch, fR, sR);
-    if (!ok) record_error(cnt, 1, 2, cR);
-    const double smax = fmax(sL, sR);   // reading R4
-    double wt = T.w[s] * T.w[t1];
-    if (D == 3) wt *= T.w[t2];
-#pragma unroll
-    for (int v = 0; v < NV; ++v) val[v] = wt * (0.5 * (fL[v] + fR[v]) - 0.5 * smax * (up[v] - um[v]));   // eqn.rusanov
+    um[v] = tlo ? b : a;   // transmissive boundary: interior trace on both sides (R5)
+    up[v] = thi ? a : b;
   }
+  double fL[NV], fR[NV], sL, sR;
+  bool ok = PH::template flux_speed<DIR>(um, gamma, ch, fL, sL);
+  ok &= PH::template flux_speed<DIR>(up, gamma, ch, fR, sR);
+  const double smax = fmax(sL, sR);   // reading R4
 #pragma unroll
-  for (int o = G / 2; o > 0; o >>= 1)
-#pragma unroll
-    for (int v = 0; v < NV; ++v) val[v] += __shfl_xor_sync(0xffffffffu, val[v], o, G);
-  if (fok && p == 0) {
-    double* out = F + ((long long)DIR * ncell + cR) * NV;
-#pragma unroll
-    for (int v = 0; v < NV; ++v) out[v] = val[v];
-  }
+  for (int v = 0; v < NV; ++v) val[v] = wt * (0.5 * (fL[v] + fR[v]) - 0.5 * smax * (up[v] - um[v]));   // eqn.rusanov
+  return ok;
 }
+
+// Transpose-reduction of K values over the G lanes of a segment: after it, lane
+// l holds the segment sum of values [base, base + max(1, K/G)).
+template <int K, int O, int G, int KP>
+struct TransposeReduce {
+  __device__ __forceinline__ static void run(double (&v)[KP], int lg, int& base) {
+    if constexpr (O >= 1) {
+      const bool upper = (lg & O) != 0;
+      if constexpr (K > 1) {
+        constexpr int H = K / 2;
+#pragma unroll
+        for (int i = 0; i < H; ++i) {
+          const double send = upper ? v[i] : v[i + H];
+          const double keep = upper ? v[i + H] : v[i];
+          v[i] = keep + __shfl_xor_sync(0xffffffffu, send, O, G);
+        }
+        if (upper) base += H;
+        TransposeReduce<H, O / 2, G, KP>::run(v, lg, base);
+      } else {
+        v[0] += __shfl_xor_sync(0xffffffffu, v[0], O, G);
+        TransposeReduce<1, O / 2, G, KP>::run(v, lg, base);
+      }
+    }
+  }
+};
+
+constexpr int pow2_at_least(int x) { return x <= 1 ? 1 : 2 * pow2_at_least((x + 1) / 2); }
 
 template <int D, int M, int SYS, int WARPS, int YC>
 __global__ void __launch_bounds__(WARPS * 32) k_face_flux_cells(const double* __restrict__ q, double* __restrict__ F,
@@ -391,10 +404,13 @@ __global__ void __launch_bounds__(WARPS * 32) k_face_flux_cells(const double* __
                                                                 const double ch, const int bmask,
                                                                 DevCounters* __restrict__ cnt,
                                                                 const __grid_constant__ DevTables T) {
-  constexpr int NS = ipow_c(M + 1, D);
+  using PH = Phys<SYS, D>;
+  constexpr int NV = PH::NV, N = M + 1, NS = ipow_c(N, D), NT = NS / N;
   constexpr int G = (NS <= 8) ? 8 : (NS <= 16 ? 16 : 32);
   constexpr int CPW = 32 / G;
+  constexpr int KP = pow2_at_least(D * NV);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int p = lane & (G - 1);
   const long long r = ((long long)blockIdx.x * WARPS + warp) * CPW + lane / G;
   const int ex = E.ext[0], ez = E.ext[2];
   const long long t = r / ex;
@@ -409,9 +425,37 @@ __global__ void __launch_bounds__(WARPS * 32) k_face_flux_cells(const double* __
   const long long cR = ok ? cx + cy * sy + cz * sz : 0;
   const int zH = (D == 3) ? H : 0;
   const bool inx = cx < H + n0, iny = cy < H + n1, inz = (D == 2) || cz < zH + n2;
-  cell_face<D, M, SYS, 0, G>(q, F, cR, cx, ok && iny && inz, H, H + n0, 1, ncell, gamma, ch, bmask, cnt, T);
-  cell_face<D, M, SYS, 1, G>(q, F, cR, cy, ok && inx && inz, H, H + n1, sy, ncell, gamma, ch, bmask, cnt, T);
-  if (D == 3) cell_face<D, M, SYS, 2, G>(q, F, cR, cz, ok && inx && iny, zH, zH + n2, sz, ncell, gamma, ch, bmask, cnt, T);
+  const bool pok = p < NS;
+  bool fok[3] = {ok && iny && inz && pok, ok && inx && inz && pok, ok && inx && iny && pok};
+  // quadrature weight of this lane's point (same (s, t1, t2) decomposition on every face)
+  const int ps = pok ? p : 0;
+  const int s = ps / NT, tt = ps - (ps / NT) * NT;
+  double wt = T.w[s] * T.w[tt % N];
+  if (D == 3) wt *= T.w[tt / N];
+  double v[KP];
+#pragma unroll
+  for (int i = D * NV; i < KP; ++i) v[i] = 0.0;
+  bool good = true;
+  good &= point_flux<D, M, SYS, 0>(q, cR, 1, ps, fok[0], (bmask & 1) && cx == H, (bmask & 2) && cx == H + n0, wt,
+                                   gamma, ch, T, v);
+  good &= point_flux<D, M, SYS, 1>(q, cR, sy, ps, fok[1], (bmask & 4) && cy == H, (bmask & 8) && cy == H + n1, wt,
+                                   gamma, ch, T, v + NV);
+  if constexpr (D == 3)
+    good &= point_flux<D, M, SYS, 2>(q, cR, sz, ps, fok[2], (bmask & 16) && cz == zH, (bmask & 32) && cz == zH + n2,
+                                     wt, gamma, ch, T, v + 2 * NV);
+  if (!good) record_error(cnt, 1, 2, cR);
+  int base = 0;
+  TransposeReduce<KP, G / 2, G, KP>::run(v, p, base);
+  constexpr int KL = (KP / G) > 1 ? (KP / G) : 1;
+#pragma unroll
+  for (int i = 0; i < KL; ++i) {
+    const int idx = base + i;
+    if (idx < D * NV) {
+      const int dir = idx / NV, var = idx - dir * NV;
+      const bool face_ok = dir == 0 ? (ok && iny && inz) : (dir == 1 ? (ok && inx && inz) : (ok && inx && iny));
+      if (face_ok) F[((long long)dir * ncell + cR) * NV + var] = v[i];
+    }
+  }
 }
 
 // ===========================================================================

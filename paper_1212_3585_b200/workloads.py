@@ -172,6 +172,8 @@ class Workload:
     ch: float = 0.0
     refine_factor: int = 3
     lmax: int = 0
+    chi_ref: float = 0.2     # refinement threshold (P:630-631 range 0.2-0.25)
+    chi_rec: float = 0.1     # recoarsening threshold (P:631-632 range 0.05-0.15)
     note: str = ""
     extra: dict = field(default_factory=dict)
 
@@ -189,8 +191,12 @@ def config(name: str, n=None) -> Workload:
                         (P,) * 6, 1.4, 0.9, 10.0, ic=isentropic_vortex())
     if name == "c3":
         nn = n or 100
+        # chi thresholds 0.1 / 0.05 (reading R14): with 0.2 a level-1 cell cut by the
+        # initial jump stays unrefined and the projection of its polynomial into
+        # the level-2 ghost cells is inadmissible at t = 0 (oracle and GPU alike)
         return Workload("c3_explosion2d_amr", 2, 0, 2, (nn, nn), (-1.0, -1.0), (1.0, 1.0),
-                        (T,) * 6, 1.4, 0.45, 0.25, ic=explosion(2), refine_factor=3, lmax=2)
+                        (T,) * 6, 1.4, 0.45, 0.25, ic=explosion(2), refine_factor=3, lmax=2,
+                        chi_ref=0.1, chi_rec=0.05)
     if name == "c4":
         nn = n or 256
         # CFL 0.3: at 0.9, 0.6 and 0.5 both the oracle and the CUDA path

@@ -89,7 +89,7 @@ def test_c3_full_size_first_macro_steps():
     # the oracle's full run to t=0.25 takes hours, so parity covers 2 macro steps)
     wl = W.config("c3")
     g, o = pair(dim=2, degree=2, n=wl.n, lo=wl.lo, hi=wl.hi, bc=wl.bc, ic=wl.ic, lmax=wl.lmax, cfl=wl.cfl,
-                refine_factor=wl.refine_factor)
+                refine_factor=wl.refine_factor, chi_ref=wl.chi_ref, chi_rec=wl.chi_rec)
     compare(g, o, 1e-14)
     for _ in range(2):
         rg = g.step(1e300, 1)
