@@ -54,6 +54,12 @@ struct AmrState {
   std::vector<double> chi;
   long long updates[kAmrMaxLevels]{};
   std::string err;
+  // incremental uploads: the tree as the device last saw it, staging buffers
+  std::vector<HCell> mirror;
+  char* dscratch = nullptr;
+  size_t dscratch_cap = 0;
+  char* hstage = nullptr;
+  size_t hstage_cap = 0;
 };
 
 namespace {
@@ -254,53 +260,100 @@ ader_status ensure_capacity(AmrState* A, std::string& err) {
   return ADER_OK;
 }
 
+// Stage host data through one pinned buffer into one device scratch buffer
+// (bump allocation per upload batch); returns device pointers.
+struct Uploader {
+  AmrState* A;
+  std::vector<std::pair<const void*, size_t>> parts;
+  size_t add(const void* p, size_t bytes) {
+    size_t off = 0;
+    for (auto& q : parts) off += (q.second + 255) / 256 * 256;
+    parts.push_back({p, bytes});
+    return off;
+  }
+  ader_status run(std::string& err) {
+    size_t tot = 0;
+    for (auto& q : parts) tot += (q.second + 255) / 256 * 256;
+    if (tot == 0) return ADER_OK;
+    cudaStream_t sm = A->k->stream;
+    if (tot > A->dscratch_cap) {
+      if (A->dscratch) { cudaStreamSynchronize(sm); cudaFree(A->dscratch); }
+      A->dscratch_cap = tot * 3 / 2 + (1 << 20);
+      ACK(cudaMalloc(&A->dscratch, A->dscratch_cap));
+    }
+    if (tot > A->hstage_cap) {
+      if (A->hstage) { cudaStreamSynchronize(sm); cudaFreeHost(A->hstage); }
+      A->hstage_cap = tot * 3 / 2 + (1 << 20);
+      ACK(cudaMallocHost(&A->hstage, A->hstage_cap));
+    }
+    ACK(cudaStreamSynchronize(sm));   // previous use of the staging buffer finished
+    size_t off = 0;
+    for (auto& q : parts) {
+      if (q.second) std::memcpy(A->hstage + off, q.first, q.second);
+      off += (q.second + 255) / 256 * 256;
+    }
+    ACK(cudaMemcpyAsync(A->dscratch, A->hstage, tot, cudaMemcpyHostToDevice, sm));
+    return ADER_OK;
+  }
+};
+
+// Push the host tree to the device: only the ids whose links or status changed
+// since the last upload (plus the map entries they occupy), and the per-level
+// id lists.
 ader_status upload_topology(AmrState* A, std::string& err) {
   ader_status s = ensure_capacity(A, err);
   if (s != ADER_OK) return s;
   const int nu = (int)A->cells.size();
-  std::vector<int> lv(nu), st(nu), mo(nu), ch(nu);
-  std::vector<long long> ix((size_t)nu * 3);
+  if ((int)A->mirror.size() < nu) A->mirror.resize(nu);
+  std::vector<long long> meta, clears, sets;
+  for (int i = 0; i < nu; ++i) {
+    const HCell& C = A->cells[i];
+    HCell& P = A->mirror[i];
+    const bool same_pos = C.alive == P.alive && C.level == P.level && C.idx[0] == P.idx[0] && C.idx[1] == P.idx[1] &&
+                          C.idx[2] == P.idx[2];
+    const bool same = same_pos && C.status == P.status && C.mother == P.mother && C.child == P.child;
+    if (same && (C.alive || !P.alive)) continue;
+    const long long m[8] = {i, C.level, C.alive ? C.status : 9, C.mother, C.child, C.idx[0], C.idx[1], C.idx[2]};
+    meta.insert(meta.end(), m, m + 8);
+    if (P.alive && (!C.alive || !same_pos)) { clears.push_back(P.level); clears.push_back(lin(A, P.level, P.idx)); clears.push_back(-1); }
+    if (C.alive && (!P.alive || !same_pos)) { sets.push_back(C.level); sets.push_back(lin(A, C.level, C.idx)); sets.push_back(i); }
+    P = C;
+  }
   for (int l = 0; l <= A->lmax; ++l) { A->lact[l].clear(); A->lvch[l].clear(); A->lvmo[l].clear(); }
   A->lall.clear();
   for (int i = 0; i < nu; ++i) {
     const HCell& C = A->cells[i];
-    lv[i] = C.level; st[i] = C.alive ? C.status : 9; mo[i] = C.mother; ch[i] = C.child;
-    for (int k = 0; k < 3; ++k) ix[(size_t)i * 3 + k] = C.idx[k];
+    if (!C.alive) continue;
+    if (C.status == 0) A->lact[C.level].push_back(i);
+    else if (C.status == 1) A->lvch[C.level].push_back(i);
+    else A->lvmo[C.level].push_back(i);
   }
-  // lists in (level, z, y, x) order (deterministic)
-  for (int l = 0; l <= A->lmax; ++l)
-    for (int id : A->hmap[l]) {
-      if (id < 0) continue;
-      const int s2 = A->cells[id].status;
-      if (s2 == 0) { A->lact[l].push_back(id); A->lall.push_back(id); }
-      else if (s2 == 1) A->lvch[l].push_back(id);
-      else A->lvmo[l].push_back(id);
-    }
-  cudaStream_t sm = A->k->stream;
-  AmrDevView& V = A->V;
-  ACK(cudaMemcpyAsync(V.level, lv.data(), sizeof(int) * nu, cudaMemcpyHostToDevice, sm));
-  ACK(cudaMemcpyAsync(V.status, st.data(), sizeof(int) * nu, cudaMemcpyHostToDevice, sm));
-  ACK(cudaMemcpyAsync(V.mother, mo.data(), sizeof(int) * nu, cudaMemcpyHostToDevice, sm));
-  ACK(cudaMemcpyAsync(V.child, ch.data(), sizeof(int) * nu, cudaMemcpyHostToDevice, sm));
-  ACK(cudaMemcpyAsync(V.idx, ix.data(), sizeof(long long) * 3 * nu, cudaMemcpyHostToDevice, sm));
-  for (int l = 0; l <= A->lmax; ++l)
-    ACK(cudaMemcpyAsync(A->dmap[l], A->hmap[l].data(), sizeof(int) * A->hmap[l].size(), cudaMemcpyHostToDevice, sm));
-  // concatenated lists
   std::vector<int> all;
   for (int l = 0; l <= A->lmax; ++l) {
     A->oact[l] = (long long)all.size(); all.insert(all.end(), A->lact[l].begin(), A->lact[l].end());
     A->ovch[l] = (long long)all.size(); all.insert(all.end(), A->lvch[l].begin(), A->lvch[l].end());
     A->ovmo[l] = (long long)all.size(); all.insert(all.end(), A->lvmo[l].begin(), A->lvmo[l].end());
+    A->lall.insert(A->lall.end(), A->lact[l].begin(), A->lact[l].end());
   }
   A->oall = (long long)all.size();
   all.insert(all.end(), A->lall.begin(), A->lall.end());
+  cudaStream_t sm = A->k->stream;
   if ((long long)all.size() > A->dlist_cap) {
     if (A->dlist) { cudaStreamSynchronize(sm); cudaFree(A->dlist); }
     A->dlist_cap = (long long)all.size() * 3 / 2 + 1024;
     ACK(cudaMalloc(&A->dlist, sizeof(int) * A->dlist_cap));
   }
-  ACK(cudaMemcpyAsync(A->dlist, all.data(), sizeof(int) * all.size(), cudaMemcpyHostToDevice, sm));
-  ACK(cudaStreamSynchronize(sm));   // host vectors go out of scope
+  Uploader up{A, {}};
+  const size_t om = up.add(meta.data(), meta.size() * sizeof(long long));
+  const size_t oc = up.add(clears.data(), clears.size() * sizeof(long long));
+  const size_t os = up.add(sets.data(), sets.size() * sizeof(long long));
+  const size_t ol = up.add(all.data(), all.size() * sizeof(int));
+  s = up.run(err);
+  if (s != ADER_OK) return s;
+  amr_launch_meta_scatter(*A->k, A->V, (const long long*)(A->dscratch + om), (int)(meta.size() / 8));
+  amr_launch_map_set(*A->k, A->V, (const long long*)(A->dscratch + oc), (int)(clears.size() / 3));
+  amr_launch_map_set(*A->k, A->V, (const long long*)(A->dscratch + os), (int)(sets.size() / 3));
+  ACK(cudaMemcpyAsync(A->dlist, A->dscratch + ol, sizeof(int) * all.size(), cudaMemcpyDeviceToDevice, sm));
   return ADER_OK;
 }
 
@@ -372,20 +425,15 @@ ader_status run_inits(AmrState* A, std::string& err) {
     else ic.push_back(z.cell);
   }
   A->inits.clear();
-  cudaStream_t sm = A->k->stream;
-  int* dp = nullptr;
-  const size_t tot = pw.size() + pp.size();
-  if (tot) {
-    ACK(cudaMalloc(&dp, sizeof(int) * tot));
-    if (!pw.empty()) ACK(cudaMemcpyAsync(dp, pw.data(), sizeof(int) * pw.size(), cudaMemcpyHostToDevice, sm));
-    if (!pp.empty()) ACK(cudaMemcpyAsync(dp + pw.size(), pp.data(), sizeof(int) * pp.size(), cudaMemcpyHostToDevice, sm));
-    amr_launch_init_from_weno(*A->k, A->V, A->st, dp, (int)(pw.size() / 2));
-    double pt[4];
-    psi_at(A, 1.0, pt);
-    amr_launch_init_from_pred(*A->k, A->V, A->st, dp + pw.size(), (int)(pp.size() / 2), pt);
-    ACK(cudaStreamSynchronize(sm));
-    cudaFree(dp);
-  }
+  Uploader up{A, {}};
+  const size_t ow = up.add(pw.data(), pw.size() * sizeof(int));
+  const size_t op = up.add(pp.data(), pp.size() * sizeof(int));
+  ader_status s = up.run(err);
+  if (s != ADER_OK) return s;
+  amr_launch_init_from_weno(*A->k, A->V, A->st, (const int*)(A->dscratch + ow), (int)(pw.size() / 2));
+  double pt[4];
+  psi_at(A, 1.0, pt);
+  amr_launch_init_from_pred(*A->k, A->V, A->st, (const int*)(A->dscratch + op), (int)(pp.size() / 2), pt);
   std::sort(ic.begin(), ic.end());
   return ic_cells(A, ic, err);
 }
@@ -498,7 +546,9 @@ ader_status adapt(AmrState* A, bool t0, std::string& err) {
       }
       cand[i] = ok;
     }
-    for (;;) {
+    bool any_cand = false;
+    for (int i = 0; i < nu2 && !any_cand; ++i) any_cand = cand[i];
+    while (any_cand) {
       // tentative simultaneous rule 7, then closure; reverted candidates retry
       const std::vector<HCell> snap_cells = A->cells;
       const std::vector<std::vector<int>> snap_map = A->hmap;
@@ -540,21 +590,19 @@ ader_status adapt(AmrState* A, bool t0, std::string& err) {
   // device: averages of coarsened mothers from their (old) children first
   if (!coarsened.empty()) {
     // children ids are still valid on the device (freed blocks are reused only later)
-    int* dl = nullptr;
-    ACK(cudaMalloc(&dl, sizeof(int) * coarsened.size()));
-    ACK(cudaMemcpyAsync(dl, coarsened.data(), sizeof(int) * coarsened.size(), cudaMemcpyHostToDevice, sm));
+    Uploader up{A, {}};
+    const size_t oc = up.add(coarsened.data(), sizeof(int) * coarsened.size());
+    ader_status s0 = up.run(err);
+    if (s0 != ADER_OK) return s0;
     // the device child links of these mothers are the pre-adapt ones
-    amr_launch_average(*A->k, A->V, dl, (int)coarsened.size());
-    ACK(cudaStreamSynchronize(sm));
-    cudaFree(dl);
+    amr_launch_average(*A->k, A->V, (const int*)(A->dscratch + oc), (int)coarsened.size());
   }
   ader_status s = upload_topology(A, err);
   if (s != ADER_OK) return s;
   s = run_inits(A, err);
   if (s != ADER_OK) return s;
   // clear the flux memory of every virtual child (synchronized time: all consumed)
-  for (int l = 1; l <= A->lmax; ++l)
-    for (int id : A->lvch[l]) ACK(cudaMemsetAsync(A->V.mem + (size_t)id * 6 * A->nv, 0, sizeof(double) * 6 * A->nv, sm));
+  for (int l = 1; l <= A->lmax; ++l) amr_launch_zero_mem(*A->k, A->V, L_vch(A, l), (int)A->lvch[l].size());
   for (int b : freed) A->free_blocks.push_back(b);
   for (auto& c : A->cells) c.isnew = false;
   ACK(cudaStreamSynchronize(sm));
@@ -591,6 +639,7 @@ AmrState* amr_create(const ader_config* cfg, KCtx* k, DevCounters* cnt, DevCount
     }
     A->hmap[l].assign((size_t)s, -1);
     if (cudaMalloc(&A->dmap[l], sizeof(int) * s) != cudaSuccess) { err = "cudaMalloc map"; delete A; return nullptr; }
+    cudaMemset(A->dmap[l], 0xff, sizeof(int) * s);   // -1 everywhere
     A->V.map[l] = A->dmap[l];
     for (int i = 0; i < 3; ++i) A->V.n[l][i] = A->n[l][i];
   }
@@ -617,6 +666,8 @@ void amr_destroy(AmrState* A) {
     if (p) cudaFree(p);
   for (int l = 0; l < kAmrMaxLevels; ++l)
     if (A->dmap[l]) cudaFree(A->dmap[l]);
+  if (A->dscratch) cudaFree(A->dscratch);
+  if (A->hstage) cudaFreeHost(A->hstage);
   delete A;
 }
 

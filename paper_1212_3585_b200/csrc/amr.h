@@ -58,6 +58,9 @@ double amr_time(const AmrState* a);
 int64_t amr_num_active(const AmrState* a);
 
 // --- kernels (amr_kernels.cu) ------------------------------------------------
+void amr_launch_meta_scatter(const KCtx& k, const AmrDevView& v, const long long* meta, int n);
+void amr_launch_map_set(const KCtx& k, const AmrDevView& v, const long long* ch, int n);
+void amr_launch_zero_mem(const KCtx& k, const AmrDevView& v, const int* list, int n);
 void amr_launch_average(const KCtx& k, const AmrDevView& v, const int* list, int n);
 void amr_launch_project(const KCtx& k, const AmrDevView& v, const SubTables& st, const int* list, int n,
                         const double* psi_tau);

@@ -431,6 +431,38 @@ __global__ void k_amr_ic(AmrDevView V, const int* __restrict__ list, int n, cons
   for (int v = 0; v < NV; ++v) V.u[(long long)c * NV + v] = acc[v];
 }
 
+// ---------------------------------------------------------------------------
+// incremental topology updates (one launch each, instead of full re-uploads)
+// meta[i] = {id, level, status, mother, child, idx0, idx1, idx2} (long long)
+__global__ void k_amr_meta_scatter(AmrDevView V, const long long* __restrict__ meta, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const long long* m = meta + (long long)i * 8;
+  const int id = (int)m[0];
+  V.level[id] = (int)m[1];
+  V.status[id] = (int)m[2];
+  V.mother[id] = (int)m[3];
+  V.child[id] = (int)m[4];
+  V.idx[(long long)id * 3] = m[5];
+  V.idx[(long long)id * 3 + 1] = m[6];
+  V.idx[(long long)id * 3 + 2] = m[7];
+}
+
+// ch[i] = {level, linear index, value}
+__global__ void k_amr_map_set(AmrDevView V, const long long* __restrict__ ch, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const long long* c = ch + (long long)i * 3;
+  const_cast<int*>(V.map[c[0]])[c[1]] = (int)c[2];
+}
+
+__global__ void k_amr_zero_mem(AmrDevView V, const int* __restrict__ list, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n * 6 * V.NV) return;
+  const int c = list[i / (6 * V.NV)], j = i % (6 * V.NV);
+  V.mem[(long long)c * 6 * V.NV + j] = 0.0;
+}
+
 // ===========================================================================
 // launchers
 // ===========================================================================
@@ -448,6 +480,24 @@ inline void cl(const KCtx& k) { if (k.launches) ++*k.launches; }
     else if (D_ == 2 && M_ == 3 && SYS_ == 1) { constexpr int D = 2, M = 3, SYS = 1; __VA_ARGS__; } \
     else if (D_ == 3 && M_ == 2 && SYS_ == 1) { constexpr int D = 3, M = 2, SYS = 1; __VA_ARGS__; } \
   } while (0)
+
+void amr_launch_meta_scatter(const KCtx& k, const AmrDevView& v, const long long* meta, int n) {
+  if (n <= 0) return;
+  cl(k);
+  k_amr_meta_scatter<<<gsz(n, 256), 256, 0, k.stream>>>(v, meta, n);
+}
+
+void amr_launch_map_set(const KCtx& k, const AmrDevView& v, const long long* ch, int n) {
+  if (n <= 0) return;
+  cl(k);
+  k_amr_map_set<<<gsz(n, 256), 256, 0, k.stream>>>(v, ch, n);
+}
+
+void amr_launch_zero_mem(const KCtx& k, const AmrDevView& v, const int* list, int n) {
+  if (n <= 0) return;
+  cl(k);
+  k_amr_zero_mem<<<gsz((long long)n * 6 * v.NV, 256), 256, 0, k.stream>>>(v, list, n);
+}
 
 void amr_launch_average(const KCtx& k, const AmrDevView& v, const int* list, int n) {
   if (n <= 0) return;
