@@ -191,11 +191,12 @@ def run_reference(args, wl):
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
-def load_traffic(wl):
+def load_traffic(wl, kernel="stdg_predictor"):
+    """dram read+write bytes per launch of `kernel` from the committed ncu capture."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         d = json.load(open(path))
-        return d.get(wl.name, {}).get("stdg_predictor_dram_bytes_per_launch")
+        return d.get(wl.name, {}).get(f"{kernel}_dram_bytes_per_launch")
     except Exception:
         return None
 
@@ -317,6 +318,54 @@ def main():
         pred_flops = kfl[ader.K_PRED] / max(1, kl[ader.K_PRED])
         achieved = pred_flops / (pred_ms_avg / 1e3) / 1e12
         peak = fp64_peak_tflops(1965.0)
+        # algorithmic bytes of one predictor launch: read w, write q of every predicted cell
+        N = wl.degree + 1
+        nvv = 9 if wl.system == 1 else wl.dim + 2
+        cells_per_launch = rep.pred_cells / max(1, kl[ader.K_PRED])
+        pred_bytes = cells_per_launch * nvv * (N ** wl.dim + N ** (wl.dim + 1)) * 8
+        hbm_peak = 6449.1
+        try:
+            hbm_peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+        except Exception:
+            pass
+        ai = pred_flops / max(1.0, pred_bytes)                       # flop / byte
+        ridge = peak * 1e12 / (hbm_peak * 1e9)
+        gbs = pred_bytes / (pred_ms_avg / 1e3) / 1e9
+        if ai >= ridge:
+            roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                    "peak_note": "FP64 FMA pipe: 148 SM x 64 lanes x 2 x 1.965 GHz (derived, DESIGN.md)",
+                    "achieved_note": "algorithmic FP64 flops of the Picard sweeps actually run / CUDA-event time"}
+        else:
+            roof = {"bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak,
+                    "peak_note": "measured copy bandwidth, MEASURED_PEAKS.json hbm_gbs (of measured)",
+                    "achieved_note": "algorithmic bytes (w read + q written per predicted cell) / CUDA-event time"}
+        roof.update({"kernel": "stdg_predictor", "traffic": load_traffic(wl, "stdg_predictor"),
+                     "arith_intensity_flop_per_byte": ai,
+                     "ridge_flop_per_byte": ridge, "alu_tflops": achieved, "alu_frac": achieved / peak,
+                     "hbm_gbs": gbs, "hbm_frac": gbs / hbm_peak})
+        # face flux (uniform grids): algorithmic bytes = every q read once + F written
+        roof_flux = None
+        if wl.lmax == 0 and kl[ader.K_FLUX]:
+            fl_ms = kms[ader.K_FLUX] / kl[ader.K_FLUX]
+            fl_flops = kfl[ader.K_FLUX] / kl[ader.K_FLUX]
+            nb = [int(k) for k in wl.n]
+            if world > 1:
+                nb = [int(np.ceil(k / p)) for k, p in zip(nb, [2, 2, 2][:wl.dim])]
+            ext = int(np.prod([k + 1 for k in nb]))
+            fl_bytes = ext * nvv * (N ** (wl.dim + 1) + wl.dim) * 8
+            f_gbs = fl_bytes / (fl_ms / 1e3) / 1e9
+            f_tf = fl_flops / (fl_ms / 1e3) / 1e12
+            f_ai = fl_flops / fl_bytes
+            roof_flux = {"kernel": "face_flux_rusanov", "bound": "alu" if f_ai >= ridge else "hbm",
+                         "achieved": f_tf if f_ai >= ridge else f_gbs, "peak": peak if f_ai >= ridge else hbm_peak,
+                         "unit": "TFLOP/s" if f_ai >= ridge else "GB/s",
+                         "frac": (f_tf / peak) if f_ai >= ridge else (f_gbs / hbm_peak),
+                         "traffic": load_traffic(wl, "face_flux_rusanov"), "arith_intensity_flop_per_byte": f_ai,
+                         "alu_tflops": f_tf, "hbm_gbs": f_gbs,
+                         "achieved_note": "algorithmic bytes (each q read once, F written) / CUDA-event time"}
+        dominant = roof
+        if roof_flux is not None and kms[ader.K_FLUX] > kms[ader.K_PRED]:
+            dominant = roof_flux
         step_ms = ms_max / args.steps
         share = {ader.KERNEL_NAMES[i]: round(kms[i] / max(1e-9, ms) , 4) for i in range(ader.K_COUNT)}
         line = {
@@ -327,10 +376,8 @@ def main():
                        "cells": list(wl.n), "system": "euler" if wl.system == 0 else "mhd_glm",
                        "flux": "rusanov", "cfl": wl.cfl, "ic": "explosion r<0.5" if "explosion" in wl.name else wl.name,
                        "parallelism": f"level-0 blocks x{world}", "l2": "inputs larger than L2 (~90 GB working set)"},
-            "roofline": {"bound": "alu", "kernel": "stdg_predictor", "achieved": achieved, "peak": peak,
-                         "unit": "TFLOP/s", "frac": achieved / peak, "traffic": load_traffic(wl),
-                         "peak_note": "FP64 FMA pipe: 148 SM x 64 lanes x 2 x 1.965 GHz (derived, DESIGN.md)",
-                         "achieved_note": "algorithmic FP64 flops of the Picard sweeps actually run / CUDA-event time"},
+            "roofline": dominant,
+            "roofline_kernels": [r for r in (roof, roof_flux) if r is not None],
             "kernel_share_of_step": share,
             "pred_sweeps_mean": rep.pred_sweeps_total / max(1, rep.pred_cells),
             "clocks": clocks,

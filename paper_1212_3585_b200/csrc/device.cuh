@@ -203,6 +203,16 @@ template <int M>
 __device__ __forceinline__ void weno1d(const DevTables& T, const double (&win)[2 * M + 1], double (&out)[M + 1]) {
   constexpr int N = M + 1;
   constexpr int NS = Stencils<M>::NS;
+  // constant data: every stencil polynomial is that constant (rec reproduces
+  // constants), so the WENO polynomial is exactly the constant
+  bool flat = true;
+#pragma unroll
+  for (int o = 1; o < 2 * M + 1; ++o) flat &= win[o] == win[0];
+  if (flat) {
+#pragma unroll
+    for (int p = 0; p < N; ++p) out[p] = win[0];
+    return;
+  }
   double ws[NS][N], om[NS];
   double sum = 0.0;
 #pragma unroll

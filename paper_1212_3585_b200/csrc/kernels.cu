@@ -89,7 +89,12 @@ __global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? 4 : 2) k_predictor(
   constexpr int G = (NS <= 8) ? 8 : (NS <= 16 ? 16 : 32);   // lanes per cell
   constexpr int CPW = 32 / G;
   static_assert(NS <= 32, "one cell must fit in a warp");
-  constexpr int FSZ = D * NV * N * NS + 8;                   // +8: bank offset between cells
+  // shared-memory layout of f*_d: lines along axis d stored contiguously (axis d
+  // fastest, padded to LP = 4 doubles), so the D_d contraction reads a line
+  // with two 16-byte loads: Fs[((d*NV + v)*N + s)*NL + line_d][pos_d]
+  constexpr int LP = 4, NL = NS / N;
+  static_assert(N <= LP, "line padding");
+  constexpr int FSZ = D * NV * N * NL * LP + 8;              // +8: bank offset between cells
   extern __shared__ double smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int slot = lane / G, node0 = lane - slot * G;
@@ -103,6 +108,11 @@ __global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? 4 : 2) k_predictor(
   ia[0] = node % N;
   ia[1] = (node / N) % N;
   ia[2] = node / (N * N);
+  // index of the node's line along each axis (the other two coordinates)
+  int line[3];
+  line[0] = ia[1] + N * ia[2];
+  line[1] = ia[0] + N * ia[2];
+  line[2] = ia[0] + N * ia[1];
   const double dtdx[3] = {dtdx0, dtdx1, dtdx2};
   double Drow[D][N];                                          // D[ia_d][j] (lane-dependent rows)
 #pragma unroll
@@ -154,7 +164,7 @@ __global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? 4 : 2) k_predictor(
 #pragma unroll
         for (int d = 0; d < D; ++d)
 #pragma unroll
-          for (int v = 0; v < NV; ++v) Fs[((d * NV + v) * N + s) * NS + node] = dtdx[d] * f[d][v];
+          for (int v = 0; v < NV; ++v) Fs[(((d * NV + v) * N + s) * NL + line[d]) * LP + ia[d]] = dtdx[d] * f[d][v];
       }
     }
     __syncwarp();
@@ -170,10 +180,12 @@ __global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? 4 : 2) k_predictor(
           double g = 0.0;
 #pragma unroll
           for (int d = 0; d < D; ++d) {
-            const int sd = (d == 0) ? 1 : (d == 1 ? N : N * N);
-            const double* fb = Fs + ((d * NV + v) * N + s) * NS + node - ia[d] * sd;
-#pragma unroll
-            for (int j = 0; j < N; ++j) g += Drow[d][j] * fb[j * sd];
+            const double2* fb = reinterpret_cast<const double2*>(Fs + (((d * NV + v) * N + s) * NL + line[d]) * LP);
+            const double2 f01 = fb[0], f23 = fb[1];
+            g += Drow[d][0] * f01.x;
+            g += Drow[d][1] * f01.y;
+            g += Drow[d][2] * f23.x;
+            if (N == 4) g += Drow[d][N - 1] * f23.y;
           }
           Gs[s] = g;
         }
@@ -359,6 +371,19 @@ __device__ __forceinline__ bool point_flux(const double* __restrict__ q, long lo
     }
     um[v] = tlo ? b : a;   // transmissive boundary: interior trace on both sides (R5)
     up[v] = thi ? a : b;
+  }
+  // equal traces (e.g. inside a constant region): eqn.rusanov reduces exactly
+  // to f(q) — 0.5 (f + f) = f and the dissipation term is 0 — so one flux
+  // evaluation gives the bitwise-identical result
+  bool same = true;
+#pragma unroll
+  for (int v = 0; v < NV; ++v) same &= um[v] == up[v];
+  if (same) {
+    double f[NV], s0;
+    const bool ok = PH::template flux_speed<DIR>(um, gamma, ch, f, s0);
+#pragma unroll
+    for (int v = 0; v < NV; ++v) val[v] = wt * f[v];
+    return ok;
   }
   double fL[NV], fR[NV], sL, sR;
   bool ok = PH::template flux_speed<DIR>(um, gamma, ch, fL, sL);
@@ -630,7 +655,7 @@ template <int D, int M, int SYS>
 size_t pred_smem() {
   constexpr int NV = Phys<SYS, D>::NV, N = M + 1, NS = ipow_c(N, D);
   constexpr int G = (NS <= 8) ? 8 : (NS <= 16 ? 16 : 32), CPW = 32 / G;
-  return sizeof(double) * ((size_t)kPredWarps * CPW * (D * NV * N * NS + 8));
+  return sizeof(double) * ((size_t)kPredWarps * CPW * (D * NV * N * (NS / N) * 4 + 8));
 }
 template <int D, int M, int SYS>
 size_t flux_smem() {
