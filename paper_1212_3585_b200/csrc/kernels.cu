@@ -92,8 +92,10 @@ __global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? 4 : 2) k_predictor(
   // shared-memory layout of f*_d: lines along axis d stored contiguously (axis d
   // fastest, padded to LP = 4 doubles), so the D_d contraction reads a line
   // with two 16-byte loads: Fs[((d*NV + v)*N + s)*NL + line_d][pos_d]
-  constexpr int LP = 4, NL = NS / N;
-  static_assert(N <= LP, "line padding");
+  // (used for N = 4; for N = 3 the padding costs occupancy and bank
+  // conflicts, and the natural node-major layout is kept)
+  constexpr bool LINES = (N == 4);
+  constexpr int LP = LINES ? 4 : N, NL = NS / N;
   constexpr int FSZ = D * NV * N * NL * LP + 8;              // +8: bank offset between cells
   extern __shared__ double smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -164,7 +166,10 @@ __global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? 4 : 2) k_predictor(
 #pragma unroll
         for (int d = 0; d < D; ++d)
 #pragma unroll
-          for (int v = 0; v < NV; ++v) Fs[(((d * NV + v) * N + s) * NL + line[d]) * LP + ia[d]] = dtdx[d] * f[d][v];
+          for (int v = 0; v < NV; ++v) {
+            if constexpr (LINES) Fs[(((d * NV + v) * N + s) * NL + line[d]) * LP + ia[d]] = dtdx[d] * f[d][v];
+            else Fs[((d * NV + v) * N + s) * NS + node] = dtdx[d] * f[d][v];
+          }
       }
     }
     __syncwarp();
@@ -180,12 +185,19 @@ __global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? 4 : 2) k_predictor(
           double g = 0.0;
 #pragma unroll
           for (int d = 0; d < D; ++d) {
-            const double2* fb = reinterpret_cast<const double2*>(Fs + (((d * NV + v) * N + s) * NL + line[d]) * LP);
-            const double2 f01 = fb[0], f23 = fb[1];
-            g += Drow[d][0] * f01.x;
-            g += Drow[d][1] * f01.y;
-            g += Drow[d][2] * f23.x;
-            if (N == 4) g += Drow[d][N - 1] * f23.y;
+            if constexpr (LINES) {
+              const double2* fb = reinterpret_cast<const double2*>(Fs + (((d * NV + v) * N + s) * NL + line[d]) * LP);
+              const double2 f01 = fb[0], f23 = fb[1];
+              g += Drow[d][0] * f01.x;
+              g += Drow[d][1] * f01.y;
+              g += Drow[d][2] * f23.x;
+              g += Drow[d][N - 1] * f23.y;
+            } else {
+              const int sd = (d == 0) ? 1 : (d == 1 ? N : N * N);
+              const double* fb = Fs + ((d * NV + v) * N + s) * NS + node - ia[d] * sd;
+#pragma unroll
+              for (int j = 0; j < N; ++j) g += Drow[d][j] * fb[j * sd];
+            }
           }
           Gs[s] = g;
         }
@@ -655,7 +667,8 @@ template <int D, int M, int SYS>
 size_t pred_smem() {
   constexpr int NV = Phys<SYS, D>::NV, N = M + 1, NS = ipow_c(N, D);
   constexpr int G = (NS <= 8) ? 8 : (NS <= 16 ? 16 : 32), CPW = 32 / G;
-  return sizeof(double) * ((size_t)kPredWarps * CPW * (D * NV * N * (NS / N) * 4 + 8));
+  constexpr int LP = (N == 4) ? 4 : N;
+  return sizeof(double) * ((size_t)kPredWarps * CPW * (D * NV * N * (NS / N) * LP + 8));
 }
 template <int D, int M, int SYS>
 size_t flux_smem() {

@@ -110,6 +110,20 @@ def test_c5_full_size_first_macro_step():
     compare(g, o, 1e-11)
 
 
+@pytest.mark.parametrize("name,n,t_end", [("c3", (16, 16), 0.08), ("c5", (16, 16), 0.3)])
+def test_full_time_twin(name, n, t_end):
+    # downscaled twin of the BASELINE AMR config, run to a final time with an
+    # adapt after every macro step: cell sets identical, averages within 1e-8
+    wl = W.config(name)
+    g, o = pair(dim=2, degree=wl.degree, n=n, lo=wl.lo, hi=wl.hi, bc=wl.bc, ic=wl.ic, lmax=2, system=wl.system,
+                gamma=wl.gamma, ch=wl.ch, cfl=wl.cfl, chi_ref=wl.chi_ref, chi_rec=wl.chi_rec,
+                refine_factor=wl.refine_factor)
+    rg = g.step(t_end, 10 ** 6)
+    ro = o.step(t_end, 10 ** 6)
+    assert rg.macro_steps == ro.steps and rg.cell_updates == ro.cell_updates
+    compare(g, o, 1e-8)
+
+
 def test_amr_conservation_periodic():
     g, _ = pair(dim=2, degree=2, n=(12, 12), lo=(0, 0), hi=(1, 1), bc=(0,) * 6, ic=W.random_smooth(2, seed=3585, amp=0.15),
                 lmax=1, cfl=0.45, chi_ref=0.02, chi_rec=0.01)
