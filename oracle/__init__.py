@@ -17,6 +17,7 @@ _LIB = None
 
 EULER, MHD = 0, 1
 PERIODIC, TRANSMISSIVE = 0, 1
+RUSANOV, OSHER = 0, 1
 
 IC_FN = C.CFUNCTYPE(None, C.POINTER(C.c_double), C.c_int64, C.POINTER(C.c_double), C.c_void_p)
 
@@ -31,6 +32,7 @@ class OrcConfig(C.Structure):
         ("ic_quad", C.c_int32),
         ("refine_factor", C.c_int32), ("lmax", C.c_int32),
         ("chi_ref", C.c_double), ("chi_rec", C.c_double), ("chi_eps", C.c_double),
+        ("flux", C.c_int32), ("flux_quad", C.c_int32),
     ]
 
 
@@ -87,7 +89,12 @@ def lib():
         L.orc_predict_cell.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
                                        dp, dp, C.c_double, C.c_int, dp, ip]
         L.orc_face_flux.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
-                                    C.c_int, dp, dp, dp]
+                                    C.c_int, C.c_int, C.c_int, dp, dp, dp]
+        L.orc_euler_jacobian.argtypes = [C.c_int, C.c_double, dp, C.c_int, dp]
+        L.orc_euler_abs_jacobian.argtypes = [C.c_int, C.c_double, dp, C.c_int, dp]
+        L.orc_osher.argtypes = [C.c_int, C.c_int, C.c_double, C.c_int, dp, dp, C.c_int, dp]
+        L.orc_numflux.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, C.c_int, dp, dp,
+                                  C.c_int, dp]
         L.orc_phys_flux.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, dp, C.c_int, dp]
         L.orc_max_speed.restype = C.c_double
         L.orc_max_speed.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, dp, C.c_int]
@@ -157,11 +164,11 @@ def predict_cell(d, M, system, gamma, ch, w, dtdx, tol=1e-13, max_sweeps=32):
     return rc, q, sw.value
 
 
-def face_flux(d, M, system, gamma, ch, direction, qL, qR):
+def face_flux(d, M, system, gamma, ch, direction, qL, qR, flux=RUSANOV, nq=3):
     qL = np.ascontiguousarray(qL, dtype=np.float64)
     qR = np.ascontiguousarray(qR, dtype=np.float64)
     F = np.zeros(qL.shape[0])
-    rc = lib().orc_face_flux(d, M, system, gamma, ch, direction, _p(qL), _p(qR), _p(F))
+    rc = lib().orc_face_flux(d, M, system, gamma, ch, flux, nq, direction, _p(qL), _p(qR), _p(F))
     assert rc == 0
     return F
 
@@ -188,6 +195,31 @@ def rusanov(system, dim, gamma, ch, uL, uR, direction):
     return f
 
 
+def euler_jacobian(dim, gamma, u, direction):
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    A = np.zeros((len(u), len(u)))
+    rc = lib().orc_euler_jacobian(dim, gamma, _p(u), direction, _p(A))
+    assert rc == 0
+    return A
+
+
+def euler_abs_jacobian(dim, gamma, u, direction):
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    A = np.zeros((len(u), len(u)))
+    rc = lib().orc_euler_abs_jacobian(dim, gamma, _p(u), direction, _p(A))
+    assert rc == 0
+    return A
+
+
+def osher(dim, gamma, uL, uR, direction, nq=3):
+    uL = np.ascontiguousarray(uL, dtype=np.float64)
+    uR = np.ascontiguousarray(uR, dtype=np.float64)
+    f = np.zeros(len(uL))
+    rc = lib().orc_osher(EULER, dim, gamma, nq, _p(uL), _p(uR), direction, _p(f))
+    assert rc == 0, rc
+    return f
+
+
 def prim_to_cons(system, dim, gamma, prim):
     prim = np.zeros(9) + np.asarray(list(prim) + [0.0] * (9 - len(prim)), dtype=np.float64)
     u = np.zeros(nvar(system, dim))
@@ -199,7 +231,7 @@ class Oracle:
     """Uniform-grid oracle run (level 0 only)."""
 
     def __init__(self, *, dim, system=EULER, degree, n, lo, hi, bc, gamma=1.4, ch=0.0,
-                 cfl=0.9, pred_tol=1e-13, pred_max_sweeps=32, ic_quad=0):
+                 cfl=0.9, pred_tol=1e-13, pred_max_sweeps=32, ic_quad=0, flux=RUSANOV, flux_quad=3):
         cfg = OrcConfig()
         cfg.dim, cfg.system, cfg.degree = dim, system, degree
         n = list(n) + [1] * (3 - len(n))
@@ -212,6 +244,7 @@ class Oracle:
             cfg.bc[k] = bc[k]
         cfg.gamma, cfg.ch, cfg.cfl = gamma, ch, cfl
         cfg.pred_tol, cfg.pred_max_sweeps, cfg.ic_quad = pred_tol, pred_max_sweeps, ic_quad
+        cfg.flux, cfg.flux_quad = flux, flux_quad
         self.cfg = cfg
         self.dim, self.degree, self.system = dim, degree, system
         self.n = n[:dim]
@@ -350,7 +383,7 @@ class AmrOracle:
 
     def __init__(self, *, dim, degree, n, lo, hi, bc, system=EULER, gamma=1.4, ch=0.0, cfl=0.45,
                  refine_factor=3, lmax=1, chi_ref=0.2, chi_rec=0.1, chi_eps=0.01, pred_tol=1e-13,
-                 pred_max_sweeps=32, ic_quad=0):
+                 pred_max_sweeps=32, ic_quad=0, flux=RUSANOV, flux_quad=3):
         L = lib()
         vp = C.c_void_p
         L.orc_amr_create.restype = vp
@@ -384,6 +417,7 @@ class AmrOracle:
         cfg.pred_tol, cfg.pred_max_sweeps, cfg.ic_quad = pred_tol, pred_max_sweeps, ic_quad
         cfg.refine_factor, cfg.lmax = refine_factor, lmax
         cfg.chi_ref, cfg.chi_rec, cfg.chi_eps = chi_ref, chi_rec, chi_eps
+        cfg.flux, cfg.flux_quad = flux, flux_quad
         self.cfg, self.dim, self.nv = cfg, dim, nvar(system, dim)
         self.ptr = L.orc_amr_create(C.byref(cfg))
         if not self.ptr:

@@ -16,7 +16,9 @@
  *       K1, K^xi, M, F0 integrals @ P:434-449, system eqn.pde.weak4
  *       @ P:451-459, Picard iteration eqn.stdg.final @ P:463-474
  *       (S = 0: neither Euler nor GLM-MHD has a source)
- *   - space-time Gauss quadrature of the Rusanov flux
+ *   - space-time Gauss quadrature of the two-point flux
+ *       Rusanov eqn.rusanov @ P:181-185, Osher-type eqn.osher @ P:186-196
+ *       (|A| by Sylvester's formula, path by Gauss-Legendre)
  *   - one-step finite-volume update eq:finite_vol
  *   - Euler system eq:Euler-system
  *   - ideal MHD with GLM cleaning, Gaussian units
@@ -359,6 +361,101 @@ int orc_rusanov(int system, int dim, double gamma, double ch, const double* uL,
   return 0;
 }
 
+/* A = df_dir/du of eq:Euler-system differentiated by hand in the
+ * conserved variables u = (rho, m_1..m_d, E), v = m/rho,
+ * p = (gamma-1)(E - rho |v|^2/2), H = (E + p)/rho:
+ *   f_0     = m_n
+ *   f_{1+k} = m_n m_k / rho + p delta_kn
+ *   f_{1+d} = v_n (E + p)                                                   */
+int orc_euler_jacobian(int dim, double gamma, const double* u, int dir, double* A) {
+  double rho, v[3], p, B[3];
+  if (cons_to_prim(ORC_EULER, dim, gamma, u, &rho, v, &p, B)) return -1;
+  const int nv = dim + 2, n = dir;
+  const double g1 = gamma - 1.0;
+  double vv = 0.0;
+  for (int k = 0; k < dim; ++k) vv += v[k] * v[k];
+  const double H = (u[1 + dim] + p) / rho;
+  for (int i = 0; i < nv * nv; ++i) A[i] = 0.0;
+  A[0 * nv + 1 + n] = 1.0;
+  for (int k = 0; k < dim; ++k) {
+    double* row = A + (1 + k) * nv;
+    row[0] = -v[n] * v[k] + (k == n ? 0.5 * g1 * vv : 0.0);
+    for (int j = 0; j < dim; ++j)
+      row[1 + j] = (j == n ? v[k] : 0.0) + (j == k ? v[n] : 0.0) - (k == n ? g1 * v[j] : 0.0);
+    row[1 + dim] = (k == n) ? g1 : 0.0;
+  }
+  double* row = A + (1 + dim) * nv;
+  row[0] = v[n] * (0.5 * g1 * vv - H);
+  for (int j = 0; j < dim; ++j) row[1 + j] = (j == n ? H : 0.0) - g1 * v[n] * v[j];
+  row[1 + dim] = gamma * v[n];
+  return 0;
+}
+
+static void matmul(int n, const double* X, const double* Y, double* Z) {
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {
+      double s = 0.0;
+      for (int k = 0; k < n; ++k) s += X[i * n + k] * Y[k * n + j];
+      Z[i * n + j] = s;
+    }
+}
+
+/* |A| = sum_i |lambda_i| prod_{j != i} (A - lambda_j I) / (lambda_i - lambda_j)
+ * (Sylvester's formula for a diagonalisable A with the distinct eigenvalues
+ * lambda = v_n - c, v_n, v_n + c of the Euler Jacobian, c^2 = gamma p / rho). */
+int orc_euler_abs_jacobian(int dim, double gamma, const double* u, int dir, double* absA) {
+  double rho, v[3], p, B[3];
+  if (cons_to_prim(ORC_EULER, dim, gamma, u, &rho, v, &p, B)) return -1;
+  const int nv = dim + 2;
+  const double c = sqrt(gamma * p / rho);
+  const double lam[3] = {v[dir] - c, v[dir], v[dir] + c};
+  double A[VMAX * VMAX], S[3][VMAX * VMAX], P[VMAX * VMAX];
+  if (orc_euler_jacobian(dim, gamma, u, dir, A)) return -1;
+  for (int i = 0; i < 3; ++i) {
+    for (int e = 0; e < nv * nv; ++e) S[i][e] = A[e];
+    for (int e = 0; e < nv; ++e) S[i][e * nv + e] -= lam[i];   /* S_i = A - lambda_i I */
+  }
+  for (int e = 0; e < nv * nv; ++e) absA[e] = 0.0;
+  for (int i = 0; i < 3; ++i) {
+    const int j0 = (i == 0) ? 1 : 0, j1 = (i == 2) ? 1 : 2;
+    matmul(nv, S[j0], S[j1], P);
+    const double coef = fabs(lam[i]) / ((lam[i] - lam[j0]) * (lam[i] - lam[j1]));
+    for (int e = 0; e < nv * nv; ++e) absA[e] += coef * P[e];
+  }
+  return 0;
+}
+
+/* eqn.osher @ P:186-196: f = (f(uL) + f(uR))/2 - (1/2) (int_0^1 |A(psi(s))| ds)
+ * (uR - uL), psi(s) = uL + s (uR - uL), the integral by nq-point Gauss-Legendre
+ * ("at least two quadrature points"). */
+int orc_osher(int system, int dim, double gamma, int nq, const double* uL, const double* uR, int dir, double* f) {
+  if (system != ORC_EULER || nq < 1 || nq > 16) return -2;
+  const int nv = dim + 2;
+  double fL[VMAX], fR[VMAX], sq[16], wq[16], du[VMAX], absA[VMAX * VMAX], D[VMAX];
+  if (orc_phys_flux(system, dim, gamma, 0.0, uL, dir, fL)) return -1;
+  if (orc_phys_flux(system, dim, gamma, 0.0, uR, dir, fR)) return -1;
+  gauss_legendre01(nq, sq, wq);
+  for (int v = 0; v < nv; ++v) { du[v] = uR[v] - uL[v]; D[v] = 0.0; }
+  for (int g = 0; g < nq; ++g) {
+    double ps[VMAX];
+    for (int v = 0; v < nv; ++v) ps[v] = uL[v] + sq[g] * du[v];
+    if (orc_euler_abs_jacobian(dim, gamma, ps, dir, absA)) return -1;
+    for (int a = 0; a < nv; ++a) {
+      double s = 0.0;
+      for (int b = 0; b < nv; ++b) s += absA[a * nv + b] * du[b];
+      D[a] += wq[g] * s;
+    }
+  }
+  for (int v = 0; v < nv; ++v) f[v] = 0.5 * (fL[v] + fR[v]) - 0.5 * D[v];
+  return 0;
+}
+
+int orc_numflux(int system, int dim, double gamma, double ch, int flux, int nq, const double* uL,
+                const double* uR, int dir, double* f) {
+  if (flux == ORC_FLUX_OSHER) return orc_osher(system, dim, gamma, nq, uL, uR, dir, f);
+  return orc_rusanov(system, dim, gamma, ch, uL, uR, dir, f);
+}
+
 /* ====================================================================== */
 /* 3. WENO reconstruction                                     */
 /* ====================================================================== */
@@ -599,7 +696,7 @@ static void eval_st(const basis_t* B, int d, int nv, const double* q, const doub
   }
 }
 
-int orc_face_flux(int d, int M, int system, double gamma, double ch, int dir,
+int orc_face_flux(int d, int M, int system, double gamma, double ch, int flux, int nq, int dir,
                   const double* qL, const double* qR, double* F) {
   const basis_t* B = basis_get(M);
   int N = B->N, nv = orc_nvar(system, d);
@@ -622,7 +719,7 @@ int orc_face_flux(int d, int M, int system, double gamma, double ch, int dir,
       if (qR) eval_st(B, d, nv, qR, xr, B->lam[s], up);
       if (!qL) memcpy(um, up, sizeof(double) * nv);
       if (!qR) memcpy(up, um, sizeof(double) * nv);
-      if (orc_rusanov(system, d, gamma, ch, um, up, dir, ft)) return 3;
+      if (orc_numflux(system, d, gamma, ch, flux, nq, um, up, dir, ft)) return 3;
       for (int v = 0; v < nv; ++v) F[v] += wgt * ft[v];
     }
   return 0;
@@ -646,7 +743,7 @@ void orc_eval_w(int d, int M, int nv, const double* w, const double* xi, double*
 
 void orc_gauss_legendre(int n, double* x, double* w) { gauss_legendre01(n, x, w); }
 
-int orc_face_flux_mapped(int d, int M, int system, double gamma, double ch, int dir,
+int orc_face_flux_mapped(int d, int M, int system, double gamma, double ch, int flux, int nq, int dir,
                          const double* qL, const double* offL, double sclL, double toffL, double tsclL,
                          const double* qR, const double* offR, double sclR, double toffR, double tsclR,
                          double* F) {
@@ -672,7 +769,7 @@ int orc_face_flux_mapped(int d, int M, int system, double gamma, double ch, int 
       if (qR) { xr[dir] = offR[dir]; eval_st(B, d, nv, qR, xr, toffR + tsclR * B->lam[s], up); }
       if (!qL) memcpy(um, up, sizeof(double) * nv);
       if (!qR) memcpy(up, um, sizeof(double) * nv);
-      if (orc_rusanov(system, d, gamma, ch, um, up, dir, ft)) return 3;
+      if (orc_numflux(system, d, gamma, ch, flux, nq, um, up, dir, ft)) return 3;
       for (int v = 0; v < nv; ++v) F[v] += wgt * ft[v];
     }
   return 0;
@@ -736,6 +833,7 @@ static int64_t pidx(const orc_ctx* c, int i, int j, int k) {
 
 orc_ctx* orc_create(const orc_config* cfg) {
   if (!cfg || (cfg->dim != 2 && cfg->dim != 3) || cfg->degree < 1 || cfg->degree + 1 > NMAX) return NULL;
+  if (cfg->flux == ORC_FLUX_OSHER && cfg->system != ORC_EULER) return NULL;   /* Osher: Euler only */
   orc_ctx* c = (orc_ctx*)calloc(1, sizeof(orc_ctx));
   c->cfg = *cfg;
   c->d = cfg->dim; c->M = cfg->degree; c->N = c->M + 1;
@@ -753,6 +851,7 @@ orc_ctx* orc_create(const orc_config* cfg) {
   if (c->cfg.pred_max_sweeps <= 0) c->cfg.pred_max_sweeps = 32;
   if (c->cfg.pred_tol <= 0) c->cfg.pred_tol = 1e-13;
   if (c->cfg.ic_quad <= 0) c->cfg.ic_quad = c->N;
+  if (c->cfg.flux_quad <= 0) c->cfg.flux_quad = 3;   /* reading R21 */
   basis_get(c->M);
   pred_get(c->d, c->M);
   return c;
@@ -966,8 +1065,8 @@ int orc_advance_box(orc_ctx* c, double dt, const int32_t* blo, const int32_t* bh
           /* R5: a transmissive boundary face takes the interior trace on both sides */
           const double* qm = (ic[dir] == 0 && c->cfg.bc[2 * dir] == ORC_BC_TRANSMISSIVE) ? NULL : &q[(e0 - stride) * nv * NST];
           const double* qp = (ic[dir] == c->n[dir] - 1 && c->cfg.bc[2 * dir + 1] == ORC_BC_TRANSMISSIVE) ? NULL : &q[(e0 + stride) * nv * NST];
-          if (orc_face_flux(d, c->M, c->cfg.system, c->cfg.gamma, c->cfg.ch, dir, qm, qc, Fm) ||
-              orc_face_flux(d, c->M, c->cfg.system, c->cfg.gamma, c->cfg.ch, dir, qc, qp, Fp)) {
+          if (orc_face_flux(d, c->M, c->cfg.system, c->cfg.gamma, c->cfg.ch, c->cfg.flux, c->cfg.flux_quad, dir, qm, qc, Fm) ||
+              orc_face_flux(d, c->M, c->cfg.system, c->cfg.gamma, c->cfg.ch, c->cfg.flux, c->cfg.flux_quad, dir, qc, qp, Fp)) {
             snprintf(c->err, sizeof(c->err), "inadmissible face state at cell (%d,%d,%d) t=%.17g", i, j, k, c->t);
             free(q); return 3;
           }
@@ -1065,7 +1164,7 @@ int orc_dump_flux(orc_ctx* c, double dt, double* F) {
           const int thi = hib && c->cfg.bc[2 * dir + 1] == ORC_BC_TRANSMISSIVE;
           if (!tlo && cell_predict(c, im[0], im[1], im[2], dt, qa, &sw)) goto fail;
           if (!thi && cell_predict(c, i, j, k, dt, qb, &sw)) goto fail;
-          if (orc_face_flux(d, c->M, c->cfg.system, c->cfg.gamma, c->cfg.ch, dir, tlo ? NULL : qa, thi ? NULL : qb, Fo)) goto fail;
+          if (orc_face_flux(d, c->M, c->cfg.system, c->cfg.gamma, c->cfg.ch, c->cfg.flux, c->cfg.flux_quad, dir, tlo ? NULL : qa, thi ? NULL : qb, Fo)) goto fail;
         }
   free(qa); free(qb);
   return 0;

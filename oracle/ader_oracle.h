@@ -24,6 +24,7 @@ extern "C" {
 
 enum { ORC_EULER = 0, ORC_MHD = 1 };
 enum { ORC_BC_PERIODIC = 0, ORC_BC_TRANSMISSIVE = 1 };
+enum { ORC_FLUX_RUSANOV = 0, ORC_FLUX_OSHER = 1 };   /* eqn.rusanov / eqn.osher */
 
 typedef struct {
   int32_t dim, system, degree;       /* d in {2,3}; M in {2,3}              */
@@ -36,6 +37,9 @@ typedef struct {
   /* AMR (used by the AMR oracle; lmax = 0 means uniform grid) */
   int32_t refine_factor, lmax;
   double chi_ref, chi_rec, chi_eps;
+  /* numerical flux: ORC_FLUX_RUSANOV or ORC_FLUX_OSHER (Euler
+   * only); flux_quad = Gauss-Legendre points of the Osher path integral */
+  int32_t flux, flux_quad;
 } orc_config;
 
 /* Batched initial-condition callback: x[n][3] -> prim[n][9]
@@ -72,15 +76,27 @@ int  orc_reconstruct_box(int d, int M, int nv, const double* ubox, double* w);
 int  orc_predict_cell(int d, int M, int system, double gamma, double ch,
                       const double* w, const double* dtdx, double tol, int max_sweeps,
                       double* q, int* sweeps);
-/* Space-time Rusanov face flux (flux:F/G/H @ P:158-172, eqn.rusanov @ P:181-185)
+/* Space-time face flux (flux:F/G/H @ P:158-172) of the selected two-point flux
+ * (eqn.rusanov @ P:181-185 or eqn.osher @ P:186-196)
  * between the left (lower) cell qL and right (upper) cell qR along dir.  At a
  * transmissive boundary face pass NULL for the exterior side: it takes the
  * interior trace (q^+ = q^-, reading R5). */
-int  orc_face_flux(int d, int M, int system, double gamma, double ch, int dir,
+int  orc_face_flux(int d, int M, int system, double gamma, double ch, int flux, int nq, int dir,
                    const double* qL, const double* qR, double* F);
 int  orc_phys_flux(int system, int dim, double gamma, double ch, const double* u, int dir, double* f);
 double orc_max_speed(int system, int dim, double gamma, double ch, const double* u, int dir);
 int  orc_rusanov(int system, int dim, double gamma, double ch, const double* uL,
+                 const double* uR, int dir, double* f);
+/* Euler Jacobian A_dir = df_dir/du (analytic, row-major nv x nv). */
+int  orc_euler_jacobian(int dim, double gamma, const double* u, int dir, double* A);
+/* |A_dir(u)| for Euler by Sylvester's formula over the three distinct
+ * eigenvalues v_n - c, v_n, v_n + c (A is diagonalisable). */
+int  orc_euler_abs_jacobian(int dim, double gamma, const double* u, int dir, double* absA);
+/* eqn.osher @ P:186-196 along the straight path psi(s) = uL + s (uR - uL),
+ * the path integral by an nq-point Gauss-Legendre rule (Euler only). */
+int  orc_osher(int system, int dim, double gamma, int nq, const double* uL, const double* uR, int dir, double* f);
+/* The selected two-point flux: flux = ORC_FLUX_RUSANOV or ORC_FLUX_OSHER. */
+int  orc_numflux(int system, int dim, double gamma, double ch, int flux, int nq, const double* uL,
                  const double* uR, int dir, double* f);
 void orc_prim_to_cons(int system, int dim, double gamma, const double* prim, double* u);
 /* q_h(xi, tau) = theta_p(xi, tau) q_p (eqn.st.q @ P:391-394), q[nv][N^(d+1)]. */
@@ -89,14 +105,14 @@ void orc_eval_st(int d, int M, int nv, const double* q, const double* xi, double
 void orc_eval_w(int d, int M, int nv, const double* w, const double* xi, double* out);
 /* n-point Gauss-Legendre rule on [0,1]. */
 void orc_gauss_legendre(int n, double* x, double* w);
-/* Space-time Rusanov flux along dir integrated over the face sub-box of the
+/* Space-time two-point flux along dir integrated over the face sub-box of the
  * left cell qL and right cell qR: the face points are given in each cell's
  * reference coordinates by affine maps xi = a + b * eta (eta the fine face /
  * time GL nodes), i.e. for cell X: xi_k = offX[k] + sclX * eta_k on the
  * tangential axes, xi_dir = posX, tau = toffX + tsclX * eta_t.  NULL side =
  * transmissive boundary (interior trace on both sides).  Used by the AMR
  * oracle for same-level and coarse-fine faces. */
-int  orc_face_flux_mapped(int d, int M, int system, double gamma, double ch, int dir,
+int  orc_face_flux_mapped(int d, int M, int system, double gamma, double ch, int flux, int nq, int dir,
                           const double* qL, const double* offL, double sclL, double toffL, double tsclL,
                           const double* qR, const double* offR, double sclR, double toffR, double tsclR,
                           double* F);

@@ -275,9 +275,9 @@ static int cell_face_flux(amr_t* A, int id, int dir, int side, int m, double* F)
   offC[dir] = side ? 1.0 : 0.0;
   if (outside(A, l, ix) && A->cfg.bc[2 * dir + side] == ORC_BC_TRANSMISSIVE) {
     /* R5: interior trace on both sides */
-    return side ? orc_face_flux_mapped(d, A->M, A->cfg.system, A->cfg.gamma, A->cfg.ch, dir, C->q, offC, 1.0, 0.0, 1.0,
+    return side ? orc_face_flux_mapped(d, A->M, A->cfg.system, A->cfg.gamma, A->cfg.ch, A->cfg.flux, A->cfg.flux_quad, dir, C->q, offC, 1.0, 0.0, 1.0,
                                        NULL, zero, 0, 0, 0, F)
-                : orc_face_flux_mapped(d, A->M, A->cfg.system, A->cfg.gamma, A->cfg.ch, dir, NULL, zero, 0, 0, 0,
+                : orc_face_flux_mapped(d, A->M, A->cfg.system, A->cfg.gamma, A->cfg.ch, A->cfg.flux, A->cfg.flux_quad, dir, NULL, zero, 0, 0, 0,
                                        C->q, offC, 1.0, 0.0, 1.0, F);
   }
   int nb = lookup(A, l, ix);
@@ -286,9 +286,9 @@ static int cell_face_flux(amr_t* A, int id, int dir, int side, int m, double* F)
   if (Nb->status == 0) {
     double offN[3] = {0, 0, 0};
     offN[dir] = side ? 0.0 : 1.0;
-    return side ? orc_face_flux_mapped(d, A->M, A->cfg.system, A->cfg.gamma, A->cfg.ch, dir, C->q, offC, 1.0, 0.0, 1.0,
+    return side ? orc_face_flux_mapped(d, A->M, A->cfg.system, A->cfg.gamma, A->cfg.ch, A->cfg.flux, A->cfg.flux_quad, dir, C->q, offC, 1.0, 0.0, 1.0,
                                        Nb->q, offN, 1.0, 0.0, 1.0, F)
-                : orc_face_flux_mapped(d, A->M, A->cfg.system, A->cfg.gamma, A->cfg.ch, dir, Nb->q, offN, 1.0, 0.0, 1.0,
+                : orc_face_flux_mapped(d, A->M, A->cfg.system, A->cfg.gamma, A->cfg.ch, A->cfg.flux, A->cfg.flux_quad, dir, Nb->q, offN, 1.0, 0.0, 1.0,
                                        C->q, offC, 1.0, 0.0, 1.0, F);
   }
   if (Nb->status == 1) {
@@ -304,9 +304,9 @@ static int cell_face_flux(amr_t* A, int id, int dir, int side, int m, double* F)
     offK[dir] = side ? 0.0 : 1.0;
     (void)Kc;
     double toff = (double)m / r, tscl = 1.0 / r;
-    int rc = side ? orc_face_flux_mapped(d, A->M, A->cfg.system, A->cfg.gamma, A->cfg.ch, dir, C->q, offC, 1.0, 0.0, 1.0,
+    int rc = side ? orc_face_flux_mapped(d, A->M, A->cfg.system, A->cfg.gamma, A->cfg.ch, A->cfg.flux, A->cfg.flux_quad, dir, C->q, offC, 1.0, 0.0, 1.0,
                                          Kc->q, offK, 1.0 / r, toff, tscl, F)
-                  : orc_face_flux_mapped(d, A->M, A->cfg.system, A->cfg.gamma, A->cfg.ch, dir, Kc->q, offK, 1.0 / r, toff, tscl,
+                  : orc_face_flux_mapped(d, A->M, A->cfg.system, A->cfg.gamma, A->cfg.ch, A->cfg.flux, A->cfg.flux_quad, dir, Kc->q, offK, 1.0 / r, toff, tscl,
                                          C->q, offC, 1.0, 0.0, 1.0, F);
     if (rc) return rc;
     /* memory variable of the virtual neighbour */
@@ -631,6 +631,7 @@ typedef struct {
 void* orc_amr_create(const orc_config* cfg) {
   if (!cfg || (cfg->dim != 2 && cfg->dim != 3) || cfg->degree < 2 || cfg->degree > 3) return NULL;
   if (cfg->lmax < 0 || cfg->lmax >= LMAXX || cfg->refine_factor < cfg->degree) return NULL;
+  if (cfg->flux == ORC_FLUX_OSHER && cfg->system != ORC_EULER) return NULL;   /* Osher: Euler only */
   amr_t* A = (amr_t*)calloc(1, sizeof(amr_t));
   A->cfg = *cfg;
   A->d = cfg->dim; A->M = cfg->degree; A->N = A->M + 1;
@@ -644,6 +645,7 @@ void* orc_amr_create(const orc_config* cfg) {
   if (A->cfg.pred_tol <= 0) A->cfg.pred_tol = 1e-13;
   if (A->cfg.pred_max_sweeps <= 0) A->cfg.pred_max_sweeps = 32;
   if (A->cfg.ic_quad <= 0) A->cfg.ic_quad = A->N;
+  if (A->cfg.flux_quad <= 0) A->cfg.flux_quad = 3;   /* reading R21 */
   orc_gauss_legendre(A->N, A->gq, A->gw);
   for (int l = 0; l <= A->lmax; ++l) {
     int64_t s = 1;
