@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define ADER_ABI_VERSION 1
+#define ADER_ABI_VERSION 2
 
 typedef struct ader_ctx ader_ctx;   /* opaque; owns all device memory it allocates */
 
@@ -43,6 +43,10 @@ typedef enum {
 
 typedef enum { ADER_EULER = 0, ADER_MHD_GLM = 1 } ader_system;
 typedef enum { ADER_BC_PERIODIC = 0, ADER_BC_TRANSMISSIVE = 1 } ader_bc;
+/* Two-point flux of the space-time face quadrature. */
+typedef enum { ADER_FLUX_RUSANOV = 0,   /* eqn.rusanov @ P:181-185                  */
+               ADER_FLUX_OSHER = 1      /* eqn.osher @ P:186-196, Euler only         */
+} ader_flux;
 
 /* Problem statement.  All lengths in cells. */
 typedef struct {
@@ -67,6 +71,9 @@ typedef struct {
   int32_t rank, world_size;     /* one rank per GPU; world_size=1 => no NCCL       */
   int32_t device;               /* CUDA device ordinal; -1 = current device        */
   uint8_t nccl_id[128];         /* ncclUniqueId from rank 0 (ader_nccl_unique_id)  */
+  int32_t flux;                 /* ader_flux; ADER_FLUX_OSHER needs system=EULER   */
+  int32_t flux_quad;            /* Gauss-Legendre points of the Osher path integral
+                                 * ("at least two"), 1..4; 0 = 3 (R21)   */
 } ader_config;
 
 /* Batched IC callback (host): x[n][3] -> prim[n][9] with
@@ -170,6 +177,10 @@ ader_status ader_kernel_stats(ader_ctx* c, double ms[ADER_K_COUNT], int64_t laun
                               double flops[ADER_K_COUNT]);
 /* Number of kernels this context has launched since ader_create. */
 ader_status ader_launch_count(const ader_ctx* c, int64_t* n);
+/* sizeof of the ABI structs as compiled into the library (no GPU needed), so a
+ * binding can check its layout: what = 0 ader_config, 1 ader_step_report,
+ * 2 ader_cell, 3 ader_partition_info, 4 ader_halo_desc; -1 for other values. */
+int64_t ader_sizeof(int32_t what);
 /* Test-only dumps of one stage on the current state (state not modified):
  *   what = 0 RECON: w[cell][nu][N^d]           (owned cells, x-fastest nodes)
  *   what = 1 PRED : q[cell][nu][N^(d+1)]       (space fastest, time slowest), step dt

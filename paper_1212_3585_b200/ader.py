@@ -15,9 +15,10 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libader_b200.so")
 _LIB = None
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 EULER, MHD_GLM = 0, 1
 PERIODIC, TRANSMISSIVE = 0, 1
+RUSANOV, OSHER = 0, 1
 K_WENO, K_PRED, K_FLUX, K_UPDATE, K_HALO, K_OTHER, K_COUNT = range(7)
 KERNEL_NAMES = ("weno_reconstruct", "stdg_predictor", "face_flux_rusanov", "fv_update", "halo", "other")
 STATUS = {0: "ADER_OK", 1: "ADER_ERR_ARG", 2: "ADER_ERR_CONFIG", 3: "ADER_ERR_SOLVER", 4: "ADER_ERR_CUDA",
@@ -38,6 +39,7 @@ class AderConfig(C.Structure):
         ("ic_quad", C.c_int32), ("adapt_every", C.c_int32),
         ("rank", C.c_int32), ("world_size", C.c_int32), ("device", C.c_int32),
         ("nccl_id", C.c_uint8 * 128),
+        ("flux", C.c_int32), ("flux_quad", C.c_int32),
     ]
 
 
@@ -99,6 +101,8 @@ def lib():
         L.ader_kernel_stats.argtypes = [vp, dp, C.POINTER(C.c_int64), dp]
         L.ader_launch_count.argtypes = [vp, C.POINTER(C.c_int64)]
         L.ader_debug_dump.argtypes = [vp, C.c_int32, C.c_double, dp, C.c_int64]
+        L.ader_sizeof.restype = C.c_int64
+        L.ader_sizeof.argtypes = [C.c_int32]
         _LIB = L
     return _LIB
 
@@ -106,7 +110,7 @@ def lib():
 EXPORTED = ("ader_create", "ader_destroy", "ader_last_error", "ader_set_stream", "ader_set_initial",
             "ader_set_cells", "ader_get_state", "ader_get_cells", "ader_time", "ader_step", "ader_refine",
             "ader_partition", "ader_halo_plan", "ader_nccl_unique_id", "ader_set_profiling", "ader_kernel_stats",
-            "ader_launch_count", "ader_debug_dump")
+            "ader_launch_count", "ader_debug_dump", "ader_sizeof")
 
 
 def _dp(a):
@@ -116,7 +120,7 @@ def _dp(a):
 def make_config(*, dim, degree, n0, lo, hi, bc, system=EULER, gamma=1.4, ch=0.0, cfl=0.9,
                 refine_factor=3, lmax=0, chi_ref=0.2, chi_rec=0.1, chi_eps=0.01, pred_tol=1e-13,
                 pred_max_sweeps=32, ic_quad=0, adapt_every=1, rank=0, world_size=1, device=-1,
-                nccl_id=None) -> AderConfig:
+                nccl_id=None, flux=RUSANOV, flux_quad=0) -> AderConfig:
     cfg = AderConfig()
     cfg.abi_version = ABI_VERSION
     cfg.dim, cfg.system, cfg.degree = dim, system, degree
@@ -134,6 +138,7 @@ def make_config(*, dim, degree, n0, lo, hi, bc, system=EULER, gamma=1.4, ch=0.0,
     cfg.pred_tol, cfg.pred_max_sweeps = pred_tol, pred_max_sweeps
     cfg.ic_quad, cfg.adapt_every = ic_quad, adapt_every
     cfg.rank, cfg.world_size, cfg.device = rank, world_size, device
+    cfg.flux, cfg.flux_quad = flux, flux_quad
     if nccl_id is not None:
         for i, b in enumerate(bytes(nccl_id)[:128]):
             cfg.nccl_id[i] = b

@@ -149,6 +149,9 @@ ader_status validate(const ader_config* cfg, std::string& why) {
   if (cfg->rank < 0 || cfg->rank >= cfg->world_size) return bad("rank out of range");
   if (cfg->ic_quad < 0 || cfg->ic_quad > 8) return bad("ic_quad must be in 0..8");
   if (cfg->pred_max_sweeps < 0 || cfg->pred_max_sweeps > 1000) return bad("pred_max_sweeps out of range");
+  if (cfg->flux != ADER_FLUX_RUSANOV && cfg->flux != ADER_FLUX_OSHER) return bad("unknown flux");
+  if (cfg->flux == ADER_FLUX_OSHER && cfg->system != ADER_EULER) return bad("the Osher flux is implemented for Euler only");
+  if (cfg->flux_quad < 0 || cfg->flux_quad > 4) return bad("flux_quad must be in 0..4");
   (void)b;
   return ADER_OK;
 }
@@ -282,8 +285,14 @@ double pred_sweep_flops(const ader_ctx* c) {
   return c->NST * flux_eval_flops(c->cfg.system, c->d) + (double)c->nv * c->NST * (2.0 * c->d * c->N + 2.0 * c->N + 1.0);
 }
 double face_flops(const ader_ctx* c) {
-  const double rus = (c->cfg.system == ADER_EULER) ? 2.0 * (12 + 2 * c->d) + 4.0 * c->nv : 2.0 * 90 + 4.0 * c->nv;
-  return c->NS * (4.0 * c->nv * c->N + rus + 2.0 * c->nv + 2.0);
+  double two_point = (c->cfg.system == ADER_EULER) ? 2.0 * (12 + 2 * c->d) + 4.0 * c->nv : 2.0 * 90 + 4.0 * c->nv;
+  if (c->cfg.flux == ADER_FLUX_OSHER) {
+    // two physical fluxes, du, and per path point: the state (nv FMA) and
+    // |A| du from the closed-form eigenvectors (~9 d + 50), then the blend
+    const int nq = c->cfg.flux_quad > 0 ? c->cfg.flux_quad : 3;
+    two_point = 2.0 * (10 + 2 * c->d) + c->nv + nq * (2.0 * c->nv + 9.0 * c->d + 50.0) + 3.0 * c->nv;
+  }
+  return c->NS * (4.0 * c->nv * c->N + two_point + 2.0 * c->nv + 2.0);
 }
 
 // ---- ghost layers ------------------------------------------------------------
@@ -609,6 +618,9 @@ static ader_status create_impl(const ader_config* cfg, ader_ctx** out) {
   }
   CK(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
   if (!build_tables(c->M, &c->k.tab)) return fail(c, ADER_ERR_CONFIG, "no tables for M=%d", c->M);
+  if (!build_osher_quadrature(cfg->flux_quad > 0 ? cfg->flux_quad : 3, &c->k.tab))
+    return fail(c, ADER_ERR_CONFIG, "no path rule for flux_quad=%d", cfg->flux_quad);
+  c->k.tab.flux = cfg->flux;
   c->k.D = c->d; c->k.M = c->M; c->k.SYS = cfg->system; c->k.NV = c->nv;
   c->k.sy = c->P[0]; c->k.sz = (long long)c->P[0] * c->P[1];
   c->k.ncell = c->ncell;
@@ -906,6 +918,17 @@ ader_status ader_launch_count(const ader_ctx* c, int64_t* n) {
   if (!c || !n) return ADER_ERR_ARG;
   *n = c->launches;
   return ADER_OK;
+}
+
+int64_t ader_sizeof(int32_t what) {
+  switch (what) {
+    case 0: return (int64_t)sizeof(ader_config);
+    case 1: return (int64_t)sizeof(ader_step_report);
+    case 2: return (int64_t)sizeof(ader_cell);
+    case 3: return (int64_t)sizeof(ader_partition_info);
+    case 4: return (int64_t)sizeof(ader_halo_desc);
+    default: return -1;
+  }
 }
 
 ader_status ader_debug_dump(ader_ctx* c, int32_t what, double dt, double* out, int64_t capacity) {

@@ -208,14 +208,26 @@ __device__ __forceinline__ void trace_coarse(const double* __restrict__ qK, bool
   }
 }
 
+// two-point flux: eqn.rusanov or, for Euler with T.flux == 1,
+// eqn.osher
 template <int SYS, int D, int DIR>
-__device__ __forceinline__ bool rusanov_pt(const double (&um)[Phys<SYS, D>::NV], const double (&up)[Phys<SYS, D>::NV],
-                                           double gamma, double ch, double (&f)[Phys<SYS, D>::NV]) {
+__device__ __forceinline__ bool numflux_pt(const double (&um)[Phys<SYS, D>::NV], const double (&up)[Phys<SYS, D>::NV],
+                                           double gamma, double ch, const DevTables& T,
+                                           double (&f)[Phys<SYS, D>::NV]) {
   using PH = Phys<SYS, D>;
   constexpr int NV = PH::NV;
   double fL[NV], fR[NV], sL, sR;
   bool ok = PH::template flux_speed<DIR>(um, gamma, ch, fL, sL);
   ok &= PH::template flux_speed<DIR>(up, gamma, ch, fR, sR);
+  if constexpr (SYS == 0) {
+    if (T.flux == 1) {
+      double dis[NV];
+      ok &= osher_dissipation<D, DIR>(um, up, gamma, T, dis);
+#pragma unroll
+      for (int v = 0; v < NV; ++v) f[v] = 0.5 * (fL[v] + fR[v]) - 0.5 * dis[v];
+      return ok;
+    }
+  }
   const double smax = fmax(sL, sR);
 #pragma unroll
   for (int v = 0; v < NV; ++v) f[v] = 0.5 * (fL[v] + fR[v]) - 0.5 * smax * (up[v] - um[v]);
@@ -242,7 +254,7 @@ __device__ bool face_flux_amr(int kind, const double* qL, const double* qR, int 
       if (kind == 4) trace_coarse<D, M, NV, DIR>(qR, false, o1, o2, m, t1, t2, s, T, S, up);
       if (kind == 1) for (int v = 0; v < NV; ++v) um[v] = up[v];
       if (kind == 2) for (int v = 0; v < NV; ++v) up[v] = um[v];
-      ok &= rusanov_pt<SYS, D, DIR>(um, up, gamma, ch, ft);
+      ok &= numflux_pt<SYS, D, DIR>(um, up, gamma, ch, T, ft);
       double wgt = T.w[s] * T.w[t1];
       if (D == 3) wgt *= T.w[t2];
 #pragma unroll

@@ -108,7 +108,63 @@ template <int D> struct Phys<0, D> {
     for (int k = 0; k < D; ++k) { u[1 + k] = rho * pr[1 + k]; ke += pr[1 + k] * pr[1 + k]; }
     u[D + 1] = pr[4] / (gamma - 1.0) + 0.5 * rho * ke;
   }
+  // acc += wq |A_DIR(u)| du with the closed-form eigenvectors of the Euler
+  // Jacobian (used by the Osher path integral, eqn.osher @ P:186-196):
+  //   |A| du = |v_n| du + (|v_n - c| - |v_n|) a1 r1 + (|v_n + c| - |v_n|) a3 r3,
+  //   dp = (gamma-1)(|v|^2 drho / 2 - v.dm + dE),  rho dv_n = dm_n - v_n drho,
+  //   a1,3 = (dp -+ c rho dv_n) / (2 c^2),  r1,3 = (1, v -+ c e_n, H -+ v_n c)
+  // (the shear and entropy waves share the eigenvalue v_n, so they enter only
+  // through |v_n| du).
+  template <int DIR>
+  __device__ __forceinline__ static bool abs_jacobian_apply(const double (&u)[NV], const double (&du)[NV],
+                                                            double gamma, double wq, double (&acc)[NV]) {
+    const double rho = u[0];
+    const double ir = fast_rcp(rho);
+    double v[D], ke = 0.0, vdm = 0.0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) { v[k] = u[1 + k] * ir; ke += v[k] * u[1 + k]; vdm += v[k] * du[1 + k]; }
+    const double p = (gamma - 1.0) * (u[D + 1] - 0.5 * ke);
+    const double gp = gamma * p;
+    const double c = fast_sqrt(gp * ir);
+    const double h2c2 = 0.5 * rho * fast_rcp(gp);   // 1 / (2 c^2)
+    const double H = (u[D + 1] + p) * ir;
+    const double vn = v[DIR];
+    const double dp = (gamma - 1.0) * (0.5 * (ke * ir) * du[0] - vdm + du[D + 1]);
+    const double rdv = du[1 + DIR] - vn * du[0];
+    const double an = fabs(vn);
+    const double k1 = wq * (fabs(vn - c) - an) * ((dp - c * rdv) * h2c2);
+    const double k3 = wq * (fabs(vn + c) - an) * ((dp + c * rdv) * h2c2);
+    const double wa = wq * an;
+    acc[0] += wa * du[0] + (k1 + k3);
+#pragma unroll
+    for (int k = 0; k < D; ++k) acc[1 + k] += wa * du[1 + k] + (k1 + k3) * v[k];
+    acc[1 + DIR] += c * (k3 - k1);
+    acc[D + 1] += wa * du[D + 1] + (k1 + k3) * H + (k3 - k1) * (vn * c);
+    return rho > 0.0 && p > 0.0;
+  }
 };
+
+// Osher-type dissipation (eqn.osher @ P:186-196, Euler only): dis =
+// sum_g w_g |A(psi(s_g))| (up - um) along psi(s) = um + s (up - um), with the
+// path rule of DevTables (oq_n Gauss-Legendre points).
+template <int D, int DIR>
+__device__ __forceinline__ bool osher_dissipation(const double (&um)[D + 2], const double (&up)[D + 2], double gamma,
+                                                  const DevTables& T, double (&dis)[D + 2]) {
+  constexpr int NV = D + 2;
+  double du[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) { du[v] = up[v] - um[v]; dis[v] = 0.0; }
+  bool ok = true;
+#pragma unroll 1
+  for (int g = 0; g < T.oq_n; ++g) {
+    const double sg = T.oq_x[g];
+    double ps[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) ps[v] = um[v] + sg * du[v];
+    ok &= Phys<0, D>::template abs_jacobian_apply<DIR>(ps, du, gamma, T.oq_w[g], dis);
+  }
+  return ok;
+}
 
 template <int D> struct Phys<1, D> {
   static constexpr int NV = 9;

@@ -3,7 +3,8 @@
 //   k_weno      a1 WENO reconstruction, one sweep
 //   k_predictor a2 local space-time DG predictor, nodal Picard form of
 //               eqn.stdg.final: q = w - T_tau sum_dir D_dir f*_dir(q)
-//   k_face_flux a3 space-time Gauss quadrature of the Rusanov flux
+//   k_face_flux_cells a3 space-time Gauss quadrature of the two-point flux,
+//               Rusanov (eqn.rusanov @ P:181-185) or Osher (eqn.osher @ P:186-196)
 //   k_update    a4 one-step FV update (eq:finite_vol @ P:147-152) fused with the
 //               CFL speed of the new state (reading R1)
 // plus ghost fill / pack / IC / gather helpers.  Layouts: see launch.h.
@@ -264,84 +265,6 @@ __global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? 4 : 2) k_predictor(
   }
 }
 
-// ===========================================================================
-// a3: face flux.  One thread per space-time quadrature point of a face
-// (N^(D-1) tangential x N time = NS points); a face per NS-lane group.
-// ===========================================================================
-template <int D, int M, int SYS, int DIR, int WARPS>
-__device__ __forceinline__ void face_flux_dir(const double* __restrict__ q, double* __restrict__ F, const Box& R,
-                                              long long sy, long long sz, long long ncell, double gamma, double ch,
-                                              int bmask, DevCounters* cnt, const DevTables& T, double* red) {
-  using PH = Phys<SYS, D>;
-  constexpr int NV = PH::NV, N = M + 1, NS = ipow_c(N, D), NST = NS * N;
-  constexpr int NT = NS / N;   // tangential points
-  constexpr int CPW = 32 / NS;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int slot = lane / NS, p = lane - slot * NS;
-  const long long rc = ((long long)blockIdx.x * WARPS + warp) * CPW + slot;
-  const bool active = slot < CPW && rc < R.count();
-  double* rw = red + (warp * CPW + (slot < CPW ? slot : CPW - 1)) * NV * NS;
-  if (active) {
-    const long long cR = box_cell(R, rc, sy, sz);
-    const long long sd = (DIR == 0) ? 1 : (DIR == 1 ? sy : sz);
-    const long long cL = cR - sd;
-    const int s = p / NT, t = p - s * NT;
-    const int t1 = t % N, t2 = t / N;
-    constexpr int ax0 = (DIR == 0) ? 1 : 0;
-    constexpr int ax1 = (DIR == 2) ? 1 : 2;
-    constexpr int sn = ipow_c(N, DIR);
-    const int base = s * NS + t1 * ipow_c(N, ax0) + (D == 3 ? t2 * ipow_c(N, ax1) : 0);
-    const double* qL = q + cL * (NV * NST) + base;
-    const double* qR = q + cR * (NV * NST) + base;
-    // transmissive boundary faces take the interior trace on both sides (reading R5)
-    const int fc = box_coord(R, rc, DIR);
-    const bool tlo = (bmask >> (2 * DIR)) & 1 && fc == R.lo[DIR];
-    const bool thi = (bmask >> (2 * DIR + 1)) & 1 && fc == R.lo[DIR] + R.ext[DIR] - 1;
-    double um[NV], up[NV];
-#pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      double a = 0.0, b = 0.0;
-#pragma unroll
-      for (int k = 0; k < N; ++k) {
-        if (!tlo) a += T.psi1[k] * __ldg(&qL[v * NST + k * sn]);   // q_h^- at xi = 1 of the left cell
-        if (!thi) b += T.psi0[k] * __ldg(&qR[v * NST + k * sn]);   // q_h^+ at xi = 0 of the right cell
-      }
-      um[v] = tlo ? b : a;
-      up[v] = thi ? a : b;
-    }
-    double fL[NV], fR[NV], sL, sR;
-    bool ok = PH::template flux_speed<DIR>(um, gamma, ch, fL, sL);
-    ok &= PH::template flux_speed<DIR>(up, gamma, ch, fR, sR);
-    if (!ok) record_error(cnt, 1, 2, cR);
-    const double smax = fmax(sL, sR);   // reading R4
-    double wt = T.w[s] * T.w[t1];
-    if (D == 3) wt *= T.w[t2];
-#pragma unroll
-    for (int v = 0; v < NV; ++v)
-      rw[v * NS + p] = wt * (0.5 * (fL[v] + fR[v]) - 0.5 * smax * (up[v] - um[v]));   // eqn.rusanov
-  }
-  __syncwarp();
-  if (active && p < NV) {
-    const long long cR = box_cell(R, rc, sy, sz);
-    double acc = 0.0;
-    for (int j = 0; j < NS; ++j) acc += rw[p * NS + j];
-    F[((long long)DIR * ncell + cR) * NV + p] = acc;
-  }
-}
-
-template <int D, int M, int SYS, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32) k_face_flux(const double* __restrict__ q, double* __restrict__ F,
-                                                          const Box R0, const Box R1, const Box R2, const long long sy,
-                                                          const long long sz, const long long ncell,
-                                                          const double gamma, const double ch, const int bmask,
-                                                          DevCounters* __restrict__ cnt,
-                                                          const __grid_constant__ DevTables T) {
-  extern __shared__ double red[];
-  if (blockIdx.y == 0) face_flux_dir<D, M, SYS, 0, WARPS>(q, F, R0, sy, sz, ncell, gamma, ch, bmask, cnt, T, red);
-  else if (blockIdx.y == 1) face_flux_dir<D, M, SYS, 1, WARPS>(q, F, R1, sy, sz, ncell, gamma, ch, bmask, cnt, T, red);
-  else if (D == 3) face_flux_dir<D, M, SYS, 2, WARPS>(q, F, R2, sy, sz, ncell, gamma, ch, bmask, cnt, T, red);
-}
-
 // ---------------------------------------------------------------------------
 // a3 (cell-grouped): one lane group (power of two >= N^D lanes, a lane per
 // space-time quadrature point) computes ALL lower faces of one cell, reading the
@@ -353,7 +276,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_face_flux(const double* __restri
 // D*NV point sums are formed by one transpose-reduction over the lane group
 // (fixed butterfly, deterministic).
 // ---------------------------------------------------------------------------
-template <int D, int M, int SYS, int DIR>
+template <int D, int M, int SYS, int DIR, int FLUX>
 __device__ __forceinline__ bool point_flux(const double* __restrict__ q, long long cR, long long sd, int p, bool fok,
                                            bool tlo, bool thi, double wt, double gamma, double ch,
                                            const DevTables& T, double* val) {
@@ -384,8 +307,8 @@ __device__ __forceinline__ bool point_flux(const double* __restrict__ q, long lo
     um[v] = tlo ? b : a;   // transmissive boundary: interior trace on both sides (R5)
     up[v] = thi ? a : b;
   }
-  // equal traces (e.g. inside a constant region): eqn.rusanov reduces exactly
-  // to f(q) — 0.5 (f + f) = f and the dissipation term is 0 — so one flux
+  // equal traces (e.g. inside a constant region): eqn.rusanov and eqn.osher
+  // reduce exactly to f(q) — 0.5 (f + f) = f and the dissipation term is 0 — so one flux
   // evaluation gives the bitwise-identical result
   bool same = true;
 #pragma unroll
@@ -400,9 +323,16 @@ __device__ __forceinline__ bool point_flux(const double* __restrict__ q, long lo
   double fL[NV], fR[NV], sL, sR;
   bool ok = PH::template flux_speed<DIR>(um, gamma, ch, fL, sL);
   ok &= PH::template flux_speed<DIR>(up, gamma, ch, fR, sR);
-  const double smax = fmax(sL, sR);   // reading R4
+  if constexpr (FLUX == 1 && SYS == 0) {
+    double dis[NV];
+    ok &= osher_dissipation<D, DIR>(um, up, gamma, T, dis);
 #pragma unroll
-  for (int v = 0; v < NV; ++v) val[v] = wt * (0.5 * (fL[v] + fR[v]) - 0.5 * smax * (up[v] - um[v]));   // eqn.rusanov
+    for (int v = 0; v < NV; ++v) val[v] = wt * (0.5 * (fL[v] + fR[v]) - 0.5 * dis[v]);   // eqn.osher
+  } else {
+    const double smax = fmax(sL, sR);   // reading R4
+#pragma unroll
+    for (int v = 0; v < NV; ++v) val[v] = wt * (0.5 * (fL[v] + fR[v]) - 0.5 * smax * (up[v] - um[v]));   // eqn.rusanov
+  }
   return ok;
 }
 
@@ -433,7 +363,7 @@ struct TransposeReduce {
 
 constexpr int pow2_at_least(int x) { return x <= 1 ? 1 : 2 * pow2_at_least((x + 1) / 2); }
 
-template <int D, int M, int SYS, int WARPS, int YC>
+template <int D, int M, int SYS, int WARPS, int YC, int FLUX>
 __global__ void __launch_bounds__(WARPS * 32) k_face_flux_cells(const double* __restrict__ q, double* __restrict__ F,
                                                                 const Box E, const int H, const int n0, const int n1,
                                                                 const int n2, const long long sy, const long long sz,
@@ -473,12 +403,12 @@ __global__ void __launch_bounds__(WARPS * 32) k_face_flux_cells(const double* __
 #pragma unroll
   for (int i = D * NV; i < KP; ++i) v[i] = 0.0;
   bool good = true;
-  good &= point_flux<D, M, SYS, 0>(q, cR, 1, ps, fok[0], (bmask & 1) && cx == H, (bmask & 2) && cx == H + n0, wt,
+  good &= point_flux<D, M, SYS, 0, FLUX>(q, cR, 1, ps, fok[0], (bmask & 1) && cx == H, (bmask & 2) && cx == H + n0, wt,
                                    gamma, ch, T, v);
-  good &= point_flux<D, M, SYS, 1>(q, cR, sy, ps, fok[1], (bmask & 4) && cy == H, (bmask & 8) && cy == H + n1, wt,
+  good &= point_flux<D, M, SYS, 1, FLUX>(q, cR, sy, ps, fok[1], (bmask & 4) && cy == H, (bmask & 8) && cy == H + n1, wt,
                                    gamma, ch, T, v + NV);
   if constexpr (D == 3)
-    good &= point_flux<D, M, SYS, 2>(q, cR, sz, ps, fok[2], (bmask & 16) && cz == zH, (bmask & 32) && cz == zH + n2,
+    good &= point_flux<D, M, SYS, 2, FLUX>(q, cR, sz, ps, fok[2], (bmask & 16) && cz == zH, (bmask & 32) && cz == zH + n2,
                                      wt, gamma, ch, T, v + 2 * NV);
   if (!good) record_error(cnt, 1, 2, cR);
   int base = 0;
@@ -670,11 +600,6 @@ size_t pred_smem() {
   constexpr int LP = (N == 4) ? 4 : N;
   return sizeof(double) * ((size_t)kPredWarps * CPW * (D * NV * N * (NS / N) * LP + 8));
 }
-template <int D, int M, int SYS>
-size_t flux_smem() {
-  constexpr int NV = Phys<SYS, D>::NV, N = M + 1, NS = ipow_c(N, D), CPW = 32 / NS;
-  return sizeof(double) * (size_t)kFluxWarps * CPW * NV * NS;
-}
 }  // namespace
 
 bool supported(int D, int M, int SYS) {
@@ -751,30 +676,13 @@ void launch_face_flux_cells(const KCtx& k, const double* q, double* F, const Box
     const long long ych = (ext.ext[1] + YC - 1) / YC;
     const long long groups = (long long)ext.ext[0] * ych * YC * ext.ext[2];
     count_launch(k);
-    k_face_flux_cells<D, M, SYS, kFluxWarps, YC><<<grid_for(groups, kFluxWarps * CPW), kFluxWarps * 32, 0, k.stream>>>(
-        q, F, ext, H, n[0], n[1], n[2], k.sy, k.sz, k.ncell, k.gamma, k.ch, bmask, cnt, k.tab);
-  });
-}
-
-void launch_face_flux(const KCtx& k, const double* q, double* F, const Box faces[3], int bmask, DevCounters* cnt) {
-  long long mx = 0;
-  for (int d = 0; d < k.D; ++d) mx = faces[d].count() > mx ? faces[d].count() : mx;
-  if (mx == 0) return;
-  ADER_DISPATCH(k.D, k.M, k.SYS, {
-    constexpr int N = M + 1;
-    constexpr int NS = ipow_c(N, D);
-    constexpr int CPW = 32 / NS;
-    const size_t sm = flux_smem<D, M, SYS>();
-    auto kern = k_face_flux<D, M, SYS, kFluxWarps>;
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      attr = true;
-    }
-    dim3 g(grid_for(mx, kFluxWarps * CPW), D);
-    count_launch(k);
-    kern<<<g, kFluxWarps * 32, sm, k.stream>>>(q, F, faces[0], faces[1], faces[2], k.sy, k.sz, k.ncell, k.gamma,
-                                                k.ch, bmask, cnt, k.tab);
+    const unsigned g = grid_for(groups, kFluxWarps * CPW);
+    if (SYS == 0 && k.tab.flux == 1)
+      k_face_flux_cells<D, M, SYS, kFluxWarps, YC, 1><<<g, kFluxWarps * 32, 0, k.stream>>>(
+          q, F, ext, H, n[0], n[1], n[2], k.sy, k.sz, k.ncell, k.gamma, k.ch, bmask, cnt, k.tab);
+    else
+      k_face_flux_cells<D, M, SYS, kFluxWarps, YC, 0><<<g, kFluxWarps * 32, 0, k.stream>>>(
+          q, F, ext, H, n[0], n[1], n[2], k.sy, k.sz, k.ncell, k.gamma, k.ch, bmask, cnt, k.tab);
   });
 }
 

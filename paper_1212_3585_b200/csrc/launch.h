@@ -60,12 +60,11 @@ void launch_predictor(const KCtx& k, const double* w, double* q, const Box& regi
 // Predictor on the cells of an id list (AMR levels): w, q indexed by id.
 void launch_predictor_list(const KCtx& k, const double* w, double* q, const Box& region, const int* list,
                            long long nlist, const double dtdx[3], double tol, int max_sweeps, DevCounters* cnt);
-// Face fluxes on the lower face of every cell of faces[dir], for dir < D.
-// bmask bit 2*dir (2*dir+1): the first (last) face along dir is a physical
-// transmissive boundary and takes the interior trace on both sides.
-void launch_face_flux(const KCtx& k, const double* q, double* F, const Box faces[3], int bmask, DevCounters* cnt);
-// Same fluxes, one lane group per cell of `ext` (owned block + 1 on each active
-// axis) computing all lower faces of that cell (L2-friendly traversal).
+// Face fluxes on the lower face of every cell of `ext` (owned block + 1 on each
+// active axis), one lane group per cell computing all its lower faces
+// (L2-friendly traversal).  bmask bit 2*dir (2*dir+1): the first (last) face
+// along dir is a physical transmissive boundary and takes the interior trace
+// on both sides.
 void launch_face_flux_cells(const KCtx& k, const double* q, double* F, const Box& ext, int H, const int n[3],
                             int bmask, DevCounters* cnt);
 // FV update of `interior` in place + max CFL speed of the new state.

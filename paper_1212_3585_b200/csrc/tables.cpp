@@ -8,8 +8,18 @@
 namespace ader {
 namespace {
 
-// Gauss-Legendre nodes / weights on [0,1] in closed form (N = 3, 4).
+// Gauss-Legendre nodes / weights on [0,1] in closed form (N = 1..4).
 bool gl_closed_form(int N, double* x, double* w) {
+  if (N == 1) {
+    x[0] = 0.5; w[0] = 1.0;
+    return true;
+  }
+  if (N == 2) {
+    const double h = std::sqrt(3.0) / 6.0;
+    x[0] = 0.5 - h; x[1] = 0.5 + h;
+    w[0] = w[1] = 0.5;
+    return true;
+  }
   if (N == 3) {
     const double h = std::sqrt(15.0) / 10.0;
     x[0] = 0.5 - h; x[1] = 0.5; x[2] = 0.5 + h;
@@ -164,6 +174,12 @@ bool build_tables(int M, DevTables* t) {
     }
   }
   return true;
+}
+
+bool build_osher_quadrature(int nq, DevTables* t) {
+  if (nq < 1 || nq > kMaxN) return false;
+  t->oq_n = nq;
+  return gl_closed_form(nq, t->oq_x, t->oq_w);
 }
 
 }  // namespace ader

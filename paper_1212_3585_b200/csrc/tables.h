@@ -20,9 +20,14 @@ struct DevTables {
   double sigma[kMaxN][kMaxN];     // oscillation indicator matrix
   double lin[4];                  // linear weights lambda_s
   double Tsum[kMaxN];             // row sums of T_tau (first Picard sweep, time-constant guess)
+  double oq_x[kMaxN], oq_w[kMaxN];// Gauss-Legendre rule of the Osher path integral
+  int oq_n;                       // its number of points (1..4)
+  int flux;                       // two-point flux: 0 Rusanov (eqn.rusanov), 1 Osher (eqn.osher)
 };
 
 // Fills t for degree M (2 or 3).  Returns false for an unsupported degree.
 bool build_tables(int M, DevTables* t);
+// Fills the nq-point path rule of eqn.osher (nq in 1..4).  Returns false otherwise.
+bool build_osher_quadrature(int nq, DevTables* t);
 
 }  // namespace ader

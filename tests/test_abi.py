@@ -37,7 +37,8 @@ def _cfg(**kw):
 @pytest.mark.parametrize("kw", [dict(dim=4), dict(degree=1), dict(degree=5), dict(n0=(0, 4)),
                                 dict(world_size=9), dict(rank=2, world_size=2), dict(gamma=1.0),
                                 dict(bc=(0, 1, 0, 0, 0, 0)), dict(dim=3, degree=3, n0=(8, 8, 8)),
-                                dict(lmax=1, refine_factor=1)])
+                                dict(lmax=1, refine_factor=1), dict(flux=2), dict(flux=1, system=1),
+                                dict(flux=1, flux_quad=5)])
 def test_create_rejects_bad_config_before_allocation(kw):
     cfg = _cfg(**kw)
     ptr = C.c_void_p()
@@ -45,6 +46,14 @@ def test_create_rejects_bad_config_before_allocation(kw):
     assert st == 2, (kw, st)
     assert not ptr
     assert len(ader.lib().ader_last_error(None)) > 0
+
+
+def test_struct_layouts_match_the_library():
+    L = ader.lib()
+    for what, st in enumerate([ader.AderConfig, ader.AderStepReport, ader.AderCell, ader.AderPartitionInfo,
+                               ader.AderHaloDesc]):
+        assert L.ader_sizeof(what) == C.sizeof(st), st
+    assert L.ader_sizeof(99) == -1
 
 
 def test_abi_version_checked():

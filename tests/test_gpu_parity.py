@@ -27,13 +27,13 @@ def rel_err(a, b, axis=None):
     return (np.abs(a2 - b2).max(axis=0) / scale).max()
 
 
-def pair(dim, degree, n, lo, hi, bc, ic, system=0, gamma=1.4, ch=0.0, cfl=0.9, ic_quad=0):
+def pair(dim, degree, n, lo, hi, bc, ic, system=0, gamma=1.4, ch=0.0, cfl=0.9, ic_quad=0, flux=0, flux_quad=3):
     cfg = ader.make_config(dim=dim, degree=degree, n0=n, lo=lo, hi=hi, bc=bc, system=system, gamma=gamma,
-                           ch=ch, cfl=cfl, ic_quad=ic_quad, device=0)
+                           ch=ch, cfl=cfl, ic_quad=ic_quad, device=0, flux=flux, flux_quad=flux_quad)
     g = ader.Solver(cfg)
     g.set_initial(ic)
     o = O.Oracle(dim=dim, degree=degree, n=n, lo=lo, hi=hi, bc=bc, system=system, gamma=gamma, ch=ch, cfl=cfl,
-                 ic_quad=ic_quad)
+                 ic_quad=ic_quad, flux=flux, flux_quad=flux_quad)
     o.set_initial(ic)
     return g, o
 
@@ -49,6 +49,17 @@ CASES = {
                       ic=W.orszag_tang(), system=1, gamma=5 / 3, ch=2.0),
     "mhd_ot_M2": dict(dim=2, degree=2, n=(14, 13), lo=(0, 0), hi=(2 * math.pi, 2 * math.pi), bc=(0,) * 6,
                       ic=W.orszag_tang(), system=1, gamma=5 / 3, ch=2.0),
+    # Osher-type flux (eqn.osher @ P:186-196; the paper's flux for the explosions)
+    "explosion2d_M2_osher": dict(dim=2, degree=2, n=(22, 21), lo=(-1, -1), hi=(1, 1), bc=(1,) * 6,
+                                 ic=W.explosion(2), flux=1),
+    "explosion2d_M3_osher_q2": dict(dim=2, degree=3, n=(15, 14), lo=(-1, -1), hi=(1, 1), bc=(1,) * 6,
+                                    ic=W.explosion(2), flux=1, flux_quad=2, cfl=0.5),
+    "explosion3d_M2_osher": dict(dim=3, degree=2, n=(9, 8, 7), lo=(-1,) * 3, hi=(1,) * 3, bc=(1,) * 6,
+                                 ic=W.explosion(3), flux=1),
+    "vortex2d_M3_osher": dict(dim=2, degree=3, n=(17, 16), lo=(0, 0), hi=(10, 10), bc=(0,) * 6,
+                              ic=W.isentropic_vortex(), flux=1),
+    "random3d_M2_osher_q4": dict(dim=3, degree=2, n=(7, 6, 9), lo=(0,) * 3, hi=(1,) * 3, bc=(0,) * 6,
+                                 ic=W.random_smooth(3, seed=1212, amp=0.08), flux=1, flux_quad=4),
 }
 
 
@@ -121,6 +132,26 @@ def test_3d_explosion_to_paper_final_time():
     assert rel_err(g.get_state(), o.get_cells()) <= 1e-8
 
 
+def test_3d_explosion_osher_to_paper_final_time():
+    # the paper's 3D explosion uses the Osher flux: run it to
+    # t_e = 0.25 at 12^3 with the C4 CFL (reading R1)
+    g, o = pair(3, 2, (12, 12, 12), (-1,) * 3, (1,) * 3, (1,) * 6, W.explosion(3), cfl=0.3, flux=1)
+    rg = g.step(0.25, 10 ** 6)
+    ro = o.step(0.25, 10 ** 6)
+    assert rg.macro_steps == ro.steps
+    assert rel_err(g.get_state(), o.get_cells()) <= 1e-8
+
+
+def test_osher_100_step_parity_and_conservation():
+    g, o = pair(2, 2, (24, 24), (0, 0), (1, 1), (0,) * 6, W.random_smooth(2, seed=3585, amp=0.2), flux=1)
+    u0 = g.get_state()
+    g.step(1e300, 100)
+    o.step(1e300, 100)
+    ug = g.get_state()
+    assert rel_err(ug, o.get_cells()) <= 1e-8
+    assert np.all(np.abs(ug.sum(0) - u0.sum(0)) <= 1e-11 * np.abs(u0).sum(0))
+
+
 def test_constant_state_bitwise():
     for dim, M, n in [(2, 2, (13, 11)), (2, 3, (9, 10)), (3, 2, (6, 7, 5))]:
         cfg = ader.make_config(dim=dim, degree=M, n0=n, lo=(0,) * dim, hi=(1,) * dim, bc=(0,) * 6, device=0)
@@ -187,9 +218,10 @@ def test_c2_512_sampled_parity():
         assert (np.abs(gg - out).max(axis=0) / scale).max() <= 1e-11, (blo, np.abs(gg - out).max(axis=0))
 
 
-def test_c4_256_sampled_parity():
+@pytest.mark.parametrize("flux", [0, 1])
+def test_c4_256_sampled_parity(flux):
     wl = W.config("c4", 256)
-    cfg = ader.make_config(dim=3, degree=2, n0=wl.n, lo=wl.lo, hi=wl.hi, bc=wl.bc, cfl=wl.cfl, device=0)
+    cfg = ader.make_config(dim=3, degree=2, n0=wl.n, lo=wl.lo, hi=wl.hi, bc=wl.bc, cfl=wl.cfl, device=0, flux=flux)
     g = ader.Solver(cfg)
     g.set_initial(wl.ic)
     rep = g.step(1e300, 1)
@@ -201,7 +233,7 @@ def test_c4_256_sampled_parity():
     dt = wl.cfl / s
     assert abs(rep.dt0 - dt) <= 1e-14 * dt
     ug = g.get_state().reshape(256, 256, 256, 5)
-    o = O.Oracle(dim=3, degree=2, n=wl.n, lo=wl.lo, hi=wl.hi, bc=wl.bc, cfl=wl.cfl)
+    o = O.Oracle(dim=3, degree=2, n=wl.n, lo=wl.lo, hi=wl.hi, bc=wl.bc, cfl=wl.cfl, flux=flux)
     scale = np.array([1.0, 1.0, 1.0, 1.0, 2.5])
     boxes = [((0, 0, 0), (2, 2, 2)), ((254, 100, 127), (256, 102, 129)),   # corner / face
              ((62, 127, 127), (65, 129, 129)),                              # across r = 0.5
