@@ -51,6 +51,8 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=3)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-box", type=int, default=12, help="edge of the oracle sample box (cells)")
+    p.add_argument("--flux", default="rusanov", choices=["rusanov", "osher"],
+                   help="two-point flux (BASELINE: rusanov; the paper's explosions use osher)")
     return p.parse_args()
 
 
@@ -111,7 +113,7 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # CPU oracle sample (cpu_baseline and --impl reference)
 # ---------------------------------------------------------------------------
-def oracle_sample(wl, edge, reps=1):
+def oracle_sample(wl, edge, reps=1, flux=0):
     """Time the oracle (single thread, as it stands) on `reps` sub-boxes of the
     workload: one step of an edge^d box straddling the initial discontinuity
     (explosion) / the vortex core.  Returns (cell-updates/s, description)."""
@@ -122,7 +124,7 @@ def oracle_sample(wl, edge, reps=1):
         n = tuple([edge] * wl.dim)
         a = O.AmrOracle(dim=wl.dim, degree=wl.degree, n=n, lo=wl.lo, hi=wl.hi, bc=wl.bc, system=wl.system,
                         gamma=wl.gamma, ch=wl.ch, cfl=wl.cfl, lmax=wl.lmax, refine_factor=wl.refine_factor,
-                        chi_ref=wl.chi_ref, chi_rec=wl.chi_rec)
+                        chi_ref=wl.chi_ref, chi_rec=wl.chi_rec, flux=flux)
         a.set_initial(wl.ic)
         ups, secs = 0, 0.0
         for _ in range(reps):
@@ -134,7 +136,7 @@ def oracle_sample(wl, edge, reps=1):
                 f"AMR oracle, single thread")
         return ups / secs, desc, ups, secs
     o = O.Oracle(dim=wl.dim, degree=wl.degree, n=wl.n, lo=wl.lo, hi=wl.hi, bc=wl.bc, system=wl.system,
-                 gamma=wl.gamma, ch=wl.ch, cfl=wl.cfl)
+                 gamma=wl.gamma, ch=wl.ch, cfl=wl.cfl, flux=flux)
     n = wl.n
     if wl.name.startswith("c4") or wl.name.startswith("c3"):
         # centre the box on x = 0.5 (r = R on the x axis), mid-plane in y, z
@@ -170,16 +172,18 @@ def run_reference(args, wl):
     if rank != 0:
         return
     edge = max(2, args.cpu_box // 2)
+    fl = 1 if args.flux == "osher" else 0
     for _ in range(args.warmup):
-        oracle_sample(wl, edge)
+        oracle_sample(wl, edge, flux=fl)
     tot_u, tot_s = 0, 0.0
     desc = ""
     for _ in range(args.steps):
-        _, desc, u, s = oracle_sample(wl, edge)
+        _, desc, u, s = oracle_sample(wl, edge, flux=fl)
         tot_u += u
         tot_s += s
     val = tot_u / tot_s
-    cfgd = {"workload": wl.name, "dim": wl.dim, "degree": wl.degree, "cells": list(wl.n), "system": "euler" if wl.system == 0 else "mhd_glm"}
+    cfgd = {"workload": wl.name, "dim": wl.dim, "degree": wl.degree, "cells": list(wl.n),
+            "system": "euler" if wl.system == 0 else "mhd_glm", "flux": args.flux}
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * tot_s / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfgd,
@@ -228,7 +232,7 @@ def main():
     cfg = ader.make_config(dim=wl.dim, degree=wl.degree, n0=wl.n, lo=wl.lo, hi=wl.hi, bc=wl.bc, system=wl.system,
                            gamma=wl.gamma, ch=wl.ch, cfl=wl.cfl, rank=rank, world_size=world, device=local,
                            nccl_id=nid, lmax=wl.lmax, refine_factor=wl.refine_factor, adapt_every=1,
-                           chi_ref=wl.chi_ref, chi_rec=wl.chi_rec)
+                           chi_ref=wl.chi_ref, chi_rec=wl.chi_rec, flux=1 if args.flux == "osher" else 0)
     s = ader.Solver(cfg)
     stream = torch.cuda.current_stream()
     s.set_stream(stream.cuda_stream)
@@ -356,11 +360,11 @@ def main():
             f_gbs = fl_bytes / (fl_ms / 1e3) / 1e9
             f_tf = fl_flops / (fl_ms / 1e3) / 1e12
             f_ai = fl_flops / fl_bytes
-            roof_flux = {"kernel": "face_flux_rusanov", "bound": "alu" if f_ai >= ridge else "hbm",
+            roof_flux = {"kernel": f"face_flux_{args.flux}", "bound": "alu" if f_ai >= ridge else "hbm",
                          "achieved": f_tf if f_ai >= ridge else f_gbs, "peak": peak if f_ai >= ridge else hbm_peak,
                          "unit": "TFLOP/s" if f_ai >= ridge else "GB/s",
                          "frac": (f_tf / peak) if f_ai >= ridge else (f_gbs / hbm_peak),
-                         "traffic": load_traffic(wl, "face_flux_rusanov"), "arith_intensity_flop_per_byte": f_ai,
+                         "traffic": load_traffic(wl, f"face_flux_{args.flux}"), "arith_intensity_flop_per_byte": f_ai,
                          "alu_tflops": f_tf, "hbm_gbs": f_gbs,
                          "achieved_note": "algorithmic bytes (each q read once, F written) / CUDA-event time"}
         dominant = roof
@@ -374,7 +378,7 @@ def main():
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": wl.name, "dim": wl.dim, "degree": wl.degree, "order": wl.degree + 1,
                        "cells": list(wl.n), "system": "euler" if wl.system == 0 else "mhd_glm",
-                       "flux": "rusanov", "cfl": wl.cfl, "ic": "explosion r<0.5" if "explosion" in wl.name else wl.name,
+                       "flux": args.flux, "cfl": wl.cfl, "ic": "explosion r<0.5" if "explosion" in wl.name else wl.name,
                        "parallelism": f"level-0 blocks x{world}", "l2": "inputs larger than L2 (~90 GB working set)"},
             "roofline": dominant,
             "roofline_kernels": [r for r in (roof, roof_flux) if r is not None],
@@ -386,7 +390,7 @@ def main():
             "ic_setup_s": t_ic,
         }
         if world == 1 and not args.no_cpu_baseline:
-            v, desc, u, secs = oracle_sample(wl, args.cpu_box)
+            v, desc, u, secs = oracle_sample(wl, args.cpu_box, flux=1 if args.flux == "osher" else 0)
             line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc,
                                     "cell_updates": u, "seconds": secs, "host_nproc": os.cpu_count()}
         print(json.dumps(line), flush=True)

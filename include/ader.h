@@ -177,6 +177,16 @@ ader_status ader_kernel_stats(ader_ctx* c, double ms[ADER_K_COUNT], int64_t laun
                               double flops[ADER_K_COUNT]);
 /* Number of kernels this context has launched since ader_create. */
 ader_status ader_launch_count(const ader_ctx* c, int64_t* n);
+/* Test-only rank group in ONE process on one GPU (no NCCL): creates the n
+ * contexts of the partition of cfg (rank i = out[i], world_size = n, uniform
+ * grids only) whose ghost slabs are exchanged by device-to-device copies in
+ * ader_debug_group_step, which advances all of them in lockstep (same phases
+ * as ader_step; the CFL max over ranks is taken on the host).  Used to check
+ * that the partitioned path reproduces the one-rank result bitwise.  Release
+ * each context with ader_destroy.  reps may be NULL or hold n reports. */
+ader_status ader_debug_group_create(const ader_config* cfg, int32_t n, ader_ctx** out);
+ader_status ader_debug_group_step(ader_ctx** ctxs, int32_t n, double t_end, int64_t max_macro_steps,
+                                  ader_step_report* reps);
 /* sizeof of the ABI structs as compiled into the library (no GPU needed), so a
  * binding can check its layout: what = 0 ader_config, 1 ader_step_report,
  * 2 ader_cell, 3 ader_partition_info, 4 ader_halo_desc; -1 for other values. */

@@ -20,7 +20,7 @@ EULER, MHD_GLM = 0, 1
 PERIODIC, TRANSMISSIVE = 0, 1
 RUSANOV, OSHER = 0, 1
 K_WENO, K_PRED, K_FLUX, K_UPDATE, K_HALO, K_OTHER, K_COUNT = range(7)
-KERNEL_NAMES = ("weno_reconstruct", "stdg_predictor", "face_flux_rusanov", "fv_update", "halo", "other")
+KERNEL_NAMES = ("weno_reconstruct", "stdg_predictor", "face_flux", "fv_update", "halo", "other")
 STATUS = {0: "ADER_OK", 1: "ADER_ERR_ARG", 2: "ADER_ERR_CONFIG", 3: "ADER_ERR_SOLVER", 4: "ADER_ERR_CUDA",
           5: "ADER_ERR_NCCL", 6: "ADER_ERR_UNSUPPORTED"}
 
@@ -101,6 +101,9 @@ def lib():
         L.ader_kernel_stats.argtypes = [vp, dp, C.POINTER(C.c_int64), dp]
         L.ader_launch_count.argtypes = [vp, C.POINTER(C.c_int64)]
         L.ader_debug_dump.argtypes = [vp, C.c_int32, C.c_double, dp, C.c_int64]
+        L.ader_debug_group_create.argtypes = [C.POINTER(AderConfig), C.c_int32, C.POINTER(vp)]
+        L.ader_debug_group_step.argtypes = [C.POINTER(vp), C.c_int32, C.c_double, C.c_int64,
+                                            C.POINTER(AderStepReport)]
         L.ader_sizeof.restype = C.c_int64
         L.ader_sizeof.argtypes = [C.c_int32]
         _LIB = L
@@ -110,7 +113,8 @@ def lib():
 EXPORTED = ("ader_create", "ader_destroy", "ader_last_error", "ader_set_stream", "ader_set_initial",
             "ader_set_cells", "ader_get_state", "ader_get_cells", "ader_time", "ader_step", "ader_refine",
             "ader_partition", "ader_halo_plan", "ader_nccl_unique_id", "ader_set_profiling", "ader_kernel_stats",
-            "ader_launch_count", "ader_debug_dump", "ader_sizeof")
+            "ader_launch_count", "ader_debug_dump", "ader_sizeof", "ader_debug_group_create",
+            "ader_debug_group_step")
 
 
 def _dp(a):
@@ -276,4 +280,71 @@ class Solver:
             e = [b + 1 for b in self.block] + ([1] if d == 2 else [])
             out = np.zeros((d, int(np.prod(e)), nv))
         self._chk(lib().ader_debug_dump(self.ptr, what, dt, _dp(out), out.size))
+        return out
+
+
+class LoopbackGroup:
+    """Test-only: the n ranks of a partition as contexts in this process on one
+    GPU, stepped in lockstep with device-copy halo exchange (ader_debug_group_*)."""
+
+    def __init__(self, cfg: AderConfig, n: int):
+        self.cfg, self.n = cfg, n
+        self.ptrs = (C.c_void_p * n)()
+        st = lib().ader_debug_group_create(C.byref(cfg), n, self.ptrs)
+        if st:
+            raise AderError(st, lib().ader_last_error(None).decode())
+        self.nv = 9 if cfg.system == MHD_GLM else cfg.dim + 2
+        self.parts = []
+        for r in range(n):
+            c = AderConfig.from_buffer_copy(cfg)
+            c.rank, c.world_size = r, n
+            self.parts.append(ader_partition(c, r))
+
+    def close(self):
+        for i in range(self.n):
+            if self.ptrs[i]:
+                lib().ader_destroy(self.ptrs[i])
+                self.ptrs[i] = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_initial(self, ic):
+        def cb(xp, n, pp, user):
+            x = np.ctypeslib.as_array(xp, shape=(n, 3))
+            p = np.ctypeslib.as_array(pp, shape=(n, 9))
+            p[:] = ic(x)
+        self._cb = IC_FN(cb)
+        for i in range(self.n):
+            st = lib().ader_set_initial(self.ptrs[i], self._cb, None)
+            if st:
+                raise AderError(st, lib().ader_last_error(self.ptrs[i]).decode())
+
+    def step(self, t_end=1e300, max_steps=1):
+        reps = (AderStepReport * self.n)()
+        st = lib().ader_debug_group_step(self.ptrs, self.n, t_end, max_steps, reps)
+        if st:
+            raise AderError(st, lib().ader_last_error(self.ptrs[0]).decode())
+        return list(reps)
+
+    def gather(self):
+        """Global state [z][y][x][nv] assembled from the ranks' owned blocks."""
+        d = self.cfg.dim
+        n0 = [self.cfg.n0[k] for k in range(3)]
+        out = np.zeros((n0[2], n0[1], n0[0], self.nv))
+        for i, pi in enumerate(self.parts):
+            lo = [pi.lo[k] for k in range(3)]
+            hi = [pi.hi[k] for k in range(3)]
+            if d == 2:
+                lo[2], hi[2] = 0, 1
+            cnt = (hi[0] - lo[0]) * (hi[1] - lo[1]) * (hi[2] - lo[2])
+            buf = np.empty((cnt, self.nv))
+            st = lib().ader_get_state(self.ptrs[i], _dp(buf), cnt)
+            if st:
+                raise AderError(st, lib().ader_last_error(self.ptrs[i]).decode())
+            out[lo[2]:hi[2], lo[1]:hi[1], lo[0]:hi[0]] = buf.reshape(hi[2] - lo[2], hi[1] - lo[1], hi[0] - lo[0],
+                                                                     self.nv)
         return out

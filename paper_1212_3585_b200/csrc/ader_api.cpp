@@ -83,6 +83,7 @@ struct ader_ctx {
   double t = 0.0;
   bool speed_valid = false;
   ncclComm_t comm = nullptr;
+  bool loopback = false;                       // test-only rank group in one process (ader_debug_group_*)
   std::string err;
   // instrumentation
   bool prof = false;
@@ -319,33 +320,55 @@ void halo_plan(int d, int H, const int n[3], const int P[3], const ader_partitio
 
 Box desc_box(const int32_t* lo, const int32_t* hi) { return make_box(lo[0], hi[0], lo[1], hi[1], lo[2], hi[2]); }
 
+void axis_plans(const ader_ctx* c, int a, ader_halo_desc* dl, ader_halo_desc* dh) {
+  halo_plan(c->d, c->H, c->n, c->P, c->part, c->cfg.rank, c->cfg.bc, a, 0, dl);
+  halo_plan(c->d, c->H, c->n, c->P, c->part, c->cfg.rank, c->cfg.bc, a, 1, dh);
+}
+
+// Ghost layers of axis a in three phases: pack the slabs remote peers need,
+// exchange them (NCCL, or the loopback copy of ader_debug_group_step), then
+// unpack + fill the local sides.
+void halo_pack(ader_ctx* c, double* u, int a) {
+  ader_halo_desc dl, dh;
+  axis_plans(c, a, &dl, &dh);
+  if (dl.kind == 1) launch_pack(c->k, u, desc_box(dl.send_lo, dl.send_hi), c->sendb[2 * a]);
+  if (dh.kind == 1) launch_pack(c->k, u, desc_box(dh.send_lo, dh.send_hi), c->sendb[2 * a + 1]);
+}
+
+ader_status halo_exchange_nccl(ader_ctx* c, int a) {
+  ader_halo_desc dl, dh;
+  axis_plans(c, a, &dl, &dh);
+  const bool remote_lo = dl.kind == 1, remote_hi = dh.kind == 1;
+  if (!remote_lo && !remote_hi) return ADER_OK;
+  const size_t cnt = (size_t)desc_box(dl.recv_lo, dl.recv_hi).count() * c->nv;
+  NK(g_nccl.GroupStart());
+  // order per peer: (send low, recv high, send high, recv low) on every rank
+  if (remote_lo) NK(g_nccl.Send(c->sendb[2 * a], cnt, ncclDouble, dl.peer, c->comm, c->k.stream));
+  if (remote_hi) NK(g_nccl.Recv(c->recvb[2 * a + 1], cnt, ncclDouble, dh.peer, c->comm, c->k.stream));
+  if (remote_hi) NK(g_nccl.Send(c->sendb[2 * a + 1], cnt, ncclDouble, dh.peer, c->comm, c->k.stream));
+  if (remote_lo) NK(g_nccl.Recv(c->recvb[2 * a], cnt, ncclDouble, dl.peer, c->comm, c->k.stream));
+  NK(g_nccl.GroupEnd());
+  return ADER_OK;
+}
+
+void halo_unpack_local(ader_ctx* c, double* u, int a) {
+  ader_halo_desc dl, dh;
+  axis_plans(c, a, &dl, &dh);
+  const Box rlo = desc_box(dl.recv_lo, dl.recv_hi), rhi = desc_box(dh.recv_lo, dh.recv_hi);
+  if (dl.kind == 1) launch_unpack(c->k, u, rlo, c->recvb[2 * a]);
+  if (dh.kind == 1) launch_unpack(c->k, u, rhi, c->recvb[2 * a + 1]);
+  // local sides: periodic wrap onto ourselves, or transmissive copy (reading R5)
+  if (dl.kind != 1) launch_fill_axis(c->k, u, rlo, a, dl.kind == 2 ? 0 : 1, c->H, c->n[a]);
+  if (dh.kind != 1) launch_fill_axis(c->k, u, rhi, a, dh.kind == 2 ? 0 : 1, c->H, c->n[a]);
+}
+
 ader_status fill_halo(ader_ctx* c, double* u) {
   Scope sc(c, ADER_K_HALO, 0.0);
-  const int H = c->H;
   for (int a = 0; a < c->d; ++a) {
-    ader_halo_desc dl, dh;
-    halo_plan(c->d, H, c->n, c->P, c->part, c->cfg.rank, c->cfg.bc, a, 0, &dl);
-    halo_plan(c->d, H, c->n, c->P, c->part, c->cfg.rank, c->cfg.bc, a, 1, &dh);
-    const bool remote_lo = dl.kind == 1, remote_hi = dh.kind == 1;
-    const Box rlo = desc_box(dl.recv_lo, dl.recv_hi), rhi = desc_box(dh.recv_lo, dh.recv_hi);
-    const Box slo = desc_box(dl.send_lo, dl.send_hi), shi = desc_box(dh.send_lo, dh.send_hi);
-    if (remote_lo || remote_hi) {
-      if (remote_lo) launch_pack(c->k, u, slo, c->sendb[2 * a]);
-      if (remote_hi) launch_pack(c->k, u, shi, c->sendb[2 * a + 1]);
-      const size_t cnt = (size_t)rlo.count() * c->nv;
-      NK(g_nccl.GroupStart());
-      // order per peer: (send low, recv high, send high, recv low) on every rank
-      if (remote_lo) NK(g_nccl.Send(c->sendb[2 * a], cnt, ncclDouble, dl.peer, c->comm, c->k.stream));
-      if (remote_hi) NK(g_nccl.Recv(c->recvb[2 * a + 1], cnt, ncclDouble, dh.peer, c->comm, c->k.stream));
-      if (remote_hi) NK(g_nccl.Send(c->sendb[2 * a + 1], cnt, ncclDouble, dh.peer, c->comm, c->k.stream));
-      if (remote_lo) NK(g_nccl.Recv(c->recvb[2 * a], cnt, ncclDouble, dl.peer, c->comm, c->k.stream));
-      NK(g_nccl.GroupEnd());
-      if (remote_lo) launch_unpack(c->k, u, rlo, c->recvb[2 * a]);
-      if (remote_hi) launch_unpack(c->k, u, rhi, c->recvb[2 * a + 1]);
-    }
-    // local sides: periodic wrap onto ourselves, or transmissive copy (reading R5)
-    if (!remote_lo) launch_fill_axis(c->k, u, rlo, a, dl.kind == 2 ? 0 : 1, H, c->n[a]);
-    if (!remote_hi) launch_fill_axis(c->k, u, rhi, a, dh.kind == 2 ? 0 : 1, H, c->n[a]);
+    halo_pack(c, u, a);
+    ader_status st = halo_exchange_nccl(c, a);
+    if (st != ADER_OK) return st;
+    halo_unpack_local(c, u, a);
   }
   return ADER_OK;
 }
@@ -554,7 +577,7 @@ ader_status ader_nccl_unique_id(uint8_t out[128]) {
   return ADER_OK;
 }
 
-static ader_status create_impl(const ader_config* cfg, ader_ctx** out);
+static ader_status create_impl(const ader_config* cfg, ader_ctx** out, bool loopback = false);
 
 ader_status ader_create(const ader_config* cfg, ader_ctx** out) {
   if (!cfg || !out) return ADER_ERR_ARG;
@@ -576,7 +599,7 @@ ader_status ader_create(const ader_config* cfg, ader_ctx** out) {
   return ADER_OK;
 }
 
-static ader_status create_impl(const ader_config* cfg, ader_ctx** out) {
+static ader_status create_impl(const ader_config* cfg, ader_ctx** out, bool loopback) {
   ader_partition_info pi;
   partition(cfg, cfg->rank, &pi);
   const int H = cfg->degree + 1;
@@ -667,11 +690,14 @@ static ader_status create_impl(const ader_config* cfg, ader_ctx** out) {
     cap = std::max(cap, s);
   }
   c->halo_cap = cap * c->nv;
+  c->loopback = loopback;
   if (cfg->world_size > 1) {
     for (int i = 0; i < 2 * c->d; ++i) {
       CK(alloc(&c->sendb[i], (size_t)c->halo_cap));
       CK(alloc(&c->recvb[i], (size_t)c->halo_cap));
     }
+  }
+  if (cfg->world_size > 1 && !loopback) {
     std::string err;
     if (!g_nccl.load(err)) return fail(c, ADER_ERR_NCCL, "%s", err.c_str());
     ncclUniqueId id;
@@ -802,6 +828,65 @@ ader_status ader_get_cells(const ader_ctx* cc, ader_cell* out, int64_t capacity,
   return ADER_OK;
 }
 
+namespace {
+// second half of a uniform macro step, after the ghost fill + WENO: predictor,
+// face fluxes, update (fused with the next CFL speed)
+void advance_dt(ader_ctx* c, double dt) {
+  run_predictor(c, dt);
+  run_flux(c);
+  cudaMemsetAsync(&c->cnt->speed_bits, 0, sizeof(unsigned long long), c->k.stream);
+  run_update(c, dt);
+  c->speed_valid = true;   // computed by the update of the new state
+  c->t += dt;
+}
+
+ader_status step_begin(ader_ctx* c, unsigned long long* sw0, unsigned long long* pc0) {
+  CK(cudaMemcpyAsync(c->hcnt, c->cnt, sizeof(DevCounters), cudaMemcpyDeviceToHost, c->k.stream));
+  CK(cudaStreamSynchronize(c->k.stream));
+  *sw0 = c->hcnt->sweeps;
+  *pc0 = c->hcnt->cells;
+  return ADER_OK;
+}
+
+ader_status step_finish(ader_ctx* c, ader_status st, ader_step_report* r, unsigned long long sw0,
+                        unsigned long long pc0) {
+  CK(cudaMemcpyAsync(c->hcnt, c->cnt, sizeof(DevCounters), cudaMemcpyDeviceToHost, c->k.stream));
+  CK(cudaStreamSynchronize(c->k.stream));
+  if (st == ADER_OK) st = check_errors(c);
+  r->t = c->t;
+  r->cell_updates = r->macro_steps * owned(c).count();
+  r->updates_per_level[0] = r->cell_updates;
+  r->pred_sweeps_total = (int64_t)(c->hcnt->sweeps - sw0);
+  r->pred_cells = (int64_t)(c->hcnt->cells - pc0);
+  r->pred_sweeps_max = c->hcnt->sweeps_max;
+  // conserved totals (diagnostic): block partials on device, summed in order here
+  const Box b = owned(c);
+  double vol = 1.0;
+  for (int k = 0; k < c->d; ++k) vol *= c->dx[k];
+  const int maxb = (int)((b.count() + 255) / 256);
+  double* part = nullptr;
+  if (cudaMalloc(&part, (size_t)maxb * c->nv * sizeof(double)) == cudaSuccess) {
+    const int nb = launch_cons_partials(c->k, c->u, b, vol, part, maxb);
+    std::vector<double> h((size_t)nb * c->nv);
+    cudaMemcpyAsync(h.data(), part, h.size() * sizeof(double), cudaMemcpyDeviceToHost, c->k.stream);
+    cudaStreamSynchronize(c->k.stream);
+    for (int i = 0; i < nb; ++i)
+      for (int v = 0; v < c->nv; ++v) r->cons_total[v] += h[(size_t)i * c->nv + v];
+    cudaFree(part);
+  }
+  return st;
+}
+
+// Reading R1: dt = CFL / speed, clipped to t_end.
+ader_status dt_from_speed(ader_ctx* c, double speed, double t_end, double* dt) {
+  double v = c->cfg.cfl / speed;
+  if (!(v > 0.0) || !std::isfinite(v)) return fail(c, ADER_ERR_SOLVER, "invalid dt %g at t=%.17g", v, c->t);
+  if (c->t + v > t_end) v = t_end - c->t;
+  *dt = v;
+  return ADER_OK;
+}
+}  // namespace
+
 ader_status ader_step(ader_ctx* c, double t_end, int64_t max_macro_steps, ader_step_report* rep) {
   if (!c) return ADER_ERR_ARG;
   const auto w0 = std::chrono::steady_clock::now();
@@ -812,60 +897,114 @@ ader_status ader_step(ader_ctx* c, double t_end, int64_t max_macro_steps, ader_s
     if (rep) rep->wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - w0).count();
     return s;
   }
+  if (c->loopback) return fail(c, ADER_ERR_ARG, "group contexts step through ader_debug_group_step");
   ader_step_report r;
   std::memset(&r, 0, sizeof(r));
-  CK(cudaMemcpyAsync(c->hcnt, c->cnt, sizeof(DevCounters), cudaMemcpyDeviceToHost, c->k.stream));
-  CK(cudaStreamSynchronize(c->k.stream));
-  const unsigned long long sw0 = c->hcnt->sweeps, pc0 = c->hcnt->cells;
-  const long long owned_cells = owned(c).count();
-  ader_status st = ADER_OK;
+  unsigned long long sw0 = 0, pc0 = 0;
+  ader_status st = step_begin(c, &sw0, &pc0);
+  if (st != ADER_OK) return st;
   while (r.macro_steps < max_macro_steps && c->t < t_end) {
     st = fill_halo(c, c->u);
     if (st != ADER_OK) break;
     run_weno(c);
-    double speed = 0.0;
+    double speed = 0.0, dt = 0.0;
     st = global_speed(c, &speed);   // overlaps the WENO sweeps
     if (st != ADER_OK) break;
-    double dt = c->cfg.cfl / speed;   // reading R1
-    if (!(dt > 0.0) || !std::isfinite(dt)) { st = fail(c, ADER_ERR_SOLVER, "invalid dt %g at t=%.17g", dt, c->t); break; }
-    if (c->t + dt > t_end) dt = t_end - c->t;
-    run_predictor(c, dt);
-    run_flux(c);
-    CK(cudaMemsetAsync(&c->cnt->speed_bits, 0, sizeof(unsigned long long), c->k.stream));
-    run_update(c, dt);
-    c->speed_valid = true;   // computed by the update of the new state
-    c->t += dt;
+    st = dt_from_speed(c, speed, t_end, &dt);
+    if (st != ADER_OK) break;
+    advance_dt(c, dt);
     r.dt0 = dt;
     r.macro_steps++;
   }
-  CK(cudaMemcpyAsync(c->hcnt, c->cnt, sizeof(DevCounters), cudaMemcpyDeviceToHost, c->k.stream));
-  CK(cudaStreamSynchronize(c->k.stream));
-  if (st == ADER_OK) st = check_errors(c);
-  r.t = c->t;
-  r.cell_updates = r.macro_steps * owned_cells;
-  r.updates_per_level[0] = r.cell_updates;
-  r.pred_sweeps_total = (int64_t)(c->hcnt->sweeps - sw0);
-  r.pred_cells = (int64_t)(c->hcnt->cells - pc0);
-  r.pred_sweeps_max = c->hcnt->sweeps_max;
-  // conserved totals (diagnostic): block partials on device, summed in order here
-  {
-    const Box b = owned(c);
-    double vol = 1.0;
-    for (int k = 0; k < c->d; ++k) vol *= c->dx[k];
-    const int maxb = (int)((b.count() + 255) / 256);
-    double* part = nullptr;
-    if (cudaMalloc(&part, (size_t)maxb * c->nv * sizeof(double)) == cudaSuccess) {
-      const int nb = launch_cons_partials(c->k, c->u, b, vol, part, maxb);
-      std::vector<double> h((size_t)nb * c->nv);
-      cudaMemcpyAsync(h.data(), part, h.size() * sizeof(double), cudaMemcpyDeviceToHost, c->k.stream);
-      cudaStreamSynchronize(c->k.stream);
-      for (int i = 0; i < nb; ++i)
-        for (int v = 0; v < c->nv; ++v) r.cons_total[v] += h[(size_t)i * c->nv + v];
-      cudaFree(part);
-    }
-  }
+  st = step_finish(c, st, &r, sw0, pc0);
   r.wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - w0).count();
   if (rep) *rep = r;
+  return st;
+}
+
+// Test-only rank group in one process (ader.h): the ranks of a partition share
+// one GPU and step in lockstep; the halo slabs that NCCL would carry are copied
+// device to device between the contexts, the CFL max is taken on the host.
+ader_status ader_debug_group_create(const ader_config* cfg, int32_t n, ader_ctx** out) {
+  if (!cfg || !out || n < 1 || n > 8) return ADER_ERR_ARG;
+  for (int i = 0; i < n; ++i) out[i] = nullptr;
+  if (cfg->lmax > 0) return ADER_ERR_UNSUPPORTED;
+  for (int i = 0; i < n; ++i) {
+    ader_config ci = *cfg;
+    ci.rank = i;
+    ci.world_size = n;
+    std::string why;
+    ader_status st = validate(&ci, why);
+    if (st == ADER_OK) st = create_impl(&ci, &out[i], true);
+    if (st != ADER_OK) {
+      g_create_err = out[i] ? out[i]->err : why;
+      for (int j = 0; j <= i; ++j) { free_ctx(out[j]); out[j] = nullptr; }
+      return st;
+    }
+  }
+  return ADER_OK;
+}
+
+ader_status ader_debug_group_step(ader_ctx** cs, int32_t n, double t_end, int64_t max_macro_steps,
+                                  ader_step_report* reps) {
+  if (!cs || n < 1) return ADER_ERR_ARG;
+  for (int i = 0; i < n; ++i)
+    if (!cs[i] || !cs[i]->loopback || cs[i]->cfg.world_size != n || cs[i]->cfg.rank != i) return ADER_ERR_ARG;
+  ader_ctx* c = cs[0];
+  const int d = c->d;
+  std::vector<ader_step_report> r(n);
+  std::vector<unsigned long long> sw0(n), pc0(n);
+  ader_status st = ADER_OK;
+  for (int i = 0; i < n && st == ADER_OK; ++i) {
+    std::memset(&r[i], 0, sizeof(r[i]));
+    st = step_begin(cs[i], &sw0[i], &pc0[i]);
+  }
+  auto sync_all = [&]() {
+    for (int i = 0; i < n; ++i) cudaStreamSynchronize(cs[i]->k.stream);
+  };
+  int64_t steps = 0;
+  while (st == ADER_OK && steps < max_macro_steps && c->t < t_end) {
+    for (int a = 0; a < d; ++a) {
+      for (int i = 0; i < n; ++i) halo_pack(cs[i], cs[i]->u, a);
+      sync_all();
+      for (int i = 0; i < n; ++i) {
+        ader_halo_desc dl, dh;
+        axis_plans(cs[i], a, &dl, &dh);
+        const size_t bytes = (size_t)desc_box(dl.recv_lo, dl.recv_hi).count() * cs[i]->nv * sizeof(double);
+        // my low ghosts = the low neighbour's high slab, my high ghosts = the high neighbour's low slab
+        if (dl.kind == 1)
+          cudaMemcpyAsync(cs[i]->recvb[2 * a], cs[dl.peer]->sendb[2 * a + 1], bytes, cudaMemcpyDeviceToDevice,
+                          cs[i]->k.stream);
+        if (dh.kind == 1)
+          cudaMemcpyAsync(cs[i]->recvb[2 * a + 1], cs[dh.peer]->sendb[2 * a], bytes, cudaMemcpyDeviceToDevice,
+                          cs[i]->k.stream);
+      }
+      sync_all();
+      for (int i = 0; i < n; ++i) halo_unpack_local(cs[i], cs[i]->u, a);
+    }
+    double speed = 0.0;
+    for (int i = 0; i < n && st == ADER_OK; ++i) {
+      run_weno(cs[i]);
+      double s = 0.0;
+      st = global_speed(cs[i], &s);   // no communicator: this rank's max
+      speed = std::max(speed, s);
+    }
+    if (st != ADER_OK) break;
+    double dt = 0.0;
+    st = dt_from_speed(c, speed, t_end, &dt);
+    if (st != ADER_OK) break;
+    for (int i = 0; i < n; ++i) {
+      advance_dt(cs[i], dt);
+      r[i].dt0 = dt;
+      r[i].macro_steps++;
+    }
+    ++steps;
+  }
+  for (int i = 0; i < n; ++i) {
+    ader_status s2 = step_finish(cs[i], st, &r[i], sw0[i], pc0[i]);
+    if (st == ADER_OK && s2 != ADER_OK) { st = s2; if (i) c->err = cs[i]->err; }
+    if (reps) reps[i] = r[i];
+  }
   return st;
 }
 

@@ -364,7 +364,7 @@ struct TransposeReduce {
 constexpr int pow2_at_least(int x) { return x <= 1 ? 1 : 2 * pow2_at_least((x + 1) / 2); }
 
 template <int D, int M, int SYS, int WARPS, int YC, int FLUX>
-__global__ void __launch_bounds__(WARPS * 32) k_face_flux_cells(const double* __restrict__ q, double* __restrict__ F,
+__global__ void __launch_bounds__(WARPS * 32, (FLUX == 1) ? 5 : (SYS == 1 ? 4 : (D == 3 ? 6 : 8))) k_face_flux_cells(const double* __restrict__ q, double* __restrict__ F,
                                                                 const Box E, const int H, const int n0, const int n1,
                                                                 const int n2, const long long sy, const long long sz,
                                                                 const long long ncell, const double gamma,
@@ -677,10 +677,15 @@ void launch_face_flux_cells(const KCtx& k, const double* q, double* F, const Box
     const long long groups = (long long)ext.ext[0] * ych * YC * ext.ext[2];
     count_launch(k);
     const unsigned g = grid_for(groups, kFluxWarps * CPW);
-    if (SYS == 0 && k.tab.flux == 1)
-      k_face_flux_cells<D, M, SYS, kFluxWarps, YC, 1><<<g, kFluxWarps * 32, 0, k.stream>>>(
-          q, F, ext, H, n[0], n[1], n[2], k.sy, k.sz, k.ncell, k.gamma, k.ch, bmask, cnt, k.tab);
-    else
+    bool done = false;
+    if constexpr (SYS == 0) {
+      if (k.tab.flux == 1) {   // eqn.osher (Euler only, checked at ader_create)
+        k_face_flux_cells<D, M, SYS, kFluxWarps, YC, 1><<<g, kFluxWarps * 32, 0, k.stream>>>(
+            q, F, ext, H, n[0], n[1], n[2], k.sy, k.sz, k.ncell, k.gamma, k.ch, bmask, cnt, k.tab);
+        done = true;
+      }
+    }
+    if (!done)
       k_face_flux_cells<D, M, SYS, kFluxWarps, YC, 0><<<g, kFluxWarps * 32, 0, k.stream>>>(
           q, F, ext, H, n[0], n[1], n[2], k.sy, k.sz, k.ncell, k.gamma, k.ch, bmask, cnt, k.tab);
   });
