@@ -178,13 +178,18 @@ ader_status ader_kernel_stats(ader_ctx* c, double ms[ADER_K_COUNT], int64_t laun
 /* Number of kernels this context has launched since ader_create. */
 ader_status ader_launch_count(const ader_ctx* c, int64_t* n);
 /* Test-only rank group in ONE process on one GPU (no NCCL): creates the n
- * contexts of the partition of cfg (rank i = out[i], world_size = n, uniform
- * grids only) whose ghost slabs are exchanged by device-to-device copies in
- * ader_debug_group_step, which advances all of them in lockstep (same phases
- * as ader_step; the CFL max over ranks is taken on the host).  Used to check
- * that the partitioned path reproduces the one-rank result bitwise.  Release
- * each context with ader_destroy.  reps may be NULL or hold n reports. */
+ * contexts of the partition of cfg (rank i = out[i], world_size = n) whose
+ * exchanges (uniform: ghost slabs; AMR: owners' averages into the other ranks'
+ * compute bands, the global indicator) are device-to-device copies / host
+ * merges; ader_debug_group_set_initial and ader_debug_group_step run all of
+ * them in lockstep with the same phases as ader_set_initial / ader_step (the
+ * CFL max over ranks is taken on the host).  Used to check that the
+ * partitioned path reproduces the one-rank result bitwise.  ader_step,
+ * ader_refine (and, for AMR, ader_set_initial) on a group context return
+ * ADER_ERR_ARG.  Release each context with ader_destroy.  reps may be NULL or
+ * hold n reports.  ader_get_cells of an AMR rank returns its own subtrees. */
 ader_status ader_debug_group_create(const ader_config* cfg, int32_t n, ader_ctx** out);
+ader_status ader_debug_group_set_initial(ader_ctx** ctxs, int32_t n, ader_ic_fn ic, void* user);
 ader_status ader_debug_group_step(ader_ctx** ctxs, int32_t n, double t_end, int64_t max_macro_steps,
                                   ader_step_report* reps);
 /* sizeof of the ABI structs as compiled into the library (no GPU needed), so a

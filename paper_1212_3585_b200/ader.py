@@ -102,6 +102,7 @@ def lib():
         L.ader_launch_count.argtypes = [vp, C.POINTER(C.c_int64)]
         L.ader_debug_dump.argtypes = [vp, C.c_int32, C.c_double, dp, C.c_int64]
         L.ader_debug_group_create.argtypes = [C.POINTER(AderConfig), C.c_int32, C.POINTER(vp)]
+        L.ader_debug_group_set_initial.argtypes = [C.POINTER(vp), C.c_int32, IC_FN, vp]
         L.ader_debug_group_step.argtypes = [C.POINTER(vp), C.c_int32, C.c_double, C.c_int64,
                                             C.POINTER(AderStepReport)]
         L.ader_sizeof.restype = C.c_int64
@@ -114,7 +115,7 @@ EXPORTED = ("ader_create", "ader_destroy", "ader_last_error", "ader_set_stream",
             "ader_set_cells", "ader_get_state", "ader_get_cells", "ader_time", "ader_step", "ader_refine",
             "ader_partition", "ader_halo_plan", "ader_nccl_unique_id", "ader_set_profiling", "ader_kernel_stats",
             "ader_launch_count", "ader_debug_dump", "ader_sizeof", "ader_debug_group_create",
-            "ader_debug_group_step")
+            "ader_debug_group_set_initial", "ader_debug_group_step")
 
 
 def _dp(a):
@@ -318,10 +319,9 @@ class LoopbackGroup:
             p = np.ctypeslib.as_array(pp, shape=(n, 9))
             p[:] = ic(x)
         self._cb = IC_FN(cb)
-        for i in range(self.n):
-            st = lib().ader_set_initial(self.ptrs[i], self._cb, None)
-            if st:
-                raise AderError(st, lib().ader_last_error(self.ptrs[i]).decode())
+        st = lib().ader_debug_group_set_initial(self.ptrs, self.n, self._cb, None)
+        if st:
+            raise AderError(st, lib().ader_last_error(self.ptrs[0]).decode())
 
     def step(self, t_end=1e300, max_steps=1):
         reps = (AderStepReport * self.n)()
@@ -329,6 +329,20 @@ class LoopbackGroup:
         if st:
             raise AderError(st, lib().ader_last_error(self.ptrs[0]).decode())
         return list(reps)
+
+    def get_cells(self):
+        """AMR: the union of the ranks' own subtrees, as ader_cell records."""
+        out = []
+        for i in range(self.n):
+            n = C.c_int64(0)
+            st = lib().ader_get_cells(self.ptrs[i], None, 0, C.byref(n))
+            arr = (AderCell * n.value)()
+            if not st:
+                st = lib().ader_get_cells(self.ptrs[i], arr, n.value, C.byref(n))
+            if st:
+                raise AderError(st, lib().ader_last_error(self.ptrs[i]).decode())
+            out.extend(arr)
+        return out
 
     def gather(self):
         """Global state [z][y][x][nv] assembled from the ranks' owned blocks."""

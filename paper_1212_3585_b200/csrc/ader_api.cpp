@@ -58,6 +58,28 @@ struct NcclApi {
   }
 };
 NcclApi g_nccl;
+
+// AmrComm hooks over the context's communicator (ctx = ncclComm_t)
+ader_status amr_nccl_p2p(void* ctx, int n, const int* peers, double* const* sendp, const size_t* scount,
+                         double* const* recvp, const size_t* rcount, cudaStream_t st) {
+  ncclComm_t comm = (ncclComm_t)ctx;
+  if (g_nccl.GroupStart() != ncclSuccess) return ADER_ERR_NCCL;
+  bool ok = true;
+  for (int i = 0; i < n; ++i) {
+    if (scount[i]) ok &= g_nccl.Send(sendp[i], scount[i], ncclDouble, peers[i], comm, st) == ncclSuccess;
+    if (rcount[i]) ok &= g_nccl.Recv(recvp[i], rcount[i], ncclDouble, peers[i], comm, st) == ncclSuccess;
+  }
+  ok &= g_nccl.GroupEnd() == ncclSuccess;
+  return ok ? ADER_OK : ADER_ERR_NCCL;
+}
+ader_status amr_nccl_sum(void* ctx, double* buf, size_t n, cudaStream_t st) {
+  return g_nccl.AllReduce(buf, buf, n, ncclDouble, ncclSum, (ncclComm_t)ctx, st) == ncclSuccess ? ADER_OK
+                                                                                               : ADER_ERR_NCCL;
+}
+ader_status amr_nccl_max_u64(void* ctx, unsigned long long* buf, cudaStream_t st) {
+  return g_nccl.AllReduce(buf, buf, 1, ncclUint64, ncclMax, (ncclComm_t)ctx, st) == ncclSuccess ? ADER_OK
+                                                                                              : ADER_ERR_NCCL;
+}
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -141,7 +163,6 @@ ader_status validate(const ader_config* cfg, std::string& why) {
       return bad("periodic bc must be set on both sides of an axis");
   if (cfg->lmax < 0 || cfg->lmax > 7) return bad("lmax out of range");
   if (cfg->lmax > 0 && cfg->refine_factor < cfg->degree) return bad("refine_factor r must be >= M (P:539-541)");
-  if (cfg->lmax > 0 && cfg->world_size > 1) return ADER_ERR_UNSUPPORTED;   // AMR: one GPU (round 1)
   if (cfg->lmax > 0 && cfg->refine_factor > 4) return bad("refine_factor must be <= 4");
   if (cfg->lmax > 0 && cfg->ic_quad > 4) return bad("AMR ic_quad must be <= 4");
   if (!(cfg->gamma > 1.0)) return bad("gamma must exceed 1");
@@ -661,8 +682,33 @@ static ader_status create_impl(const ader_config* cfg, ader_ctx** out, bool loop
     CK(cudaMemset(c->cnt, 0, sizeof(DevCounters)));
     CK(cudaMallocHost(&c->hcnt, sizeof(DevCounters)));
     std::memset(c->hcnt, 0, sizeof(DevCounters));
+    AmrRanks ranks;
+    ranks.rank = cfg->rank;
+    ranks.world = cfg->world_size;
+    for (int p = 0; p < cfg->world_size; ++p) {
+      ader_partition_info pp;
+      partition(cfg, p, &pp);
+      for (int k = 0; k < 3; ++k) { ranks.lo[p][k] = pp.lo[k]; ranks.hi[p][k] = pp.hi[k]; }
+    }
+    AmrComm comm;
+    if (cfg->world_size > 1 && !loopback) {
+      std::string err;
+      if (!g_nccl.load(err)) return fail(c, ADER_ERR_NCCL, "%s", err.c_str());
+      ncclUniqueId id;
+      std::memcpy(&id, cfg->nccl_id, sizeof(id));
+      ncclResult_t r = g_nccl.CommInitRank(&c->comm, cfg->world_size, id, cfg->rank);
+      if (r != ncclSuccess) {
+        c->comm = nullptr;
+        return fail(c, ADER_ERR_NCCL, "ncclCommInitRank: %s", g_nccl.GetErrorString(r));
+      }
+      comm.ctx = c->comm;
+      comm.p2p = amr_nccl_p2p;
+      comm.sum = amr_nccl_sum;
+      comm.max_u64 = amr_nccl_max_u64;
+    }
+    c->loopback = loopback;
     std::string err;
-    c->amr = amr_create(cfg, &c->k, c->cnt, c->hcnt, err);
+    c->amr = amr_create(cfg, &c->k, c->cnt, c->hcnt, ranks, comm, err);
     if (!c->amr) return fail(c, ADER_ERR_CUDA, "amr_create: %s", err.c_str());
     return ADER_OK;
   }
@@ -724,6 +770,8 @@ double ader_time(const ader_ctx* c) { return c ? (c->amr ? amr_time(c->amr) : c-
 
 ader_status ader_set_initial(ader_ctx* c, ader_ic_fn ic, void* user) {
   if (!c || !ic) return ADER_ERR_ARG;
+  if (c->amr && c->loopback && c->cfg.world_size > 1)
+    return fail(c, ADER_ERR_ARG, "AMR group contexts are initialised through ader_debug_group_set_initial");
   if (c->amr) {
     std::string e;
     ader_status s = amr_set_initial(c->amr, ic, user, e);
@@ -890,6 +938,7 @@ ader_status dt_from_speed(ader_ctx* c, double speed, double t_end, double* dt) {
 ader_status ader_step(ader_ctx* c, double t_end, int64_t max_macro_steps, ader_step_report* rep) {
   if (!c) return ADER_ERR_ARG;
   const auto w0 = std::chrono::steady_clock::now();
+  if (c->loopback) return fail(c, ADER_ERR_ARG, "group contexts step through ader_debug_group_step");
   if (c->amr) {
     std::string e;
     ader_status s = amr_step(c->amr, t_end, max_macro_steps, rep, e);
@@ -897,7 +946,6 @@ ader_status ader_step(ader_ctx* c, double t_end, int64_t max_macro_steps, ader_s
     if (rep) rep->wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - w0).count();
     return s;
   }
-  if (c->loopback) return fail(c, ADER_ERR_ARG, "group contexts step through ader_debug_group_step");
   ader_step_report r;
   std::memset(&r, 0, sizeof(r));
   unsigned long long sw0 = 0, pc0 = 0;
@@ -928,7 +976,6 @@ ader_status ader_step(ader_ctx* c, double t_end, int64_t max_macro_steps, ader_s
 ader_status ader_debug_group_create(const ader_config* cfg, int32_t n, ader_ctx** out) {
   if (!cfg || !out || n < 1 || n > 8) return ADER_ERR_ARG;
   for (int i = 0; i < n; ++i) out[i] = nullptr;
-  if (cfg->lmax > 0) return ADER_ERR_UNSUPPORTED;
   for (int i = 0; i < n; ++i) {
     ader_config ci = *cfg;
     ci.rank = i;
@@ -945,12 +992,44 @@ ader_status ader_debug_group_create(const ader_config* cfg, int32_t n, ader_ctx*
   return ADER_OK;
 }
 
+ader_status ader_debug_group_set_initial(ader_ctx** cs, int32_t n, ader_ic_fn ic, void* user) {
+  if (!cs || n < 1 || !ic) return ADER_ERR_ARG;
+  for (int i = 0; i < n; ++i)
+    if (!cs[i] || !cs[i]->loopback || cs[i]->cfg.world_size != n || cs[i]->cfg.rank != i ||
+        (cs[i]->amr != nullptr) != (cs[0]->amr != nullptr))
+      return ADER_ERR_ARG;
+  if (!cs[0]->amr) {
+    for (int i = 0; i < n; ++i) {
+      ader_status s = ader_set_initial(cs[i], ic, user);
+      if (s != ADER_OK) return s;
+    }
+    return ADER_OK;
+  }
+  std::vector<AmrState*> g(n);
+  for (int i = 0; i < n; ++i) g[i] = cs[i]->amr;
+  std::string e;
+  ader_status s = amr_group_set_initial(g.data(), n, ic, user, e);
+  if (s != ADER_OK) cs[0]->err = e;
+  return s;
+}
+
 ader_status ader_debug_group_step(ader_ctx** cs, int32_t n, double t_end, int64_t max_macro_steps,
                                   ader_step_report* reps) {
   if (!cs || n < 1) return ADER_ERR_ARG;
   for (int i = 0; i < n; ++i)
     if (!cs[i] || !cs[i]->loopback || cs[i]->cfg.world_size != n || cs[i]->cfg.rank != i) return ADER_ERR_ARG;
   ader_ctx* c = cs[0];
+  if (c->amr) {
+    std::vector<AmrState*> g(n);
+    for (int i = 0; i < n; ++i) {
+      if (!cs[i]->amr) return ADER_ERR_ARG;
+      g[i] = cs[i]->amr;
+    }
+    std::string e;
+    ader_status s = amr_group_step(g.data(), n, t_end, max_macro_steps, reps, e);
+    if (s != ADER_OK) c->err = e;
+    return s;
+  }
   const int d = c->d;
   std::vector<ader_step_report> r(n);
   std::vector<unsigned long long> sw0(n), pc0(n);
@@ -1011,6 +1090,7 @@ ader_status ader_debug_group_step(ader_ctx** cs, int32_t n, double t_end, int64_
 ader_status ader_refine(ader_ctx* c, ader_step_report* rep) {
   if (!c) return ADER_ERR_ARG;
   if (rep) std::memset(rep, 0, sizeof(*rep));
+  if (c->loopback && c->cfg.world_size > 1) return fail(c, ADER_ERR_ARG, "group contexts adapt inside ader_debug_group_step");
   if (c->amr) {
     std::string e;
     ader_status s = amr_adapt(c->amr, e);

@@ -60,6 +60,22 @@ struct AmrState {
   size_t dscratch_cap = 0;
   char* hstage = nullptr;
   size_t hstage_cap = 0;
+  // multi-rank (amr.h): ownership, compute set, owned active lists, exchange plans
+  AmrRanks ranks;
+  AmrComm comm;
+  int band = 0;                                       // compute-set margin in level-0 cells
+  std::vector<char> own, comp;                        // per id
+  long long nlev[kAmrMaxLevels]{};                    // alive cells per level (whole tree)
+  std::vector<int> lown[kAmrMaxLevels], lownall;      // owned active cells
+  long long oown[kAmrMaxLevels]{}, oownall = 0;
+  struct XPlan {                                      // per level, ids ascending per peer
+    std::vector<int> sids, rids;
+    std::vector<long long> soff, roff;                // [world + 1] offsets into sids / rids
+    long long dso = 0, dro = 0;                       // their offsets inside dlist
+  } xp[kAmrMaxLevels];
+  double* xsend = nullptr;
+  double* xrecv = nullptr;
+  size_t xcap = 0;                                    // doubles
 };
 
 namespace {
@@ -104,6 +120,38 @@ struct AScope {
 };
 
 long long lin(const AmrState* A, int l, const long long* ix) { return (ix[2] * A->n[l][1] + ix[1]) * A->n[l][0] + ix[0]; }
+
+// level-0 ancestor index of a cell
+void ancestor0(const AmrState* A, const HCell& C, long long a[3]) {
+  long long f = 1;
+  for (int l = 0; l < C.level; ++l) f *= A->r;
+  for (int k = 0; k < 3; ++k) a[k] = k < A->d ? C.idx[k] / f : 0;
+}
+
+int owner_of(const AmrState* A, const long long a[3]) {
+  for (int p = 0; p < A->ranks.world; ++p) {
+    bool in = true;
+    for (int k = 0; k < A->d && in; ++k) in = a[k] >= A->ranks.lo[p][k] && a[k] < A->ranks.hi[p][k];
+    if (in) return p;
+  }
+  return -1;
+}
+
+// is level-0 cell a within `band` cells (per axis, periodic wrap) of rank p's block?
+bool in_comp(const AmrState* A, int p, const long long a[3]) {
+  for (int k = 0; k < A->d; ++k) {
+    const long long lo = A->ranks.lo[p][k], hi = A->ranks.hi[p][k] - 1, n0 = A->n[0][k];
+    const bool per = A->cfg.bc[2 * k] == ADER_BC_PERIODIC;
+    long long best = -1;
+    for (int sh = per ? -1 : 0; sh <= (per ? 1 : 0); ++sh) {
+      const long long x = a[k] + sh * n0;
+      const long long dd = x < lo ? lo - x : (x > hi ? x - hi : 0);
+      if (best < 0 || dd < best) best = dd;
+    }
+    if (best > A->band) return false;
+  }
+  return true;
+}
 
 int hlookup(const AmrState* A, int l, const long long* ix0, bool skip_outside) {
   long long ix[3] = {ix0[0], ix0[1], ix0[2]};
@@ -256,6 +304,7 @@ ader_status ensure_capacity(AmrState* A, std::string& err) {
   ACK(grow((void**)&V.mother, sizeof(int)));
   ACK(grow((void**)&V.child, sizeof(int)));
   ACK(grow((void**)&V.idx, sizeof(long long) * 3));
+  if (A->ranks.world > 1) ACK(grow((void**)&V.own, 1));
   A->cap = nc;
   return ADER_OK;
 }
@@ -319,24 +368,79 @@ ader_status upload_topology(AmrState* A, std::string& err) {
     if (C.alive && (!P.alive || !same_pos)) { sets.push_back(C.level); sets.push_back(lin(A, C.level, C.idx)); sets.push_back(i); }
     P = C;
   }
-  for (int l = 0; l <= A->lmax; ++l) { A->lact[l].clear(); A->lvch[l].clear(); A->lvmo[l].clear(); }
+  for (int l = 0; l <= A->lmax; ++l) {
+    A->lact[l].clear(); A->lvch[l].clear(); A->lvmo[l].clear(); A->lown[l].clear();
+    A->xp[l] = AmrState::XPlan();
+  }
   A->lall.clear();
+  A->lownall.clear();
+  const int W = A->ranks.world, me = A->ranks.rank;
+  A->own.assign(nu, 0);
+  A->comp.assign(nu, 0);
+  std::vector<int> owner(W > 1 ? nu : 0, -1);
+  std::vector<std::vector<int>> send_to(W > 1 ? (size_t)(A->lmax + 1) * W : 0);
+  for (int l = 0; l < kAmrMaxLevels; ++l) A->nlev[l] = 0;
   for (int i = 0; i < nu; ++i) {
     const HCell& C = A->cells[i];
     if (!C.alive) continue;
+    A->nlev[C.level]++;
+    if (W > 1) {
+      long long a0[3];
+      ancestor0(A, C, a0);
+      owner[i] = owner_of(A, a0);
+      A->own[i] = owner[i] == me;
+      A->comp[i] = A->own[i] || in_comp(A, me, a0);
+      if (A->own[i] && C.status == 0)
+        for (int p = 0; p < W; ++p)
+          if (p != me && in_comp(A, p, a0)) send_to[(size_t)C.level * W + p].push_back(i);
+    } else {
+      A->own[i] = A->comp[i] = 1;
+    }
+    if (!A->comp[i]) continue;
     if (C.status == 0) A->lact[C.level].push_back(i);
     else if (C.status == 1) A->lvch[C.level].push_back(i);
     else A->lvmo[C.level].push_back(i);
+    if (A->own[i] && C.status == 0) A->lown[C.level].push_back(i);
   }
+  size_t xneed = 0;
+  if (W > 1)
+    for (int l = 0; l <= A->lmax; ++l) {
+      AmrState::XPlan& X = A->xp[l];
+      X.soff.assign(W + 1, 0);
+      X.roff.assign(W + 1, 0);
+      for (int p = 0; p < W; ++p) {
+        X.soff[p] = (long long)X.sids.size();
+        if (p != me) X.sids.insert(X.sids.end(), send_to[(size_t)l * W + p].begin(), send_to[(size_t)l * W + p].end());
+        X.roff[p] = (long long)X.rids.size();
+        if (p != me)
+          for (int i : A->lact[l])
+            if (owner[i] == p) X.rids.push_back(i);
+      }
+      X.soff[W] = (long long)X.sids.size();
+      X.roff[W] = (long long)X.rids.size();
+      xneed = std::max(xneed, std::max(X.sids.size(), X.rids.size()) * (size_t)A->nv);
+    }
   std::vector<int> all;
   for (int l = 0; l <= A->lmax; ++l) {
     A->oact[l] = (long long)all.size(); all.insert(all.end(), A->lact[l].begin(), A->lact[l].end());
     A->ovch[l] = (long long)all.size(); all.insert(all.end(), A->lvch[l].begin(), A->lvch[l].end());
     A->ovmo[l] = (long long)all.size(); all.insert(all.end(), A->lvmo[l].begin(), A->lvmo[l].end());
+    A->oown[l] = (long long)all.size(); all.insert(all.end(), A->lown[l].begin(), A->lown[l].end());
+    A->xp[l].dso = (long long)all.size(); all.insert(all.end(), A->xp[l].sids.begin(), A->xp[l].sids.end());
+    A->xp[l].dro = (long long)all.size(); all.insert(all.end(), A->xp[l].rids.begin(), A->xp[l].rids.end());
     A->lall.insert(A->lall.end(), A->lact[l].begin(), A->lact[l].end());
+    A->lownall.insert(A->lownall.end(), A->lown[l].begin(), A->lown[l].end());
   }
   A->oall = (long long)all.size();
   all.insert(all.end(), A->lall.begin(), A->lall.end());
+  A->oownall = (long long)all.size();
+  all.insert(all.end(), A->lownall.begin(), A->lownall.end());
+  if (xneed > A->xcap) {
+    if (A->xsend) { cudaStreamSynchronize(A->k->stream); cudaFree(A->xsend); cudaFree(A->xrecv); }
+    A->xcap = xneed * 3 / 2 + 1024;
+    ACK(cudaMalloc(&A->xsend, sizeof(double) * A->xcap));
+    ACK(cudaMalloc(&A->xrecv, sizeof(double) * A->xcap));
+  }
   cudaStream_t sm = A->k->stream;
   if ((long long)all.size() > A->dlist_cap) {
     if (A->dlist) { cudaStreamSynchronize(sm); cudaFree(A->dlist); }
@@ -348,8 +452,10 @@ ader_status upload_topology(AmrState* A, std::string& err) {
   const size_t oc = up.add(clears.data(), clears.size() * sizeof(long long));
   const size_t os = up.add(sets.data(), sets.size() * sizeof(long long));
   const size_t ol = up.add(all.data(), all.size() * sizeof(int));
+  const size_t oo = W > 1 ? up.add(A->own.data(), A->own.size()) : 0;
   s = up.run(err);
   if (s != ADER_OK) return s;
+  if (W > 1) ACK(cudaMemcpyAsync(A->V.own, A->dscratch + oo, A->own.size(), cudaMemcpyDeviceToDevice, sm));
   amr_launch_meta_scatter(*A->k, A->V, (const long long*)(A->dscratch + om), (int)(meta.size() / 8));
   amr_launch_map_set(*A->k, A->V, (const long long*)(A->dscratch + oc), (int)(clears.size() / 3));
   amr_launch_map_set(*A->k, A->V, (const long long*)(A->dscratch + os), (int)(sets.size() / 3));
@@ -438,16 +544,81 @@ ader_status run_inits(AmrState* A, std::string& err) {
   return ic_cells(A, ic, err);
 }
 
-ader_status fetch_speed(AmrState* A, double* speed, std::string& err) {
-  cudaStream_t sm = A->k->stream;
-  ACK(cudaMemsetAsync(&A->cnt->speed_bits, 0, sizeof(unsigned long long), sm));
-  double inv[3] = {0, 0, 0};
-  for (int k = 0; k < A->d; ++k) inv[k] = 1.0 / A->dx[0][k];
-  amr_launch_cfl(*A->k, A->V, A->dlist + A->oall, (int)A->lall.size(), inv, A->cnt);
-  ACK(cudaMemcpyAsync(A->hcnt, A->cnt, sizeof(DevCounters), cudaMemcpyDeviceToHost, sm));
-  ACK(cudaStreamSynchronize(sm));
-  unsigned long long b = A->hcnt->speed_bits;
-  std::memcpy(speed, &b, sizeof(double));
+using Group = std::vector<AmrState*>;
+
+// CFL speed (reading R1) over the owned active cells, maximised over the ranks
+ader_status fetch_speed(const Group& G, double* speed, std::string& err) {
+  double best = 0.0;
+  for (AmrState* A : G) {
+    cudaStream_t sm = A->k->stream;
+    ACK(cudaMemsetAsync(&A->cnt->speed_bits, 0, sizeof(unsigned long long), sm));
+    double inv[3] = {0, 0, 0};
+    for (int k = 0; k < A->d; ++k) inv[k] = 1.0 / A->dx[0][k];
+    amr_launch_cfl(*A->k, A->V, A->dlist + A->oownall, (int)A->lownall.size(), inv, A->cnt);
+    if (G.size() == 1 && A->ranks.world > 1) {
+      ader_status s = A->comm.max_u64(A->comm.ctx, &A->cnt->speed_bits, sm);
+      if (s != ADER_OK) { err = "allreduce(max) of the CFL speed failed"; return s; }
+    }
+    ACK(cudaMemcpyAsync(A->hcnt, A->cnt, sizeof(DevCounters), cudaMemcpyDeviceToHost, sm));
+    ACK(cudaStreamSynchronize(sm));
+    unsigned long long b = A->hcnt->speed_bits;
+    double v;
+    std::memcpy(&v, &b, sizeof(double));
+    best = std::max(best, v);
+  }
+  *speed = best;
+  return ADER_OK;
+}
+
+// Owners' new averages of the active cells of level l overwrite the other
+// ranks' copies (compute-set band); NCCL through the hooks for one context per
+// rank, device copies inside a loopback group.
+ader_status exchange(const Group& G, int l, std::string& err) {
+  if (G[0]->ranks.world <= 1) return ADER_OK;
+  for (AmrState* A : G) {
+    const AmrState::XPlan& X = A->xp[l];
+    amr_launch_rows_gather(*A->k, A->V.u, A->dlist + X.dso, (int)X.sids.size(), A->nv, A->xsend);
+  }
+  const int W = G[0]->ranks.world;
+  if (G.size() > 1) {
+    for (AmrState* A : G) ACK(cudaStreamSynchronize(A->k->stream));
+    for (AmrState* A : G) {
+      const int me = A->ranks.rank;
+      for (int p = 0; p < W; ++p) {
+        if (p == me) continue;
+        const AmrState* P = G[p];
+        const long long n = A->xp[l].roff[p + 1] - A->xp[l].roff[p];
+        if (n != P->xp[l].soff[me + 1] - P->xp[l].soff[me]) { err = "exchange plans disagree"; return ADER_ERR_SOLVER; }
+        if (n)
+          ACK(cudaMemcpyAsync(A->xrecv + A->xp[l].roff[p] * A->nv, P->xsend + P->xp[l].soff[me] * A->nv,
+                              sizeof(double) * n * A->nv, cudaMemcpyDeviceToDevice, A->k->stream));
+      }
+    }
+    // the peers' send buffers are reused by their next exchange
+    for (AmrState* A : G) ACK(cudaStreamSynchronize(A->k->stream));
+  } else {
+    AmrState* A = G[0];
+    const AmrState::XPlan& X = A->xp[l];
+    std::vector<int> peers;
+    std::vector<double*> sp, rp;
+    std::vector<size_t> sc, rc;
+    for (int p = 0; p < W; ++p) {
+      const size_t ns = (size_t)(X.soff[p + 1] - X.soff[p]), nr = (size_t)(X.roff[p + 1] - X.roff[p]);
+      if (p == A->ranks.rank || (!ns && !nr)) continue;
+      peers.push_back(p);
+      sp.push_back(A->xsend + X.soff[p] * A->nv); sc.push_back(ns * A->nv);
+      rp.push_back(A->xrecv + X.roff[p] * A->nv); rc.push_back(nr * A->nv);
+    }
+    if (!peers.empty()) {
+      ader_status s = A->comm.p2p(A->comm.ctx, (int)peers.size(), peers.data(), sp.data(), sc.data(), rp.data(),
+                                  rc.data(), A->k->stream);
+      if (s != ADER_OK) { err = "halo exchange of the AMR averages failed"; return s; }
+    }
+  }
+  for (AmrState* A : G) {
+    const AmrState::XPlan& X = A->xp[l];
+    amr_launch_rows_scatter(*A->k, A->V.u, A->dlist + X.dro, (int)X.rids.size(), A->nv, A->xrecv);
+  }
   return ADER_OK;
 }
 
@@ -469,43 +640,55 @@ ader_status check_err(AmrState* A, std::string& err) {
 }
 
 // ---- local time stepping (recursive form of eqn.update.criterion, R15) -------
-void advance(AmrState* A, int l, int m, double dt0) {
+ader_status advance(const Group& G, int l, int m, double dt0, std::string& err) {
+  AmrState* A0 = G[0];
   double dt = dt0;
-  for (int k = 0; k < l; ++k) dt /= A->r;
+  for (int k = 0; k < l; ++k) dt /= A0->r;
   double dtdx[3] = {0, 0, 0};
-  for (int k = 0; k < A->d; ++k) dtdx[k] = dt / A->dx[l][k];
-  // ghost refresh (R16): averaging of virtual mothers on levels >= l, finest first
-  {
-    AScope sc(A, ADER_K_HALO, 0.0);
-    for (int lv = A->lmax - 1; lv >= l; --lv) amr_launch_average(*A->k, A->V, L_vmo(A, lv), (int)A->lvmo[lv].size());
-    if (l >= 1) {
-      double pt[4];
-      psi_at(A, (double)m / A->r, pt);
-      amr_launch_project(*A->k, A->V, A->st, L_vch(A, l), (int)A->lvch[l].size(), pt);
+  for (int k = 0; k < A0->d; ++k) dtdx[k] = dt / A0->dx[l][k];
+  for (AmrState* A : G) {
+    // ghost refresh (R16): averaging of virtual mothers on levels >= l, finest first
+    {
+      AScope sc(A, ADER_K_HALO, 0.0);
+      for (int lv = A->lmax - 1; lv >= l; --lv) amr_launch_average(*A->k, A->V, L_vmo(A, lv), (int)A->lvmo[lv].size());
+      if (l >= 1) {
+        double pt[4];
+        psi_at(A, (double)m / A->r, pt);
+        amr_launch_project(*A->k, A->V, A->st, L_vch(A, l), (int)A->lvch[l].size(), pt);
+      }
     }
+    const int na = (int)A->lact[l].size();
+    const int W = 2 * A->M + 1;
+    double wfl = 0.0;   // 1D WENO problems of the per-cell box reconstruction
+    {
+      double per = 0.0, rows = 1.0;
+      for (int k = 0; k < A->d; ++k) { per += rows * (A->d - k == 1 ? 1.0 : std::pow((double)W, A->d - 1 - k)); rows *= A->N; }
+      const int N = A->N, nS = (A->M % 2 == 0) ? 3 : 4;
+      wfl = (double)na * A->nv * per * (nS * (4.0 * N * N + 2.0 * N + 6.0) + 1.0 + 3.0 * N * nS);
+    }
+    { AScope sc(A, ADER_K_WENO, wfl); amr_launch_weno(*A->k, A->V, L_act(A, l), na); }
+    { AScope sc(A, ADER_K_PRED, 0.0);
+      amr_launch_predictor(*A->k, A->V, L_act(A, l), na, dtdx, A->cfg.pred_tol, A->cfg.pred_max_sweeps, A->cnt); }
   }
-  const int na = (int)A->lact[l].size();
-  const int W = 2 * A->M + 1;
-  double wfl = 0.0;   // 1D WENO problems of the per-cell box reconstruction
-  {
-    double per = 0.0, rows = 1.0;
-    for (int k = 0; k < A->d; ++k) { per += rows * (A->d - k == 1 ? 1.0 : std::pow((double)W, A->d - 1 - k)); rows *= A->N; }
-    const int N = A->N, nS = (A->M % 2 == 0) ? 3 : 4;
-    wfl = (double)na * A->nv * per * (nS * (4.0 * N * N + 2.0 * N + 6.0) + 1.0 + 3.0 * N * nS);
+  if (l < A0->lmax && A0->nlev[l + 1] > 0)
+    for (int k = 0; k < A0->r; ++k) {
+      ader_status s = advance(G, l + 1, k, dt0, err);
+      if (s != ADER_OK) return s;
+    }
+  for (AmrState* A : G) {
+    const int na = (int)A->lact[l].size();
+    { AScope sc(A, ADER_K_FLUX, 0.0); amr_launch_flux_update(*A->k, A->V, A->st, L_act(A, l), na, m, dtdx, A->cnt); }
+    A->updates[l] += (long long)A->lown[l].size();
   }
-  { AScope sc(A, ADER_K_WENO, wfl); amr_launch_weno(*A->k, A->V, L_act(A, l), na); }
-  { AScope sc(A, ADER_K_PRED, 0.0);
-    amr_launch_predictor(*A->k, A->V, L_act(A, l), na, dtdx, A->cfg.pred_tol, A->cfg.pred_max_sweeps, A->cnt); }
-  if (l < A->lmax && (A->lact[l + 1].size() + A->lvch[l + 1].size() + A->lvmo[l + 1].size()) > 0)
-    for (int k = 0; k < A->r; ++k) advance(A, l + 1, k, dt0);
-  { AScope sc(A, ADER_K_FLUX, 0.0); amr_launch_flux_update(*A->k, A->V, A->st, L_act(A, l), na, m, dtdx, A->cnt); }
-  A->updates[l] += na;
+  AScope sc(A0, ADER_K_HALO, 0.0);
+  return exchange(G, l, err);
 }
 
 // ---- adapt (rules 1-7) --------------------------------------------------------
-ader_status adapt(AmrState* A, bool t0, std::string& err) {
+// phase 1: ghost refresh at t^{n+1}, indicator and WENO polynomials of the
+// compute-set active cells (device); the local chi array comes back to the host
+ader_status adapt_indicator(AmrState* A, bool t0, std::vector<double>& chi, std::string& err) {
   cudaStream_t sm = A->k->stream;
-  int nb[26];
   if (!t0) {
     // ghost refresh at t^{n+1}: averages (finest first), projections at tau = 1
     for (int lv = A->lmax - 1; lv >= 0; --lv) amr_launch_average(*A->k, A->V, L_vmo(A, lv), (int)A->lvmo[lv].size());
@@ -518,9 +701,20 @@ ader_status adapt(AmrState* A, bool t0, std::string& err) {
   amr_launch_indicator(*A->k, A->V, A->dlist + A->oall, na, A->cfg.chi_eps);
   if (!t0)
     for (int l = 0; l <= A->lmax; ++l) amr_launch_weno(*A->k, A->V, L_act(A, l), (int)A->lact[l].size());
-  std::vector<double> chi(A->cells.size(), 0.0);
+  chi.assign(A->cells.size(), 0.0);
   ACK(cudaMemcpyAsync(chi.data(), A->V.chi, sizeof(double) * A->cells.size(), cudaMemcpyDeviceToHost, sm));
   ACK(cudaStreamSynchronize(sm));
+  // only the owner's chi is authoritative (its 3^d box lies inside the band)
+  for (size_t i = 0; i < chi.size(); ++i)
+    if (i >= A->own.size() || !A->own[i]) chi[i] = 0.0;
+  return ADER_OK;
+}
+
+// phase 2 (same on every rank, on the global chi): marks, closure, simultaneous
+// recoarsening, GC, device topology, new-cell initialisation
+ader_status adapt_apply(AmrState* A, bool t0, const std::vector<double>& chi, std::string& err) {
+  cudaStream_t sm = A->k->stream;
+  int nb[26];
   for (auto& c : A->cells) c.isnew = false;
   const int nu = (int)A->cells.size();
   std::vector<char> mark(nu, 0);
@@ -609,13 +803,52 @@ ader_status adapt(AmrState* A, bool t0, std::string& err) {
   return ADER_OK;
 }
 
+// One adapt pass of every rank of the group on the global indicator.
+ader_status adapt(const Group& G, bool t0, std::string& err) {
+  std::vector<double> chi, mine;
+  for (AmrState* A : G) {
+    ader_status s = adapt_indicator(A, t0, mine, err);
+    if (s != ADER_OK) return s;
+    if (chi.size() < mine.size()) chi.resize(mine.size(), 0.0);
+    for (size_t i = 0; i < mine.size(); ++i) chi[i] += mine[i];   // one owner per cell: exact
+  }
+  AmrState* A0 = G[0];
+  if (G.size() == 1 && A0->ranks.world > 1 && !chi.empty()) {
+    cudaStream_t sm = A0->k->stream;
+    ACK(cudaMemcpyAsync(A0->V.chi, chi.data(), sizeof(double) * chi.size(), cudaMemcpyHostToDevice, sm));
+    ader_status s = A0->comm.sum(A0->comm.ctx, A0->V.chi, chi.size(), sm);
+    if (s != ADER_OK) { err = "allreduce(sum) of the indicator failed"; return s; }
+    ACK(cudaMemcpyAsync(chi.data(), A0->V.chi, sizeof(double) * chi.size(), cudaMemcpyDeviceToHost, sm));
+    ACK(cudaStreamSynchronize(sm));
+  }
+  for (AmrState* A : G) {
+    ader_status s = adapt_apply(A, t0, chi, err);
+    if (s != ADER_OK) return s;
+  }
+  // the band copies of new / re-initialised active cells come from their owners
+  for (int l = 0; l <= A0->lmax; ++l) {
+    ader_status s = exchange(G, l, err);
+    if (s != ADER_OK) return s;
+  }
+  for (AmrState* A : G) ACK(cudaStreamSynchronize(A->k->stream));
+  return ADER_OK;
+}
+
 }  // namespace
 
 // ===========================================================================
-AmrState* amr_create(const ader_config* cfg, KCtx* k, DevCounters* cnt, DevCounters* hcnt, std::string& err) {
+AmrState* amr_create(const ader_config* cfg, KCtx* k, DevCounters* cnt, DevCounters* hcnt, const AmrRanks& ranks,
+                     const AmrComm& comm, std::string& err) {
   AmrState* A = new AmrState();
   A->cfg = *cfg;
   A->k = k; A->cnt = cnt; A->hcnt = hcnt;
+  A->ranks = ranks;
+  A->comm = comm;
+  // compute-set margin: the dependency chain of an owned update (face
+  // neighbours' predictors, their WENO boxes, the coarser mothers projected into
+  // virtual children, finer cells depositing flux memory) stays within
+  // (M+1) sum_l r^-l < 2 (M+1) level-0 cells of the owned block for r >= M
+  A->band = 2 * (cfg->degree + 1);
   A->d = cfg->dim; A->M = cfg->degree; A->N = A->M + 1;
   A->nv = cfg->system == ADER_MHD_GLM ? 9 : cfg->dim + 2;
   A->NS = 1;
@@ -661,7 +894,7 @@ void amr_destroy(AmrState* A) {
   if (!A) return;
   cudaStreamSynchronize(A->k->stream);
   void* ps[] = {A->V.u, A->V.mem, A->V.w, A->V.q, A->V.chi, A->V.level, A->V.status, A->V.mother, A->V.child, A->V.idx,
-                A->dlist};
+                A->V.own, A->dlist, A->xsend, A->xrecv};
   for (void* p : ps)
     if (p) cudaFree(p);
   for (int l = 0; l < kAmrMaxLevels; ++l)
@@ -675,67 +908,98 @@ double amr_time(const AmrState* A) { return A->t; }
 
 int64_t amr_num_active(const AmrState* A) { return (int64_t)A->lall.size(); }
 
-ader_status amr_set_initial(AmrState* A, ader_ic_fn ic, void* user, std::string& err) {
-  A->ic = ic; A->user = user;
-  std::vector<int> ids;
-  for (int i = 0; i < (int)A->cells.size(); ++i)
-    if (A->cells[i].alive) ids.push_back(i);
-  ader_status s = ic_cells(A, ids, err);
-  if (s != ADER_OK) return s;
-  for (int l = 0; l < A->lmax; ++l) {     // initial hierarchy (R20)
-    s = adapt(A, true, err);
+namespace {
+ader_status set_initial(const Group& G, ader_ic_fn ic, void* user, std::string& err) {
+  for (AmrState* A : G) {
+    A->ic = ic; A->user = user;
+    std::vector<int> ids;
+    for (int i = 0; i < (int)A->cells.size(); ++i)
+      if (A->cells[i].alive) ids.push_back(i);
+    ader_status s = ic_cells(A, ids, err);
     if (s != ADER_OK) return s;
   }
-  A->t = 0.0;
+  for (int l = 0; l < G[0]->lmax; ++l) {     // initial hierarchy (R20)
+    ader_status s = adapt(G, true, err);
+    if (s != ADER_OK) return s;
+  }
+  for (AmrState* A : G) A->t = 0.0;
   return ADER_OK;
 }
 
-ader_status amr_adapt(AmrState* A, std::string& err) { return adapt(A, false, err); }
-
-ader_status amr_step(AmrState* A, double t_end, int64_t max_steps, ader_step_report* rep, std::string& err) {
-  ader_step_report R;
-  std::memset(&R, 0, sizeof(R));
-  for (int l = 0; l < kAmrMaxLevels; ++l) A->updates[l] = 0;
+ader_status step(const Group& G, double t_end, int64_t max_steps, ader_step_report* reps, std::string& err) {
+  const size_t n = G.size();
+  std::vector<ader_step_report> R(n);
+  std::vector<unsigned long long> sw0(n), pc0(n);
+  for (size_t i = 0; i < n; ++i) {
+    AmrState* A = G[i];
+    std::memset(&R[i], 0, sizeof(R[i]));
+    for (int l = 0; l < kAmrMaxLevels; ++l) A->updates[l] = 0;
+    ACK(cudaMemcpyAsync(A->hcnt, A->cnt, sizeof(DevCounters), cudaMemcpyDeviceToHost, A->k->stream));
+    ACK(cudaStreamSynchronize(A->k->stream));
+    sw0[i] = A->hcnt->sweeps; pc0[i] = A->hcnt->cells;
+  }
   ader_status s = ADER_OK;
-  cudaStream_t sm = A->k->stream;
-  ACK(cudaMemcpyAsync(A->hcnt, A->cnt, sizeof(DevCounters), cudaMemcpyDeviceToHost, sm));
-  ACK(cudaStreamSynchronize(sm));
-  const unsigned long long sw0 = A->hcnt->sweeps, pc0 = A->hcnt->cells;
-  while (R.macro_steps < max_steps && A->t < t_end) {
+  AmrState* A0 = G[0];
+  int64_t steps = 0;
+  while (steps < max_steps && A0->t < t_end) {
     double speed = 0.0;
-    s = fetch_speed(A, &speed, err);
+    s = fetch_speed(G, &speed, err);
+    for (size_t i = 0; i < n && s == ADER_OK; ++i) s = check_err(G[i], err);
     if (s != ADER_OK) break;
-    s = check_err(A, err);
-    if (s != ADER_OK) break;
-    double dt = A->cfg.cfl / speed;
+    double dt = A0->cfg.cfl / speed;
     if (!(dt > 0.0) || !std::isfinite(dt)) { err = "invalid dt"; s = ADER_ERR_SOLVER; break; }
-    if (A->t + dt > t_end) dt = t_end - A->t;
-    advance(A, 0, 0, dt);
-    s = check_err(A, err);
+    if (A0->t + dt > t_end) dt = t_end - A0->t;
+    s = advance(G, 0, 0, dt, err);
+    for (size_t i = 0; i < n && s == ADER_OK; ++i) s = check_err(G[i], err);
     if (s != ADER_OK) break;
-    A->t += dt;
-    R.dt0 = dt;
-    R.macro_steps++;
-    if (A->cfg.adapt_every > 0 && R.macro_steps % A->cfg.adapt_every == 0) {
-      s = adapt(A, false, err);
+    for (size_t i = 0; i < n; ++i) { G[i]->t += dt; R[i].dt0 = dt; R[i].macro_steps++; }
+    ++steps;
+    if (A0->cfg.adapt_every > 0 && steps % A0->cfg.adapt_every == 0) {
+      s = adapt(G, false, err);
       if (s != ADER_OK) break;
     }
   }
-  ACK(cudaMemcpyAsync(A->hcnt, A->cnt, sizeof(DevCounters), cudaMemcpyDeviceToHost, sm));
-  ACK(cudaStreamSynchronize(sm));
-  R.t = A->t;
-  for (int l = 0; l < kAmrMaxLevels && l <= A->lmax; ++l) { R.updates_per_level[l] = A->updates[l]; R.cell_updates += A->updates[l]; }
-  R.pred_sweeps_total = (int64_t)(A->hcnt->sweeps - sw0);
-  R.pred_cells = (int64_t)(A->hcnt->cells - pc0);
-  R.pred_sweeps_max = A->hcnt->sweeps_max;
-  if (rep) *rep = R;
+  for (size_t i = 0; i < n; ++i) {
+    AmrState* A = G[i];
+    ACK(cudaMemcpyAsync(A->hcnt, A->cnt, sizeof(DevCounters), cudaMemcpyDeviceToHost, A->k->stream));
+    ACK(cudaStreamSynchronize(A->k->stream));
+    R[i].t = A->t;
+    for (int l = 0; l < kAmrMaxLevels && l <= A->lmax; ++l) {
+      R[i].updates_per_level[l] = A->updates[l];
+      R[i].cell_updates += A->updates[l];
+    }
+    R[i].pred_sweeps_total = (int64_t)(A->hcnt->sweeps - sw0[i]);
+    R[i].pred_cells = (int64_t)(A->hcnt->cells - pc0[i]);
+    R[i].pred_sweeps_max = A->hcnt->sweeps_max;
+    if (reps) reps[i] = R[i];
+  }
   return s;
+}
+}  // namespace
+
+ader_status amr_set_initial(AmrState* A, ader_ic_fn ic, void* user, std::string& err) {
+  return set_initial(Group{A}, ic, user, err);
+}
+
+ader_status amr_adapt(AmrState* A, std::string& err) { return adapt(Group{A}, false, err); }
+
+ader_status amr_step(AmrState* A, double t_end, int64_t max_steps, ader_step_report* rep, std::string& err) {
+  return step(Group{A}, t_end, max_steps, rep, err);
+}
+
+ader_status amr_group_set_initial(AmrState* const* g, int n, ader_ic_fn ic, void* user, std::string& err) {
+  return set_initial(Group(g, g + n), ic, user, err);
+}
+
+ader_status amr_group_step(AmrState* const* g, int n, double t_end, int64_t max_steps, ader_step_report* reps,
+                           std::string& err) {
+  return step(Group(g, g + n), t_end, max_steps, reps, err);
 }
 
 ader_status amr_get_cells(AmrState* A, ader_cell* out, int64_t cap, int64_t* n, std::string& err) {
   int64_t cnt = 0;
   for (int l = 0; l <= A->lmax; ++l)
-    for (int id : A->hmap[l]) cnt += id >= 0;
+    for (int id : A->hmap[l]) cnt += id >= 0 && A->own[id];
   *n = cnt;
   if (!out) return ADER_OK;
   if (cap < cnt) { err = "capacity too small"; return ADER_ERR_ARG; }
@@ -745,7 +1009,7 @@ ader_status amr_get_cells(AmrState* A, ader_cell* out, int64_t cap, int64_t* n, 
   int64_t i = 0;
   for (int l = 0; l <= A->lmax; ++l)
     for (int id : A->hmap[l]) {
-      if (id < 0) continue;
+      if (id < 0 || !A->own[id]) continue;
       ader_cell& e = out[i++];
       std::memset(&e, 0, sizeof(e));
       const HCell& C = A->cells[id];

@@ -40,6 +40,7 @@ struct AmrDevView {            // raw device pointers handed to kernels
   double* chi;                 // [cap]
   int* level; int* status; int* mother; int* child;
   long long* idx;              // [cap][3]
+  unsigned char* own;          // [cap] multi-rank: 1 = this rank's cell (errors count); nullptr for one rank
   const int* map[kAmrMaxLevels];
   long long n[kAmrMaxLevels][3];
   int bc[6];
@@ -48,11 +49,39 @@ struct AmrDevView {            // raw device pointers handed to kernels
 
 struct AmrState;
 
-AmrState* amr_create(const ader_config* cfg, KCtx* k, DevCounters* cnt, DevCounters* hcnt, std::string& err);
+// Multi-rank AMR: every rank mirrors the whole tree (the adapt is
+// deterministic integer logic on the global indicator), owns the subtrees of
+// its level-0 block and computes the cells whose level-0 ancestor lies within
+// `band` level-0 cells of that block; after every level update the owners'
+// new averages overwrite the other ranks' copies.  With one context per rank
+// the collectives go through these hooks (NCCL, ader_api.cpp); a loopback
+// group (several contexts in one process) exchanges by device copies.
+struct AmrComm {
+  void* ctx = nullptr;
+  // grouped point-to-point: to peers[i] send scount[i] doubles from sendp[i],
+  // from peers[i] receive rcount[i] doubles into recvp[i]
+  ader_status (*p2p)(void* ctx, int n, const int* peers, double* const* sendp, const size_t* scount,
+                     double* const* recvp, const size_t* rcount, cudaStream_t s) = nullptr;
+  ader_status (*sum)(void* ctx, double* buf, size_t n, cudaStream_t s) = nullptr;            // in place
+  ader_status (*max_u64)(void* ctx, unsigned long long* buf, cudaStream_t s) = nullptr;      // in place
+};
+
+struct AmrRanks {
+  int rank = 0, world = 1;
+  int lo[8][3]{}, hi[8][3]{};   // level-0 block [lo, hi) of every rank
+};
+
+AmrState* amr_create(const ader_config* cfg, KCtx* k, DevCounters* cnt, DevCounters* hcnt, const AmrRanks& ranks,
+                     const AmrComm& comm, std::string& err);
 void amr_destroy(AmrState* a);
 ader_status amr_set_initial(AmrState* a, ader_ic_fn ic, void* user, std::string& err);
 ader_status amr_step(AmrState* a, double t_end, int64_t max_steps, ader_step_report* rep, std::string& err);
 ader_status amr_adapt(AmrState* a, std::string& err);
+// lockstep variants over the ranks of a loopback group (one process, one GPU)
+ader_status amr_group_set_initial(AmrState* const* g, int n, ader_ic_fn ic, void* user, std::string& err);
+ader_status amr_group_step(AmrState* const* g, int n, double t_end, int64_t max_steps, ader_step_report* reps,
+                           std::string& err);
+// cells of this rank's subtrees (all cells for one rank)
 ader_status amr_get_cells(AmrState* a, ader_cell* out, int64_t cap, int64_t* n, std::string& err);
 double amr_time(const AmrState* a);
 int64_t amr_num_active(const AmrState* a);
@@ -61,6 +90,8 @@ int64_t amr_num_active(const AmrState* a);
 void amr_launch_meta_scatter(const KCtx& k, const AmrDevView& v, const long long* meta, int n);
 void amr_launch_map_set(const KCtx& k, const AmrDevView& v, const long long* ch, int n);
 void amr_launch_zero_mem(const KCtx& k, const AmrDevView& v, const int* list, int n);
+void amr_launch_rows_gather(const KCtx& k, const double* u, const int* ids, int n, int nv, double* out);
+void amr_launch_rows_scatter(const KCtx& k, double* u, const int* ids, int n, int nv, const double* in);
 void amr_launch_average(const KCtx& k, const AmrDevView& v, const int* list, int n);
 void amr_launch_project(const KCtx& k, const AmrDevView& v, const SubTables& st, const int* list, int n,
                         const double* psi_tau);

@@ -342,7 +342,7 @@ __global__ void __launch_bounds__(64) k_amr_flux_update(AmrDevView V, const __gr
 #pragma unroll
     for (int v = 0; v < NV; ++v) uu[v] = uu[v] - dtdx[2] * (Fp[v] - Fm[v]);
   }
-  if (!ok) amr_error(cnt, 1, 2, c);
+  if (!ok && (!V.own || V.own[c])) amr_error(cnt, 1, 2, c);   // multi-rank: band cells' errors do not count
 #pragma unroll
   for (int v = 0; v < NV; ++v) V.u[(long long)c * NV + v] = uu[v];
 }
@@ -475,6 +475,20 @@ __global__ void k_amr_zero_mem(AmrDevView V, const int* __restrict__ list, int n
   V.mem[(long long)c * 6 * V.NV + j] = 0.0;
 }
 
+// multi-rank exchange of cell averages: out[i][v] = u[ids[i]][v] / u[ids[i]][v] = in[i][v]
+__global__ void k_amr_rows_gather(const double* __restrict__ u, const int* __restrict__ ids, int n, int nv,
+                                  double* __restrict__ out) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long long)n * nv) return;
+  out[i] = u[(long long)ids[i / nv] * nv + i % nv];
+}
+__global__ void k_amr_rows_scatter(double* __restrict__ u, const int* __restrict__ ids, int n, int nv,
+                                   const double* __restrict__ in) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long long)n * nv) return;
+  u[(long long)ids[i / nv] * nv + i % nv] = in[i];
+}
+
 // ===========================================================================
 // launchers
 // ===========================================================================
@@ -503,6 +517,18 @@ void amr_launch_map_set(const KCtx& k, const AmrDevView& v, const long long* ch,
   if (n <= 0) return;
   cl(k);
   k_amr_map_set<<<gsz(n, 256), 256, 0, k.stream>>>(v, ch, n);
+}
+
+void amr_launch_rows_gather(const KCtx& k, const double* u, const int* ids, int n, int nv, double* out) {
+  if (n <= 0) return;
+  cl(k);
+  k_amr_rows_gather<<<gsz((long long)n * nv, 256), 256, 0, k.stream>>>(u, ids, n, nv, out);
+}
+
+void amr_launch_rows_scatter(const KCtx& k, double* u, const int* ids, int n, int nv, const double* in) {
+  if (n <= 0) return;
+  cl(k);
+  k_amr_rows_scatter<<<gsz((long long)n * nv, 256), 256, 0, k.stream>>>(u, ids, n, nv, in);
 }
 
 void amr_launch_zero_mem(const KCtx& k, const AmrDevView& v, const int* list, int n) {
@@ -556,7 +582,7 @@ void amr_launch_predictor(const KCtx& k, const AmrDevView& v, const int* list, i
                           double tol, int max_sweeps, DevCounters* cnt) {
   if (n <= 0) return;
   Box none{{0, 0, 0}, {0, 0, 0}};
-  launch_predictor_list(k, v.w, v.q, none, list, n, dtdx, tol, max_sweeps, cnt);
+  launch_predictor_list(k, v.w, v.q, none, list, n, dtdx, tol, max_sweeps, cnt, v.own);
 }
 
 void amr_launch_flux_update(const KCtx& k, const AmrDevView& v, const SubTables& st, const int* list, int n, int m,

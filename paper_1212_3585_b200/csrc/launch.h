@@ -57,9 +57,11 @@ void launch_weno_sweep(const KCtx& k, int sweep, const double* src, double* dst,
 // Predictor on `region`: w -> q.
 void launch_predictor(const KCtx& k, const double* w, double* q, const Box& region, const double dtdx[3],
                       double tol, int max_sweeps, DevCounters* cnt);
-// Predictor on the cells of an id list (AMR levels): w, q indexed by id.
+// Predictor on the cells of an id list (AMR levels): w, q indexed by id.  If
+// emask is given only cells with emask[id] != 0 report solver errors.
 void launch_predictor_list(const KCtx& k, const double* w, double* q, const Box& region, const int* list,
-                           long long nlist, const double dtdx[3], double tol, int max_sweeps, DevCounters* cnt);
+                           long long nlist, const double dtdx[3], double tol, int max_sweeps, DevCounters* cnt,
+                           const unsigned char* emask = nullptr);
 // Face fluxes on the lower face of every cell of `ext` (owned block + 1 on each
 // active axis), one lane group per cell computing all its lower faces
 // (L2-friendly traversal).  bmask bit 2*dir (2*dir+1): the first (last) face

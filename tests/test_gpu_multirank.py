@@ -7,6 +7,12 @@ slabs NCCL would carry copied device to device and the CFL max taken on the
 host.  Every cell's arithmetic is local, so any partition must reproduce the
 one-rank state bit for bit.  Only the NCCL calls themselves
 are not exercised here (one GPU per box).
+
+AMR: every rank mirrors the tree, computes the cells whose level-0 ancestor
+lies within the band of its level-0 block, and the owners' new averages are
+copied into the other ranks' bands after every level update; the indicator is
+merged over the owners.  The union of the ranks' subtrees must equal the
+one-rank tree bit for bit (cell sets, statuses and averages).
 """
 import math
 
@@ -71,3 +77,48 @@ def test_group_rejects_thin_blocks_and_plain_step():
     st = ader.lib().ader_step(grp.ptrs[0], 1e300, 1, None)
     assert st == 1
     grp.close()
+
+
+AMR_CASES = {
+    "explosion2d_l2_x4": (dict(dim=2, degree=2, n0=(30, 30), lo=(-1, -1), hi=(1, 1), bc=(1,) * 6, lmax=2, cfl=0.45,
+                               chi_ref=0.1, chi_rec=0.05), W.explosion(2), 4, 4),
+    "explosion2d_l2_osher_x2": (dict(dim=2, degree=2, n0=(24, 20), lo=(-1, -1), hi=(1, 1), bc=(1,) * 6, lmax=2,
+                                     cfl=0.45, chi_ref=0.1, chi_rec=0.05, flux=1), W.explosion(2), 2, 3),
+    "vortex2d_M3_l1_periodic_x3": (dict(dim=2, degree=3, n0=(30, 24), lo=(0, 0), hi=(10, 10), bc=(0,) * 6, lmax=1,
+                                        cfl=0.9, chi_ref=0.01, chi_rec=0.005), W.isentropic_vortex(), 3, 3),
+    "ot_mhd_M3_l1_x4": (dict(dim=2, degree=3, n0=(32, 32), lo=(0, 0), hi=(2 * math.pi, 2 * math.pi), bc=(0,) * 6,
+                             lmax=1, system=1, gamma=5 / 3, ch=2.0, cfl=0.45, chi_ref=0.02, chi_rec=0.01),
+                        W.orszag_tang(), 4, 2),
+    "explosion3d_l1_x2": (dict(dim=3, degree=2, n0=(16, 10, 10), lo=(-1,) * 3, hi=(1,) * 3, bc=(1,) * 6, lmax=1,
+                               cfl=0.3), W.explosion(3), 2, 2),
+    "explosion2d_l2_x8_long": (dict(dim=2, degree=2, n0=(40, 32), lo=(-1, -1), hi=(1, 1), bc=(1,) * 6, lmax=2,
+                                    cfl=0.45, chi_ref=0.1, chi_rec=0.05), W.explosion(2), 8, 12),
+}
+
+
+def _key_sorted(cells, nv):
+    rows = sorted(((c.level, c.idx[2], c.idx[1], c.idx[0], c.status, tuple(c.u[:nv])) for c in cells))
+    return rows
+
+
+@pytest.mark.parametrize("name", list(AMR_CASES))
+def test_amr_partition_reproduces_one_rank_bitwise(name):
+    kw, ic, nr, steps = AMR_CASES[name]
+    nv = 9 if kw.get("system", 0) == 1 else kw["dim"] + 2
+    one = ader.Solver(ader.make_config(device=0, adapt_every=1, **kw))
+    one.set_initial(ic)
+    grp = ader.LoopbackGroup(ader.make_config(device=0, adapt_every=1, **kw), nr)
+    grp.set_initial(ic)
+    a, b = _key_sorted(one.get_cells(), nv), _key_sorted(grp.get_cells(), nv)
+    assert a == b                                      # initial hierarchy
+    r1 = one.step(1e300, steps)
+    reps = grp.step(1e300, steps)
+    assert all(r.dt0 == r1.dt0 for r in reps)
+    assert sum(r.cell_updates for r in reps) == r1.cell_updates
+    a, b = _key_sorted(one.get_cells(), nv), _key_sorted(grp.get_cells(), nv)
+    assert len(a) == len(b)
+    assert [x[:5] for x in a] == [x[:5] for x in b]    # cell sets and statuses
+    bad = [(x, y) for x, y in zip(a, b) if x != y]
+    assert not bad, bad[:3]                            # averages bit for bit
+    grp.close()
+    one.close()
