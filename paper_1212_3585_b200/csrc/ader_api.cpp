@@ -652,6 +652,9 @@ static ader_status create_impl(const ader_config* cfg, ader_ctx** out, bool loop
     c->inv_dx[k] = (k < c->d) ? 1.0 / c->dx[k] : 0.0;
   }
   c->ncell = (long long)c->P[0] * c->P[1] * c->P[2];
+  if (cfg->lmax == 0 && (double)c->ncell * c->nv * std::pow((double)c->N, c->d - 1) >= 4294967040.0)
+    return fail(c, ADER_ERR_CONFIG, "rank block of %lld padded cells exceeds the 32-bit kernel indexing; use more ranks",
+                c->ncell);
   if (cfg->device >= 0) CK(cudaSetDevice(cfg->device));
   int dev = 0;
   CK(cudaGetDevice(&dev));

@@ -57,26 +57,27 @@ __global__ void __launch_bounds__(256) k_weno(const double* __restrict__ src, do
   constexpr int N = M + 1;
   constexpr int NT = ipow_c(N, K);
   constexpr int NIN = NV * NT;
-  const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  long long cell;
-  int inner;
+  // 32-bit index decomposition (the launcher guarantees < 2^32 threads)
+  const unsigned gid = blockIdx.x * blockDim.x + threadIdx.x;
+  const unsigned r = gid / NIN;
+  const int inner = (int)(gid - r * NIN);
+  const unsigned ex = (unsigned)R.ext[0], ey = (unsigned)R.ext[1], ez = (unsigned)R.ext[2];
+  const unsigned ty = r / ex;
+  const unsigned x = r - ty * ex;
+  unsigned y, z;
   if constexpr (YC > 1) {
-    const long long ych = (R.ext[1] + YC - 1) / YC;
-    if (gid >= (long long)R.ext[0] * ych * YC * R.ext[2] * NIN) return;
-    const long long r = gid / NIN;
-    inner = (int)(gid - r * NIN);
-    const long long x = r % R.ext[0], t = r / R.ext[0];
-    const long long yi = t % YC, t2 = t / YC;
-    const long long z = t2 % R.ext[2], yb = t2 / R.ext[2];
-    const long long y = yb * YC + yi;
-    if (y >= R.ext[1]) return;
-    cell = (R.lo[0] + x) + (R.lo[1] + y) * sy + (R.lo[2] + z) * sz;
+    const unsigned t2 = ty / YC;
+    const unsigned yb = t2 / ez;
+    z = t2 - yb * ez;
+    y = yb * YC + (ty % YC);
+    if (yb >= (ey + YC - 1) / YC || y >= ey) return;
   } else {
-    if (gid >= R.count() * NIN) return;
-    const long long r = gid / NIN;
-    inner = (int)(gid - r * NIN);
-    cell = box_cell(R, r, sy, sz);
+    z = ty / ey;
+    y = ty - z * ey;
+    if (z >= ez) return;
   }
+  const long long cell = (long long)(R.lo[0] + (int)x) + (long long)(R.lo[1] + (int)y) * sy +
+                         (long long)(R.lo[2] + (int)z) * sz;
   double win[2 * M + 1];
 #pragma unroll
   for (int o = -M; o <= M; ++o) win[o + M] = __ldg(&src[(cell + o * astride) * NIN + inner]);
@@ -293,8 +294,8 @@ __global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? 4 : 2) k_predictor(
 // neighbours' q (read for the same cell) were touched a few MB earlier and are
 // still in L2 (the plain x-y-z order re-reads the -z neighbour from HBM).
 // The D faces are evaluated together (independent dependency chains) and the
-// D*NV point sums are formed by one transpose-reduction over the lane group
-// (fixed butterfly, deterministic).
+// D*NV point sums are formed through shared memory in a fixed order
+// (deterministic).
 // ---------------------------------------------------------------------------
 template <int D, int M, int SYS, int DIR, int FLUX>
 __device__ __forceinline__ bool point_flux(const double* __restrict__ q, long long cR, long long sd, int p, bool fok,
@@ -315,14 +316,18 @@ __device__ __forceinline__ bool point_flux(const double* __restrict__ q, long lo
   const int base = s * NS + t1 * ipow_c(N, ax0) + (D == 3 ? t2 * ipow_c(N, ax1) : 0);
   const double* qL = q + cL * (NV * NST) + base;
   const double* qR = q + cR * (NV * NST) + base;
+  // both traces unpredicated (the padded grid holds a ghost layer on every
+  // side, so the far-side reads stay in bounds; their values are discarded at
+  // transmissive boundaries)
   double um[NV], up[NV];
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
-    double a = 0.0, b = 0.0;
+    double a = T.psi1[0] * __ldg(&qL[v * NST]);   // q_h^- (xi = 1 of the left cell)
+    double b = T.psi0[0] * __ldg(&qR[v * NST]);   // q_h^+ (xi = 0 of the right cell)
 #pragma unroll
-    for (int k = 0; k < N; ++k) {
-      if (!tlo) a += T.psi1[k] * __ldg(&qL[v * NST + k * sn]);   // q_h^- (xi = 1 of the left cell)
-      if (!thi) b += T.psi0[k] * __ldg(&qR[v * NST + k * sn]);   // q_h^+ (xi = 0 of the right cell)
+    for (int k = 1; k < N; ++k) {
+      a += T.psi1[k] * __ldg(&qL[v * NST + k * sn]);
+      b += T.psi0[k] * __ldg(&qR[v * NST + k * sn]);
     }
     um[v] = tlo ? b : a;   // transmissive boundary: interior trace on both sides (R5)
     up[v] = thi ? a : b;
@@ -357,31 +362,6 @@ __device__ __forceinline__ bool point_flux(const double* __restrict__ q, long lo
   return ok;
 }
 
-// Transpose-reduction of K values over the G lanes of a segment: after it, lane
-// l holds the segment sum of values [base, base + max(1, K/G)).
-template <int K, int O, int G, int KP>
-struct TransposeReduce {
-  __device__ __forceinline__ static void run(double (&v)[KP], int lg, int& base) {
-    if constexpr (O >= 1) {
-      const bool upper = (lg & O) != 0;
-      if constexpr (K > 1) {
-        constexpr int H = K / 2;
-#pragma unroll
-        for (int i = 0; i < H; ++i) {
-          const double send = upper ? v[i] : v[i + H];
-          const double keep = upper ? v[i + H] : v[i];
-          v[i] = keep + __shfl_xor_sync(0xffffffffu, send, O, G);
-        }
-        if (upper) base += H;
-        TransposeReduce<H, O / 2, G, KP>::run(v, lg, base);
-      } else {
-        v[0] += __shfl_xor_sync(0xffffffffu, v[0], O, G);
-        TransposeReduce<1, O / 2, G, KP>::run(v, lg, base);
-      }
-    }
-  }
-};
-
 constexpr int pow2_at_least(int x) { return x <= 1 ? 1 : 2 * pow2_at_least((x + 1) / 2); }
 
 template <int D, int M, int SYS, int WARPS, int YC, int FLUX>
@@ -399,16 +379,17 @@ __global__ void __launch_bounds__(WARPS * 32, (FLUX == 1) ? 5 : (SYS == 1 ? 4 : 
   constexpr int KP = pow2_at_least(D * NV);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int p = lane & (G - 1);
-  const long long r = ((long long)blockIdx.x * WARPS + warp) * CPW + lane / G;
-  const int ex = E.ext[0], ez = E.ext[2];
-  const long long t = r / ex;
+  // 32-bit index decomposition (the launcher guarantees < 2^32 cell groups)
+  const unsigned r = (blockIdx.x * WARPS + warp) * CPW + lane / G;
+  const unsigned ex = (unsigned)E.ext[0], ez = (unsigned)E.ext[2];
+  const unsigned t = r / ex;
   const int x = (int)(r - t * ex);
   const int yi = (int)(t % YC);
-  const long long t2 = t / YC;
-  const int z = (int)(t2 % ez);
-  const long long yb = t2 / ez;
+  const unsigned t2 = t / YC;
+  const unsigned yb = t2 / ez;
+  const int z = (int)(t2 - yb * ez);
   const int y = (int)(yb * YC + yi);
-  const bool ok = y < E.ext[1] && yb * YC < E.ext[1];
+  const bool ok = y < E.ext[1];
   const int cx = E.lo[0] + x, cy = E.lo[1] + y, cz = E.lo[2] + z;
   const long long cR = ok ? cx + cy * sy + cz * sz : 0;
   const int zH = (D == 3) ? H : 0;
@@ -421,8 +402,6 @@ __global__ void __launch_bounds__(WARPS * 32, (FLUX == 1) ? 5 : (SYS == 1 ? 4 : 
   double wt = T.w[s] * T.w[tt % N];
   if (D == 3) wt *= T.w[tt / N];
   double v[KP];
-#pragma unroll
-  for (int i = D * NV; i < KP; ++i) v[i] = 0.0;
   bool good = true;
   good &= point_flux<D, M, SYS, 0, FLUX>(q, cR, 1, ps, fok[0], (bmask & 1) && cx == H, (bmask & 2) && cx == H + n0, wt,
                                    gamma, ch, T, v);
@@ -432,17 +411,24 @@ __global__ void __launch_bounds__(WARPS * 32, (FLUX == 1) ? 5 : (SYS == 1 ? 4 : 
     good &= point_flux<D, M, SYS, 2, FLUX>(q, cR, sz, ps, fok[2], (bmask & 16) && cz == zH, (bmask & 32) && cz == zH + n2,
                                      wt, gamma, ch, T, v + 2 * NV);
   if (!good) record_error(cnt, 1, 2, cR);
-  int base = 0;
-  TransposeReduce<KP, G / 2, G, KP>::run(v, p, base);
-  constexpr int KL = (KP / G) > 1 ? (KP / G) : 1;
+  // point sums through shared memory: lane p stores its K = D*NV weighted
+  // point fluxes in column p, then lane i sums row i over the NS points in
+  // order (rows padded to G+1 doubles: conflict-free column writes and row reads)
+  constexpr int K = D * NV;
+  __shared__ double red[WARPS * CPW][K][G + 1];
+  double(*rb)[G + 1] = red[warp * CPW + lane / G];
+  if (pok) {
 #pragma unroll
-  for (int i = 0; i < KL; ++i) {
-    const int idx = base + i;
-    if (idx < D * NV) {
-      const int dir = idx / NV, var = idx - dir * NV;
-      const bool face_ok = dir == 0 ? (ok && iny && inz) : (dir == 1 ? (ok && inx && inz) : (ok && inx && iny));
-      if (face_ok) F[((long long)dir * ncell + cR) * NV + var] = v[i];
-    }
+    for (int i = 0; i < K; ++i) rb[i][p] = v[i];
+  }
+  __syncwarp();
+  for (int i = p; i < K; i += G) {
+    double acc = rb[i][0];
+#pragma unroll
+    for (int j = 1; j < NS; ++j) acc += rb[i][j];
+    const int dir = i / NV, var = i - dir * NV;
+    const bool face_ok = dir == 0 ? (ok && iny && inz) : (dir == 1 ? (ok && inx && inz) : (ok && inx && iny));
+    if (face_ok) F[((long long)dir * ncell + cR) * NV + var] = acc;
   }
 }
 
@@ -636,7 +622,9 @@ static void weno_sweep_nv(const KCtx& k, const double* src, double* dst, const B
   const long long per = ipow_c(N, K);
   if (R.count() == 0) return;
   const long long rows = (YC > 1) ? (long long)R.ext[0] * ((R.ext[1] + YC - 1) / YC) * YC * R.ext[2] : R.count();
-  const unsigned g = grid_for(rows * k.NV * per, 256);
+  const long long threads = rows * k.NV * per;
+  if (threads >= (1LL << 32) - 256) return;   // guarded at ader_create (32-bit thread indexing)
+  const unsigned g = grid_for(threads, 256);
   count_launch(k);
   switch (k.NV) {
     case 4: k_weno<M, K, 4, YC><<<g, 256, 0, k.stream>>>(src, dst, R, k.sy, k.sz, astride, k.tab); break;
