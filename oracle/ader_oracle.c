@@ -834,6 +834,8 @@ static int64_t pidx(const orc_ctx* c, int i, int j, int k) {
 orc_ctx* orc_create(const orc_config* cfg) {
   if (!cfg || (cfg->dim != 2 && cfg->dim != 3) || cfg->degree < 1 || cfg->degree + 1 > NMAX) return NULL;
   if (cfg->flux == ORC_FLUX_OSHER && cfg->system != ORC_EULER) return NULL;   /* Osher: Euler only */
+  for (int k = 0; k < 2 * cfg->dim; ++k)
+    if (cfg->bc[k] == ORC_BC_REFLECTIVE && (cfg->system != ORC_EULER || cfg->n[k / 2] < cfg->degree + 1)) return NULL;
   orc_ctx* c = (orc_ctx*)calloc(1, sizeof(orc_ctx));
   c->cfg = *cfg;
   c->d = cfg->dim; c->M = cfg->degree; c->N = c->M + 1;
@@ -937,13 +939,30 @@ int orc_get_cells(const orc_ctx* c, double* u) {
 }
 
 /* Ghost cells (reading R5): periodic wrap, or transmissive copy of the
- * nearest interior cell (index clamped per axis). */
+ * nearest interior cell (index clamped per axis); reflective walls (R22) take
+ * the mirror cell (index -1-i / 2n-1-i) with the normal momentum negated. */
 static int ghost_src(const orc_ctx* c, int axis, int i) {
   int n = c->n[axis];
   if (i >= 0 && i < n) return i;
   int side = (i < 0) ? 0 : 1;
   if (c->cfg.bc[2 * axis + side] == ORC_BC_PERIODIC) return ((i % n) + n) % n;
+  if (c->cfg.bc[2 * axis + side] == ORC_BC_REFLECTIVE) return (i < 0) ? -1 - i : 2 * n - 1 - i;
   return (i < 0) ? 0 : n - 1;
+}
+static int ghost_reflected(const orc_ctx* c, int axis, int i) {
+  if (i >= 0 && i < c->n[axis]) return 0;
+  return c->cfg.bc[2 * axis + (i < 0 ? 0 : 1)] == ORC_BC_REFLECTIVE;
+}
+
+void orc_reflect_poly(int d, int M, int nv, int dir, const double* q, double* out) {
+  int N = M + 1, NST = ipow(N, d + 1), pi[4];
+  for (int p = 0; p < NST; ++p) {
+    decode(p, N, d + 1, pi);
+    pi[dir] = N - 1 - pi[dir];
+    int src = 0;
+    for (int k = d; k >= 0; --k) src = src * N + pi[k];
+    for (int v = 0; v < nv; ++v) out[v * NST + p] = (v == 1 + dir ? -1.0 : 1.0) * q[v * NST + src];
+  }
 }
 
 int64_t orc_num_padded(const orc_ctx* c) { return c->npad; }
@@ -961,7 +980,11 @@ static void fill_ghosts(orc_ctx* c) {
       for (int i = lo[0]; i < hi[0]; ++i) {
         int si = ghost_src(c, 0, i), sj = ghost_src(c, 1, j), sk = (c->d == 3) ? ghost_src(c, 2, k) : 0;
         if (si == i && sj == j && sk == k) continue;
-        memcpy(&c->u[pidx(c, i, j, k) * c->nv], &c->u[pidx(c, si, sj, sk) * c->nv], sizeof(double) * c->nv);
+        double* g = &c->u[pidx(c, i, j, k) * c->nv];
+        memcpy(g, &c->u[pidx(c, si, sj, sk) * c->nv], sizeof(double) * c->nv);
+        const int ii[3] = {i, j, k};
+        for (int a = 0; a < c->d; ++a)
+          if (ghost_reflected(c, a, ii[a])) g[1 + a] = -g[1 + a];
       }
 }
 
@@ -992,12 +1015,13 @@ static void gather_box(const orc_ctx* c, int i, int j, int k, double* box) {
   (void)W;
 }
 
-/* Ghost cell beyond a transmissive boundary (its predictor is never used). */
+/* Ghost cell beyond a transmissive or reflective boundary (its predictor is
+ * never used: boundary faces use the interior trace, R5, or its reflection, R22). */
 static int beyond_transmissive(const orc_ctx* c, int i, int j, int k) {
   const int ii[3] = {i, j, k};
   for (int a = 0; a < c->d; ++a) {
-    if (ii[a] < 0 && c->cfg.bc[2 * a] == ORC_BC_TRANSMISSIVE) return 1;
-    if (ii[a] >= c->n[a] && c->cfg.bc[2 * a + 1] == ORC_BC_TRANSMISSIVE) return 1;
+    if (ii[a] < 0 && c->cfg.bc[2 * a] != ORC_BC_PERIODIC) return 1;
+    if (ii[a] >= c->n[a] && c->cfg.bc[2 * a + 1] != ORC_BC_PERIODIC) return 1;
   }
   return 0;
 }
@@ -1031,6 +1055,7 @@ int orc_advance_box(orc_ctx* c, double dt, const int32_t* blo, const int32_t* bh
   }
   int64_t next = (int64_t)ext[0] * ext[1] * ext[2];
   double* q = (double*)calloc((size_t)next * nv * NST, sizeof(double));
+  double qref[VMAX * 256], qref2[VMAX * 256];   /* reflected polynomials (N^(d+1) <= 256) */
   int64_t sw_tot = 0; int sw_max = 0;
   int off = 1;
   /* 1. reconstruction + predictor on the box and its face neighbours */
@@ -1062,9 +1087,20 @@ int orc_advance_box(orc_ctx* c, double dt, const int32_t* blo, const int32_t* bh
           int64_t stride = (dir == 0) ? 1 : (dir == 1) ? ext[0] : (int64_t)ext[0] * ext[1];
           const int ic[3] = {i, j, k};
           const double* qc = &q[e0 * nv * NST];
-          /* R5: a transmissive boundary face takes the interior trace on both sides */
-          const double* qm = (ic[dir] == 0 && c->cfg.bc[2 * dir] == ORC_BC_TRANSMISSIVE) ? NULL : &q[(e0 - stride) * nv * NST];
-          const double* qp = (ic[dir] == c->n[dir] - 1 && c->cfg.bc[2 * dir + 1] == ORC_BC_TRANSMISSIVE) ? NULL : &q[(e0 + stride) * nv * NST];
+          /* R5: a transmissive boundary face takes the interior trace on both
+           * sides; R22: a reflective wall faces the reflected polynomial */
+          const double* qm = &q[(e0 - stride) * nv * NST];
+          const double* qp = &q[(e0 + stride) * nv * NST];
+          if (ic[dir] == 0 && c->cfg.bc[2 * dir] == ORC_BC_TRANSMISSIVE) qm = NULL;
+          if (ic[dir] == c->n[dir] - 1 && c->cfg.bc[2 * dir + 1] == ORC_BC_TRANSMISSIVE) qp = NULL;
+          if (ic[dir] == 0 && c->cfg.bc[2 * dir] == ORC_BC_REFLECTIVE) {
+            orc_reflect_poly(d, c->M, nv, dir, qc, qref);
+            qm = qref;
+          }
+          if (ic[dir] == c->n[dir] - 1 && c->cfg.bc[2 * dir + 1] == ORC_BC_REFLECTIVE) {
+            orc_reflect_poly(d, c->M, nv, dir, qc, qref2);
+            qp = qref2;
+          }
           if (orc_face_flux(d, c->M, c->cfg.system, c->cfg.gamma, c->cfg.ch, c->cfg.flux, c->cfg.flux_quad, dir, qm, qc, Fm) ||
               orc_face_flux(d, c->M, c->cfg.system, c->cfg.gamma, c->cfg.ch, c->cfg.flux, c->cfg.flux_quad, dir, qc, qp, Fp)) {
             snprintf(c->err, sizeof(c->err), "inadmissible face state at cell (%d,%d,%d) t=%.17g", i, j, k, c->t);
@@ -1162,8 +1198,12 @@ int orc_dump_flux(orc_ctx* c, double dt, double* F) {
           const int hib = ii[dir] == c->n[dir];
           const int tlo = lob && c->cfg.bc[2 * dir] == ORC_BC_TRANSMISSIVE;
           const int thi = hib && c->cfg.bc[2 * dir + 1] == ORC_BC_TRANSMISSIVE;
-          if (!tlo && cell_predict(c, im[0], im[1], im[2], dt, qa, &sw)) goto fail;
-          if (!thi && cell_predict(c, i, j, k, dt, qb, &sw)) goto fail;
+          const int rlo = lob && c->cfg.bc[2 * dir] == ORC_BC_REFLECTIVE;
+          const int rhi = hib && c->cfg.bc[2 * dir + 1] == ORC_BC_REFLECTIVE;
+          if (!tlo && !rlo && cell_predict(c, im[0], im[1], im[2], dt, qa, &sw)) goto fail;
+          if (!thi && !rhi && cell_predict(c, i, j, k, dt, qb, &sw)) goto fail;
+          if (rlo) orc_reflect_poly(d, c->M, nv, dir, qb, qa);   /* R22 */
+          if (rhi) orc_reflect_poly(d, c->M, nv, dir, qa, qb);
           if (orc_face_flux(d, c->M, c->cfg.system, c->cfg.gamma, c->cfg.ch, c->cfg.flux, c->cfg.flux_quad, dir, tlo ? NULL : qa, thi ? NULL : qb, Fo)) goto fail;
         }
   free(qa); free(qb);

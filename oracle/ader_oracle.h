@@ -23,7 +23,7 @@ extern "C" {
 #define ORC_MAXV 9            /* conserved variables (MHD-GLM)               */
 
 enum { ORC_EULER = 0, ORC_MHD = 1 };
-enum { ORC_BC_PERIODIC = 0, ORC_BC_TRANSMISSIVE = 1 };
+enum { ORC_BC_PERIODIC = 0, ORC_BC_TRANSMISSIVE = 1, ORC_BC_REFLECTIVE = 2 };   /* reflective: Euler only (R22) */
 enum { ORC_FLUX_RUSANOV = 0, ORC_FLUX_OSHER = 1 };   /* eqn.rusanov / eqn.osher */
 
 typedef struct {
@@ -87,6 +87,10 @@ int  orc_phys_flux(int system, int dim, double gamma, double ch, const double* u
 double orc_max_speed(int system, int dim, double gamma, double ch, const double* u, int dir);
 int  orc_rusanov(int system, int dim, double gamma, double ch, const double* uL,
                  const double* uR, int dir, double* f);
+/* Reflected space-time polynomial across a wall normal to dir (reading R22):
+ * node order reversed along dir (the GL nodes are symmetric, lambda_{N-1-a} =
+ * 1 - lambda_a) and the normal momentum negated.  q, out [nv][N^(d+1)]. */
+void orc_reflect_poly(int d, int M, int nv, int dir, const double* q, double* out);
 /* Euler Jacobian A_dir = df_dir/du (analytic, row-major nv x nv). */
 int  orc_euler_jacobian(int dim, double gamma, const double* u, int dir, double* A);
 /* |A_dir(u)| for Euler by Sylvester's formula over the three distinct

@@ -82,20 +82,25 @@ static int alloc_block(amr_t* A, int cnt) {
 }
 
 /* Cell at level l and (possibly out-of-domain) index ix: periodic wrap or
- * transmissive clamp per axis (reading R5), -1 if missing. */
-static int lookup(const amr_t* A, int l, const int64_t* ix0) {
+ * transmissive clamp per axis (reading R5), reflective mirror (R22: the
+ * caller negates the momentum of the axes flagged in *flip), -1 if missing. */
+static int lookup_flip(const amr_t* A, int l, const int64_t* ix0, int* flip) {
   int64_t ix[3] = {ix0[0], ix0[1], ix0[2]};
+  int fl = 0;
   for (int k = 0; k < A->d; ++k) {
     int64_t n = A->n[l][k];
     if (ix[k] < 0 || ix[k] >= n) {
       int side = ix[k] < 0 ? 0 : 1;
       if (A->cfg.bc[2 * k + side] == ORC_BC_PERIODIC) ix[k] = ((ix[k] % n) + n) % n;
+      else if (A->cfg.bc[2 * k + side] == ORC_BC_REFLECTIVE) { ix[k] = ix[k] < 0 ? -1 - ix[k] : 2 * n - 1 - ix[k]; fl |= 1 << k; }
       else ix[k] = ix[k] < 0 ? 0 : n - 1;
     }
   }
   if (A->d == 2) ix[2] = 0;
+  if (flip) *flip = fl;
   return A->map[l][lin_idx(A, l, ix)];
 }
+static int lookup(const amr_t* A, int l, const int64_t* ix0) { return lookup_flip(A, l, ix0, NULL); }
 
 static int outside(const amr_t* A, int l, const int64_t* ix) {
   for (int k = 0; k < A->d; ++k)
@@ -179,9 +184,12 @@ static int gather_box(const amr_t* A, int id, double* box) {
     for (int dy = -M; dy <= M; ++dy)
       for (int dx = -M; dx <= M; ++dx, ++b) {
         int64_t ix[3] = {C->idx[0] + dx, C->idx[1] + dy, C->idx[2] + dz};
-        int n = lookup(A, C->level, ix);
+        int fl = 0;
+        int n = lookup_flip(A, C->level, ix, &fl);
         if (n < 0) return -1;
         memcpy(&box[b * nv], A->c[n].u, sizeof(double) * nv);
+        for (int k = 0; k < A->d; ++k)
+          if (fl & (1 << k)) box[b * nv + 1 + k] = -box[b * nv + 1 + k];   /* R22 mirror */
       }
   return 0;
 }
@@ -273,6 +281,19 @@ static int cell_face_flux(amr_t* A, int id, int dir, int side, int m, double* F)
   ix[dir] += side ? 1 : -1;
   double zero[3] = {0, 0, 0}, offC[3] = {0, 0, 0};
   offC[dir] = side ? 1.0 : 0.0;
+  if (outside(A, l, ix) && A->cfg.bc[2 * dir + side] == ORC_BC_REFLECTIVE) {
+    /* R22: the wall faces the reflected polynomial of the cell itself */
+    double* qr = (double*)malloc(sizeof(double) * nv * A->NST);
+    orc_reflect_poly(d, A->M, nv, dir, C->q, qr);
+    double offR[3] = {0, 0, 0};
+    offR[dir] = side ? 0.0 : 1.0;
+    int rc = side ? orc_face_flux_mapped(d, A->M, A->cfg.system, A->cfg.gamma, A->cfg.ch, A->cfg.flux, A->cfg.flux_quad, dir, C->q, offC, 1.0, 0.0, 1.0,
+                                         qr, offR, 1.0, 0.0, 1.0, F)
+                  : orc_face_flux_mapped(d, A->M, A->cfg.system, A->cfg.gamma, A->cfg.ch, A->cfg.flux, A->cfg.flux_quad, dir, qr, offR, 1.0, 0.0, 1.0,
+                                         C->q, offC, 1.0, 0.0, 1.0, F);
+    free(qr);
+    return rc;
+  }
   if (outside(A, l, ix) && A->cfg.bc[2 * dir + side] == ORC_BC_TRANSMISSIVE) {
     /* R5: interior trace on both sides */
     return side ? orc_face_flux_mapped(d, A->M, A->cfg.system, A->cfg.gamma, A->cfg.ch, A->cfg.flux, A->cfg.flux_quad, dir, C->q, offC, 1.0, 0.0, 1.0,
@@ -632,6 +653,8 @@ void* orc_amr_create(const orc_config* cfg) {
   if (!cfg || (cfg->dim != 2 && cfg->dim != 3) || cfg->degree < 2 || cfg->degree > 3) return NULL;
   if (cfg->lmax < 0 || cfg->lmax >= LMAXX || cfg->refine_factor < cfg->degree) return NULL;
   if (cfg->flux == ORC_FLUX_OSHER && cfg->system != ORC_EULER) return NULL;   /* Osher: Euler only */
+  for (int k = 0; k < 2 * cfg->dim; ++k)
+    if (cfg->bc[k] == ORC_BC_REFLECTIVE && (cfg->system != ORC_EULER || cfg->n[k / 2] < cfg->degree + 1)) return NULL;
   amr_t* A = (amr_t*)calloc(1, sizeof(amr_t));
   A->cfg = *cfg;
   A->d = cfg->dim; A->M = cfg->degree; A->N = A->M + 1;
