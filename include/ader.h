@@ -42,7 +42,10 @@ typedef enum {
 } ader_status;
 
 typedef enum { ADER_EULER = 0, ADER_MHD_GLM = 1 } ader_system;
-typedef enum { ADER_BC_PERIODIC = 0, ADER_BC_TRANSMISSIVE = 1 } ader_bc;
+typedef enum { ADER_BC_PERIODIC = 0,
+               ADER_BC_TRANSMISSIVE = 1,   /* reading R5 */
+               ADER_BC_REFLECTIVE = 2      /* reflecting wall, reading R22 (Euler only) */
+} ader_bc;
 /* Two-point flux of the space-time face quadrature. */
 typedef enum { ADER_FLUX_RUSANOV = 0,   /* eqn.rusanov @ P:181-185                  */
                ADER_FLUX_OSHER = 1      /* eqn.osher @ P:186-196, Euler only         */
@@ -156,7 +159,8 @@ ader_status ader_partition(const ader_config* cfg, int32_t rank, ader_partition_
  * the owned range.  kind: 0 axis unused, 1 exchange with `peer` (send
  * send_lo..send_hi, receive into recv_lo..recv_hi; NCCL order per peer: send
  * low, recv high, send high, recv low), 2 periodic wrap onto itself, 3
- * transmissive copy of the nearest owned cell (reading R5). */
+ * transmissive copy of the nearest owned cell (reading R5), 4 reflective
+ * mirror of the owned cells with the normal momentum negated (R22). */
 typedef struct {
   int32_t kind, peer;
   int32_t send_lo[3], send_hi[3];

@@ -156,8 +156,13 @@ ader_status validate(const ader_config* cfg, std::string& why) {
   if (cfg->dim == 2 && cfg->n0[2] != 1) return bad("n0[2] must be 1 in 2D");
   for (int k = 0; k < cfg->dim; ++k)
     if (!(cfg->hi[k] > cfg->lo[k])) return bad("hi must exceed lo");
-  for (int k = 0; k < 2 * cfg->dim; ++k)
-    if (cfg->bc[k] != ADER_BC_PERIODIC && cfg->bc[k] != ADER_BC_TRANSMISSIVE) return bad("bad bc");
+  for (int k = 0; k < 2 * cfg->dim; ++k) {
+    if (cfg->bc[k] != ADER_BC_PERIODIC && cfg->bc[k] != ADER_BC_TRANSMISSIVE && cfg->bc[k] != ADER_BC_REFLECTIVE)
+      return bad("bad bc");
+    if (cfg->bc[k] == ADER_BC_REFLECTIVE && cfg->system != ADER_EULER) return bad("reflective walls are Euler only");
+    if (cfg->bc[k] == ADER_BC_REFLECTIVE && cfg->n0[k / 2] < cfg->degree + 1)
+      return bad("a reflective axis needs at least M+1 cells");
+  }
   for (int k = 0; k < cfg->dim; ++k)
     if ((cfg->bc[2 * k] == ADER_BC_PERIODIC) != (cfg->bc[2 * k + 1] == ADER_BC_PERIODIC))
       return bad("periodic bc must be set on both sides of an axis");
@@ -336,7 +341,7 @@ void halo_plan(int d, int H, const int n[3], const int P[3], const ader_partitio
   const int nb = part.nbr[2 * a + side];
   if (nb >= 0 && nb != rank) { o->kind = 1; o->peer = nb; }
   else if (nb >= 0 && bc[2 * a + side] == ADER_BC_PERIODIC) o->kind = 2;
-  else o->kind = 3;
+  else o->kind = bc[2 * a + side] == ADER_BC_REFLECTIVE ? 4 : 3;
 }
 
 Box desc_box(const int32_t* lo, const int32_t* hi) { return make_box(lo[0], hi[0], lo[1], hi[1], lo[2], hi[2]); }
@@ -379,8 +384,9 @@ void halo_unpack_local(ader_ctx* c, double* u, int a) {
   if (dl.kind == 1) launch_unpack(c->k, u, rlo, c->recvb[2 * a]);
   if (dh.kind == 1) launch_unpack(c->k, u, rhi, c->recvb[2 * a + 1]);
   // local sides: periodic wrap onto ourselves, or transmissive copy (reading R5)
-  if (dl.kind != 1) launch_fill_axis(c->k, u, rlo, a, dl.kind == 2 ? 0 : 1, c->H, c->n[a]);
-  if (dh.kind != 1) launch_fill_axis(c->k, u, rhi, a, dh.kind == 2 ? 0 : 1, c->H, c->n[a]);
+  auto mode = [](int kind) { return kind == 2 ? 0 : (kind == 4 ? 2 : 1); };
+  if (dl.kind != 1) launch_fill_axis(c->k, u, rlo, a, mode(dl.kind), c->H, c->n[a]);
+  if (dh.kind != 1) launch_fill_axis(c->k, u, rhi, a, mode(dh.kind), c->H, c->n[a]);
 }
 
 ader_status fill_halo(ader_ctx* c, double* u) {
@@ -420,19 +426,21 @@ void run_weno(ader_ctx* c) {
 }
 
 // Physical transmissive sides of this rank's block (bit 2a: low side of axis a).
-int transmissive_mask(const ader_ctx* c) {
+int boundary_mask(const ader_ctx* c, int bc) {
   int m = 0;
   for (int a = 0; a < c->d; ++a) {
-    if (c->part.nbr[2 * a] < 0 && c->cfg.bc[2 * a] == ADER_BC_TRANSMISSIVE) m |= 1 << (2 * a);
-    if (c->part.nbr[2 * a + 1] < 0 && c->cfg.bc[2 * a + 1] == ADER_BC_TRANSMISSIVE) m |= 1 << (2 * a + 1);
+    if (c->part.nbr[2 * a] < 0 && c->cfg.bc[2 * a] == bc) m |= 1 << (2 * a);
+    if (c->part.nbr[2 * a + 1] < 0 && c->cfg.bc[2 * a + 1] == bc) m |= 1 << (2 * a + 1);
   }
   return m;
 }
+int transmissive_mask(const ader_ctx* c) { return boundary_mask(c, ADER_BC_TRANSMISSIVE); }
+int reflective_mask(const ader_ctx* c) { return boundary_mask(c, ADER_BC_REFLECTIVE); }
 
 void run_predictor(ader_ctx* c, double dt) {
   // owned block + the face-neighbour layer, except beyond transmissive sides (R5)
   Box r = grown(c, 1);
-  const int tm = transmissive_mask(c);
+  const int tm = transmissive_mask(c) | reflective_mask(c);   // no predictor beyond walls either (R22)
   for (int a = 0; a < c->d; ++a) {
     if (tm & (1 << (2 * a))) { r.lo[a] += 1; r.ext[a] -= 1; }
     if (tm & (1 << (2 * a + 1))) r.ext[a] -= 1;
@@ -461,7 +469,7 @@ void run_flux(ader_ctx* c) {
   Scope s(c, ADER_K_FLUX, face_flops(c) * nf);
   const int H = c->H, zH = c->d == 3 ? H : 0;
   const Box ext = make_box(H, H + c->n[0] + 1, H, H + c->n[1] + 1, zH, zH + c->n[2] + (c->d == 3 ? 1 : 0));
-  launch_face_flux_cells(c->k, c->q, c->F, ext, H, c->n, transmissive_mask(c), c->cnt);
+  launch_face_flux_cells(c->k, c->q, c->F, ext, H, c->n, transmissive_mask(c), reflective_mask(c), c->cnt);
 }
 
 void run_update(ader_ctx* c, double dt) {
@@ -627,7 +635,9 @@ static ader_status create_impl(const ader_config* cfg, ader_ctx** out, bool loop
   for (int k = 0; k < cfg->dim; ++k) {
     const bool remote = (pi.nbr[2 * k] >= 0 && pi.nbr[2 * k] != cfg->rank) ||
                         (pi.nbr[2 * k + 1] >= 0 && pi.nbr[2 * k + 1] != cfg->rank);
-    if (remote && pi.hi[k] - pi.lo[k] < H) {
+    const bool wall = (pi.nbr[2 * k] < 0 && cfg->bc[2 * k] == ADER_BC_REFLECTIVE) ||
+                      (pi.nbr[2 * k + 1] < 0 && cfg->bc[2 * k + 1] == ADER_BC_REFLECTIVE);
+    if ((remote || wall) && pi.hi[k] - pi.lo[k] < H) {
       g_create_err = "rank block thinner than the ghost layer (M+1)";
       return ADER_ERR_CONFIG;
     }

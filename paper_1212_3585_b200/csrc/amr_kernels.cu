@@ -17,19 +17,37 @@ namespace ader {
 
 constexpr int ipow_a(int b, int e) { return e == 0 ? 1 : b * ipow_a(b, e - 1); }
 
-__device__ __forceinline__ int amr_lookup(const AmrDevView& V, int l, long long x, long long y, long long z) {
+// same-level cell at a (possibly out-of-domain) index: periodic wrap,
+// transmissive clamp (R5) or reflective mirror (R22; bit k of *flip set: the
+// caller negates the momentum along k)
+__device__ __forceinline__ int amr_lookup_flip(const AmrDevView& V, int l, long long x, long long y, long long z,
+                                               int* flip) {
   long long c[3] = {x, y, z};
+  int fl = 0;
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
     if (k >= V.D) { c[k] = 0; continue; }
     const long long n = V.n[l][k];
     if (c[k] < 0 || c[k] >= n) {
       const int side = c[k] < 0 ? 0 : 1;
-      if (V.bc[2 * k + side] == ADER_BC_PERIODIC) c[k] = ((c[k] % n) + n) % n;
+      const int bc = V.bc[2 * k + side];
+      if (bc == ADER_BC_PERIODIC) c[k] = ((c[k] % n) + n) % n;
+      else if (bc == ADER_BC_REFLECTIVE) { c[k] = c[k] < 0 ? -1 - c[k] : 2 * n - 1 - c[k]; fl |= 1 << k; }
       else c[k] = c[k] < 0 ? 0 : n - 1;
     }
   }
+  if (flip) *flip = fl;
   return V.map[l][(c[2] * V.n[l][1] + c[1]) * V.n[l][0] + c[0]];
+}
+__device__ __forceinline__ int amr_lookup(const AmrDevView& V, int l, long long x, long long y, long long z) {
+  return amr_lookup_flip(V, l, x, y, z, nullptr);
+}
+// cell average component v seen through a (possibly reflecting) lookup
+__device__ __forceinline__ double amr_u_at(const AmrDevView& V, int l, long long x, long long y, long long z, int v) {
+  int fl = 0;
+  const int id = amr_lookup_flip(V, l, x, y, z, &fl);
+  const double a = V.u[(long long)id * V.NV + v];
+  return (v >= 1 && v <= V.D && ((fl >> (v - 1)) & 1)) ? -a : a;
 }
 
 __device__ __forceinline__ void amr_error(DevCounters* c, int code, int stage, long long cell) {
@@ -117,7 +135,7 @@ __global__ void __launch_bounds__(128) k_amr_weno(AmrDevView V, const int* __res
     for (int jy = 0; jy < W; ++jy) {
       double win[W];
 #pragma unroll
-      for (int o = 0; o < W; ++o) win[o] = V.u[(long long)amr_lookup(V, l, x0 + o - M, y0 + jy - M, 0) * NV + v];
+      for (int o = 0; o < W; ++o) win[o] = amr_u_at(V, l, x0 + o - M, y0 + jy - M, 0, v);
       double out[N];
       weno1d<M>(T, win, out);
 #pragma unroll
@@ -140,7 +158,7 @@ __global__ void __launch_bounds__(128) k_amr_weno(AmrDevView V, const int* __res
         double win[W], out[N];
 #pragma unroll
         for (int o = 0; o < W; ++o)
-          win[o] = V.u[(long long)amr_lookup(V, l, x0 + o - M, y0 + jy - M, z0 + jz - M) * NV + v];
+          win[o] = amr_u_at(V, l, x0 + o - M, y0 + jy - M, z0 + jz - M, v);
         weno1d<M>(T, win, out);
 #pragma unroll
         for (int a = 0; a < N; ++a) wx[jy][a] = out[a];
@@ -235,7 +253,8 @@ __device__ __forceinline__ bool numflux_pt(const double (&um)[Phys<SYS, D>::NV],
 }
 
 // kind: 0 same level (qL, qR full faces), 1 left boundary (qR only), 2 right
-// boundary (qL only), 3 coarse left (qL = K), 4 coarse right (qR = K)
+// boundary (qL only), 3 coarse left (qL = K), 4 coarse right (qR = K),
+// 5 left wall (qR only, q^- = reflected q^+), 6 right wall (qL only)
 template <int D, int M, int SYS, int DIR>
 __device__ bool face_flux_amr(int kind, const double* qL, const double* qR, int o1, int o2, int m, double gamma,
                               double ch, const DevTables& T, const SubTables& S, double (&F)[Phys<SYS, D>::NV]) {
@@ -248,8 +267,10 @@ __device__ bool face_flux_amr(int kind, const double* qL, const double* qR, int 
     for (int t = 0; t < NT; ++t) {
       const int t1 = t % N, t2 = t / N;
       double um[NV], up[NV], ft[NV];
-      if (kind == 0 || kind == 2 || kind == 4) trace_full<D, M, NV, DIR>(qL, true, t1, t2, s, T, um);
-      if (kind == 0 || kind == 1 || kind == 3) trace_full<D, M, NV, DIR>(qR, false, t1, t2, s, T, up);
+      if (kind == 0 || kind == 2 || kind == 4 || kind == 6) trace_full<D, M, NV, DIR>(qL, true, t1, t2, s, T, um);
+      if (kind == 0 || kind == 1 || kind == 3 || kind == 5) trace_full<D, M, NV, DIR>(qR, false, t1, t2, s, T, up);
+      if (kind == 5) { for (int v = 0; v < NV; ++v) um[v] = up[v]; um[1 + DIR] = -up[1 + DIR]; }   // R22
+      if (kind == 6) { for (int v = 0; v < NV; ++v) up[v] = um[v]; up[1 + DIR] = -um[1 + DIR]; }
       if (kind == 3) trace_coarse<D, M, NV, DIR>(qL, true, o1, o2, m, t1, t2, s, T, S, um);
       if (kind == 4) trace_coarse<D, M, NV, DIR>(qR, false, o1, o2, m, t1, t2, s, T, S, up);
       if (kind == 1) for (int v = 0; v < NV; ++v) um[v] = up[v];
@@ -274,6 +295,8 @@ __device__ bool cell_face(const AmrDevView& V, int c, int side, int m, double ga
   const bool out = ix[DIR] < 0 || ix[DIR] >= V.n[l][DIR];
   if (out && V.bc[2 * DIR + side] == ADER_BC_TRANSMISSIVE)
     return face_flux_amr<D, M, SYS, DIR>(side ? 2 : 1, qc, qc, 0, 0, 0, gamma, ch, T, S, F);
+  if (out && V.bc[2 * DIR + side] == ADER_BC_REFLECTIVE)
+    return face_flux_amr<D, M, SYS, DIR>(side ? 6 : 5, qc, qc, 0, 0, 0, gamma, ch, T, S, F);
   const int nb = amr_lookup(V, l, ix[0], ix[1], ix[2]);
   if (nb < 0) return false;
   const int st = V.status[nb];

@@ -299,8 +299,8 @@ __global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? 4 : 2) k_predictor(
 // ---------------------------------------------------------------------------
 template <int D, int M, int SYS, int DIR, int FLUX>
 __device__ __forceinline__ bool point_flux(const double* __restrict__ q, long long cR, long long sd, int p, bool fok,
-                                           bool tlo, bool thi, double wt, double gamma, double ch,
-                                           const DevTables& T, double* val) {
+                                           bool tlo, bool thi, bool rlo, bool rhi, double wt, double gamma,
+                                           double ch, const DevTables& T, double* val) {
   using PH = Phys<SYS, D>;
   constexpr int NV = PH::NV, N = M + 1, NS = ipow_c(N, D), NST = NS * N;
   constexpr int NT = NS / N;
@@ -329,9 +329,13 @@ __device__ __forceinline__ bool point_flux(const double* __restrict__ q, long lo
       a += T.psi1[k] * __ldg(&qL[v * NST + k * sn]);
       b += T.psi0[k] * __ldg(&qR[v * NST + k * sn]);
     }
-    um[v] = tlo ? b : a;   // transmissive boundary: interior trace on both sides (R5)
-    up[v] = thi ? a : b;
+    um[v] = (tlo || rlo) ? b : a;   // transmissive boundary: interior trace on both sides (R5)
+    up[v] = (thi || rhi) ? a : b;
   }
+  // reflective wall (R22): the exterior state is the interior trace with the
+  // normal momentum negated
+  if (rlo) um[1 + DIR] = -um[1 + DIR];
+  if (rhi) up[1 + DIR] = -up[1 + DIR];
   // equal traces (e.g. inside a constant region): eqn.rusanov and eqn.osher
   // reduce exactly to f(q) — 0.5 (f + f) = f and the dissipation term is 0 — so one flux
   // evaluation gives the bitwise-identical result
@@ -369,7 +373,7 @@ __global__ void __launch_bounds__(WARPS * 32, (FLUX == 1) ? 5 : (SYS == 1 ? 4 : 
                                                                 const Box E, const int H, const int n0, const int n1,
                                                                 const int n2, const long long sy, const long long sz,
                                                                 const long long ncell, const double gamma,
-                                                                const double ch, const int bmask,
+                                                                const double ch, const int bmask, const int rmask,
                                                                 DevCounters* __restrict__ cnt,
                                                                 const __grid_constant__ DevTables T) {
   using PH = Phys<SYS, D>;
@@ -403,13 +407,14 @@ __global__ void __launch_bounds__(WARPS * 32, (FLUX == 1) ? 5 : (SYS == 1 ? 4 : 
   if (D == 3) wt *= T.w[tt / N];
   double v[KP];
   bool good = true;
-  good &= point_flux<D, M, SYS, 0, FLUX>(q, cR, 1, ps, fok[0], (bmask & 1) && cx == H, (bmask & 2) && cx == H + n0, wt,
-                                   gamma, ch, T, v);
-  good &= point_flux<D, M, SYS, 1, FLUX>(q, cR, sy, ps, fok[1], (bmask & 4) && cy == H, (bmask & 8) && cy == H + n1, wt,
-                                   gamma, ch, T, v + NV);
+  good &= point_flux<D, M, SYS, 0, FLUX>(q, cR, 1, ps, fok[0], (bmask & 1) && cx == H, (bmask & 2) && cx == H + n0,
+                                         (rmask & 1) && cx == H, (rmask & 2) && cx == H + n0, wt, gamma, ch, T, v);
+  good &= point_flux<D, M, SYS, 1, FLUX>(q, cR, sy, ps, fok[1], (bmask & 4) && cy == H, (bmask & 8) && cy == H + n1,
+                                         (rmask & 4) && cy == H, (rmask & 8) && cy == H + n1, wt, gamma, ch, T, v + NV);
   if constexpr (D == 3)
-    good &= point_flux<D, M, SYS, 2, FLUX>(q, cR, sz, ps, fok[2], (bmask & 16) && cz == zH, (bmask & 32) && cz == zH + n2,
-                                     wt, gamma, ch, T, v + 2 * NV);
+    good &= point_flux<D, M, SYS, 2, FLUX>(q, cR, sz, ps, fok[2], (bmask & 16) && cz == zH,
+                                           (bmask & 32) && cz == zH + n2, (rmask & 16) && cz == zH,
+                                           (rmask & 32) && cz == zH + n2, wt, gamma, ch, T, v + 2 * NV);
   if (!good) record_error(cnt, 1, 2, cR);
   // point sums through shared memory: lane p stores its K = D*NV weighted
   // point fluxes in column p, then lane i sums row i over the NS points in
@@ -517,13 +522,15 @@ __global__ void k_fill_axis(double* __restrict__ u, const Box R, const long long
   c[1] = R.lo[1] + (int)(t % R.ext[1]);
   c[2] = R.lo[2] + (int)(t / R.ext[1]);
   int i = c[axis] - H;
-  if (mode == 0) i = ((i % n) + n) % n;
-  else i = i < 0 ? 0 : (i >= n ? n - 1 : i);
+  if (mode == 0) i = ((i % n) + n) % n;                      // periodic wrap
+  else if (mode == 2) i = i < 0 ? -1 - i : (i >= n ? 2 * n - 1 - i : i);   // reflective mirror (R22)
+  else i = i < 0 ? 0 : (i >= n ? n - 1 : i);                 // transmissive copy (R5)
   int s[3] = {c[0], c[1], c[2]};
   s[axis] = i + H;
   const long long dst = c[0] + c[1] * sy + c[2] * sz;
   const long long src = s[0] + s[1] * sy + s[2] * sz;
-  u[dst * nv + v] = u[src * nv + v];
+  const double val = u[src * nv + v];
+  u[dst * nv + v] = (mode == 2 && v == 1 + axis) ? -val : val;   // wall: normal momentum negated
 }
 
 __global__ void k_pack(const double* __restrict__ src, const Box R, const long long sy, const long long sz,
@@ -680,7 +687,7 @@ void launch_predictor_list(const KCtx& k, const double* w, double* q, const Box&
 namespace {
 template <int D, int M, int SYS>
 void flux_cells_for(const KCtx& k, const double* q, double* F, const Box& ext, int H, const int n[3], int bmask,
-                    DevCounters* cnt) {
+                    int rmask, DevCounters* cnt) {
   constexpr int YC = 16;
   constexpr int NS = ipow_c(M + 1, D);
   constexpr int CPW = 32 / ((NS <= 8) ? 8 : (NS <= 16 ? 16 : 32));
@@ -691,19 +698,19 @@ void flux_cells_for(const KCtx& k, const double* q, double* F, const Box& ext, i
   if constexpr (SYS == 0) {
     if (k.tab.flux == 1) {   // eqn.osher (Euler only, checked at ader_create)
       k_face_flux_cells<D, M, SYS, kFluxWarps, YC, 1><<<g, kFluxWarps * 32, 0, k.stream>>>(
-          q, F, ext, H, n[0], n[1], n[2], k.sy, k.sz, k.ncell, k.gamma, k.ch, bmask, cnt, k.tab);
+          q, F, ext, H, n[0], n[1], n[2], k.sy, k.sz, k.ncell, k.gamma, k.ch, bmask, rmask, cnt, k.tab);
       return;
     }
   }
   k_face_flux_cells<D, M, SYS, kFluxWarps, YC, 0><<<g, kFluxWarps * 32, 0, k.stream>>>(
-      q, F, ext, H, n[0], n[1], n[2], k.sy, k.sz, k.ncell, k.gamma, k.ch, bmask, cnt, k.tab);
+      q, F, ext, H, n[0], n[1], n[2], k.sy, k.sz, k.ncell, k.gamma, k.ch, bmask, rmask, cnt, k.tab);
 }
 }  // namespace
 
 void launch_face_flux_cells(const KCtx& k, const double* q, double* F, const Box& ext, int H, const int n[3],
-                            int bmask, DevCounters* cnt) {
+                            int bmask, int rmask, DevCounters* cnt) {
   if (ext.count() == 0) return;
-  ADER_DISPATCH(k.D, k.M, k.SYS, (flux_cells_for<D, M, SYS>(k, q, F, ext, H, n, bmask, cnt)));
+  ADER_DISPATCH(k.D, k.M, k.SYS, (flux_cells_for<D, M, SYS>(k, q, F, ext, H, n, bmask, rmask, cnt)));
 }
 
 void launch_update(const KCtx& k, double* u, const double* F, const Box& R, const double dtdx[3],

@@ -66,9 +66,10 @@ void launch_predictor_list(const KCtx& k, const double* w, double* q, const Box&
 // active axis), one lane group per cell computing all its lower faces
 // (L2-friendly traversal).  bmask bit 2*dir (2*dir+1): the first (last) face
 // along dir is a physical transmissive boundary and takes the interior trace
-// on both sides.
+// on both sides; rmask, same bits: a reflective wall (R22), the exterior state
+// is the interior trace with the normal momentum negated.
 void launch_face_flux_cells(const KCtx& k, const double* q, double* F, const Box& ext, int H, const int n[3],
-                            int bmask, DevCounters* cnt);
+                            int bmask, int rmask, DevCounters* cnt);
 // FV update of `interior` in place + max CFL speed of the new state.
 void launch_update(const KCtx& k, double* u, const double* F, const Box& interior, const double dtdx[3],
                    const double inv_dx[3], DevCounters* cnt);
@@ -76,7 +77,8 @@ void launch_cfl_speed(const KCtx& k, const double* u, const Box& interior, const
                       DevCounters* cnt);
 // Ghost copy along one axis: for every cell of `region` (halo cells), copy the
 // cell at map(coord[axis]) with the other coordinates unchanged.
-//   mode 0: periodic wrap within [H, H+n), mode 1: clamp to [H, H+n-1]
+//   mode 0: periodic wrap within [H, H+n), mode 1: clamp to [H, H+n-1],
+//   mode 2: mirror about the wall with the normal momentum negated (R22)
 void launch_fill_axis(const KCtx& k, double* u, const Box& region, int axis, int mode, int H, int n);
 // Pack / unpack a box of u into / from a contiguous buffer [box cell][nu].
 void launch_pack(const KCtx& k, const double* u, const Box& b, double* buf);

@@ -60,6 +60,9 @@ CASES = {
                                  ic=W.explosion(2), lmax=2, flux=1),
     "explosion3d_l1_osher": dict(dim=3, degree=2, n=(6, 6, 6), lo=(-1,) * 3, hi=(1,) * 3, bc=(1,) * 6,
                                  ic=W.explosion(3), lmax=1, cfl=0.3, flux=1),
+    # reflective walls at x = 0 and y = 0 (R22): the explosion quadrant
+    "quadrant_explosion_walls_l2": dict(dim=2, degree=2, n=(12, 12), lo=(0, 0), hi=(1, 1), bc=(2, 1, 2, 1, 0, 0),
+                                        ic=W.explosion(2), lmax=2),
 }
 
 
@@ -80,7 +83,8 @@ def test_one_macro_step(name):
     compare(g, o, 1e-11)
 
 
-@pytest.mark.parametrize("name", ["explosion2d_l2", "vortex2d_M3_l1", "explosion2d_l2_osher"])
+@pytest.mark.parametrize("name", ["explosion2d_l2", "vortex2d_M3_l1", "explosion2d_l2_osher",
+                                  "quadrant_explosion_walls_l2"])
 def test_several_macro_steps_with_adapt(name):
     g, o = pair(**CASES[name])
     rg = g.step(1e300, 4)

@@ -39,6 +39,8 @@ CASES = {
                                 W.random_smooth(3, seed=1212, amp=0.08), 6, 3),
     "ot_mhd_M3_periodic_x2": (dict(dim=2, degree=3, n0=(16, 18), lo=(0, 0), hi=(2 * math.pi, 2 * math.pi),
                                    bc=(0,) * 6, system=1, gamma=5 / 3, ch=2.0), W.orszag_tang(), 2, 4),
+    "box2d_walls_x4": (dict(dim=2, degree=2, n0=(20, 18), lo=(0, 0), hi=(1, 1), bc=(2,) * 6, cfl=0.45),
+                       W.random_smooth(2, seed=3585, amp=0.2), 4, 5),
 }
 
 
@@ -93,6 +95,8 @@ AMR_CASES = {
                                cfl=0.3), W.explosion(3), 2, 2),
     "explosion2d_l2_x8_long": (dict(dim=2, degree=2, n0=(40, 32), lo=(-1, -1), hi=(1, 1), bc=(1,) * 6, lmax=2,
                                     cfl=0.45, chi_ref=0.1, chi_rec=0.05), W.explosion(2), 8, 12),
+    "quadrant_walls_l2_x4": (dict(dim=2, degree=2, n0=(24, 24), lo=(0, 0), hi=(1, 1), bc=(2, 1, 2, 1, 0, 0), lmax=2,
+                                  cfl=0.45, chi_ref=0.1, chi_rec=0.05), W.explosion(2), 4, 5),
 }
 
 

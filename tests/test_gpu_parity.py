@@ -60,6 +60,15 @@ CASES = {
                               ic=W.isentropic_vortex(), flux=1),
     "random3d_M2_osher_q4": dict(dim=3, degree=2, n=(7, 6, 9), lo=(0,) * 3, hi=(1,) * 3, bc=(0,) * 6,
                                  ic=W.random_smooth(3, seed=1212, amp=0.08), flux=1, flux_quad=4),
+    # reflective walls (reading R22; blast waves / DMR)
+    "box2d_M2_reflective": dict(dim=2, degree=2, n=(14, 13), lo=(0, 0), hi=(1, 1), bc=(2,) * 6,
+                                ic=W.random_smooth(2, seed=3585, amp=0.2), cfl=0.45),
+    "quadrant_explosion_walls": dict(dim=2, degree=2, n=(16, 15), lo=(0, 0), hi=(1, 1), bc=(2, 1, 2, 1, 0, 0),
+                                     ic=W.explosion(2), cfl=0.45),
+    "box2d_M3_walls_x_periodic_y": dict(dim=2, degree=3, n=(12, 11), lo=(0, 0), hi=(1, 1), bc=(2, 2, 0, 0, 0, 0),
+                                        ic=W.random_smooth(2, seed=1212, amp=0.15), cfl=0.45),
+    "box3d_M2_reflective_osher": dict(dim=3, degree=2, n=(7, 6, 8), lo=(0,) * 3, hi=(1,) * 3, bc=(2,) * 6,
+                                      ic=W.random_smooth(3, seed=3585, amp=0.1), cfl=0.3, flux=1),
 }
 
 
@@ -150,6 +159,18 @@ def test_osher_100_step_parity_and_conservation():
     ug = g.get_state()
     assert rel_err(ug, o.get_cells()) <= 1e-8
     assert np.all(np.abs(ug.sum(0) - u0.sum(0)) <= 1e-11 * np.abs(u0).sum(0))
+
+
+def test_closed_box_50_steps_parity_and_conservation():
+    # all walls reflective: mass and energy are conserved to round-off
+    g, o = pair(2, 2, (20, 18), (0, 0), (1, 1), (2,) * 6, W.random_smooth(2, seed=3585, amp=0.2), cfl=0.45)
+    u0 = g.get_state()
+    g.step(1e300, 50)
+    o.step(1e300, 50)
+    ug = g.get_state()
+    assert rel_err(ug, o.get_cells()) <= 1e-8
+    for v in (0, 3):
+        assert abs(ug[:, v].sum() - u0[:, v].sum()) <= 1e-11 * np.abs(u0[:, v]).sum()
 
 
 def test_constant_state_bitwise():
