@@ -386,7 +386,7 @@ __device__ __forceinline__ bool point_flux(const double* __restrict__ q, long lo
 constexpr int pow2_at_least(int x) { return x <= 1 ? 1 : 2 * pow2_at_least((x + 1) / 2); }
 
 template <int D, int M, int SYS, int WARPS, int YC, int FLUX>
-__global__ void __launch_bounds__(WARPS * 32, (FLUX == 1) ? 5 : (SYS == 1 ? 4 : (D == 3 ? 6 : 8))) k_face_flux_cells(const double* __restrict__ q, double* __restrict__ F,
+__global__ void __launch_bounds__(WARPS * 32, (FLUX == 1) ? 5 : (SYS == 1 ? 4 : (D == 3 ? 7 : 8))) k_face_flux_cells(const double* __restrict__ q, double* __restrict__ F,
                                                                 const Box E, const int H, const int n0, const int n1,
                                                                 const int n2, const long long sy, const long long sz,
                                                                 const long long ncell, const double gamma,
@@ -484,7 +484,7 @@ constexpr int lines_smem_doubles() {
   return 7 * Phys<SYS, 3>::NV * ipow_c(M + 1, 4) + 3 * Phys<SYS, 3>::NV * (32 + 1);
 }
 
-template <int M, int SYS, int WARPS, int YC, int FLUX>
+template <int M, int SYS, int WARPS, int YC, int FLUX, int RUN>
 __global__ void __launch_bounds__(WARPS * 32, 8 / WARPS) k_face_flux_lines(
     const double* __restrict__ q, double* __restrict__ F, const Box E, const int H, const int n0, const int n1,
     const int n2, const long long sy, const long long sz, const long long ncell, const double gamma, const double ch,
@@ -507,26 +507,32 @@ __global__ void __launch_bounds__(WARPS * 32, 8 / WARPS) k_face_flux_lines(
   const int s = ps / NT, tt = ps - (ps / NT) * NT;
   double wt = T.w[s] * T.w[tt % N] * T.w[tt / N];
   const unsigned ex = (unsigned)E.ext[0], ey = (unsigned)E.ext[1], ez = (unsigned)E.ext[2];
-  const unsigned nlines = ((ey + YC - 1) / YC) * YC * ez;
+  const unsigned nxr = (ex + RUN - 1) / RUN;   // x-runs per line
+  const unsigned nitems = nxr * ((ey + YC - 1) / YC) * YC * ez;
   const unsigned gw = blockIdx.x * WARPS + warp, nw = gridDim.x * WARPS;
   const int zH = H;
-  for (unsigned li = gw; li < nlines; li += nw) {
+  // items: runs of RUN cells, x-run fastest, then y inside chunks of YC rows,
+  // then z, then the chunk (short reuse distance of the neighbour blocks in L2)
+  for (unsigned it = gw; it < nitems; it += nw) {
+    const unsigned xr = it % nxr, li = it / nxr;
     const unsigned yi = li % YC, t2 = li / YC;
     const unsigned yb = t2 / ez, z = t2 - yb * ez;
     const unsigned y = yb * YC + yi;
     if (y >= ey) continue;
+    const unsigned x0 = xr * RUN, x1 = min(ex, x0 + RUN);
     const int cy = E.lo[1] + (int)y, cz = E.lo[2] + (int)z;
-    const long long c0 = (long long)E.lo[0] + cy * sy + cz * sz;
+    const long long c0 = (long long)E.lo[0] + x0 + cy * sy + cz * sz;
     const bool iny = cy < H + n1, inz = cz < zH + n2;
+    const unsigned len = x1 - x0;
     // prologue: x-neighbour of the first cell, the first cell and its y-, z-neighbours
     copy_block_async<BLK>(ring[2], q + (c0 - 1) * BLK, lane);
     copy_block_async<BLK>(ring[0], q + c0 * BLK, lane);
     copy_block_async<BLK>(ybuf[0], q + (c0 - sy) * BLK, lane);
     copy_block_async<BLK>(zbuf[0], q + (c0 - sz) * BLK, lane);
     cp_async_commit();
-    for (unsigned i = 0; i < ex; ++i) {
+    for (unsigned i = 0; i < len; ++i) {
       const long long c = c0 + i;
-      if (i + 1 < ex) {
+      if (i + 1 < len) {
         copy_block_async<BLK>(ring[(i + 1) % 3], q + (c + 1) * BLK, lane);
         copy_block_async<BLK>(ybuf[(i + 1) & 1], q + (c + 1 - sy) * BLK, lane);
         copy_block_async<BLK>(zbuf[(i + 1) & 1], q + (c + 1 - sz) * BLK, lane);
@@ -536,7 +542,7 @@ __global__ void __launch_bounds__(WARPS * 32, 8 / WARPS) k_face_flux_lines(
         cp_async_wait<0>();
       }
       __syncwarp();
-      const int cx = E.lo[0] + (int)i;
+      const int cx = E.lo[0] + (int)(x0 + i);
       const bool inx = cx < H + n0;
       const double* own = ring[i % 3];
       double v[K];
@@ -822,7 +828,8 @@ void flux_lines_launch(const KCtx& k, const double* q, double* F, const Box& ext
                        int rmask, DevCounters* cnt) {
   constexpr int YC = 16, WARPS = 2;
   const size_t sm = sizeof(double) * (size_t)WARPS * lines_smem_doubles<M, SYS>();
-  auto kern = k_face_flux_lines<M, SYS, WARPS, YC, FLUX>;
+  constexpr int RUN = 16;
+  auto kern = k_face_flux_lines<M, SYS, WARPS, YC, FLUX, RUN>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -831,9 +838,9 @@ void flux_lines_launch(const KCtx& k, const double* q, double* F, const Box& ext
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WARPS * 32, sm);
   if (per_sm < 1) per_sm = 1;
-  const long long lines = (long long)((ext.ext[1] + YC - 1) / YC) * YC * ext.ext[2];
+  const long long items = (long long)((ext.ext[0] + RUN - 1) / RUN) * ((ext.ext[1] + YC - 1) / YC) * YC * ext.ext[2];
   const long long want = 148LL * per_sm;
-  const unsigned g = (unsigned)std::min(want, (lines + WARPS - 1) / WARPS);
+  const unsigned g = (unsigned)std::min(want, (items + WARPS - 1) / WARPS);
   count_launch(k);
   kern<<<g, WARPS * 32, sm, k.stream>>>(q, F, ext, H, n[0], n[1], n[2], k.sy, k.sz, k.ncell, k.gamma, k.ch, bmask,
                                         rmask, cnt, k.tab);
