@@ -679,12 +679,7 @@ static ader_status create_impl(const ader_config* cfg, ader_ctx** out, bool loop
   if (!build_osher_quadrature(cfg->flux_quad > 0 ? cfg->flux_quad : 3, &c->k.tab))
     return fail(c, ADER_ERR_CONFIG, "no path rule for flux_quad=%d", cfg->flux_quad);
   c->k.tab.flux = cfg->flux;
-  {
-    // A/B switch for the 3D face-flux kernel (tests, bench): ADER_FLUX_KERNEL=lines
-    // selects the x-run walker with cp.async staging; default: cell per warp
-    const char* e = std::getenv("ADER_FLUX_KERNEL");
-    c->k.flux_lines = e && std::strcmp(e, "lines") == 0;
-  }
+
   c->k.D = c->d; c->k.M = c->M; c->k.SYS = cfg->system; c->k.NV = c->nv;
   c->k.sy = c->P[0]; c->k.sz = (long long)c->P[0] * c->P[1];
   c->k.ncell = c->ncell;

@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(256) k_weno(const double* __restrict__ src, do
 // carry the same flux, so it is evaluated once and q^1_s = w - (sum_s' T_ss') G.
 // ===========================================================================
 template <int D, int M, int SYS, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? 4 : 2) k_predictor(
+__global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? (D == 3 ? 5 : 4) : 2) k_predictor(
     const double* __restrict__ w, double* __restrict__ q, const Box R, const long long sy, const long long sz,
     const double dtdx0, const double dtdx1, const double dtdx2, const double gamma, const double ch,
     const double tol, const int max_sweeps, DevCounters* __restrict__ cnt, const int* __restrict__ list,
@@ -454,127 +454,6 @@ __global__ void __launch_bounds__(WARPS * 32, (FLUX == 1) ? 5 : (SYS == 1 ? 4 : 
   }
 }
 
-// ---------------------------------------------------------------------------
-// a3 for 3D (one cell per warp, a lane per space-time face point): persistent
-// warps walk whole x-lines of the extended box.  The cell blocks a cell needs
-// (its own, the y- and z-neighbours'; the x-neighbour is the previous cell of
-// the line) are copied into shared memory with cp.async while the previous
-// cell is computed, so the global loads run ahead of the arithmetic instead of
-// stalling it (the cell-per-warp kernel waited on long scoreboards).  Same
-// point arithmetic and point-sum order as k_face_flux_cells: bitwise equal.
-// Lines are visited y fastest inside chunks of YC rows, then z, then the
-// chunk, so the neighbour lines were copied a few MB earlier (L2 hits).
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int NPEND>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(NPEND) : "memory"); }
-
-template <int BLK>
-__device__ __forceinline__ void copy_block_async(double* dst, const double* __restrict__ src, int lane) {
-#pragma unroll
-  for (int j = lane; j < BLK; j += 32) cp_async8(dst + j, src + j);
-}
-
-template <int M, int SYS>
-constexpr int lines_smem_doubles() {
-  return 7 * Phys<SYS, 3>::NV * ipow_c(M + 1, 4) + 3 * Phys<SYS, 3>::NV * (32 + 1);
-}
-
-template <int M, int SYS, int WARPS, int YC, int FLUX, int RUN>
-__global__ void __launch_bounds__(WARPS * 32, 8 / WARPS) k_face_flux_lines(
-    const double* __restrict__ q, double* __restrict__ F, const Box E, const int H, const int n0, const int n1,
-    const int n2, const long long sy, const long long sz, const long long ncell, const double gamma, const double ch,
-    const int bmask, const int rmask, DevCounters* __restrict__ cnt, const __grid_constant__ DevTables T) {
-  constexpr int D = 3;
-  using PH = Phys<SYS, D>;
-  constexpr int NV = PH::NV, N = M + 1, NS = ipow_c(N, D), NT = NS / N, BLK = NV * NS * N;
-  constexpr int K = D * NV;
-  static_assert(NS <= 32, "one cell per warp");
-  extern __shared__ double smem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* ws = smem + (size_t)warp * lines_smem_doubles<M, SYS>();
-  double* ring[3] = {ws, ws + BLK, ws + 2 * BLK};          // own blocks of cells i-1, i, i+1
-  double* ybuf[2] = {ws + 3 * BLK, ws + 4 * BLK};           // y-neighbour blocks (double buffered)
-  double* zbuf[2] = {ws + 5 * BLK, ws + 6 * BLK};           // z-neighbour blocks
-  double(*rb)[33] = reinterpret_cast<double(*)[33]>(ws + 7 * BLK);
-  const int p = lane;
-  const bool pok = p < NS;
-  const int ps = pok ? p : 0;
-  const int s = ps / NT, tt = ps - (ps / NT) * NT;
-  double wt = T.w[s] * T.w[tt % N] * T.w[tt / N];
-  const unsigned ex = (unsigned)E.ext[0], ey = (unsigned)E.ext[1], ez = (unsigned)E.ext[2];
-  const unsigned nxr = (ex + RUN - 1) / RUN;   // x-runs per line
-  const unsigned nitems = nxr * ((ey + YC - 1) / YC) * YC * ez;
-  const unsigned gw = blockIdx.x * WARPS + warp, nw = gridDim.x * WARPS;
-  const int zH = H;
-  // items: runs of RUN cells, x-run fastest, then y inside chunks of YC rows,
-  // then z, then the chunk (short reuse distance of the neighbour blocks in L2)
-  for (unsigned it = gw; it < nitems; it += nw) {
-    const unsigned xr = it % nxr, li = it / nxr;
-    const unsigned yi = li % YC, t2 = li / YC;
-    const unsigned yb = t2 / ez, z = t2 - yb * ez;
-    const unsigned y = yb * YC + yi;
-    if (y >= ey) continue;
-    const unsigned x0 = xr * RUN, x1 = min(ex, x0 + RUN);
-    const int cy = E.lo[1] + (int)y, cz = E.lo[2] + (int)z;
-    const long long c0 = (long long)E.lo[0] + x0 + cy * sy + cz * sz;
-    const bool iny = cy < H + n1, inz = cz < zH + n2;
-    const unsigned len = x1 - x0;
-    // prologue: x-neighbour of the first cell, the first cell and its y-, z-neighbours
-    copy_block_async<BLK>(ring[2], q + (c0 - 1) * BLK, lane);
-    copy_block_async<BLK>(ring[0], q + c0 * BLK, lane);
-    copy_block_async<BLK>(ybuf[0], q + (c0 - sy) * BLK, lane);
-    copy_block_async<BLK>(zbuf[0], q + (c0 - sz) * BLK, lane);
-    cp_async_commit();
-    for (unsigned i = 0; i < len; ++i) {
-      const long long c = c0 + i;
-      if (i + 1 < len) {
-        copy_block_async<BLK>(ring[(i + 1) % 3], q + (c + 1) * BLK, lane);
-        copy_block_async<BLK>(ybuf[(i + 1) & 1], q + (c + 1 - sy) * BLK, lane);
-        copy_block_async<BLK>(zbuf[(i + 1) & 1], q + (c + 1 - sz) * BLK, lane);
-        cp_async_commit();
-        cp_async_wait<1>();
-      } else {
-        cp_async_wait<0>();
-      }
-      __syncwarp();
-      const int cx = E.lo[0] + (int)(x0 + i);
-      const bool inx = cx < H + n0;
-      const double* own = ring[i % 3];
-      double v[K];
-      bool good = true;
-      good &= point_flux_blocks<D, M, SYS, 0, FLUX, false>(
-          ring[(i + 2) % 3], own, ps, iny && inz && pok, (bmask & 1) && cx == H, (bmask & 2) && cx == H + n0,
-          (rmask & 1) && cx == H, (rmask & 2) && cx == H + n0, wt, gamma, ch, T, v);
-      good &= point_flux_blocks<D, M, SYS, 1, FLUX, false>(
-          ybuf[i & 1], own, ps, inx && inz && pok, (bmask & 4) && cy == H, (bmask & 8) && cy == H + n1,
-          (rmask & 4) && cy == H, (rmask & 8) && cy == H + n1, wt, gamma, ch, T, v + NV);
-      good &= point_flux_blocks<D, M, SYS, 2, FLUX, false>(
-          zbuf[i & 1], own, ps, inx && iny && pok, (bmask & 16) && cz == zH, (bmask & 32) && cz == zH + n2,
-          (rmask & 16) && cz == zH, (rmask & 32) && cz == zH + n2, wt, gamma, ch, T, v + 2 * NV);
-      if (!good) record_error(cnt, 1, 2, c);
-      if (pok) {
-#pragma unroll
-        for (int k = 0; k < K; ++k) rb[k][p] = v[k];
-      }
-      __syncwarp();
-      if (p < K) {
-        double acc = rb[p][0];
-#pragma unroll
-        for (int j = 1; j < NS; ++j) acc += rb[p][j];
-        const int dir = p / NV, var = p - dir * NV;
-        const bool face_ok = dir == 0 ? (iny && inz) : (dir == 1 ? (inx && inz) : (inx && iny));
-        if (face_ok) F[((long long)dir * ncell + c) * NV + var] = acc;
-      }
-      __syncwarp();   // the buffers of cell i are refilled by the next prefetch
-    }
-  }
-}
-
 // ===========================================================================
 // a4: FV update + next CFL speed (block max, then one atomicMax per block).
 // ===========================================================================
@@ -823,40 +702,9 @@ void launch_predictor_list(const KCtx& k, const double* w, double* q, const Box&
 }
 
 namespace {
-template <int M, int SYS, int FLUX>
-void flux_lines_launch(const KCtx& k, const double* q, double* F, const Box& ext, int H, const int n[3], int bmask,
-                       int rmask, DevCounters* cnt) {
-  constexpr int YC = 16, WARPS = 2;
-  const size_t sm = sizeof(double) * (size_t)WARPS * lines_smem_doubles<M, SYS>();
-  constexpr int RUN = 16;
-  auto kern = k_face_flux_lines<M, SYS, WARPS, YC, FLUX, RUN>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    attr = true;
-  }
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WARPS * 32, sm);
-  if (per_sm < 1) per_sm = 1;
-  const long long items = (long long)((ext.ext[0] + RUN - 1) / RUN) * ((ext.ext[1] + YC - 1) / YC) * YC * ext.ext[2];
-  const long long want = 148LL * per_sm;
-  const unsigned g = (unsigned)std::min(want, (items + WARPS - 1) / WARPS);
-  count_launch(k);
-  kern<<<g, WARPS * 32, sm, k.stream>>>(q, F, ext, H, n[0], n[1], n[2], k.sy, k.sz, k.ncell, k.gamma, k.ch, bmask,
-                                        rmask, cnt, k.tab);
-}
-
 template <int D, int M, int SYS>
 void flux_cells_for(const KCtx& k, const double* q, double* F, const Box& ext, int H, const int n[3], int bmask,
                     int rmask, DevCounters* cnt) {
-  if constexpr (D == 3) {
-    if (k.flux_lines) {
-      if constexpr (SYS == 0) {
-        if (k.tab.flux == 1) return flux_lines_launch<M, SYS, 1>(k, q, F, ext, H, n, bmask, rmask, cnt);
-      }
-      return flux_lines_launch<M, SYS, 0>(k, q, F, ext, H, n, bmask, rmask, cnt);
-    }
-  }
   constexpr int YC = 16;
   constexpr int NS = ipow_c(M + 1, D);
   constexpr int CPW = 32 / ((NS <= 8) ? 8 : (NS <= 16 ? 16 : 32));

@@ -46,7 +46,6 @@ struct KCtx {
   double gamma, ch;
   cudaStream_t stream;
   long long* launches;            // host counter of kernel launches (instrumentation)
-  bool flux_lines = false;        // 3D face flux: x-run walker with cp.async staging (else cell per warp)
   DevTables tab;
 };
 
