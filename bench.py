@@ -81,7 +81,13 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.perf_counter(), line.strip()))
+
+    def window(self, t0, t1):
+        # samples taken inside [t0, t1] (host clock); the sampler is started
+        # before the warm-up so that nvidia-smi's own start-up (NVML init can
+        # hold the driver for a while) never falls inside the timed region
+        self.t0, self.t1 = t0, t1
 
     def stop(self):
         if not self.proc:
@@ -94,7 +100,9 @@ class ClockSampler:
         self.t.join(timeout=2)
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        t0, t1 = getattr(self, "t0", -1e300), getattr(self, "t1", 1e300)
+        lines = [ln for ts, ln in self.lines if t0 - 0.25 <= ts <= t1 + 0.25] or [ln for _, ln in self.lines[-3:]]
+        for ln in lines:
             parts = [x.strip() for x in ln.split(",")]
             if len(parts) < 8:
                 continue
@@ -246,6 +254,8 @@ def main():
             dist.barrier()
             torch.cuda.synchronize()
 
+    clk = ClockSampler(local)
+    clk.start()
     # warm-up
     if args.warmup:
         s.step(1e300, args.warmup)
@@ -253,15 +263,15 @@ def main():
     # timed region: exactly K macro steps
     s.set_profiling(True)
     l0 = s.launch_count()
-    clk = ClockSampler(local)
-    clk.start()
-    time.sleep(0.3)
+    time.sleep(0.5)
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    h0 = time.perf_counter()
     e0.record(stream)
     rep = s.step(1e300, args.steps)
     e1.record(stream)
     barrier()
+    clk.window(h0, time.perf_counter())
     clocks = clk.stop()
     ms = e0.elapsed_time(e1)
     launches = s.launch_count() - l0

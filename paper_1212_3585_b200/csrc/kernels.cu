@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(256) k_weno(const double* __restrict__ src, do
 // carry the same flux, so it is evaluated once and q^1_s = w - (sum_s' T_ss') G.
 // ===========================================================================
 template <int D, int M, int SYS, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? (D == 3 ? 5 : 4) : 2) k_predictor(
+__global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? 4 : 2) k_predictor(
     const double* __restrict__ w, double* __restrict__ q, const Box R, const long long sy, const long long sz,
     const double dtdx0, const double dtdx1, const double dtdx2, const double gamma, const double ch,
     const double tol, const int max_sweeps, DevCounters* __restrict__ cnt, const int* __restrict__ list,
@@ -304,9 +304,9 @@ __device__ __forceinline__ double ldq(const double* p) {
 }
 
 // One space-time quadrature point of the face between the cell blocks qL0
-// (lower side) and qR0 (upper side), [NV][N^(D+1)] each, in global (GLOBAL)
-// or shared memory.
-template <int D, int M, int SYS, int DIR, int FLUX, bool GLOBAL>
+// (lower side) and qR0 (upper side), [NV][N^(D+1)] each, in global (GL_L,
+// GL_R) or shared memory.
+template <int D, int M, int SYS, int DIR, int FLUX, bool GL_L, bool GL_R = GL_L>
 __device__ __forceinline__ bool point_flux_blocks(const double* qL0, const double* qR0, int p, bool fok, bool tlo,
                                                   bool thi, bool rlo, bool rhi, double wt, double gamma, double ch,
                                                   const DevTables& T, double* val) {
@@ -330,12 +330,12 @@ __device__ __forceinline__ bool point_flux_blocks(const double* qL0, const doubl
   double um[NV], up[NV];
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
-    double a = T.psi1[0] * ldq<GLOBAL>(&qL[v * NST]);   // q_h^- (xi = 1 of the left cell)
-    double b = T.psi0[0] * ldq<GLOBAL>(&qR[v * NST]);   // q_h^+ (xi = 0 of the right cell)
+    double a = T.psi1[0] * ldq<GL_L>(&qL[v * NST]);   // q_h^- (xi = 1 of the left cell)
+    double b = T.psi0[0] * ldq<GL_R>(&qR[v * NST]);   // q_h^+ (xi = 0 of the right cell)
 #pragma unroll
     for (int k = 1; k < N; ++k) {
-      a += T.psi1[k] * ldq<GLOBAL>(&qL[v * NST + k * sn]);
-      b += T.psi0[k] * ldq<GLOBAL>(&qR[v * NST + k * sn]);
+      a += T.psi1[k] * ldq<GL_L>(&qL[v * NST + k * sn]);
+      b += T.psi0[k] * ldq<GL_R>(&qR[v * NST + k * sn]);
     }
     um[v] = (tlo || rlo) ? b : a;   // transmissive boundary: interior trace on both sides (R5)
     up[v] = (thi || rhi) ? a : b;
@@ -424,19 +424,35 @@ __global__ void __launch_bounds__(WARPS * 32, (FLUX == 1) ? 5 : (SYS == 1 ? 4 : 
   if (D == 3) wt *= T.w[tt / N];
   double v[KP];
   bool good = true;
-  good &= point_flux<D, M, SYS, 0, FLUX>(q, cR, 1, ps, fok[0], (bmask & 1) && cx == H, (bmask & 2) && cx == H + n0,
-                                         (rmask & 1) && cx == H, (rmask & 2) && cx == H + n0, wt, gamma, ch, T, v);
-  good &= point_flux<D, M, SYS, 1, FLUX>(q, cR, sy, ps, fok[1], (bmask & 4) && cy == H, (bmask & 8) && cy == H + n1,
-                                         (rmask & 4) && cy == H, (rmask & 8) && cy == H + n1, wt, gamma, ch, T, v + NV);
+  constexpr int K = D * NV;
+  constexpr int BLK = NV * NS * N;
+  // the cell's own block is read by all D faces: one coalesced pass into
+  // shared memory (when it fits next to the reduction buffer), the lower
+  // neighbours' pencils straight from global memory
+  constexpr bool STAGE = sizeof(double) * WARPS * CPW * (BLK + K * (G + 1)) <= 44 * 1024;
+  __shared__ double ownb[STAGE ? WARPS * CPW : 1][STAGE ? BLK : 1];
+  const double* qown = q + cR * BLK;
+  if constexpr (STAGE) {
+    double* ob = ownb[warp * CPW + lane / G];
+    if (ok)
+      for (int j = p; j < BLK; j += G) ob[j] = __ldg(qown + j);
+    __syncwarp();
+    qown = ob;
+  }
+  good &= point_flux_blocks<D, M, SYS, 0, FLUX, true, !STAGE>(
+      q + (cR - 1) * BLK, qown, ps, fok[0], (bmask & 1) && cx == H, (bmask & 2) && cx == H + n0,
+      (rmask & 1) && cx == H, (rmask & 2) && cx == H + n0, wt, gamma, ch, T, v);
+  good &= point_flux_blocks<D, M, SYS, 1, FLUX, true, !STAGE>(
+      q + (cR - sy) * BLK, qown, ps, fok[1], (bmask & 4) && cy == H, (bmask & 8) && cy == H + n1,
+      (rmask & 4) && cy == H, (rmask & 8) && cy == H + n1, wt, gamma, ch, T, v + NV);
   if constexpr (D == 3)
-    good &= point_flux<D, M, SYS, 2, FLUX>(q, cR, sz, ps, fok[2], (bmask & 16) && cz == zH,
-                                           (bmask & 32) && cz == zH + n2, (rmask & 16) && cz == zH,
-                                           (rmask & 32) && cz == zH + n2, wt, gamma, ch, T, v + 2 * NV);
+    good &= point_flux_blocks<D, M, SYS, 2, FLUX, true, !STAGE>(
+        q + (cR - sz) * BLK, qown, ps, fok[2], (bmask & 16) && cz == zH, (bmask & 32) && cz == zH + n2,
+        (rmask & 16) && cz == zH, (rmask & 32) && cz == zH + n2, wt, gamma, ch, T, v + 2 * NV);
   if (!good) record_error(cnt, 1, 2, cR);
   // point sums through shared memory: lane p stores its K = D*NV weighted
   // point fluxes in column p, then lane i sums row i over the NS points in
   // order (rows padded to G+1 doubles: conflict-free column writes and row reads)
-  constexpr int K = D * NV;
   __shared__ double red[WARPS * CPW][K][G + 1];
   double(*rb)[G + 1] = red[warp * CPW + lane / G];
   if (pok) {
