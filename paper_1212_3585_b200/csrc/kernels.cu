@@ -426,19 +426,10 @@ __global__ void __launch_bounds__(WARPS * 32, (FLUX == 1) ? 5 : (SYS == 1 ? 4 : 
   bool good = true;
   constexpr int K = D * NV;
   constexpr int BLK = NV * NS * N;
-  // the cell's own block is read by all D faces: one coalesced pass into
-  // shared memory (when it fits next to the reduction buffer), the lower
-  // neighbours' pencils straight from global memory
-  constexpr bool STAGE = sizeof(double) * WARPS * CPW * (BLK + K * (G + 1)) <= 44 * 1024;
-  __shared__ double ownb[STAGE ? WARPS * CPW : 1][STAGE ? BLK : 1];
+  // (staging the cell's own block in shared memory for its D faces was
+  // tried: 1.6x slower at 256^3 — the pencil reads stay global / L1)
   const double* qown = q + cR * BLK;
-  if constexpr (STAGE) {
-    double* ob = ownb[warp * CPW + lane / G];
-    if (ok)
-      for (int j = p; j < BLK; j += G) ob[j] = __ldg(qown + j);
-    __syncwarp();
-    qown = ob;
-  }
+  constexpr bool STAGE = false;
   good &= point_flux_blocks<D, M, SYS, 0, FLUX, true, !STAGE>(
       q + (cR - 1) * BLK, qown, ps, fok[0], (bmask & 1) && cx == H, (bmask & 2) && cx == H + n0,
       (rmask & 1) && cx == H, (rmask & 2) && cx == H + n0, wt, gamma, ch, T, v);
