@@ -64,16 +64,19 @@ class ClockSampler:
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, device=0):
+    def __init__(self, device=0, period_ms=None):
         self.device = device
         self.proc = None
         self.lines = []
+        self.period_ms = int(os.environ.get("ADER_BENCH_CLOCK_MS", "200")) if period_ms is None else period_ms
 
     def start(self):
+        if self.period_ms <= 0:   # diagnostics only: no sampler
+            return
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", str(self.period_ms)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except Exception:

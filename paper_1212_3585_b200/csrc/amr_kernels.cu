@@ -371,6 +371,141 @@ __global__ void __launch_bounds__(64) k_amr_flux_update(AmrDevView V, const __gr
 }
 
 // ---------------------------------------------------------------------------
+// Lane-parallel variant: a lane group of G >= N^D lanes per cell, a lane per
+// space-time point of the face being processed (as in k_face_flux_cells), the
+// point sums through shared memory in point order.  Face kinds, coarse-fine
+// traces, flux memory deposit / consumption and the update are those of
+// cell_face / k_amr_flux_update above (which remain the reference form).
+template <int D, int M, int SYS, int DIR>
+__device__ __forceinline__ bool amr_face_point(int kind, const double* qL, const double* qR, int o1, int o2, int m,
+                                               int s, int t1, int t2, double gamma, double ch, const DevTables& T,
+                                               const SubTables& S, double (&ft)[Phys<SYS, D>::NV]) {
+  constexpr int NV = Phys<SYS, D>::NV;
+  double um[NV], up[NV];
+  if (kind == 0 || kind == 2 || kind == 4 || kind == 6) trace_full<D, M, NV, DIR>(qL, true, t1, t2, s, T, um);
+  if (kind == 0 || kind == 1 || kind == 3 || kind == 5) trace_full<D, M, NV, DIR>(qR, false, t1, t2, s, T, up);
+  if (kind == 5) { for (int v = 0; v < NV; ++v) um[v] = up[v]; um[1 + DIR] = -up[1 + DIR]; }   // R22
+  if (kind == 6) { for (int v = 0; v < NV; ++v) up[v] = um[v]; up[1 + DIR] = -um[1 + DIR]; }
+  if (kind == 3) trace_coarse<D, M, NV, DIR>(qL, true, o1, o2, m, t1, t2, s, T, S, um);
+  if (kind == 4) trace_coarse<D, M, NV, DIR>(qR, false, o1, o2, m, t1, t2, s, T, S, up);
+  if (kind == 1) for (int v = 0; v < NV; ++v) um[v] = up[v];
+  if (kind == 2) for (int v = 0; v < NV; ++v) up[v] = um[v];
+  return numflux_pt<SYS, D, DIR>(um, up, gamma, ch, T, ft);
+}
+
+template <int D, int M, int SYS, int DIR, int G>
+__device__ __forceinline__ bool amr_cell_face_w(const AmrDevView& V, int c, bool valid, int side, int m, int p,
+                                                double gamma, double ch, const DevTables& T, const SubTables& S,
+                                                double (*rb)[G + 1], double* Fout) {
+  constexpr int NV = Phys<SYS, D>::NV, N = M + 1, NS = ipow_a(N, D), NST = NS * N, NT = NS / N;
+  const int l = V.level[c];
+  long long ix[3] = {V.idx[(long long)c * 3], V.idx[(long long)c * 3 + 1], V.idx[(long long)c * 3 + 2]};
+  ix[DIR] += side ? 1 : -1;
+  const double* qc = V.q + (long long)c * NV * NST;
+  const bool out = ix[DIR] < 0 || ix[DIR] >= V.n[l][DIR];
+  // kind: 0..6 as in face_flux_amr, 7 memory of own virtual children, -1 error.
+  // Every lane group of the warp runs the same two __syncwarp()s whatever its
+  // kind (2D: several cells per warp).
+  int kind = -1, nb = -1, o1 = 0, o2 = 0;
+  const double *qL = qc, *qR = qc;
+  if (out && V.bc[2 * DIR + side] == ADER_BC_TRANSMISSIVE) kind = side ? 2 : 1;
+  else if (out && V.bc[2 * DIR + side] == ADER_BC_REFLECTIVE) kind = side ? 6 : 5;
+  else {
+    nb = amr_lookup(V, l, ix[0], ix[1], ix[2]);
+    const int st = nb >= 0 ? V.status[nb] : 9;
+    if (st == 0) {
+      const double* qn = V.q + (long long)nb * NV * NST;
+      kind = 0;
+      qL = side ? qc : qn;
+      qR = side ? qn : qc;
+    } else if (st == 1) {
+      // coarse-fine: the virtual neighbour scales its mother's q_h down
+      const double* qK = V.q + (long long)V.mother[nb] * NV * NST;
+      constexpr int ax0 = (DIR == 0) ? 1 : 0, ax1 = (DIR == 2) ? 1 : 2;
+      o1 = (int)(V.idx[(long long)c * 3 + ax0] % V.r);
+      o2 = (D == 3) ? (int)(V.idx[(long long)c * 3 + ax1] % V.r) : 0;
+      kind = side ? 4 : 3;
+      qL = side ? qc : qK;
+      qR = side ? qK : qc;
+    } else if (st == -1) {
+      kind = V.child[c] >= 0 ? 7 : -1;
+    }
+  }
+  bool ok = kind >= 0;
+  if (valid && kind >= 0 && kind < 7 && p < NS) {
+    const int s = p / NT, t = p - s * NT, t1 = t % N, t2 = t / N;
+    double ft[NV];
+    ok = amr_face_point<D, M, SYS, DIR>(kind, qL, qR, o1, o2, m, s, t1, t2, gamma, ch, T, S, ft);
+    double wgt = T.w[s] * T.w[t1];
+    if (D == 3) wgt *= T.w[t2];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) rb[v][p] = wgt * ft[v];
+  }
+  __syncwarp();
+  if (valid && p < NV) {
+    if (kind == 7) {
+      // virtual mother: the memory of our own virtual children on this face (eqn.memory.sum)
+      const int ch0 = V.child[c];
+      double acc = 0.0;
+      for (int qd = 0; qd < V.rd; ++qd) {
+        const int off[3] = {qd % V.r, (qd / V.r) % V.r, qd / (V.r * V.r)};
+        if (off[DIR] != (side ? V.r - 1 : 0)) continue;
+        double* mm = V.mem + ((long long)(ch0 + qd) * 6 + 2 * DIR + side) * NV;
+        acc += mm[p];
+        mm[p] = 0.0;
+      }
+      Fout[p] = acc / (double)V.rd;
+    } else if (kind >= 0) {
+      double acc = rb[p][0];
+#pragma unroll
+      for (int j = 1; j < NS; ++j) acc += rb[p][j];
+      Fout[p] = acc;
+      if (kind == 3 || kind == 4) V.mem[((long long)nb * 6 + 2 * DIR + (side ? 0 : 1)) * NV + p] += acc;   // nb's face toward c
+    }
+  }
+  __syncwarp();
+  return ok;
+}
+
+template <int D, int M, int SYS, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) k_amr_flux_update_w(AmrDevView V, const __grid_constant__ SubTables S,
+                                                                   const int* __restrict__ list, int n, int m,
+                                                                   double dtdx0, double dtdx1, double dtdx2,
+                                                                   double gamma, double ch, DevCounters* cnt,
+                                                                   const __grid_constant__ DevTables T) {
+  constexpr int NV = Phys<SYS, D>::NV, NS = ipow_a(M + 1, D);
+  constexpr int G = (NS <= 8) ? 8 : (NS <= 16 ? 16 : 32);
+  constexpr int CPW = 32 / G;
+  __shared__ double red[WARPS * CPW][NV][G + 1];
+  __shared__ double Fs[WARPS * CPW][6][NV];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int p = lane & (G - 1), grp = warp * CPW + lane / G;
+  const int i = (blockIdx.x * WARPS + warp) * CPW + lane / G;
+  const bool valid = i < n;
+  const int c = list[valid ? i : 0];
+  double(*rb)[G + 1] = red[grp];
+  double* F = &Fs[grp][0][0];
+  bool ok = true;
+  ok &= amr_cell_face_w<D, M, SYS, 0, G>(V, c, valid, 0, m, p, gamma, ch, T, S, rb, F + 0 * NV);
+  ok &= amr_cell_face_w<D, M, SYS, 0, G>(V, c, valid, 1, m, p, gamma, ch, T, S, rb, F + 1 * NV);
+  ok &= amr_cell_face_w<D, M, SYS, 1, G>(V, c, valid, 0, m, p, gamma, ch, T, S, rb, F + 2 * NV);
+  ok &= amr_cell_face_w<D, M, SYS, 1, G>(V, c, valid, 1, m, p, gamma, ch, T, S, rb, F + 3 * NV);
+  if constexpr (D == 3) {
+    ok &= amr_cell_face_w<D, M, SYS, 2, G>(V, c, valid, 0, m, p, gamma, ch, T, S, rb, F + 4 * NV);
+    ok &= amr_cell_face_w<D, M, SYS, 2, G>(V, c, valid, 1, m, p, gamma, ch, T, S, rb, F + 5 * NV);
+  }
+  if (valid && !ok && (!V.own || V.own[c])) amr_error(cnt, 1, 2, c);   // multi-rank: band cells' errors do not count
+  __syncwarp();
+  if (valid && p < NV) {
+    const double dtdx[3] = {dtdx0, dtdx1, dtdx2};
+    double uu = V.u[(long long)c * NV + p];
+#pragma unroll
+    for (int d = 0; d < D; ++d) uu = uu - dtdx[d] * (F[(2 * d + 1) * NV + p] - F[(2 * d) * NV + p]);
+    V.u[(long long)c * NV + p] = uu;
+  }
+}
+
+// ---------------------------------------------------------------------------
 template <int D, int SYS>
 __global__ void __launch_bounds__(256) k_amr_cfl(AmrDevView V, const int* __restrict__ list, int n, double i0,
                                                  double i1, double i2, double gamma, double ch,
@@ -612,9 +747,13 @@ void amr_launch_flux_update(const KCtx& k, const AmrDevView& v, const SubTables&
                             const double dtdx[3], DevCounters* cnt) {
   if (n <= 0) return;
   cl(k);
-  AMR_DISPATCH(k.D, k.M, k.SYS,
-               k_amr_flux_update<D, M, SYS><<<gsz(n, 64), 64, 0, k.stream>>>(v, st, list, n, m, dtdx[0], dtdx[1],
-                                                                            dtdx[2], k.gamma, k.ch, cnt, k.tab));
+  AMR_DISPATCH(k.D, k.M, k.SYS, {
+    constexpr int NS = ipow_a(M + 1, D);
+    constexpr int CPW = 32 / ((NS <= 8) ? 8 : (NS <= 16 ? 16 : 32));
+    constexpr int WARPS = 4;
+    k_amr_flux_update_w<D, M, SYS, WARPS><<<gsz(n, WARPS * CPW), WARPS * 32, 0, k.stream>>>(
+        v, st, list, n, m, dtdx[0], dtdx[1], dtdx[2], k.gamma, k.ch, cnt, k.tab);
+  });
 }
 
 void amr_launch_cfl(const KCtx& k, const AmrDevView& v, const int* list, int n, const double inv_dx0[3],
