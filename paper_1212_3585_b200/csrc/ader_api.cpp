@@ -103,6 +103,8 @@ struct ader_ctx {
   long long halo_cap = 0;
   DevCounters* cnt = nullptr;                  // device
   DevCounters* hcnt = nullptr;                 // pinned host mirror
+  StepState* st = nullptr;                     // device step control (uniform path)
+  StepState* hst = nullptr;                    // pinned host mirror
   double t = 0.0;
   bool speed_valid = false;
   ncclComm_t comm = nullptr;
@@ -438,7 +440,7 @@ int boundary_mask(const ader_ctx* c, int bc) {
 int transmissive_mask(const ader_ctx* c) { return boundary_mask(c, ADER_BC_TRANSMISSIVE); }
 int reflective_mask(const ader_ctx* c) { return boundary_mask(c, ADER_BC_REFLECTIVE); }
 
-void run_predictor(ader_ctx* c, double dt) {
+void run_predictor(ader_ctx* c, double dt, const double* dtdx_dev = nullptr) {
   // owned block + the face-neighbour layer, except beyond transmissive sides (R5)
   Box r = grown(c, 1);
   const int tm = transmissive_mask(c) | reflective_mask(c);   // no predictor beyond walls either (R22)
@@ -449,7 +451,7 @@ void run_predictor(ader_ctx* c, double dt) {
   double dtdx[3] = {0, 0, 0};
   for (int k = 0; k < c->d; ++k) dtdx[k] = dt / c->dx[k];
   Scope s(c, ADER_K_PRED, 0.0);   // flops from the sweep counter (ader_kernel_stats)
-  launch_predictor(c->k, c->w, c->q, r, dtdx, c->cfg.pred_tol, c->cfg.pred_max_sweeps, c->cnt);
+  launch_predictor(c->k, c->w, c->q, r, dtdx, c->cfg.pred_tol, c->cfg.pred_max_sweeps, c->cnt, dtdx_dev);
 }
 
 void face_boxes(const ader_ctx* c, Box fb[3]) {
@@ -473,12 +475,12 @@ void run_flux(ader_ctx* c) {
   launch_face_flux_cells(c->k, c->q, c->F, ext, H, c->n, transmissive_mask(c), reflective_mask(c), c->cnt);
 }
 
-void run_update(ader_ctx* c, double dt) {
+void run_update(ader_ctx* c, double dt, const double* dtdx_dev = nullptr) {
   const Box r = owned(c);
   double dtdx[3] = {0, 0, 0};
   for (int k = 0; k < c->d; ++k) dtdx[k] = dt / c->dx[k];
   Scope s(c, ADER_K_UPDATE, (double)r.count() * c->nv * 3.0 * c->d);
-  launch_update(c->k, c->u, c->F, r, dtdx, c->inv_dx, c->cnt);
+  launch_update(c->k, c->u, c->F, r, dtdx, c->inv_dx, c->cnt, dtdx_dev);
 }
 
 ader_status check_errors(ader_ctx* c) {
@@ -486,6 +488,8 @@ ader_status check_errors(ader_ctx* c) {
   const long long cell = (long long)c->hcnt->err_cell;
   const long long x = cell % c->P[0], y = (cell / c->P[0]) % c->P[1], z = cell / ((long long)c->P[0] * c->P[1]);
   const int zH = c->d == 3 ? c->H : 0;
+  if (c->hcnt->err_code == 3)
+    return fail(c, ADER_ERR_SOLVER, "invalid time step (CFL speed not positive and finite) at t=%.17g", c->t);
   const char* what = c->hcnt->err_code == 1 ? "inadmissible state (rho<=0 or p<=0)" : "predictor reached pred_max_sweeps";
   const char* stage[] = {"?", "predictor", "face flux", "update", "cfl"};
   return fail(c, ADER_ERR_SOLVER, "%s in %s at cell (%lld,%lld,%lld), level 0, t=%.17g", what,
@@ -521,6 +525,8 @@ void free_ctx(ader_ctx* c) {
   double* bufs[] = {c->u, c->wx, c->wxy, c->w, c->q, c->F, c->stage};
   for (double* b : bufs)
     if (b) cudaFree(b);
+  if (c->st) cudaFree(c->st);
+  if (c->hst) cudaFreeHost(c->hst);
   for (int i = 0; i < 6; ++i) {
     if (c->sendb[i]) cudaFree(c->sendb[i]);
     if (c->recvb[i]) cudaFree(c->recvb[i]);
@@ -742,6 +748,10 @@ static ader_status create_impl(const ader_config* cfg, ader_ctx** out, bool loop
   CK(cudaMemset(c->cnt, 0, sizeof(DevCounters)));
   CK(cudaMallocHost(&c->hcnt, sizeof(DevCounters)));
   std::memset(c->hcnt, 0, sizeof(DevCounters));
+  CK(cudaMalloc(&c->st, sizeof(StepState)));
+  CK(cudaMemset(c->st, 0, sizeof(StepState)));
+  CK(cudaMallocHost(&c->hst, sizeof(StepState)));
+  std::memset(c->hst, 0, sizeof(StepState));
   // halo buffers (largest slab over axes)
   long long cap = 0;
   for (int a = 0; a < c->d; ++a) {
@@ -833,6 +843,10 @@ ader_status ader_set_initial(ader_ctx* c, ader_ic_fn ic, void* user) {
   }
   cudaFree(dprim);
   cudaFree(dwq);
+  {
+    StepState s0{};   // time restarts at 0
+    CK(cudaMemcpy(c->st, &s0, sizeof(StepState), cudaMemcpyHostToDevice));
+  }
   c->t = 0.0;
   c->speed_valid = false;
   return ADER_OK;
@@ -894,14 +908,49 @@ ader_status ader_get_cells(const ader_ctx* cc, ader_cell* out, int64_t capacity,
 namespace {
 // second half of a uniform macro step, after the ghost fill + WENO: predictor,
 // face fluxes, update (fused with the next CFL speed)
-void advance_dt(ader_ctx* c, double dt) {
-  run_predictor(c, dt);
+void advance_dt(ader_ctx* c, double dt, const double* dtdx_dev = nullptr) {
+  run_predictor(c, dt, dtdx_dev);
   run_flux(c);
   cudaMemsetAsync(&c->cnt->speed_bits, 0, sizeof(unsigned long long), c->k.stream);
-  run_update(c, dt);
+  run_update(c, dt, dtdx_dev);
   c->speed_valid = true;   // computed by the update of the new state
   c->t += dt;
 }
+
+// One macro step enqueued without a host round trip: ghost layers, WENO, the
+// CFL speed (from the previous update, or a CFL kernel), NCCL max over ranks,
+// dt on the device (k_step_dt), predictor, fluxes, update.
+ader_status enqueue_step(ader_ctx* c, double t_end) {
+  ader_status st = fill_halo(c, c->u);
+  if (st != ADER_OK) return st;
+  run_weno(c);
+  {
+    Scope sc(c, ADER_K_OTHER, 0.0);
+    if (!c->speed_valid) {
+      CK(cudaMemsetAsync(&c->cnt->speed_bits, 0, sizeof(unsigned long long), c->k.stream));
+      launch_cfl_speed(c->k, c->u, owned(c), c->inv_dx, c->cnt);
+    }
+    if (c->comm)
+      NK(g_nccl.AllReduce(&c->cnt->speed_bits, &c->cnt->speed_bits, 1, ncclUint64, ncclMax, c->comm, c->k.stream));
+    launch_step_dt(c->k, c->cnt, c->st, c->cfg.cfl, t_end, c->dx);
+  }
+  run_predictor(c, 0.0, c->st->dtdx);
+  run_flux(c);
+  CK(cudaMemsetAsync(&c->cnt->speed_bits, 0, sizeof(unsigned long long), c->k.stream));
+  run_update(c, 0.0, c->st->dtdx);
+  c->speed_valid = true;
+  return ADER_OK;
+}
+
+// host mirror of the step control (synchronises the stream)
+ader_status read_state(ader_ctx* c) {
+  CK(cudaMemcpyAsync(c->hst, c->st, sizeof(StepState), cudaMemcpyDeviceToHost, c->k.stream));
+  CK(cudaMemcpyAsync(c->hcnt, c->cnt, sizeof(DevCounters), cudaMemcpyDeviceToHost, c->k.stream));
+  CK(cudaStreamSynchronize(c->k.stream));
+  c->t = c->hst->t;
+  return ADER_OK;
+}
+
 
 ader_status step_begin(ader_ctx* c, unsigned long long* sw0, unsigned long long* pc0) {
   CK(cudaMemcpyAsync(c->hcnt, c->cnt, sizeof(DevCounters), cudaMemcpyDeviceToHost, c->k.stream));
@@ -966,19 +1015,25 @@ ader_status ader_step(ader_ctx* c, double t_end, int64_t max_macro_steps, ader_s
   unsigned long long sw0 = 0, pc0 = 0;
   ader_status st = step_begin(c, &sw0, &pc0);
   if (st != ADER_OK) return st;
-  while (r.macro_steps < max_macro_steps && c->t < t_end) {
-    st = fill_halo(c, c->u);
+  st = read_state(c);
+  if (st != ADER_OK) return st;
+  const long long steps0 = c->hst->steps;
+  // enqueue the steps in chunks; dt lives on the device, the host only checks
+  // time / errors between chunks (steps past t_end are no-ops, dt = 0)
+  const int64_t chunk = 16;
+  int64_t enq = 0;
+  while (enq < max_macro_steps && c->t < t_end) {
+    const int64_t nstep = std::min<int64_t>(chunk, max_macro_steps - enq);
+    for (int64_t i = 0; i < nstep && st == ADER_OK; ++i) st = enqueue_step(c, t_end);
     if (st != ADER_OK) break;
-    run_weno(c);
-    double speed = 0.0, dt = 0.0;
-    st = global_speed(c, &speed);   // overlaps the WENO sweeps
+    enq += nstep;
+    st = read_state(c);
     if (st != ADER_OK) break;
-    st = dt_from_speed(c, speed, t_end, &dt);
-    if (st != ADER_OK) break;
-    advance_dt(c, dt);
-    r.dt0 = dt;
-    r.macro_steps++;
+    if (c->hcnt->err_code) break;
   }
+  if (st == ADER_OK) st = read_state(c);
+  r.macro_steps = c->hst->steps - steps0;
+  r.dt0 = c->hst->last_dt;
   st = step_finish(c, st, &r, sw0, pc0);
   r.wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - w0).count();
   if (rep) *rep = r;

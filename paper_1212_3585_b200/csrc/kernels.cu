@@ -103,7 +103,8 @@ __global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? 4 : 2) k_predictor(
     const double* __restrict__ w, double* __restrict__ q, const Box R, const long long sy, const long long sz,
     const double dtdx0, const double dtdx1, const double dtdx2, const double gamma, const double ch,
     const double tol, const int max_sweeps, DevCounters* __restrict__ cnt, const int* __restrict__ list,
-    const long long nlist, const unsigned char* __restrict__ emask, const __grid_constant__ DevTables T) {
+    const long long nlist, const unsigned char* __restrict__ emask, const double* __restrict__ dtdx_dev,
+    const __grid_constant__ DevTables T) {
   using PH = Phys<SYS, D>;
   constexpr int NV = PH::NV, N = M + 1, NS = ipow_c(N, D), NST = NS * N;
   constexpr int G = (NS <= 8) ? 8 : (NS <= 16 ? 16 : 32);   // lanes per cell
@@ -135,7 +136,8 @@ __global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? 4 : 2) k_predictor(
   line[0] = ia[1] + N * ia[2];
   line[1] = ia[0] + N * ia[2];
   line[2] = ia[0] + N * ia[1];
-  const double dtdx[3] = {dtdx0, dtdx1, dtdx2};
+  const double dtdx[3] = {dtdx_dev ? dtdx_dev[0] : dtdx0, dtdx_dev ? dtdx_dev[1] : dtdx1,
+                          dtdx_dev ? dtdx_dev[2] : dtdx2};
   double Drow[D][N];                                          // D[ia_d][j] (lane-dependent rows)
 #pragma unroll
   for (int d = 0; d < D; ++d)
@@ -484,14 +486,16 @@ __global__ void __launch_bounds__(256) k_update(double* __restrict__ u, const do
                                                 const long long sy, const long long sz, const long long ncell,
                                                 const double dtdx0, const double dtdx1, const double dtdx2,
                                                 const double idx0, const double idx1, const double idx2,
-                                                const double gamma, const double ch, DevCounters* __restrict__ cnt) {
+                                                const double gamma, const double ch, DevCounters* __restrict__ cnt,
+                                                const double* __restrict__ dtdx_dev) {
   using PH = Phys<SYS, D>;
   constexpr int NV = PH::NV;
   const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   double s = 0.0;
   if (r < R.count()) {
     const long long c = box_cell(R, r, sy, sz);
-    const double dtdx[3] = {dtdx0, dtdx1, dtdx2};
+    const double dtdx[3] = {dtdx_dev ? dtdx_dev[0] : dtdx0, dtdx_dev ? dtdx_dev[1] : dtdx1,
+                            dtdx_dev ? dtdx_dev[2] : dtdx2};
     const long long st[3] = {1, sy, sz};
     double uu[NV];
 #pragma unroll
@@ -534,6 +538,33 @@ __global__ void __launch_bounds__(256) k_cfl_speed(const double* __restrict__ u,
 // ===========================================================================
 // helpers
 // ===========================================================================
+// dt of the next step from the reduced CFL speed (reading R1), on the device
+__global__ void k_step_dt(DevCounters* __restrict__ cnt, StepState* __restrict__ st, const double cfl,
+                          const double t_end, const double dx0, const double dx1, const double dx2, const int d) {
+  const unsigned long long b = cnt->speed_bits;
+  const double speed = __longlong_as_double((long long)b);
+  double dt = cfl / speed;
+  if (!(dt > 0.0) || !isfinite(dt)) {
+    if (atomicCAS(&cnt->err_code, 0, 3) == 0) { cnt->err_stage = 4; cnt->err_cell = 0; }
+    dt = 0.0;
+  }
+  const double t = st->t;
+  if (!(t < t_end)) dt = 0.0;             // past t_end: the step is a no-op
+  else if (t + dt > t_end) dt = t_end - t;
+  const double dx[3] = {dx0, dx1, dx2};
+  st->dt = dt;
+  for (int k = 0; k < 3; ++k) st->dtdx[k] = k < d ? dt / dx[k] : 0.0;
+  st->t = t + dt;
+  if (dt > 0.0) { st->steps += 1; st->last_dt = dt; }
+}
+
+__global__ void k_set_dt(StepState* __restrict__ st, const double dt, const double dx0, const double dx1,
+                         const double dx2, const int d) {
+  const double dx[3] = {dx0, dx1, dx2};
+  st->dt = dt;
+  for (int k = 0; k < 3; ++k) st->dtdx[k] = k < d ? dt / dx[k] : 0.0;
+}
+
 __global__ void k_fill_axis(double* __restrict__ u, const Box R, const long long sy, const long long sz, const int nv,
                             const int axis, const int mode, const int H, const int n) {
   const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -679,13 +710,13 @@ void launch_weno_sweep(const KCtx& k, int sweep, const double* src, double* dst,
 }
 
 void launch_predictor(const KCtx& k, const double* w, double* q, const Box& region, const double dtdx[3],
-                      double tol, int max_sweeps, DevCounters* cnt) {
-  launch_predictor_list(k, w, q, region, nullptr, 0, dtdx, tol, max_sweeps, cnt);
+                      double tol, int max_sweeps, DevCounters* cnt, const double* dtdx_dev) {
+  launch_predictor_list(k, w, q, region, nullptr, 0, dtdx, tol, max_sweeps, cnt, nullptr, dtdx_dev);
 }
 
 void launch_predictor_list(const KCtx& k, const double* w, double* q, const Box& region, const int* list,
                            long long nlist, const double dtdx[3], double tol, int max_sweeps, DevCounters* cnt,
-                           const unsigned char* emask) {
+                           const unsigned char* emask, const double* dtdx_dev) {
   const long long count = list ? nlist : region.count();
   if (count == 0) return;
   ADER_DISPATCH(k.D, k.M, k.SYS, {
@@ -704,7 +735,7 @@ void launch_predictor_list(const KCtx& k, const double* w, double* q, const Box&
     const unsigned g = need < 148u * 16u ? need : 148u * 16u;
     count_launch(k);
     kern<<<g, kPredWarps * 32, sm, k.stream>>>(w, q, region, k.sy, k.sz, dtdx[0], dtdx[1], dtdx[2], k.gamma,
-                                                k.ch, tol, max_sweeps, cnt, list, nlist, emask, k.tab);
+                                                k.ch, tol, max_sweeps, cnt, list, nlist, emask, dtdx_dev, k.tab);
   });
 }
 
@@ -738,13 +769,13 @@ void launch_face_flux_cells(const KCtx& k, const double* q, double* F, const Box
 }
 
 void launch_update(const KCtx& k, double* u, const double* F, const Box& R, const double dtdx[3],
-                   const double inv_dx[3], DevCounters* cnt) {
+                   const double inv_dx[3], DevCounters* cnt, const double* dtdx_dev) {
   if (R.count() == 0) return;
   const unsigned g = grid_for(R.count(), 256);
   count_launch(k);
 #define UPD(D_, S_)                                                                                   \
   k_update<D_, S_><<<g, 256, 0, k.stream>>>(u, F, R, k.sy, k.sz, k.ncell, dtdx[0], dtdx[1], dtdx[2], \
-                                             inv_dx[0], inv_dx[1], inv_dx[2], k.gamma, k.ch, cnt)
+                                             inv_dx[0], inv_dx[1], inv_dx[2], k.gamma, k.ch, cnt, dtdx_dev)
   if (k.D == 2 && k.SYS == 0) UPD(2, 0);
   else if (k.D == 3 && k.SYS == 0) UPD(3, 0);
   else if (k.D == 2 && k.SYS == 1) UPD(2, 1);
@@ -763,6 +794,16 @@ void launch_cfl_speed(const KCtx& k, const double* u, const Box& R, const double
   else if (k.D == 2 && k.SYS == 1) SPD(2, 1);
   else if (k.D == 3 && k.SYS == 1) SPD(3, 1);
 #undef SPD
+}
+
+void launch_step_dt(const KCtx& k, DevCounters* cnt, StepState* st, double cfl, double t_end, const double dx[3]) {
+  count_launch(k);
+  k_step_dt<<<1, 1, 0, k.stream>>>(cnt, st, cfl, t_end, dx[0], dx[1], dx[2], k.D);
+}
+
+void launch_set_dt(const KCtx& k, StepState* st, double dt, const double dx[3]) {
+  count_launch(k);
+  k_set_dt<<<1, 1, 0, k.stream>>>(st, dt, dx[0], dx[1], dx[2], k.D);
 }
 
 void launch_fill_axis(const KCtx& k, double* u, const Box& region, int axis, int mode, int H, int n) {

@@ -31,6 +31,15 @@ struct DevCounters {              // device-resident, zeroed by the host
   int pad;
 };
 
+// Device-resident step control of the uniform path: the time step is formed
+// on the GPU from the reduced CFL speed, so K macro steps are enqueued without
+// a host round trip per step (the host only reads this back every few steps).
+struct StepState {
+  double t, dt, last_dt;          // time reached, dt of the last step, last positive dt
+  double dtdx[3];                 // dt / dx_dir of the last step (read by predictor / update)
+  long long steps;                // steps with dt > 0
+};
+
 // Instrumentation hook (CUDA events around launches, set by ader_api.cpp).
 struct ProfHook {
   void* ctx = nullptr;
@@ -54,14 +63,15 @@ bool supported(int D, int M, int SYS);
 
 // WENO sweep k along axis k (k = 0 x, 1 y, 2 z) on the cells of `region`.
 void launch_weno_sweep(const KCtx& k, int sweep, const double* src, double* dst, const Box& region);
-// Predictor on `region`: w -> q.
+// Predictor on `region`: w -> q.  dtdx_dev (optional): read dt/dx from the
+// device (StepState::dtdx) instead of dtdx.
 void launch_predictor(const KCtx& k, const double* w, double* q, const Box& region, const double dtdx[3],
-                      double tol, int max_sweeps, DevCounters* cnt);
+                      double tol, int max_sweeps, DevCounters* cnt, const double* dtdx_dev = nullptr);
 // Predictor on the cells of an id list (AMR levels): w, q indexed by id.  If
 // emask is given only cells with emask[id] != 0 report solver errors.
 void launch_predictor_list(const KCtx& k, const double* w, double* q, const Box& region, const int* list,
                            long long nlist, const double dtdx[3], double tol, int max_sweeps, DevCounters* cnt,
-                           const unsigned char* emask = nullptr);
+                           const unsigned char* emask = nullptr, const double* dtdx_dev = nullptr);
 // Face fluxes on the lower face of every cell of `ext` (owned block + 1 on each
 // active axis), one lane group per cell computing all its lower faces
 // (L2-friendly traversal).  bmask bit 2*dir (2*dir+1): the first (last) face
@@ -72,7 +82,13 @@ void launch_face_flux_cells(const KCtx& k, const double* q, double* F, const Box
                             int bmask, int rmask, DevCounters* cnt);
 // FV update of `interior` in place + max CFL speed of the new state.
 void launch_update(const KCtx& k, double* u, const double* F, const Box& interior, const double dtdx[3],
-                   const double inv_dx[3], DevCounters* cnt);
+                   const double inv_dx[3], DevCounters* cnt, const double* dtdx_dev = nullptr);
+// dt of the next step on the device (reading R1): dt = cfl / speed (speed from
+// cnt->speed_bits, max over ranks), clipped to t_end, 0 once t >= t_end;
+// updates st (t, dt, dtdx = dt / dx, steps).  Invalid dt -> err_code 3.
+void launch_step_dt(const KCtx& k, DevCounters* cnt, StepState* st, double cfl, double t_end, const double dx[3]);
+// set st to a host-chosen dt (loopback groups, debug dumps)
+void launch_set_dt(const KCtx& k, StepState* st, double dt, const double dx[3]);
 void launch_cfl_speed(const KCtx& k, const double* u, const Box& interior, const double inv_dx[3],
                       DevCounters* cnt);
 // Ghost copy along one axis: for every cell of `region` (halo cells), copy the
