@@ -48,7 +48,7 @@ def parse():
     p.add_argument("--config", default="c4")
     p.add_argument("--n", type=int, default=0)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--e2e-steps", type=int, default=3)
+    p.add_argument("--e2e-steps", type=int, default=5)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-box", type=int, default=12, help="edge of the oracle sample box (cells)")
     p.add_argument("--flux", default="rusanov", choices=["rusanov", "osher"],

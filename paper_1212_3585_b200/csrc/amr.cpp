@@ -9,7 +9,10 @@
 #include "amr.h"
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -76,6 +79,9 @@ struct AmrState {
   double* xsend = nullptr;
   double* xrecv = nullptr;
   size_t xcap = 0;                                    // doubles
+  // host-side phase timers (seconds), printed at destroy if ADER_AMR_TIMING is set
+  double tm_speed = 0, tm_advance = 0, tm_check = 0, tm_ind = 0, tm_apply = 0, tm_exch = 0;
+  long long tm_steps = 0;
 };
 
 namespace {
@@ -804,14 +810,19 @@ ader_status adapt_apply(AmrState* A, bool t0, const std::vector<double>& chi, st
 }
 
 // One adapt pass of every rank of the group on the global indicator.
+double now_s() { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); }
+
 ader_status adapt(const Group& G, bool t0, std::string& err) {
   std::vector<double> chi, mine;
+  double w0 = now_s();
   for (AmrState* A : G) {
     ader_status s = adapt_indicator(A, t0, mine, err);
     if (s != ADER_OK) return s;
     if (chi.size() < mine.size()) chi.resize(mine.size(), 0.0);
     for (size_t i = 0; i < mine.size(); ++i) chi[i] += mine[i];   // one owner per cell: exact
   }
+  G[0]->tm_ind += now_s() - w0;
+  w0 = now_s();
   AmrState* A0 = G[0];
   if (G.size() == 1 && A0->ranks.world > 1 && !chi.empty()) {
     cudaStream_t sm = A0->k->stream;
@@ -825,12 +836,15 @@ ader_status adapt(const Group& G, bool t0, std::string& err) {
     ader_status s = adapt_apply(A, t0, chi, err);
     if (s != ADER_OK) return s;
   }
+  A0->tm_apply += now_s() - w0;
+  w0 = now_s();
   // the band copies of new / re-initialised active cells come from their owners
   for (int l = 0; l <= A0->lmax; ++l) {
     ader_status s = exchange(G, l, err);
     if (s != ADER_OK) return s;
   }
   for (AmrState* A : G) ACK(cudaStreamSynchronize(A->k->stream));
+  A0->tm_exch += now_s() - w0;
   return ADER_OK;
 }
 
@@ -892,6 +906,14 @@ AmrState* amr_create(const ader_config* cfg, KCtx* k, DevCounters* cnt, DevCount
 
 void amr_destroy(AmrState* A) {
   if (!A) return;
+  if (std::getenv("ADER_AMR_TIMING") && A->tm_steps)
+    std::fprintf(stderr,
+                 "amr host phases over %lld macro steps (ms/step): speed+sync %.3f, advance enqueue %.3f, "
+                 "check/sync %.3f, adapt: indicator+sync %.3f, apply (host tree, uploads, inits) %.3f, "
+                 "exchange+sync %.3f; cells %zu\n",
+                 A->tm_steps, 1e3 * A->tm_speed / A->tm_steps, 1e3 * A->tm_advance / A->tm_steps,
+                 1e3 * A->tm_check / A->tm_steps, 1e3 * A->tm_ind / A->tm_steps, 1e3 * A->tm_apply / A->tm_steps,
+                 1e3 * A->tm_exch / A->tm_steps, A->cells.size());
   cudaStreamSynchronize(A->k->stream);
   void* ps[] = {A->V.u, A->V.mem, A->V.w, A->V.q, A->V.chi, A->V.level, A->V.status, A->V.mother, A->V.child, A->V.idx,
                 A->V.own, A->dlist, A->xsend, A->xrecv};
@@ -943,14 +965,21 @@ ader_status step(const Group& G, double t_end, int64_t max_steps, ader_step_repo
   int64_t steps = 0;
   while (steps < max_steps && A0->t < t_end) {
     double speed = 0.0;
+    double w0 = now_s();
     s = fetch_speed(G, &speed, err);
     for (size_t i = 0; i < n && s == ADER_OK; ++i) s = check_err(G[i], err);
+    A0->tm_speed += now_s() - w0;
     if (s != ADER_OK) break;
     double dt = A0->cfg.cfl / speed;
     if (!(dt > 0.0) || !std::isfinite(dt)) { err = "invalid dt"; s = ADER_ERR_SOLVER; break; }
     if (A0->t + dt > t_end) dt = t_end - A0->t;
+    w0 = now_s();
     s = advance(G, 0, 0, dt, err);
+    A0->tm_advance += now_s() - w0;
+    w0 = now_s();
     for (size_t i = 0; i < n && s == ADER_OK; ++i) s = check_err(G[i], err);
+    A0->tm_check += now_s() - w0;
+    A0->tm_steps++;
     if (s != ADER_OK) break;
     for (size_t i = 0; i < n; ++i) { G[i]->t += dt; R[i].dt0 = dt; R[i].macro_steps++; }
     ++steps;

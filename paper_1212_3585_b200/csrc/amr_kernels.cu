@@ -3,7 +3,7 @@
 //   k_amr_project   projection of the mother's q_h into virtual children
 //   k_amr_weno      dimension-by-dimension WENO of a listed active cell
 //   k_predictor     (kernels.cu, list mode) space-time predictor
-//   k_amr_flux_update  face fluxes incl. coarse-fine faces with flux memory
+//   k_amr_flux_update_w face fluxes incl. coarse-fine faces with flux memory
 //                   (eqn.memory.sum) + one-step update (eq:finite_vol)
 //   k_amr_indicator refinement indicator, reading R14 of eqn.indicator,
 //                   evaluated without FMA contraction (bit-exact flags, H2)
@@ -252,130 +252,16 @@ __device__ __forceinline__ bool numflux_pt(const double (&um)[Phys<SYS, D>::NV],
   return ok;
 }
 
-// kind: 0 same level (qL, qR full faces), 1 left boundary (qR only), 2 right
-// boundary (qL only), 3 coarse left (qL = K), 4 coarse right (qR = K),
-// 5 left wall (qR only, q^- = reflected q^+), 6 right wall (qL only)
-template <int D, int M, int SYS, int DIR>
-__device__ bool face_flux_amr(int kind, const double* qL, const double* qR, int o1, int o2, int m, double gamma,
-                              double ch, const DevTables& T, const SubTables& S, double (&F)[Phys<SYS, D>::NV]) {
-  constexpr int NV = Phys<SYS, D>::NV, N = M + 1;
-  constexpr int NT = (D == 3) ? N * N : N;
-  bool ok = true;
-#pragma unroll
-  for (int v = 0; v < NV; ++v) F[v] = 0.0;
-  for (int s = 0; s < N; ++s)
-    for (int t = 0; t < NT; ++t) {
-      const int t1 = t % N, t2 = t / N;
-      double um[NV], up[NV], ft[NV];
-      if (kind == 0 || kind == 2 || kind == 4 || kind == 6) trace_full<D, M, NV, DIR>(qL, true, t1, t2, s, T, um);
-      if (kind == 0 || kind == 1 || kind == 3 || kind == 5) trace_full<D, M, NV, DIR>(qR, false, t1, t2, s, T, up);
-      if (kind == 5) { for (int v = 0; v < NV; ++v) um[v] = up[v]; um[1 + DIR] = -up[1 + DIR]; }   // R22
-      if (kind == 6) { for (int v = 0; v < NV; ++v) up[v] = um[v]; up[1 + DIR] = -um[1 + DIR]; }
-      if (kind == 3) trace_coarse<D, M, NV, DIR>(qL, true, o1, o2, m, t1, t2, s, T, S, um);
-      if (kind == 4) trace_coarse<D, M, NV, DIR>(qR, false, o1, o2, m, t1, t2, s, T, S, up);
-      if (kind == 1) for (int v = 0; v < NV; ++v) um[v] = up[v];
-      if (kind == 2) for (int v = 0; v < NV; ++v) up[v] = um[v];
-      ok &= numflux_pt<SYS, D, DIR>(um, up, gamma, ch, T, ft);
-      double wgt = T.w[s] * T.w[t1];
-      if (D == 3) wgt *= T.w[t2];
-#pragma unroll
-      for (int v = 0; v < NV; ++v) F[v] += wgt * ft[v];
-    }
-  return ok;
-}
-
-template <int D, int M, int SYS, int DIR>
-__device__ bool cell_face(const AmrDevView& V, int c, int side, int m, double gamma, double ch, const DevTables& T,
-                          const SubTables& S, double (&F)[Phys<SYS, D>::NV]) {
-  constexpr int NV = Phys<SYS, D>::NV, N = M + 1, NS = ipow_a(N, D), NST = NS * N;
-  const int l = V.level[c];
-  long long ix[3] = {V.idx[(long long)c * 3], V.idx[(long long)c * 3 + 1], V.idx[(long long)c * 3 + 2]};
-  ix[DIR] += side ? 1 : -1;
-  const double* qc = V.q + (long long)c * NV * NST;
-  const bool out = ix[DIR] < 0 || ix[DIR] >= V.n[l][DIR];
-  if (out && V.bc[2 * DIR + side] == ADER_BC_TRANSMISSIVE)
-    return face_flux_amr<D, M, SYS, DIR>(side ? 2 : 1, qc, qc, 0, 0, 0, gamma, ch, T, S, F);
-  if (out && V.bc[2 * DIR + side] == ADER_BC_REFLECTIVE)
-    return face_flux_amr<D, M, SYS, DIR>(side ? 6 : 5, qc, qc, 0, 0, 0, gamma, ch, T, S, F);
-  const int nb = amr_lookup(V, l, ix[0], ix[1], ix[2]);
-  if (nb < 0) return false;
-  const int st = V.status[nb];
-  if (st == 0) {
-    const double* qn = V.q + (long long)nb * NV * NST;
-    return side ? face_flux_amr<D, M, SYS, DIR>(0, qc, qn, 0, 0, 0, gamma, ch, T, S, F)
-                : face_flux_amr<D, M, SYS, DIR>(0, qn, qc, 0, 0, 0, gamma, ch, T, S, F);
-  }
-  if (st == 1) {
-    // coarse-fine: the virtual neighbour scales its mother's q_h down
-    const int K = V.mother[nb];
-    const double* qK = V.q + (long long)K * NV * NST;
-    constexpr int ax0 = (DIR == 0) ? 1 : 0, ax1 = (DIR == 2) ? 1 : 2;
-    const int o1 = (int)(V.idx[(long long)c * 3 + ax0] % V.r);
-    const int o2 = (D == 3) ? (int)(V.idx[(long long)c * 3 + ax1] % V.r) : 0;
-    bool ok = side ? face_flux_amr<D, M, SYS, DIR>(4, qc, qK, o1, o2, m, gamma, ch, T, S, F)
-                   : face_flux_amr<D, M, SYS, DIR>(3, qK, qc, o1, o2, m, gamma, ch, T, S, F);
-    double* mm = V.mem + ((long long)nb * 6 + 2 * DIR + (side ? 0 : 1)) * NV;   // nb's face toward c
-#pragma unroll
-    for (int v = 0; v < NV; ++v) mm[v] += F[v];
-    return ok;
-  }
-  // virtual mother: sum the memory of our own virtual children on this face (eqn.memory.sum)
-  const int ch0 = V.child[c];
-  if (ch0 < 0) return false;
-#pragma unroll
-  for (int v = 0; v < NV; ++v) F[v] = 0.0;
-  for (int qd = 0; qd < V.rd; ++qd) {
-    const int off[3] = {qd % V.r, (qd / V.r) % V.r, qd / (V.r * V.r)};
-    if (off[DIR] != (side ? V.r - 1 : 0)) continue;
-    double* mm = V.mem + ((long long)(ch0 + qd) * 6 + 2 * DIR + side) * NV;
-#pragma unroll
-    for (int v = 0; v < NV; ++v) { F[v] += mm[v]; mm[v] = 0.0; }
-  }
-#pragma unroll
-  for (int v = 0; v < NV; ++v) F[v] = F[v] / (double)V.rd;
-  return true;
-}
-
-template <int D, int M, int SYS>
-__global__ void __launch_bounds__(64) k_amr_flux_update(AmrDevView V, const __grid_constant__ SubTables S,
-                                                        const int* __restrict__ list, int n, int m, double dtdx0,
-                                                        double dtdx1, double dtdx2, double gamma, double ch,
-                                                        DevCounters* cnt, const __grid_constant__ DevTables T) {
-  constexpr int NV = Phys<SYS, D>::NV;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int c = list[i];
-  const double dtdx[3] = {dtdx0, dtdx1, dtdx2};
-  double uu[NV];
-#pragma unroll
-  for (int v = 0; v < NV; ++v) uu[v] = V.u[(long long)c * NV + v];
-  bool ok = true;
-  double Fm[NV], Fp[NV];
-  ok &= cell_face<D, M, SYS, 0>(V, c, 0, m, gamma, ch, T, S, Fm);
-  ok &= cell_face<D, M, SYS, 0>(V, c, 1, m, gamma, ch, T, S, Fp);
-#pragma unroll
-  for (int v = 0; v < NV; ++v) uu[v] = uu[v] - dtdx[0] * (Fp[v] - Fm[v]);
-  ok &= cell_face<D, M, SYS, 1>(V, c, 0, m, gamma, ch, T, S, Fm);
-  ok &= cell_face<D, M, SYS, 1>(V, c, 1, m, gamma, ch, T, S, Fp);
-#pragma unroll
-  for (int v = 0; v < NV; ++v) uu[v] = uu[v] - dtdx[1] * (Fp[v] - Fm[v]);
-  if (D == 3) {
-    ok &= cell_face<D, M, SYS, 2>(V, c, 0, m, gamma, ch, T, S, Fm);
-    ok &= cell_face<D, M, SYS, 2>(V, c, 1, m, gamma, ch, T, S, Fp);
-#pragma unroll
-    for (int v = 0; v < NV; ++v) uu[v] = uu[v] - dtdx[2] * (Fp[v] - Fm[v]);
-  }
-  if (!ok && (!V.own || V.own[c])) amr_error(cnt, 1, 2, c);   // multi-rank: band cells' errors do not count
-#pragma unroll
-  for (int v = 0; v < NV; ++v) V.u[(long long)c * NV + v] = uu[v];
-}
-
 // ---------------------------------------------------------------------------
-// Lane-parallel variant: a lane group of G >= N^D lanes per cell, a lane per
+// a3 + a4 on the tree: face fluxes (same level, coarse-fine with flux memory,
+// against virtual mothers, boundaries, walls) and the update of the active
+// cells of one level.  A lane group of G >= N^D lanes per cell, a lane per
 // space-time point of the face being processed (as in k_face_flux_cells), the
-// point sums through shared memory in point order.  Face kinds, coarse-fine
-// traces, flux memory deposit / consumption and the update are those of
-// cell_face / k_amr_flux_update above (which remain the reference form).
+// point sums through shared memory in point order.
+// face kinds: 0 same level (qL, qR full faces), 1 left boundary (qR only),
+// 2 right boundary (qL only), 3 coarse left (qL = mother K), 4 coarse right
+// (qR = K), 5 left wall (q^- = reflected q^+), 6 right wall, 7 memory of the
+// cell's own virtual children (eqn.memory.sum @ P:693-709)
 template <int D, int M, int SYS, int DIR>
 __device__ __forceinline__ bool amr_face_point(int kind, const double* qL, const double* qR, int o1, int o2, int m,
                                                int s, int t1, int t2, double gamma, double ch, const DevTables& T,
@@ -403,9 +289,8 @@ __device__ __forceinline__ bool amr_cell_face_w(const AmrDevView& V, int c, bool
   ix[DIR] += side ? 1 : -1;
   const double* qc = V.q + (long long)c * NV * NST;
   const bool out = ix[DIR] < 0 || ix[DIR] >= V.n[l][DIR];
-  // kind: 0..6 as in face_flux_amr, 7 memory of own virtual children, -1 error.
-  // Every lane group of the warp runs the same two __syncwarp()s whatever its
-  // kind (2D: several cells per warp).
+  // kind as listed above, -1 error.  Every lane group of the warp runs the
+  // same two __syncwarp()s whatever its kind (2D: several cells per warp).
   int kind = -1, nb = -1, o1 = 0, o2 = 0;
   const double *qL = qc, *qR = qc;
   if (out && V.bc[2 * DIR + side] == ADER_BC_TRANSMISSIVE) kind = side ? 2 : 1;
