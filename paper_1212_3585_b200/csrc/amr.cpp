@@ -81,6 +81,8 @@ struct AmrState {
   size_t xcap = 0;                                    // doubles
   // host-side phase timers (seconds), printed at destroy if ADER_AMR_TIMING is set
   double tm_speed = 0, tm_advance = 0, tm_check = 0, tm_ind = 0, tm_apply = 0, tm_exch = 0;
+  double tm_a[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // adapt_apply sub-phases
+  double tm_u[4] = {0, 0, 0, 0};                // upload_topology: capacity, host scans, staging
   long long tm_steps = 0;
 };
 
@@ -91,6 +93,8 @@ namespace {
     cudaError_t e_ = (call);                                                             \
     if (e_ != cudaSuccess) { err = std::string(#call) + ": " + cudaGetErrorString(e_); return ADER_ERR_CUDA; } \
   } while (0)
+
+double now_s() { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); }
 
 double lagrange(const DevTables& T, int N, int p, double x) {
   double v = 1.0;
@@ -285,7 +289,10 @@ void garbage_collect(AmrState* A, std::vector<int>* freed) {
 ader_status ensure_capacity(AmrState* A, std::string& err) {
   const int need = (int)A->cells.size();
   if (need <= A->cap) return ADER_OK;
-  const int nc = std::max(need + need / 2, 1024);
+  // grow geometrically from a reserve of (1 + r^d) level-0 cells: every
+  // reallocation copies all per-id arrays and synchronises the stream
+  const long long n0 = A->n[0][0] * A->n[0][1] * A->n[0][2];
+  const int nc = (int)std::min<long long>(std::max<long long>({2LL * need, n0 * (1 + A->rd), 1024}), 2000000000LL);
   auto grow = [&](void** p, size_t elem) -> cudaError_t {
     void* np = nullptr;
     cudaError_t e = cudaMalloc(&np, (size_t)nc * elem);
@@ -356,8 +363,10 @@ struct Uploader {
 // since the last upload (plus the map entries they occupy), and the per-level
 // id lists.
 ader_status upload_topology(AmrState* A, std::string& err) {
+  double w0 = now_s();
   ader_status s = ensure_capacity(A, err);
   if (s != ADER_OK) return s;
+  A->tm_u[0] += now_s() - w0; w0 = now_s();
   const int nu = (int)A->cells.size();
   if ((int)A->mirror.size() < nu) A->mirror.resize(nu);
   std::vector<long long> meta, clears, sets;
@@ -454,6 +463,7 @@ ader_status upload_topology(AmrState* A, std::string& err) {
     ACK(cudaMalloc(&A->dlist, sizeof(int) * A->dlist_cap));
   }
   Uploader up{A, {}};
+  A->tm_u[1] += now_s() - w0; w0 = now_s();
   const size_t om = up.add(meta.data(), meta.size() * sizeof(long long));
   const size_t oc = up.add(clears.data(), clears.size() * sizeof(long long));
   const size_t os = up.add(sets.data(), sets.size() * sizeof(long long));
@@ -462,6 +472,7 @@ ader_status upload_topology(AmrState* A, std::string& err) {
   s = up.run(err);
   if (s != ADER_OK) return s;
   if (W > 1) ACK(cudaMemcpyAsync(A->V.own, A->dscratch + oo, A->own.size(), cudaMemcpyDeviceToDevice, sm));
+  A->tm_u[2] += now_s() - w0; w0 = now_s();
   amr_launch_meta_scatter(*A->k, A->V, (const long long*)(A->dscratch + om), (int)(meta.size() / 8));
   amr_launch_map_set(*A->k, A->V, (const long long*)(A->dscratch + oc), (int)(clears.size() / 3));
   amr_launch_map_set(*A->k, A->V, (const long long*)(A->dscratch + os), (int)(sets.size() / 3));
@@ -721,6 +732,7 @@ ader_status adapt_indicator(AmrState* A, bool t0, std::vector<double>& chi, std:
 ader_status adapt_apply(AmrState* A, bool t0, const std::vector<double>& chi, std::string& err) {
   cudaStream_t sm = A->k->stream;
   int nb[26];
+  double w0 = now_s();
   for (auto& c : A->cells) c.isnew = false;
   const int nu = (int)A->cells.size();
   std::vector<char> mark(nu, 0);
@@ -728,7 +740,9 @@ ader_status adapt_apply(AmrState* A, bool t0, const std::vector<double>& chi, st
     mark[i] = A->cells[i].alive && A->cells[i].status == 0 && A->cells[i].level < A->lmax && chi[i] > A->cfg.chi_ref;
   for (int i = 0; i < nu; ++i)
     if (mark[i]) refine_cell(A, i, t0);
+  A->tm_a[0] += now_s() - w0; w0 = now_s();
   closure(A, t0);
+  A->tm_a[1] += now_s() - w0; w0 = now_s();
   std::vector<int> freed;
   std::vector<int> coarsened;
   if (!t0) {
@@ -786,7 +800,9 @@ ader_status adapt_apply(AmrState* A, bool t0, const std::vector<double>& chi, st
       A->inits.resize(snap_inits);
     }
   }
+  A->tm_a[2] += now_s() - w0; w0 = now_s();
   garbage_collect(A, &freed);
+  A->tm_a[3] += now_s() - w0; w0 = now_s();
   // device: averages of coarsened mothers from their (old) children first
   if (!coarsened.empty()) {
     // children ids are still valid on the device (freed blocks are reused only later)
@@ -797,8 +813,10 @@ ader_status adapt_apply(AmrState* A, bool t0, const std::vector<double>& chi, st
     // the device child links of these mothers are the pre-adapt ones
     amr_launch_average(*A->k, A->V, (const int*)(A->dscratch + oc), (int)coarsened.size());
   }
+  A->tm_a[4] += now_s() - w0; w0 = now_s();
   ader_status s = upload_topology(A, err);
   if (s != ADER_OK) return s;
+  A->tm_a[5] += now_s() - w0; w0 = now_s();
   s = run_inits(A, err);
   if (s != ADER_OK) return s;
   // clear the flux memory of every virtual child (synchronized time: all consumed)
@@ -806,12 +824,11 @@ ader_status adapt_apply(AmrState* A, bool t0, const std::vector<double>& chi, st
   for (int b : freed) A->free_blocks.push_back(b);
   for (auto& c : A->cells) c.isnew = false;
   ACK(cudaStreamSynchronize(sm));
+  A->tm_a[6] += now_s() - w0;
   return ADER_OK;
 }
 
 // One adapt pass of every rank of the group on the global indicator.
-double now_s() { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); }
-
 ader_status adapt(const Group& G, bool t0, std::string& err) {
   std::vector<double> chi, mine;
   double w0 = now_s();
@@ -914,6 +931,15 @@ void amr_destroy(AmrState* A) {
                  A->tm_steps, 1e3 * A->tm_speed / A->tm_steps, 1e3 * A->tm_advance / A->tm_steps,
                  1e3 * A->tm_check / A->tm_steps, 1e3 * A->tm_ind / A->tm_steps, 1e3 * A->tm_apply / A->tm_steps,
                  1e3 * A->tm_exch / A->tm_steps, A->cells.size());
+  if (std::getenv("ADER_AMR_TIMING") && A->tm_steps)
+    std::fprintf(stderr, "  apply (ms/step): marks+refine %.3f, closure %.3f, recoarsening %.3f, GC %.3f, "
+                         "coarsened averages %.3f, upload topology %.3f, inits+sync %.3f\n",
+                 1e3 * A->tm_a[0] / A->tm_steps, 1e3 * A->tm_a[1] / A->tm_steps, 1e3 * A->tm_a[2] / A->tm_steps,
+                 1e3 * A->tm_a[3] / A->tm_steps, 1e3 * A->tm_a[4] / A->tm_steps, 1e3 * A->tm_a[5] / A->tm_steps,
+                 1e3 * A->tm_a[6] / A->tm_steps);
+  if (std::getenv("ADER_AMR_TIMING") && A->tm_steps)
+    std::fprintf(stderr, "  upload (ms/step): capacity %.3f, host scans/lists %.3f, staging+H2D %.3f\n",
+                 1e3 * A->tm_u[0] / A->tm_steps, 1e3 * A->tm_u[1] / A->tm_steps, 1e3 * A->tm_u[2] / A->tm_steps);
   cudaStreamSynchronize(A->k->stream);
   void* ps[] = {A->V.u, A->V.mem, A->V.w, A->V.q, A->V.chi, A->V.level, A->V.status, A->V.mother, A->V.child, A->V.idx,
                 A->V.own, A->dlist, A->xsend, A->xrecv};
