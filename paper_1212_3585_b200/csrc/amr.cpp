@@ -79,6 +79,10 @@ struct AmrState {
   double* xsend = nullptr;
   double* xrecv = nullptr;
   size_t xcap = 0;                                    // doubles
+  // undo journal of the tentative recoarsening (instead of copying the tree)
+  bool jon = false;
+  std::vector<std::pair<int, HCell>> jcells;          // (id, previous value)
+  std::vector<std::pair<std::pair<int, long long>, int>> jmap;   // ((level, linear index), previous id)
   // host-side phase timers (seconds), printed at destroy if ADER_AMR_TIMING is set
   double tm_speed = 0, tm_advance = 0, tm_check = 0, tm_ind = 0, tm_apply = 0, tm_exch = 0;
   double tm_a[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // adapt_apply sub-phases
@@ -194,6 +198,16 @@ int voronoi(const AmrState* A, int id, int* out) {
   return cnt;
 }
 
+// writable cell / map entry; records the previous value while journaling
+HCell& wcell(AmrState* A, int i) {
+  if (A->jon) A->jcells.push_back({i, A->cells[i]});
+  return A->cells[i];
+}
+void set_map(AmrState* A, int l, long long k, int v) {
+  if (A->jon) A->jmap.push_back({{l, k}, A->hmap[l][k]});
+  A->hmap[l][k] = v;
+}
+
 int alloc_block(AmrState* A) {
   if (!A->free_blocks.empty()) {
     const int id = A->free_blocks.back();
@@ -207,11 +221,10 @@ int alloc_block(AmrState* A) {
 
 int make_children(AmrState* A, int m, int status) {
   const int id = alloc_block(A);
-  HCell& Mc = A->cells[m];
-  Mc.child = id;
-  const int l = Mc.level + 1;
+  wcell(A, m).child = id;
+  const int l = A->cells[m].level + 1;
   for (int q = 0; q < A->rd; ++q) {
-    HCell& C = A->cells[id + q];
+    HCell& C = wcell(A, id + q);
     C = HCell();
     C.alive = true;
     C.level = l;
@@ -219,7 +232,7 @@ int make_children(AmrState* A, int m, int status) {
     C.mother = m;
     const int off[3] = {q % A->r, (q / A->r) % A->r, A->d == 3 ? q / (A->r * A->r) : 0};
     for (int k = 0; k < 3; ++k) C.idx[k] = k < A->d ? A->cells[m].idx[k] * A->r + off[k] : 0;
-    A->hmap[l][lin(A, l, C.idx)] = id + q;
+    set_map(A, l, lin(A, l, C.idx), id + q);
   }
   return id;
 }
@@ -228,23 +241,23 @@ void destroy_children(AmrState* A, int m, std::vector<int>* freed) {
   const int ch = A->cells[m].child;
   if (ch < 0) return;
   for (int q = 0; q < A->rd; ++q) {
-    HCell& C = A->cells[ch + q];
-    if (C.child >= 0) destroy_children(A, ch + q, freed);
-    A->hmap[C.level][lin(A, C.level, C.idx)] = -1;
-    C = HCell();
+    if (A->cells[ch + q].child >= 0) destroy_children(A, ch + q, freed);
+    const HCell& C = A->cells[ch + q];
+    set_map(A, C.level, lin(A, C.level, C.idx), -1);
+    wcell(A, ch + q) = HCell();
   }
   freed->push_back(ch);
-  A->cells[m].child = -1;
+  wcell(A, m).child = -1;
 }
 
 void refine_cell(AmrState* A, int c, bool t0) {
   if (A->cells[c].child < 0) make_children(A, c, 0);
   else
-    for (int q = 0; q < A->rd; ++q) A->cells[A->cells[c].child + q].status = 0;
-  A->cells[c].status = -1;
+    for (int q = 0; q < A->rd; ++q) wcell(A, A->cells[c].child + q).status = 0;
+  wcell(A, c).status = -1;
   const int ch = A->cells[c].child;
   for (int q = 0; q < A->rd; ++q) {
-    A->cells[ch + q].isnew = true;
+    wcell(A, ch + q).isnew = true;
     A->inits.push_back({ch + q, c, t0 ? 2 : 0});
   }
 }
@@ -764,10 +777,13 @@ ader_status adapt_apply(AmrState* A, bool t0, const std::vector<double>& chi, st
     for (int i = 0; i < nu2 && !any_cand; ++i) any_cand = cand[i];
     while (any_cand) {
       // tentative simultaneous rule 7, then closure; reverted candidates retry
-      const std::vector<HCell> snap_cells = A->cells;
-      const std::vector<std::vector<int>> snap_map = A->hmap;
+      // (the changes are journaled and undone in reverse order on a revert)
+      const size_t snap_size = A->cells.size();
       const std::vector<int> snap_free = A->free_blocks;
       const size_t snap_inits = A->inits.size();
+      A->jon = true;
+      A->jcells.clear();
+      A->jmap.clear();
       std::vector<char> destroy(nu2, 0);
       for (int i = 0; i < nu2; ++i) {
         if (!cand[i]) continue;
@@ -781,10 +797,11 @@ ader_status adapt_apply(AmrState* A, bool t0, const std::vector<double>& chi, st
         if (!cand[i]) continue;
         if (destroy[i]) destroy_children(A, i, &fr);
         else
-          for (int q = 0; q < A->rd; ++q) A->cells[A->cells[i].child + q].status = 1;
-        A->cells[i].status = 0;
+          for (int q = 0; q < A->rd; ++q) wcell(A, A->cells[i].child + q).status = 1;
+        wcell(A, i).status = 0;
       }
       closure(A, false);
+      A->jon = false;
       bool reverted = false;
       for (int i = 0; i < nu2; ++i)
         if (cand[i] && A->cells[i].status == -1) { cand[i] = 0; reverted = true; }
@@ -794,8 +811,10 @@ ader_status adapt_apply(AmrState* A, bool t0, const std::vector<double>& chi, st
           if (cand[i]) coarsened.push_back(i);
         break;
       }
-      A->cells = snap_cells;
-      A->hmap = snap_map;
+      for (size_t j = A->jmap.size(); j-- > 0;) A->hmap[A->jmap[j].first.first][A->jmap[j].first.second] = A->jmap[j].second;
+      for (size_t j = A->jcells.size(); j-- > 0;)
+        if ((size_t)A->jcells[j].first < snap_size) A->cells[A->jcells[j].first] = A->jcells[j].second;
+      A->cells.resize(snap_size);
       A->free_blocks = snap_free;
       A->inits.resize(snap_inits);
     }

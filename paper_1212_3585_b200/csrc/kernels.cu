@@ -387,7 +387,7 @@ __device__ __forceinline__ bool point_flux(const double* __restrict__ q, long lo
 
 constexpr int pow2_at_least(int x) { return x <= 1 ? 1 : 2 * pow2_at_least((x + 1) / 2); }
 
-template <int D, int M, int SYS, int WARPS, int YC, int FLUX>
+template <int D, int M, int SYS, int WARPS, int YC, int FLUX, bool PREFETCH = true>
 __global__ void __launch_bounds__(WARPS * 32, (FLUX == 1) ? 5 : (SYS == 1 ? 4 : (D == 3 ? 7 : 8))) k_face_flux_cells(const double* __restrict__ q, double* __restrict__ F,
                                                                 const Box E, const int H, const int n0, const int n1,
                                                                 const int n2, const long long sy, const long long sz,
@@ -432,6 +432,17 @@ __global__ void __launch_bounds__(WARPS * 32, (FLUX == 1) ? 5 : (SYS == 1 ? 4 : 
   // tried: 1.6x slower at 256^3 — the pencil reads stay global / L1)
   const double* qown = q + cR * BLK;
   constexpr bool STAGE = false;
+  if constexpr (PREFETCH) {
+    // the D+1 blocks this cell reads, requested into L1 by the whole lane
+    // group at once (no scoreboard wait), so the dependent pencil loads of
+    // the D faces hit L1 instead of queueing one face after the other
+    if (ok) {
+      const double* blk[4] = {qown, q + (cR - 1) * BLK, q + (cR - sy) * BLK, q + (cR - sz) * BLK};
+#pragma unroll
+      for (int b = 0; b <= D; ++b)
+        for (int j = p * 16; j < BLK; j += G * 16) asm volatile("prefetch.global.L1 [%0];" ::"l"(blk[b] + j));
+    }
+  }
   good &= point_flux_blocks<D, M, SYS, 0, FLUX, true, !STAGE>(
       q + (cR - 1) * BLK, qown, ps, fok[0], (bmask & 1) && cx == H, (bmask & 2) && cx == H + n0,
       (rmask & 1) && cx == H, (rmask & 2) && cx == H + n0, wt, gamma, ch, T, v);
