@@ -1024,10 +1024,16 @@ ader_status ader_step(ader_ctx* c, double t_end, int64_t max_macro_steps, ader_s
   int64_t enq = 0;
   while (enq < max_macro_steps && c->t < t_end) {
     const int64_t nstep = std::min<int64_t>(chunk, max_macro_steps - enq);
+    const auto h0 = std::chrono::steady_clock::now();
     for (int64_t i = 0; i < nstep && st == ADER_OK; ++i) st = enqueue_step(c, t_end);
     if (st != ADER_OK) break;
     enq += nstep;
+    const auto h1 = std::chrono::steady_clock::now();
     st = read_state(c);
+    if (std::getenv("ADER_GAP_TRACE"))
+      std::fprintf(stderr, "step chunk: %lld steps enqueued in %.3f ms, read-back after %.3f ms\n", (long long)nstep,
+                   std::chrono::duration<double, std::milli>(h1 - h0).count(),
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h1).count());
     if (st != ADER_OK) break;
     if (c->hcnt->err_code) break;
   }
@@ -1200,6 +1206,24 @@ ader_status ader_kernel_stats(ader_ctx* c, double ms[ADER_K_COUNT], int64_t laun
   }
   CK(cudaMemcpy(c->hcnt, c->cnt, sizeof(DevCounters), cudaMemcpyDeviceToHost));
   if (flops) flops[ADER_K_PRED] = (double)(c->hcnt->sweeps - c->prof_sweeps0) * c->kflops_sweep;
+  if (std::getenv("ADER_GAP_TRACE") && c->recs.size() > 1) {
+    // diagnostics: idle gaps of the stream between consecutive timed scopes
+    std::vector<std::pair<float, int>> gaps;
+    double tot = 0.0;
+    for (size_t i = 1; i < c->recs.size(); ++i) {
+      if (!c->recs[i - 1].e1 || !c->recs[i].e0) continue;
+      float g = 0.f;
+      if (cudaEventElapsedTime(&g, c->recs[i - 1].e1, c->recs[i].e0) != cudaSuccess) continue;
+      tot += g;
+      gaps.push_back({g, (int)i});
+    }
+    std::sort(gaps.begin(), gaps.end(), [](auto& a, auto& b) { return a.first > b.first; });
+    std::fprintf(stderr, "gap trace: %zu scopes, idle between scopes %.3f ms; largest:", c->recs.size(), tot);
+    for (size_t j = 0; j < gaps.size() && j < 6; ++j)
+      std::fprintf(stderr, " %.3f ms before scope %d (kind %d)", gaps[j].first, gaps[j].second,
+                   c->recs[gaps[j].second].kind);
+    std::fprintf(stderr, "\n");
+  }
   return ADER_OK;
 }
 
