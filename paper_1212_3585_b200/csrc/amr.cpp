@@ -302,10 +302,11 @@ void garbage_collect(AmrState* A, std::vector<int>* freed) {
 ader_status ensure_capacity(AmrState* A, std::string& err) {
   const int need = (int)A->cells.size();
   if (need <= A->cap) return ADER_OK;
-  // grow geometrically from a reserve of (1 + r^d) level-0 cells: every
+  // grow geometrically from a reserve of (1 + r^d lmax) level-0 cells: every
   // reallocation copies all per-id arrays and synchronises the stream
   const long long n0 = A->n[0][0] * A->n[0][1] * A->n[0][2];
-  const int nc = (int)std::min<long long>(std::max<long long>({2LL * need, n0 * (1 + A->rd), 1024}), 2000000000LL);
+  const int nc = (int)std::min<long long>(std::max<long long>({2LL * need, n0 * (1 + A->rd * std::max(1, A->lmax)), 1024}),
+                                          2000000000LL);
   auto grow = [&](void** p, size_t elem) -> cudaError_t {
     void* np = nullptr;
     cudaError_t e = cudaMalloc(&np, (size_t)nc * elem);

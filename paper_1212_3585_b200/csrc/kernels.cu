@@ -176,8 +176,9 @@ __global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? 4 : 2) k_predictor(
   // one Picard sweep; FIRST: the iterate is the time-constant guess (one flux level)
   auto sweep_once = [&](auto first_tag) {
     constexpr bool FIRST = decltype(first_tag)::value;
+    const bool live = !conv && nsw < max_sweeps;   // this cell still iterates
     constexpr int NT = FIRST ? 1 : N;                          // distinct time levels of the iterate
-    if (!conv && lane_ok) {
+    if (live && lane_ok) {
       // nodal fluxes f*_dir = (dt/dx_dir) f_dir(q) (eqn.nodal.eval @ P:405-412)
 #pragma unroll
       for (int s = 0; s < NT; ++s) {
@@ -198,7 +199,7 @@ __global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? 4 : 2) k_predictor(
     // convergence bookkeeping in FP32 with directed rounding: |dq| rounded up,
     // |q| rounded down, so a passed test implies the exact FP64 test (R2)
     float dmax = 0.f, qmax = 0.f;
-    if (!conv && lane_ok) {
+    if (live && lane_ok) {
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
         double Gs[NT];
@@ -246,35 +247,15 @@ __global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? 4 : 2) k_predictor(
       dmax = fmaxf(dmax, __shfl_xor_sync(0xffffffffu, dmax, o, G));
       qmax = fmaxf(qmax, __shfl_xor_sync(0xffffffffu, qmax, o, G));
     }
-    if (!conv) {
+    if (live) {
       ++nsw;
       if ((double)dmax <= tol * (1.0 + (double)qmax)) conv = true;   // reading R2
     }
   };
-  // exact shortcut: a cell whose w is one state at every node (constant data,
-  // away from fronts) is the fixed point of the Picard map (the D contractions
-  // of equal fluxes vanish in exact arithmetic), so q = w at every time node;
-  // counted as the one sweep that would confirm it
-  {
-    bool flat = cell_ok;
-#pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      const double w0 = __shfl_sync(0xffffffffu, wv[v], 0, G);   // node 0 of this lane group
-      flat &= !lane_ok || wv[v] == w0;
-    }
-    const unsigned gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << (slot * G);
-    flat = cell_ok && (__ballot_sync(0xffffffffu, !flat) & gmask) == 0u;
-    if (flat && max_sweeps >= 1) {
-#pragma unroll
-      for (int v = 0; v < NV; ++v)
-#pragma unroll
-        for (int s = 0; s < N; ++s) qv[v][s] = wv[v];
-      conv = true;
-      nsw = 1;
-    }
-  }
   if (max_sweeps >= 1) sweep_once(std::integral_constant<bool, true>());
-  while (nsw < max_sweeps && !__all_sync(0xffffffffu, conv)) {
+  // every lane takes part in the vote (lane groups of a warp may stop at
+  // different sweep counts)
+  while (!__all_sync(0xffffffffu, conv || nsw >= max_sweeps)) {
     __syncwarp();
     sweep_once(std::integral_constant<bool, false>());
   }
