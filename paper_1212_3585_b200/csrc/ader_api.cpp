@@ -105,6 +105,9 @@ struct ader_ctx {
   DevCounters* hcnt = nullptr;                 // pinned host mirror
   StepState* st = nullptr;                     // device step control (uniform path)
   StepState* hst = nullptr;                    // pinned host mirror
+  double* cons_part = nullptr;                 // conserved-total block partials (device)
+  double* cons_host = nullptr;                 // pinned host copy
+  int cons_cap = 0;                            // blocks
   double t = 0.0;
   bool speed_valid = false;
   ncclComm_t comm = nullptr;
@@ -527,6 +530,8 @@ void free_ctx(ader_ctx* c) {
     if (b) cudaFree(b);
   if (c->st) cudaFree(c->st);
   if (c->hst) cudaFreeHost(c->hst);
+  if (c->cons_part) cudaFree(c->cons_part);
+  if (c->cons_host) cudaFreeHost(c->cons_host);
   for (int i = 0; i < 6; ++i) {
     if (c->sendb[i]) cudaFree(c->sendb[i]);
     if (c->recvb[i]) cudaFree(c->recvb[i]);
@@ -752,6 +757,9 @@ static ader_status create_impl(const ader_config* cfg, ader_ctx** out, bool loop
   CK(cudaMemset(c->st, 0, sizeof(StepState)));
   CK(cudaMallocHost(&c->hst, sizeof(StepState)));
   std::memset(c->hst, 0, sizeof(StepState));
+  c->cons_cap = (int)((owned(c).count() + 255) / 256);
+  CK(cudaMalloc(&c->cons_part, (size_t)c->cons_cap * c->nv * sizeof(double)));
+  CK(cudaMallocHost(&c->cons_host, (size_t)c->cons_cap * c->nv * sizeof(double)));
   // halo buffers (largest slab over axes)
   long long cap = 0;
   for (int a = 0; a < c->d; ++a) {
@@ -975,16 +983,16 @@ ader_status step_finish(ader_ctx* c, ader_status st, ader_step_report* r, unsign
   const Box b = owned(c);
   double vol = 1.0;
   for (int k = 0; k < c->d; ++k) vol *= c->dx[k];
+  // (buffers allocated at ader_create: a cudaMalloc / cudaFree here stalled the
+  // stream for hundreds of ms on some boxes)
   const int maxb = (int)((b.count() + 255) / 256);
-  double* part = nullptr;
-  if (cudaMalloc(&part, (size_t)maxb * c->nv * sizeof(double)) == cudaSuccess) {
-    const int nb = launch_cons_partials(c->k, c->u, b, vol, part, maxb);
-    std::vector<double> h((size_t)nb * c->nv);
-    cudaMemcpyAsync(h.data(), part, h.size() * sizeof(double), cudaMemcpyDeviceToHost, c->k.stream);
-    cudaStreamSynchronize(c->k.stream);
+  if (c->cons_part && maxb <= c->cons_cap) {
+    const int nb = launch_cons_partials(c->k, c->u, b, vol, c->cons_part, maxb);
+    CK(cudaMemcpyAsync(c->cons_host, c->cons_part, (size_t)nb * c->nv * sizeof(double), cudaMemcpyDeviceToHost,
+                       c->k.stream));
+    CK(cudaStreamSynchronize(c->k.stream));
     for (int i = 0; i < nb; ++i)
-      for (int v = 0; v < c->nv; ++v) r->cons_total[v] += h[(size_t)i * c->nv + v];
-    cudaFree(part);
+      for (int v = 0; v < c->nv; ++v) r->cons_total[v] += c->cons_host[(size_t)i * c->nv + v];
   }
   return st;
 }

@@ -179,7 +179,8 @@ class Workload:
 
 
 def config(name: str, n=None) -> Workload:
-    """Named workloads.  c1..c5 follow BASELINE.json configs[0..4]."""
+    """Named workloads.  c1..c5 follow BASELINE.json configs[0..4]; c6 is the
+    paper's 3D AMR explosion (SURVEY §8f #2)."""
     P, T = 0, 1
     if name == "c1":
         nn = n or 32
@@ -208,4 +209,13 @@ def config(name: str, n=None) -> Workload:
         return Workload("c5_orszag_tang_mhd", 2, 1, 3, (nn, nn), (0.0, 0.0),
                         (2 * math.pi, 2 * math.pi), (P,) * 6, 5.0 / 3.0, 0.9, 0.5,
                         ic=orszag_tang(), ch=2.0, refine_factor=3, lmax=3)
+    if name == "c6":
+        # the paper's 3D explosion on an AMR grid (P:1094-1097:
+        # 34^3 level 0, r = 3, lmax = 2, third order); Rusanov flux (the Osher
+        # scheme is inadmissible on this problem at comparable resolution,
+        # reading R21), CFL 0.3 (R1), chi thresholds as C3
+        nn = n or 34
+        return Workload("c6_explosion3d_amr", 3, 0, 2, (nn, nn, nn), (-1.0,) * 3, (1.0,) * 3,
+                        (T,) * 6, 1.4, 0.3, 0.25, ic=explosion(3), refine_factor=3, lmax=2,
+                        chi_ref=0.1, chi_rec=0.05)
     raise KeyError(name)
