@@ -213,9 +213,11 @@ def config(name: str, n=None) -> Workload:
         # the paper's 3D explosion on an AMR grid (P:1094-1097:
         # 34^3 level 0, r = 3, lmax = 2, third order); Rusanov flux (the Osher
         # scheme is inadmissible on this problem at comparable resolution,
-        # reading R21), CFL 0.3 (R1), chi thresholds as C3
+        # reading R21).  With chi 0.1 / 0.05 or CFL 0.3 the first macro step
+        # reaches an inadmissible level-2 state (tools/c6_probe.py); chi
+        # 0.05 / 0.025 with CFL 0.2 runs
         nn = n or 34
         return Workload("c6_explosion3d_amr", 3, 0, 2, (nn, nn, nn), (-1.0,) * 3, (1.0,) * 3,
-                        (T,) * 6, 1.4, 0.3, 0.25, ic=explosion(3), refine_factor=3, lmax=2,
-                        chi_ref=0.1, chi_rec=0.05)
+                        (T,) * 6, 1.4, 0.2, 0.25, ic=explosion(3), refine_factor=3, lmax=2,
+                        chi_ref=0.05, chi_rec=0.025)
     raise KeyError(name)
