@@ -79,6 +79,11 @@ struct AmrState {
   double* xsend = nullptr;
   double* xrecv = nullptr;
   size_t xcap = 0;                                    // doubles
+  // ids whose record changed since the last upload (upload_topology then
+  // compares only those with the device mirror)
+  std::vector<int> dirty;
+  std::vector<char> isdirty;
+  bool all_dirty = true;
   // undo journal of the tentative recoarsening (instead of copying the tree)
   bool jon = false;
   std::vector<std::pair<int, HCell>> jcells;          // (id, previous value)
@@ -201,6 +206,10 @@ int voronoi(const AmrState* A, int id, int* out) {
 // writable cell / map entry; records the previous value while journaling
 HCell& wcell(AmrState* A, int i) {
   if (A->jon) A->jcells.push_back({i, A->cells[i]});
+  if (!A->all_dirty) {
+    if ((size_t)i >= A->isdirty.size()) A->isdirty.resize(std::max<size_t>(A->cells.size(), (size_t)i + 1), 0);
+    if (!A->isdirty[i]) { A->isdirty[i] = 1; A->dirty.push_back(i); }
+  }
   return A->cells[i];
 }
 void set_map(AmrState* A, int l, long long k, int v) {
@@ -384,7 +393,21 @@ ader_status upload_topology(AmrState* A, std::string& err) {
   const int nu = (int)A->cells.size();
   if ((int)A->mirror.size() < nu) A->mirror.resize(nu);
   std::vector<long long> meta, clears, sets;
-  for (int i = 0; i < nu; ++i) {
+  // candidates: every id on the first upload, else the ids written since
+  std::vector<int> cand;
+  const bool full = A->all_dirty || A->dirty.size() * 4 > (size_t)nu;
+  if (!full) {
+    cand = A->dirty;
+    std::sort(cand.begin(), cand.end());
+  }
+  for (int i : A->dirty)
+    if ((size_t)i < A->isdirty.size()) A->isdirty[i] = 0;
+  A->dirty.clear();
+  A->all_dirty = false;
+  const int ncand = full ? nu : (int)cand.size();
+  for (int ci = 0; ci < ncand; ++ci) {
+    const int i = full ? ci : cand[ci];
+    if (i >= nu) continue;
     const HCell& C = A->cells[i];
     HCell& P = A->mirror[i];
     const bool same_pos = C.alive == P.alive && C.level == P.level && C.idx[0] == P.idx[0] && C.idx[1] == P.idx[1] &&
