@@ -206,12 +206,13 @@ def run_reference(args, wl):
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
-def load_traffic(wl, kernel="stdg_predictor"):
-    """dram read+write bytes per launch of `kernel` from the committed ncu capture."""
+def load_traffic(wl, kernel="stdg_predictor", what="dram_bytes_per_launch"):
+    """dram read+write bytes per launch (or the hardware-counted FP64 fraction,
+    what="fp64_hw_frac") of `kernel` from the committed ncu capture."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         d = json.load(open(path))
-        return d.get(wl.name, {}).get(f"{kernel}_dram_bytes_per_launch")
+        return d.get(wl.name, {}).get(f"{kernel}_{what}")
     except Exception:
         return None
 
@@ -357,6 +358,7 @@ def main():
                     "peak_note": "measured copy bandwidth, MEASURED_PEAKS.json hbm_gbs (of measured)",
                     "achieved_note": "algorithmic bytes (w read + q written per predicted cell) / CUDA-event time"}
         roof.update({"kernel": "stdg_predictor", "traffic": load_traffic(wl, "stdg_predictor"),
+                     "ncu_fp64_hw_frac": load_traffic(wl, "stdg_predictor", "fp64_hw_frac"),
                      "arith_intensity_flop_per_byte": ai,
                      "ridge_flop_per_byte": ridge, "alu_tflops": achieved, "alu_frac": achieved / peak,
                      "hbm_gbs": gbs, "hbm_frac": gbs / hbm_peak})
@@ -378,6 +380,7 @@ def main():
                          "unit": "TFLOP/s" if f_ai >= ridge else "GB/s",
                          "frac": (f_tf / peak) if f_ai >= ridge else (f_gbs / hbm_peak),
                          "traffic": load_traffic(wl, f"face_flux_{args.flux}"), "arith_intensity_flop_per_byte": f_ai,
+                         "ncu_fp64_hw_frac": load_traffic(wl, f"face_flux_{args.flux}", "fp64_hw_frac"),
                          "alu_tflops": f_tf, "hbm_gbs": f_gbs,
                          "achieved_note": "algorithmic bytes (each q read once, F written) / CUDA-event time"}
         dominant = roof
