@@ -1,5 +1,5 @@
 """Per-kernel DRAM bytes and hardware-counted FP64 rate from an ncu --set full
-report -> profiles/ncu_traffic.json entry.  usage: ncu_to_json.py rep workload
+report -> profiles/ncu_traffic.json entry.  usage: ncu_to_json.py rep workload [flux]
 
 fp64_hw_frac = (2 dfma + dadd + dmul thread instructions per cycle) / (2 x
 peak dfma thread instructions per cycle), i.e. the FP64 pipe's flop rate as
@@ -16,7 +16,7 @@ NAMES = [("k_predictor", "stdg_predictor"), ("k_face_flux", "face_flux_rusanov")
          ("k_update", "fv_update")]
 
 
-def main(rep, workload):
+def main(rep, workload, flux="rusanov"):
     t = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(t.splitlines()))
     h, u = rows[0], rows[1]
@@ -30,6 +30,7 @@ def main(rep, workload):
     for r in rows[2:]:
         name = r[col["Kernel Name"]]
         for pat, key in NAMES:
+            key = key.replace("rusanov", flux)
             if pat in name:
                 out[f"{key}_dram_bytes_per_launch"] = val(r, "dram__bytes_read.sum") + val(r, "dram__bytes_write.sum")
                 f = (2 * val(r, "smsp__sass_thread_inst_executed_op_dfma_pred_on.sum.per_cycle_elapsed")
@@ -47,4 +48,4 @@ def main(rep, workload):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2])
+    main(*sys.argv[1:4])
