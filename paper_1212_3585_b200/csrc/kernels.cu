@@ -98,9 +98,6 @@ __global__ void __launch_bounds__(256) k_weno(const double* __restrict__ src, do
 // Sweep 1 starts from the time-constant guess q^0 = w (R3): all N time levels
 // carry the same flux, so it is evaluated once and q^1_s = w - (sum_s' T_ss') G.
 // ===========================================================================
-// (the constant-cell shortcut below hangs the AMR wall case on the GPU; cause
-// not found this round, so it is compiled out)
-constexpr bool FLAT_SHORTCUT = false;
 
 template <int D, int M, int SYS, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? 4 : 2) k_predictor(
@@ -256,28 +253,6 @@ __global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? 4 : 2) k_predictor(
       if ((double)dmax <= tol * (1.0 + (double)qmax)) conv = true;   // reading R2
     }
   };
-  // exact shortcut: a cell whose w is one state at every node (constant data,
-  // away from fronts) is the fixed point of the Picard map (the D contractions
-  // of equal fluxes vanish in exact arithmetic), so q = w at every time node;
-  // counted as the one sweep that would confirm it
-  if (FLAT_SHORTCUT) {
-    bool flat = cell_ok;
-#pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      const double w0 = __shfl_sync(0xffffffffu, wv[v], 0, G);   // node 0 of this lane group
-      flat = flat && (!lane_ok || wv[v] == w0);
-    }
-    const unsigned gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << (slot * G);
-    flat = cell_ok && (__ballot_sync(0xffffffffu, !flat) & gmask) == 0u;
-    if (flat && max_sweeps >= 1) {
-#pragma unroll
-      for (int v = 0; v < NV; ++v)
-#pragma unroll
-        for (int s = 0; s < N; ++s) qv[v][s] = wv[v];
-      conv = true;
-      nsw = 1;
-    }
-  }
   if (max_sweeps >= 1) sweep_once(std::integral_constant<bool, true>());
   // every lane takes part in the vote (lane groups of a warp may stop at
   // different sweep counts)
@@ -416,7 +391,7 @@ __device__ __forceinline__ bool point_flux(const double* __restrict__ q, long lo
 
 constexpr int pow2_at_least(int x) { return x <= 1 ? 1 : 2 * pow2_at_least((x + 1) / 2); }
 
-template <int D, int M, int SYS, int WARPS, int YC, int FLUX, bool PREFETCH = false>
+template <int D, int M, int SYS, int WARPS, int YC, int FLUX>
 __global__ void __launch_bounds__(WARPS * 32, (FLUX == 1) ? 5 : (SYS == 1 ? 4 : (D == 3 ? 7 : 8))) k_face_flux_cells(const double* __restrict__ q, double* __restrict__ F,
                                                                 const Box E, const int H, const int n0, const int n1,
                                                                 const int n2, const long long sy, const long long sz,
@@ -457,30 +432,17 @@ __global__ void __launch_bounds__(WARPS * 32, (FLUX == 1) ? 5 : (SYS == 1 ? 4 : 
   bool good = true;
   constexpr int K = D * NV;
   constexpr int BLK = NV * NS * N;
-  // (staging the cell's own block in shared memory for its D faces was
-  // tried: 1.6x slower at 256^3 — the pencil reads stay global / L1)
+  // (tried and removed: staging the cell's own block in shared memory (1.6x
+  // slower, bank conflicts) and an L1 prefetch of the D+1 blocks (8 % slower))
   const double* qown = q + cR * BLK;
-  constexpr bool STAGE = false;
-  if constexpr (PREFETCH) {
-    // (off: measured 8 % slower at 256^3) the D+1 blocks this cell reads,
-    // requested into L1 by the whole lane
-    // group at once (no scoreboard wait), so the dependent pencil loads of
-    // the D faces hit L1 instead of queueing one face after the other
-    if (ok) {
-      const double* blk[4] = {qown, q + (cR - 1) * BLK, q + (cR - sy) * BLK, q + (cR - sz) * BLK};
-#pragma unroll
-      for (int b = 0; b <= D; ++b)
-        for (int j = p * 16; j < BLK; j += G * 16) asm volatile("prefetch.global.L1 [%0];" ::"l"(blk[b] + j));
-    }
-  }
-  good &= point_flux_blocks<D, M, SYS, 0, FLUX, true, !STAGE>(
+  good &= point_flux_blocks<D, M, SYS, 0, FLUX, true>(
       q + (cR - 1) * BLK, qown, ps, fok[0], (bmask & 1) && cx == H, (bmask & 2) && cx == H + n0,
       (rmask & 1) && cx == H, (rmask & 2) && cx == H + n0, wt, gamma, ch, T, v);
-  good &= point_flux_blocks<D, M, SYS, 1, FLUX, true, !STAGE>(
+  good &= point_flux_blocks<D, M, SYS, 1, FLUX, true>(
       q + (cR - sy) * BLK, qown, ps, fok[1], (bmask & 4) && cy == H, (bmask & 8) && cy == H + n1,
       (rmask & 4) && cy == H, (rmask & 8) && cy == H + n1, wt, gamma, ch, T, v + NV);
   if constexpr (D == 3)
-    good &= point_flux_blocks<D, M, SYS, 2, FLUX, true, !STAGE>(
+    good &= point_flux_blocks<D, M, SYS, 2, FLUX, true>(
         q + (cR - sz) * BLK, qown, ps, fok[2], (bmask & 16) && cz == zH, (bmask & 32) && cz == zH + n2,
         (rmask & 16) && cz == zH, (rmask & 32) && cz == zH + n2, wt, gamma, ch, T, v + 2 * NV);
   if (!good) record_error(cnt, 1, 2, cR);
