@@ -427,12 +427,23 @@ ader_status upload_topology(AmrState* A, std::string& err) {
   A->lall.clear();
   A->lownall.clear();
   const int W = A->ranks.world, me = A->ranks.rank;
-  A->own.assign(nu, 0);
-  A->comp.assign(nu, 0);
+  A->own.assign(nu, W > 1 ? 0 : 1);
+  A->comp.assign(nu, W > 1 ? 0 : 1);
   std::vector<int> owner(W > 1 ? nu : 0, -1);
   std::vector<std::vector<int>> send_to(W > 1 ? (size_t)(A->lmax + 1) * W : 0);
   for (int l = 0; l < kAmrMaxLevels; ++l) A->nlev[l] = 0;
-  for (int i = 0; i < nu; ++i) {
+  if (W == 1) {
+    // one rank: every alive cell is owned and computed; lists in id order
+    for (int l = 0; l <= A->lmax; ++l) { A->lact[l].reserve(nu); A->lvch[l].reserve(nu / 2); A->lvmo[l].reserve(nu / 8); }
+    for (int i = 0; i < nu; ++i) {
+      const HCell& C = A->cells[i];
+      if (!C.alive) continue;
+      A->nlev[C.level]++;
+      (C.status == 0 ? A->lact : (C.status == 1 ? A->lvch : A->lvmo))[C.level].push_back(i);
+    }
+    for (int l = 0; l <= A->lmax; ++l) A->lown[l] = A->lact[l];
+  }
+  for (int i = 0; i < (W > 1 ? nu : 0); ++i) {
     const HCell& C = A->cells[i];
     if (!C.alive) continue;
     A->nlev[C.level]++;
