@@ -340,10 +340,7 @@ def main():
         N = wl.degree + 1
         nvv = 9 if wl.system == 1 else wl.dim + 2
         cells_per_launch = rep.pred_cells / max(1, kl[ader.K_PRED])
-        # 3D uniform: the predictor reads the y-sweep output w_xy and forms the z
-        # sweep itself (N^(d-1) input doubles per variable), else the full w
-        fused = wl.dim == 3 and wl.lmax == 0 and os.environ.get("ADER_NO_FUSEZ") is None
-        pred_bytes = cells_per_launch * nvv * (N ** (wl.dim - 1 if fused else wl.dim) + N ** (wl.dim + 1)) * 8
+        pred_bytes = cells_per_launch * nvv * (N ** wl.dim + N ** (wl.dim + 1)) * 8
         hbm_peak = 6449.1
         try:
             hbm_peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
@@ -359,7 +356,7 @@ def main():
         else:
             roof = {"bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak,
                     "peak_note": "measured copy bandwidth, MEASURED_PEAKS.json hbm_gbs (of measured)",
-                    "achieved_note": "algorithmic bytes (w or, 3D, w_xy read + q written per predicted cell) / CUDA-event time"}
+                    "achieved_note": "algorithmic bytes (w read + q written per predicted cell) / CUDA-event time"}
         roof.update({"kernel": "stdg_predictor", "traffic": load_traffic(wl, "stdg_predictor"),
                      "ncu_fp64_hw_frac": load_traffic(wl, "stdg_predictor", "fp64_hw_frac"),
                      "arith_intensity_flop_per_byte": ai,

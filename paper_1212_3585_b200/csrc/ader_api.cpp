@@ -112,7 +112,6 @@ struct ader_ctx {
   bool speed_valid = false;
   ncclComm_t comm = nullptr;
   bool loopback = false;                       // test-only rank group in one process (ader_debug_group_*)
-  bool fuse_z = true;                          // 3D: z-sweep WENO inside the predictor (ADER_NO_FUSEZ=1: off)
   std::string err;
   // instrumentation
   bool prof = false;
@@ -408,9 +407,8 @@ ader_status fill_halo(ader_ctx* c, double* u) {
 }
 
 // ---- one stage each ----------------------------------------------------------
-void run_weno(ader_ctx* c, bool full = false) {
-  // x sweep on the rows needed by the y (and z) sweeps, ..., last sweep on block+1;
-  // 3D with fuse_z: the z sweep is formed inside the predictor (unless full)
+void run_weno(ader_ctx* c) {
+  // x sweep on the rows needed by the y (and z) sweeps, ..., last sweep on block+1
   const int H = c->H, M = c->M;
   const int zH = c->d == 3 ? H : 0;
   const int nx = c->n[0], ny = c->n[1], nz = c->n[2];
@@ -425,13 +423,11 @@ void run_weno(ader_ctx* c, bool full = false) {
     const Box rx = make_box(H - 1, H + nx + 1, H - 1 - M, H + ny + 1 + M, zH - 1 - M, zH + nz + 1 + M);
     const Box ry = make_box(H - 1, H + nx + 1, H - 1, H + ny + 1, zH - 1 - M, zH + nz + 1 + M);
     const Box rz = grown(c, 1);
-    const bool zsweep = full || !c->fuse_z;
     Scope s(c, ADER_K_WENO,
-            weno_problem_flops(M) *
-                (rx.count() * c->nv + ry.count() * c->nv * c->N + (zsweep ? rz.count() * c->nv * c->N * c->N : 0)));
+            weno_problem_flops(M) * (rx.count() * c->nv + ry.count() * c->nv * c->N + rz.count() * c->nv * c->N * c->N));
     launch_weno_sweep(c->k, 0, c->u, c->wx, rx);
     launch_weno_sweep(c->k, 1, c->wx, c->wxy, ry);
-    if (zsweep) launch_weno_sweep(c->k, 2, c->wxy, dst_last, rz);
+    launch_weno_sweep(c->k, 2, c->wxy, dst_last, rz);
   }
 }
 
@@ -458,9 +454,7 @@ void run_predictor(ader_ctx* c, double dt, const double* dtdx_dev = nullptr) {
   double dtdx[3] = {0, 0, 0};
   for (int k = 0; k < c->d; ++k) dtdx[k] = dt / c->dx[k];
   Scope s(c, ADER_K_PRED, 0.0);   // flops from the sweep counter (ader_kernel_stats)
-  const bool fz = c->d == 3 && c->fuse_z;
-  launch_predictor(c->k, fz ? c->wxy : c->w, c->q, r, dtdx, c->cfg.pred_tol, c->cfg.pred_max_sweeps, c->cnt, dtdx_dev,
-                   fz);
+  launch_predictor(c->k, c->w, c->q, r, dtdx, c->cfg.pred_tol, c->cfg.pred_max_sweeps, c->cnt, dtdx_dev);
 }
 
 void face_boxes(const ader_ctx* c, Box fb[3]) {
@@ -696,7 +690,6 @@ static ader_status create_impl(const ader_config* cfg, ader_ctx** out, bool loop
   if (!build_osher_quadrature(cfg->flux_quad > 0 ? cfg->flux_quad : 3, &c->k.tab))
     return fail(c, ADER_ERR_CONFIG, "no path rule for flux_quad=%d", cfg->flux_quad);
   c->k.tab.flux = cfg->flux;
-  c->fuse_z = std::getenv("ADER_NO_FUSEZ") == nullptr;
 
   c->k.D = c->d; c->k.M = c->M; c->k.SYS = cfg->system; c->k.NV = c->nv;
   c->k.sy = c->P[0]; c->k.sz = (long long)c->P[0] * c->P[1];
@@ -1265,7 +1258,7 @@ ader_status ader_debug_dump(ader_ctx* c, int32_t what, double dt, double* out, i
   const Box b = owned(c);
   ader_status st = fill_halo(c, c->u);
   if (st != ADER_OK) return st;
-  run_weno(c, what == 0);   // the RECON dump needs the full w (z sweep included)
+  run_weno(c);
   if (what == 0) {
     if (capacity < b.count() * c->nv * c->NS) return fail(c, ADER_ERR_ARG, "capacity too small");
     launch_gather(c->k, c->w, c->nv * c->NS, b, c->stage);

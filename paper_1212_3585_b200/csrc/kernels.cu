@@ -99,12 +99,7 @@ __global__ void __launch_bounds__(256) k_weno(const double* __restrict__ src, do
 // carry the same flux, so it is evaluated once and q^1_s = w - (sum_s' T_ss') G.
 // ===========================================================================
 
-// FUSEZ (3D box mode): w is the y-sweep output w_xy [cell][NV][N^2] and each
-// lane forms its node's w by the z-sweep WENO itself (the same weno1d on the
-// same window as k_weno<M,2>, so bitwise the same w), which saves writing and
-// re-reading the full w (1080 B per cell at M=2); cells are then visited x
-// fastest inside y-chunks of 16 rows so the 2M+1 w_xy planes stay in L2.
-template <int D, int M, int SYS, int WARPS, bool FUSEZ = false>
+template <int D, int M, int SYS, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? 4 : 2) k_predictor(
     const double* __restrict__ w, double* __restrict__ q, const Box R, const long long sy, const long long sz,
     const double dtdx0, const double dtdx1, const double dtdx2, const double gamma, const double ch,
@@ -130,25 +125,9 @@ __global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? 4 : 2) k_predictor(
   const bool lane_ok = node0 < NS;
   const int node = lane_ok ? node0 : NS - 1;
   double* Fs = smem + (warp * CPW + slot) * FSZ;
-  // cells of a box (uniform grid) or of an id list (AMR level); FUSEZ: box
-  // cells in y-chunks, -1 for the padding rows of the last chunk
-  constexpr int YCH = 16;
-  const long long count = list ? nlist
-                               : (FUSEZ ? (long long)R.ext[0] * ((R.ext[1] + YCH - 1) / YCH) * YCH * R.ext[2]
-                                        : R.count());
-  auto cell_of = [&](long long r) -> long long {
-    if (list) return (long long)list[r];
-    if constexpr (FUSEZ) {
-      const long long x = r % R.ext[0], t = r / R.ext[0];
-      const long long yi = t % YCH, t2 = t / YCH;
-      const long long z = t2 % R.ext[2], yb = t2 / R.ext[2];
-      const long long y = yb * YCH + yi;
-      if (y >= R.ext[1]) return -1;
-      return (R.lo[0] + x) + (R.lo[1] + y) * sy + (R.lo[2] + z) * sz;
-    } else {
-      return box_cell(R, r, sy, sz);
-    }
-  };
+  // cells of a box (uniform grid) or of an id list (AMR level)
+  const long long count = list ? nlist : R.count();
+  auto cell_of = [&](long long r) -> long long { return list ? (long long)list[r] : box_cell(R, r, sy, sz); };
   int ia[3];
   ia[0] = node % N;
   ia[1] = (node / N) % N;
@@ -166,61 +145,32 @@ __global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? 4 : 2) k_predictor(
 #pragma unroll
     for (int j = 0; j < N; ++j) Drow[d][j] = T.D[ia[d]][j];
 
-  // node value of w for cell c (FUSEZ: the z-sweep WENO of the lane's (x, y) pencil)
-  auto load_w = [&](long long c, double (&out)[NV]) {
-    if constexpr (FUSEZ) {
-      constexpr int N2 = N * N;
-      const int xy = ia[0] + N * ia[1];
-#pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        double win[2 * M + 1], wo[N];
-#pragma unroll
-        for (int o = 0; o < 2 * M + 1; ++o) win[o] = __ldg(&w[(c + (o - M) * sz) * (NV * N2) + v * N2 + xy]);
-        weno1d<M>(T, win, wo);
-        double r = wo[0];
-#pragma unroll
-        for (int a = 1; a < N; ++a) r = (ia[2] == a) ? wo[a] : r;
-        out[v] = r;
-      }
-    } else {
-#pragma unroll
-      for (int v = 0; v < NV; ++v) out[v] = __ldg(&w[c * (NV * NS) + v * NS + node]);
-    }
-  };
   // persistent warps: the warp walks cell groups with a stride of the whole
   // grid and prefetches the next group's w while it iterates on the current one
-  // (FUSEZ: w is formed at the top of the iteration instead)
   const long long wstride = (long long)gridDim.x * WARPS;
   long long wb = (long long)blockIdx.x * WARPS + warp;        // warp-uniform iteration index
   double wn[NV];
-  if constexpr (!FUSEZ) {
+  {
     const long long r0 = wb * CPW + slot;
     const long long c0 = r0 < count ? cell_of(r0) : 0;
-    if (r0 < count) load_w(c0, wn);
-    else
-      for (int v = 0; v < NV; ++v) wn[v] = 1.0;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) wn[v] = r0 < count ? __ldg(&w[c0 * (NV * NS) + v * NS + node]) : 1.0;
   }
   unsigned long long acc_sweeps = 0, acc_cells = 0;
   int acc_max = 0;
   for (; wb * CPW < count; wb += wstride) {
   const long long rc = wb * CPW + slot;
-  const long long cell0 = rc < count ? cell_of(rc) : -1;
-  const bool cell_ok = cell0 >= 0;
+  const bool cell_ok = rc < count;
   const bool active = cell_ok && lane_ok;
-  const long long cell = cell_ok ? cell0 : 0;
+  const long long cell = cell_ok ? cell_of(rc) : 0;
   double wv[NV], qv[NV][N];
-  if constexpr (FUSEZ) {
-    if (cell_ok) load_w(cell, wv);
-    else
-      for (int v = 0; v < NV; ++v) wv[v] = 1.0;
-  } else {
 #pragma unroll
-    for (int v = 0; v < NV; ++v) wv[v] = wn[v];
+  for (int v = 0; v < NV; ++v) wv[v] = wn[v];
+  {
     const long long rn = (wb + wstride) * CPW + slot;
     const long long cn = rn < count ? cell_of(rn) : 0;
-    if (rn < count) load_w(cn, wn);
-    else
-      for (int v = 0; v < NV; ++v) wn[v] = 1.0;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) wn[v] = rn < count ? __ldg(&w[cn * (NV * NS) + v * NS + node]) : 1.0;
   }
   bool conv = !cell_ok, bad = false;
   int nsw = 0;
@@ -763,51 +713,32 @@ void launch_weno_sweep(const KCtx& k, int sweep, const double* src, double* dst,
 }
 
 void launch_predictor(const KCtx& k, const double* w, double* q, const Box& region, const double dtdx[3],
-                      double tol, int max_sweeps, DevCounters* cnt, const double* dtdx_dev, bool fusez) {
-  launch_predictor_list(k, w, q, region, nullptr, 0, dtdx, tol, max_sweeps, cnt, nullptr, dtdx_dev, fusez);
+                      double tol, int max_sweeps, DevCounters* cnt, const double* dtdx_dev) {
+  launch_predictor_list(k, w, q, region, nullptr, 0, dtdx, tol, max_sweeps, cnt, nullptr, dtdx_dev);
 }
-
-namespace {
-template <int D, int M, int SYS, bool FUSEZ>
-void predictor_launch(const KCtx& k, const double* w, double* q, const Box& region, const int* list, long long nlist,
-                      long long count, const double dtdx[3], double tol, int max_sweeps, DevCounters* cnt,
-                      const unsigned char* emask, const double* dtdx_dev) {
-  constexpr int N = M + 1;
-  constexpr int NS = ipow_c(N, D);
-  constexpr int CPW = 32 / ((NS <= 8) ? 8 : (NS <= 16 ? 16 : 32));
-  const size_t sm = pred_smem<D, M, SYS>();
-  auto kern = k_predictor<D, M, SYS, kPredWarps, FUSEZ>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    attr = true;
-  }
-  // persistent grid: enough CTAs for every SM at full occupancy, a few times over
-  const unsigned need = grid_for(count, kPredWarps * CPW);
-  const unsigned g = need < 148u * 16u ? need : 148u * 16u;
-  count_launch(k);
-  kern<<<g, kPredWarps * 32, sm, k.stream>>>(w, q, region, k.sy, k.sz, dtdx[0], dtdx[1], dtdx[2], k.gamma, k.ch, tol,
-                                              max_sweeps, cnt, list, nlist, emask, dtdx_dev, k.tab);
-}
-}  // namespace
 
 void launch_predictor_list(const KCtx& k, const double* w, double* q, const Box& region, const int* list,
                            long long nlist, const double dtdx[3], double tol, int max_sweeps, DevCounters* cnt,
-                           const unsigned char* emask, const double* dtdx_dev, bool fusez) {
+                           const unsigned char* emask, const double* dtdx_dev) {
   const long long count = list ? nlist : region.count();
   if (count == 0) return;
   ADER_DISPATCH(k.D, k.M, k.SYS, {
-    bool done = false;
-    if constexpr (D == 3) {
-      if (fusez && !list) {
-        predictor_launch<D, M, SYS, true>(k, w, q, region, list, nlist, count, dtdx, tol, max_sweeps, cnt, emask,
-                                          dtdx_dev);
-        done = true;
-      }
+    constexpr int N = M + 1;
+    constexpr int NS = ipow_c(N, D);
+    constexpr int CPW = 32 / ((NS <= 8) ? 8 : (NS <= 16 ? 16 : 32));
+    const size_t sm = pred_smem<D, M, SYS>();
+    auto kern = k_predictor<D, M, SYS, kPredWarps>;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      attr = true;
     }
-    if (!done)
-      predictor_launch<D, M, SYS, false>(k, w, q, region, list, nlist, count, dtdx, tol, max_sweeps, cnt, emask,
-                                         dtdx_dev);
+    // persistent grid: enough CTAs for every SM at full occupancy, a few times over
+    const unsigned need = grid_for(count, kPredWarps * CPW);
+    const unsigned g = need < 148u * 16u ? need : 148u * 16u;
+    count_launch(k);
+    kern<<<g, kPredWarps * 32, sm, k.stream>>>(w, q, region, k.sy, k.sz, dtdx[0], dtdx[1], dtdx[2], k.gamma,
+                                                k.ch, tol, max_sweeps, cnt, list, nlist, emask, dtdx_dev, k.tab);
   });
 }
 

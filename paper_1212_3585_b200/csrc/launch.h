@@ -65,17 +65,13 @@ bool supported(int D, int M, int SYS);
 void launch_weno_sweep(const KCtx& k, int sweep, const double* src, double* dst, const Box& region);
 // Predictor on `region`: w -> q.  dtdx_dev (optional): read dt/dx from the
 // device (StepState::dtdx) instead of dtdx.
-// fusez (3D, box mode): w is the y-sweep output w_xy and the predictor forms
-// the z-sweep WENO itself (k_weno's z sweep is then skipped).
 void launch_predictor(const KCtx& k, const double* w, double* q, const Box& region, const double dtdx[3],
-                      double tol, int max_sweeps, DevCounters* cnt, const double* dtdx_dev = nullptr,
-                      bool fusez = false);
+                      double tol, int max_sweeps, DevCounters* cnt, const double* dtdx_dev = nullptr);
 // Predictor on the cells of an id list (AMR levels): w, q indexed by id.  If
 // emask is given only cells with emask[id] != 0 report solver errors.
 void launch_predictor_list(const KCtx& k, const double* w, double* q, const Box& region, const int* list,
                            long long nlist, const double dtdx[3], double tol, int max_sweeps, DevCounters* cnt,
-                           const unsigned char* emask = nullptr, const double* dtdx_dev = nullptr,
-                           bool fusez = false);
+                           const unsigned char* emask = nullptr, const double* dtdx_dev = nullptr);
 // Face fluxes on the lower face of every cell of `ext` (owned block + 1 on each
 // active axis), one lane group per cell computing all its lower faces
 // (L2-friendly traversal).  bmask bit 2*dir (2*dir+1): the first (last) face
