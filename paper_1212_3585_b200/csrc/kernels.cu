@@ -127,7 +127,14 @@ __global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? 4 : 2) k_predictor(
   double* Fs = smem + (warp * CPW + slot) * FSZ;
   // cells of a box (uniform grid) or of an id list (AMR level)
   const long long count = list ? nlist : R.count();
-  auto cell_of = [&](long long r) -> long long { return list ? (long long)list[r] : box_cell(R, r, sy, sz); };
+  // (32-bit index decomposition: a rank's box holds < 2^31 cells)
+  const unsigned bx = (unsigned)R.ext[0], by = (unsigned)R.ext[1];
+  auto cell_of = [&](long long r) -> long long {
+    if (list) return (long long)list[r];
+    const unsigned ur = (unsigned)r, t = ur / bx, z = t / by;
+    return (long long)(R.lo[0] + (int)(ur - t * bx)) + (long long)(R.lo[1] + (int)(t - z * by)) * sy +
+           (long long)(R.lo[2] + (int)z) * sz;
+  };
   int ia[3];
   ia[0] = node % N;
   ia[1] = (node / N) % N;
@@ -197,9 +204,12 @@ __global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? 4 : 2) k_predictor(
       }
     }
     __syncwarp();
-    // convergence bookkeeping in FP32 with directed rounding: |dq| rounded up,
-    // |q| rounded down, so a passed test implies the exact FP64 test (R2)
-    float dmax = 0.f, qmax = 0.f;
+    // convergence bookkeeping on the high words of |dq| and |q| (monotone in
+    // the value for non-negative doubles): max hi(|dq|) + 1 bounds |dq| from
+    // above, max hi(|q|) with a zero low word bounds |q| from below, so a
+    // passed test implies the exact FP64 test (R2); 32-bit integer max and
+    // shuffles instead of FP64 -> FP32 conversions
+    unsigned dmax = 0u, qmax = 0u;
     if (live && lane_ok) {
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
@@ -236,8 +246,8 @@ __global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? 4 : 2) k_predictor(
             for (int s2 = 0; s2 < NT; ++s2) acc -= T.T[s][s2] * Gs[s2];
           }
           const double prev = FIRST ? wv[v] : qv[v][s];
-          dmax = fmaxf(dmax, __double2float_ru(fabs(acc - prev)));
-          qmax = fmaxf(qmax, __double2float_rd(fabs(acc)));
+          dmax = max(dmax, (unsigned)__double2hiint(fabs(acc - prev)));
+          qmax = max(qmax, (unsigned)__double2hiint(fabs(acc)));
           qv[v][s] = acc;
         }
       }
@@ -245,12 +255,13 @@ __global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? 4 : 2) k_predictor(
     // per-cell max over the lane group (segmented butterfly)
 #pragma unroll
     for (int o = G / 2; o > 0; o >>= 1) {
-      dmax = fmaxf(dmax, __shfl_xor_sync(0xffffffffu, dmax, o, G));
-      qmax = fmaxf(qmax, __shfl_xor_sync(0xffffffffu, qmax, o, G));
+      dmax = max(dmax, __shfl_xor_sync(0xffffffffu, dmax, o, G));
+      qmax = max(qmax, __shfl_xor_sync(0xffffffffu, qmax, o, G));
     }
     if (live) {
       ++nsw;
-      if ((double)dmax <= tol * (1.0 + (double)qmax)) conv = true;   // reading R2
+      const double dup = __hiloint2double((int)(dmax + 1u), 0), qlo = __hiloint2double((int)qmax, 0);
+      if (dup <= tol * (1.0 + qlo)) conv = true;   // reading R2
     }
   };
   if (max_sweeps >= 1) sweep_once(std::integral_constant<bool, true>());
