@@ -16,7 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB = None
 
 EULER, MHD = 0, 1
-PERIODIC, TRANSMISSIVE, REFLECTIVE = 0, 1, 2
+PERIODIC, TRANSMISSIVE, REFLECTIVE, INFLOW = 0, 1, 2, 3
 RUSANOV, OSHER = 0, 1
 
 IC_FN = C.CFUNCTYPE(None, C.POINTER(C.c_double), C.c_int64, C.POINTER(C.c_double), C.c_void_p)

@@ -836,6 +836,8 @@ orc_ctx* orc_create(const orc_config* cfg) {
   if (cfg->flux == ORC_FLUX_OSHER && cfg->system != ORC_EULER) return NULL;   /* Osher: Euler only */
   for (int k = 0; k < 2 * cfg->dim; ++k)
     if (cfg->bc[k] == ORC_BC_REFLECTIVE && (cfg->system != ORC_EULER || cfg->n[k / 2] < cfg->degree + 1)) return NULL;
+  for (int k = 0; k < cfg->dim; ++k)
+    if ((cfg->bc[2 * k] == ORC_BC_PERIODIC) != (cfg->bc[2 * k + 1] == ORC_BC_PERIODIC)) return NULL;
   orc_ctx* c = (orc_ctx*)calloc(1, sizeof(orc_ctx));
   c->cfg = *cfg;
   c->d = cfg->dim; c->M = cfg->degree; c->N = c->M + 1;
@@ -865,7 +867,8 @@ double orc_time(const orc_ctx* c) { return c->t; }
 int64_t orc_num_cells(const orc_ctx* c) { return (int64_t)c->n[0] * c->n[1] * c->n[2]; }
 
 int orc_set_initial(orc_ctx* c, orc_ic_fn ic, void* user) {
-  int32_t lo[3] = {0, 0, 0}, hi[3] = {c->n[0], c->n[1], c->n[2]};
+  /* the box reaches into the ghost layer on inflow sides (clipped there) */
+  int32_t lo[3] = {-c->G, -c->G, -c->G}, hi[3] = {c->n[0] + c->G, c->n[1] + c->G, c->n[2] + c->G};
   return orc_set_initial_box(c, ic, user, lo, hi);
 }
 
@@ -876,8 +879,11 @@ int orc_set_initial_box(orc_ctx* c, orc_ic_fn ic, void* user, const int32_t* blo
   int nq = ipow(Q, d);
   int bl[3], be[3];
   for (int k = 0; k < 3; ++k) {
-    bl[k] = (k < d) ? (blo[k] < 0 ? 0 : blo[k]) : 0;
-    int h = (k < d) ? (bhi[k] > c->n[k] ? c->n[k] : bhi[k]) : 1;
+    /* inflow sides (R23): the ghost layer takes IC averages too */
+    const int glo = (k < d && c->cfg.bc[2 * k] == ORC_BC_INFLOW) ? -c->G : 0;
+    const int ghi = (k < d && c->cfg.bc[2 * k + 1] == ORC_BC_INFLOW) ? c->n[k] + c->G : c->n[k];
+    bl[k] = (k < d) ? (blo[k] < glo ? glo : blo[k]) : 0;
+    int h = (k < d) ? (bhi[k] > ghi ? ghi : bhi[k]) : 1;
     be[k] = h > bl[k] ? h - bl[k] : 0;
   }
   int64_t ncell = (int64_t)be[0] * be[1] * be[2];
@@ -947,6 +953,7 @@ static int ghost_src(const orc_ctx* c, int axis, int i) {
   int side = (i < 0) ? 0 : 1;
   if (c->cfg.bc[2 * axis + side] == ORC_BC_PERIODIC) return ((i % n) + n) % n;
   if (c->cfg.bc[2 * axis + side] == ORC_BC_REFLECTIVE) return (i < 0) ? -1 - i : 2 * n - 1 - i;
+  if (c->cfg.bc[2 * axis + side] == ORC_BC_INFLOW) return i;   /* R23: the ghost keeps its IC average */
   return (i < 0) ? 0 : n - 1;
 }
 static int ghost_reflected(const orc_ctx* c, int axis, int i) {
@@ -1020,8 +1027,9 @@ static void gather_box(const orc_ctx* c, int i, int j, int k, double* box) {
 static int beyond_transmissive(const orc_ctx* c, int i, int j, int k) {
   const int ii[3] = {i, j, k};
   for (int a = 0; a < c->d; ++a) {
-    if (ii[a] < 0 && c->cfg.bc[2 * a] != ORC_BC_PERIODIC) return 1;
-    if (ii[a] >= c->n[a] && c->cfg.bc[2 * a + 1] != ORC_BC_PERIODIC) return 1;
+    const int lo = c->cfg.bc[2 * a], hi = c->cfg.bc[2 * a + 1];
+    if (ii[a] < 0 && (lo == ORC_BC_TRANSMISSIVE || lo == ORC_BC_REFLECTIVE)) return 1;
+    if (ii[a] >= c->n[a] && (hi == ORC_BC_TRANSMISSIVE || hi == ORC_BC_REFLECTIVE)) return 1;
   }
   return 0;
 }

@@ -23,7 +23,8 @@ extern "C" {
 #define ORC_MAXV 9            /* conserved variables (MHD-GLM)               */
 
 enum { ORC_EULER = 0, ORC_MHD = 1 };
-enum { ORC_BC_PERIODIC = 0, ORC_BC_TRANSMISSIVE = 1, ORC_BC_REFLECTIVE = 2 };   /* reflective: Euler only (R22) */
+enum { ORC_BC_PERIODIC = 0, ORC_BC_TRANSMISSIVE = 1, ORC_BC_REFLECTIVE = 2,   /* reflective: Euler only (R22) */
+       ORC_BC_INFLOW = 3 };   /* Dirichlet inflow: ghost cells keep the IC averages (R23), uniform grids */
 enum { ORC_FLUX_RUSANOV = 0, ORC_FLUX_OSHER = 1 };   /* eqn.rusanov / eqn.osher */
 
 typedef struct {

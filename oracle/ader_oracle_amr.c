@@ -653,8 +653,10 @@ void* orc_amr_create(const orc_config* cfg) {
   if (!cfg || (cfg->dim != 2 && cfg->dim != 3) || cfg->degree < 2 || cfg->degree > 3) return NULL;
   if (cfg->lmax < 0 || cfg->lmax >= LMAXX || cfg->refine_factor < cfg->degree) return NULL;
   if (cfg->flux == ORC_FLUX_OSHER && cfg->system != ORC_EULER) return NULL;   /* Osher: Euler only */
-  for (int k = 0; k < 2 * cfg->dim; ++k)
+  for (int k = 0; k < 2 * cfg->dim; ++k) {
     if (cfg->bc[k] == ORC_BC_REFLECTIVE && (cfg->system != ORC_EULER || cfg->n[k / 2] < cfg->degree + 1)) return NULL;
+    if (cfg->bc[k] == ORC_BC_INFLOW) return NULL;   /* R23: uniform grids only */
+  }
   amr_t* A = (amr_t*)calloc(1, sizeof(amr_t));
   A->cfg = *cfg;
   A->d = cfg->dim; A->M = cfg->degree; A->N = A->M + 1;

@@ -17,7 +17,7 @@ _LIB = None
 
 ABI_VERSION = 2
 EULER, MHD_GLM = 0, 1
-PERIODIC, TRANSMISSIVE, REFLECTIVE = 0, 1, 2
+PERIODIC, TRANSMISSIVE, REFLECTIVE, INFLOW = 0, 1, 2, 3
 RUSANOV, OSHER = 0, 1
 K_WENO, K_PRED, K_FLUX, K_UPDATE, K_HALO, K_OTHER, K_COUNT = range(7)
 KERNEL_NAMES = ("weno_reconstruct", "stdg_predictor", "face_flux", "fv_update", "halo", "other")
