@@ -836,8 +836,6 @@ orc_ctx* orc_create(const orc_config* cfg) {
   if (cfg->flux == ORC_FLUX_OSHER && cfg->system != ORC_EULER) return NULL;   /* Osher: Euler only */
   for (int k = 0; k < 2 * cfg->dim; ++k)
     if (cfg->bc[k] == ORC_BC_REFLECTIVE && (cfg->system != ORC_EULER || cfg->n[k / 2] < cfg->degree + 1)) return NULL;
-  for (int k = 0; k < cfg->dim; ++k)
-    if ((cfg->bc[2 * k] == ORC_BC_PERIODIC) != (cfg->bc[2 * k + 1] == ORC_BC_PERIODIC)) return NULL;
   orc_ctx* c = (orc_ctx*)calloc(1, sizeof(orc_ctx));
   c->cfg = *cfg;
   c->d = cfg->dim; c->M = cfg->degree; c->N = c->M + 1;

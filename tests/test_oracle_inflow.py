@@ -39,8 +39,6 @@ def test_riemann_problem_on_the_inflow_boundary(M):
     assert errs[0] < 0.03 and errs[1] < 0.7 * errs[0], errs
 
 
-def test_inflow_rejected_for_amr_and_one_sided_periodic():
+def test_inflow_rejected_for_amr():
     with pytest.raises(ValueError):
         O.AmrOracle(dim=2, degree=2, n=(8, 8), lo=(0, 0), hi=(1, 1), bc=(I, T, P, P, 0, 0), lmax=1)
-    with pytest.raises(ValueError):
-        O.Oracle(dim=2, degree=2, n=(8, 8), lo=(0, 0), hi=(1, 1), bc=(P, I, P, P, 0, 0))
