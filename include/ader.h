@@ -44,7 +44,9 @@ typedef enum {
 typedef enum { ADER_EULER = 0, ADER_MHD_GLM = 1 } ader_system;
 typedef enum { ADER_BC_PERIODIC = 0,
                ADER_BC_TRANSMISSIVE = 1,   /* reading R5 */
-               ADER_BC_REFLECTIVE = 2      /* reflecting wall, reading R22 (Euler only) */
+               ADER_BC_REFLECTIVE = 2,     /* reflecting wall, reading R22 (Euler only) */
+               ADER_BC_INFLOW = 3          /* Dirichlet inflow: the ghost layer keeps the IC cell
+                                            * averages (reading R23; uniform grids) */
 } ader_bc;
 /* Two-point flux of the space-time face quadrature. */
 typedef enum { ADER_FLUX_RUSANOV = 0,   /* eqn.rusanov @ P:181-185                  */
@@ -160,7 +162,8 @@ ader_status ader_partition(const ader_config* cfg, int32_t rank, ader_partition_
  * send_lo..send_hi, receive into recv_lo..recv_hi; NCCL order per peer: send
  * low, recv high, send high, recv low), 2 periodic wrap onto itself, 3
  * transmissive copy of the nearest owned cell (reading R5), 4 reflective
- * mirror of the owned cells with the normal momentum negated (R22). */
+ * mirror of the owned cells with the normal momentum negated (R22), 5 inflow
+ * (the ghost cells keep their initial values, R23). */
 typedef struct {
   int32_t kind, peer;
   int32_t send_lo[3], send_hi[3];

@@ -163,8 +163,10 @@ ader_status validate(const ader_config* cfg, std::string& why) {
   for (int k = 0; k < cfg->dim; ++k)
     if (!(cfg->hi[k] > cfg->lo[k])) return bad("hi must exceed lo");
   for (int k = 0; k < 2 * cfg->dim; ++k) {
-    if (cfg->bc[k] != ADER_BC_PERIODIC && cfg->bc[k] != ADER_BC_TRANSMISSIVE && cfg->bc[k] != ADER_BC_REFLECTIVE)
+    if (cfg->bc[k] != ADER_BC_PERIODIC && cfg->bc[k] != ADER_BC_TRANSMISSIVE && cfg->bc[k] != ADER_BC_REFLECTIVE &&
+        cfg->bc[k] != ADER_BC_INFLOW)
       return bad("bad bc");
+    if (cfg->bc[k] == ADER_BC_INFLOW && cfg->lmax > 0) return ADER_ERR_UNSUPPORTED;   // R23: uniform grids
     if (cfg->bc[k] == ADER_BC_REFLECTIVE && cfg->system != ADER_EULER) return bad("reflective walls are Euler only");
     if (cfg->bc[k] == ADER_BC_REFLECTIVE && cfg->n0[k / 2] < cfg->degree + 1)
       return bad("a reflective axis needs at least M+1 cells");
@@ -347,7 +349,7 @@ void halo_plan(int d, int H, const int n[3], const int P[3], const ader_partitio
   const int nb = part.nbr[2 * a + side];
   if (nb >= 0 && nb != rank) { o->kind = 1; o->peer = nb; }
   else if (nb >= 0 && bc[2 * a + side] == ADER_BC_PERIODIC) o->kind = 2;
-  else o->kind = bc[2 * a + side] == ADER_BC_REFLECTIVE ? 4 : 3;
+  else o->kind = bc[2 * a + side] == ADER_BC_REFLECTIVE ? 4 : (bc[2 * a + side] == ADER_BC_INFLOW ? 5 : 3);
 }
 
 Box desc_box(const int32_t* lo, const int32_t* hi) { return make_box(lo[0], hi[0], lo[1], hi[1], lo[2], hi[2]); }
@@ -391,8 +393,9 @@ void halo_unpack_local(ader_ctx* c, double* u, int a) {
   if (dh.kind == 1) launch_unpack(c->k, u, rhi, c->recvb[2 * a + 1]);
   // local sides: periodic wrap onto ourselves, or transmissive copy (reading R5)
   auto mode = [](int kind) { return kind == 2 ? 0 : (kind == 4 ? 2 : 1); };
-  if (dl.kind != 1) launch_fill_axis(c->k, u, rlo, a, mode(dl.kind), c->H, c->n[a]);
-  if (dh.kind != 1) launch_fill_axis(c->k, u, rhi, a, mode(dh.kind), c->H, c->n[a]);
+  // (kind 5, inflow: the ghost cells keep their initial values, R23)
+  if (dl.kind != 1 && dl.kind != 5) launch_fill_axis(c->k, u, rlo, a, mode(dl.kind), c->H, c->n[a]);
+  if (dh.kind != 1 && dh.kind != 5) launch_fill_axis(c->k, u, rhi, a, mode(dh.kind), c->H, c->n[a]);
 }
 
 ader_status fill_halo(ader_ctx* c, double* u) {
@@ -626,7 +629,7 @@ ader_status ader_create(const ader_config* cfg, ader_ctx** out) {
   std::string why;
   ader_status st = validate(cfg, why);
   if (st != ADER_OK) {
-    g_create_err = st == ADER_ERR_UNSUPPORTED ? "configuration not supported yet (lmax > 0)" : why;
+    g_create_err = st == ADER_ERR_UNSUPPORTED ? "configuration not supported (inflow boundaries need lmax = 0)" : why;
     return st;
   }
   ader_ctx* c = nullptr;
@@ -823,7 +826,13 @@ ader_status ader_set_initial(ader_ctx* c, ader_ic_fn ic, void* user) {
     for (int k = 0; k < d; ++k) wg *= qw[gi[k]];
     wq[g] = wg;
   }
-  const long long ncells = (long long)c->n[0] * c->n[1] * c->n[2];
+  // IC box: the owned block, grown into the ghost layer on inflow sides (R23)
+  int off[3] = {0, 0, 0}, ext[3] = {c->n[0], c->n[1], c->n[2]};
+  for (int k = 0; k < d; ++k) {
+    if (c->part.nbr[2 * k] < 0 && c->cfg.bc[2 * k] == ADER_BC_INFLOW) { off[k] = -c->H; ext[k] += c->H; }
+    if (c->part.nbr[2 * k + 1] < 0 && c->cfg.bc[2 * k + 1] == ADER_BC_INFLOW) ext[k] += c->H;
+  }
+  const long long ncells = (long long)ext[0] * ext[1] * ext[2];
   const long long chunk = std::max<long long>(1, std::min<long long>(ncells, (1 << 22) / nq));
   std::vector<double> x((size_t)chunk * nq * 3), pr((size_t)chunk * nq * 9);
   double *dprim = nullptr, *dwq = nullptr;
@@ -834,8 +843,8 @@ ader_status ader_set_initial(ader_ctx* c, ader_ic_fn ic, void* user) {
     const long long ncur = std::min(chunk, ncells - c0);
     for (long long i = 0; i < ncur; ++i) {
       const long long lin = c0 + i;
-      const long long ii[3] = {lin % c->n[0] + c->part.lo[0], (lin / c->n[0]) % c->n[1] + c->part.lo[1],
-                               lin / ((long long)c->n[0] * c->n[1]) + c->part.lo[2]};
+      const long long ii[3] = {lin % ext[0] + off[0] + c->part.lo[0], (lin / ext[0]) % ext[1] + off[1] + c->part.lo[1],
+                               lin / ((long long)ext[0] * ext[1]) + off[2] + c->part.lo[2]};
       for (int g = 0; g < nq; ++g) {
         const int gi[3] = {g % Q, (g / Q) % Q, g / (Q * Q)};
         double* xp = &x[(i * nq + g) * 3];
@@ -846,7 +855,7 @@ ader_status ader_set_initial(ader_ctx* c, ader_ic_fn ic, void* user) {
     std::fill(pr.begin(), pr.begin() + ncur * nq * 9, 0.0);
     ic(x.data(), ncur * nq, pr.data(), user);
     CK(cudaMemcpyAsync(dprim, pr.data(), (size_t)ncur * nq * 9 * sizeof(double), cudaMemcpyHostToDevice, c->k.stream));
-    launch_ic_average(c->k, c->u, dprim, dwq, nq, c0, ncur, c->n, c->H);
+    launch_ic_average(c->k, c->u, dprim, dwq, nq, c0, ncur, ext, c->H, off);
     CK(cudaStreamSynchronize(c->k.stream));
   }
   cudaFree(dprim);

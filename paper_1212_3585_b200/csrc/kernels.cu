@@ -616,7 +616,8 @@ __global__ void k_pack(const double* __restrict__ src, const Box R, const long l
 template <int D, int SYS>
 __global__ void k_ic_average(double* __restrict__ u, const double* __restrict__ prim, const double* __restrict__ wq,
                              const int nq, const long long first, const long long ncells, const int n0, const int n1,
-                             const int H, const long long sy, const long long sz, const double gamma) {
+                             const int H, const long long sy, const long long sz, const double gamma,
+                             const int o0, const int o1, const int o2) {
   using PH = Phys<SYS, D>;
   constexpr int NV = PH::NV;
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -632,7 +633,7 @@ __global__ void k_ic_average(double* __restrict__ u, const double* __restrict__ 
 #pragma unroll
     for (int v = 0; v < NV; ++v) acc[v] += wq[g] * uu[v];
   }
-  const long long c = (x + H) + (y + H) * sy + (D == 3 ? (z + H) : z) * sz;
+  const long long c = (x + o0 + H) + (y + o1 + H) * sy + (D == 3 ? (z + o2 + H) : z) * sz;
 #pragma unroll
   for (int v = 0; v < NV; ++v) u[c * NV + v] = acc[v];
 }
@@ -856,12 +857,13 @@ void launch_scatter(const KCtx& k, double* dst, int stride, const Box& b, const 
 }
 
 void launch_ic_average(const KCtx& k, double* u, const double* prim, const double* wq, int nq, long long first,
-                       long long ncells, const int n[3], int H) {
+                       long long ncells, const int n[3], int H, const int off[3]) {
   if (ncells == 0) return;
   const unsigned g = grid_for(ncells, 128);
   count_launch(k);
 #define ICA(D_, S_) \
-  k_ic_average<D_, S_><<<g, 128, 0, k.stream>>>(u, prim, wq, nq, first, ncells, n[0], n[1], H, k.sy, k.sz, k.gamma)
+  k_ic_average<D_, S_><<<g, 128, 0, k.stream>>>(u, prim, wq, nq, first, ncells, n[0], n[1], H, k.sy, k.sz, k.gamma, \
+                                                 off[0], off[1], off[2])
   if (k.D == 2 && k.SYS == 0) ICA(2, 0);
   else if (k.D == 3 && k.SYS == 0) ICA(3, 0);
   else if (k.D == 2 && k.SYS == 1) ICA(2, 1);

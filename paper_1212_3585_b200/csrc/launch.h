@@ -101,8 +101,10 @@ void launch_pack(const KCtx& k, const double* u, const Box& b, double* buf);
 void launch_unpack(const KCtx& k, double* u, const Box& b, const double* buf);
 // IC cell averages: prim[cell][nq][9] at the GL points of `ncells` consecutive
 // owned cells starting at owned linear index first; weights wq[nq].
+// IC cell averages of the box of extents n[] starting at the owned-block offset
+// off[] (<= 0: into the ghost layer, inflow sides), cells x fastest.
 void launch_ic_average(const KCtx& k, double* u, const double* prim, const double* wq, int nq,
-                       long long first, long long ncells, const int n[3], int H);
+                       long long first, long long ncells, const int n[3], int H, const int off[3]);
 // Owned cells <-> compact [cell][stride] buffers (x fastest within the block).
 void launch_gather(const KCtx& k, const double* src, int stride, const Box& b, double* out);
 void launch_scatter(const KCtx& k, double* dst, int stride, const Box& b, const double* in);

@@ -41,6 +41,8 @@ CASES = {
                                    bc=(0,) * 6, system=1, gamma=5 / 3, ch=2.0), W.orszag_tang(), 2, 4),
     "box2d_walls_x4": (dict(dim=2, degree=2, n0=(20, 18), lo=(0, 0), hi=(1, 1), bc=(2,) * 6, cfl=0.45),
                        W.random_smooth(2, seed=3585, amp=0.2), 4, 5),
+    "inflow3d_x4": (dict(dim=3, degree=2, n0=(12, 10, 9), lo=(0,) * 3, hi=(1,) * 3, bc=(3, 1, 0, 0, 3, 1), cfl=0.3),
+                    W.random_smooth(3, seed=1212, amp=0.08), 4, 3),
 }
 
 

@@ -69,6 +69,11 @@ CASES = {
                                         ic=W.random_smooth(2, seed=1212, amp=0.15), cfl=0.45),
     "box3d_M2_reflective_osher": dict(dim=3, degree=2, n=(7, 6, 8), lo=(0,) * 3, hi=(1,) * 3, bc=(2,) * 6,
                                       ic=W.random_smooth(3, seed=3585, amp=0.1), cfl=0.3, flux=1),
+    # Dirichlet inflow (reading R23): a Riemann problem on the inflow boundary
+    "inflow_riemann_2d_M2": dict(dim=2, degree=2, n=(30, 5), lo=(0, 0), hi=(1, 1.0 / 6), bc=(3, 1, 0, 0, 0, 0),
+                                 ic=W.shock_tube(0, 0.0, left=(1.0, 0.75, 1.0), right=(0.125, 0.0, 0.1)), cfl=0.5),
+    "inflow_3d_M2": dict(dim=3, degree=2, n=(9, 6, 7), lo=(0,) * 3, hi=(1,) * 3, bc=(3, 1, 0, 0, 3, 1),
+                         ic=W.random_smooth(3, seed=1212, amp=0.08), cfl=0.3),
 }
 
 
@@ -171,6 +176,15 @@ def test_closed_box_50_steps_parity_and_conservation():
     assert rel_err(ug, o.get_cells()) <= 1e-8
     for v in (0, 3):
         assert abs(ug[:, v].sum() - u0[:, v].sum()) <= 1e-11 * np.abs(u0[:, v]).sum()
+
+
+def test_inflow_riemann_problem_to_final_time():
+    WL, WR = (1.0, 0.75, 1.0), (0.125, 0.0, 0.1)
+    g, o = pair(2, 3, (40, 2), (0, 0), (1, 0.05), (3, 1, 0, 0, 0, 0), W.shock_tube(0, 0.0, left=WL, right=WR), cfl=0.5)
+    rg = g.step(0.2, 10 ** 6)
+    ro = o.step(0.2, 10 ** 6)
+    assert rg.macro_steps == ro.steps
+    assert rel_err(g.get_state(), o.get_cells()) <= 1e-8
 
 
 def test_constant_state_bitwise():
