@@ -341,7 +341,12 @@ void halo_plan(int d, int H, const int n[3], const int P[3], const ader_partitio
   for (int b = 0; b < 3; ++b) {
     if (b >= d) { lo[b] = 0; hi[b] = 1; continue; }
     if (b < a) { lo[b] = 0; hi[b] = P[b]; }      // processed axes: full padded extent
-    else { lo[b] = H; hi[b] = H + n[b]; }        // unprocessed axes: owned extent
+    else {                                       // unprocessed axes: owned extent, plus the
+      lo[b] = H;                                 // inflow ghost layers (set at initialisation,
+      hi[b] = H + n[b];                          // R23) so that their edges are filled too
+      if (b != a && part.nbr[2 * b] < 0 && bc[2 * b] == ADER_BC_INFLOW) lo[b] = 0;
+      if (b != a && part.nbr[2 * b + 1] < 0 && bc[2 * b + 1] == ADER_BC_INFLOW) hi[b] = P[b];
+    }
   }
   for (int b = 0; b < 3; ++b) { o->send_lo[b] = o->recv_lo[b] = lo[b]; o->send_hi[b] = o->recv_hi[b] = hi[b]; }
   if (side == 0) { o->recv_lo[a] = 0; o->recv_hi[a] = H; o->send_lo[a] = H; o->send_hi[a] = 2 * H; }
