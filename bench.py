@@ -53,6 +53,8 @@ def parse():
     p.add_argument("--cpu-box", type=int, default=12, help="edge of the oracle sample box (cells)")
     p.add_argument("--flux", default="rusanov", choices=["rusanov", "osher"],
                    help="two-point flux (BASELINE: rusanov; the paper's explosions use osher)")
+    p.add_argument("--load-balance", type=int, default=1, choices=[0, 1],
+                   help="AMR at N>1: re-cut the level-0 blocks after every adapt (reading R24)")
     return p.parse_args()
 
 
@@ -244,7 +246,8 @@ def main():
     cfg = ader.make_config(dim=wl.dim, degree=wl.degree, n0=wl.n, lo=wl.lo, hi=wl.hi, bc=wl.bc, system=wl.system,
                            gamma=wl.gamma, ch=wl.ch, cfl=wl.cfl, rank=rank, world_size=world, device=local,
                            nccl_id=nid, lmax=wl.lmax, refine_factor=wl.refine_factor, adapt_every=1,
-                           chi_ref=wl.chi_ref, chi_rec=wl.chi_rec, flux=1 if args.flux == "osher" else 0)
+                           chi_ref=wl.chi_ref, chi_rec=wl.chi_rec, flux=1 if args.flux == "osher" else 0,
+                           load_balance=1 if (wl.lmax > 0 and world > 1 and args.load_balance) else 0)
     s = ader.Solver(cfg)
     stream = torch.cuda.current_stream()
     s.set_stream(stream.cuda_stream)
@@ -395,7 +398,7 @@ def main():
             "config": {"workload": wl.name, "dim": wl.dim, "degree": wl.degree, "order": wl.degree + 1,
                        "cells": list(wl.n), "system": "euler" if wl.system == 0 else "mhd_glm",
                        "flux": args.flux, "cfl": wl.cfl, "ic": "explosion r<0.5" if "explosion" in wl.name else wl.name,
-                       "parallelism": f"level-0 blocks x{world}", "l2": "inputs larger than L2 (~90 GB working set)"},
+                       "parallelism": f"level-0 blocks x{world}" + (" (dynamic RCB)" if cfg.load_balance else ""), "l2": "inputs larger than L2 (~90 GB working set)"},
             "roofline": dominant,
             "roofline_kernels": [r for r in (roof, roof_flux) if r is not None],
             "kernel_share_of_step": share,

@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define ADER_ABI_VERSION 2
+#define ADER_ABI_VERSION 3
 
 typedef struct ader_ctx ader_ctx;   /* opaque; owns all device memory it allocates */
 
@@ -79,6 +79,12 @@ typedef struct {
   int32_t flux;                 /* ader_flux; ADER_FLUX_OSHER needs system=EULER   */
   int32_t flux_quad;            /* Gauss-Legendre points of the Osher path integral
                                  * ("at least two"), 1..4; 0 = 3 (R21)   */
+  int32_t load_balance;         /* AMR, world_size > 1: 0 = static Cartesian blocks
+                                 * (ader_partition); 1 = dynamic: after every adapt the
+                                 * level-0 cells are re-cut by ader_rcb_partition on
+                                 * their subtrees' local steps when that lowers the
+                                 * imbalance (reading R24; the paper's future work,
+                                 * P:809-810)                                       */
 } ader_config;
 
 /* Batched IC callback (host): x[n][3] -> prim[n][9] with
@@ -92,7 +98,7 @@ typedef struct {
   int64_t updates_per_level[8];
   int64_t pred_sweeps_total;      /* Picard sweeps summed over predicted cells     */
   int32_t pred_sweeps_max;
-  int32_t pad_;
+  int32_t rebalances;             /* dynamic load-balancing repartitions (R24)     */
   int64_t pred_cells;             /* cells run through the predictor (incl. halo)  */
   double  cons_total[9];          /* sum of u * cell volume over owned active cells*/
   double  wall_s;
@@ -170,6 +176,18 @@ typedef struct {
   int32_t recv_lo[3], recv_hi[3];
 } ader_halo_desc;
 ader_status ader_halo_plan(const ader_config* cfg, int32_t rank, int32_t axis, int32_t side, ader_halo_desc* out);
+/* Dynamic load balancing of the AMR level-0 cells (reading R24; host only).
+ * Recursive coordinate bisection: the box is cut across its longest axis
+ * (lowest axis on ties) at the plane that brings the lower part's weight
+ * closest to floor(np/2)/np of the box total (first such plane), leaving at
+ * least as many planes as ranks on each side, and both halves recurse; rank
+ * p0.. takes the lower part.  weights[n0[0]*n0[1]*n0[2]] (x fastest) are the
+ * per-level-0-cell costs (the solver uses sum over active subtree cells of
+ * r^level, i.e. local steps per macro step); boxes[world][6] receives lo[3],
+ * hi[3] per rank.  ADER_ERR_ARG if an axis is too short to give every rank a
+ * plane, or on bad arguments. */
+ader_status ader_rcb_partition(int32_t dim, const int32_t n0[3], const int64_t* weights, int32_t world,
+                               int32_t* boxes);
 /* 128-byte ncclUniqueId for rank 0 to broadcast (loads libnccl.so.2 lazily). */
 ader_status ader_nccl_unique_id(uint8_t out[128]);
 

@@ -15,7 +15,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libader_b200.so")
 _LIB = None
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 EULER, MHD_GLM = 0, 1
 PERIODIC, TRANSMISSIVE, REFLECTIVE, INFLOW = 0, 1, 2, 3
 RUSANOV, OSHER = 0, 1
@@ -39,7 +39,7 @@ class AderConfig(C.Structure):
         ("ic_quad", C.c_int32), ("adapt_every", C.c_int32),
         ("rank", C.c_int32), ("world_size", C.c_int32), ("device", C.c_int32),
         ("nccl_id", C.c_uint8 * 128),
-        ("flux", C.c_int32), ("flux_quad", C.c_int32),
+        ("flux", C.c_int32), ("flux_quad", C.c_int32), ("load_balance", C.c_int32),
     ]
 
 
@@ -47,7 +47,7 @@ class AderStepReport(C.Structure):
     _fields_ = [
         ("t", C.c_double), ("dt0", C.c_double),
         ("macro_steps", C.c_int64), ("cell_updates", C.c_int64), ("updates_per_level", C.c_int64 * 8),
-        ("pred_sweeps_total", C.c_int64), ("pred_sweeps_max", C.c_int32), ("pad_", C.c_int32),
+        ("pred_sweeps_total", C.c_int64), ("pred_sweeps_max", C.c_int32), ("rebalances", C.c_int32),
         ("pred_cells", C.c_int64), ("cons_total", C.c_double * 9), ("wall_s", C.c_double),
     ]
 
@@ -115,7 +115,7 @@ EXPORTED = ("ader_create", "ader_destroy", "ader_last_error", "ader_set_stream",
             "ader_set_cells", "ader_get_state", "ader_get_cells", "ader_time", "ader_step", "ader_refine",
             "ader_partition", "ader_halo_plan", "ader_nccl_unique_id", "ader_set_profiling", "ader_kernel_stats",
             "ader_launch_count", "ader_debug_dump", "ader_sizeof", "ader_debug_group_create",
-            "ader_debug_group_set_initial", "ader_debug_group_step")
+            "ader_debug_group_set_initial", "ader_debug_group_step", "ader_rcb_partition")
 
 
 def _dp(a):
@@ -125,7 +125,7 @@ def _dp(a):
 def make_config(*, dim, degree, n0, lo, hi, bc, system=EULER, gamma=1.4, ch=0.0, cfl=0.9,
                 refine_factor=3, lmax=0, chi_ref=0.2, chi_rec=0.1, chi_eps=0.01, pred_tol=1e-13,
                 pred_max_sweeps=32, ic_quad=0, adapt_every=1, rank=0, world_size=1, device=-1,
-                nccl_id=None, flux=RUSANOV, flux_quad=0) -> AderConfig:
+                nccl_id=None, flux=RUSANOV, flux_quad=0, load_balance=0) -> AderConfig:
     cfg = AderConfig()
     cfg.abi_version = ABI_VERSION
     cfg.dim, cfg.system, cfg.degree = dim, system, degree
@@ -143,7 +143,7 @@ def make_config(*, dim, degree, n0, lo, hi, bc, system=EULER, gamma=1.4, ch=0.0,
     cfg.pred_tol, cfg.pred_max_sweeps = pred_tol, pred_max_sweeps
     cfg.ic_quad, cfg.adapt_every = ic_quad, adapt_every
     cfg.rank, cfg.world_size, cfg.device = rank, world_size, device
-    cfg.flux, cfg.flux_quad = flux, flux_quad
+    cfg.flux, cfg.flux_quad, cfg.load_balance = flux, flux_quad, load_balance
     if nccl_id is not None:
         for i, b in enumerate(bytes(nccl_id)[:128]):
             cfg.nccl_id[i] = b
@@ -156,6 +156,21 @@ def ader_partition(cfg: AderConfig, rank: int) -> AderPartitionInfo:
     if st:
         raise AderError(st, "ader_partition rejected the configuration")
     return info
+
+
+def ader_rcb_partition(dim: int, n0, weights, world: int):
+    """Level-0 blocks of the dynamic load balancing (ader.h: ader_rcb_partition):
+    weights[z][y][x] (x fastest in memory) -> [(lo[3], hi[3])] per rank."""
+    import numpy as np
+    n = list(n0) + [1] * (3 - len(n0))
+    w = np.ascontiguousarray(weights, dtype=np.int64).reshape(-1)
+    if w.size != n[0] * n[1] * n[2]:
+        raise ValueError("weights must have n0[0]*n0[1]*n0[2] entries")
+    boxes = (C.c_int32 * (6 * world))()
+    st = lib().ader_rcb_partition(dim, (C.c_int32 * 3)(*n), w.ctypes.data_as(C.POINTER(C.c_int64)), world, boxes)
+    if st:
+        raise AderError(st, "ader_rcb_partition rejected the arguments")
+    return [(tuple(boxes[6 * p:6 * p + 3]), tuple(boxes[6 * p + 3:6 * p + 6])) for p in range(world)]
 
 
 def ader_halo_plan(cfg: AderConfig, rank: int, axis: int, side: int) -> AderHaloDesc:

@@ -187,6 +187,7 @@ ader_status validate(const ader_config* cfg, std::string& why) {
   if (cfg->flux != ADER_FLUX_RUSANOV && cfg->flux != ADER_FLUX_OSHER) return bad("unknown flux");
   if (cfg->flux == ADER_FLUX_OSHER && cfg->system != ADER_EULER) return bad("the Osher flux is implemented for Euler only");
   if (cfg->flux_quad < 0 || cfg->flux_quad > 4) return bad("flux_quad must be in 0..4");
+  if (cfg->load_balance < 0 || cfg->load_balance > 1) return bad("load_balance must be 0 or 1");
   (void)b;
   return ADER_OK;
 }
@@ -598,6 +599,27 @@ ader_status ader_partition(const ader_config* cfg, int32_t rank, ader_partition_
   if (st != ADER_OK) return st;
   if (rank < 0 || rank >= cfg->world_size) return ADER_ERR_ARG;
   partition(cfg, rank, out);
+  return ADER_OK;
+}
+
+ader_status ader_rcb_partition(int32_t dim, const int32_t n0[3], const int64_t* weights, int32_t world,
+                               int32_t* boxes) {
+  if (!n0 || !weights || !boxes || dim < 1 || dim > 3 || world < 1 || world > 8) return ADER_ERR_ARG;
+  long long n[3];
+  for (int k = 0; k < 3; ++k) {
+    n[k] = k < dim ? n0[k] : 1;
+    if (n[k] < 1) return ADER_ERR_ARG;
+  }
+  const long long tot = n[0] * n[1] * n[2];
+  std::vector<long long> w((size_t)tot);
+  for (long long i = 0; i < tot; ++i) {
+    if (weights[i] < 0) return ADER_ERR_ARG;
+    w[(size_t)i] = weights[i];
+  }
+  int lo[8][3], hi[8][3];
+  if (!rcb_partition(dim, n, w.data(), world, lo, hi)) return ADER_ERR_ARG;
+  for (int p = 0; p < world; ++p)
+    for (int k = 0; k < 3; ++k) { boxes[6 * p + k] = lo[p][k]; boxes[6 * p + 3 + k] = hi[p][k]; }
   return ADER_OK;
 }
 

@@ -93,6 +93,7 @@ struct AmrState {
   double tm_a[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // adapt_apply sub-phases
   double tm_u[4] = {0, 0, 0, 0};                // upload_topology: capacity, host scans, staging
   long long tm_steps = 0;
+  int nrebal = 0;                               // dynamic load-balancing repartitions (R24)
 };
 
 namespace {
@@ -882,6 +883,123 @@ ader_status adapt_apply(AmrState* A, bool t0, const std::vector<double>& chi, st
   return ADER_OK;
 }
 
+// ---- dynamic load balancing (reading R24) ----------
+// cost of a level-0 cell: local steps per macro step of its active subtree
+// cells (sum of r^level); identical on every rank (the tree is replicated)
+std::vector<long long> level0_weights(const AmrState* A) {
+  std::vector<long long> w((size_t)(A->n[0][0] * A->n[0][1] * A->n[0][2]), 0);
+  long long rl[kAmrMaxLevels];
+  rl[0] = 1;
+  for (int l = 1; l < kAmrMaxLevels; ++l) rl[l] = rl[l - 1] * A->r;
+  for (const HCell& C : A->cells) {
+    if (!C.alive || C.status != 0) continue;
+    long long a0[3];
+    ancestor0(A, C, a0);
+    w[(size_t)lin(A, 0, a0)] += rl[C.level];
+  }
+  return w;
+}
+
+// max over ranks of the rank's cost, over the mean
+double imbalance(const AmrState* A, const AmrRanks& R, const std::vector<long long>& w) {
+  long long tot = 0, mx = 0;
+  for (int p = 0; p < R.world; ++p) {
+    long long s = 0;
+    for (long long z = R.lo[p][2]; z < R.hi[p][2]; ++z)
+      for (long long y = R.lo[p][1]; y < R.hi[p][1]; ++y)
+        for (long long x = R.lo[p][0]; x < R.hi[p][0]; ++x) s += w[(size_t)((z * A->n[0][1] + y) * A->n[0][0] + x)];
+    tot += s;
+    mx = std::max(mx, s);
+  }
+  return tot > 0 ? (double)mx * R.world / (double)tot : 1.0;
+}
+
+// Re-cut the level-0 blocks when that lowers the imbalance by more than 2 %
+// (and the current one exceeds 5 %).  At synchronized time the only state of
+// a cell is its average (the flux memory is cleared, WENO / predictor dofs are
+// recomputed every step), so the move is: every rank contributes the averages
+// of the cells it owns under the old blocks to a zeroed per-id array, one sum
+// over the ranks (exact: a single non-zero term per entry) gives every rank
+// all averages, the ownership / compute sets / exchange plans are rebuilt for
+// the new blocks and each rank copies the rows of its new compute set.
+ader_status rebalance(const Group& G, std::string& err) {
+  AmrState* A0 = G[0];
+  const int W = A0->ranks.world;
+  if (W <= 1 || A0->cfg.load_balance != 1) return ADER_OK;
+  const std::vector<long long> w = level0_weights(A0);
+  AmrRanks nr = A0->ranks;
+  if (!rcb_partition(A0->d, A0->n[0], w.data(), W, nr.lo, nr.hi)) return ADER_OK;
+  const double cur = imbalance(A0, A0->ranks, w), nxt = imbalance(A0, nr, w);
+  if (!(cur > 1.05 && nxt * 1.02 < cur)) return ADER_OK;
+  const size_t nu = A0->cells.size(), nv = (size_t)A0->nv;
+  std::vector<double*> buf(G.size(), nullptr), tmp(G.size(), nullptr);
+  ader_status s = ADER_OK;
+  auto cleanup = [&]() {
+    for (AmrState* A : G) cudaStreamSynchronize(A->k->stream);
+    for (size_t g = 0; g < G.size(); ++g) { cudaFree(buf[g]); cudaFree(tmp[g]); }
+  };
+  auto ids_of = [&](const AmrState* A, const std::vector<char>& mask) {
+    std::vector<int> ids;
+    for (size_t i = 0; i < nu; ++i)
+      if (A->cells[i].alive && mask[i]) ids.push_back((int)i);
+    return ids;
+  };
+  // 1. owners' rows (old blocks) into zeroed per-id arrays
+  for (size_t g = 0; g < G.size() && s == ADER_OK; ++g) {
+    AmrState* A = G[g];
+    cudaStream_t sm = A->k->stream;
+    if (cudaMalloc(&buf[g], sizeof(double) * nu * nv) != cudaSuccess ||
+        cudaMalloc(&tmp[g], sizeof(double) * nu * nv) != cudaSuccess) { err = "cudaMalloc (rebalance)"; s = ADER_ERR_CUDA; break; }
+    cudaMemsetAsync(buf[g], 0, sizeof(double) * nu * nv, sm);
+    const std::vector<int> ids = ids_of(A, A->own);
+    Uploader up{A, {}};
+    const size_t oi = up.add(ids.data(), sizeof(int) * ids.size());
+    s = up.run(err);
+    if (s != ADER_OK) break;
+    const int* dids = (const int*)(A->dscratch + oi);
+    amr_launch_rows_gather(*A->k, A->V.u, dids, (int)ids.size(), A->nv, tmp[g]);
+    amr_launch_rows_scatter(*A->k, buf[g], dids, (int)ids.size(), A->nv, tmp[g]);
+  }
+  // 2. sum over the ranks
+  if (s == ADER_OK && G.size() == 1) {
+    s = A0->comm.sum(A0->comm.ctx, buf[0], nu * nv, A0->k->stream);
+    if (s != ADER_OK) err = "allreduce(sum) of the migrated averages failed";
+  } else if (s == ADER_OK) {
+    std::vector<double> tot(nu * nv, 0.0), part(nu * nv);
+    for (size_t g = 0; g < G.size() && s == ADER_OK; ++g) {
+      cudaStream_t sm = G[g]->k->stream;
+      if (cudaMemcpyAsync(part.data(), buf[g], sizeof(double) * nu * nv, cudaMemcpyDeviceToHost, sm) != cudaSuccess ||
+          cudaStreamSynchronize(sm) != cudaSuccess) { err = "rebalance download"; s = ADER_ERR_CUDA; break; }
+      for (size_t i = 0; i < tot.size(); ++i) tot[i] += part[i];
+    }
+    for (size_t g = 0; g < G.size() && s == ADER_OK; ++g) {
+      cudaStream_t sm = G[g]->k->stream;
+      if (cudaMemcpyAsync(buf[g], tot.data(), sizeof(double) * nu * nv, cudaMemcpyHostToDevice, sm) != cudaSuccess ||
+          cudaStreamSynchronize(sm) != cudaSuccess) { err = "rebalance upload"; s = ADER_ERR_CUDA; break; }
+    }
+  }
+  // 3. new blocks: ownership, compute sets, lists, exchange plans; then the
+  //    rows of the new compute set
+  for (size_t g = 0; g < G.size() && s == ADER_OK; ++g) {
+    AmrState* A = G[g];
+    for (int p = 0; p < W; ++p)
+      for (int k = 0; k < 3; ++k) { A->ranks.lo[p][k] = nr.lo[p][k]; A->ranks.hi[p][k] = nr.hi[p][k]; }
+    s = upload_topology(A, err);
+    if (s != ADER_OK) break;
+    const std::vector<int> ids = ids_of(A, A->comp);
+    Uploader up{A, {}};
+    const size_t oi = up.add(ids.data(), sizeof(int) * ids.size());
+    s = up.run(err);
+    if (s != ADER_OK) break;
+    const int* dids = (const int*)(A->dscratch + oi);
+    amr_launch_rows_gather(*A->k, buf[g], dids, (int)ids.size(), A->nv, tmp[g]);
+    amr_launch_rows_scatter(*A->k, A->V.u, dids, (int)ids.size(), A->nv, tmp[g]);
+    A->nrebal++;
+  }
+  cleanup();
+  return s;
+}
+
 // One adapt pass of every rank of the group on the global indicator.
 ader_status adapt(const Group& G, bool t0, std::string& err) {
   std::vector<double> chi, mine;
@@ -916,12 +1034,57 @@ ader_status adapt(const Group& G, bool t0, std::string& err) {
   }
   for (AmrState* A : G) ACK(cudaStreamSynchronize(A->k->stream));
   A0->tm_exch += now_s() - w0;
-  return ADER_OK;
+  return rebalance(G, err);
 }
 
 }  // namespace
 
 // ===========================================================================
+namespace {
+bool rcb_box(int d, const long long n0[3], const long long* w, const int blo[3], const int bhi[3], int p0, int np,
+             int lo[][3], int hi[][3]) {
+  if (np == 1) {
+    for (int k = 0; k < 3; ++k) { lo[p0][k] = blo[k]; hi[p0][k] = bhi[k]; }
+    return true;
+  }
+  int ax = 0;
+  for (int k = 1; k < d; ++k)
+    if (bhi[k] - blo[k] > bhi[ax] - blo[ax]) ax = k;
+  const int n1 = np / 2, n2 = np - n1, ext = bhi[ax] - blo[ax];
+  if (ext < np) return false;
+  std::vector<long long> plane((size_t)ext, 0);
+  long long tot = 0;
+  for (long long z = blo[2]; z < bhi[2]; ++z)
+    for (long long y = blo[1]; y < bhi[1]; ++y)
+      for (long long x = blo[0]; x < bhi[0]; ++x) {
+        const long long c[3] = {x, y, z};
+        const long long v = w[(size_t)((z * n0[1] + y) * n0[0] + x)];
+        plane[(size_t)(c[ax] - blo[ax])] += v;
+        tot += v;
+      }
+  int cut = -1;
+  long long best = 0, acc = 0;
+  for (int c = blo[ax] + 1; c < bhi[ax]; ++c) {
+    acc += plane[(size_t)(c - 1 - blo[ax])];
+    if (c - blo[ax] < n1 || bhi[ax] - c < n2) continue;
+    const long long dev = std::llabs(acc * np - tot * n1);
+    if (cut < 0 || dev < best) { cut = c; best = dev; }
+  }
+  int lhi[3] = {bhi[0], bhi[1], bhi[2]}, ulo[3] = {blo[0], blo[1], blo[2]};
+  lhi[ax] = cut;
+  ulo[ax] = cut;
+  return rcb_box(d, n0, w, blo, lhi, p0, n1, lo, hi) && rcb_box(d, n0, w, ulo, bhi, p0 + n1, n2, lo, hi);
+}
+}  // namespace
+
+bool rcb_partition(int d, const long long n0[3], const long long* w, int world, int lo[][3], int hi[][3]) {
+  const int blo[3] = {0, 0, 0};
+  const int bhi[3] = {(int)n0[0], d >= 2 ? (int)n0[1] : 1, d >= 3 ? (int)n0[2] : 1};
+  return world >= 1 && rcb_box(d, n0, w, blo, bhi, 0, world, lo, hi);
+}
+
+int amr_rebalances(const AmrState* A) { return A->nrebal; }
+
 AmrState* amr_create(const ader_config* cfg, KCtx* k, DevCounters* cnt, DevCounters* hcnt, const AmrRanks& ranks,
                      const AmrComm& comm, std::string& err) {
   AmrState* A = new AmrState();
@@ -1032,6 +1195,7 @@ ader_status step(const Group& G, double t_end, int64_t max_steps, ader_step_repo
   const size_t n = G.size();
   std::vector<ader_step_report> R(n);
   std::vector<unsigned long long> sw0(n), pc0(n);
+  std::vector<int> rb0(n);
   for (size_t i = 0; i < n; ++i) {
     AmrState* A = G[i];
     std::memset(&R[i], 0, sizeof(R[i]));
@@ -1039,6 +1203,7 @@ ader_status step(const Group& G, double t_end, int64_t max_steps, ader_step_repo
     ACK(cudaMemcpyAsync(A->hcnt, A->cnt, sizeof(DevCounters), cudaMemcpyDeviceToHost, A->k->stream));
     ACK(cudaStreamSynchronize(A->k->stream));
     sw0[i] = A->hcnt->sweeps; pc0[i] = A->hcnt->cells;
+    rb0[i] = A->nrebal;
   }
   ader_status s = ADER_OK;
   AmrState* A0 = G[0];
@@ -1080,6 +1245,7 @@ ader_status step(const Group& G, double t_end, int64_t max_steps, ader_step_repo
     R[i].pred_sweeps_total = (int64_t)(A->hcnt->sweeps - sw0[i]);
     R[i].pred_cells = (int64_t)(A->hcnt->cells - pc0[i]);
     R[i].pred_sweeps_max = A->hcnt->sweeps_max;
+    R[i].rebalances = A->nrebal - rb0[i];
     if (reps) reps[i] = R[i];
   }
   return s;

@@ -71,12 +71,18 @@ struct AmrRanks {
   int lo[8][3]{}, hi[8][3]{};   // level-0 block [lo, hi) of every rank
 };
 
+// Recursive coordinate bisection of the level-0 cells (reading R24, the
+// algorithm of ader_rcb_partition in ader.h): w[n0 x * y * z] >= 0, boxes into
+// lo/hi[world].  False if some box cannot give each of its ranks a plane.
+bool rcb_partition(int d, const long long n0[3], const long long* w, int world, int lo[][3], int hi[][3]);
+
 AmrState* amr_create(const ader_config* cfg, KCtx* k, DevCounters* cnt, DevCounters* hcnt, const AmrRanks& ranks,
                      const AmrComm& comm, std::string& err);
 void amr_destroy(AmrState* a);
 ader_status amr_set_initial(AmrState* a, ader_ic_fn ic, void* user, std::string& err);
 ader_status amr_step(AmrState* a, double t_end, int64_t max_steps, ader_step_report* rep, std::string& err);
 ader_status amr_adapt(AmrState* a, std::string& err);
+int amr_rebalances(const AmrState* a);   // repartitions so far (dynamic load balancing)
 // lockstep variants over the ranks of a loopback group (one process, one GPU)
 ader_status amr_group_set_initial(AmrState* const* g, int n, ader_ic_fn ic, void* user, std::string& err);
 ader_status amr_group_step(AmrState* const* g, int n, double t_end, int64_t max_steps, ader_step_report* reps,

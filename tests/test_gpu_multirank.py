@@ -128,3 +128,47 @@ def test_amr_partition_reproduces_one_rank_bitwise(name):
     assert not bad, bad[:3]                            # averages bit for bit
     grp.close()
     one.close()
+
+
+# Dynamic load balancing (reading R24): after every adapt the level-0 blocks
+# are re-cut by recursive coordinate bisection on the subtrees' local steps and
+# the averages move to their new owners.  The partition must still reproduce
+# one rank bit for bit, and the owned local steps must end up more even than
+# with the static blocks (the blast sits in one corner / one end).
+LB_CASES = {
+    "quadrant_walls_l2_x4": (dict(dim=2, degree=2, n0=(24, 24), lo=(0, 0), hi=(1, 1), bc=(2, 1, 2, 1, 0, 0), lmax=2,
+                                  cfl=0.45, chi_ref=0.1, chi_rec=0.05), W.explosion(2), 4, 5),
+    "offcentre_l1_x3": (dict(dim=2, degree=2, n0=(48, 16), lo=(-1, -1), hi=(5, 1), bc=(1,) * 6, lmax=1, cfl=0.45,
+                             chi_ref=0.1, chi_rec=0.05), W.explosion(2), 3, 4),
+    "offcentre3d_l1_x2": (dict(dim=3, degree=2, n0=(20, 8, 8), lo=(-1, -1, -1), hi=(4, 1, 1), bc=(1,) * 6, lmax=1,
+                               cfl=0.3), W.explosion(3), 2, 2),
+}
+
+
+@pytest.mark.parametrize("name", list(LB_CASES))
+def test_dynamic_load_balance_keeps_bitwise_parity_and_evens_the_load(name):
+    kw, ic, nr, steps = LB_CASES[name]
+    nv = kw["dim"] + 2
+    one = ader.Solver(ader.make_config(device=0, adapt_every=1, **kw))
+    one.set_initial(ic)
+    r1 = one.step(1e300, steps)
+    a = _key_sorted(one.get_cells(), nv)
+    one.close()
+    imb = {}
+    for lb in (0, 1):
+        grp = ader.LoopbackGroup(ader.make_config(device=0, adapt_every=1, load_balance=lb, **kw), nr)
+        grp.set_initial(ic)
+        reps = grp.step(1e300, steps)
+        assert all(r.dt0 == r1.dt0 for r in reps)
+        assert sum(r.cell_updates for r in reps) == r1.cell_updates
+        b = _key_sorted(grp.get_cells(), nv)
+        assert len(a) == len(b)
+        bad = [(x, y) for x, y in zip(a, b) if x != y]
+        assert not bad, (lb, bad[:3])
+        loads = [r.cell_updates for r in reps]
+        imb[lb] = max(loads) * nr / sum(loads)
+        if lb == 0:
+            assert all(r.rebalances == 0 for r in reps)
+        grp.close()
+    print(f"{name}: owned local-step imbalance static {imb[0]:.3f} -> dynamic {imb[1]:.3f}")
+    assert imb[1] < imb[0] and imb[1] < 1.3, imb
