@@ -46,8 +46,10 @@ struct AmrState {
   int* dlist = nullptr;
   long long dlist_cap = 0;
   // lists (host) and their offsets inside dlist
-  std::vector<int> lact[kAmrMaxLevels], lvch[kAmrMaxLevels], lvmo[kAmrMaxLevels], lall;
-  long long oact[kAmrMaxLevels]{}, ovch[kAmrMaxLevels]{}, ovmo[kAmrMaxLevels]{}, oall = 0;
+  // (dlist: the active lists of all levels first, so that their concatenation
+  // is the all-levels active list at oall = 0; one rank: owned = active)
+  std::vector<int> lact[kAmrMaxLevels], lvch[kAmrMaxLevels], lvmo[kAmrMaxLevels];
+  long long oact[kAmrMaxLevels]{}, ovch[kAmrMaxLevels]{}, ovmo[kAmrMaxLevels]{}, oall = 0, nall = 0;
   SubTables st{};
   double t = 0.0;
   ader_ic_fn ic = nullptr;
@@ -69,8 +71,8 @@ struct AmrState {
   int band = 0;                                       // compute-set margin in level-0 cells
   std::vector<char> own, comp;                        // per id
   long long nlev[kAmrMaxLevels]{};                    // alive cells per level (whole tree)
-  std::vector<int> lown[kAmrMaxLevels], lownall;      // owned active cells
-  long long oown[kAmrMaxLevels]{}, oownall = 0;
+  std::vector<int> lown[kAmrMaxLevels];               // owned active cells (multi-rank)
+  long long nown[kAmrMaxLevels]{}, oownall = 0, nownall = 0;
   struct XPlan {                                      // per level, ids ascending per peer
     std::vector<int> sids, rids;
     std::vector<long long> soff, roff;                // [world + 1] offsets into sids / rids
@@ -425,8 +427,6 @@ ader_status upload_topology(AmrState* A, std::string& err) {
     A->lact[l].clear(); A->lvch[l].clear(); A->lvmo[l].clear(); A->lown[l].clear();
     A->xp[l] = AmrState::XPlan();
   }
-  A->lall.clear();
-  A->lownall.clear();
   const int W = A->ranks.world, me = A->ranks.rank;
   A->own.assign(nu, W > 1 ? 0 : 1);
   A->comp.assign(nu, W > 1 ? 0 : 1);
@@ -442,7 +442,6 @@ ader_status upload_topology(AmrState* A, std::string& err) {
       A->nlev[C.level]++;
       (C.status == 0 ? A->lact : (C.status == 1 ? A->lvch : A->lvmo))[C.level].push_back(i);
     }
-    for (int l = 0; l <= A->lmax; ++l) A->lown[l] = A->lact[l];
   }
   for (int i = 0; i < (W > 1 ? nu : 0); ++i) {
     const HCell& C = A->cells[i];
@@ -484,21 +483,35 @@ ader_status upload_topology(AmrState* A, std::string& err) {
       X.roff[W] = (long long)X.rids.size();
       xneed = std::max(xneed, std::max(X.sids.size(), X.rids.size()) * (size_t)A->nv);
     }
+  size_t tot = 0;
+  for (int l = 0; l <= A->lmax; ++l)
+    tot += A->lact[l].size() + A->lvch[l].size() + A->lvmo[l].size() + A->lown[l].size() + A->xp[l].sids.size() +
+           A->xp[l].rids.size();
   std::vector<int> all;
+  all.reserve(tot);
+  A->oall = 0;
   for (int l = 0; l <= A->lmax; ++l) {
     A->oact[l] = (long long)all.size(); all.insert(all.end(), A->lact[l].begin(), A->lact[l].end());
+  }
+  A->nall = (long long)all.size();
+  if (W > 1) {
+    A->oownall = (long long)all.size();
+    for (int l = 0; l <= A->lmax; ++l) {
+      A->nown[l] = (long long)A->lown[l].size();
+      all.insert(all.end(), A->lown[l].begin(), A->lown[l].end());
+    }
+    A->nownall = (long long)all.size() - A->oownall;
+  } else {
+    for (int l = 0; l <= A->lmax; ++l) A->nown[l] = (long long)A->lact[l].size();
+    A->oownall = A->oall;
+    A->nownall = A->nall;
+  }
+  for (int l = 0; l <= A->lmax; ++l) {
     A->ovch[l] = (long long)all.size(); all.insert(all.end(), A->lvch[l].begin(), A->lvch[l].end());
     A->ovmo[l] = (long long)all.size(); all.insert(all.end(), A->lvmo[l].begin(), A->lvmo[l].end());
-    A->oown[l] = (long long)all.size(); all.insert(all.end(), A->lown[l].begin(), A->lown[l].end());
     A->xp[l].dso = (long long)all.size(); all.insert(all.end(), A->xp[l].sids.begin(), A->xp[l].sids.end());
     A->xp[l].dro = (long long)all.size(); all.insert(all.end(), A->xp[l].rids.begin(), A->xp[l].rids.end());
-    A->lall.insert(A->lall.end(), A->lact[l].begin(), A->lact[l].end());
-    A->lownall.insert(A->lownall.end(), A->lown[l].begin(), A->lown[l].end());
   }
-  A->oall = (long long)all.size();
-  all.insert(all.end(), A->lall.begin(), A->lall.end());
-  A->oownall = (long long)all.size();
-  all.insert(all.end(), A->lownall.begin(), A->lownall.end());
   if (xneed > A->xcap) {
     if (A->xsend) { cudaStreamSynchronize(A->k->stream); cudaFree(A->xsend); cudaFree(A->xrecv); }
     A->xcap = xneed * 3 / 2 + 1024;
@@ -620,7 +633,7 @@ ader_status fetch_speed(const Group& G, double* speed, std::string& err) {
     ACK(cudaMemsetAsync(&A->cnt->speed_bits, 0, sizeof(unsigned long long), sm));
     double inv[3] = {0, 0, 0};
     for (int k = 0; k < A->d; ++k) inv[k] = 1.0 / A->dx[0][k];
-    amr_launch_cfl(*A->k, A->V, A->dlist + A->oownall, (int)A->lownall.size(), inv, A->cnt);
+    amr_launch_cfl(*A->k, A->V, A->dlist + A->oownall, (int)A->nownall, inv, A->cnt);
     if (G.size() == 1 && A->ranks.world > 1) {
       ader_status s = A->comm.max_u64(A->comm.ctx, &A->cnt->speed_bits, sm);
       if (s != ADER_OK) { err = "allreduce(max) of the CFL speed failed"; return s; }
@@ -744,7 +757,7 @@ ader_status advance(const Group& G, int l, int m, double dt0, std::string& err) 
   for (AmrState* A : G) {
     const int na = (int)A->lact[l].size();
     { AScope sc(A, ADER_K_FLUX, 0.0); amr_launch_flux_update(*A->k, A->V, A->st, L_act(A, l), na, m, dtdx, A->cnt); }
-    A->updates[l] += (long long)A->lown[l].size();
+    A->updates[l] += A->nown[l];
   }
   AScope sc(A0, ADER_K_HALO, 0.0);
   return exchange(G, l, err);
@@ -763,7 +776,7 @@ ader_status adapt_indicator(AmrState* A, bool t0, std::vector<double>& chi, std:
     for (int l = 1; l <= A->lmax; ++l) amr_launch_project(*A->k, A->V, A->st, L_vch(A, l), (int)A->lvch[l].size(), pt);
   }
   // indicator on all active cells (device), WENO polynomials of all active cells (R18)
-  const int na = (int)A->lall.size();
+  const int na = (int)A->nall;
   amr_launch_indicator(*A->k, A->V, A->dlist + A->oall, na, A->cfg.chi_eps);
   if (!t0)
     for (int l = 0; l <= A->lmax; ++l) amr_launch_weno(*A->k, A->V, L_act(A, l), (int)A->lact[l].size());
@@ -1171,7 +1184,7 @@ void amr_destroy(AmrState* A) {
 
 double amr_time(const AmrState* A) { return A->t; }
 
-int64_t amr_num_active(const AmrState* A) { return (int64_t)A->lall.size(); }
+int64_t amr_num_active(const AmrState* A) { return (int64_t)A->nall; }
 
 namespace {
 ader_status set_initial(const Group& G, ader_ic_fn ic, void* user, std::string& err) {
