@@ -1285,19 +1285,36 @@ ader_status amr_group_step(AmrState* const* g, int n, double t_end, int64_t max_
 }
 
 ader_status amr_get_cells(AmrState* A, ader_cell* out, int64_t cap, int64_t* n, std::string& err) {
+  // this rank's cells per level; in (level, z, y, x) order either by a scan of
+  // the level's dense map or, when the map is much larger than the level's
+  // cell count (deep, sparse levels), by sorting the ids on their map index
+  std::vector<std::vector<int>> per(A->lmax + 1);
+  for (int i = 0; i < (int)A->cells.size(); ++i)
+    if (A->cells[i].alive && A->own[i]) per[A->cells[i].level].push_back(i);
   int64_t cnt = 0;
-  for (int l = 0; l <= A->lmax; ++l)
-    for (int id : A->hmap[l]) cnt += id >= 0 && A->own[id];
+  for (const auto& v : per) cnt += (int64_t)v.size();
   *n = cnt;
   if (!out) return ADER_OK;
   if (cap < cnt) { err = "capacity too small"; return ADER_ERR_ARG; }
   std::vector<double> u(A->cells.size() * A->nv);
   ACK(cudaMemcpyAsync(u.data(), A->V.u, sizeof(double) * u.size(), cudaMemcpyDeviceToHost, A->k->stream));
   ACK(cudaStreamSynchronize(A->k->stream));
+  for (int l = 0; l <= A->lmax; ++l) {
+    std::vector<int>& ids = per[l];
+    if (A->hmap[l].size() > 32 * ids.size()) {
+      std::vector<std::pair<long long, int>> key(ids.size());
+      for (size_t j = 0; j < ids.size(); ++j) key[j] = {lin(A, l, A->cells[ids[j]].idx), ids[j]};
+      std::sort(key.begin(), key.end());
+      for (size_t j = 0; j < ids.size(); ++j) ids[j] = key[j].second;
+    } else {
+      ids.clear();
+      for (int id : A->hmap[l])
+        if (id >= 0 && A->own[id]) ids.push_back(id);
+    }
+  }
   int64_t i = 0;
   for (int l = 0; l <= A->lmax; ++l)
-    for (int id : A->hmap[l]) {
-      if (id < 0 || !A->own[id]) continue;
+    for (int id : per[l]) {
       ader_cell& e = out[i++];
       std::memset(&e, 0, sizeof(e));
       const HCell& C = A->cells[id];
