@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <thread>
 #include <vector>
 
 namespace ader {
@@ -107,6 +108,23 @@ namespace {
   } while (0)
 
 double now_s() { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); }
+
+// host threads for the O(cells) scans of the tree mirror (one below 256k ids)
+int host_threads(int n) {
+  if (n < (1 << 18)) return 1;
+  const unsigned hc = std::thread::hardware_concurrency();
+  return (int)std::max(1u, std::min(8u, hc ? hc : 1u));
+}
+
+// fn(t, i0, i1) on T contiguous chunks of [0, n), chunk 0 on the calling thread
+template <class F>
+void parallel_chunks(int n, int T, F fn) {
+  std::vector<std::thread> th;
+  for (int t = 1; t < T; ++t)
+    th.emplace_back(fn, t, (int)((long long)n * t / T), (int)((long long)n * (t + 1) / T));
+  fn(0, 0, (int)((long long)n / T));
+  for (auto& x : th) x.join();
+}
 
 double lagrange(const DevTables& T, int N, int p, double x) {
   double v = 1.0;
@@ -435,12 +453,32 @@ ader_status upload_topology(AmrState* A, std::string& err) {
   for (int l = 0; l < kAmrMaxLevels; ++l) A->nlev[l] = 0;
   if (W == 1) {
     // one rank: every alive cell is owned and computed; lists in id order
-    for (int l = 0; l <= A->lmax; ++l) { A->lact[l].reserve(nu); A->lvch[l].reserve(nu / 2); A->lvmo[l].reserve(nu / 8); }
-    for (int i = 0; i < nu; ++i) {
-      const HCell& C = A->cells[i];
-      if (!C.alive) continue;
-      A->nlev[C.level]++;
-      (C.status == 0 ? A->lact : (C.status == 1 ? A->lvch : A->lvmo))[C.level].push_back(i);
+    // (contiguous id chunks scanned by host threads, appended in chunk order)
+    struct Part {
+      std::vector<int> l[3][kAmrMaxLevels];
+      long long n[kAmrMaxLevels]{};
+    };
+    const int T = host_threads(nu);
+    std::vector<Part> parts(T);
+    parallel_chunks(nu, T, [&](int t, int i0, int i1) {
+      Part& P = parts[t];
+      for (int i = i0; i < i1; ++i) {
+        const HCell& C = A->cells[i];
+        if (!C.alive) continue;
+        P.n[C.level]++;
+        P.l[C.status == 0 ? 0 : (C.status == 1 ? 1 : 2)][C.level].push_back(i);
+      }
+    });
+    for (int l = 0; l <= A->lmax; ++l) {
+      size_t na = 0, nc = 0, nm = 0;
+      for (const Part& P : parts) { na += P.l[0][l].size(); nc += P.l[1][l].size(); nm += P.l[2][l].size(); }
+      A->lact[l].reserve(na); A->lvch[l].reserve(nc); A->lvmo[l].reserve(nm);
+      for (const Part& P : parts) {
+        A->nlev[l] += P.n[l];
+        A->lact[l].insert(A->lact[l].end(), P.l[0][l].begin(), P.l[0][l].end());
+        A->lvch[l].insert(A->lvch[l].end(), P.l[1][l].begin(), P.l[1][l].end());
+        A->lvmo[l].insert(A->lvmo[l].end(), P.l[2][l].begin(), P.l[2][l].end());
+      }
     }
   }
   for (int i = 0; i < (W > 1 ? nu : 0); ++i) {
@@ -798,8 +836,10 @@ ader_status adapt_apply(AmrState* A, bool t0, const std::vector<double>& chi, st
   for (auto& c : A->cells) c.isnew = false;
   const int nu = (int)A->cells.size();
   std::vector<char> mark(nu, 0);
-  for (int i = 0; i < nu; ++i)
-    mark[i] = A->cells[i].alive && A->cells[i].status == 0 && A->cells[i].level < A->lmax && chi[i] > A->cfg.chi_ref;
+  parallel_chunks(nu, host_threads(nu), [&](int, int i0, int i1) {
+    for (int i = i0; i < i1; ++i)
+      mark[i] = A->cells[i].alive && A->cells[i].status == 0 && A->cells[i].level < A->lmax && chi[i] > A->cfg.chi_ref;
+  });
   for (int i = 0; i < nu; ++i)
     if (mark[i]) refine_cell(A, i, t0);
   A->tm_a[0] += now_s() - w0; w0 = now_s();
