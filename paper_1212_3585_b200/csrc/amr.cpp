@@ -318,7 +318,19 @@ void closure(AmrState* A, bool t0) {
 
 void garbage_collect(AmrState* A, std::vector<int>* freed) {
   int nb[26];
-  for (int i = 0; i < (int)A->cells.size(); ++i) {
+  // candidates (active cells with children) found by a threaded scan; no
+  // candidate descends from another (an active cell has no active
+  // descendant), so visiting them in id order afterwards equals the serial scan
+  const int nu = (int)A->cells.size(), T = host_threads(nu);
+  std::vector<std::vector<int>> part(T);
+  parallel_chunks(nu, T, [&](int t, int i0, int i1) {
+    for (int i = i0; i < i1; ++i) {
+      const HCell& C = A->cells[i];
+      if (C.alive && C.status == 0 && C.child >= 0) part[t].push_back(i);
+    }
+  });
+  for (const auto& P : part)
+  for (const int i : P) {
     HCell& C = A->cells[i];
     if (!C.alive || C.status != 0 || C.child < 0) continue;
     const int k = voronoi(A, i, nb);
@@ -850,18 +862,21 @@ ader_status adapt_apply(AmrState* A, bool t0, const std::vector<double>& chi, st
   if (!t0) {
     const int nu2 = (int)A->cells.size();
     std::vector<char> cand(nu2, 0);
-    for (int i = 0; i < nu2; ++i) {
-      const HCell& C = A->cells[i];
-      if (!C.alive || C.status != -1) continue;
-      bool ok = true;
-      for (int q = 0; q < A->rd && ok; ++q) {
-        const int kid = C.child + q;
-        const HCell& K = A->cells[kid];
-        if (K.status != 0 || K.child >= 0 || K.isnew || !(kid < nu && chi[kid] < A->cfg.chi_rec) || (kid < nu && mark[kid]))
-          ok = false;
+    parallel_chunks(nu2, host_threads(nu2), [&](int, int i0, int i1) {
+      for (int i = i0; i < i1; ++i) {
+        const HCell& C = A->cells[i];
+        if (!C.alive || C.status != -1) continue;
+        bool ok = true;
+        for (int q = 0; q < A->rd && ok; ++q) {
+          const int kid = C.child + q;
+          const HCell& K = A->cells[kid];
+          if (K.status != 0 || K.child >= 0 || K.isnew || !(kid < nu && chi[kid] < A->cfg.chi_rec) ||
+              (kid < nu && mark[kid]))
+            ok = false;
+        }
+        cand[i] = ok;
       }
-      cand[i] = ok;
-    }
+    });
     bool any_cand = false;
     for (int i = 0; i < nu2 && !any_cand; ++i) any_cand = cand[i];
     while (any_cand) {
