@@ -430,8 +430,12 @@ ader_status upload_topology(AmrState* A, std::string& err) {
   std::vector<int> cand;
   const bool full = A->all_dirty || A->dirty.size() * 4 > (size_t)nu;
   if (!full) {
-    cand = A->dirty;
-    std::sort(cand.begin(), cand.end());
+    // the written ids in id order: a scan of the byte flags is cheaper than
+    // sorting the (up to nu / 4) ids
+    cand.reserve(A->dirty.size());
+    const size_t lim = std::min(A->isdirty.size(), (size_t)nu);
+    for (size_t i = 0; i < lim; ++i)
+      if (A->isdirty[i]) cand.push_back((int)i);
   }
   for (int i : A->dirty)
     if ((size_t)i < A->isdirty.size()) A->isdirty[i] = 0;
@@ -453,6 +457,7 @@ ader_status upload_topology(AmrState* A, std::string& err) {
     if (C.alive && (!P.alive || !same_pos)) { sets.push_back(C.level); sets.push_back(lin(A, C.level, C.idx)); sets.push_back(i); }
     P = C;
   }
+  A->tm_u[3] += now_s() - w0;
   for (int l = 0; l <= A->lmax; ++l) {
     A->lact[l].clear(); A->lvch[l].clear(); A->lvmo[l].clear(); A->lown[l].clear();
     A->xp[l] = AmrState::XPlan();
@@ -1223,8 +1228,9 @@ void amr_destroy(AmrState* A) {
                  1e3 * A->tm_a[3] / A->tm_steps, 1e3 * A->tm_a[4] / A->tm_steps, 1e3 * A->tm_a[5] / A->tm_steps,
                  1e3 * A->tm_a[6] / A->tm_steps);
   if (std::getenv("ADER_AMR_TIMING") && A->tm_steps)
-    std::fprintf(stderr, "  upload (ms/step): capacity %.3f, host scans/lists %.3f, staging+H2D %.3f\n",
-                 1e3 * A->tm_u[0] / A->tm_steps, 1e3 * A->tm_u[1] / A->tm_steps, 1e3 * A->tm_u[2] / A->tm_steps);
+    std::fprintf(stderr, "  upload (ms/step): capacity %.3f, host scans/lists %.3f (of which mirror diff %.3f), staging+H2D %.3f\n",
+                 1e3 * A->tm_u[0] / A->tm_steps, 1e3 * A->tm_u[1] / A->tm_steps, 1e3 * A->tm_u[3] / A->tm_steps,
+                 1e3 * A->tm_u[2] / A->tm_steps);
   cudaStreamSynchronize(A->k->stream);
   void* ps[] = {A->V.u, A->V.mem, A->V.w, A->V.q, A->V.chi, A->V.level, A->V.status, A->V.mother, A->V.child, A->V.idx,
                 A->V.own, A->dlist, A->xsend, A->xrecv};
