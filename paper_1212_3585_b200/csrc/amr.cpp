@@ -396,12 +396,12 @@ struct Uploader {
     cudaStream_t sm = A->k->stream;
     if (tot > A->dscratch_cap) {
       if (A->dscratch) { cudaStreamSynchronize(sm); cudaFree(A->dscratch); }
-      A->dscratch_cap = tot * 3 / 2 + (1 << 20);
+      A->dscratch_cap = tot * 2 + (1 << 20);   // geometric: pinned / device reallocations are slow
       ACK(cudaMalloc(&A->dscratch, A->dscratch_cap));
     }
     if (tot > A->hstage_cap) {
       if (A->hstage) { cudaStreamSynchronize(sm); cudaFreeHost(A->hstage); }
-      A->hstage_cap = tot * 3 / 2 + (1 << 20);
+      A->hstage_cap = tot * 2 + (1 << 20);
       ACK(cudaMallocHost(&A->hstage, A->hstage_cap));
     }
     ACK(cudaStreamSynchronize(sm));   // previous use of the staging buffer finished
