@@ -142,6 +142,10 @@ LB_CASES = {
                              chi_ref=0.1, chi_rec=0.05), W.explosion(2), 3, 4),
     "offcentre3d_l1_x2": (dict(dim=3, degree=2, n0=(20, 8, 8), lo=(-1, -1, -1), hi=(4, 1, 1), bc=(1,) * 6, lmax=1,
                                cfl=0.3), W.explosion(3), 2, 2),
+    # periodic wrap of the compute band around re-cut (non-grid) blocks
+    "vortex_periodic_M3_l1_x4": (dict(dim=2, degree=3, n0=(24, 24), lo=(0, 0), hi=(10, 10), bc=(0,) * 6, lmax=1,
+                                      cfl=0.9, chi_ref=0.01, chi_rec=0.005), W.isentropic_vortex(center=(2.0, 2.5)),
+                                 4, 3),
 }
 
 
