@@ -578,7 +578,7 @@ static int adapt(amr_t* A, int at_t0) {
         if (reconstruct(A, i)) return 3;
   /* 2. refinement marks R = {active, chi > chi_ref, level < lmax} */
   int nu = A->nused;
-  int* mark = (int*)calloc(nu, sizeof(int));
+  int* mark = (int*)calloc((size_t)(nu > 0 ? nu : 1), sizeof(int));
   for (int i = 0; i < nu; ++i)
     mark[i] = A->c[i].alive && A->c[i].status == 0 && A->c[i].level < A->lmax && A->c[i].chi > A->cfg.chi_ref;
   for (int i = 0; i < nu; ++i)
