@@ -107,6 +107,8 @@ def lib():
                                             C.POINTER(AderStepReport)]
         L.ader_sizeof.restype = C.c_int64
         L.ader_sizeof.argtypes = [C.c_int32]
+        L.ader_rcb_partition.argtypes = [C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int64), C.c_int32,
+                                         C.POINTER(C.c_int32)]
         _LIB = L
     return _LIB
 

@@ -96,3 +96,14 @@ def test_library_is_sm100a_only():
                          text=True).stdout
     assert "sm_100a" in out
     assert "sm_90" not in out and "sm_80" not in out
+
+
+def test_missing_library_fails_loudly(monkeypatch):
+    # the product path has no CPU fallback: without the built extension the
+    # binding raises instead of computing anything
+    monkeypatch.setattr(ader, "_LIB", None)
+    monkeypatch.setattr(ader, "LIB_PATH", os.path.join(ROOT, "no_such_dir", "libader_b200.so"))
+    with pytest.raises(ImportError):
+        ader.lib()
+    with pytest.raises(ImportError):
+        ader.Solver(_cfg())
