@@ -121,6 +121,11 @@ int  orc_face_flux_mapped(int d, int M, int system, double gamma, double ch, int
                           const double* qL, const double* offL, double sclL, double toffL, double tsclL,
                           const double* qR, const double* offR, double sclR, double toffR, double tsclR,
                           double* F);
+/* Projection of a mother cell's polynomial into its child sub-box off[d]
+ * (0 <= off_k < r): mean over the child box of w_h (mode 0,
+ * poly = w[nv][N^d]) or of q_h(., tau) (mode 1, poly = q[nv][N^(d+1)]). */
+void orc_project_subbox(int d, int M, int nv, int r, int mode, const double* poly, const int* off, double tau,
+                        double* out);
 /* Loehner-type indicator chi of eqn.indicator in the discretised
  * reading R14 from the 3^d same-level box of Phi (x fastest). */
 double orc_indicator(int d, const double* phi, double eps);

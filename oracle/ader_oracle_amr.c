@@ -209,20 +209,33 @@ static int reconstruct(amr_t* A, int id) {
   return 0;
 }
 
-/* cell average over child sub-box `off` of the polynomial (mode 0: WENO w,
- * mode 1: space-time q at tau) of cell m, by an N-point GL rule (exact). */
-static void subbox_average(const amr_t* A, int m, const int* off, int mode, double tau, double* out) {
-  int d = A->d, N = A->N, nv = A->nv, np = 1;
+/* Projection of a mother polynomial into the child sub-box `off`:
+ * the child's cell average (1/|child|) int_child poly d x, i.e. the mean over
+ * xi in prod_k [off_k/r, (off_k+1)/r] of the mother's WENO polynomial w_h
+ * (mode 0) or of its space-time polynomial q_h at time fraction tau (mode 1),
+ * by the N-point Gauss-Legendre rule on the child box (exact: degree <= M per
+ * axis).  Exported for the pins in tests/test_oracle_pins_r2.py. */
+void orc_project_subbox(int d, int M, int nv, int r, int mode, const double* poly, const int* off, double tau,
+                        double* out) {
+  int N = M + 1, np = 1;
+  double gq[8], gw[8];
+  orc_gauss_legendre(N, gq, gw);
   for (int k = 0; k < d; ++k) np *= N;
   for (int v = 0; v < nv; ++v) out[v] = 0.0;
   for (int g = 0; g < np; ++g) {
     int gi[3] = {g % N, (g / N) % N, g / (N * N)};
     double xi[3], wg = 1.0, val[VMAX];
-    for (int k = 0; k < d; ++k) { xi[k] = (off[k] + A->gq[gi[k]]) / A->r; wg *= A->gw[gi[k]]; }
-    if (mode == 0) orc_eval_w(d, A->M, nv, A->c[m].w, xi, val);
-    else orc_eval_st(d, A->M, nv, A->c[m].q, xi, tau, val);
+    for (int k = 0; k < d; ++k) { xi[k] = (off[k] + gq[gi[k]]) / r; wg *= gw[gi[k]]; }
+    if (mode == 0) orc_eval_w(d, M, nv, poly, xi, val);
+    else orc_eval_st(d, M, nv, poly, xi, tau, val);
     for (int v = 0; v < nv; ++v) out[v] += wg * val[v];
   }
+}
+
+/* cell average over child sub-box `off` of the polynomial (mode 0: WENO w,
+ * mode 1: space-time q at tau) of cell m */
+static void subbox_average(const amr_t* A, int m, const int* off, int mode, double tau, double* out) {
+  orc_project_subbox(A->d, A->M, A->nv, A->r, mode, mode == 0 ? A->c[m].w : A->c[m].q, off, tau, out);
 }
 
 static void child_off(const amr_t* A, int id, int* off) {
