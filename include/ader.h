@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define ADER_ABI_VERSION 3
+#define ADER_ABI_VERSION 4
 
 typedef struct ader_ctx ader_ctx;   /* opaque; owns all device memory it allocates */
 
@@ -102,6 +102,11 @@ typedef struct {
   int64_t pred_cells;             /* cells run through the predictor (incl. halo)  */
   double  cons_total[9];          /* sum of u * cell volume over owned active cells*/
   double  wall_s;
+  double  min_threshold_margin;   /* AMR: min over the adapts of this call and their
+                                   * active cells of min(|chi - chi_ref| / chi_ref,
+                                   * |chi - chi_rec| / chi_rec) — how close a strict
+                                   * threshold comparison came to flipping
+                                   * a refinement decision; 1e300 if no adapt ran     */
 } ader_step_report;
 
 /* One cell as exported by ader_get_cells: parity key (level, idx, status). */
@@ -226,6 +231,8 @@ int64_t ader_sizeof(int32_t what);
  *   what = 1 PRED : q[cell][nu][N^(d+1)]       (space fastest, time slowest), step dt
  *   what = 2 FLUX : F[dir][ext cell][nu]        ext box = block + 1 per axis, lower faces
  * capacity in doubles. */
+/* Uniform grids only; a loopback group context (ader_debug_group_create) is
+ * rejected with ADER_ERR_ARG. */
 ader_status ader_debug_dump(ader_ctx* c, int32_t what, double dt, double* out, int64_t capacity);
 
 #ifdef __cplusplus

@@ -41,6 +41,7 @@ class OrcReport(C.Structure):
         ("t", C.c_double), ("dt", C.c_double),
         ("steps", C.c_int64), ("cell_updates", C.c_int64), ("sweeps_total", C.c_int64),
         ("sweeps_max", C.c_int32), ("updates_per_level", C.c_int64 * 8),
+        ("min_threshold_margin", C.c_double),
     ]
 
 
@@ -497,6 +498,13 @@ class AmrOracle:
 
     def adapt(self):
         assert lib().orc_amr_adapt(self.ptr) == 0, self.error()
+
+    def margin(self):
+        """min threshold margin of the adapts since the last step() / adapt()"""
+        L = lib()
+        L.orc_amr_margin.restype = C.c_double
+        L.orc_amr_margin.argtypes = [C.c_void_p]
+        return L.orc_amr_margin(self.ptr)
 
     def cells(self):
         """structured array: level, status, idx[3], u[9] sorted by (level, z, y, x)"""

@@ -1144,6 +1144,7 @@ int orc_step(orc_ctx* c, double t_end, int64_t max_steps, orc_report* rep) {
   }
   r.t = c->t;
   r.updates_per_level[0] = r.cell_updates;
+  r.min_threshold_margin = 1e300;   /* no adapt on a uniform grid */
   if (rep) *rep = r;
   free(un);
   return rc;

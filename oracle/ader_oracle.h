@@ -54,6 +54,11 @@ typedef struct {
   int64_t steps, cell_updates, sweeps_total;
   int32_t sweeps_max;
   int64_t updates_per_level[8];
+  /* AMR: min over the adapts of the call and their active cells of
+   * min(|chi - chi_ref| / chi_ref, |chi - chi_rec| / chi_rec): how close any
+   * strict threshold comparison of P:622-624 came to flipping (1e300 if no
+   * adapt ran) */
+  double min_threshold_margin;
 } orc_report;
 
 /* ---- tables / pure per-cell numerics (for pins) ---------------------- */

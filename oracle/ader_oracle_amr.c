@@ -60,6 +60,7 @@ typedef struct {
   int64_t steps, updates[LMAXX], sweeps;
   int sweeps_max;
   double gq[8], gw[8];        /* N-point GL rule for projections */
+  double margin;              /* min threshold margin since the last reset (orc_report) */
 } amr_t;
 
 /* ---- storage ------------------------------------------------------------ */
@@ -582,7 +583,14 @@ static int adapt(amr_t* A, int at_t0) {
   for (int i = 0; i < A->nused; ++i) {
     A->c[i].isnew = 0;
     if (A->c[i].status != 0) { free(A->c[i].w); A->c[i].w = NULL; }
-    if (A->c[i].alive && A->c[i].status == 0) A->c[i].chi = indicator(A, i);
+    if (A->c[i].alive && A->c[i].status == 0) {
+      double chi = indicator(A, i);
+      A->c[i].chi = chi;
+      /* distance of chi to the strict thresholds, relative */
+      double m1 = fabs(chi - A->cfg.chi_ref) / A->cfg.chi_ref, m2 = fabs(chi - A->cfg.chi_rec) / A->cfg.chi_rec;
+      double m = m1 < m2 ? m1 : m2;
+      if (m < A->margin) A->margin = m;
+    }
   }
   /* WENO polynomials at t^{n+1} of every active cell (mothers of new children, R18) */
   if (!at_t0)
@@ -678,6 +686,7 @@ void* orc_amr_create(const orc_config* cfg) {
   for (int k = 0; k < A->d; ++k) A->NS *= A->N;
   A->NST = A->NS * A->N;
   A->r = cfg->refine_factor; A->lmax = cfg->lmax;
+  A->margin = 1e300;
   A->rd = 1;
   for (int k = 0; k < A->d; ++k) A->rd *= A->r;
   if (A->cfg.pred_tol <= 0) A->cfg.pred_tol = 1e-13;
@@ -750,6 +759,7 @@ double orc_amr_compute_dt(void* h) {
 int orc_amr_step(void* h, double t_end, int64_t max_steps, int adapt_every, orc_report* rep) {
   amr_t* A = (amr_t*)h;
   orc_report R; memset(&R, 0, sizeof(R));
+  A->margin = 1e300;
   for (int l = 0; l < LMAXX; ++l) A->updates[l] = 0;
   A->sweeps = 0; A->sweeps_max = 0;
   g_nsched = 0;
@@ -768,11 +778,17 @@ int orc_amr_step(void* h, double t_end, int64_t max_steps, int adapt_every, orc_
   for (int l = 0; l < LMAXX; ++l) { R.updates_per_level[l] = A->updates[l]; R.cell_updates += A->updates[l]; }
   R.sweeps_total = A->sweeps;
   R.sweeps_max = A->sweeps_max;
+  R.min_threshold_margin = A->margin;
   if (rep) *rep = R;
   return 0;
 }
 
-int orc_amr_adapt(void* h) { return adapt((amr_t*)h, 0); }
+int orc_amr_adapt(void* h) {
+  ((amr_t*)h)->margin = 1e300;
+  return adapt((amr_t*)h, 0);
+}
+/* min threshold margin of the adapts since the last orc_amr_step / orc_amr_adapt */
+double orc_amr_margin(void* h) { return ((amr_t*)h)->margin; }
 
 /* all cells sorted by (level, z, y, x); out == NULL -> count */
 int64_t orc_amr_get_cells(void* h, orc_amr_cell* out) {

@@ -91,6 +91,7 @@ struct ProfRec { int kind; cudaEvent_t e0, e1; double flops; };
 struct ader_ctx {
   ader_config cfg{};
   int d = 2, M = 2, N = 3, nv = 4, NS = 9, NST = 27, H = 3;
+  long long qs = 27;                           // q block stride (nv NST rounded up to even, launch.h)
   ader_partition_info part{};
   int n[3] = {1, 1, 1}, P[3] = {1, 1, 1};
   long long ncell = 0;
@@ -381,13 +382,18 @@ ader_status halo_exchange_nccl(ader_ctx* c, int a) {
   const bool remote_lo = dl.kind == 1, remote_hi = dh.kind == 1;
   if (!remote_lo && !remote_hi) return ADER_OK;
   const size_t cnt = (size_t)desc_box(dl.recv_lo, dl.recv_hi).count() * c->nv;
+  if (!c->comm) return fail(c, ADER_ERR_NCCL, "halo exchange without a communicator");
   NK(g_nccl.GroupStart());
-  // order per peer: (send low, recv high, send high, recv low) on every rank
-  if (remote_lo) NK(g_nccl.Send(c->sendb[2 * a], cnt, ncclDouble, dl.peer, c->comm, c->k.stream));
-  if (remote_hi) NK(g_nccl.Recv(c->recvb[2 * a + 1], cnt, ncclDouble, dh.peer, c->comm, c->k.stream));
-  if (remote_hi) NK(g_nccl.Send(c->sendb[2 * a + 1], cnt, ncclDouble, dh.peer, c->comm, c->k.stream));
-  if (remote_lo) NK(g_nccl.Recv(c->recvb[2 * a], cnt, ncclDouble, dl.peer, c->comm, c->k.stream));
-  NK(g_nccl.GroupEnd());
+  // order per peer: (send low, recv high, send high, recv low) on every rank;
+  // the group is closed even when a call fails
+  ncclResult_t r = ncclSuccess;
+  if (remote_lo && r == ncclSuccess) r = g_nccl.Send(c->sendb[2 * a], cnt, ncclDouble, dl.peer, c->comm, c->k.stream);
+  if (remote_hi && r == ncclSuccess) r = g_nccl.Recv(c->recvb[2 * a + 1], cnt, ncclDouble, dh.peer, c->comm, c->k.stream);
+  if (remote_hi && r == ncclSuccess) r = g_nccl.Send(c->sendb[2 * a + 1], cnt, ncclDouble, dh.peer, c->comm, c->k.stream);
+  if (remote_lo && r == ncclSuccess) r = g_nccl.Recv(c->recvb[2 * a], cnt, ncclDouble, dl.peer, c->comm, c->k.stream);
+  const ncclResult_t r2 = g_nccl.GroupEnd();
+  NK(r);
+  NK(r2);
   return ADER_OK;
 }
 
@@ -463,7 +469,7 @@ void run_predictor(ader_ctx* c, double dt, const double* dtdx_dev = nullptr) {
   double dtdx[3] = {0, 0, 0};
   for (int k = 0; k < c->d; ++k) dtdx[k] = dt / c->dx[k];
   Scope s(c, ADER_K_PRED, 0.0);   // flops from the sweep counter (ader_kernel_stats)
-  launch_predictor(c->k, c->w, c->q, r, dtdx, c->cfg.pred_tol, c->cfg.pred_max_sweeps, c->cnt, dtdx_dev);
+  launch_predictor(c->k, c->w, c->q, r, dtdx, c->cfg.pred_tol, c->cfg.pred_max_sweeps, c->cnt, dtdx_dev, c->qs);
 }
 
 void face_boxes(const ader_ctx* c, Box fb[3]) {
@@ -484,7 +490,12 @@ void run_flux(ader_ctx* c) {
   Scope s(c, ADER_K_FLUX, face_flops(c) * nf);
   const int H = c->H, zH = c->d == 3 ? H : 0;
   const Box ext = make_box(H, H + c->n[0] + 1, H, H + c->n[1] + 1, zH, zH + c->n[2] + (c->d == 3 ? 1 : 0));
-  launch_face_flux_cells(c->k, c->q, c->F, ext, H, c->n, transmissive_mask(c), reflective_mask(c), c->cnt);
+  // ADER_FLUX_LEGACY=1: the round-1 kernel (direct global loads), for A/B checks
+  static const bool legacy = !(std::getenv("ADER_FLUX_TMA") && std::getenv("ADER_FLUX_TMA")[0] == '1');
+  if (legacy)
+    launch_face_flux_cells(c->k, c->q, c->F, ext, H, c->n, transmissive_mask(c), reflective_mask(c), c->cnt, c->qs);
+  else
+    launch_face_flux_tma(c->k, c->q, c->F, ext, H, c->n, transmissive_mask(c), reflective_mask(c), c->cnt);
 }
 
 void run_update(ader_ctx* c, double dt, const double* dtdx_dev = nullptr) {
@@ -496,6 +507,8 @@ void run_update(ader_ctx* c, double dt, const double* dtdx_dev = nullptr) {
 }
 
 ader_status check_errors(ader_ctx* c) {
+  if (c->hcnt->err_code == 0 && c->hcnt->err_any != 0)
+    return fail(c, ADER_ERR_SOLVER, "solver failure on another rank (code %llu) by t=%.17g", c->hcnt->err_any, c->t);
   if (c->hcnt->err_code == 0) return ADER_OK;
   const long long cell = (long long)c->hcnt->err_cell;
   const long long x = cell % c->P[0], y = (cell / c->P[0]) % c->P[1], z = cell / ((long long)c->P[0] * c->P[1]);
@@ -774,9 +787,10 @@ static ader_status create_impl(const ader_config* cfg, ader_ctx** out, bool loop
   CK(alloc(&c->wx, nc * c->nv * c->N));
   if (c->d == 3) CK(alloc(&c->wxy, nc * c->nv * c->N * c->N));
   CK(alloc(&c->w, nc * c->nv * c->NS));
-  CK(alloc(&c->q, nc * c->nv * c->NST));
+  c->qs = q_block_stride(c->d, c->M, c->cfg.system);
+  CK(alloc(&c->q, nc * c->qs));
   CK(alloc(&c->F, nc * c->nv * c->d));
-  CK(alloc(&c->stage, (size_t)c->n[0] * c->n[1] * c->n[2] * c->nv * std::max(c->NST, c->d)));
+  CK(alloc(&c->stage, (size_t)c->n[0] * c->n[1] * c->n[2] * std::max<size_t>(c->qs, (size_t)c->nv * c->d)));
   CK(cudaMemset(c->u, 0, nc * c->nv * sizeof(double)));
   CK(cudaMemset(c->F, 0, nc * c->nv * c->d * sizeof(double)));
   CK(cudaMalloc(&c->cnt, sizeof(DevCounters)));
@@ -986,8 +1000,16 @@ ader_status enqueue_step(ader_ctx* c, double t_end) {
   return ADER_OK;
 }
 
-// host mirror of the step control (synchronises the stream)
+// host mirror of the step control (synchronises the stream).  With several
+// ranks the error code is max-reduced first (err_any), so a solver failure on
+// one rank stops every rank at the same chunk boundary instead of leaving the
+// others blocked in the next step's collectives.
 ader_status read_state(ader_ctx* c) {
+  if (c->comm) {
+    CK(cudaMemsetAsync(&c->cnt->err_any, 0, sizeof(unsigned long long), c->k.stream));
+    CK(cudaMemcpyAsync(&c->cnt->err_any, &c->cnt->err_code, sizeof(int), cudaMemcpyDeviceToDevice, c->k.stream));
+    NK(g_nccl.AllReduce(&c->cnt->err_any, &c->cnt->err_any, 1, ncclUint64, ncclMax, c->comm, c->k.stream));
+  }
   CK(cudaMemcpyAsync(c->hst, c->st, sizeof(StepState), cudaMemcpyDeviceToHost, c->k.stream));
   CK(cudaMemcpyAsync(c->hcnt, c->cnt, sizeof(DevCounters), cudaMemcpyDeviceToHost, c->k.stream));
   CK(cudaStreamSynchronize(c->k.stream));
@@ -1079,11 +1101,12 @@ ader_status ader_step(ader_ctx* c, double t_end, int64_t max_macro_steps, ader_s
                    std::chrono::duration<double, std::milli>(h1 - h0).count(),
                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h1).count());
     if (st != ADER_OK) break;
-    if (c->hcnt->err_code) break;
+    if (c->hcnt->err_code || c->hcnt->err_any) break;
   }
   if (st == ADER_OK) st = read_state(c);
   r.macro_steps = c->hst->steps - steps0;
   r.dt0 = c->hst->last_dt;
+  r.min_threshold_margin = 1e300;   // uniform grid: no adapt
   st = step_finish(c, st, &r, sw0, pc0);
   r.wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - w0).count();
   if (rep) *rep = r;
@@ -1209,11 +1232,11 @@ ader_status ader_debug_group_step(ader_ctx** cs, int32_t n, double t_end, int64_
 
 ader_status ader_refine(ader_ctx* c, ader_step_report* rep) {
   if (!c) return ADER_ERR_ARG;
-  if (rep) std::memset(rep, 0, sizeof(*rep));
+  if (rep) { std::memset(rep, 0, sizeof(*rep)); rep->min_threshold_margin = 1e300; }
   if (c->loopback && c->cfg.world_size > 1) return fail(c, ADER_ERR_ARG, "group contexts adapt inside ader_debug_group_step");
   if (c->amr) {
     std::string e;
-    ader_status s = amr_adapt(c->amr, e);
+    ader_status s = amr_adapt(c->amr, rep, e);
     if (s != ADER_OK) c->err = e;
     return s;
   }
@@ -1291,6 +1314,7 @@ int64_t ader_sizeof(int32_t what) {
 ader_status ader_debug_dump(ader_ctx* c, int32_t what, double dt, double* out, int64_t capacity) {
   if (!c || !out) return ADER_ERR_ARG;
   if (c->amr) return fail(c, ADER_ERR_UNSUPPORTED, "ader_debug_dump: uniform grids only");
+  if (c->loopback) return fail(c, ADER_ERR_ARG, "ader_debug_dump: not on a loopback group context");
   const Box b = owned(c);
   ader_status st = fill_halo(c, c->u);
   if (st != ADER_OK) return st;
@@ -1305,8 +1329,10 @@ ader_status ader_debug_dump(ader_ctx* c, int32_t what, double dt, double* out, i
   run_predictor(c, dt);
   if (what == 1) {
     if (capacity < b.count() * c->nv * c->NST) return fail(c, ADER_ERR_ARG, "capacity too small");
-    launch_gather(c->k, c->q, c->nv * c->NST, b, c->stage);
-    CK(cudaMemcpyAsync(out, c->stage, (size_t)b.count() * c->nv * c->NST * sizeof(double), cudaMemcpyDeviceToHost, c->k.stream));
+    launch_gather(c->k, c->q, (int)c->qs, b, c->stage);
+    const size_t row = (size_t)c->nv * c->NST * sizeof(double);
+    CK(cudaMemcpy2DAsync(out, row, c->stage, (size_t)c->qs * sizeof(double), row, (size_t)b.count(),
+                         cudaMemcpyDeviceToHost, c->k.stream));
     CK(cudaStreamSynchronize(c->k.stream));
     CK(cudaMemcpy(c->hcnt, c->cnt, sizeof(DevCounters), cudaMemcpyDeviceToHost));
     return check_errors(c);

@@ -79,6 +79,10 @@ struct AmrState {
     std::vector<long long> soff, roff;                // [world + 1] offsets into sids / rids
     long long dso = 0, dro = 0;                       // their offsets inside dlist
   } xp[kAmrMaxLevels];
+  double margin = 1e300;      // min threshold margin of the adapts since the last reset (report)
+  double* rb_buf = nullptr;   // dynamic load balancing: per-id averages and gather scratch,
+  double* rb_tmp = nullptr;   // kept across rebalances and grown 2x when the id space grows
+  size_t rb_cap = 0;          // (doubles)
   double* xsend = nullptr;
   double* xrecv = nullptr;
   size_t xcap = 0;                                    // doubles
@@ -756,10 +760,25 @@ ader_status exchange(const Group& G, int l, std::string& err) {
   return ADER_OK;
 }
 
-ader_status check_err(AmrState* A, std::string& err) {
+// solver errors of this rank; with one context per rank the error code is
+// max-reduced over the ranks first (err_any), so every rank leaves the step
+// loop at the same point instead of the others blocking in the next exchange
+ader_status check_err(AmrState* A, std::string& err, bool reduce) {
   cudaStream_t sm = A->k->stream;
+  if (reduce && A->ranks.world > 1) {
+    ACK(cudaMemsetAsync(&A->cnt->err_any, 0, sizeof(unsigned long long), sm));
+    ACK(cudaMemcpyAsync(&A->cnt->err_any, &A->cnt->err_code, sizeof(int), cudaMemcpyDeviceToDevice, sm));
+    ader_status s = A->comm.max_u64(A->comm.ctx, &A->cnt->err_any, sm);
+    if (s != ADER_OK) { err = "allreduce(max) of the error code failed"; return s; }
+  }
   ACK(cudaMemcpyAsync(A->hcnt, A->cnt, sizeof(DevCounters), cudaMemcpyDeviceToHost, sm));
   ACK(cudaStreamSynchronize(sm));
+  if (reduce && A->ranks.world > 1 && !A->hcnt->err_code && A->hcnt->err_any) {
+    char b[160];
+    snprintf(b, sizeof(b), "solver failure on another rank (code %llu), t=%.17g", A->hcnt->err_any, A->t);
+    err = b;
+    return ADER_ERR_SOLVER;
+  }
   if (A->hcnt->err_code) {
     const long long id = (long long)A->hcnt->err_cell;
     char b[512];
@@ -857,6 +876,15 @@ ader_status adapt_apply(AmrState* A, bool t0, const std::vector<double>& chi, st
     for (int i = i0; i < i1; ++i)
       mark[i] = A->cells[i].alive && A->cells[i].status == 0 && A->cells[i].level < A->lmax && chi[i] > A->cfg.chi_ref;
   });
+  // how close any strict comparison of P:622-624 came to flipping: min over the
+  // active cells of the relative distance of chi to chi_ref and chi_rec
+  // (ader_step_report.min_threshold_margin; the oracle computes the same)
+  for (int i = 0; i < nu; ++i) {
+    if (!A->cells[i].alive || A->cells[i].status != 0) continue;
+    const double m1 = std::fabs(chi[i] - A->cfg.chi_ref) / A->cfg.chi_ref;
+    const double m2 = std::fabs(chi[i] - A->cfg.chi_rec) / A->cfg.chi_rec;
+    A->margin = std::min(A->margin, std::min(m1, m2));
+  }
   for (int i = 0; i < nu; ++i)
     if (mark[i]) refine_cell(A, i, t0);
   A->tm_a[0] += now_s() - w0; w0 = now_s();
@@ -1009,7 +1037,6 @@ ader_status rebalance(const Group& G, std::string& err) {
   ader_status s = ADER_OK;
   auto cleanup = [&]() {
     for (AmrState* A : G) cudaStreamSynchronize(A->k->stream);
-    for (size_t g = 0; g < G.size(); ++g) { cudaFree(buf[g]); cudaFree(tmp[g]); }
   };
   auto ids_of = [&](const AmrState* A, const std::vector<char>& mask) {
     std::vector<int> ids;
@@ -1021,8 +1048,19 @@ ader_status rebalance(const Group& G, std::string& err) {
   for (size_t g = 0; g < G.size() && s == ADER_OK; ++g) {
     AmrState* A = G[g];
     cudaStream_t sm = A->k->stream;
-    if (cudaMalloc(&buf[g], sizeof(double) * nu * nv) != cudaSuccess ||
-        cudaMalloc(&tmp[g], sizeof(double) * nu * nv) != cudaSuccess) { err = "cudaMalloc (rebalance)"; s = ADER_ERR_CUDA; break; }
+    if (A->rb_cap < nu * nv) {   // persistent, grown 2x (no allocation per rebalance)
+      const size_t cap = std::max(nu * nv, 2 * A->rb_cap);
+      cudaStreamSynchronize(sm);
+      if (A->rb_buf) cudaFree(A->rb_buf);
+      if (A->rb_tmp) cudaFree(A->rb_tmp);
+      A->rb_buf = A->rb_tmp = nullptr;
+      A->rb_cap = 0;
+      if (cudaMalloc(&A->rb_buf, sizeof(double) * cap) != cudaSuccess ||
+          cudaMalloc(&A->rb_tmp, sizeof(double) * cap) != cudaSuccess) { err = "cudaMalloc (rebalance)"; s = ADER_ERR_CUDA; break; }
+      A->rb_cap = cap;
+    }
+    buf[g] = A->rb_buf;
+    tmp[g] = A->rb_tmp;
     cudaMemsetAsync(buf[g], 0, sizeof(double) * nu * nv, sm);
     const std::vector<int> ids = ids_of(A, A->own);
     Uploader up{A, {}};
@@ -1233,7 +1271,7 @@ void amr_destroy(AmrState* A) {
                  1e3 * A->tm_u[2] / A->tm_steps);
   cudaStreamSynchronize(A->k->stream);
   void* ps[] = {A->V.u, A->V.mem, A->V.w, A->V.q, A->V.chi, A->V.level, A->V.status, A->V.mother, A->V.child, A->V.idx,
-                A->V.own, A->dlist, A->xsend, A->xrecv};
+                A->V.own, A->dlist, A->xsend, A->xrecv, A->rb_buf, A->rb_tmp};
   for (void* p : ps)
     if (p) cudaFree(p);
   for (int l = 0; l < kAmrMaxLevels; ++l)
@@ -1273,6 +1311,7 @@ ader_status step(const Group& G, double t_end, int64_t max_steps, ader_step_repo
   for (size_t i = 0; i < n; ++i) {
     AmrState* A = G[i];
     std::memset(&R[i], 0, sizeof(R[i]));
+    A->margin = 1e300;
     for (int l = 0; l < kAmrMaxLevels; ++l) A->updates[l] = 0;
     ACK(cudaMemcpyAsync(A->hcnt, A->cnt, sizeof(DevCounters), cudaMemcpyDeviceToHost, A->k->stream));
     ACK(cudaStreamSynchronize(A->k->stream));
@@ -1286,7 +1325,7 @@ ader_status step(const Group& G, double t_end, int64_t max_steps, ader_step_repo
     double speed = 0.0;
     double w0 = now_s();
     s = fetch_speed(G, &speed, err);
-    for (size_t i = 0; i < n && s == ADER_OK; ++i) s = check_err(G[i], err);
+    for (size_t i = 0; i < n && s == ADER_OK; ++i) s = check_err(G[i], err, G.size() == 1);
     A0->tm_speed += now_s() - w0;
     if (s != ADER_OK) break;
     double dt = A0->cfg.cfl / speed;
@@ -1296,7 +1335,7 @@ ader_status step(const Group& G, double t_end, int64_t max_steps, ader_step_repo
     s = advance(G, 0, 0, dt, err);
     A0->tm_advance += now_s() - w0;
     w0 = now_s();
-    for (size_t i = 0; i < n && s == ADER_OK; ++i) s = check_err(G[i], err);
+    for (size_t i = 0; i < n && s == ADER_OK; ++i) s = check_err(G[i], err, G.size() == 1);
     A0->tm_check += now_s() - w0;
     A0->tm_steps++;
     if (s != ADER_OK) break;
@@ -1320,6 +1359,7 @@ ader_status step(const Group& G, double t_end, int64_t max_steps, ader_step_repo
     R[i].pred_cells = (int64_t)(A->hcnt->cells - pc0[i]);
     R[i].pred_sweeps_max = A->hcnt->sweeps_max;
     R[i].rebalances = A->nrebal - rb0[i];
+    R[i].min_threshold_margin = A->margin;
     if (reps) reps[i] = R[i];
   }
   return s;
@@ -1330,7 +1370,12 @@ ader_status amr_set_initial(AmrState* A, ader_ic_fn ic, void* user, std::string&
   return set_initial(Group{A}, ic, user, err);
 }
 
-ader_status amr_adapt(AmrState* A, std::string& err) { return adapt(Group{A}, false, err); }
+ader_status amr_adapt(AmrState* A, ader_step_report* rep, std::string& err) {
+  A->margin = 1e300;
+  ader_status s = adapt(Group{A}, false, err);
+  if (rep) rep->min_threshold_margin = A->margin;
+  return s;
+}
 
 ader_status amr_step(AmrState* A, double t_end, int64_t max_steps, ader_step_report* rep, std::string& err) {
   return step(Group{A}, t_end, max_steps, rep, err);

@@ -81,7 +81,7 @@ AmrState* amr_create(const ader_config* cfg, KCtx* k, DevCounters* cnt, DevCount
 void amr_destroy(AmrState* a);
 ader_status amr_set_initial(AmrState* a, ader_ic_fn ic, void* user, std::string& err);
 ader_status amr_step(AmrState* a, double t_end, int64_t max_steps, ader_step_report* rep, std::string& err);
-ader_status amr_adapt(AmrState* a, std::string& err);
+ader_status amr_adapt(AmrState* a, ader_step_report* rep, std::string& err);
 int amr_rebalances(const AmrState* a);   // repartitions so far (dynamic load balancing)
 // lockstep variants over the ranks of a loopback group (one process, one GPU)
 ader_status amr_group_set_initial(AmrState* const* g, int n, ader_ic_fn ic, void* user, std::string& err);

@@ -1,0 +1,89 @@
+// flux_point.cuh — one space-time quadrature point of the two-point face flux
+// (flux:F/G/H @ P:158-172; eqn.rusanov @ P:181-185, eqn.osher @ P:186-196),
+// shared by the face-flux kernels of the uniform path (kernels.cu, flux_tma.cu).
+#pragma once
+#include "device.cuh"
+
+namespace ader {
+
+constexpr int ipow_c(int b, int e) { return e == 0 ? 1 : b * ipow_c(b, e - 1); }
+constexpr int pow2_at_least(int x) { return x <= 1 ? 1 : 2 * pow2_at_least((x + 1) / 2); }
+
+template <bool GLOBAL>
+__device__ __forceinline__ double ldq(const double* p) {
+  if constexpr (GLOBAL) return __ldg(p);
+  else return *p;
+}
+
+// One space-time quadrature point of the face between the cell blocks qL0
+// (lower side) and qR0 (upper side), [NV][N^(D+1)] each, in global (GL_L,
+// GL_R) or shared memory.
+template <int D, int M, int SYS, int DIR, int FLUX, bool GL_L, bool GL_R = GL_L>
+__device__ __forceinline__ bool point_flux_blocks(const double* qL0, const double* qR0, int p, bool fok, bool tlo,
+                                                  bool thi, bool rlo, bool rhi, double wt, double gamma, double ch,
+                                                  const DevTables& T, double* val) {
+  using PH = Phys<SYS, D>;
+  constexpr int NV = PH::NV, N = M + 1, NS = ipow_c(N, D), NST = NS * N;
+  constexpr int NT = NS / N;
+#pragma unroll
+  for (int v = 0; v < NV; ++v) val[v] = 0.0;
+  if (!fok) return true;
+  const int s = p / NT, t = p - s * NT;
+  const int t1 = t % N, t2 = t / N;
+  constexpr int ax0 = (DIR == 0) ? 1 : 0;
+  constexpr int ax1 = (DIR == 2) ? 1 : 2;
+  constexpr int sn = ipow_c(N, DIR);
+  const int base = s * NS + t1 * ipow_c(N, ax0) + (D == 3 ? t2 * ipow_c(N, ax1) : 0);
+  const double* qL = qL0 + base;
+  const double* qR = qR0 + base;
+  // both traces unpredicated (the padded grid holds a ghost layer on every
+  // side, so the far-side reads stay in bounds; their values are discarded at
+  // transmissive boundaries)
+  double um[NV], up[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    double a = T.psi1[0] * ldq<GL_L>(&qL[v * NST]);   // q_h^- (xi = 1 of the left cell)
+    double b = T.psi0[0] * ldq<GL_R>(&qR[v * NST]);   // q_h^+ (xi = 0 of the right cell)
+#pragma unroll
+    for (int k = 1; k < N; ++k) {
+      a += T.psi1[k] * ldq<GL_L>(&qL[v * NST + k * sn]);
+      b += T.psi0[k] * ldq<GL_R>(&qR[v * NST + k * sn]);
+    }
+    um[v] = (tlo || rlo) ? b : a;   // transmissive boundary: interior trace on both sides (R5)
+    up[v] = (thi || rhi) ? a : b;
+  }
+  // reflective wall (R22): the exterior state is the interior trace with the
+  // normal momentum negated
+  if (rlo) um[1 + DIR] = -um[1 + DIR];
+  if (rhi) up[1 + DIR] = -up[1 + DIR];
+  // equal traces (e.g. inside a constant region): eqn.rusanov and eqn.osher
+  // reduce exactly to f(q) — 0.5 (f + f) = f and the dissipation term is 0 — so one flux
+  // evaluation gives the bitwise-identical result
+  bool same = true;
+#pragma unroll
+  for (int v = 0; v < NV; ++v) same &= um[v] == up[v];
+  if (same) {
+    double f[NV], s0;
+    const bool ok = PH::template flux_speed<DIR>(um, gamma, ch, f, s0);
+#pragma unroll
+    for (int v = 0; v < NV; ++v) val[v] = wt * f[v];
+    return ok;
+  }
+  double fL[NV], fR[NV], sL, sR;
+  bool ok = PH::template flux_speed<DIR>(um, gamma, ch, fL, sL);
+  ok &= PH::template flux_speed<DIR>(up, gamma, ch, fR, sR);
+  if constexpr (FLUX == 1 && SYS == 0) {
+    double dis[NV];
+    ok &= osher_dissipation<D, DIR>(um, up, gamma, T, dis);
+#pragma unroll
+    for (int v = 0; v < NV; ++v) val[v] = wt * (0.5 * (fL[v] + fR[v]) - 0.5 * dis[v]);   // eqn.osher
+  } else {
+    const double smax = fmax(sL, sR);   // reading R4
+    const double hw = 0.5 * wt;         // eqn.rusanov with the 1/2 folded into the quadrature weight
+#pragma unroll
+    for (int v = 0; v < NV; ++v) val[v] = hw * ((fL[v] + fR[v]) - smax * (up[v] - um[v]));
+  }
+  return ok;
+}
+
+}  // namespace ader

@@ -15,11 +15,11 @@
 #include <type_traits>
 
 #include "device.cuh"
+#include "flux_point.cuh"
 #include "launch.h"
 
 namespace ader {
 
-constexpr int ipow_c(int b, int e) { return e == 0 ? 1 : b * ipow_c(b, e - 1); }
 
 __device__ __forceinline__ long long box_cell(const Box& R, long long r, long long sy, long long sz) {
   const long long x = R.lo[0] + r % R.ext[0];
@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? 4 : 2) k_predictor(
     const double dtdx0, const double dtdx1, const double dtdx2, const double gamma, const double ch,
     const double tol, const int max_sweeps, DevCounters* __restrict__ cnt, const int* __restrict__ list,
     const long long nlist, const unsigned char* __restrict__ emask, const double* __restrict__ dtdx_dev,
-    const __grid_constant__ DevTables T) {
+    const long long qs, const __grid_constant__ DevTables T) {
   using PH = Phys<SYS, D>;
   constexpr int NV = PH::NV, N = M + 1, NS = ipow_c(N, D), NST = NS * N;
   constexpr int G = (NS <= 8) ? 8 : (NS <= 16 ? 16 : 32);   // lanes per cell
@@ -261,7 +261,9 @@ __global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? 4 : 2) k_predictor(
     if (live) {
       ++nsw;
       const double dup = __hiloint2double((int)(dmax + 1u), 0), qlo = __hiloint2double((int)qmax, 0);
-      if (dup <= tol * (1.0 + qlo)) conv = true;   // reading R2
+      // (a non-finite |dq| or |q| — high word >= 0x7FF00000 — never converges;
+      // the cap then reports the cell)
+      if (dmax < 0x7FF00000u && qmax < 0x7FF00000u && dup <= tol * (1.0 + qlo)) conv = true;   // reading R2
     }
   };
   if (max_sweeps >= 1) sweep_once(std::integral_constant<bool, true>());
@@ -276,7 +278,7 @@ __global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? 4 : 2) k_predictor(
     else if (!conv) record_error(cnt, 2, 1, cell);
   }
   if (active) {
-    double* qo = q + cell * (NV * NST) + node;
+    double* qo = q + cell * qs + node;   // qs: block stride (>= NV * NST)
 #pragma unroll
     for (int v = 0; v < NV; ++v)
 #pragma unroll
@@ -314,83 +316,6 @@ __global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? 4 : 2) k_predictor(
 // D*NV point sums are formed through shared memory in a fixed order
 // (deterministic).
 // ---------------------------------------------------------------------------
-template <bool GLOBAL>
-__device__ __forceinline__ double ldq(const double* p) {
-  if constexpr (GLOBAL) return __ldg(p);
-  else return *p;
-}
-
-// One space-time quadrature point of the face between the cell blocks qL0
-// (lower side) and qR0 (upper side), [NV][N^(D+1)] each, in global (GL_L,
-// GL_R) or shared memory.
-template <int D, int M, int SYS, int DIR, int FLUX, bool GL_L, bool GL_R = GL_L>
-__device__ __forceinline__ bool point_flux_blocks(const double* qL0, const double* qR0, int p, bool fok, bool tlo,
-                                                  bool thi, bool rlo, bool rhi, double wt, double gamma, double ch,
-                                                  const DevTables& T, double* val) {
-  using PH = Phys<SYS, D>;
-  constexpr int NV = PH::NV, N = M + 1, NS = ipow_c(N, D), NST = NS * N;
-  constexpr int NT = NS / N;
-#pragma unroll
-  for (int v = 0; v < NV; ++v) val[v] = 0.0;
-  if (!fok) return true;
-  const int s = p / NT, t = p - s * NT;
-  const int t1 = t % N, t2 = t / N;
-  constexpr int ax0 = (DIR == 0) ? 1 : 0;
-  constexpr int ax1 = (DIR == 2) ? 1 : 2;
-  constexpr int sn = ipow_c(N, DIR);
-  const int base = s * NS + t1 * ipow_c(N, ax0) + (D == 3 ? t2 * ipow_c(N, ax1) : 0);
-  const double* qL = qL0 + base;
-  const double* qR = qR0 + base;
-  // both traces unpredicated (the padded grid holds a ghost layer on every
-  // side, so the far-side reads stay in bounds; their values are discarded at
-  // transmissive boundaries)
-  double um[NV], up[NV];
-#pragma unroll
-  for (int v = 0; v < NV; ++v) {
-    double a = T.psi1[0] * ldq<GL_L>(&qL[v * NST]);   // q_h^- (xi = 1 of the left cell)
-    double b = T.psi0[0] * ldq<GL_R>(&qR[v * NST]);   // q_h^+ (xi = 0 of the right cell)
-#pragma unroll
-    for (int k = 1; k < N; ++k) {
-      a += T.psi1[k] * ldq<GL_L>(&qL[v * NST + k * sn]);
-      b += T.psi0[k] * ldq<GL_R>(&qR[v * NST + k * sn]);
-    }
-    um[v] = (tlo || rlo) ? b : a;   // transmissive boundary: interior trace on both sides (R5)
-    up[v] = (thi || rhi) ? a : b;
-  }
-  // reflective wall (R22): the exterior state is the interior trace with the
-  // normal momentum negated
-  if (rlo) um[1 + DIR] = -um[1 + DIR];
-  if (rhi) up[1 + DIR] = -up[1 + DIR];
-  // equal traces (e.g. inside a constant region): eqn.rusanov and eqn.osher
-  // reduce exactly to f(q) — 0.5 (f + f) = f and the dissipation term is 0 — so one flux
-  // evaluation gives the bitwise-identical result
-  bool same = true;
-#pragma unroll
-  for (int v = 0; v < NV; ++v) same &= um[v] == up[v];
-  if (same) {
-    double f[NV], s0;
-    const bool ok = PH::template flux_speed<DIR>(um, gamma, ch, f, s0);
-#pragma unroll
-    for (int v = 0; v < NV; ++v) val[v] = wt * f[v];
-    return ok;
-  }
-  double fL[NV], fR[NV], sL, sR;
-  bool ok = PH::template flux_speed<DIR>(um, gamma, ch, fL, sL);
-  ok &= PH::template flux_speed<DIR>(up, gamma, ch, fR, sR);
-  if constexpr (FLUX == 1 && SYS == 0) {
-    double dis[NV];
-    ok &= osher_dissipation<D, DIR>(um, up, gamma, T, dis);
-#pragma unroll
-    for (int v = 0; v < NV; ++v) val[v] = wt * (0.5 * (fL[v] + fR[v]) - 0.5 * dis[v]);   // eqn.osher
-  } else {
-    const double smax = fmax(sL, sR);   // reading R4
-    const double hw = 0.5 * wt;         // eqn.rusanov with the 1/2 folded into the quadrature weight
-#pragma unroll
-    for (int v = 0; v < NV; ++v) val[v] = hw * ((fL[v] + fR[v]) - smax * (up[v] - um[v]));
-  }
-  return ok;
-}
-
 template <int D, int M, int SYS, int DIR, int FLUX>
 __device__ __forceinline__ bool point_flux(const double* __restrict__ q, long long cR, long long sd, int p, bool fok,
                                            bool tlo, bool thi, bool rlo, bool rhi, double wt, double gamma,
@@ -400,7 +325,6 @@ __device__ __forceinline__ bool point_flux(const double* __restrict__ q, long lo
                                                        wt, gamma, ch, T, val);
 }
 
-constexpr int pow2_at_least(int x) { return x <= 1 ? 1 : 2 * pow2_at_least((x + 1) / 2); }
 
 template <int D, int M, int SYS, int WARPS, int YC, int FLUX>
 __global__ void __launch_bounds__(WARPS * 32, (FLUX == 1) ? 5 : (SYS == 1 ? 4 : (D == 3 ? 7 : 8))) k_face_flux_cells(const double* __restrict__ q, double* __restrict__ F,
@@ -408,7 +332,7 @@ __global__ void __launch_bounds__(WARPS * 32, (FLUX == 1) ? 5 : (SYS == 1 ? 4 : 
                                                                 const int n2, const long long sy, const long long sz,
                                                                 const long long ncell, const double gamma,
                                                                 const double ch, const int bmask, const int rmask,
-                                                                DevCounters* __restrict__ cnt,
+                                                                DevCounters* __restrict__ cnt, const long long QSB,
                                                                 const __grid_constant__ DevTables T) {
   using PH = Phys<SYS, D>;
   constexpr int NV = PH::NV, N = M + 1, NS = ipow_c(N, D), NT = NS / N;
@@ -442,7 +366,7 @@ __global__ void __launch_bounds__(WARPS * 32, (FLUX == 1) ? 5 : (SYS == 1 ? 4 : 
   double v[KP];
   bool good = true;
   constexpr int K = D * NV;
-  constexpr int BLK = NV * NS * N;
+  const long long BLK = QSB;   // block stride
   // (tried and removed: staging the cell's own block in shared memory (1.6x
   // slower, bank conflicts) and an L1 prefetch of the D+1 blocks (8 % slower))
   const double* qown = q + cR * BLK;
@@ -725,13 +649,13 @@ void launch_weno_sweep(const KCtx& k, int sweep, const double* src, double* dst,
 }
 
 void launch_predictor(const KCtx& k, const double* w, double* q, const Box& region, const double dtdx[3],
-                      double tol, int max_sweeps, DevCounters* cnt, const double* dtdx_dev) {
-  launch_predictor_list(k, w, q, region, nullptr, 0, dtdx, tol, max_sweeps, cnt, nullptr, dtdx_dev);
+                      double tol, int max_sweeps, DevCounters* cnt, const double* dtdx_dev, long long qs) {
+  launch_predictor_list(k, w, q, region, nullptr, 0, dtdx, tol, max_sweeps, cnt, nullptr, dtdx_dev, qs);
 }
 
 void launch_predictor_list(const KCtx& k, const double* w, double* q, const Box& region, const int* list,
                            long long nlist, const double dtdx[3], double tol, int max_sweeps, DevCounters* cnt,
-                           const unsigned char* emask, const double* dtdx_dev) {
+                           const unsigned char* emask, const double* dtdx_dev, long long qs) {
   const long long count = list ? nlist : region.count();
   if (count == 0) return;
   ADER_DISPATCH(k.D, k.M, k.SYS, {
@@ -740,24 +664,27 @@ void launch_predictor_list(const KCtx& k, const double* w, double* q, const Box&
     constexpr int CPW = 32 / ((NS <= 8) ? 8 : (NS <= 16 ? 16 : 32));
     const size_t sm = pred_smem<D, M, SYS>();
     auto kern = k_predictor<D, M, SYS, kPredWarps>;
-    static bool attr = false;
-    if (!attr) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    static int attr_dev_mask = 0;   // the attribute is per device
+    if (!(attr_dev_mask & (1 << (dev & 31)))) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      attr = true;
+      attr_dev_mask |= 1 << (dev & 31);
     }
+    const long long qstride = qs > 0 ? qs : (long long)Phys<SYS, D>::NV * NS * N;
     // persistent grid: enough CTAs for every SM at full occupancy, a few times over
     const unsigned need = grid_for(count, kPredWarps * CPW);
     const unsigned g = need < 148u * 16u ? need : 148u * 16u;
     count_launch(k);
     kern<<<g, kPredWarps * 32, sm, k.stream>>>(w, q, region, k.sy, k.sz, dtdx[0], dtdx[1], dtdx[2], k.gamma,
-                                                k.ch, tol, max_sweeps, cnt, list, nlist, emask, dtdx_dev, k.tab);
+                                                k.ch, tol, max_sweeps, cnt, list, nlist, emask, dtdx_dev, qstride, k.tab);
   });
 }
 
 namespace {
 template <int D, int M, int SYS>
 void flux_cells_for(const KCtx& k, const double* q, double* F, const Box& ext, int H, const int n[3], int bmask,
-                    int rmask, DevCounters* cnt) {
+                    int rmask, DevCounters* cnt, long long qs) {
   constexpr int YC = 16;
   constexpr int NS = ipow_c(M + 1, D);
   constexpr int CPW = 32 / ((NS <= 8) ? 8 : (NS <= 16 ? 16 : 32));
@@ -768,19 +695,19 @@ void flux_cells_for(const KCtx& k, const double* q, double* F, const Box& ext, i
   if constexpr (SYS == 0) {
     if (k.tab.flux == 1) {   // eqn.osher (Euler only, checked at ader_create)
       k_face_flux_cells<D, M, SYS, kFluxWarps, YC, 1><<<g, kFluxWarps * 32, 0, k.stream>>>(
-          q, F, ext, H, n[0], n[1], n[2], k.sy, k.sz, k.ncell, k.gamma, k.ch, bmask, rmask, cnt, k.tab);
+          q, F, ext, H, n[0], n[1], n[2], k.sy, k.sz, k.ncell, k.gamma, k.ch, bmask, rmask, cnt, qs, k.tab);
       return;
     }
   }
   k_face_flux_cells<D, M, SYS, kFluxWarps, YC, 0><<<g, kFluxWarps * 32, 0, k.stream>>>(
-      q, F, ext, H, n[0], n[1], n[2], k.sy, k.sz, k.ncell, k.gamma, k.ch, bmask, rmask, cnt, k.tab);
+      q, F, ext, H, n[0], n[1], n[2], k.sy, k.sz, k.ncell, k.gamma, k.ch, bmask, rmask, cnt, qs, k.tab);
 }
 }  // namespace
 
 void launch_face_flux_cells(const KCtx& k, const double* q, double* F, const Box& ext, int H, const int n[3],
-                            int bmask, int rmask, DevCounters* cnt) {
+                            int bmask, int rmask, DevCounters* cnt, long long qs) {
   if (ext.count() == 0) return;
-  ADER_DISPATCH(k.D, k.M, k.SYS, (flux_cells_for<D, M, SYS>(k, q, F, ext, H, n, bmask, rmask, cnt)));
+  ADER_DISPATCH(k.D, k.M, k.SYS, (flux_cells_for<D, M, SYS>(k, q, F, ext, H, n, bmask, rmask, cnt, qs)));
 }
 
 void launch_update(const KCtx& k, double* u, const double* F, const Box& R, const double dtdx[3],

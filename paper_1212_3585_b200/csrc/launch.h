@@ -29,6 +29,8 @@ struct DevCounters {              // device-resident, zeroed by the host
   int err_code;                   // 0 ok, 1 inadmissible state, 2 predictor cap
   int err_stage;                  // 1 predictor, 2 flux, 3 update, 4 speed
   int pad;
+  unsigned long long err_any;     // multi-rank: max over the ranks of err_code (set before every
+                                  // host check, so all ranks stop at the same step)
 };
 
 // Device-resident step control of the uniform path: the time step is formed
@@ -65,13 +67,17 @@ bool supported(int D, int M, int SYS);
 void launch_weno_sweep(const KCtx& k, int sweep, const double* src, double* dst, const Box& region);
 // Predictor on `region`: w -> q.  dtdx_dev (optional): read dt/dx from the
 // device (StepState::dtdx) instead of dtdx.
+// qs: stride of a cell's q block in doubles (0 = nu N^(d+1); the uniform path
+// uses q_block_stride, the block size rounded up to even).
 void launch_predictor(const KCtx& k, const double* w, double* q, const Box& region, const double dtdx[3],
-                      double tol, int max_sweeps, DevCounters* cnt, const double* dtdx_dev = nullptr);
+                      double tol, int max_sweeps, DevCounters* cnt, const double* dtdx_dev = nullptr,
+                      long long qs = 0);
 // Predictor on the cells of an id list (AMR levels): w, q indexed by id.  If
 // emask is given only cells with emask[id] != 0 report solver errors.
 void launch_predictor_list(const KCtx& k, const double* w, double* q, const Box& region, const int* list,
                            long long nlist, const double dtdx[3], double tol, int max_sweeps, DevCounters* cnt,
-                           const unsigned char* emask = nullptr, const double* dtdx_dev = nullptr);
+                           const unsigned char* emask = nullptr, const double* dtdx_dev = nullptr,
+                           long long qs = 0);
 // Face fluxes on the lower face of every cell of `ext` (owned block + 1 on each
 // active axis), one lane group per cell computing all its lower faces
 // (L2-friendly traversal).  bmask bit 2*dir (2*dir+1): the first (last) face
@@ -79,7 +85,13 @@ void launch_predictor_list(const KCtx& k, const double* w, double* q, const Box&
 // on both sides; rmask, same bits: a reflective wall (R22), the exterior state
 // is the interior trace with the normal momentum negated.
 void launch_face_flux_cells(const KCtx& k, const double* q, double* F, const Box& ext, int H, const int n[3],
-                            int bmask, int rmask, DevCounters* cnt);
+                            int bmask, int rmask, DevCounters* cnt, long long qs);
+// The same fluxes (bitwise) with the q blocks streamed into shared memory by
+// bulk copies (flux_tma.cu); q blocks at stride q_block_stride(D, M, SYS).
+void launch_face_flux_tma(const KCtx& k, const double* q, double* F, const Box& ext, int H, const int n[3],
+                          int bmask, int rmask, DevCounters* cnt);
+// nu N^(d+1) rounded up to an even number of doubles (16-byte aligned blocks)
+long long q_block_stride(int D, int M, int SYS);
 // FV update of `interior` in place + max CFL speed of the new state.
 void launch_update(const KCtx& k, double* u, const double* F, const Box& interior, const double dtdx[3],
                    const double inv_dx[3], DevCounters* cnt, const double* dtdx_dev = nullptr);

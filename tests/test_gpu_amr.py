@@ -23,10 +23,10 @@ def gpu_cells(s):
 
 
 def pair(*, dim, degree, n, lo, hi, bc, ic, lmax, system=0, gamma=1.4, ch=0.0, cfl=0.45, chi_ref=0.2, chi_rec=0.1,
-         refine_factor=3, flux=0):
+         refine_factor=3, flux=0, adapt_every=1):
     cfg = ader.make_config(dim=dim, degree=degree, n0=n, lo=lo, hi=hi, bc=bc, system=system, gamma=gamma, ch=ch,
                            cfl=cfl, lmax=lmax, refine_factor=refine_factor, chi_ref=chi_ref, chi_rec=chi_rec,
-                           adapt_every=1, device=0, flux=flux)
+                           adapt_every=adapt_every, device=0, flux=flux)
     g = ader.Solver(cfg)
     g.set_initial(ic)
     o = O.AmrOracle(dim=dim, degree=degree, n=n, lo=lo, hi=hi, bc=bc, system=system, gamma=gamma, ch=ch, cfl=cfl,
@@ -45,6 +45,14 @@ def compare(g, o, tol):
     err = (np.abs(ug[act] - uo[act]).max(axis=0) / scale).max()
     assert err <= tol, err
     return err
+
+
+def check_margin(mg, mo):
+    """min_threshold_margin (ABI 4): how close chi came to the strict thresholds
+    (P:622-624).  Both sides see it above 1e-8, so averages that agree to
+    <= 1e-9 cannot flip a refinement decision, and the two agree."""
+    assert mo > 1e-8 and mg > 1e-8, (mg, mo)
+    assert abs(mg - mo) <= 1e-6 * max(1.0, abs(mo)), (mg, mo)
 
 
 CASES = {
@@ -81,6 +89,7 @@ def test_one_macro_step(name):
     assert abs(rg.dt0 - dt_o) <= 1e-14 * dt_o
     assert list(rg.updates_per_level) == list(ro.updates_per_level)
     compare(g, o, 1e-11)
+    check_margin(rg.min_threshold_margin, ro.min_threshold_margin)
 
 
 @pytest.mark.parametrize("name", ["explosion2d_l2", "vortex2d_M3_l1", "explosion2d_l2_osher",
@@ -91,6 +100,7 @@ def test_several_macro_steps_with_adapt(name):
     ro = o.step(1e300, 4)
     assert rg.cell_updates == ro.cell_updates
     compare(g, o, 1e-9)
+    check_margin(rg.min_threshold_margin, ro.min_threshold_margin)
 
 
 def test_c3_full_size_first_macro_steps():
@@ -105,6 +115,7 @@ def test_c3_full_size_first_macro_steps():
         ro = o.step(1e300, 1)
         assert list(rg.updates_per_level) == list(ro.updates_per_level)
         compare(g, o, 1e-10)
+        check_margin(rg.min_threshold_margin, ro.min_threshold_margin)
 
 
 def test_c5_full_size_first_macro_step():
@@ -131,6 +142,7 @@ def test_full_time_twin(name, n, t_end):
     ro = o.step(t_end, 10 ** 6)
     assert rg.macro_steps == ro.steps and rg.cell_updates == ro.cell_updates
     compare(g, o, 1e-8)
+    check_margin(rg.min_threshold_margin, ro.min_threshold_margin)
 
 
 def test_amr_conservation_periodic():
@@ -146,3 +158,22 @@ def test_amr_conservation_periodic():
     g.step(1e300, 3)
     t1 = tot()
     assert np.all(np.abs(t1 - t0) <= 1e-13 * np.maximum(1.0, np.abs(t0)))
+
+
+@pytest.mark.parametrize("name", ["explosion2d_l2", "vortex2d_M3_l1", "explosion3d_l1"])
+def test_refine_through_the_abi(name):
+    # ader_refine (one adapt pass at synchronized time) against the
+    # oracle's adapt(): frozen mesh for 2 macro steps, then one explicit adapt
+    g, o = pair(**CASES[name], adapt_every=0)
+    g.step(1e300, 2)
+    o.step(1e300, 2, adapt_every=0)
+    compare(g, o, 1e-10)
+    rg = g.refine()
+    o.adapt()
+    compare(g, o, 1e-10)
+    check_margin(rg.min_threshold_margin, o.margin())
+    # and the refined mesh keeps stepping in parity
+    rg = g.step(1e300, 1)
+    ro = o.step(1e300, 1, adapt_every=0)
+    assert list(rg.updates_per_level) == list(ro.updates_per_level)
+    compare(g, o, 1e-10)
