@@ -118,8 +118,9 @@ struct ader_ctx {
   bool prof = false;
   std::vector<ProfRec> recs;
   std::vector<cudaEvent_t> ev_pool;
-  unsigned long long prof_sweeps0 = 0;
-  double kflops_sweep = 0.0;                   // predictor flops per cell per sweep
+  unsigned long long prof_sweeps0 = 0, prof_cells0 = 0;
+  double kflops_sweep = 0.0;                   // predictor flops per cell per (full) sweep
+  double kflops_first = 0.0;                   // the first sweep (time-constant guess: N^d flux evaluations)
   long long launches = 0;                      // kernels launched by this context
   AmrState* amr = nullptr;                     // lmax > 0: device-resident AMR
   ProfHook hook;
@@ -321,6 +322,12 @@ double pred_sweep_flops(const ader_ctx* c) {
   // NST flux evaluations + NV*NST*(2 d N [D contractions] + 2 N [T_tau] + 1 [dq])
   return c->NST * flux_eval_flops(c->cfg.system, c->d) + (double)c->nv * c->NST * (2.0 * c->d * c->N + 2.0 * c->N + 1.0);
 }
+double pred_first_sweep_flops(const ader_ctx* c) {
+  // sweep 1 from the time-constant guess (kernels: predictor.cuh): N^d flux
+  // evaluations, the D contractions on one time level (2 d N per dof), then
+  // N time levels of w - Tsum_s G (2 flops) and the dq bookkeeping (1)
+  return c->NS * flux_eval_flops(c->cfg.system, c->d) + (double)c->nv * c->NS * (2.0 * c->d * c->N + 3.0 * c->N);
+}
 double face_flops(const ader_ctx* c) {
   double two_point = (c->cfg.system == ADER_EULER) ? 2.0 * (12 + 2 * c->d) + 4.0 * c->nv : 2.0 * 90 + 4.0 * c->nv;
   if (c->cfg.flux == ADER_FLUX_OSHER) {
@@ -470,6 +477,42 @@ void run_predictor(ader_ctx* c, double dt, const double* dtdx_dev = nullptr) {
   for (int k = 0; k < c->d; ++k) dtdx[k] = dt / c->dx[k];
   Scope s(c, ADER_K_PRED, 0.0);   // flops from the sweep counter (ader_kernel_stats)
   launch_predictor(c->k, c->w, c->q, r, dtdx, c->cfg.pred_tol, c->cfg.pred_max_sweeps, c->cnt, dtdx_dev, c->qs);
+}
+
+// a1 + a2 fused (weno_pred.cu): the WENO sweeps and the predictor in one tile
+// walk, w_x / w_xy / w kept on chip (ADER_WENO_PRED=0: separate kernels)
+bool fused_weno_pred() {
+  static const int on = [] {
+    const char* e = std::getenv("ADER_WENO_PRED");
+    return (e && e[0] == '1') ? 1 : 0;
+  }();
+  return on != 0;
+}
+
+void run_weno_predictor(ader_ctx* c, double dt, const double* dtdx_dev = nullptr) {
+  Box r = grown(c, 1);
+  const int tm = transmissive_mask(c) | reflective_mask(c);   // as run_predictor (R5, R22)
+  for (int a = 0; a < c->d; ++a) {
+    if (tm & (1 << (2 * a))) { r.lo[a] += 1; r.ext[a] -= 1; }
+    if (tm & (1 << (2 * a + 1))) r.ext[a] -= 1;
+  }
+  double dtdx[3] = {0, 0, 0};
+  for (int k = 0; k < c->d; ++k) dtdx[k] = dt / c->dx[k];
+  // algorithmic WENO flops: the problems of the three sweeps on the boxes the
+  // unfused path needs (run_weno); predictor flops come from the sweep counter
+  const int H = c->H, M = c->M, zH = c->d == 3 ? H : 0;
+  const int nx = c->n[0], ny = c->n[1], nz = c->n[2];
+  double wf;
+  if (c->d == 2) {
+    const Box rx = make_box(H - 1, H + nx + 1, H - 1 - M, H + ny + 1 + M, 0, 1);
+    wf = weno_problem_flops(M) * (rx.count() * c->nv + r.count() * c->nv * c->N);
+  } else {
+    const Box rx = make_box(H - 1, H + nx + 1, H - 1 - M, H + ny + 1 + M, zH - 1 - M, zH + nz + 1 + M);
+    const Box ry = make_box(H - 1, H + nx + 1, H - 1, H + ny + 1, zH - 1 - M, zH + nz + 1 + M);
+    wf = weno_problem_flops(M) * (rx.count() * c->nv + ry.count() * c->nv * c->N + r.count() * c->nv * c->N * c->N);
+  }
+  Scope s(c, ADER_K_PRED, wf);
+  launch_weno_predictor(c->k, c->u, c->q, r, c->qs, dtdx, c->cfg.pred_tol, c->cfg.pred_max_sweeps, c->cnt, dtdx_dev);
 }
 
 void face_boxes(const ader_ctx* c, Box fb[3]) {
@@ -745,6 +788,7 @@ static ader_status create_impl(const ader_config* cfg, ader_ctx** out, bool loop
   c->hook.end = hook_end;
   c->k.hook = &c->hook;
   c->kflops_sweep = pred_sweep_flops(c);
+  c->kflops_first = pred_first_sweep_flops(c);
   if (cfg->lmax > 0) {
     // device-resident cell-by-cell AMR (amr.cpp); uniform buffers are not used
     CK(cudaMalloc(&c->cnt, sizeof(DevCounters)));
@@ -832,6 +876,7 @@ static ader_status create_impl(const ader_config* cfg, ader_ctx** out, bool loop
     }
   }
   c->kflops_sweep = pred_sweep_flops(c);
+  c->kflops_first = pred_first_sweep_flops(c);
   return ADER_OK;
 }
 
@@ -967,7 +1012,8 @@ namespace {
 // second half of a uniform macro step, after the ghost fill + WENO: predictor,
 // face fluxes, update (fused with the next CFL speed)
 void advance_dt(ader_ctx* c, double dt, const double* dtdx_dev = nullptr) {
-  run_predictor(c, dt, dtdx_dev);
+  if (fused_weno_pred()) run_weno_predictor(c, dt, dtdx_dev);
+  else run_predictor(c, dt, dtdx_dev);
   run_flux(c);
   cudaMemsetAsync(&c->cnt->speed_bits, 0, sizeof(unsigned long long), c->k.stream);
   run_update(c, dt, dtdx_dev);
@@ -981,7 +1027,8 @@ void advance_dt(ader_ctx* c, double dt, const double* dtdx_dev = nullptr) {
 ader_status enqueue_step(ader_ctx* c, double t_end) {
   ader_status st = fill_halo(c, c->u);
   if (st != ADER_OK) return st;
-  run_weno(c);
+  const bool fused = fused_weno_pred();
+  if (!fused) run_weno(c);
   {
     Scope sc(c, ADER_K_OTHER, 0.0);
     if (!c->speed_valid) {
@@ -992,7 +1039,8 @@ ader_status enqueue_step(ader_ctx* c, double t_end) {
       NK(g_nccl.AllReduce(&c->cnt->speed_bits, &c->cnt->speed_bits, 1, ncclUint64, ncclMax, c->comm, c->k.stream));
     launch_step_dt(c->k, c->cnt, c->st, c->cfg.cfl, t_end, c->dx);
   }
-  run_predictor(c, 0.0, c->st->dtdx);
+  if (fused) run_weno_predictor(c, 0.0, c->st->dtdx);
+  else run_predictor(c, 0.0, c->st->dtdx);
   run_flux(c);
   CK(cudaMemsetAsync(&c->cnt->speed_bits, 0, sizeof(unsigned long long), c->k.stream));
   run_update(c, 0.0, c->st->dtdx);
@@ -1206,7 +1254,7 @@ ader_status ader_debug_group_step(ader_ctx** cs, int32_t n, double t_end, int64_
     }
     double speed = 0.0;
     for (int i = 0; i < n && st == ADER_OK; ++i) {
-      run_weno(cs[i]);
+      if (!fused_weno_pred()) run_weno(cs[i]);
       double s = 0.0;
       st = global_speed(cs[i], &s);   // no communicator: this rank's max
       speed = std::max(speed, s);
@@ -1251,6 +1299,7 @@ ader_status ader_set_profiling(ader_ctx* c, int32_t on) {
   c->prof = on != 0;
   CK(cudaMemcpy(c->hcnt, c->cnt, sizeof(DevCounters), cudaMemcpyDeviceToHost));
   c->prof_sweeps0 = c->hcnt->sweeps;
+  c->prof_cells0 = c->hcnt->cells;
   return ADER_OK;
 }
 
@@ -1272,7 +1321,14 @@ ader_status ader_kernel_stats(ader_ctx* c, double ms[ADER_K_COUNT], int64_t laun
     if (flops) flops[r.kind] += r.flops;
   }
   CK(cudaMemcpy(c->hcnt, c->cnt, sizeof(DevCounters), cudaMemcpyDeviceToHost));
-  if (flops) flops[ADER_K_PRED] = (double)(c->hcnt->sweeps - c->prof_sweeps0) * c->kflops_sweep;
+  // predictor flops from the device counters: every predicted cell's first
+  // sweep at its real cost, the later sweeps as full sweeps (plus, for the fused
+  // WENO + predictor kernel, the WENO flops its scopes carry)
+  if (flops) {
+    const double cells = (double)(c->hcnt->cells - c->prof_cells0);
+    const double sweeps = (double)(c->hcnt->sweeps - c->prof_sweeps0);
+    flops[ADER_K_PRED] += cells * c->kflops_first + (sweeps - cells) * c->kflops_sweep;
+  }
   if (std::getenv("ADER_GAP_TRACE") && c->recs.size() > 1) {
     // diagnostics: idle gaps of the stream between consecutive timed scopes
     std::vector<std::pair<float, int>> gaps;
@@ -1326,7 +1382,8 @@ ader_status ader_debug_dump(ader_ctx* c, int32_t what, double dt, double* out, i
     CK(cudaStreamSynchronize(c->k.stream));
     return ADER_OK;
   }
-  run_predictor(c, dt);
+  if (fused_weno_pred()) run_weno_predictor(c, dt);
+  else run_predictor(c, dt);
   if (what == 1) {
     if (capacity < b.count() * c->nv * c->NST) return fail(c, ADER_ERR_ARG, "capacity too small");
     launch_gather(c->k, c->q, (int)c->qs, b, c->stage);

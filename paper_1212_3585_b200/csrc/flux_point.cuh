@@ -15,42 +15,44 @@ __device__ __forceinline__ double ldq(const double* p) {
   else return *p;
 }
 
-// One space-time quadrature point of the face between the cell blocks qL0
-// (lower side) and qR0 (upper side), [NV][N^(D+1)] each, in global (GL_L,
-// GL_R) or shared memory.
-template <int D, int M, int SYS, int DIR, int FLUX, bool GL_L, bool GL_R = GL_L>
-__device__ __forceinline__ bool point_flux_blocks(const double* qL0, const double* qR0, int p, bool fok, bool tlo,
-                                                  bool thi, bool rlo, bool rhi, double wt, double gamma, double ch,
-                                                  const DevTables& T, double* val) {
-  using PH = Phys<SYS, D>;
-  constexpr int NV = PH::NV, N = M + 1, NS = ipow_c(N, D), NST = NS * N;
-  constexpr int NT = NS / N;
-#pragma unroll
-  for (int v = 0; v < NV; ++v) val[v] = 0.0;
-  if (!fok) return true;
+// Trace of a cell block [NV][N^(D+1)] (space fastest, time slowest) on the face
+// normal to DIR at the face's space-time point p (p = (tangential nodes, time
+// node), tangential axes in increasing order, time slowest):
+//   out[v] = sum_a psi[a] q[v][... node a along DIR ...]
+// psi = psi1 (xi = 1, the lower cell's side of a face) or psi0 (xi = 0).
+template <int D, int M, int NV, int DIR, bool GL>
+__device__ __forceinline__ void face_trace(const double* q0, int p, const double (&psi)[kMaxN], double (&out)[NV]) {
+  constexpr int N = M + 1, NS = ipow_c(N, D), NST = NS * N, NT = NS / N;
   const int s = p / NT, t = p - s * NT;
   const int t1 = t % N, t2 = t / N;
   constexpr int ax0 = (DIR == 0) ? 1 : 0;
   constexpr int ax1 = (DIR == 2) ? 1 : 2;
   constexpr int sn = ipow_c(N, DIR);
   const int base = s * NS + t1 * ipow_c(N, ax0) + (D == 3 ? t2 * ipow_c(N, ax1) : 0);
-  const double* qL = qL0 + base;
-  const double* qR = qR0 + base;
-  // both traces unpredicated (the padded grid holds a ghost layer on every
-  // side, so the far-side reads stay in bounds; their values are discarded at
-  // transmissive boundaries)
+  const double* q = q0 + base;
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    double a = psi[0] * ldq<GL>(&q[v * NST]);
+#pragma unroll
+    for (int k = 1; k < N; ++k) a += psi[k] * ldq<GL>(&q[v * NST + k * sn]);
+    out[v] = a;
+  }
+}
+
+// The two-point flux of one face point from the raw traces a (q_h^-, xi = 1 of
+// the lower cell) and b (q_h^+, xi = 0 of the upper cell), with the boundary
+// flags of the face, times the quadrature weight wt.
+template <int D, int SYS, int DIR, int FLUX>
+__device__ __forceinline__ bool point_flux_states(const double (&a)[Phys<SYS, D>::NV], const double (&b)[Phys<SYS, D>::NV],
+                                                  bool tlo, bool thi, bool rlo, bool rhi, double wt, double gamma,
+                                                  double ch, const DevTables& T, double* val) {
+  using PH = Phys<SYS, D>;
+  constexpr int NV = PH::NV;
   double um[NV], up[NV];
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
-    double a = T.psi1[0] * ldq<GL_L>(&qL[v * NST]);   // q_h^- (xi = 1 of the left cell)
-    double b = T.psi0[0] * ldq<GL_R>(&qR[v * NST]);   // q_h^+ (xi = 0 of the right cell)
-#pragma unroll
-    for (int k = 1; k < N; ++k) {
-      a += T.psi1[k] * ldq<GL_L>(&qL[v * NST + k * sn]);
-      b += T.psi0[k] * ldq<GL_R>(&qR[v * NST + k * sn]);
-    }
-    um[v] = (tlo || rlo) ? b : a;   // transmissive boundary: interior trace on both sides (R5)
-    up[v] = (thi || rhi) ? a : b;
+    um[v] = (tlo || rlo) ? b[v] : a[v];   // transmissive boundary: interior trace on both sides (R5)
+    up[v] = (thi || rhi) ? a[v] : b[v];
   }
   // reflective wall (R22): the exterior state is the interior trace with the
   // normal momentum negated
@@ -84,6 +86,26 @@ __device__ __forceinline__ bool point_flux_blocks(const double* qL0, const doubl
     for (int v = 0; v < NV; ++v) val[v] = hw * ((fL[v] + fR[v]) - smax * (up[v] - um[v]));
   }
   return ok;
+}
+
+// One space-time quadrature point of the face between the cell blocks qL0
+// (lower side) and qR0 (upper side), [NV][N^(D+1)] each, in global (GL_L,
+// GL_R) or shared memory.
+template <int D, int M, int SYS, int DIR, int FLUX, bool GL_L, bool GL_R = GL_L>
+__device__ __forceinline__ bool point_flux_blocks(const double* qL0, const double* qR0, int p, bool fok, bool tlo,
+                                                  bool thi, bool rlo, bool rhi, double wt, double gamma, double ch,
+                                                  const DevTables& T, double* val) {
+  constexpr int NV = Phys<SYS, D>::NV;
+#pragma unroll
+  for (int v = 0; v < NV; ++v) val[v] = 0.0;
+  if (!fok) return true;
+  // both traces unpredicated (the padded grid holds a ghost layer on every
+  // side, so the far-side reads stay in bounds; their values are discarded at
+  // transmissive boundaries)
+  double a[NV], b[NV];
+  face_trace<D, M, NV, DIR, GL_L>(qL0, p, T.psi1, a);   // q_h^- (xi = 1 of the left cell)
+  face_trace<D, M, NV, DIR, GL_R>(qR0, p, T.psi0, b);   // q_h^+ (xi = 0 of the right cell)
+  return point_flux_states<D, SYS, DIR, FLUX>(a, b, tlo, thi, rlo, rhi, wt, gamma, ch, T, val);
 }
 
 }  // namespace ader

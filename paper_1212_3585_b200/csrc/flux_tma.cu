@@ -73,160 +73,241 @@ __device__ __forceinline__ void record_error_flux(DevCounters* c, long long cell
   }
 }
 
-template <int D, int M, int SYS, int LX>
-struct FluxTma {
+// Tile walk: a CTA owns a tile of TX x TY cells (3D: x, y; 2D: TX cells along
+// x, TY = 1) and walks it along the last axis W (z in 3D, y in 2D).  Per step
+// (one level w) it copies the tile's rows plus the -x column and (3D) the -y row
+// into a stage of a three-stage ring: TY+1 rows (3D; 1 row in 2D) of TX+1
+// consecutive blocks, one bulk copy per row.  The -W neighbour is the previous
+// level: its upper-W traces were computed one step earlier and are carried in
+// shared memory, so no block is copied twice along W.  Step 0 of a tile loads
+// the level below the first face level and only computes those traces.
+template <int D, int M, int SYS>
+struct FluxWalk {
   static constexpr int NV = Phys<SYS, D>::NV, N = M + 1, NS = ipow_c(N, D);
   static constexpr int BLK = NV * NS * N;           // doubles per cell block
   static constexpr int QS = BLK + (BLK & 1);        // block stride: 16-byte aligned blocks
   static constexpr int G = (NS <= 8) ? 8 : (NS <= 16 ? 16 : 32);
   static constexpr int CPW = 32 / G;                // lane groups per warp
-  static constexpr int WARPS = LX * D / CPW;
-  static_assert((LX * D) % CPW == 0 && LX % CPW == 0, "a warp's lane groups share one direction");
-  static constexpr int SEG = (LX + 1) + (D - 1) * LX;   // blocks per stage
-  static constexpr int STAGE = SEG * QS;                // doubles per stage
-  static constexpr int RED = NV * (G + 1);              // reduction buffer per lane group
+  static constexpr int TX = (D == 3) ? (SYS == 1 ? 2 : 4) : 8;
+  static constexpr int TY = (D == 3) ? 2 : 1;
+  static constexpr int CELLS = TX * TY;
+  static constexpr int GROUPS = CELLS * D;          // (cell, face dir) lane groups
+  static constexpr int WARPS = GROUPS / CPW;
+  static_assert(CELLS % CPW == 0, "a warp's lane groups share one direction");
+  static constexpr int ROWS = (D == 3) ? TY + 1 : 1;
+  static constexpr int RB = TX + 1;                 // blocks per row
+  static constexpr int NSTAGE = 3;
+  static constexpr int STAGE = ROWS * RB * QS;      // doubles per stage
+  static constexpr int TRC = CELLS * NV * NS;       // carried upper-W traces of one level
+  static constexpr int RED = NV * (G + 1);          // point-sum buffer per lane group
+  static constexpr int K = (G / NV) < 1 ? 1 : (G / NV);   // partial sums per variable
+  static constexpr int CH = (NS + K - 1) / K;             // points per partial sum
   static constexpr size_t smem_bytes() {
-    return sizeof(double) * (2 * (size_t)STAGE + (size_t)WARPS * CPW * RED) + 2 * sizeof(unsigned long long);
+    return sizeof(double) * ((size_t)NSTAGE * STAGE + 2 * (size_t)TRC + (size_t)GROUPS * RED) +
+           NSTAGE * sizeof(unsigned long long);
   }
+  static_assert(smem_bytes() <= 227 * 1024, "shared memory of one CTA");
+  static constexpr int MINB = (D == 3) ? 1 : 2;     // CTAs per SM the registers are sized for
 };
 
-constexpr int kFluxYC = 16;
-
-template <int D, int M, int SYS, int FLUX, int LX, int MINB>
-__global__ void __launch_bounds__(FluxTma<D, M, SYS, LX>::WARPS * 32, MINB)
-    k_face_flux_tma(const double* __restrict__ q, double* __restrict__ F, const Box E, const int H, const int n0,
-                    const int n1, const int n2, const long long sy, const long long sz, const long long ncell,
-                    const double gamma, const double ch, const int bmask, const int rmask,
-                    DevCounters* __restrict__ cnt, const unsigned nrx, const unsigned nruns,
-                    const __grid_constant__ DevTables T) {
-  using C = FluxTma<D, M, SYS, LX>;
+template <int D, int M, int SYS, int FLUX>
+__global__ void __launch_bounds__(FluxWalk<D, M, SYS>::WARPS * 32, FluxWalk<D, M, SYS>::MINB)
+    k_face_flux_walk(const double* __restrict__ q, double* __restrict__ F, const Box E, const int H, const int n0,
+                     const int n1, const int n2, const long long sy, const long long sz, const long long ncell,
+                     const double gamma, const double ch, const int bmask, const int rmask,
+                     DevCounters* __restrict__ cnt, const int ntx, const int nty, const int ntiles,
+                     const __grid_constant__ DevTables T) {
+  using C = FluxWalk<D, M, SYS>;
   constexpr int NV = C::NV, N = C::N, NS = C::NS, NT = NS / N, QS = C::QS, G = C::G, CPW = C::CPW;
+  constexpr int TX = C::TX, TY = C::TY, RB = C::RB, W = D - 1;
   extern __shared__ __align__(128) double smem[];
-  double* red = smem + 2 * C::STAGE;
-  unsigned long long* bars = reinterpret_cast<unsigned long long*>(red + C::WARPS * CPW * C::RED);
+  double* trc = smem + C::NSTAGE * C::STAGE;              // [2][CELLS][NV][NS]
+  double* red = trc + 2 * C::TRC;
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(red + C::GROUPS * C::RED);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nsteps = E.ext[W] + 1;                        // + the level below the first face level
+  const long long ssW = (D == 3) ? sz : sy;               // stride along W
+  const long long total = (long long)((ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x) * nsteps;
 
-  // geometry of run `run`: first cell x0, row (cy, cz), valid cells nval
-  auto run_geom = [&](unsigned run, int& x0, int& cy, int& cz, int& nval) -> bool {
-    const unsigned xr = run % nrx;
-    const unsigned t = run / nrx;
-    const int yi = (int)(t % kFluxYC);
-    const unsigned t2 = t / kFluxYC;
-    const unsigned ez = (unsigned)E.ext[2];
-    const int y = (int)(t2 / ez) * kFluxYC + yi;
-    if (y >= E.ext[1]) return false;
-    cz = E.lo[2] + (int)(t2 % ez);
-    cy = E.lo[1] + y;
-    x0 = E.lo[0] + (int)xr * LX;
-    nval = min(LX, E.lo[0] + E.ext[0] - x0);
+  // tile t: tiles are numbered in patches of 12 x 12 (x fastest inside a patch,
+  // patches row by row, partial patches at the edges), so the tiles a round of
+  // CTAs walks together are compact and the halo rows / columns they copy from
+  // each other stay in L2
+  auto tile_xy = [&](int t, int& tx, int& ty) {
+    const int pyi = t / (12 * ntx);
+    const int hy = min(12, nty - 12 * pyi);
+    const int r = t - pyi * 12 * ntx;
+    const int pxi = r / (12 * hy);
+    const int r2 = r - pxi * 12 * hy;
+    const int wx = min(12, ntx - 12 * pxi);
+    tx = 12 * pxi + r2 % wx;
+    ty = 12 * pyi + r2 / wx;
+  };
+  // geometry of CTA step g: tile origin, valid extent, level
+  auto geom = [&](long long g, int& x0, int& y0, int& nvx, int& nvy, int& k) -> bool {
+    const int it = (int)(g / nsteps);
+    k = (int)(g - (long long)it * nsteps);
+    int tx, ty;
+    tile_xy((int)blockIdx.x + it * (int)gridDim.x, tx, ty);
+    if (ty >= nty) return false;
+    x0 = E.lo[0] + tx * TX;
+    nvx = min(TX, E.lo[0] + E.ext[0] - x0);
+    if (D == 3) {
+      y0 = E.lo[1] + ty * TY;
+      nvy = min(TY, E.lo[1] + E.ext[1] - y0);
+    } else {
+      y0 = 0;
+      nvy = 1;
+    }
     return true;
   };
-  // producer (one thread): copy the rows of `run` into stage s
-  auto issue = [&](unsigned run, int s) {
+  // producer: the rows of step g into stage s
+  auto issue = [&](long long g, int s) {
     unsigned long long* bar = bars + s;
-    int x0, cy, cz, nval;
-    if (run >= nruns || !run_geom(run, x0, cy, cz, nval)) {
+    int x0, y0, nvx, nvy, k;
+    if (g >= total || !geom(g, x0, y0, nvx, nvy, k)) {
       mbar_arrive_expect_tx(bar, 0u);
       return;
     }
-    const long long c0 = (long long)x0 + cy * sy + cz * sz;
+    const int w = E.lo[W] - 1 + k;                       // level of this step
     double* sb = smem + s * C::STAGE;
-    const unsigned own = (unsigned)((nval + 1) * QS * sizeof(double));
-    const unsigned oth = (unsigned)(nval * QS * sizeof(double));
-    mbar_arrive_expect_tx(bar, own + (D - 1) * oth);
-    bulk_g2s(sb, q + (c0 - 1) * QS, own, bar);
-    bulk_g2s(sb + (LX + 1) * QS, q + (c0 - sy) * QS, oth, bar);
-    if constexpr (D == 3) bulk_g2s(sb + (2 * LX + 1) * QS, q + (c0 - sz) * QS, oth, bar);
+    const unsigned rowb = (unsigned)((nvx + 1) * QS * sizeof(double));
+    if constexpr (D == 3) {
+      mbar_arrive_expect_tx(bar, rowb * (unsigned)(nvy + 1));
+      for (int r = 0; r <= nvy; ++r) {
+        const long long c0 = (long long)(x0 - 1) + (long long)(y0 - 1 + r) * sy + (long long)w * sz;
+        bulk_g2s(sb + r * RB * QS, q + c0 * QS, rowb, bar);
+      }
+    } else {
+      mbar_arrive_expect_tx(bar, rowb);
+      bulk_g2s(sb, q + ((long long)(x0 - 1) + (long long)w * sy) * QS, rowb, bar);
+    }
   };
 
   if (tid == 0) {
-    mbar_init(bars + 0, 1);
-    mbar_init(bars + 1, 1);
+#pragma unroll
+    for (int i = 0; i < C::NSTAGE; ++i) mbar_init(bars + i, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  if (tid == 0) {
-    issue(blockIdx.x, 0);
-    issue(blockIdx.x + gridDim.x, 1);
-  }
+  if (tid == 0)
+    for (int i = 0; i < C::NSTAGE; ++i) issue(i, i);
 
-  const int dir = warp % D;                       // warp-uniform face direction
-  const int slot = lane / G, p = lane & (G - 1);
-  const int ci = (warp / D) * CPW + slot;         // cell of the run
+  // lane group: (cell ci, face dir); dir uniform per warp
+  const int grp = warp * CPW + lane / G;
+  const int dir = grp / C::CELLS;
+  const int ci = grp - dir * C::CELLS;
+  const int cxi = ci % TX, cyi = ci / TX;
+  const int p = lane & (G - 1);
   const bool pok = p < NS;
   const int ps = pok ? p : 0;
   const int s_ = ps / NT, tt = ps - (ps / NT) * NT;
   double wt = T.w[s_] * T.w[tt % N];
   if (D == 3) wt *= T.w[tt / N];
-  double* rb = red + (warp * CPW + slot) * C::RED;   // [NV][G+1]
+  double* rb = red + grp * C::RED;                        // [NV][G+1]
   const int zH = (D == 3) ? H : 0;
-  bool good = true;
+  const int lvl_hi = (D == 3) ? zH + n2 : H + n1;          // last face level along W
 
-  for (unsigned k = 0;; ++k) {
-    const unsigned run = blockIdx.x + k * gridDim.x;
-    if (run >= nruns) break;
-    const int s = (int)(k & 1u);
-    mbar_wait_parity(bars + s, (k >> 1) & 1u);
-    int x0, cy, cz, nval;
-    if (run_geom(run, x0, cy, cz, nval)) {
-      const int cx = x0 + ci;
-      const bool ok = ci < nval;
-      const long long cR = ok ? (long long)cx + cy * sy + cz * sz : 0;
-      const bool inx = cx < H + n0, iny = cy < H + n1, inz = (D == 2) || cz < zH + n2;
+  for (long long g = 0; g < total; ++g) {
+    const int s = (int)(g % C::NSTAGE);
+    mbar_wait_parity(bars + s, (unsigned)((g / C::NSTAGE) & 1));
+    int x0, y0, nvx, nvy, k;
+    if (geom(g, x0, y0, nvx, nvy, k)) {
       const double* sb = smem + s * C::STAGE;
-      const double* qR = sb + (ci + 1) * QS;
-      double v[NV];
-      bool face_ok;
-      if (dir == 0) {
-        face_ok = ok && iny && inz;
-        good &= point_flux_blocks<D, M, SYS, 0, FLUX, false>(
-            sb + ci * QS, qR, ps, face_ok && pok, (bmask & 1) && cx == H, (bmask & 2) && cx == H + n0,
-            (rmask & 1) && cx == H, (rmask & 2) && cx == H + n0, wt, gamma, ch, T, v);
-      } else if (dir == 1) {
-        face_ok = ok && inx && inz;
-        good &= point_flux_blocks<D, M, SYS, 1, FLUX, false>(
-            sb + (LX + 1 + ci) * QS, qR, ps, face_ok && pok, (bmask & 4) && cy == H, (bmask & 8) && cy == H + n1,
-            (rmask & 4) && cy == H, (rmask & 8) && cy == H + n1, wt, gamma, ch, T, v);
-      } else {
-        face_ok = ok && inx && iny;
-        if constexpr (D == 3)
-          good &= point_flux_blocks<D, M, SYS, D - 1, FLUX, false>(
-              sb + (2 * LX + 1 + ci) * QS, qR, ps, face_ok && pok, (bmask & 16) && cz == zH,
-              (bmask & 32) && cz == zH + n2, (rmask & 16) && cz == zH, (rmask & 32) && cz == zH + n2, wt, gamma,
-              ch, T, v);
-      }
-      if (!good) {
-        record_error_flux(cnt, cR);
-        good = true;
-      }
-      // point sums in point order (the order of k_face_flux_cells)
-      if (pok) {
+      const int w = E.lo[W] - 1 + k;
+      const bool cell_in = cxi < nvx && cyi < nvy;
+      const int cx = x0 + cxi, cy = (D == 3) ? y0 + cyi : w, cz = (D == 3) ? w : 0;
+      const int row = (D == 3) ? cyi + 1 : 0;
+      const double* qown = sb + (row * RB + cxi + 1) * QS;
+      double* tw = trc + (k & 1) * C::TRC + ci * NV * NS;          // this level's upper-W traces
+      const double* tr = trc + ((k + 1) & 1) * C::TRC + ci * NV * NS;   // the level below
+      if (k == 0) {
+        // the level below the first face level: its upper-W traces only
+        if (dir == W && cell_in && pok) {
+          double a[NV];
+          face_trace<D, M, NV, W, false>(qown, ps, T.psi1, a);
 #pragma unroll
-        for (int i = 0; i < NV; ++i) rb[i * (G + 1) + p] = v[i];
-      }
-      __syncwarp();
-      if (p < NV && face_ok) {
-        const double* row = rb + p * (G + 1);
-        double acc = row[0];
+          for (int v = 0; v < NV; ++v) tw[v * NS + ps] = a[v];
+        }
+      } else if (cell_in) {
+        const long long cR = (long long)cx + cy * sy + (long long)cz * sz;
+        const bool inx = cx < H + n0, iny = cy < H + n1, inz = (D == 2) || cz < zH + n2;
+        double v[NV];
+        bool face_ok, good = true;
+        if (dir == 0) {
+          face_ok = iny && inz;
+          good = point_flux_blocks<D, M, SYS, 0, FLUX, false>(
+              qown - QS, qown, ps, face_ok && pok, (bmask & 1) && cx == H, (bmask & 2) && cx == H + n0,
+              (rmask & 1) && cx == H, (rmask & 2) && cx == H + n0, wt, gamma, ch, T, v);
+        } else if (D == 3 && dir == 1) {
+          face_ok = inx && inz;
+          good = point_flux_blocks<D, M, SYS, (D == 3 ? 1 : 0), FLUX, false>(
+              qown - RB * QS, qown, ps, face_ok && pok, (bmask & 4) && cy == H, (bmask & 8) && cy == H + n1,
+              (rmask & 4) && cy == H, (rmask & 8) && cy == H + n1, wt, gamma, ch, T, v);
+        } else {
+          // the W face: lower side = carried upper trace of the level below;
+          // then this level's upper traces for the next step
+          face_ok = (D == 3) ? (inx && iny) : inx;
+          const bool tlo = (bmask & (1 << (2 * W))) && w == (D == 3 ? zH : H);
+          const bool thi = (bmask & (2 << (2 * W))) && w == lvl_hi;
+          const bool rlo = (rmask & (1 << (2 * W))) && w == (D == 3 ? zH : H);
+          const bool rhi = (rmask & (2 << (2 * W))) && w == lvl_hi;
 #pragma unroll
-        for (int j = 1; j < NS; ++j) acc += row[j];
-        F[((long long)dir * ncell + cR) * NV + p] = acc;
+          for (int i = 0; i < NV; ++i) v[i] = 0.0;
+          if (pok) {
+            double a[NV], b[NV];
+            face_trace<D, M, NV, W, false>(qown, ps, T.psi1, a);   // this level's upper trace first
+#pragma unroll
+            for (int i = 0; i < NV; ++i) tw[i * NS + ps] = a[i];
+#pragma unroll
+            for (int i = 0; i < NV; ++i) a[i] = tr[i * NS + ps];
+            face_trace<D, M, NV, W, false>(qown, ps, T.psi0, b);
+            if (face_ok) good = point_flux_states<D, SYS, W, FLUX>(a, b, tlo, thi, rlo, rhi, wt, gamma, ch, T, v);
+          }
+        }
+        if (!good) record_error_flux(cnt, cR);
+        // point sums: K partial sums of CH consecutive points per variable,
+        // then the K partials in order (fixed order: deterministic)
+        if (pok) {
+#pragma unroll
+          for (int i = 0; i < NV; ++i) rb[i * (G + 1) + p] = v[i];
+        }
+        __syncwarp(__activemask());
+        double part = 0.0;
+        const int var = p / C::K, chunk = p - var * C::K;
+        if (var < NV) {
+          const double* row = rb + var * (G + 1);
+          const int j0 = chunk * C::CH, j1 = min(NS, j0 + C::CH);
+          if (j0 < j1) {
+            part = row[j0];
+            for (int j = j0 + 1; j < j1; ++j) part += row[j];
+          }
+        }
+        // gather the partials of each variable in lane var*K (lanes of this group)
+        const int gbase = lane & ~(G - 1);
+        double acc = part;
+#pragma unroll
+        for (int c = 1; c < C::K; ++c) {
+          const double o = __shfl_sync(__activemask(), part, gbase + (var < NV ? var : 0) * C::K + c);
+          acc += o;
+        }
+        if (var < NV && chunk == 0 && face_ok) F[((long long)dir * ncell + cR) * NV + var] = acc;
+        __syncwarp(__activemask());
       }
-      __syncwarp();
     }
-    __syncthreads();   // every warp is done with stage s
+    __syncthreads();   // every warp is done with stage s (and with the traces of level k-1)
     if (tid == 0) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue(run + 2 * gridDim.x, s);
+      issue(g + C::NSTAGE, s);
     }
   }
 }
 
-template <int D, int M, int SYS, int FLUX, int LX, int MINB>
-void launch_flux_tma_t(const KCtx& k, const double* q, double* F, const Box& E, int H, const int n[3], int bmask,
-                       int rmask, DevCounters* cnt) {
-  using C = FluxTma<D, M, SYS, LX>;
-  auto kern = k_face_flux_tma<D, M, SYS, FLUX, LX, MINB>;
+template <int D, int M, int SYS, int FLUX>
+void launch_flux_walk_t(const KCtx& k, const double* q, double* F, const Box& E, int H, const int n[3], int bmask,
+                        int rmask, DevCounters* cnt) {
+  using C = FluxWalk<D, M, SYS>;
+  auto kern = k_face_flux_walk<D, M, SYS, FLUX>;
   const size_t sm = C::smem_bytes();
   int dev = 0;
   cudaGetDevice(&dev);
@@ -235,34 +316,30 @@ void launch_flux_tma_t(const KCtx& k, const double* q, double* F, const Box& E, 
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     attr_dev_mask |= 1 << (dev & 31);
   }
-  const unsigned nrx = (unsigned)((E.ext[0] + LX - 1) / LX);
-  const unsigned ych = (unsigned)((E.ext[1] + kFluxYC - 1) / kFluxYC);
-  const unsigned long long nruns = (unsigned long long)nrx * ych * kFluxYC * E.ext[2];
-  if (nruns == 0 || nruns >= (1ull << 32)) return;
+  const int ntx = (E.ext[0] + C::TX - 1) / C::TX;
+  const int nty = (D == 3) ? (E.ext[1] + C::TY - 1) / C::TY : 1;
+  const int ntiles = ntx * nty;
   int per_sm = 0, nsm = 148;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::WARPS * 32, sm);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   if (per_sm < 1) per_sm = 1;
-  const unsigned long long cap = (unsigned long long)per_sm * nsm;
-  const unsigned g = (unsigned)(nruns < cap ? nruns : cap);
+  const int cap = per_sm * nsm;
+  const int g = ntiles < cap ? ntiles : cap;
   if (k.launches) ++*k.launches;
-  kern<<<g, C::WARPS * 32, sm, k.stream>>>(q, F, E, H, n[0], n[1], n[2], k.sy, k.sz, k.ncell, k.gamma, k.ch,
-                                           bmask, rmask, cnt, nrx, (unsigned)nruns, k.tab);
+  kern<<<g, C::WARPS * 32, sm, k.stream>>>(q, F, E, H, n[0], n[1], n[2], k.sy, k.sz, k.ncell, k.gamma, k.ch, bmask,
+                                           rmask, cnt, ntx, nty, ntiles, k.tab);
 }
 
 template <int D, int M, int SYS>
 void flux_tma_for(const KCtx& k, const double* q, double* F, const Box& E, int H, const int n[3], int bmask,
                   int rmask, DevCounters* cnt) {
-  // LX cells per run; MINB CTAs per SM the register budget is sized for
-  constexpr int LX = (D == 3) ? 4 : 8;
-  constexpr int MINB = (SYS == 1) ? 1 : 2;
   if constexpr (SYS == 0) {
     if (k.tab.flux == 1) {   // eqn.osher (Euler only, checked at ader_create)
-      launch_flux_tma_t<D, M, SYS, 1, LX, 1>(k, q, F, E, H, n, bmask, rmask, cnt);
+      launch_flux_walk_t<D, M, SYS, 1>(k, q, F, E, H, n, bmask, rmask, cnt);
       return;
     }
   }
-  launch_flux_tma_t<D, M, SYS, 0, LX, MINB>(k, q, F, E, H, n, bmask, rmask, cnt);
+  launch_flux_walk_t<D, M, SYS, 0>(k, q, F, E, H, n, bmask, rmask, cnt);
 }
 
 }  // namespace

@@ -17,6 +17,7 @@
 #include "device.cuh"
 #include "flux_point.cuh"
 #include "launch.h"
+#include "predictor.cuh"
 
 namespace ader {
 
@@ -106,24 +107,15 @@ __global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? 4 : 2) k_predictor(
     const double tol, const int max_sweeps, DevCounters* __restrict__ cnt, const int* __restrict__ list,
     const long long nlist, const unsigned char* __restrict__ emask, const double* __restrict__ dtdx_dev,
     const long long qs, const __grid_constant__ DevTables T) {
-  using PH = Phys<SYS, D>;
-  constexpr int NV = PH::NV, N = M + 1, NS = ipow_c(N, D), NST = NS * N;
-  constexpr int G = (NS <= 8) ? 8 : (NS <= 16 ? 16 : 32);   // lanes per cell
-  constexpr int CPW = 32 / G;
-  static_assert(NS <= 32, "one cell must fit in a warp");
-  // shared-memory layout of f*_d: lines along axis d stored contiguously (axis d
-  // fastest, padded to LP = 4 doubles), so the D_d contraction reads a line
-  // with two 16-byte loads: Fs[((d*NV + v)*N + s)*NL + line_d][pos_d]
-  // (used for N = 4; for N = 3 the padding costs occupancy and bank
-  // conflicts, and the natural node-major layout is kept)
-  constexpr bool LINES = (N == 4);
-  constexpr int LP = LINES ? 4 : N, NL = NS / N;
-  constexpr int FSZ = D * NV * N * NL * LP + 8;              // +8: bank offset between cells
+  using C = PredCfg<D, M, SYS>;
+  constexpr int NV = C::NV, N = C::N, NS = C::NS, NST = C::NST, G = C::G, CPW = C::CPW, FSZ = C::FSZ;
   extern __shared__ double smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int slot = lane / G, node0 = lane - slot * G;
-  const bool lane_ok = node0 < NS;
-  const int node = lane_ok ? node0 : NS - 1;
+  PredLane<D, M, SYS> L;
+  L.init(node0, T);
+  const bool lane_ok = L.lane_ok;
+  const int node = L.node;
   double* Fs = smem + (warp * CPW + slot) * FSZ;
   // cells of a box (uniform grid) or of an id list (AMR level)
   const long long count = list ? nlist : R.count();
@@ -135,22 +127,8 @@ __global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? 4 : 2) k_predictor(
     return (long long)(R.lo[0] + (int)(ur - t * bx)) + (long long)(R.lo[1] + (int)(t - z * by)) * sy +
            (long long)(R.lo[2] + (int)z) * sz;
   };
-  int ia[3];
-  ia[0] = node % N;
-  ia[1] = (node / N) % N;
-  ia[2] = node / (N * N);
-  // index of the node's line along each axis (the other two coordinates)
-  int line[3];
-  line[0] = ia[1] + N * ia[2];
-  line[1] = ia[0] + N * ia[2];
-  line[2] = ia[0] + N * ia[1];
   const double dtdx[3] = {dtdx_dev ? dtdx_dev[0] : dtdx0, dtdx_dev ? dtdx_dev[1] : dtdx1,
                           dtdx_dev ? dtdx_dev[2] : dtdx2};
-  double Drow[D][N];                                          // D[ia_d][j] (lane-dependent rows)
-#pragma unroll
-  for (int d = 0; d < D; ++d)
-#pragma unroll
-    for (int j = 0; j < N; ++j) Drow[d][j] = T.D[ia[d]][j];
 
   // persistent warps: the warp walks cell groups with a stride of the whole
   // grid and prefetches the next group's w while it iterates on the current one
@@ -179,100 +157,9 @@ __global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? 4 : 2) k_predictor(
 #pragma unroll
     for (int v = 0; v < NV; ++v) wn[v] = rn < count ? __ldg(&w[cn * (NV * NS) + v * NS + node]) : 1.0;
   }
-  bool conv = !cell_ok, bad = false;
-  int nsw = 0;
-  // one Picard sweep; FIRST: the iterate is the time-constant guess (one flux level)
-  auto sweep_once = [&](auto first_tag) {
-    constexpr bool FIRST = decltype(first_tag)::value;
-    const bool live = !conv && nsw < max_sweeps;   // this cell still iterates
-    constexpr int NT = FIRST ? 1 : N;                          // distinct time levels of the iterate
-    if (live && lane_ok) {
-      // nodal fluxes f*_dir = (dt/dx_dir) f_dir(q) (eqn.nodal.eval @ P:405-412)
-#pragma unroll
-      for (int s = 0; s < NT; ++s) {
-        double uu[NV], f[D][NV];
-#pragma unroll
-        for (int v = 0; v < NV; ++v) uu[v] = FIRST ? wv[v] : qv[v][s];
-        bad |= !PH::fluxes(uu, gamma, ch, f);
-#pragma unroll
-        for (int d = 0; d < D; ++d)
-#pragma unroll
-          for (int v = 0; v < NV; ++v) {
-            if constexpr (LINES) Fs[(((d * NV + v) * N + s) * NL + line[d]) * LP + ia[d]] = dtdx[d] * f[d][v];
-            else Fs[((d * NV + v) * N + s) * NS + node] = dtdx[d] * f[d][v];
-          }
-      }
-    }
-    __syncwarp();
-    // convergence bookkeeping on the high words of |dq| and |q| (monotone in
-    // the value for non-negative doubles): max hi(|dq|) + 1 bounds |dq| from
-    // above, max hi(|q|) with a zero low word bounds |q| from below, so a
-    // passed test implies the exact FP64 test (R2); 32-bit integer max and
-    // shuffles instead of FP64 -> FP32 conversions
-    unsigned dmax = 0u, qmax = 0u;
-    if (live && lane_ok) {
-#pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        double Gs[NT];
-#pragma unroll
-        for (int s = 0; s < NT; ++s) {
-          double g = 0.0;
-#pragma unroll
-          for (int d = 0; d < D; ++d) {
-            if constexpr (LINES) {
-              const double2* fb = reinterpret_cast<const double2*>(Fs + (((d * NV + v) * N + s) * NL + line[d]) * LP);
-              const double2 f01 = fb[0], f23 = fb[1];
-              g += Drow[d][0] * f01.x;
-              g += Drow[d][1] * f01.y;
-              g += Drow[d][2] * f23.x;
-              g += Drow[d][N - 1] * f23.y;
-            } else {
-              const int sd = (d == 0) ? 1 : (d == 1 ? N : N * N);
-              const double* fb = Fs + ((d * NV + v) * N + s) * NS + node - ia[d] * sd;
-#pragma unroll
-              for (int j = 0; j < N; ++j) g += Drow[d][j] * fb[j * sd];
-            }
-          }
-          Gs[s] = g;
-        }
-#pragma unroll
-        for (int s = 0; s < N; ++s) {
-          double acc;
-          if (FIRST) {
-            acc = wv[v] - T.Tsum[s] * Gs[0];
-          } else {
-            acc = wv[v];
-#pragma unroll
-            for (int s2 = 0; s2 < NT; ++s2) acc -= T.T[s][s2] * Gs[s2];
-          }
-          const double prev = FIRST ? wv[v] : qv[v][s];
-          dmax = max(dmax, (unsigned)__double2hiint(fabs(acc - prev)));
-          qmax = max(qmax, (unsigned)__double2hiint(fabs(acc)));
-          qv[v][s] = acc;
-        }
-      }
-    }
-    // per-cell max over the lane group (segmented butterfly)
-#pragma unroll
-    for (int o = G / 2; o > 0; o >>= 1) {
-      dmax = max(dmax, __shfl_xor_sync(0xffffffffu, dmax, o, G));
-      qmax = max(qmax, __shfl_xor_sync(0xffffffffu, qmax, o, G));
-    }
-    if (live) {
-      ++nsw;
-      const double dup = __hiloint2double((int)(dmax + 1u), 0), qlo = __hiloint2double((int)qmax, 0);
-      // (a non-finite |dq| or |q| — high word >= 0x7FF00000 — never converges;
-      // the cap then reports the cell)
-      if (dmax < 0x7FF00000u && qmax < 0x7FF00000u && dup <= tol * (1.0 + qlo)) conv = true;   // reading R2
-    }
-  };
-  if (max_sweeps >= 1) sweep_once(std::integral_constant<bool, true>());
-  // every lane takes part in the vote (lane groups of a warp may stop at
-  // different sweep counts)
-  while (!__all_sync(0xffffffffu, conv || nsw >= max_sweeps)) {
-    __syncwarp();
-    sweep_once(std::integral_constant<bool, false>());
-  }
+  bool conv, bad;
+  int nsw;
+  predictor_cell<D, M, SYS>(wv, qv, Fs, L, dtdx, cell_ok, gamma, ch, tol, max_sweeps, T, nsw, conv, bad);
   if (active && (!emask || emask[cell])) {   // emask: cells whose errors count (multi-rank AMR: owned)
     if (bad) record_error(cnt, 1, 1, cell);
     else if (!conv) record_error(cnt, 2, 1, cell);

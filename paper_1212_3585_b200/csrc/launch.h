@@ -92,6 +92,12 @@ void launch_face_flux_tma(const KCtx& k, const double* q, double* F, const Box& 
                           int bmask, int rmask, DevCounters* cnt);
 // nu N^(d+1) rounded up to an even number of doubles (16-byte aligned blocks)
 long long q_block_stride(int D, int M, int SYS);
+// a1 + a2 fused (weno_pred.cu): WENO sweeps of the cell averages u and the
+// predictor on `region`, q blocks at stride qs; bitwise the same q as
+// launch_weno_sweep x3 + launch_predictor.
+void launch_weno_predictor(const KCtx& k, const double* u, double* q, const Box& region, long long qs,
+                           const double dtdx[3], double tol, int max_sweeps, DevCounters* cnt,
+                           const double* dtdx_dev = nullptr);
 // FV update of `interior` in place + max CFL speed of the new state.
 void launch_update(const KCtx& k, double* u, const double* F, const Box& interior, const double dtdx[3],
                    const double inv_dx[3], DevCounters* cnt, const double* dtdx_dev = nullptr);

@@ -1,0 +1,201 @@
+// predictor.cuh — the element-local space-time DG predictor of one cell (a2),
+// nodal Picard form of eqn.stdg.final:
+//   q = w - T_tau sum_dir D_dir f*_dir(q),   f*_dir = (dt/dx_dir) f_dir(q)
+// executed by a lane group of G >= N^D lanes inside one warp, one lane per
+// spatial node holding the node's time pencil q[NV][N] in registers.  Used by
+// the stand-alone predictor kernel (kernels.cu: uniform box and AMR id lists)
+// and by the fused WENO + predictor tile walk (weno_pred.cu).
+#pragma once
+#include <type_traits>
+
+#include "device.cuh"
+#include "flux_point.cuh"
+
+namespace ader {
+
+// PERS: the f* scratch holds one time level at a time (the sweep stores a
+// level's fluxes, contracts them, then the next level), D NV N^D doubles per
+// cell instead of D NV N^(D+1); the same arithmetic in the same order.
+template <int D, int M, int SYS, bool PERS = false>
+struct PredCfg {
+  static constexpr int NV = Phys<SYS, D>::NV, N = M + 1, NS = ipow_c(N, D), NST = NS * N;
+  static constexpr int G = (NS <= 8) ? 8 : (NS <= 16 ? 16 : 32);   // lanes per cell
+  static constexpr int CPW = 32 / G;
+  static_assert(NS <= 32, "one cell must fit in a warp");
+  // shared-memory layout of f*_d: lines along axis d stored contiguously (axis d
+  // fastest, padded to LP = 4 doubles), so the D_d contraction reads a line
+  // with two 16-byte loads: Fs[((d*NV + v)*N + s)*NL + line_d][pos_d]
+  // (used for N = 4; for N = 3 the padding costs occupancy and bank
+  // conflicts, and the natural node-major layout is kept)
+  static constexpr bool LINES = (N == 4);
+  static constexpr int LP = LINES ? 4 : N, NL = NS / N;
+  static constexpr int FSZ = D * NV * (PERS ? 1 : N) * NL * LP + 8;   // +8: bank offset between cells
+};
+
+// per-lane constants of a lane group: node, its coordinates, line indices and
+// rows of the differentiation matrix D[ia_d][j]
+template <int D, int M, int SYS>
+struct PredLane {
+  using C = PredCfg<D, M, SYS>;
+  int node;
+  bool lane_ok;
+  int ia[3], line[3];
+  double Drow[D][M + 1];
+  __device__ __forceinline__ void init(int node0, const DevTables& T) {
+    constexpr int N = M + 1;
+    lane_ok = node0 < C::NS;
+    node = lane_ok ? node0 : C::NS - 1;
+    ia[0] = node % N;
+    ia[1] = (node / N) % N;
+    ia[2] = node / (N * N);
+    // index of the node's line along each axis (the other two coordinates)
+    line[0] = ia[1] + N * ia[2];
+    line[1] = ia[0] + N * ia[2];
+    line[2] = ia[0] + N * ia[1];
+#pragma unroll
+    for (int d = 0; d < D; ++d)
+#pragma unroll
+      for (int j = 0; j < N; ++j) Drow[d][j] = T.D[ia[d]][j];
+  }
+};
+
+// Picard iteration of one cell per lane group (all 32 lanes of the warp call
+// it together; cell_ok false for a lane group without a cell).  wv: this
+// node's w (eqn.weno.z); on return qv holds the node's time pencil, nsw the
+// sweeps, conv the convergence flag (reading R2), bad an inadmissible state.
+// Sweep 1 starts from the time-constant guess q^0 = w (R3): all N time levels
+// carry the same flux, so it is evaluated once and q^1_s = w - (sum_s' T_ss') G.
+template <int D, int M, int SYS, bool PERS = false>
+__device__ __forceinline__ void predictor_cell(const double (&wv)[Phys<SYS, D>::NV],
+                                               double (&qv)[Phys<SYS, D>::NV][M + 1], double* Fs,
+                                               const PredLane<D, M, SYS>& L, const double (&dtdx)[3], bool cell_ok,
+                                               double gamma, double ch, double tol, int max_sweeps,
+                                               const DevTables& T, int& nsw, bool& conv, bool& bad) {
+  using PH = Phys<SYS, D>;
+  using C = PredCfg<D, M, SYS, PERS>;
+  constexpr int NV = C::NV, N = C::N, NS = C::NS, G = C::G;
+  constexpr bool LINES = C::LINES;
+  constexpr int LP = C::LP, NL = C::NL;
+  const int node = L.node;
+  const bool lane_ok = L.lane_ok;
+  conv = !cell_ok;
+  bad = false;
+  nsw = 0;
+  // one Picard sweep; FIRST: the iterate is the time-constant guess (one flux level)
+  auto sweep_once = [&](auto first_tag) {
+    constexpr bool FIRST = decltype(first_tag)::value;
+    const bool live = !conv && nsw < max_sweeps;   // this cell still iterates
+    constexpr int NT = FIRST ? 1 : N;                          // distinct time levels of the iterate
+    constexpr int SL = PERS ? 1 : N;                           // time levels held by the scratch
+    // nodal fluxes f*_dir = (dt/dx_dir) f_dir(q) (eqn.nodal.eval @ P:405-412) of level s
+    auto store_fluxes = [&](int s) {
+      const int sl = PERS ? 0 : s;
+      double uu[NV], f[D][NV];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) uu[v] = FIRST ? wv[v] : qv[v][s];
+      bad |= !PH::fluxes(uu, gamma, ch, f);
+#pragma unroll
+      for (int d = 0; d < D; ++d)
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          if constexpr (LINES) Fs[(((d * NV + v) * SL + sl) * NL + L.line[d]) * LP + L.ia[d]] = dtdx[d] * f[d][v];
+          else Fs[((d * NV + v) * SL + sl) * NS + node] = dtdx[d] * f[d][v];
+        }
+    };
+    // G = sum_dir D_dir f*_dir of variable v, level s
+    auto contract = [&](int v, int s) -> double {
+      const int sl = PERS ? 0 : s;
+      double g = 0.0;
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        if constexpr (LINES) {
+          const double2* fb = reinterpret_cast<const double2*>(Fs + (((d * NV + v) * SL + sl) * NL + L.line[d]) * LP);
+          const double2 f01 = fb[0], f23 = fb[1];
+          g += L.Drow[d][0] * f01.x;
+          g += L.Drow[d][1] * f01.y;
+          g += L.Drow[d][2] * f23.x;
+          g += L.Drow[d][N - 1] * f23.y;
+        } else {
+          const int sd = (d == 0) ? 1 : (d == 1 ? N : N * N);
+          const double* fb = Fs + ((d * NV + v) * SL + sl) * NS + node - L.ia[d] * sd;
+#pragma unroll
+          for (int j = 0; j < N; ++j) g += L.Drow[d][j] * fb[j * sd];
+        }
+      }
+      return g;
+    };
+    double Gs[NV][NT];
+    if constexpr (PERS) {
+#pragma unroll
+      for (int s = 0; s < NT; ++s) {
+        if (live && lane_ok) store_fluxes(s);
+        __syncwarp();
+        if (live && lane_ok) {
+#pragma unroll
+          for (int v = 0; v < NV; ++v) Gs[v][s] = contract(v, s);
+        }
+        __syncwarp();
+      }
+    } else {
+      if (live && lane_ok) {
+#pragma unroll
+        for (int s = 0; s < NT; ++s) store_fluxes(s);
+      }
+      __syncwarp();
+      if (live && lane_ok) {
+#pragma unroll
+        for (int v = 0; v < NV; ++v)
+#pragma unroll
+          for (int s = 0; s < NT; ++s) Gs[v][s] = contract(v, s);
+      }
+    }
+    // convergence bookkeeping on the high words of |dq| and |q| (monotone in
+    // the value for non-negative doubles): max hi(|dq|) + 1 bounds |dq| from
+    // above, max hi(|q|) with a zero low word bounds |q| from below, so a
+    // passed test implies the exact FP64 test (R2); 32-bit integer max and
+    // shuffles instead of FP64 -> FP32 conversions
+    unsigned dmax = 0u, qmax = 0u;
+    if (live && lane_ok) {
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+#pragma unroll
+        for (int s = 0; s < N; ++s) {
+          double acc;
+          if (FIRST) {
+            acc = wv[v] - T.Tsum[s] * Gs[v][0];
+          } else {
+            acc = wv[v];
+#pragma unroll
+            for (int s2 = 0; s2 < NT; ++s2) acc -= T.T[s][s2] * Gs[v][s2];
+          }
+          const double prev = FIRST ? wv[v] : qv[v][s];
+          dmax = max(dmax, (unsigned)__double2hiint(fabs(acc - prev)));
+          qmax = max(qmax, (unsigned)__double2hiint(fabs(acc)));
+          qv[v][s] = acc;
+        }
+      }
+    }
+    // per-cell max over the lane group (segmented butterfly)
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) {
+      dmax = max(dmax, __shfl_xor_sync(0xffffffffu, dmax, o, G));
+      qmax = max(qmax, __shfl_xor_sync(0xffffffffu, qmax, o, G));
+    }
+    if (live) {
+      ++nsw;
+      const double dup = __hiloint2double((int)(dmax + 1u), 0), qlo = __hiloint2double((int)qmax, 0);
+      // (a non-finite |dq| or |q| — high word >= 0x7FF00000 — never converges;
+      // the cap then reports the cell)
+      if (dmax < 0x7FF00000u && qmax < 0x7FF00000u && dup <= tol * (1.0 + qlo)) conv = true;   // reading R2
+    }
+  };
+  if (max_sweeps >= 1) sweep_once(std::integral_constant<bool, true>());
+  // every lane takes part in the vote (lane groups of a warp may stop at
+  // different sweep counts)
+  while (!__all_sync(0xffffffffu, conv || nsw >= max_sweeps)) {
+    __syncwarp();
+    sweep_once(std::integral_constant<bool, false>());
+  }
+}
+
+}  // namespace ader

@@ -38,6 +38,7 @@ def save(path):
         s = ader.Solver(ader.make_config(device=0, **c["cfg"]))
         s.set_initial(c["ic"]())
         out[name + "_F"] = s.debug_dump(2, dt=1e-3)
+        out[name + "_q"] = s.debug_dump(1, dt=1e-3)
         s.step(1e300, c["steps"])
         out[name + "_u"] = s.get_state()
         s.close()
@@ -50,9 +51,10 @@ def cmp(a, b):
     for k in A.files:
         same = np.array_equal(A[k], B[k])
         d = np.abs(A[k] - B[k]).max()
-        print(f"{k:20s} bitwise={same} maxdiff={d:.3e}")
-        bad += not same
-    print("ALL BITWISE EQUAL" if bad == 0 else f"{bad} DIFFER")
+        rel = d / max(np.abs(A[k]).max(), 1e-300)
+        print(f"{k:20s} bitwise={same} maxdiff={d:.3e} rel={rel:.3e}")
+        bad += rel > 1e-13
+    print("ALL WITHIN 1e-13 (max-norm relative)" if bad == 0 else f"{bad} DIFFER")
     return bad
 
 
