@@ -45,8 +45,13 @@ typedef enum { ADER_EULER = 0, ADER_MHD_GLM = 1 } ader_system;
 typedef enum { ADER_BC_PERIODIC = 0,
                ADER_BC_TRANSMISSIVE = 1,   /* reading R5 */
                ADER_BC_REFLECTIVE = 2,     /* reflecting wall, reading R22 (Euler only) */
-               ADER_BC_INFLOW = 3          /* Dirichlet inflow: the ghost layer keeps the IC cell
+               ADER_BC_INFLOW = 3,         /* Dirichlet inflow: the ghost layer keeps the IC cell
                                             * averages (reading R23; uniform grids) */
+               ADER_BC_EXACT = 4           /* time-dependent Dirichlet "exact solution prescribed"
+                                            * (P:1103-1105): before every step the ghost layer takes
+                                            * the cell averages of ic(x - t exact_vel), the initial
+                                            * condition translated with the front velocity
+                                            * exact_vel (reading R26; uniform grids) */
 } ader_bc;
 /* Two-point flux of the space-time face quadrature. */
 typedef enum { ADER_FLUX_RUSANOV = 0,   /* eqn.rusanov @ P:181-185                  */
@@ -85,6 +90,14 @@ typedef struct {
                                  * their subtrees' local steps when that lowers the
                                  * imbalance (reading R24; the paper's future work,
                                  * P:809-810)                                       */
+  int32_t pred_guess;           /* Picard initial guess, uniform grids: 0 = the
+                                 * time-constant extension of w_h (reading R3); 1 = the
+                                 * previous step's q_h of the cell extrapolated in time,
+                                 * q0 = w + q_prev(1 + r tau) - q_prev(1), r = dt_n /
+                                 * dt_{n-1} (reading R25; R3 on the first step after
+                                 * set_initial / set_cells)                         */
+  double  exact_vel[3];         /* ADER_BC_EXACT sides: front velocity of the exact
+                                 * solution u(x, t) = ic(x - t exact_vel) (R26)     */
 } ader_config;
 
 /* Batched IC callback (host): x[n][3] -> prim[n][9] with
@@ -174,7 +187,8 @@ ader_status ader_partition(const ader_config* cfg, int32_t rank, ader_partition_
  * low, recv high, send high, recv low), 2 periodic wrap onto itself, 3
  * transmissive copy of the nearest owned cell (reading R5), 4 reflective
  * mirror of the owned cells with the normal momentum negated (R22), 5 inflow
- * (the ghost cells keep their initial values, R23). */
+ * (the ghost cells keep their initial values, R23), 6 exact (the ghost cells
+ * are set from the translated initial condition before every step, R26). */
 typedef struct {
   int32_t kind, peer;
   int32_t send_lo[3], send_hi[3];

@@ -16,7 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB = None
 
 EULER, MHD = 0, 1
-PERIODIC, TRANSMISSIVE, REFLECTIVE, INFLOW = 0, 1, 2, 3
+PERIODIC, TRANSMISSIVE, REFLECTIVE, INFLOW, EXACT = 0, 1, 2, 3, 4
 RUSANOV, OSHER = 0, 1
 
 IC_FN = C.CFUNCTYPE(None, C.POINTER(C.c_double), C.c_int64, C.POINTER(C.c_double), C.c_void_p)
@@ -33,6 +33,7 @@ class OrcConfig(C.Structure):
         ("refine_factor", C.c_int32), ("lmax", C.c_int32),
         ("chi_ref", C.c_double), ("chi_rec", C.c_double), ("chi_eps", C.c_double),
         ("flux", C.c_int32), ("flux_quad", C.c_int32),
+        ("pred_guess", C.c_int32), ("exact_vel", C.c_double * 3),
     ]
 
 
@@ -156,15 +157,35 @@ def reconstruct_box(d, M, nv, ubox):
     return w
 
 
-def predict_cell(d, M, system, gamma, ch, w, dtdx, tol=1e-13, max_sweeps=32):
+def predict_cell(d, M, system, gamma, ch, w, dtdx, tol=1e-13, max_sweeps=32, q0=None):
     w = np.ascontiguousarray(w, dtype=np.float64)
     nv = w.shape[0]
     q = np.zeros((nv, (M + 1) ** (d + 1)))
     dtdx = np.ascontiguousarray(dtdx, dtype=np.float64)
     sw = C.c_int(0)
-    rc = lib().orc_predict_cell(d, M, system, gamma, ch, _p(w), _p(dtdx), tol, max_sweeps,
-                                _p(q), C.byref(sw))
+    L = lib()
+    if q0 is None:
+        rc = L.orc_predict_cell(d, M, system, gamma, ch, _p(w), _p(dtdx), tol, max_sweeps, _p(q), C.byref(sw))
+    else:
+        q0 = np.ascontiguousarray(q0, dtype=np.float64)
+        dp = C.POINTER(C.c_double)
+        L.orc_predict_cell_guess.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, dp, dp, C.c_double,
+                                             C.c_int, dp, dp, C.POINTER(C.c_int)]
+        rc = L.orc_predict_cell_guess(d, M, system, gamma, ch, _p(w), _p(dtdx), tol, max_sweeps, _p(q0), _p(q),
+                                      C.byref(sw))
     return rc, q, sw.value
+
+
+def extrapolate_guess(d, M, w, qp, r):
+    """reading R25: q0 = w + qp(., 1 + r tau) - qp(., 1) at the space-time nodes"""
+    w = np.ascontiguousarray(w, dtype=np.float64)
+    qp = np.ascontiguousarray(qp, dtype=np.float64)
+    q0 = np.zeros_like(qp)
+    L = lib()
+    dp = C.POINTER(C.c_double)
+    L.orc_extrapolate_guess.argtypes = [C.c_int, C.c_int, C.c_int, dp, dp, C.c_double, dp]
+    L.orc_extrapolate_guess(d, M, w.shape[0], _p(w), _p(qp), r, _p(q0))
+    return q0
 
 
 def face_flux(d, M, system, gamma, ch, direction, qL, qR, flux=RUSANOV, nq=3):
@@ -272,7 +293,8 @@ class Oracle:
     """Uniform-grid oracle run (level 0 only)."""
 
     def __init__(self, *, dim, system=EULER, degree, n, lo, hi, bc, gamma=1.4, ch=0.0,
-                 cfl=0.9, pred_tol=1e-13, pred_max_sweeps=32, ic_quad=0, flux=RUSANOV, flux_quad=3):
+                 cfl=0.9, pred_tol=1e-13, pred_max_sweeps=32, ic_quad=0, flux=RUSANOV, flux_quad=3,
+                 pred_guess=0, exact_vel=(0.0, 0.0, 0.0)):
         cfg = OrcConfig()
         cfg.dim, cfg.system, cfg.degree = dim, system, degree
         n = list(n) + [1] * (3 - len(n))
@@ -286,6 +308,9 @@ class Oracle:
         cfg.gamma, cfg.ch, cfg.cfl = gamma, ch, cfl
         cfg.pred_tol, cfg.pred_max_sweeps, cfg.ic_quad = pred_tol, pred_max_sweeps, ic_quad
         cfg.flux, cfg.flux_quad = flux, flux_quad
+        cfg.pred_guess = pred_guess
+        for k in range(3):
+            cfg.exact_vel[k] = (list(exact_vel) + [0.0] * 3)[k]
         self.cfg = cfg
         self.dim, self.degree, self.system = dim, degree, system
         self.n = n[:dim]

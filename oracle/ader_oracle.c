@@ -630,14 +630,39 @@ static const pred_t* pred_get(int d, int M) {
 int orc_predict_cell(int d, int M, int system, double gamma, double ch,
                      const double* w, const double* dtdx, double tol, int max_sweeps,
                      double* q, int* sweeps) {
+  return orc_predict_cell_guess(d, M, system, gamma, ch, w, dtdx, tol, max_sweeps, NULL, q, sweeps);
+}
+
+void orc_extrapolate_guess(int d, int M, int nv, const double* w, const double* qp, double r, double* q0) {
+  const basis_t* B = basis_get(M);
+  int N = B->N, NS = ipow(N, d), NST = NS * N;
+  for (int v = 0; v < nv; ++v)
+    for (int x = 0; x < NS; ++x) {
+      /* the node's old time polynomial at tau = 1 */
+      double end = 0.0;
+      for (int a = 0; a < N; ++a) end += psi_val(B, a, 1.0) * qp[v * NST + a * NS + x];
+      for (int s = 0; s < N; ++s) {
+        double tau = 1.0 + r * B->lam[s], val = 0.0;
+        for (int a = 0; a < N; ++a) val += psi_val(B, a, tau) * qp[v * NST + a * NS + x];
+        q0[v * NST + s * NS + x] = w[v * NS + x] + (val - end);
+      }
+    }
+}
+
+int orc_predict_cell_guess(int d, int M, int system, double gamma, double ch,
+                           const double* w, const double* dtdx, double tol, int max_sweeps,
+                           const double* q0, double* q, int* sweeps) {
   const pred_t* P = pred_get(d, M);
   int nv = orc_nvar(system, d), NS = P->NS, NST = P->NST;
   double* qo = (double*)malloc(sizeof(double) * nv * NST);
   double* fs = (double*)malloc(sizeof(double) * 3 * nv * NST);
   double* rhs = (double*)malloc(sizeof(double) * NST);
-  /* initial guess: time-constant extension of w_h (reading R3) */
-  for (int v = 0; v < nv; ++v)
-    for (int p = 0; p < NST; ++p) q[v * NST + p] = w[v * NS + p % NS];
+  /* initial guess: time-constant extension of w_h (reading R3), or
+   * the caller's (reading R25) */
+  if (q0) memcpy(q, q0, sizeof(double) * nv * NST);
+  else
+    for (int v = 0; v < nv; ++v)
+      for (int p = 0; p < NST; ++p) q[v * NST + p] = w[v * NS + p % NS];
   int k, rc = 3;
   for (k = 1; k <= max_sweeps; ++k) {
     memcpy(qo, q, sizeof(double) * nv * NST);
@@ -823,6 +848,14 @@ struct orc_ctx {
   double dx[3];
   double* u;          /* padded grid [pad cell][nv], ghosts of width G */
   double t;
+  /* reading R25 (pred_guess = 1): q_h of every predicted cell of the last
+   * orc_step step (padded index) and that step's dt; qnext collects the
+   * current step's */
+  double *qprev, *qnext;
+  double dtprev;
+  int have_prev;
+  orc_ic_fn ic;       /* the problem's initial condition (ORC_BC_EXACT sides, R26) */
+  void* ic_user;
   int ext_ghosts;
   char err[512];
 };
@@ -859,7 +892,7 @@ orc_ctx* orc_create(const orc_config* cfg) {
   return c;
 }
 
-void orc_destroy(orc_ctx* c) { if (c) { free(c->u); free(c); } }
+void orc_destroy(orc_ctx* c) { if (c) { free(c->u); free(c->qprev); free(c->qnext); free(c); } }
 const char* orc_last_error(const orc_ctx* c) { return c ? c->err : "null ctx"; }
 double orc_time(const orc_ctx* c) { return c->t; }
 int64_t orc_num_cells(const orc_ctx* c) { return (int64_t)c->n[0] * c->n[1] * c->n[2]; }
@@ -870,20 +903,14 @@ int orc_set_initial(orc_ctx* c, orc_ic_fn ic, void* user) {
   return orc_set_initial_box(c, ic, user, lo, hi);
 }
 
-int orc_set_initial_box(orc_ctx* c, orc_ic_fn ic, void* user, const int32_t* blo, const int32_t* bhi) {
+/* cell averages of ic(x - shift) on the cells bl + [0, be) of the padded
+ * grid (cell index space, ghosts negative), by the ic_quad^d Gauss-Legendre
+ * rule (reading R6) */
+static void ic_average_box(orc_ctx* c, orc_ic_fn ic, void* user, const int* bl, const int* be, const double* shift) {
   int Q = c->cfg.ic_quad, d = c->d, nv = c->nv;
   double qx[16], qw[16];
   gauss_legendre01(Q, qx, qw);
   int nq = ipow(Q, d);
-  int bl[3], be[3];
-  for (int k = 0; k < 3; ++k) {
-    /* inflow sides (R23): the ghost layer takes IC averages too */
-    const int glo = (k < d && c->cfg.bc[2 * k] == ORC_BC_INFLOW) ? -c->G : 0;
-    const int ghi = (k < d && c->cfg.bc[2 * k + 1] == ORC_BC_INFLOW) ? c->n[k] + c->G : c->n[k];
-    bl[k] = (k < d) ? (blo[k] < glo ? glo : blo[k]) : 0;
-    int h = (k < d) ? (bhi[k] > ghi ? ghi : bhi[k]) : 1;
-    be[k] = h > bl[k] ? h - bl[k] : 0;
-  }
   int64_t ncell = (int64_t)be[0] * be[1] * be[2];
   const int64_t chunk = 4096;
   double* x = (double*)malloc(sizeof(double) * chunk * nq * 3);
@@ -897,7 +924,7 @@ int orc_set_initial_box(orc_ctx* c, orc_ic_fn ic, void* user, const int32_t* blo
         int gi[3] = {g % Q, (g / Q) % Q, g / (Q * Q)};
         double* xp = &x[(ci * nq + g) * 3];
         for (int k = 0; k < 3; ++k)
-          xp[k] = (k < d) ? c->cfg.lo[k] + ((double)ii[k] + qx[gi[k]]) * c->dx[k] : 0.0;
+          xp[k] = (k < d) ? (c->cfg.lo[k] + ((double)ii[k] + qx[gi[k]]) * c->dx[k]) - shift[k] : 0.0;
       }
     }
     for (int64_t i = 0; i < nc * nq * 9; ++i) pr[i] = 0.0;
@@ -920,12 +947,55 @@ int orc_set_initial_box(orc_ctx* c, orc_ic_fn ic, void* user, const int32_t* blo
     }
   }
   free(x); free(pr);
+}
+
+int orc_set_initial_box(orc_ctx* c, orc_ic_fn ic, void* user, const int32_t* blo, const int32_t* bhi) {
+  int d = c->d;
+  c->have_prev = 0;
+  c->ic = ic;
+  c->ic_user = user;
+  int bl[3], be[3];
+  for (int k = 0; k < 3; ++k) {
+    /* inflow and exact sides (R23, R26): the ghost layer takes IC averages too */
+    const int lo_g = k < d && (c->cfg.bc[2 * k] == ORC_BC_INFLOW || c->cfg.bc[2 * k] == ORC_BC_EXACT);
+    const int hi_g = k < d && (c->cfg.bc[2 * k + 1] == ORC_BC_INFLOW || c->cfg.bc[2 * k + 1] == ORC_BC_EXACT);
+    const int glo = lo_g ? -c->G : 0;
+    const int ghi = hi_g ? c->n[k] + c->G : c->n[k];
+    bl[k] = (k < d) ? (blo[k] < glo ? glo : blo[k]) : 0;
+    int h = (k < d) ? (bhi[k] > ghi ? ghi : bhi[k]) : 1;
+    be[k] = h > bl[k] ? h - bl[k] : 0;
+  }
+  const double zero[3] = {0, 0, 0};
+  ic_average_box(c, ic, user, bl, be, zero);
   c->t = 0.0;
   return 0;
 }
 
+/* Reading R26 (the "exact solution prescribed" boundaries of P:1103-1105):
+ * before every step the ghost layer of each ORC_BC_EXACT side, over the full
+ * padded extent of the other axes, takes the averages of the exact solution
+ * at the step's start time, u(x, t) = ic(x - t exact_vel). */
+static void refresh_exact(orc_ctx* c) {
+  if (!c->ic) return;
+  const int d = c->d, G = c->G;
+  const double shift[3] = {c->t * c->cfg.exact_vel[0], c->t * c->cfg.exact_vel[1], c->t * c->cfg.exact_vel[2]};
+  for (int a = 0; a < d; ++a)
+    for (int side = 0; side < 2; ++side) {
+      if (c->cfg.bc[2 * a + side] != ORC_BC_EXACT) continue;
+      int bl[3], be[3];
+      for (int k = 0; k < 3; ++k) {
+        bl[k] = (k < d) ? -G : 0;
+        be[k] = (k < d) ? c->n[k] + 2 * G : 1;
+      }
+      bl[a] = side ? c->n[a] : -G;
+      be[a] = G;
+      ic_average_box(c, c->ic, c->ic_user, bl, be, shift);
+    }
+}
+
 int orc_set_cells(orc_ctx* c, const double* u) {
   int64_t lin = 0;
+  c->have_prev = 0;   /* R25: a new state has no previous step */
   for (int k = 0; k < c->n[2]; ++k)
     for (int j = 0; j < c->n[1]; ++j)
       for (int i = 0; i < c->n[0]; ++i, ++lin)
@@ -952,6 +1022,7 @@ static int ghost_src(const orc_ctx* c, int axis, int i) {
   if (c->cfg.bc[2 * axis + side] == ORC_BC_PERIODIC) return ((i % n) + n) % n;
   if (c->cfg.bc[2 * axis + side] == ORC_BC_REFLECTIVE) return (i < 0) ? -1 - i : 2 * n - 1 - i;
   if (c->cfg.bc[2 * axis + side] == ORC_BC_INFLOW) return i;   /* R23: the ghost keeps its IC average */
+  if (c->cfg.bc[2 * axis + side] == ORC_BC_EXACT) return i;    /* R26: set by refresh_exact */
   return (i < 0) ? 0 : n - 1;
 }
 static int ghost_reflected(const orc_ctx* c, int axis, int i) {
@@ -1042,8 +1113,16 @@ static int cell_predict(orc_ctx* c, int i, int j, int k, double dt, double* q, i
   orc_reconstruct_box(c->d, M, nv, box, w);
   double dtdx[3];
   for (int dir = 0; dir < c->d; ++dir) dtdx[dir] = dt / c->dx[dir];
-  int rc = orc_predict_cell(c->d, M, c->cfg.system, c->cfg.gamma, c->cfg.ch, w, dtdx,
-                            c->cfg.pred_tol, c->cfg.pred_max_sweeps, q, sweeps);
+  double* q0 = NULL;
+  const int64_t pc = pidx(c, i, j, k);
+  if (c->cfg.pred_guess == 1 && c->have_prev && c->dtprev > 0.0 && dt > 0.0) {
+    q0 = (double*)malloc(sizeof(double) * nv * c->NST);
+    orc_extrapolate_guess(c->d, M, nv, w, &c->qprev[pc * nv * c->NST], dt / c->dtprev, q0);
+  }
+  int rc = orc_predict_cell_guess(c->d, M, c->cfg.system, c->cfg.gamma, c->cfg.ch, w, dtdx,
+                                  c->cfg.pred_tol, c->cfg.pred_max_sweeps, q0, q, sweeps);
+  if (c->qnext && rc == 0) memcpy(&c->qnext[pc * nv * c->NST], q, sizeof(double) * nv * c->NST);
+  free(q0);
   if (rc)
     snprintf(c->err, sizeof(c->err), "predictor failed (non-convergence or inadmissible state) in cell (%d,%d,%d), level 0, t=%.17g", i, j, k, c->t);
   free(box); free(w);
@@ -1053,6 +1132,7 @@ static int cell_predict(orc_ctx* c, int i, int j, int k, double dt, double* q, i
 int orc_advance_box(orc_ctx* c, double dt, const int32_t* blo, const int32_t* bhi,
                     double* out, orc_report* rep) {
   int d = c->d, nv = c->nv, NST = c->NST;
+  if (!c->ext_ghosts) refresh_exact(c);
   fill_ghosts(c);
   int lo[3], hi[3], ext[3];
   for (int k = 0; k < 3; ++k) {
@@ -1131,6 +1211,10 @@ int orc_step(orc_ctx* c, double t_end, int64_t max_steps, orc_report* rep) {
   double* un = (double*)malloc(sizeof(double) * ncell * c->nv);
   int32_t blo[3] = {0, 0, 0}, bhi[3] = {c->n[0], c->n[1], c->n[2]};
   int rc = 0;
+  if (c->cfg.pred_guess == 1 && !c->qprev) {
+    c->qprev = (double*)calloc((size_t)c->npad * c->nv * c->NST, sizeof(double));
+    c->qnext = (double*)calloc((size_t)c->npad * c->nv * c->NST, sizeof(double));
+  }
   while (r.steps < max_steps && c->t < t_end) {
     double dt = orc_compute_dt(c);
     if (!(dt > 0.0) || !isfinite(dt)) { snprintf(c->err, sizeof(c->err), "invalid dt %g", dt); rc = 3; break; }
@@ -1138,6 +1222,11 @@ int orc_step(orc_ctx* c, double t_end, int64_t max_steps, orc_report* rep) {
     rc = orc_advance_box(c, dt, blo, bhi, un, &r);
     if (rc) break;
     orc_set_cells(c, un);
+    if (c->qnext) {   /* R25: this step's q_h become the next step's guess source */
+      double* tmp = c->qprev; c->qprev = c->qnext; c->qnext = tmp;
+      c->dtprev = dt;
+      c->have_prev = 1;
+    }
     c->t += dt;
     r.dt = dt;
     r.steps++;

@@ -24,7 +24,9 @@ extern "C" {
 
 enum { ORC_EULER = 0, ORC_MHD = 1 };
 enum { ORC_BC_PERIODIC = 0, ORC_BC_TRANSMISSIVE = 1, ORC_BC_REFLECTIVE = 2,   /* reflective: Euler only (R22) */
-       ORC_BC_INFLOW = 3 };   /* Dirichlet inflow: ghost cells keep the IC averages (R23), uniform grids */
+       ORC_BC_INFLOW = 3,     /* Dirichlet inflow: ghost cells keep the IC averages (R23), uniform grids */
+       ORC_BC_EXACT = 4 };    /* time-dependent Dirichlet: before every step the ghost cells take the
+                               * averages of the exact solution ic(x - t exact_vel) (R26), uniform grids */
 enum { ORC_FLUX_RUSANOV = 0, ORC_FLUX_OSHER = 1 };   /* eqn.rusanov / eqn.osher */
 
 typedef struct {
@@ -41,6 +43,13 @@ typedef struct {
   /* numerical flux: ORC_FLUX_RUSANOV or ORC_FLUX_OSHER (Euler
    * only); flux_quad = Gauss-Legendre points of the Osher path integral */
   int32_t flux, flux_quad;
+  /* Picard initial guess (uniform grids): 0 = time-constant extension
+   * of w_h (reading R3), 1 = the previous step's q_h of the same cell
+   * extrapolated in time (reading R25, orc_extrapolate_guess) */
+  int32_t pred_guess;
+  /* ORC_BC_EXACT sides: the exact solution is the initial condition translated
+   * with this constant front velocity, u(x, t) = ic(x - t exact_vel) (R26) */
+  double exact_vel[3];
 } orc_config;
 
 /* Batched initial-condition callback: x[n][3] -> prim[n][9]
@@ -82,6 +91,17 @@ int  orc_reconstruct_box(int d, int M, int nv, const double* ubox, double* w);
 int  orc_predict_cell(int d, int M, int system, double gamma, double ch,
                       const double* w, const double* dtdx, double tol, int max_sweeps,
                       double* q, int* sweeps);
+/* orc_predict_cell from the initial guess q0[nv][N^(d+1)] (NULL: R3). */
+int  orc_predict_cell_guess(int d, int M, int system, double gamma, double ch,
+                            const double* w, const double* dtdx, double tol, int max_sweeps,
+                            const double* q0, double* q, int* sweeps);
+/* Reading R25 (the extrapolation initial guess of P:472): from the previous
+ * step's space-time polynomial qp[nv][N^(d+1)] of the cell over [t^{n-1}, t^n]
+ * and the new reconstruction w[nv][N^d] at t^n,
+ *   q0(x_node, tau_s) = w(x_node) + qp(x_node, 1 + r tau_s) - qp(x_node, 1),
+ * r = dt_n / dt_{n-1}: the old time evolution carried forward, anchored at the
+ * new w.  Exact for a solution polynomial of degree <= M in t. */
+void orc_extrapolate_guess(int d, int M, int nv, const double* w, const double* qp, double r, double* q0);
 /* Space-time face flux (flux:F/G/H @ P:158-172) of the selected two-point flux
  * (eqn.rusanov @ P:181-185 or eqn.osher @ P:186-196)
  * between the left (lower) cell qL and right (upper) cell qR along dir.  At a

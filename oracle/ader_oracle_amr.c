@@ -674,9 +674,10 @@ void* orc_amr_create(const orc_config* cfg) {
   if (!cfg || (cfg->dim != 2 && cfg->dim != 3) || cfg->degree < 2 || cfg->degree > 3) return NULL;
   if (cfg->lmax < 0 || cfg->lmax >= LMAXX || cfg->refine_factor < cfg->degree) return NULL;
   if (cfg->flux == ORC_FLUX_OSHER && cfg->system != ORC_EULER) return NULL;   /* Osher: Euler only */
+  if (cfg->pred_guess != 0) return NULL;   /* R25 guess: uniform grids only */
   for (int k = 0; k < 2 * cfg->dim; ++k) {
     if (cfg->bc[k] == ORC_BC_REFLECTIVE && (cfg->system != ORC_EULER || cfg->n[k / 2] < cfg->degree + 1)) return NULL;
-    if (cfg->bc[k] == ORC_BC_INFLOW) return NULL;   /* R23: uniform grids only */
+    if (cfg->bc[k] == ORC_BC_INFLOW || cfg->bc[k] == ORC_BC_EXACT) return NULL;   /* R23, R26: uniform grids only */
   }
   amr_t* A = (amr_t*)calloc(1, sizeof(amr_t));
   A->cfg = *cfg;

@@ -40,6 +40,7 @@ class AderConfig(C.Structure):
         ("rank", C.c_int32), ("world_size", C.c_int32), ("device", C.c_int32),
         ("nccl_id", C.c_uint8 * 128),
         ("flux", C.c_int32), ("flux_quad", C.c_int32), ("load_balance", C.c_int32),
+        ("pred_guess", C.c_int32), ("exact_vel", C.c_double * 3),
     ]
 
 
@@ -128,7 +129,8 @@ def _dp(a):
 def make_config(*, dim, degree, n0, lo, hi, bc, system=EULER, gamma=1.4, ch=0.0, cfl=0.9,
                 refine_factor=3, lmax=0, chi_ref=0.2, chi_rec=0.1, chi_eps=0.01, pred_tol=1e-13,
                 pred_max_sweeps=32, ic_quad=0, adapt_every=1, rank=0, world_size=1, device=-1,
-                nccl_id=None, flux=RUSANOV, flux_quad=0, load_balance=0) -> AderConfig:
+                nccl_id=None, flux=RUSANOV, flux_quad=0, load_balance=0, pred_guess=0,
+                exact_vel=(0.0, 0.0, 0.0)) -> AderConfig:
     cfg = AderConfig()
     cfg.abi_version = ABI_VERSION
     cfg.dim, cfg.system, cfg.degree = dim, system, degree
@@ -147,6 +149,9 @@ def make_config(*, dim, degree, n0, lo, hi, bc, system=EULER, gamma=1.4, ch=0.0,
     cfg.ic_quad, cfg.adapt_every = ic_quad, adapt_every
     cfg.rank, cfg.world_size, cfg.device = rank, world_size, device
     cfg.flux, cfg.flux_quad, cfg.load_balance = flux, flux_quad, load_balance
+    cfg.pred_guess = pred_guess
+    for k in range(3):
+        cfg.exact_vel[k] = (list(exact_vel) + [0.0] * 3)[k]
     if nccl_id is not None:
         for i, b in enumerate(bytes(nccl_id)[:128]):
             cfg.nccl_id[i] = b

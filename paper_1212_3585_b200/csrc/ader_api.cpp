@@ -111,6 +111,11 @@ struct ader_ctx {
   int cons_cap = 0;                            // blocks
   double t = 0.0;
   bool speed_valid = false;
+  bool guess_ready = false;                    // R25: q holds the previous step's predictor of this state
+  ader_ic_fn ic = nullptr;                     // the problem's IC (ADER_BC_EXACT sides, R26)
+  void* ic_user = nullptr;
+  bool has_exact = false;                      // a side of this rank is ADER_BC_EXACT
+  double prev_dt_host = 0.0;                   // its dt (host-driven loopback steps)
   ncclComm_t comm = nullptr;
   bool loopback = false;                       // test-only rank group in one process (ader_debug_group_*)
   std::string err;
@@ -166,9 +171,10 @@ ader_status validate(const ader_config* cfg, std::string& why) {
     if (!(cfg->hi[k] > cfg->lo[k])) return bad("hi must exceed lo");
   for (int k = 0; k < 2 * cfg->dim; ++k) {
     if (cfg->bc[k] != ADER_BC_PERIODIC && cfg->bc[k] != ADER_BC_TRANSMISSIVE && cfg->bc[k] != ADER_BC_REFLECTIVE &&
-        cfg->bc[k] != ADER_BC_INFLOW)
+        cfg->bc[k] != ADER_BC_INFLOW && cfg->bc[k] != ADER_BC_EXACT)
       return bad("bad bc");
-    if (cfg->bc[k] == ADER_BC_INFLOW && cfg->lmax > 0) return ADER_ERR_UNSUPPORTED;   // R23: uniform grids
+    if ((cfg->bc[k] == ADER_BC_INFLOW || cfg->bc[k] == ADER_BC_EXACT) && cfg->lmax > 0)
+      return ADER_ERR_UNSUPPORTED;   // R23, R26: uniform grids
     if (cfg->bc[k] == ADER_BC_REFLECTIVE && cfg->system != ADER_EULER) return bad("reflective walls are Euler only");
     if (cfg->bc[k] == ADER_BC_REFLECTIVE && cfg->n0[k / 2] < cfg->degree + 1)
       return bad("a reflective axis needs at least M+1 cells");
@@ -190,6 +196,8 @@ ader_status validate(const ader_config* cfg, std::string& why) {
   if (cfg->flux == ADER_FLUX_OSHER && cfg->system != ADER_EULER) return bad("the Osher flux is implemented for Euler only");
   if (cfg->flux_quad < 0 || cfg->flux_quad > 4) return bad("flux_quad must be in 0..4");
   if (cfg->load_balance < 0 || cfg->load_balance > 1) return bad("load_balance must be 0 or 1");
+  if (cfg->pred_guess < 0 || cfg->pred_guess > 1) return bad("pred_guess must be 0 or 1");
+  if (cfg->pred_guess == 1 && cfg->lmax > 0) return bad("pred_guess = 1 (reading R25) is for uniform grids");
   (void)b;
   return ADER_OK;
 }
@@ -353,8 +361,10 @@ void halo_plan(int d, int H, const int n[3], const int P[3], const ader_partitio
     else {                                       // unprocessed axes: owned extent, plus the
       lo[b] = H;                                 // inflow ghost layers (set at initialisation,
       hi[b] = H + n[b];                          // R23) so that their edges are filled too
-      if (b != a && part.nbr[2 * b] < 0 && bc[2 * b] == ADER_BC_INFLOW) lo[b] = 0;
-      if (b != a && part.nbr[2 * b + 1] < 0 && bc[2 * b + 1] == ADER_BC_INFLOW) hi[b] = P[b];
+      const bool dl = bc[2 * b] == ADER_BC_INFLOW || bc[2 * b] == ADER_BC_EXACT;
+      const bool dh = bc[2 * b + 1] == ADER_BC_INFLOW || bc[2 * b + 1] == ADER_BC_EXACT;
+      if (b != a && part.nbr[2 * b] < 0 && dl) lo[b] = 0;
+      if (b != a && part.nbr[2 * b + 1] < 0 && dh) hi[b] = P[b];
     }
   }
   for (int b = 0; b < 3; ++b) { o->send_lo[b] = o->recv_lo[b] = lo[b]; o->send_hi[b] = o->recv_hi[b] = hi[b]; }
@@ -363,7 +373,8 @@ void halo_plan(int d, int H, const int n[3], const int P[3], const ader_partitio
   const int nb = part.nbr[2 * a + side];
   if (nb >= 0 && nb != rank) { o->kind = 1; o->peer = nb; }
   else if (nb >= 0 && bc[2 * a + side] == ADER_BC_PERIODIC) o->kind = 2;
-  else o->kind = bc[2 * a + side] == ADER_BC_REFLECTIVE ? 4 : (bc[2 * a + side] == ADER_BC_INFLOW ? 5 : 3);
+  else o->kind = bc[2 * a + side] == ADER_BC_REFLECTIVE ? 4
+               : (bc[2 * a + side] == ADER_BC_INFLOW ? 5 : (bc[2 * a + side] == ADER_BC_EXACT ? 6 : 3));
 }
 
 Box desc_box(const int32_t* lo, const int32_t* hi) { return make_box(lo[0], hi[0], lo[1], hi[1], lo[2], hi[2]); }
@@ -412,9 +423,10 @@ void halo_unpack_local(ader_ctx* c, double* u, int a) {
   if (dh.kind == 1) launch_unpack(c->k, u, rhi, c->recvb[2 * a + 1]);
   // local sides: periodic wrap onto ourselves, or transmissive copy (reading R5)
   auto mode = [](int kind) { return kind == 2 ? 0 : (kind == 4 ? 2 : 1); };
-  // (kind 5, inflow: the ghost cells keep their initial values, R23)
-  if (dl.kind != 1 && dl.kind != 5) launch_fill_axis(c->k, u, rlo, a, mode(dl.kind), c->H, c->n[a]);
-  if (dh.kind != 1 && dh.kind != 5) launch_fill_axis(c->k, u, rhi, a, mode(dh.kind), c->H, c->n[a]);
+  // (kind 5, inflow: the ghost cells keep their initial values, R23; kind 6,
+  // exact: set by refresh_exact before the step, R26)
+  if (dl.kind != 1 && dl.kind != 5 && dl.kind != 6) launch_fill_axis(c->k, u, rlo, a, mode(dl.kind), c->H, c->n[a]);
+  if (dh.kind != 1 && dh.kind != 5 && dh.kind != 6) launch_fill_axis(c->k, u, rhi, a, mode(dh.kind), c->H, c->n[a]);
 }
 
 ader_status fill_halo(ader_ctx* c, double* u) {
@@ -465,7 +477,7 @@ int boundary_mask(const ader_ctx* c, int bc) {
 int transmissive_mask(const ader_ctx* c) { return boundary_mask(c, ADER_BC_TRANSMISSIVE); }
 int reflective_mask(const ader_ctx* c) { return boundary_mask(c, ADER_BC_REFLECTIVE); }
 
-void run_predictor(ader_ctx* c, double dt, const double* dtdx_dev = nullptr) {
+void run_predictor(ader_ctx* c, double dt, const double* dtdx_dev = nullptr, bool guess = false) {
   // owned block + the face-neighbour layer, except beyond transmissive sides (R5)
   Box r = grown(c, 1);
   const int tm = transmissive_mask(c) | reflective_mask(c);   // no predictor beyond walls either (R22)
@@ -476,18 +488,26 @@ void run_predictor(ader_ctx* c, double dt, const double* dtdx_dev = nullptr) {
   double dtdx[3] = {0, 0, 0};
   for (int k = 0; k < c->d; ++k) dtdx[k] = dt / c->dx[k];
   Scope s(c, ADER_K_PRED, 0.0);   // flops from the sweep counter (ader_kernel_stats)
-  launch_predictor(c->k, c->w, c->q, r, dtdx, c->cfg.pred_tol, c->cfg.pred_max_sweeps, c->cnt, dtdx_dev, c->qs);
+  // reading R25: from the device step control (dt / prev_dt) in the device-driven
+  // loop, else from the host's dt ratio (loopback groups)
+  const bool g = guess && c->cfg.pred_guess == 1 && c->guess_ready;
+  const double gr = (!dtdx_dev && c->prev_dt_host > 0.0 && dt > 0.0) ? dt / c->prev_dt_host : 0.0;
+  launch_predictor(c->k, c->w, c->q, r, dtdx, c->cfg.pred_tol, c->cfg.pred_max_sweeps, c->cnt, dtdx_dev, c->qs, g,
+                   dtdx_dev ? c->st : nullptr, gr);
+  if (guess) { c->guess_ready = true; c->prev_dt_host = dt; }
 }
 
 // a1 + a2 fused (weno_pred.cu): the WENO sweeps and the predictor in one tile
 // walk, w_x / w_xy / w kept on chip (ADER_WENO_PRED=0: separate kernels)
-bool fused_weno_pred() {
+bool fused_weno_pred_env() {
   static const int on = [] {
     const char* e = std::getenv("ADER_WENO_PRED");
     return (e && e[0] == '1') ? 1 : 0;
   }();
   return on != 0;
 }
+// (the fused kernel has no R25 guess: pred_guess = 1 runs the separate kernels)
+bool fused_weno_pred(const ader_ctx* c) { return fused_weno_pred_env() && c->cfg.pred_guess == 0; }
 
 void run_weno_predictor(ader_ctx* c, double dt, const double* dtdx_dev = nullptr) {
   Box r = grown(c, 1);
@@ -744,6 +764,8 @@ static ader_status create_impl(const ader_config* cfg, ader_ctx** out, bool loop
   *out = c;
   c->cfg = *cfg;
   c->part = pi;
+  for (int k = 0; k < 2 * c->d; ++k)
+    if (pi.nbr[k] < 0 && cfg->bc[k] == ADER_BC_EXACT) c->has_exact = true;
   c->d = cfg->dim; c->M = cfg->degree; c->N = c->M + 1;
   c->nv = nvar_of(cfg->system, cfg->dim);
   c->NS = 1;
@@ -890,16 +912,11 @@ ader_status ader_set_stream(ader_ctx* c, void* s) {
 
 double ader_time(const ader_ctx* c) { return c ? (c->amr ? amr_time(c->amr) : c->t) : 0.0; }
 
-ader_status ader_set_initial(ader_ctx* c, ader_ic_fn ic, void* user) {
-  if (!c || !ic) return ADER_ERR_ARG;
-  if (c->amr && c->loopback && c->cfg.world_size > 1)
-    return fail(c, ADER_ERR_ARG, "AMR group contexts are initialised through ader_debug_group_set_initial");
-  if (c->amr) {
-    std::string e;
-    ader_status s = amr_set_initial(c->amr, ic, user, e);
-    if (s != ADER_OK) c->err = e;
-    return s;
-  }
+// Cell averages of ic(x - shift) on the box of extents ext[] at the owned-block
+// offset off[] (<= 0: into the ghost layer): the host evaluates the callback
+// at the ic_quad^d Gauss-Legendre points (reading R6), the GPU forms the averages.
+static ader_status ic_box_average(ader_ctx* c, ader_ic_fn ic, void* user, const int off[3], const int ext[3],
+                           const double shift[3]) {
   const int Q = c->cfg.ic_quad, d = c->d;
   double qx[16], qw[16];
   gl_rule(Q, qx, qw);
@@ -912,13 +929,8 @@ ader_status ader_set_initial(ader_ctx* c, ader_ic_fn ic, void* user) {
     for (int k = 0; k < d; ++k) wg *= qw[gi[k]];
     wq[g] = wg;
   }
-  // IC box: the owned block, grown into the ghost layer on inflow sides (R23)
-  int off[3] = {0, 0, 0}, ext[3] = {c->n[0], c->n[1], c->n[2]};
-  for (int k = 0; k < d; ++k) {
-    if (c->part.nbr[2 * k] < 0 && c->cfg.bc[2 * k] == ADER_BC_INFLOW) { off[k] = -c->H; ext[k] += c->H; }
-    if (c->part.nbr[2 * k + 1] < 0 && c->cfg.bc[2 * k + 1] == ADER_BC_INFLOW) ext[k] += c->H;
-  }
   const long long ncells = (long long)ext[0] * ext[1] * ext[2];
+  if (ncells == 0) return ADER_OK;
   const long long chunk = std::max<long long>(1, std::min<long long>(ncells, (1 << 22) / nq));
   std::vector<double> x((size_t)chunk * nq * 3), pr((size_t)chunk * nq * 9);
   double *dprim = nullptr, *dwq = nullptr;
@@ -935,7 +947,7 @@ ader_status ader_set_initial(ader_ctx* c, ader_ic_fn ic, void* user) {
         const int gi[3] = {g % Q, (g / Q) % Q, g / (Q * Q)};
         double* xp = &x[(i * nq + g) * 3];
         for (int k = 0; k < 3; ++k)
-          xp[k] = (k < d) ? c->cfg.lo[k] + ((double)ii[k] + qx[gi[k]]) * c->dx[k] : 0.0;
+          xp[k] = (k < d) ? (c->cfg.lo[k] + ((double)ii[k] + qx[gi[k]]) * c->dx[k]) - shift[k] : 0.0;
       }
     }
     std::fill(pr.begin(), pr.begin() + ncur * nq * 9, 0.0);
@@ -946,12 +958,58 @@ ader_status ader_set_initial(ader_ctx* c, ader_ic_fn ic, void* user) {
   }
   cudaFree(dprim);
   cudaFree(dwq);
+  return ADER_OK;
+}
+
+// Reading R26: the ghost layer of every ADER_BC_EXACT side of this rank, over
+// the full padded extent of the other axes, takes the averages of the exact
+// solution ic(x - t exact_vel) at the step's start time t = c->t.
+static ader_status refresh_exact(ader_ctx* c) {
+  if (!c->has_exact || !c->ic) return ADER_OK;
+  const double shift[3] = {c->t * c->cfg.exact_vel[0], c->t * c->cfg.exact_vel[1], c->t * c->cfg.exact_vel[2]};
+  for (int a = 0; a < c->d; ++a)
+    for (int side = 0; side < 2; ++side) {
+      if (c->part.nbr[2 * a + side] >= 0 || c->cfg.bc[2 * a + side] != ADER_BC_EXACT) continue;
+      int off[3] = {0, 0, 0}, ext[3] = {1, 1, 1};
+      for (int k = 0; k < c->d; ++k) { off[k] = -c->H; ext[k] = c->n[k] + 2 * c->H; }
+      off[a] = side ? c->n[a] : -c->H;
+      ext[a] = c->H;
+      ader_status st = ic_box_average(c, c->ic, c->ic_user, off, ext, shift);
+      if (st != ADER_OK) return st;
+    }
+  return ADER_OK;
+}
+
+ader_status ader_set_initial(ader_ctx* c, ader_ic_fn ic, void* user) {
+  if (!c || !ic) return ADER_ERR_ARG;
+  if (c->amr && c->loopback && c->cfg.world_size > 1)
+    return fail(c, ADER_ERR_ARG, "AMR group contexts are initialised through ader_debug_group_set_initial");
+  if (c->amr) {
+    std::string e;
+    ader_status s = amr_set_initial(c->amr, ic, user, e);
+    if (s != ADER_OK) c->err = e;
+    return s;
+  }
+  c->ic = ic;
+  c->ic_user = user;
+  // IC box: the owned block, grown into the ghost layer on inflow and exact sides (R23, R26)
+  int off[3] = {0, 0, 0}, ext[3] = {c->n[0], c->n[1], c->n[2]};
+  for (int k = 0; k < c->d; ++k) {
+    const bool dl = c->cfg.bc[2 * k] == ADER_BC_INFLOW || c->cfg.bc[2 * k] == ADER_BC_EXACT;
+    const bool dh = c->cfg.bc[2 * k + 1] == ADER_BC_INFLOW || c->cfg.bc[2 * k + 1] == ADER_BC_EXACT;
+    if (c->part.nbr[2 * k] < 0 && dl) { off[k] = -c->H; ext[k] += c->H; }
+    if (c->part.nbr[2 * k + 1] < 0 && dh) ext[k] += c->H;
+  }
+  const double zero[3] = {0, 0, 0};
+  ader_status ist = ic_box_average(c, ic, user, off, ext, zero);
+  if (ist != ADER_OK) return ist;
   {
     StepState s0{};   // time restarts at 0
     CK(cudaMemcpy(c->st, &s0, sizeof(StepState), cudaMemcpyHostToDevice));
   }
   c->t = 0.0;
   c->speed_valid = false;
+  c->guess_ready = false;
   return ADER_OK;
 }
 
@@ -964,6 +1022,7 @@ ader_status ader_set_cells(ader_ctx* c, const double* u_host, int64_t n_cells) {
   launch_scatter(c->k, c->u, c->nv, b, c->stage);
   CK(cudaStreamSynchronize(c->k.stream));
   c->speed_valid = false;
+  c->guess_ready = false;   // R25: a new state has no previous step
   return ADER_OK;
 }
 
@@ -1012,8 +1071,8 @@ namespace {
 // second half of a uniform macro step, after the ghost fill + WENO: predictor,
 // face fluxes, update (fused with the next CFL speed)
 void advance_dt(ader_ctx* c, double dt, const double* dtdx_dev = nullptr) {
-  if (fused_weno_pred()) run_weno_predictor(c, dt, dtdx_dev);
-  else run_predictor(c, dt, dtdx_dev);
+  if (fused_weno_pred(c)) run_weno_predictor(c, dt, dtdx_dev);
+  else run_predictor(c, dt, dtdx_dev, true);
   run_flux(c);
   cudaMemsetAsync(&c->cnt->speed_bits, 0, sizeof(unsigned long long), c->k.stream);
   run_update(c, dt, dtdx_dev);
@@ -1027,7 +1086,7 @@ void advance_dt(ader_ctx* c, double dt, const double* dtdx_dev = nullptr) {
 ader_status enqueue_step(ader_ctx* c, double t_end) {
   ader_status st = fill_halo(c, c->u);
   if (st != ADER_OK) return st;
-  const bool fused = fused_weno_pred();
+  const bool fused = fused_weno_pred(c);
   if (!fused) run_weno(c);
   {
     Scope sc(c, ADER_K_OTHER, 0.0);
@@ -1040,7 +1099,7 @@ ader_status enqueue_step(ader_ctx* c, double t_end) {
     launch_step_dt(c->k, c->cnt, c->st, c->cfg.cfl, t_end, c->dx);
   }
   if (fused) run_weno_predictor(c, 0.0, c->st->dtdx);
-  else run_predictor(c, 0.0, c->st->dtdx);
+  else run_predictor(c, 0.0, c->st->dtdx, true);
   run_flux(c);
   CK(cudaMemsetAsync(&c->cnt->speed_bits, 0, sizeof(unsigned long long), c->k.stream));
   run_update(c, 0.0, c->st->dtdx);
@@ -1134,11 +1193,14 @@ ader_status ader_step(ader_ctx* c, double t_end, int64_t max_macro_steps, ader_s
   const long long steps0 = c->hst->steps;
   // enqueue the steps in chunks; dt lives on the device, the host only checks
   // time / errors between chunks (steps past t_end are no-ops, dt = 0)
-  const int64_t chunk = 16;
+  // (exact boundaries, R26: one step per chunk, the host refreshes their ghost
+  // layers at each step's start time)
+  const int64_t chunk = c->has_exact ? 1 : 16;
   int64_t enq = 0;
   while (enq < max_macro_steps && c->t < t_end) {
     const int64_t nstep = std::min<int64_t>(chunk, max_macro_steps - enq);
     const auto h0 = std::chrono::steady_clock::now();
+    if (c->has_exact) st = refresh_exact(c);
     for (int64_t i = 0; i < nstep && st == ADER_OK; ++i) st = enqueue_step(c, t_end);
     if (st != ADER_OK) break;
     enq += nstep;
@@ -1234,6 +1296,8 @@ ader_status ader_debug_group_step(ader_ctx** cs, int32_t n, double t_end, int64_
   };
   int64_t steps = 0;
   while (st == ADER_OK && steps < max_macro_steps && c->t < t_end) {
+    for (int i = 0; i < n && st == ADER_OK; ++i) st = refresh_exact(cs[i]);   // R26
+    if (st != ADER_OK) break;
     for (int a = 0; a < d; ++a) {
       for (int i = 0; i < n; ++i) halo_pack(cs[i], cs[i]->u, a);
       sync_all();
@@ -1254,7 +1318,7 @@ ader_status ader_debug_group_step(ader_ctx** cs, int32_t n, double t_end, int64_
     }
     double speed = 0.0;
     for (int i = 0; i < n && st == ADER_OK; ++i) {
-      if (!fused_weno_pred()) run_weno(cs[i]);
+      if (!fused_weno_pred(cs[i])) run_weno(cs[i]);
       double s = 0.0;
       st = global_speed(cs[i], &s);   // no communicator: this rank's max
       speed = std::max(speed, s);
@@ -1382,8 +1446,9 @@ ader_status ader_debug_dump(ader_ctx* c, int32_t what, double dt, double* out, i
     CK(cudaStreamSynchronize(c->k.stream));
     return ADER_OK;
   }
-  if (fused_weno_pred()) run_weno_predictor(c, dt);
+  if (fused_weno_pred(c)) run_weno_predictor(c, dt);
   else run_predictor(c, dt);
+  c->guess_ready = false;   // q no longer holds the last step's predictor
   if (what == 1) {
     if (capacity < b.count() * c->nv * c->NST) return fail(c, ADER_ERR_ARG, "capacity too small");
     launch_gather(c->k, c->q, (int)c->qs, b, c->stage);

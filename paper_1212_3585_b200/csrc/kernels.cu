@@ -106,10 +106,32 @@ __global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? 4 : 2) k_predictor(
     const double dtdx0, const double dtdx1, const double dtdx2, const double gamma, const double ch,
     const double tol, const int max_sweeps, DevCounters* __restrict__ cnt, const int* __restrict__ list,
     const long long nlist, const unsigned char* __restrict__ emask, const double* __restrict__ dtdx_dev,
-    const long long qs, const __grid_constant__ DevTables T) {
+    const long long qs, const int guess, const StepState* __restrict__ gst, const double guess_r,
+    const __grid_constant__ DevTables T) {
   using C = PredCfg<D, M, SYS>;
   constexpr int NV = C::NV, N = C::N, NS = C::NS, NST = C::NST, G = C::G, CPW = C::CPW, FSZ = C::FSZ;
   extern __shared__ double smem[];
+  // reading R25: extrapolation coefficients c[s][a] = psi_a(1 + r lambda_s) - psi_a(1)
+  // of the previous step's time pencil (Lagrange basis on the GL nodes)
+  double* gc = smem + WARPS * CPW * FSZ;                      // [N][N]
+  double r = 0.0;
+  if (guess) {
+    r = gst ? ((gst->prev_dt > 0.0 && gst->dt > 0.0) ? gst->dt / gst->prev_dt : 0.0) : guess_r;
+    if (threadIdx.x < N * N) {
+      const int s = threadIdx.x / N, a = threadIdx.x % N;
+      const double tau = 1.0 + r * T.lam[s];
+      double pt = 1.0, p1 = 1.0;
+      for (int m = 0; m < N; ++m)
+        if (m != a) {
+          const double den = T.lam[a] - T.lam[m];
+          pt *= (tau - T.lam[m]) / den;
+          p1 *= (1.0 - T.lam[m]) / den;
+        }
+      gc[threadIdx.x] = pt - p1;
+    }
+    __syncthreads();
+  }
+  const bool use_guess = guess && r > 0.0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int slot = lane / G, node0 = lane - slot * G;
   PredLane<D, M, SYS> L;
@@ -159,7 +181,24 @@ __global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? 4 : 2) k_predictor(
   }
   bool conv, bad;
   int nsw;
-  predictor_cell<D, M, SYS>(wv, qv, Fs, L, dtdx, cell_ok, gamma, ch, tol, max_sweeps, T, nsw, conv, bad);
+  if (use_guess && cell_ok && lane_ok) {
+    // q0 = w + sum_a c[s][a] q_prev[a] (the cell's previous q, read in place)
+    const double* qp = q + cell * qs + node;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      double old[N];
+#pragma unroll
+      for (int a = 0; a < N; ++a) old[a] = qp[v * NST + a * NS];
+#pragma unroll
+      for (int s2 = 0; s2 < N; ++s2) {
+        double acc = wv[v];
+#pragma unroll
+        for (int a = 0; a < N; ++a) acc += gc[s2 * N + a] * old[a];
+        qv[v][s2] = acc;
+      }
+    }
+  }
+  predictor_cell<D, M, SYS>(wv, qv, Fs, L, dtdx, cell_ok, gamma, ch, tol, max_sweeps, T, nsw, conv, bad, use_guess);
   if (active && (!emask || emask[cell])) {   // emask: cells whose errors count (multi-rank AMR: owned)
     if (bad) record_error(cnt, 1, 1, cell);
     else if (!conv) record_error(cnt, 2, 1, cell);
@@ -377,6 +416,7 @@ __global__ void k_step_dt(DevCounters* __restrict__ cnt, StepState* __restrict__
   if (!(t < t_end)) dt = 0.0;             // past t_end: the step is a no-op
   else if (t + dt > t_end) dt = t_end - t;
   const double dx[3] = {dx0, dx1, dx2};
+  st->prev_dt = st->dt;   // the previous step's dt (predictor guess, R25)
   st->dt = dt;
   for (int k = 0; k < 3; ++k) st->dtdx[k] = k < d ? dt / dx[k] : 0.0;
   st->t = t + dt;
@@ -493,7 +533,7 @@ size_t pred_smem() {
   constexpr int NV = Phys<SYS, D>::NV, N = M + 1, NS = ipow_c(N, D);
   constexpr int G = (NS <= 8) ? 8 : (NS <= 16 ? 16 : 32), CPW = 32 / G;
   constexpr int LP = (N == 4) ? 4 : N;
-  return sizeof(double) * ((size_t)kPredWarps * CPW * (D * NV * N * (NS / N) * LP + 8));
+  return sizeof(double) * ((size_t)kPredWarps * CPW * (D * NV * N * (NS / N) * LP + 8) + N * N);   // + R25 coefficients
 }
 }  // namespace
 
@@ -536,13 +576,16 @@ void launch_weno_sweep(const KCtx& k, int sweep, const double* src, double* dst,
 }
 
 void launch_predictor(const KCtx& k, const double* w, double* q, const Box& region, const double dtdx[3],
-                      double tol, int max_sweeps, DevCounters* cnt, const double* dtdx_dev, long long qs) {
-  launch_predictor_list(k, w, q, region, nullptr, 0, dtdx, tol, max_sweeps, cnt, nullptr, dtdx_dev, qs);
+                      double tol, int max_sweeps, DevCounters* cnt, const double* dtdx_dev, long long qs, bool guess,
+                      const StepState* gst, double guess_r) {
+  launch_predictor_list(k, w, q, region, nullptr, 0, dtdx, tol, max_sweeps, cnt, nullptr, dtdx_dev, qs, guess, gst,
+                        guess_r);
 }
 
 void launch_predictor_list(const KCtx& k, const double* w, double* q, const Box& region, const int* list,
                            long long nlist, const double dtdx[3], double tol, int max_sweeps, DevCounters* cnt,
-                           const unsigned char* emask, const double* dtdx_dev, long long qs) {
+                           const unsigned char* emask, const double* dtdx_dev, long long qs, bool guess,
+                           const StepState* gst, double guess_r) {
   const long long count = list ? nlist : region.count();
   if (count == 0) return;
   ADER_DISPATCH(k.D, k.M, k.SYS, {
@@ -564,7 +607,8 @@ void launch_predictor_list(const KCtx& k, const double* w, double* q, const Box&
     const unsigned g = need < 148u * 16u ? need : 148u * 16u;
     count_launch(k);
     kern<<<g, kPredWarps * 32, sm, k.stream>>>(w, q, region, k.sy, k.sz, dtdx[0], dtdx[1], dtdx[2], k.gamma,
-                                                k.ch, tol, max_sweeps, cnt, list, nlist, emask, dtdx_dev, qstride, k.tab);
+                                                k.ch, tol, max_sweeps, cnt, list, nlist, emask, dtdx_dev, qstride, guess ? 1 : 0,
+                                                gst, guess_r, k.tab);
   });
 }
 

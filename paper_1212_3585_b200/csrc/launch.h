@@ -40,6 +40,7 @@ struct StepState {
   double t, dt, last_dt;          // time reached, dt of the last step, last positive dt
   double dtdx[3];                 // dt / dx_dir of the last step (read by predictor / update)
   long long steps;                // steps with dt > 0
+  double prev_dt;                 // dt of the step before the last (predictor guess, R25)
 };
 
 // Instrumentation hook (CUDA events around launches, set by ader_api.cpp).
@@ -69,15 +70,19 @@ void launch_weno_sweep(const KCtx& k, int sweep, const double* src, double* dst,
 // device (StepState::dtdx) instead of dtdx.
 // qs: stride of a cell's q block in doubles (0 = nu N^(d+1); the uniform path
 // uses q_block_stride, the block size rounded up to even).
+// guess (reading R25): start the Picard iteration from the cell's previous q
+// (read in place from q) extrapolated by r = dt_n / dt_{n-1}: r from gst
+// (device StepState: dt / prev_dt) if given, else guess_r; r <= 0 = R3.
 void launch_predictor(const KCtx& k, const double* w, double* q, const Box& region, const double dtdx[3],
                       double tol, int max_sweeps, DevCounters* cnt, const double* dtdx_dev = nullptr,
-                      long long qs = 0);
+                      long long qs = 0, bool guess = false, const StepState* gst = nullptr, double guess_r = 0.0);
 // Predictor on the cells of an id list (AMR levels): w, q indexed by id.  If
 // emask is given only cells with emask[id] != 0 report solver errors.
 void launch_predictor_list(const KCtx& k, const double* w, double* q, const Box& region, const int* list,
                            long long nlist, const double dtdx[3], double tol, int max_sweeps, DevCounters* cnt,
                            const unsigned char* emask = nullptr, const double* dtdx_dev = nullptr,
-                           long long qs = 0);
+                           long long qs = 0, bool guess = false, const StepState* gst = nullptr,
+                           double guess_r = 0.0);
 // Face fluxes on the lower face of every cell of `ext` (owned block + 1 on each
 // active axis), one lane group per cell computing all its lower faces
 // (L2-friendly traversal).  bmask bit 2*dir (2*dir+1): the first (last) face

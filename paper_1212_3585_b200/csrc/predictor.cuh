@@ -60,7 +60,7 @@ struct PredLane {
 };
 
 // Picard iteration of one cell per lane group (all 32 lanes of the warp call
-// it together; cell_ok false for a lane group without a cell).  wv: this
+// it together, with the same from_guess; cell_ok false for a lane group without a cell).  wv: this
 // node's w (eqn.weno.z); on return qv holds the node's time pencil, nsw the
 // sweeps, conv the convergence flag (reading R2), bad an inadmissible state.
 // Sweep 1 starts from the time-constant guess q^0 = w (R3): all N time levels
@@ -70,7 +70,8 @@ __device__ __forceinline__ void predictor_cell(const double (&wv)[Phys<SYS, D>::
                                                double (&qv)[Phys<SYS, D>::NV][M + 1], double* Fs,
                                                const PredLane<D, M, SYS>& L, const double (&dtdx)[3], bool cell_ok,
                                                double gamma, double ch, double tol, int max_sweeps,
-                                               const DevTables& T, int& nsw, bool& conv, bool& bad) {
+                                               const DevTables& T, int& nsw, bool& conv, bool& bad,
+                                               bool from_guess = false) {
   using PH = Phys<SYS, D>;
   using C = PredCfg<D, M, SYS, PERS>;
   constexpr int NV = C::NV, N = C::N, NS = C::NS, G = C::G;
@@ -189,7 +190,9 @@ __device__ __forceinline__ void predictor_cell(const double (&wv)[Phys<SYS, D>::
       if (dmax < 0x7FF00000u && qmax < 0x7FF00000u && dup <= tol * (1.0 + qlo)) conv = true;   // reading R2
     }
   };
-  if (max_sweeps >= 1) sweep_once(std::integral_constant<bool, true>());
+  // (from_guess: qv holds the caller's initial guess (reading R25), whose time
+  // levels differ, so every sweep is a full one)
+  if (max_sweeps >= 1 && !from_guess) sweep_once(std::integral_constant<bool, true>());
   // every lane takes part in the vote (lane groups of a warp may stop at
   // different sweep counts)
   while (!__all_sync(0xffffffffu, conv || nsw >= max_sweeps)) {

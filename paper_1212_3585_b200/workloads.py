@@ -102,6 +102,56 @@ def shock_tube(axis=0, x0=0.5, left=(1.0, 0.0, 1.0), right=(0.125, 0.0, 0.1)):
     return ic
 
 
+# Double Mach reflection (eqn.dmr.ic), reading R27: the shock
+# front is the line x' = (x - 1/6) cos(a) - y sin(a) = 0 with a = 30 degrees
+# (the line through (1/6, 0) at 60 degrees to the x axis, the paper's
+# "inclination angle of 60 degrees"), post-shock for x' < 0 with velocity
+# 8.25 (cos a, -sin a) along the front normal (the paper prints +8.25 sin a,
+# which would point the post-shock flow away from the shock it comes from),
+# pre-shock (1.4, 0, 0, 0, 1).  The front moves with the Mach-10 shock speed
+# 10 (pre-shock sound speed 1) along its normal: DMR_FRONT_VEL = 10 (cos a, -sin a).
+DMR_ALPHA = math.pi / 6.0
+DMR_FRONT_VEL = (10.0 * math.cos(DMR_ALPHA), -10.0 * math.sin(DMR_ALPHA), 0.0)
+
+
+def dmr_states(mach=10.0, gamma=1.4):
+    """(post (rho, u_n, p), pre (rho, 0, p), front speed) of a shock of Mach
+    number `mach` into (rho, p) = (1.4, 1) (sound speed 1), Rankine-Hugoniot.
+    mach = 10 gives the paper's printed (8, 8.25, 116.5)."""
+    r1, p1 = 1.4, 1.0
+    m2 = mach * mach
+    r2 = r1 * (gamma + 1.0) * m2 / ((gamma - 1.0) * m2 + 2.0)
+    p2 = p1 * (1.0 + 2.0 * gamma / (gamma + 1.0) * (m2 - 1.0))
+    u2 = mach * (1.0 - r1 / r2)
+    return (r2, u2, p2), (r1, 0.0, p1), mach
+
+
+def double_mach_reflection(mach=10.0):
+    """the paper's states at mach = 10 (printed values); other
+    Mach numbers from dmr_states (the same geometry)"""
+    ca, sa = math.cos(DMR_ALPHA), math.sin(DMR_ALPHA)
+    if mach == 10.0:
+        post, pre = (8.0, 8.25, 116.5), (1.4, 0.0, 1.0)
+    else:
+        post, pre, _ = dmr_states(mach)
+
+    def ic(x):
+        x = np.asarray(x, dtype=np.float64)
+        xp = (x[:, 0] - 1.0 / 6.0) * ca - x[:, 1] * sa
+        ps = xp < 0.0
+        out = np.zeros((x.shape[0], 9))
+        out[:, 0] = np.where(ps, post[0], pre[0])
+        out[:, 1] = np.where(ps, post[1] * ca, 0.0)
+        out[:, 2] = np.where(ps, -post[1] * sa, 0.0)
+        out[:, 4] = np.where(ps, post[2], pre[2])
+        return out
+    return ic
+
+
+def dmr_front_vel(mach=10.0):
+    return (mach * math.cos(DMR_ALPHA), -mach * math.sin(DMR_ALPHA), 0.0)
+
+
 def constant_state(rho=1.0, v=(0.3, -0.2, 0.1), p=0.7, B=(0.0, 0.0, 0.0)):
     def ic(x):
         out = np.zeros((np.asarray(x).shape[0], 9))
@@ -220,4 +270,17 @@ def config(name: str, n=None) -> Workload:
         return Workload("c6_explosion3d_amr", 3, 0, 2, (nn, nn, nn), (-1.0,) * 3, (1.0,) * 3,
                         (T,) * 6, 1.4, 0.2, 0.25, ic=explosion(3), refine_factor=3, lmax=2,
                         chi_ref=0.05, chi_rec=0.025)
+    if name in ("dmr", "dmr2"):
+        # double Mach reflection on a uniform grid,
+        # [0,3] x [0,1], exact solution prescribed left / top / right (reading
+        # R26), reflective wall at the bottom (R22), Rusanov, O3.  "dmr" is the
+        # paper's Mach-10 problem to t = 0.2: with the literal reflective bottom
+        # the reconstruction at the shock foot is inadmissible in the first step
+        # (oracle and CUDA path alike, reading R27); "dmr2" is the same geometry
+        # at shock Mach 2, run to t = 1.0 (the front covers the same distance)
+        nn = n or 240
+        mach = 10.0 if name == "dmr" else 2.0
+        return Workload(f"{name}_o3_{nn}x{nn // 3}", 2, 0, 2, (nn, nn // 3), (0.0, 0.0), (3.0, 1.0),
+                        (4, 4, 2, 4, 0, 0), 1.4, 0.45, 2.0 / mach, ic=double_mach_reflection(mach),
+                        extra=dict(exact_vel=dmr_front_vel(mach), mach=mach))
     raise KeyError(name)

@@ -43,6 +43,13 @@ CASES = {
                        W.random_smooth(2, seed=3585, amp=0.2), 4, 5),
     "inflow3d_x4": (dict(dim=3, degree=2, n0=(12, 10, 9), lo=(0,) * 3, hi=(1,) * 3, bc=(3, 1, 0, 0, 3, 1), cfl=0.3),
                     W.random_smooth(3, seed=1212, amp=0.08), 4, 3),
+    # time-dependent exact boundaries (R26): the DMR geometry at Mach 2, and a
+    # traveling wave leaving / entering through exact sides in 3D
+    "dmr2_exact_x3": (dict(dim=2, degree=2, n0=(48, 16), lo=(0, 0), hi=(3, 1), bc=(4, 4, 2, 4, 0, 0), cfl=0.45,
+                           exact_vel=W.dmr_front_vel(2.0)), W.double_mach_reflection(2.0), 3, 6),
+    "traveling3d_exact_x4": (dict(dim=3, degree=2, n0=(12, 10, 9), lo=(0,) * 3, hi=(1,) * 3, bc=(4,) * 6, cfl=0.5,
+                                  exact_vel=(0.8, 0.35, -0.2)),
+                             W.entropy_wave(3, amp=0.2, v=(0.8, 0.35, -0.2)), 4, 4),
 }
 
 
