@@ -40,6 +40,21 @@ def fp64_peak_tflops(mhz):
     return SM_COUNT * FP64_FMA_PER_CLK * 2 * mhz * 1e6 / 1e12
 
 
+def fp64_peak():
+    """(peak TFLOP/s, note): the measured DFMA throughput of this pool's B200s
+    (tools/fp64_peak.cu under tools/gpu_fp64_peak.sh, SM clock sampled during
+    the run; sustained = 4 s back to back, the regime of a kernel timed inside
+    a long step), else the figure derived from unit counts and clocks."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "round2_fp64_peak.json")))
+        return float(d["fp64_fma_tflops_sustained"]), (
+            f"measured DFMA sustained {d['fp64_fma_tflops_sustained']:.1f} TF/s at median "
+            f"{d['sm_mhz_median_under_load']:.0f} MHz (burst {d['fp64_fma_tflops_burst']:.1f}; derived "
+            f"{fp64_peak_tflops(1965.0):.1f} at 1965 MHz), profiles/round2_fp64_peak.json (of measured)")
+    except Exception:
+        return fp64_peak_tflops(1965.0), "FP64 FMA pipe: 148 SM x 64 lanes x 2 x 1.965 GHz (derived, DESIGN.md)"
+
+
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
@@ -51,6 +66,8 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=5)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-box", type=int, default=12, help="edge of the oracle sample box (cells)")
+    p.add_argument("--pred-guess", type=int, default=0, choices=[0, 1],
+                   help="Picard initial guess: 0 time-constant (R3), 1 extrapolated previous q (R25)")
     p.add_argument("--flux", default="rusanov", choices=["rusanov", "osher"],
                    help="two-point flux (BASELINE: rusanov; the paper's explosions use osher)")
     p.add_argument("--load-balance", type=int, default=1, choices=[0, 1],
@@ -247,7 +264,8 @@ def main():
                            gamma=wl.gamma, ch=wl.ch, cfl=wl.cfl, rank=rank, world_size=world, device=local,
                            nccl_id=nid, lmax=wl.lmax, refine_factor=wl.refine_factor, adapt_every=1,
                            chi_ref=wl.chi_ref, chi_rec=wl.chi_rec, flux=1 if args.flux == "osher" else 0,
-                           load_balance=1 if (wl.lmax > 0 and world > 1 and args.load_balance) else 0)
+                           load_balance=1 if (wl.lmax > 0 and world > 1 and args.load_balance) else 0,
+                           pred_guess=args.pred_guess, exact_vel=wl.extra.get("exact_vel", (0.0, 0.0, 0.0)))
     s = ader.Solver(cfg)
     stream = torch.cuda.current_stream()
     s.set_stream(stream.cuda_stream)
@@ -338,7 +356,7 @@ def main():
         pred_ms_avg = kms[ader.K_PRED] / max(1, kl[ader.K_PRED])
         pred_flops = kfl[ader.K_PRED] / max(1, kl[ader.K_PRED])
         achieved = pred_flops / (pred_ms_avg / 1e3) / 1e12
-        peak = fp64_peak_tflops(1965.0)
+        peak, peak_note = fp64_peak()
         # algorithmic bytes of one predictor launch: read w, write q of every predicted cell
         N = wl.degree + 1
         nvv = 9 if wl.system == 1 else wl.dim + 2
@@ -354,8 +372,9 @@ def main():
         gbs = pred_bytes / (pred_ms_avg / 1e3) / 1e9
         if ai >= ridge:
             roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                    "peak_note": "FP64 FMA pipe: 148 SM x 64 lanes x 2 x 1.965 GHz (derived, DESIGN.md)",
-                    "achieved_note": "algorithmic FP64 flops of the Picard sweeps actually run / CUDA-event time"}
+                    "peak_note": peak_note,
+                    "achieved_note": "algorithmic FP64 flops of the Picard sweeps actually run (first sweep at "
+                                     "its N^d-flux cost) / CUDA-event time"}
         else:
             roof = {"bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak,
                     "peak_note": "measured copy bandwidth, MEASURED_PEAKS.json hbm_gbs (of measured)",
@@ -389,6 +408,14 @@ def main():
         dominant = roof
         if roof_flux is not None and kms[ader.K_FLUX] > kms[ader.K_PRED]:
             dominant = roof_flux
+        # north_star: the stdg_predictor + weno_reconstruct path against the FP64 roofline
+        pw_ms = kms[ader.K_WENO] + kms[ader.K_PRED]
+        pw_tf = (kfl[ader.K_WENO] + kfl[ader.K_PRED]) / max(1, args.steps) / (pw_ms / max(1, args.steps) / 1e3) / 1e12 \
+            if pw_ms > 0 else 0.0
+        pred_weno = {"kernels": "weno_reconstruct + stdg_predictor", "alu_tflops": pw_tf, "peak": peak,
+                     "frac": pw_tf / peak, "ms_per_step": pw_ms / max(1, args.steps),
+                     "note": "algorithmic FP64 flops (WENO problems of the three sweeps + Picard sweeps) / "
+                             "their CUDA-event time"}
         step_ms = ms_max / args.steps
         share = {ader.KERNEL_NAMES[i]: round(kms[i] / max(1e-9, ms) , 4) for i in range(ader.K_COUNT)}
         line = {
@@ -398,9 +425,16 @@ def main():
             "config": {"workload": wl.name, "dim": wl.dim, "degree": wl.degree, "order": wl.degree + 1,
                        "cells": list(wl.n), "system": "euler" if wl.system == 0 else "mhd_glm",
                        "flux": args.flux, "cfl": wl.cfl, "ic": "explosion r<0.5" if "explosion" in wl.name else wl.name,
-                       "parallelism": f"level-0 blocks x{world}" + (" (dynamic RCB)" if cfg.load_balance else ""), "l2": "inputs larger than L2 (~90 GB working set)"},
+                       "parallelism": f"level-0 blocks x{world}" + (" (dynamic RCB)" if cfg.load_balance else ""),
+                       "l2": "inputs larger than L2 (~90 GB working set)" if wl.lmax == 0 and wl.dim == 3 else
+                             "state + stage arrays re-written every step (no flush)",
+                       **({"lmax": wl.lmax, "refine_factor": wl.refine_factor, "chi_ref": wl.chi_ref,
+                           "chi_rec": wl.chi_rec, "chi_note": "outside the paper's 0.2-0.25 / 0.05-0.15 ranges "
+                           "(P:630-632) where noted in DESIGN.md R1"} if wl.lmax > 0 else {}),
+                       "pred_guess": args.pred_guess},
             "roofline": dominant,
             "roofline_kernels": [r for r in (roof, roof_flux) if r is not None],
+            "pred_weno_fp64": pred_weno,
             "kernel_share_of_step": share,
             "pred_sweeps_mean": rep.pred_sweeps_total / max(1, rep.pred_cells),
             "clocks": clocks,
