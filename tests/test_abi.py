@@ -39,7 +39,7 @@ def _cfg(**kw):
                                 dict(bc=(0, 1, 0, 0, 0, 0)), dict(dim=3, degree=3, n0=(8, 8, 8)),
                                 dict(lmax=1, refine_factor=1), dict(flux=2), dict(flux=1, system=1),
                                 dict(flux=1, flux_quad=5), dict(bc=(2, 2, 0, 0, 0, 0), system=1),
-                                dict(bc=(2, 2, 0, 0, 0, 0), n0=(2, 16)), dict(bc=(4,) * 6),
+                                dict(bc=(2, 2, 0, 0, 0, 0), n0=(2, 16)), dict(bc=(5,) * 6),
                                 dict(load_balance=2), dict(load_balance=-1)])
 def test_create_rejects_bad_config_before_allocation(kw):
     cfg = _cfg(**kw)
