@@ -353,69 +353,76 @@ def main():
                "note": "AMR: no per-step host input; wall clock incl. ader_get_cells readback"}
 
     if rank == 0:
-        pred_ms_avg = kms[ader.K_PRED] / max(1, kl[ader.K_PRED])
-        pred_flops = kfl[ader.K_PRED] / max(1, kl[ader.K_PRED])
-        achieved = pred_flops / (pred_ms_avg / 1e3) / 1e12
         peak, peak_note = fp64_peak()
-        # algorithmic bytes of one predictor launch: read w, write q of every predicted cell
         N = wl.degree + 1
         nvv = 9 if wl.system == 1 else wl.dim + 2
-        cells_per_launch = rep.pred_cells / max(1, kl[ader.K_PRED])
-        pred_bytes = cells_per_launch * nvv * (N ** wl.dim + N ** (wl.dim + 1)) * 8
         hbm_peak = 6449.1
         try:
             hbm_peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
         except Exception:
             pass
-        ai = pred_flops / max(1.0, pred_bytes)                       # flop / byte
         ridge = peak * 1e12 / (hbm_peak * 1e9)
-        gbs = pred_bytes / (pred_ms_avg / 1e3) / 1e9
-        if ai >= ridge:
-            roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                    "peak_note": peak_note,
-                    "achieved_note": "algorithmic FP64 flops of the Picard sweeps actually run (first sweep at "
-                                     "its N^d-flux cost) / CUDA-event time"}
-        else:
-            roof = {"bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak,
-                    "peak_note": "measured copy bandwidth, MEASURED_PEAKS.json hbm_gbs (of measured)",
-                    "achieved_note": "algorithmic bytes (w read + q written per predicted cell) / CUDA-event time"}
-        roof.update({"kernel": "stdg_predictor", "traffic": load_traffic(wl, "stdg_predictor"),
-                     "ncu_fp64_hw_frac": load_traffic(wl, "stdg_predictor", "fp64_hw_frac"),
-                     "arith_intensity_flop_per_byte": ai,
-                     "ridge_flop_per_byte": ridge, "alu_tflops": achieved, "alu_frac": achieved / peak,
-                     "hbm_gbs": gbs, "hbm_frac": gbs / hbm_peak})
-        # face flux (uniform grids): algorithmic bytes = every q read once + F written
-        roof_flux = None
-        if wl.lmax == 0 and kl[ader.K_FLUX]:
-            fl_ms = kms[ader.K_FLUX] / kl[ader.K_FLUX]
-            fl_flops = kfl[ader.K_FLUX] / kl[ader.K_FLUX]
-            nb = [int(k) for k in wl.n]
-            if world > 1:
-                nb = [int(np.ceil(k / p)) for k, p in zip(nb, [2, 2, 2][:wl.dim])]
-            ext = int(np.prod([k + 1 for k in nb]))
-            fl_bytes = ext * nvv * (N ** (wl.dim + 1) + wl.dim) * 8
-            f_gbs = fl_bytes / (fl_ms / 1e3) / 1e9
-            f_tf = fl_flops / (fl_ms / 1e3) / 1e12
-            f_ai = fl_flops / fl_bytes
-            roof_flux = {"kernel": f"face_flux_{args.flux}", "bound": "alu" if f_ai >= ridge else "hbm",
-                         "achieved": f_tf if f_ai >= ridge else f_gbs, "peak": peak if f_ai >= ridge else hbm_peak,
-                         "unit": "TFLOP/s" if f_ai >= ridge else "GB/s",
-                         "frac": (f_tf / peak) if f_ai >= ridge else (f_gbs / hbm_peak),
-                         "traffic": load_traffic(wl, f"face_flux_{args.flux}"), "arith_intensity_flop_per_byte": f_ai,
-                         "ncu_fp64_hw_frac": load_traffic(wl, f"face_flux_{args.flux}", "fp64_hw_frac"),
-                         "alu_tflops": f_tf, "hbm_gbs": f_gbs,
-                         "achieved_note": "algorithmic bytes (each q read once, F written) / CUDA-event time"}
-        dominant = roof
-        if roof_flux is not None and kms[ader.K_FLUX] > kms[ader.K_PRED]:
-            dominant = roof_flux
+
+        def entry(kernel, ms_avg, flops, nbytes, bytes_note, flops_note):
+            """roofline of one kernel class: bound by its algorithmic intensity vs the ridge"""
+            tf = flops / (ms_avg / 1e3) / 1e12
+            gbs = nbytes / (ms_avg / 1e3) / 1e9
+            ai = flops / max(1.0, nbytes)
+            if ai >= ridge:
+                e = {"bound": "alu", "achieved": tf, "peak": peak, "unit": "TFLOP/s", "frac": tf / peak,
+                     "peak_note": peak_note, "achieved_note": flops_note}
+            else:
+                e = {"bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak,
+                     "peak_note": "measured copy bandwidth, MEASURED_PEAKS.json hbm_gbs (of measured)",
+                     "achieved_note": bytes_note}
+            e.update({"kernel": kernel, "traffic": load_traffic(wl, kernel),
+                      "ncu_fp64_hw_frac": load_traffic(wl, kernel, "fp64_hw_frac"),
+                      "arith_intensity_flop_per_byte": ai, "ridge_flop_per_byte": ridge, "alu_tflops": tf,
+                      "alu_frac": tf / peak, "hbm_gbs": gbs, "hbm_frac": gbs / hbm_peak, "ms_per_launch": ms_avg})
+            return e
+
+        # face box of the uniform path: owned + 1 per axis (faces = its lower faces)
+        nb = [int(k) for k in wl.n]
+        if world > 1:
+            nb = [int(np.ceil(k / p)) for k, p in zip(nb, [2, 2, 2][:wl.dim])]
+        ext = int(np.prod([k + 1 for k in nb]))
+        sweeps_note = "algorithmic FP64 flops of the Picard sweeps actually run (first sweep at its N^d-flux cost)"
+        entries = []
+        if kl[ader.K_PRED]:
+            # algorithmic bytes of one predictor launch: read w, write q of every predicted cell
+            cells_per_launch = rep.pred_cells / max(1, kl[ader.K_PRED])
+            entries.append(entry("stdg_predictor", kms[ader.K_PRED] / kl[ader.K_PRED],
+                                 kfl[ader.K_PRED] / kl[ader.K_PRED],
+                                 cells_per_launch * nvv * (N ** wl.dim + N ** (wl.dim + 1)) * 8,
+                                 "algorithmic bytes (w read + q written per predicted cell) / CUDA-event time",
+                                 sweeps_note + " / CUDA-event time"))
+        if wl.lmax == 0 and kl[ader.K_FLUX] and not kl[ader.K_PRED_FLUX]:
+            # face flux: algorithmic bytes = every q read once + F written
+            entries.append(entry(f"face_flux_{args.flux}", kms[ader.K_FLUX] / kl[ader.K_FLUX],
+                                 kfl[ader.K_FLUX] / kl[ader.K_FLUX], ext * nvv * (N ** (wl.dim + 1) + wl.dim) * 8,
+                                 "algorithmic bytes (each q read once, F written) / CUDA-event time",
+                                 "algorithmic FP64 flops of the face quadrature / CUDA-event time"))
+        if kl[ader.K_PRED_FLUX]:
+            # fused a2 + a3 walk (+ its tile-face kernel): w read, F written; q never leaves the SM
+            cells_per_launch = rep.pred_cells / max(1, kl[ader.K_PRED_FLUX])
+            entries.append(entry(f"stdg_predictor+face_flux_{args.flux}", kms[ader.K_PRED_FLUX] / kl[ader.K_PRED_FLUX],
+                                 kfl[ader.K_PRED_FLUX] / kl[ader.K_PRED_FLUX],
+                                 cells_per_launch * nvv * N ** wl.dim * 8 + ext * nvv * wl.dim * 8,
+                                 "algorithmic bytes (w read per predicted cell + F written) / CUDA-event time",
+                                 sweeps_note + " + the face quadrature's flops / CUDA-event time (walk + "
+                                 "tile-face kernel)"))
+        kind_of = {"stdg_predictor": ader.K_PRED, f"face_flux_{args.flux}": ader.K_FLUX,
+                   f"stdg_predictor+face_flux_{args.flux}": ader.K_PRED_FLUX}
+        dominant = max(entries, key=lambda e: kms[kind_of[e["kernel"]]]) if entries else None
         # north_star: the stdg_predictor + weno_reconstruct path against the FP64 roofline
-        pw_ms = kms[ader.K_WENO] + kms[ader.K_PRED]
-        pw_tf = (kfl[ader.K_WENO] + kfl[ader.K_PRED]) / max(1, args.steps) / (pw_ms / max(1, args.steps) / 1e3) / 1e12 \
+        pk = ader.K_PRED_FLUX if kl[ader.K_PRED_FLUX] else ader.K_PRED
+        pw_ms = kms[ader.K_WENO] + kms[pk]
+        pw_tf = (kfl[ader.K_WENO] + kfl[pk]) / max(1, args.steps) / (pw_ms / max(1, args.steps) / 1e3) / 1e12 \
             if pw_ms > 0 else 0.0
-        pred_weno = {"kernels": "weno_reconstruct + stdg_predictor", "alu_tflops": pw_tf, "peak": peak,
+        pred_weno = {"kernels": "weno_reconstruct + " + ader.KERNEL_NAMES[pk], "alu_tflops": pw_tf, "peak": peak,
                      "frac": pw_tf / peak, "ms_per_step": pw_ms / max(1, args.steps),
-                     "note": "algorithmic FP64 flops (WENO problems of the three sweeps + Picard sweeps) / "
-                             "their CUDA-event time"}
+                     "note": "algorithmic FP64 flops (WENO problems of the three sweeps + Picard sweeps"
+                             + (" + face quadrature" if pk == ader.K_PRED_FLUX else "") + ") / their CUDA-event time"}
         step_ms = ms_max / args.steps
         share = {ader.KERNEL_NAMES[i]: round(kms[i] / max(1e-9, ms) , 4) for i in range(ader.K_COUNT)}
         line = {
@@ -433,7 +440,7 @@ def main():
                            "(P:630-632) where noted in DESIGN.md R1"} if wl.lmax > 0 else {}),
                        "pred_guess": args.pred_guess},
             "roofline": dominant,
-            "roofline_kernels": [r for r in (roof, roof_flux) if r is not None],
+            "roofline_kernels": entries,
             "pred_weno_fp64": pred_weno,
             "kernel_share_of_step": share,
             "pred_sweeps_mean": rep.pred_sweeps_total / max(1, rep.pred_cells),

@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define ADER_ABI_VERSION 4
+#define ADER_ABI_VERSION 5
 
 typedef struct ader_ctx ader_ctx;   /* opaque; owns all device memory it allocates */
 
@@ -98,6 +98,12 @@ typedef struct {
                                  * set_initial / set_cells)                         */
   double  exact_vel[3];         /* ADER_BC_EXACT sides: front velocity of the exact
                                  * solution u(x, t) = ic(x - t exact_vel) (R26)     */
+  int32_t fuse_pred_flux;       /* uniform grids: 0 = separate a2 (predictor) and a3
+                                 * (face flux) kernels with q_h in HBM (default); 1 = both
+                                 * in one tile walk with q_h kept on chip (pred_flux.cu;
+                                 * measured slower at C4; ignored with
+                                 * pred_guess = 1, which reads the previous q_h).  The
+                                 * same fluxes either way (bitwise for Euler).         */
 } ader_config;
 
 /* Batched IC callback (host): x[n][3] -> prim[n][9] with
@@ -212,7 +218,8 @@ ader_status ader_nccl_unique_id(uint8_t out[128]);
 
 /* --- instrumentation / test hooks ---------------------------------------- */
 enum { ADER_K_WENO = 0, ADER_K_PRED = 1, ADER_K_FLUX = 2, ADER_K_UPDATE = 3,
-       ADER_K_HALO = 4, ADER_K_OTHER = 5, ADER_K_COUNT = 6 };
+       ADER_K_HALO = 4, ADER_K_OTHER = 5, ADER_K_PRED_FLUX = 6 /* fused a2 + a3 tile walk */,
+       ADER_K_COUNT = 7 };
 /* When on, every kernel launch is bracketed by CUDA events on the launch
  * stream; ader_kernel_stats returns, per kernel class, total device ms,
  * launch count and the algorithmic FP64 flops of those launches. */

@@ -15,12 +15,13 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libader_b200.so")
 _LIB = None
 
-ABI_VERSION = 4
+ABI_VERSION = 5
 EULER, MHD_GLM = 0, 1
 PERIODIC, TRANSMISSIVE, REFLECTIVE, INFLOW = 0, 1, 2, 3
 RUSANOV, OSHER = 0, 1
-K_WENO, K_PRED, K_FLUX, K_UPDATE, K_HALO, K_OTHER, K_COUNT = range(7)
-KERNEL_NAMES = ("weno_reconstruct", "stdg_predictor", "face_flux", "fv_update", "halo", "other")
+K_WENO, K_PRED, K_FLUX, K_UPDATE, K_HALO, K_OTHER, K_PRED_FLUX, K_COUNT = range(8)
+KERNEL_NAMES = ("weno_reconstruct", "stdg_predictor", "face_flux", "fv_update", "halo", "other",
+                "stdg_predictor+face_flux")
 STATUS = {0: "ADER_OK", 1: "ADER_ERR_ARG", 2: "ADER_ERR_CONFIG", 3: "ADER_ERR_SOLVER", 4: "ADER_ERR_CUDA",
           5: "ADER_ERR_NCCL", 6: "ADER_ERR_UNSUPPORTED"}
 
@@ -40,7 +41,7 @@ class AderConfig(C.Structure):
         ("rank", C.c_int32), ("world_size", C.c_int32), ("device", C.c_int32),
         ("nccl_id", C.c_uint8 * 128),
         ("flux", C.c_int32), ("flux_quad", C.c_int32), ("load_balance", C.c_int32),
-        ("pred_guess", C.c_int32), ("exact_vel", C.c_double * 3),
+        ("pred_guess", C.c_int32), ("exact_vel", C.c_double * 3), ("fuse_pred_flux", C.c_int32),
     ]
 
 
@@ -130,7 +131,7 @@ def make_config(*, dim, degree, n0, lo, hi, bc, system=EULER, gamma=1.4, ch=0.0,
                 refine_factor=3, lmax=0, chi_ref=0.2, chi_rec=0.1, chi_eps=0.01, pred_tol=1e-13,
                 pred_max_sweeps=32, ic_quad=0, adapt_every=1, rank=0, world_size=1, device=-1,
                 nccl_id=None, flux=RUSANOV, flux_quad=0, load_balance=0, pred_guess=0,
-                exact_vel=(0.0, 0.0, 0.0)) -> AderConfig:
+                exact_vel=(0.0, 0.0, 0.0), fuse_pred_flux=None) -> AderConfig:
     cfg = AderConfig()
     cfg.abi_version = ABI_VERSION
     cfg.dim, cfg.system, cfg.degree = dim, system, degree
@@ -150,6 +151,11 @@ def make_config(*, dim, degree, n0, lo, hi, bc, system=EULER, gamma=1.4, ch=0.0,
     cfg.rank, cfg.world_size, cfg.device = rank, world_size, device
     cfg.flux, cfg.flux_quad, cfg.load_balance = flux, flux_quad, load_balance
     cfg.pred_guess = pred_guess
+    # uniform grids: 0 = separate predictor and face-flux kernels (default), 1 = the
+    # fused tile walk; ADER_FUSE_PRED_FLUX sets the default (A/B tooling)
+    if fuse_pred_flux is None:
+        fuse_pred_flux = int(os.environ.get("ADER_FUSE_PRED_FLUX", "0"))
+    cfg.fuse_pred_flux = fuse_pred_flux
     for k in range(3):
         cfg.exact_vel[k] = (list(exact_vel) + [0.0] * 3)[k]
     if nccl_id is not None:

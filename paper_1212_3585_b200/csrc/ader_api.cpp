@@ -92,6 +92,7 @@ struct ader_ctx {
   ader_config cfg{};
   int d = 2, M = 2, N = 3, nv = 4, NS = 9, NST = 27, H = 3;
   long long qs = 27;                           // q block stride (nv NST rounded up to even, launch.h)
+  double* pfb = nullptr;                       // face-trace buffer of the fused a2+a3 walk (pred_flux.cu)
   ader_partition_info part{};
   int n[3] = {1, 1, 1}, P[3] = {1, 1, 1};
   long long ncell = 0;
@@ -198,6 +199,7 @@ ader_status validate(const ader_config* cfg, std::string& why) {
   if (cfg->load_balance < 0 || cfg->load_balance > 1) return bad("load_balance must be 0 or 1");
   if (cfg->pred_guess < 0 || cfg->pred_guess > 1) return bad("pred_guess must be 0 or 1");
   if (cfg->pred_guess == 1 && cfg->lmax > 0) return bad("pred_guess = 1 (reading R25) is for uniform grids");
+  if (cfg->fuse_pred_flux < 0 || cfg->fuse_pred_flux > 1) return bad("fuse_pred_flux must be 0 or 1");
   (void)b;
   return ADER_OK;
 }
@@ -561,6 +563,39 @@ void run_flux(ader_ctx* c) {
     launch_face_flux_tma(c->k, c->q, c->F, ext, H, c->n, transmissive_mask(c), reflective_mask(c), c->cnt);
 }
 
+// predictor region: the owned block + the face-neighbour layer, except beyond
+// transmissive sides and walls (R5, R22)
+Box predictor_region(const ader_ctx* c) {
+  Box r = grown(c, 1);
+  const int tm = transmissive_mask(c) | reflective_mask(c);
+  for (int a = 0; a < c->d; ++a) {
+    if (tm & (1 << (2 * a))) { r.lo[a] += 1; r.ext[a] -= 1; }
+    if (tm & (1 << (2 * a + 1))) r.ext[a] -= 1;
+  }
+  return r;
+}
+
+// a2 + a3 in one tile walk (pred_flux.cu): q_h stays on chip (fuse_pred_flux = 1;
+// pred_guess = 1 reads the previous q_h and keeps the separate kernels)
+bool fused_pred_flux(const ader_ctx* c) {
+  return c->pfb && c->cfg.fuse_pred_flux == 1 && c->cfg.pred_guess == 0 && !fused_weno_pred(c);
+}
+
+void run_pred_flux(ader_ctx* c, double dt, const double* dtdx_dev = nullptr) {
+  const Box r = predictor_region(c);
+  double dtdx[3] = {0, 0, 0};
+  for (int k = 0; k < c->d; ++k) dtdx[k] = dt / c->dx[k];
+  Box fb[3];
+  face_boxes(c, fb);
+  long long nf = 0;
+  for (int k = 0; k < c->d; ++k) nf += fb[k].count();
+  // flops: the faces' here, the Picard sweeps' from the device counters (ader_kernel_stats)
+  Scope s(c, ADER_K_PRED_FLUX, face_flops(c) * nf);
+  launch_pred_flux(c->k, c->w, c->F, c->pfb, r, c->H, c->n, transmissive_mask(c), reflective_mask(c),
+                   c->cfg.pred_tol, c->cfg.pred_max_sweeps, c->cnt, dtdx, dtdx_dev);
+  c->guess_ready = false;
+}
+
 void run_update(ader_ctx* c, double dt, const double* dtdx_dev = nullptr) {
   const Box r = owned(c);
   double dtdx[3] = {0, 0, 0};
@@ -610,7 +645,7 @@ void free_ctx(ader_ctx* c) {
   if (!c) return;
   if (c->k.stream) cudaStreamSynchronize(c->k.stream);
   if (c->amr) amr_destroy(c->amr);
-  double* bufs[] = {c->u, c->wx, c->wxy, c->w, c->q, c->F, c->stage};
+  double* bufs[] = {c->u, c->wx, c->wxy, c->w, c->q, c->F, c->stage, c->pfb};
   for (double* b : bufs)
     if (b) cudaFree(b);
   if (c->st) cudaFree(c->st);
@@ -856,6 +891,11 @@ static ader_status create_impl(const ader_config* cfg, ader_ctx** out, bool loop
   c->qs = q_block_stride(c->d, c->M, c->cfg.system);
   CK(alloc(&c->q, nc * c->qs));
   CK(alloc(&c->F, nc * c->nv * c->d));
+  if (cfg->fuse_pred_flux == 1 && cfg->pred_guess == 0) {
+    const long long nb = pred_flux_buffer_doubles(c->d, c->M, cfg->system, predictor_region(c), c->H, c->n);
+    if (nb < 0) return fail(c, ADER_ERR_CUDA, "pred_flux: unsupported (d, M, system)");
+    CK(alloc(&c->pfb, (size_t)std::max(1LL, nb)));
+  }
   CK(alloc(&c->stage, (size_t)c->n[0] * c->n[1] * c->n[2] * std::max<size_t>(c->qs, (size_t)c->nv * c->d)));
   CK(cudaMemset(c->u, 0, nc * c->nv * sizeof(double)));
   CK(cudaMemset(c->F, 0, nc * c->nv * c->d * sizeof(double)));
@@ -1071,9 +1111,12 @@ namespace {
 // second half of a uniform macro step, after the ghost fill + WENO: predictor,
 // face fluxes, update (fused with the next CFL speed)
 void advance_dt(ader_ctx* c, double dt, const double* dtdx_dev = nullptr) {
-  if (fused_weno_pred(c)) run_weno_predictor(c, dt, dtdx_dev);
-  else run_predictor(c, dt, dtdx_dev, true);
-  run_flux(c);
+  if (fused_pred_flux(c)) run_pred_flux(c, dt, dtdx_dev);
+  else {
+    if (fused_weno_pred(c)) run_weno_predictor(c, dt, dtdx_dev);
+    else run_predictor(c, dt, dtdx_dev, true);
+    run_flux(c);
+  }
   cudaMemsetAsync(&c->cnt->speed_bits, 0, sizeof(unsigned long long), c->k.stream);
   run_update(c, dt, dtdx_dev);
   c->speed_valid = true;   // computed by the update of the new state
@@ -1098,9 +1141,12 @@ ader_status enqueue_step(ader_ctx* c, double t_end) {
       NK(g_nccl.AllReduce(&c->cnt->speed_bits, &c->cnt->speed_bits, 1, ncclUint64, ncclMax, c->comm, c->k.stream));
     launch_step_dt(c->k, c->cnt, c->st, c->cfg.cfl, t_end, c->dx);
   }
-  if (fused) run_weno_predictor(c, 0.0, c->st->dtdx);
-  else run_predictor(c, 0.0, c->st->dtdx, true);
-  run_flux(c);
+  if (fused_pred_flux(c)) run_pred_flux(c, 0.0, c->st->dtdx);
+  else {
+    if (fused) run_weno_predictor(c, 0.0, c->st->dtdx);
+    else run_predictor(c, 0.0, c->st->dtdx, true);
+    run_flux(c);
+  }
   CK(cudaMemsetAsync(&c->cnt->speed_bits, 0, sizeof(unsigned long long), c->k.stream));
   run_update(c, 0.0, c->st->dtdx);
   c->speed_valid = true;
@@ -1388,10 +1434,18 @@ ader_status ader_kernel_stats(ader_ctx* c, double ms[ADER_K_COUNT], int64_t laun
   // predictor flops from the device counters: every predicted cell's first
   // sweep at its real cost, the later sweeps as full sweeps (plus, for the fused
   // WENO + predictor kernel, the WENO flops its scopes carry)
+  // (fused a2 + a3 walk: its scopes carry the face flops, the sweeps are added here)
   if (flops) {
     const double cells = (double)(c->hcnt->cells - c->prof_cells0);
     const double sweeps = (double)(c->hcnt->sweeps - c->prof_sweeps0);
-    flops[ADER_K_PRED] += cells * c->kflops_first + (sweeps - cells) * c->kflops_sweep;
+    int np = 0, npf = 0;
+    for (auto& r : c->recs) {
+      if (!r.e1) continue;
+      np += r.kind == ADER_K_PRED;
+      npf += r.kind == ADER_K_PRED_FLUX;
+    }
+    flops[(np == 0 && npf > 0) ? ADER_K_PRED_FLUX : ADER_K_PRED] +=
+        cells * c->kflops_first + (sweeps - cells) * c->kflops_sweep;
   }
   if (std::getenv("ADER_GAP_TRACE") && c->recs.size() > 1) {
     // diagnostics: idle gaps of the stream between consecutive timed scopes
@@ -1446,7 +1500,13 @@ ader_status ader_debug_dump(ader_ctx* c, int32_t what, double dt, double* out, i
     CK(cudaStreamSynchronize(c->k.stream));
     return ADER_OK;
   }
-  if (fused_weno_pred(c)) run_weno_predictor(c, dt);
+  // FLUX stage of the fused a2 + a3 walk: the fluxes come from the walk (q_h is
+  // never stored there); the PRED stage always runs the separate predictor
+  const bool walk = what == 2 && fused_pred_flux(c);
+  if (walk) {
+    CK(cudaMemsetAsync(c->F, 0, (size_t)c->ncell * c->nv * c->d * sizeof(double), c->k.stream));
+    run_pred_flux(c, dt);
+  } else if (fused_weno_pred(c)) run_weno_predictor(c, dt);
   else run_predictor(c, dt);
   c->guess_ready = false;   // q no longer holds the last step's predictor
   if (what == 1) {
@@ -1460,8 +1520,10 @@ ader_status ader_debug_dump(ader_ctx* c, int32_t what, double dt, double* out, i
     return check_errors(c);
   }
   if (what == 2) {
-    CK(cudaMemsetAsync(c->F, 0, (size_t)c->ncell * c->nv * c->d * sizeof(double), c->k.stream));
-    run_flux(c);
+    if (!walk) {
+      CK(cudaMemsetAsync(c->F, 0, (size_t)c->ncell * c->nv * c->d * sizeof(double), c->k.stream));
+      run_flux(c);
+    }
     const int zH = c->d == 3 ? c->H : 0;
     const Box e = make_box(c->H, c->H + c->n[0] + 1, c->H, c->H + c->n[1] + 1, zH, zH + c->n[2] + (c->d == 3 ? 1 : 0));
     if (capacity < e.count() * c->nv * c->d) return fail(c, ADER_ERR_ARG, "capacity too small");

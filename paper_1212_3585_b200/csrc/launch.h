@@ -103,6 +103,16 @@ long long q_block_stride(int D, int M, int SYS);
 void launch_weno_predictor(const KCtx& k, const double* u, double* q, const Box& region, long long qs,
                            const double dtdx[3], double tol, int max_sweeps, DevCounters* cnt,
                            const double* dtdx_dev = nullptr);
+// a2 + a3 fused (pred_flux.cu): the predictor on the cells of PR and the
+// lower-face fluxes of the face box (owned + 1, as launch_face_flux_cells) in
+// one tile walk with q kept in shared memory; faces between tiles go through
+// the face-trace buffer bnd (pred_flux_buffer_doubles doubles).  Bitwise the
+// same F as launch_predictor + launch_face_flux_cells.
+void launch_pred_flux(const KCtx& k, const double* w, double* F, double* bnd, const Box& PR, int H, const int n[3],
+                      int bmask, int rmask, double tol, int max_sweeps, DevCounters* cnt, const double dtdx[3],
+                      const double* dtdx_dev = nullptr);
+// size of that buffer (-1: unsupported (D, M, SYS))
+long long pred_flux_buffer_doubles(int D, int M, int SYS, const Box& PR, int H, const int n[3]);
 // FV update of `interior` in place + max CFL speed of the new state.
 void launch_update(const KCtx& k, double* u, const double* F, const Box& interior, const double dtdx[3],
                    const double inv_dx[3], DevCounters* cnt, const double* dtdx_dev = nullptr);
