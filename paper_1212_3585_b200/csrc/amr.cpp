@@ -70,6 +70,8 @@ struct AmrState {
   AmrRanks ranks;
   AmrComm comm;
   int band = 0;                                       // compute-set margin in level-0 cells
+  bool band_sets = false;                             // ADER_AMR_BAND=1: the uniform band instead of R28 sets
+  std::vector<int> lpres[kAmrMaxLevels];              // active cells whose averages this rank holds (multi-rank)
   std::vector<char> own, comp;                        // per id
   long long nlev[kAmrMaxLevels]{};                    // alive cells per level (whole tree)
   std::vector<int> lown[kAmrMaxLevels];               // owned active cells (multi-rank)
@@ -226,6 +228,156 @@ int voronoi(const AmrState* A, int id, int* out) {
         out[cnt++] = hlookup(A, C.level, ix, true);
       }
   return cnt;
+}
+
+// ---- multi-rank compute sets from the dependencies of the owned updates ------
+// (reading R28; replaces the uniform 2(M+1) level-0 band).  Bit p of the masks
+// = rank p.  With an exchange of the owners' active averages after every level
+// update, a rank must itself compute (WENO + predictor + flux/update):
+//   P  its owned active cells; the active face neighbours of owned cells and the
+//      active mothers of virtual-child face neighbours (their q_h enter the
+//      owned faces); the active fine cells across the faces of the virtual
+//      children of owned cells (they deposit the flux memory the owned update
+//      consumes, eqn.memory.sum); the active mothers of virtual children inside
+//      the WENO box of any P cell (projection), recursively;
+// and must hold current averages of
+//   R  the active cells in the (2M+1)^d WENO boxes of P cells and below the
+//      virtual mothers in them (received from their owners after each update);
+//   V  the virtual cells in those boxes (projected / averaged locally, R16).
+// Every rank evaluates the masks of all ranks on its copy of the tree (the
+// result is the same everywhere), so both sides of an exchange agree.
+// Cells whose neighbourhood lies inside their owner's block only carry their
+// owner's bit; work is done near block boundaries (dist0) and for cells that
+// received foreign bits.
+struct RankSets {
+  std::vector<unsigned char> P, R, V;
+  std::vector<signed char> owner;     // per id, -1 for dead ids
+};
+
+void rank_sets(const AmrState* A, RankSets& S) {
+  const int nu = (int)A->cells.size(), d = A->d, M = A->M, W = A->ranks.world;
+  S.P.assign(nu, 0); S.R.assign(nu, 0); S.V.assign(nu, 0); S.owner.assign(nu, -1);
+  // owner of every level-0 cell, and its Chebyshev distance (capped) to the
+  // nearest level-0 cell of another owner (periodic wrap)
+  const long long n0x = A->n[0][0], n0y = A->n[0][1], n0z = A->n[0][2], n0 = n0x * n0y * n0z;
+  std::vector<signed char> own0(n0);
+  for (long long z = 0; z < n0z; ++z)
+    for (long long y = 0; y < n0y; ++y)
+      for (long long x = 0; x < n0x; ++x) {
+        const long long a[3] = {x, y, z};
+        own0[(z * n0y + y) * n0x + x] = (signed char)owner_of(A, a);
+      }
+  auto wrap0 = [&](long long c, int k, bool& ok) -> long long {
+    const long long nn = A->n[0][k];
+    if (c >= 0 && c < nn) return c;
+    if (A->cfg.bc[2 * k + (c < 0 ? 0 : 1)] != ADER_BC_PERIODIC) { ok = false; return 0; }
+    return ((c % nn) + nn) % nn;
+  };
+  // does the box of level-0 ancestors [alo, ahi] (per axis, wrapped) hold a cell not owned by o?
+  auto foreign_in = [&](const long long* alo, const long long* ahi, int o) {
+    for (long long z = alo[2]; z <= ahi[2]; ++z)
+      for (long long y = alo[1]; y <= ahi[1]; ++y)
+        for (long long x = alo[0]; x <= ahi[0]; ++x) {
+          bool ok = true;
+          const long long xx = wrap0(x, 0, ok), yy = d > 1 ? wrap0(y, 1, ok) : 0, zz = d > 2 ? wrap0(z, 2, ok) : 0;
+          if (ok && own0[(zz * n0y + yy) * n0x + xx] != o) return true;
+        }
+    return false;
+  };
+  // cells whose level-l box of radius rad may reach a foreign level-0 cell
+  auto near_foreign = [&](const HCell& C, int rad, int o) {
+    long long f = 1;
+    for (int l = 0; l < C.level; ++l) f *= A->r;
+    long long alo[3] = {0, 0, 0}, ahi[3] = {0, 0, 0};
+    for (int k = 0; k < d; ++k) {
+      const long long lo = C.idx[k] - rad, hi = C.idx[k] + rad;
+      alo[k] = lo >= 0 ? lo / f : -((-lo + f - 1) / f);
+      ahi[k] = hi >= 0 ? hi / f : -((-hi + f - 1) / f);
+    }
+    return foreign_in(alo, ahi, o);
+  };
+  for (int i = 0; i < nu; ++i) {
+    const HCell& C = A->cells[i];
+    if (!C.alive) continue;
+    long long a0[3];
+    ancestor0(A, C, a0);
+    S.owner[i] = own0[(a0[2] * n0y + a0[1]) * n0x + a0[0]];
+    const unsigned char ob = (unsigned char)(1u << S.owner[i]);
+    if (C.status == 0) S.P[i] = ob;
+    else S.V[i] = ob;
+  }
+  (void)W;
+  std::vector<int> work;
+  auto addP = [&](int c, unsigned char m) {
+    if ((S.P[c] | m) != S.P[c]) { S.P[c] |= m; work.push_back(c); }
+  };
+  // face neighbours of owned cells near a foreign block
+  for (int i = 0; i < nu; ++i) {
+    const HCell& C = A->cells[i];
+    if (!C.alive || C.status != 0 || !near_foreign(C, 1, S.owner[i])) continue;
+    const unsigned char ob = (unsigned char)(1u << S.owner[i]);
+    for (int dir = 0; dir < d; ++dir)
+      for (int side = 0; side < 2; ++side) {
+        long long ix[3] = {C.idx[0], C.idx[1], C.idx[2]};
+        ix[dir] += side ? 1 : -1;
+        const int nb = hlookup(A, C.level, ix, true);
+        if (nb < 0 || S.owner[nb] == S.owner[i]) continue;
+        const HCell& Nb = A->cells[nb];
+        if (Nb.status == 0) addP(nb, ob);
+        else if (Nb.status == 1) addP(Nb.mother, ob);
+        else if (C.child >= 0) {
+          // the fine cells across this face from our virtual children deposit our flux memory
+          for (int q = 0; q < A->rd; ++q) {
+            const HCell& K = A->cells[C.child + q];
+            const long long off = K.idx[dir] - C.idx[dir] * A->r;
+            if (off != (side ? A->r - 1 : 0)) continue;
+            long long jx[3] = {K.idx[0], K.idx[1], K.idx[2]};
+            jx[dir] += side ? 1 : -1;
+            const int f = hlookup(A, K.level, jx, true);
+            if (f >= 0 && A->cells[f].status == 0) addP(f, ob);
+          }
+        }
+      }
+  }
+  // WENO boxes: owner-only P cells whose box may reach a foreign block, and
+  // every cell that received foreign bits
+  for (int i = 0; i < nu; ++i) {
+    const HCell& C = A->cells[i];
+    if (C.alive && C.status == 0 && S.P[i] == (unsigned char)(1u << S.owner[i]) && near_foreign(C, M, S.owner[i]))
+      work.push_back(i);
+  }
+  std::vector<int> stack;
+  while (!work.empty()) {
+    const int p = work.back();
+    work.pop_back();
+    const unsigned char m = S.P[p];
+    const HCell& C = A->cells[p];
+    const int zr = d == 3 ? M : 0, yr = d >= 2 ? M : 0;
+    for (int dz = -zr; dz <= zr; ++dz)
+      for (int dy = -yr; dy <= yr; ++dy)
+        for (int dx = -M; dx <= M; ++dx) {
+          const long long ix[3] = {C.idx[0] + dx, C.idx[1] + dy, C.idx[2] + dz};
+          const int b = hlookup(A, C.level, ix, false);
+          if (b < 0) continue;
+          const HCell& B = A->cells[b];
+          if (B.status == 0) { S.R[b] |= m; continue; }
+          S.V[b] |= m;
+          if (B.status == 1) { addP(B.mother, m); continue; }
+          // virtual mother: everything below it is averaged into it
+          stack.push_back(b);
+          while (!stack.empty()) {
+            const int v = stack.back();
+            stack.pop_back();
+            const int ch = A->cells[v].child;
+            if (ch < 0) continue;
+            for (int q = 0; q < A->rd; ++q) {
+              const HCell& K = A->cells[ch + q];
+              if (K.status == 0) S.R[ch + q] |= m;
+              else if (K.status == -1) { S.V[ch + q] |= m; stack.push_back(ch + q); }
+            }
+          }
+        }
+  }
 }
 
 // writable cell / map entry; records the previous value while journaling
@@ -463,7 +615,7 @@ ader_status upload_topology(AmrState* A, std::string& err) {
   }
   A->tm_u[3] += now_s() - w0;
   for (int l = 0; l <= A->lmax; ++l) {
-    A->lact[l].clear(); A->lvch[l].clear(); A->lvmo[l].clear(); A->lown[l].clear();
+    A->lact[l].clear(); A->lvch[l].clear(); A->lvmo[l].clear(); A->lown[l].clear(); A->lpres[l].clear();
     A->xp[l] = AmrState::XPlan();
   }
   const int W = A->ranks.world, me = A->ranks.rank;
@@ -502,26 +654,48 @@ ader_status upload_topology(AmrState* A, std::string& err) {
       }
     }
   }
+  RankSets RS;
+  const bool dep = W > 1 && !A->band_sets;
+  if (dep) rank_sets(A, RS);
+  const unsigned char mb = (unsigned char)(1u << me);
   for (int i = 0; i < (W > 1 ? nu : 0); ++i) {
     const HCell& C = A->cells[i];
     if (!C.alive) continue;
     A->nlev[C.level]++;
-    if (W > 1) {
+    bool compute;   // this rank runs WENO + predictor + flux/update (active) or the ghost fill (virtual)
+    if (dep) {
+      owner[i] = RS.owner[i];
+      A->own[i] = owner[i] == me;
+      if (C.status == 0) {
+        compute = RS.P[i] & mb;
+        A->comp[i] = A->own[i] || ((RS.P[i] | RS.R[i]) & mb);
+        if (A->own[i])
+          for (int p = 0; p < W; ++p)
+            if (p != me && ((RS.P[i] | RS.R[i]) >> p & 1)) send_to[(size_t)C.level * W + p].push_back(i);
+      } else {
+        // virtual children of cells this rank computes also get their flux memory
+        // cleared / projected (R16); virtual cells in the boxes (V)
+        compute = (RS.V[i] & mb) || (C.status == 1 && (RS.P[C.mother] & mb));
+        A->comp[i] = compute;
+      }
+    } else {
       long long a0[3];
       ancestor0(A, C, a0);
       owner[i] = owner_of(A, a0);
       A->own[i] = owner[i] == me;
       A->comp[i] = A->own[i] || in_comp(A, me, a0);
+      compute = A->comp[i];
       if (A->own[i] && C.status == 0)
         for (int p = 0; p < W; ++p)
           if (p != me && in_comp(A, p, a0)) send_to[(size_t)C.level * W + p].push_back(i);
-    } else {
-      A->own[i] = A->comp[i] = 1;
     }
-    if (!A->comp[i]) continue;
-    if (C.status == 0) A->lact[C.level].push_back(i);
-    else if (C.status == 1) A->lvch[C.level].push_back(i);
-    else A->lvmo[C.level].push_back(i);
+    if (C.status == 0) {
+      if (compute) A->lact[C.level].push_back(i);
+      if (A->comp[i]) A->lpres[C.level].push_back(i);
+    } else if (compute) {
+      if (C.status == 1) A->lvch[C.level].push_back(i);
+      else A->lvmo[C.level].push_back(i);
+    }
     if (A->own[i] && C.status == 0) A->lown[C.level].push_back(i);
   }
   size_t xneed = 0;
@@ -535,7 +709,7 @@ ader_status upload_topology(AmrState* A, std::string& err) {
         if (p != me) X.sids.insert(X.sids.end(), send_to[(size_t)l * W + p].begin(), send_to[(size_t)l * W + p].end());
         X.roff[p] = (long long)X.rids.size();
         if (p != me)
-          for (int i : A->lact[l])
+          for (int i : A->lpres[l])
             if (owner[i] == p) X.rids.push_back(i);
       }
       X.soff[W] = (long long)X.sids.size();
@@ -1097,6 +1271,8 @@ ader_status rebalance(const Group& G, std::string& err) {
       for (int k = 0; k < 3; ++k) { A->ranks.lo[p][k] = nr.lo[p][k]; A->ranks.hi[p][k] = nr.hi[p][k]; }
     s = upload_topology(A, err);
     if (s != ADER_OK) break;
+    // virtual children that entered this rank's lists: no flux memory from before
+    for (int l = 1; l <= A->lmax; ++l) amr_launch_zero_mem(*A->k, A->V, L_vch(A, l), (int)A->lvch[l].size());
     const std::vector<int> ids = ids_of(A, A->comp);
     Uploader up{A, {}};
     const size_t oi = up.add(ids.data(), sizeof(int) * ids.size());
@@ -1208,6 +1384,10 @@ AmrState* amr_create(const ader_config* cfg, KCtx* k, DevCounters* cnt, DevCount
   // virtual children, finer cells depositing flux memory) stays within
   // (M+1) sum_l r^-l < 2 (M+1) level-0 cells of the owned block for r >= M
   A->band = 2 * (cfg->degree + 1);
+  {
+    const char* e = std::getenv("ADER_AMR_BAND");   // A/B: the round-1 uniform band
+    A->band_sets = e && e[0] == '1';
+  }
   A->d = cfg->dim; A->M = cfg->degree; A->N = A->M + 1;
   A->nv = cfg->system == ADER_MHD_GLM ? 9 : cfg->dim + 2;
   A->NS = 1;

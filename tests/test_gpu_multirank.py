@@ -183,3 +183,30 @@ def test_dynamic_load_balance_keeps_bitwise_parity_and_evens_the_load(name):
         grp.close()
     print(f"{name}: owned local-step imbalance static {imb[0]:.3f} -> dynamic {imb[1]:.3f}")
     assert imb[1] < imb[0] and imb[1] < 1.3, imb
+
+
+# Reading R28: the multi-rank compute sets follow the dependencies of the owned
+# updates instead of a 2(M+1) level-0 band on every level.  The partition must
+# still reproduce one rank bit for bit, and the computed cells (local steps of
+# all ranks' predictors) stay within 1.2x the owned ones at 8 ranks.
+@pytest.mark.parametrize("name", ["explosion2d_l2_x8_long"])
+def test_amr_dependency_sets_cut_redundant_work(name, monkeypatch):
+    kw, ic, nr, steps = AMR_CASES[name]
+    nv = kw["dim"] + 2
+    one = ader.Solver(ader.make_config(device=0, adapt_every=1, **kw))
+    one.set_initial(ic)
+    r1 = one.step(1e300, steps)
+    a = _key_sorted(one.get_cells(), nv)
+    one.close()
+    ratio = {}
+    for band in ("1", "0"):
+        monkeypatch.setenv("ADER_AMR_BAND", band)
+        grp = ader.LoopbackGroup(ader.make_config(device=0, adapt_every=1, **kw), nr)
+        grp.set_initial(ic)
+        reps = grp.step(1e300, steps)
+        assert sum(r.cell_updates for r in reps) == r1.cell_updates
+        assert _key_sorted(grp.get_cells(), nv) == a
+        ratio[band] = sum(r.pred_cells for r in reps) / sum(r.cell_updates for r in reps)
+        grp.close()
+    print(f"{name}: computed / owned local steps band {ratio['1']:.3f} -> dependency sets {ratio['0']:.3f}")
+    assert ratio["0"] < ratio["1"] and ratio["0"] <= 1.2, ratio
