@@ -213,6 +213,29 @@ ader_status ader_halo_plan(const ader_config* cfg, int32_t rank, int32_t axis, i
  * plane, or on bad arguments. */
 ader_status ader_rcb_partition(int32_t dim, const int32_t n0[3], const int64_t* weights, int32_t world,
                                int32_t* boxes);
+/* Collectives of a rank group supplied by the caller on the host (e.g. an MPI
+ * or gloo process group) instead of NCCL: the library stages device buffers
+ * through pinned host memory and synchronises its stream around every call.
+ * Each callback returns 0 on success; any other value fails the step with
+ * ADER_ERR_NCCL.
+ *   p2p: n entries; to peers[i] send scount[i] doubles from send[i], from
+ *        peers[i] receive rcount[i] doubles into recv[i] (counts may be 0).
+ *        Messages between one pair of ranks must be matched in entry order
+ *        (the library orders its entries so that both sides agree).
+ *   allreduce_sum / allreduce_max_u64: in place over all ranks.
+ * The pointers passed to the callbacks are valid only during the call. */
+typedef struct {
+  void* user;
+  int32_t (*p2p)(void* user, int32_t n, const int32_t* peers, const double* const* send, const int64_t* scount,
+                 double* const* recv, const int64_t* rcount);
+  int32_t (*allreduce_sum)(void* user, double* buf, int64_t n);
+  int32_t (*allreduce_max_u64)(void* user, uint64_t* buf, int64_t n);
+} ader_host_comm;
+/* ader_create for rank cfg->rank of a group of cfg->world_size >= 2 processes
+ * whose collectives go through *comm (copied; comm->user must outlive the
+ * context).  cfg->nccl_id is ignored.  Errors as ader_create; ADER_ERR_ARG if
+ * a callback is missing. */
+ader_status ader_create_host_comm(const ader_config* cfg, const ader_host_comm* comm, ader_ctx** out);
 /* 128-byte ncclUniqueId for rank 0 to broadcast (loads libnccl.so.2 lazily). */
 ader_status ader_nccl_unique_id(uint8_t out[128]);
 

@@ -69,6 +69,16 @@ class AderHaloDesc(C.Structure):
                 ("recv_lo", C.c_int32 * 3), ("recv_hi", C.c_int32 * 3)]
 
 
+P2P_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.POINTER(C.c_double)),
+                     C.POINTER(C.c_int64), C.POINTER(C.POINTER(C.c_double)), C.POINTER(C.c_int64))
+SUM_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.POINTER(C.c_double), C.c_int64)
+MAXU_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.POINTER(C.c_uint64), C.c_int64)
+
+
+class AderHostComm(C.Structure):
+    _fields_ = [("user", C.c_void_p), ("p2p", P2P_FN), ("allreduce_sum", SUM_FN), ("allreduce_max_u64", MAXU_FN)]
+
+
 class AderError(RuntimeError):
     def __init__(self, status, msg):
         super().__init__(f"{STATUS.get(status, status)}: {msg}")
@@ -84,6 +94,7 @@ def lib():
         L = C.CDLL(LIB_PATH)
         vp, dp = C.c_void_p, C.POINTER(C.c_double)
         L.ader_create.argtypes = [C.POINTER(AderConfig), C.POINTER(vp)]
+        L.ader_create_host_comm.argtypes = [C.POINTER(AderConfig), C.POINTER(AderHostComm), C.POINTER(vp)]
         L.ader_destroy.argtypes = [vp]
         L.ader_destroy.restype = None
         L.ader_last_error.argtypes = [vp]
@@ -120,7 +131,8 @@ EXPORTED = ("ader_create", "ader_destroy", "ader_last_error", "ader_set_stream",
             "ader_set_cells", "ader_get_state", "ader_get_cells", "ader_time", "ader_step", "ader_refine",
             "ader_partition", "ader_halo_plan", "ader_nccl_unique_id", "ader_set_profiling", "ader_kernel_stats",
             "ader_launch_count", "ader_debug_dump", "ader_sizeof", "ader_debug_group_create",
-            "ader_debug_group_set_initial", "ader_debug_group_step", "ader_rcb_partition")
+            "ader_debug_group_set_initial", "ader_debug_group_step", "ader_rcb_partition",
+            "ader_create_host_comm")
 
 
 def _dp(a):
@@ -203,17 +215,64 @@ def ader_nccl_unique_id() -> bytes:
     return bytes(buf)
 
 
-class Solver:
-    """One rank's context: ader_create ... ader_destroy."""
+def host_comm(obj) -> AderHostComm:
+    """ader_host_comm over a Python object with methods
+        p2p(peers, sends, recv_counts) -> list of received numpy arrays
+        allreduce_sum(np.ndarray) -> None (in place)
+        allreduce_max_u64(np.ndarray) -> None (in place)
+    (e.g. a torch.distributed gloo group).  Marshalling only."""
+    def p2p(user, n, peers, send, scount, recv, rcount):
+        try:
+            pe = [peers[i] for i in range(n)]
+            sends = [np.ctypeslib.as_array(send[i], shape=(scount[i],)).copy() if scount[i] else
+                     np.zeros(0) for i in range(n)]
+            got = obj.p2p(pe, sends, [rcount[i] for i in range(n)])
+            for i in range(n):
+                if rcount[i]:
+                    np.ctypeslib.as_array(recv[i], shape=(rcount[i],))[:] = got[i]
+            return 0
+        except Exception as e:   # noqa: BLE001 — reported to the library as a failed collective
+            print("ader host p2p failed:", e)
+            return 1
 
-    def __init__(self, cfg: AderConfig):
+    def asum(user, buf, n):
+        try:
+            obj.allreduce_sum(np.ctypeslib.as_array(buf, shape=(n,)))
+            return 0
+        except Exception as e:   # noqa: BLE001
+            print("ader host allreduce_sum failed:", e)
+            return 1
+
+    def amax(user, buf, n):
+        try:
+            obj.allreduce_max_u64(np.ctypeslib.as_array(buf, shape=(n,)))
+            return 0
+        except Exception as e:   # noqa: BLE001
+            print("ader host allreduce_max failed:", e)
+            return 1
+
+    hc = AderHostComm()
+    hc.p2p, hc.allreduce_sum, hc.allreduce_max_u64 = P2P_FN(p2p), SUM_FN(asum), MAXU_FN(amax)
+    hc._keep = (hc.p2p, hc.allreduce_sum, hc.allreduce_max_u64, obj)
+    return hc
+
+
+class Solver:
+    """One rank's context: ader_create ... ader_destroy (comm: optional host
+    collectives, ader_create_host_comm)."""
+
+    def __init__(self, cfg: AderConfig, comm=None):
         self.cfg = cfg
         self.nv = 9 if cfg.system == MHD_GLM else cfg.dim + 2
         self.N = cfg.degree + 1
         self.part = ader_partition(cfg, cfg.rank)
         self.block = [self.part.hi[k] - self.part.lo[k] for k in range(cfg.dim)]
         self.ptr = C.c_void_p()
-        st = lib().ader_create(C.byref(cfg), C.byref(self.ptr))
+        self._comm = host_comm(comm) if comm is not None else None
+        if self._comm is not None:
+            st = lib().ader_create_host_comm(C.byref(cfg), C.byref(self._comm), C.byref(self.ptr))
+        else:
+            st = lib().ader_create(C.byref(cfg), C.byref(self.ptr))
         if st:
             raise AderError(st, lib().ader_last_error(None).decode())
 

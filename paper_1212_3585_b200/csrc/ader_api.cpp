@@ -81,6 +81,75 @@ ader_status amr_nccl_max_u64(void* ctx, unsigned long long* buf, cudaStream_t st
   return g_nccl.AllReduce(buf, buf, 1, ncclUint64, ncclMax, (ncclComm_t)ctx, st) == ncclSuccess ? ADER_OK
                                                                                               : ADER_ERR_NCCL;
 }
+
+// Collectives through the caller's host callbacks (ader_create_host_comm): the
+// device buffers are staged through one pinned buffer; the stream is
+// synchronised around every call, so the caller's collective sees finished data.
+struct HostComm {
+  ader_host_comm u{};
+  char* pin = nullptr;
+  size_t cap = 0;
+  bool grow(size_t bytes) {
+    if (bytes <= cap) return true;
+    if (pin) cudaFreeHost(pin);
+    pin = nullptr;
+    cap = 0;
+    if (cudaMallocHost(&pin, bytes * 3 / 2 + 4096) != cudaSuccess) return false;
+    cap = bytes * 3 / 2 + 4096;
+    return true;
+  }
+  ~HostComm() { if (pin) cudaFreeHost(pin); }
+};
+ader_status host_p2p(void* ctx, int n, const int* peers, double* const* sendp, const size_t* scount,
+                     double* const* recvp, const size_t* rcount, cudaStream_t st) {
+  HostComm* h = (HostComm*)ctx;
+  size_t tot = 0;
+  for (int i = 0; i < n; ++i) tot += scount[i] + rcount[i];
+  if (!h->grow(tot * sizeof(double))) return ADER_ERR_CUDA;
+  std::vector<const double*> hs(n);
+  std::vector<double*> hr(n);
+  std::vector<int64_t> sc(n), rc(n);
+  std::vector<int32_t> pe(n);
+  double* b = (double*)h->pin;
+  for (int i = 0; i < n; ++i) {
+    hs[i] = b;
+    if (scount[i] && cudaMemcpyAsync(b, sendp[i], scount[i] * sizeof(double), cudaMemcpyDeviceToHost, st) != cudaSuccess)
+      return ADER_ERR_CUDA;
+    b += scount[i];
+    hr[i] = b;
+    b += rcount[i];
+    sc[i] = (int64_t)scount[i];
+    rc[i] = (int64_t)rcount[i];
+    pe[i] = peers[i];
+  }
+  if (cudaStreamSynchronize(st) != cudaSuccess) return ADER_ERR_CUDA;
+  if (h->u.p2p(h->u.user, n, pe.data(), hs.data(), sc.data(), hr.data(), rc.data()) != 0) return ADER_ERR_NCCL;
+  for (int i = 0; i < n; ++i)
+    if (rcount[i] && cudaMemcpyAsync(recvp[i], hr[i], rcount[i] * sizeof(double), cudaMemcpyHostToDevice, st) != cudaSuccess)
+      return ADER_ERR_CUDA;
+  return cudaStreamSynchronize(st) == cudaSuccess ? ADER_OK : ADER_ERR_CUDA;
+}
+ader_status host_sum(void* ctx, double* buf, size_t n, cudaStream_t st) {
+  HostComm* h = (HostComm*)ctx;
+  if (!h->grow(n * sizeof(double))) return ADER_ERR_CUDA;
+  if (cudaMemcpyAsync(h->pin, buf, n * sizeof(double), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return ADER_ERR_CUDA;
+  if (h->u.allreduce_sum(h->u.user, (double*)h->pin, (int64_t)n) != 0) return ADER_ERR_NCCL;
+  if (cudaMemcpyAsync(buf, h->pin, n * sizeof(double), cudaMemcpyHostToDevice, st) != cudaSuccess) return ADER_ERR_CUDA;
+  return cudaStreamSynchronize(st) == cudaSuccess ? ADER_OK : ADER_ERR_CUDA;
+}
+ader_status host_max_u64(void* ctx, unsigned long long* buf, cudaStream_t st) {
+  HostComm* h = (HostComm*)ctx;
+  if (!h->grow(sizeof(unsigned long long))) return ADER_ERR_CUDA;
+  if (cudaMemcpyAsync(h->pin, buf, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return ADER_ERR_CUDA;
+  if (h->u.allreduce_max_u64(h->u.user, (uint64_t*)h->pin, 1) != 0) return ADER_ERR_NCCL;
+  if (cudaMemcpyAsync(buf, h->pin, sizeof(unsigned long long), cudaMemcpyHostToDevice, st) != cudaSuccess)
+    return ADER_ERR_CUDA;
+  return cudaStreamSynchronize(st) == cudaSuccess ? ADER_OK : ADER_ERR_CUDA;
+}
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -118,6 +187,8 @@ struct ader_ctx {
   bool has_exact = false;                      // a side of this rank is ADER_BC_EXACT
   double prev_dt_host = 0.0;                   // its dt (host-driven loopback steps)
   ncclComm_t comm = nullptr;
+  HostComm* hostcomm = nullptr;                // collectives through host callbacks (ader_create_host_comm)
+  AmrComm coll{};                              // the rank group's collectives (NCCL or host callbacks)
   bool loopback = false;                       // test-only rank group in one process (ader_debug_group_*)
   std::string err;
   // instrumentation
@@ -402,18 +473,24 @@ ader_status halo_exchange_nccl(ader_ctx* c, int a) {
   const bool remote_lo = dl.kind == 1, remote_hi = dh.kind == 1;
   if (!remote_lo && !remote_hi) return ADER_OK;
   const size_t cnt = (size_t)desc_box(dl.recv_lo, dl.recv_hi).count() * c->nv;
-  if (!c->comm) return fail(c, ADER_ERR_NCCL, "halo exchange without a communicator");
-  NK(g_nccl.GroupStart());
-  // order per peer: (send low, recv high, send high, recv low) on every rank;
-  // the group is closed even when a call fails
-  ncclResult_t r = ncclSuccess;
-  if (remote_lo && r == ncclSuccess) r = g_nccl.Send(c->sendb[2 * a], cnt, ncclDouble, dl.peer, c->comm, c->k.stream);
-  if (remote_hi && r == ncclSuccess) r = g_nccl.Recv(c->recvb[2 * a + 1], cnt, ncclDouble, dh.peer, c->comm, c->k.stream);
-  if (remote_hi && r == ncclSuccess) r = g_nccl.Send(c->sendb[2 * a + 1], cnt, ncclDouble, dh.peer, c->comm, c->k.stream);
-  if (remote_lo && r == ncclSuccess) r = g_nccl.Recv(c->recvb[2 * a], cnt, ncclDouble, dl.peer, c->comm, c->k.stream);
-  const ncclResult_t r2 = g_nccl.GroupEnd();
-  NK(r);
-  NK(r2);
+  if (!c->coll.p2p) return fail(c, ADER_ERR_NCCL, "halo exchange without a communicator");
+  // order on every rank: send low, recv high, send high, recv low (messages
+  // between one pair of ranks then match in order, also when both neighbours
+  // are the same rank)
+  int peers[4];
+  double* sp[4];
+  double* rp[4];
+  size_t sc[4], rc[4];
+  int n = 0;
+  auto add = [&](int peer, double* s_, size_t ns, double* r_, size_t nr) {
+    peers[n] = peer; sp[n] = s_; sc[n] = ns; rp[n] = r_; rc[n] = nr; ++n;
+  };
+  if (remote_lo) add(dl.peer, c->sendb[2 * a], cnt, nullptr, 0);
+  if (remote_hi) add(dh.peer, nullptr, 0, c->recvb[2 * a + 1], cnt);
+  if (remote_hi) add(dh.peer, c->sendb[2 * a + 1], cnt, nullptr, 0);
+  if (remote_lo) add(dl.peer, nullptr, 0, c->recvb[2 * a], cnt);
+  const ader_status st = c->coll.p2p(c->coll.ctx, n, peers, sp, sc, rp, rc, c->k.stream);
+  if (st != ADER_OK) return fail(c, st, "halo exchange (axis %d) failed", a);
   return ADER_OK;
 }
 
@@ -627,8 +704,8 @@ ader_status global_speed(ader_ctx* c, double* speed) {
     Scope s(c, ADER_K_OTHER, 0.0);
     launch_cfl_speed(c->k, c->u, owned(c), c->inv_dx, c->cnt);
   }
-  if (c->comm)
-    NK(g_nccl.AllReduce(&c->cnt->speed_bits, &c->cnt->speed_bits, 1, ncclUint64, ncclMax, c->comm, c->k.stream));
+  if (c->coll.max_u64 && c->coll.max_u64(c->coll.ctx, &c->cnt->speed_bits, c->k.stream) != ADER_OK)
+    return fail(c, ADER_ERR_NCCL, "allreduce(max) of the CFL speed failed");
   CK(cudaMemcpyAsync(c->hcnt, c->cnt, sizeof(DevCounters), cudaMemcpyDeviceToHost, c->k.stream));
   CK(cudaStreamSynchronize(c->k.stream));
   ader_status st = check_errors(c);
@@ -661,6 +738,7 @@ void free_ctx(ader_ctx* c) {
   for (auto& r : c->recs) { if (r.e0) cudaEventDestroy(r.e0); if (r.e1) cudaEventDestroy(r.e1); }
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   if (c->comm) g_nccl.CommDestroy(c->comm);
+  delete c->hostcomm;
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
   delete c;
 }
@@ -759,7 +837,29 @@ ader_status ader_nccl_unique_id(uint8_t out[128]) {
   return ADER_OK;
 }
 
-static ader_status create_impl(const ader_config* cfg, ader_ctx** out, bool loopback = false);
+static ader_status create_impl(const ader_config* cfg, ader_ctx** out, bool loopback = false,
+                               const ader_host_comm* hc = nullptr);
+
+ader_status ader_create_host_comm(const ader_config* cfg, const ader_host_comm* comm, ader_ctx** out) {
+  if (!cfg || !out || !comm || !comm->p2p || !comm->allreduce_sum || !comm->allreduce_max_u64) return ADER_ERR_ARG;
+  *out = nullptr;
+  std::string why;
+  ader_status st = validate(cfg, why);
+  if (st == ADER_OK && cfg->world_size < 2) { st = ADER_ERR_CONFIG; why = "ader_create_host_comm needs world_size >= 2"; }
+  if (st != ADER_OK) {
+    g_create_err = st == ADER_ERR_UNSUPPORTED ? "configuration not supported" : why;
+    return st;
+  }
+  ader_ctx* c = nullptr;
+  st = create_impl(cfg, &c, false, comm);
+  if (st != ADER_OK) {
+    g_create_err = c ? c->err : "allocation failed";
+    free_ctx(c);
+    return st;
+  }
+  *out = c;
+  return ADER_OK;
+}
 
 ader_status ader_create(const ader_config* cfg, ader_ctx** out) {
   if (!cfg || !out) return ADER_ERR_ARG;
@@ -781,7 +881,7 @@ ader_status ader_create(const ader_config* cfg, ader_ctx** out) {
   return ADER_OK;
 }
 
-static ader_status create_impl(const ader_config* cfg, ader_ctx** out, bool loopback) {
+static ader_status create_impl(const ader_config* cfg, ader_ctx** out, bool loopback, const ader_host_comm* hc) {
   ader_partition_info pi;
   partition(cfg, cfg->rank, &pi);
   const int H = cfg->degree + 1;
@@ -861,7 +961,14 @@ static ader_status create_impl(const ader_config* cfg, ader_ctx** out, bool loop
       for (int k = 0; k < 3; ++k) { ranks.lo[p][k] = pp.lo[k]; ranks.hi[p][k] = pp.hi[k]; }
     }
     AmrComm comm;
-    if (cfg->world_size > 1 && !loopback) {
+    if (cfg->world_size > 1 && !loopback && hc) {
+      c->hostcomm = new HostComm();
+      c->hostcomm->u = *hc;
+      comm.ctx = c->hostcomm;
+      comm.p2p = host_p2p;
+      comm.sum = host_sum;
+      comm.max_u64 = host_max_u64;
+    } else if (cfg->world_size > 1 && !loopback) {
       std::string err;
       if (!g_nccl.load(err)) return fail(c, ADER_ERR_NCCL, "%s", err.c_str());
       ncclUniqueId id;
@@ -926,7 +1033,14 @@ static ader_status create_impl(const ader_config* cfg, ader_ctx** out, bool loop
       CK(alloc(&c->recvb[i], (size_t)c->halo_cap));
     }
   }
-  if (cfg->world_size > 1 && !loopback) {
+  if (cfg->world_size > 1 && !loopback && hc) {
+    c->hostcomm = new HostComm();
+    c->hostcomm->u = *hc;
+    c->coll.ctx = c->hostcomm;
+    c->coll.p2p = host_p2p;
+    c->coll.sum = host_sum;
+    c->coll.max_u64 = host_max_u64;
+  } else if (cfg->world_size > 1 && !loopback) {
     std::string err;
     if (!g_nccl.load(err)) return fail(c, ADER_ERR_NCCL, "%s", err.c_str());
     ncclUniqueId id;
@@ -936,6 +1050,10 @@ static ader_status create_impl(const ader_config* cfg, ader_ctx** out, bool loop
       c->comm = nullptr;
       return fail(c, ADER_ERR_NCCL, "ncclCommInitRank: %s", g_nccl.GetErrorString(r));
     }
+    c->coll.ctx = c->comm;
+    c->coll.p2p = amr_nccl_p2p;
+    c->coll.sum = amr_nccl_sum;
+    c->coll.max_u64 = amr_nccl_max_u64;
   }
   c->kflops_sweep = pred_sweep_flops(c);
   c->kflops_first = pred_first_sweep_flops(c);
@@ -1137,8 +1255,8 @@ ader_status enqueue_step(ader_ctx* c, double t_end) {
       CK(cudaMemsetAsync(&c->cnt->speed_bits, 0, sizeof(unsigned long long), c->k.stream));
       launch_cfl_speed(c->k, c->u, owned(c), c->inv_dx, c->cnt);
     }
-    if (c->comm)
-      NK(g_nccl.AllReduce(&c->cnt->speed_bits, &c->cnt->speed_bits, 1, ncclUint64, ncclMax, c->comm, c->k.stream));
+    if (c->coll.max_u64 && c->coll.max_u64(c->coll.ctx, &c->cnt->speed_bits, c->k.stream) != ADER_OK)
+      return fail(c, ADER_ERR_NCCL, "allreduce(max) of the CFL speed failed");
     launch_step_dt(c->k, c->cnt, c->st, c->cfg.cfl, t_end, c->dx);
   }
   if (fused_pred_flux(c)) run_pred_flux(c, 0.0, c->st->dtdx);
@@ -1158,10 +1276,11 @@ ader_status enqueue_step(ader_ctx* c, double t_end) {
 // one rank stops every rank at the same chunk boundary instead of leaving the
 // others blocked in the next step's collectives.
 ader_status read_state(ader_ctx* c) {
-  if (c->comm) {
+  if (c->coll.max_u64) {
     CK(cudaMemsetAsync(&c->cnt->err_any, 0, sizeof(unsigned long long), c->k.stream));
     CK(cudaMemcpyAsync(&c->cnt->err_any, &c->cnt->err_code, sizeof(int), cudaMemcpyDeviceToDevice, c->k.stream));
-    NK(g_nccl.AllReduce(&c->cnt->err_any, &c->cnt->err_any, 1, ncclUint64, ncclMax, c->comm, c->k.stream));
+    if (c->coll.max_u64(c->coll.ctx, &c->cnt->err_any, c->k.stream) != ADER_OK)
+      return fail(c, ADER_ERR_NCCL, "allreduce(max) of the error code failed");
   }
   CK(cudaMemcpyAsync(c->hst, c->st, sizeof(StepState), cudaMemcpyDeviceToHost, c->k.stream));
   CK(cudaMemcpyAsync(c->hcnt, c->cnt, sizeof(DevCounters), cudaMemcpyDeviceToHost, c->k.stream));
