@@ -1,5 +1,5 @@
 """Per-kernel DRAM bytes and hardware-counted FP64 rate from an ncu --set full
-report -> profiles/ncu_traffic.json entry.  usage: ncu_to_json.py rep workload [flux]
+report -> profiles/ncu_traffic.json entry.  usage: ncu_to_json.py rep workload [flux] [source label]
 
 fp64_hw_frac = (2 dfma + dadd + dmul thread instructions per cycle) / (2 x
 peak dfma thread instructions per cycle), i.e. the FP64 pipe's flop rate as
@@ -16,7 +16,7 @@ NAMES = [("k_predictor", "stdg_predictor"), ("k_face_flux", "face_flux_rusanov")
          ("k_update", "fv_update")]
 
 
-def main(rep, workload, flux="rusanov"):
+def main(rep, workload, flux="rusanov", label=""):
     t = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(t.splitlines()))
     h, u = rows[0], rows[1]
@@ -39,7 +39,7 @@ def main(rep, workload, flux="rusanov"):
                 peak = 2 * val(r, "sm__sass_thread_inst_executed_op_dfma_pred_on.sum.peak_sustained")
                 out[f"{key}_fp64_hw_frac"] = f / peak
                 break
-    out["source"] = f"ncu --set full capture {os.path.basename(rep)} (profiles/round1_final_ncu_summary.txt)"
+    out["source"] = f"ncu --set full capture {os.path.basename(rep)}" + (f": {label}" if label else "")
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     d = json.load(open(path)) if os.path.exists(path) else {}
     d[workload] = out
