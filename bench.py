@@ -143,10 +143,13 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # CPU oracle sample (cpu_baseline and --impl reference)
 # ---------------------------------------------------------------------------
-def oracle_sample(wl, edge, reps=1, flux=0):
-    """Time the oracle (single thread, as it stands) on `reps` sub-boxes of the
-    workload: one step of an edge^d box straddling the initial discontinuity
-    (explosion) / the vortex core.  Returns (cell-updates/s, description)."""
+def oracle_sample(wl, edge, reps=1, flux=0, nbox=1, seed=3585):
+    """Time the oracle (single thread, as it stands) on a bounded sample of the
+    workload.  Uniform grids: one step of `nbox` edge^d boxes at seeded random
+    positions over the whole domain (so constant regions and fronts enter in
+    the workload's own proportion; each box plus its face-neighbour layer is
+    reconstructed and predicted).  AMR: one macro step of the AMR oracle on an
+    edge^d level-0 grid.  Returns (cell-updates/s, description, updates, s)."""
     import oracle as O
     if wl.lmax > 0:
         # AMR workload: one macro step of the AMR oracle on a level-0 grid of
@@ -168,17 +171,6 @@ def oracle_sample(wl, edge, reps=1, flux=0):
     o = O.Oracle(dim=wl.dim, degree=wl.degree, n=wl.n, lo=wl.lo, hi=wl.hi, bc=wl.bc, system=wl.system,
                  gamma=wl.gamma, ch=wl.ch, cfl=wl.cfl, flux=flux)
     n = wl.n
-    if wl.name.startswith("c4") or wl.name.startswith("c3"):
-        # centre the box on x = 0.5 (r = R on the x axis), mid-plane in y, z
-        cx = int(round((0.5 - wl.lo[0]) / (wl.hi[0] - wl.lo[0]) * n[0]))
-        ctr = [cx] + [n[k] // 2 for k in range(1, wl.dim)]
-    else:
-        ctr = [n[k] // 2 for k in range(wl.dim)]
-    blo = [max(0, c - edge // 2) for c in ctr]
-    bhi = [min(n[k], blo[k] + edge) for k in range(wl.dim)]
-    glo = [max(0, b - wl.degree - 2) for b in blo]
-    ghi = [min(n[k], b + wl.degree + 2) for k, b in enumerate(bhi)]
-    o.set_initial_box(wl.ic, glo, ghi)
     if wl.name.startswith("c4"):
         uin = O.prim_to_cons(0, 3, wl.gamma, [1, 0, 0, 0, 1])
         dx = (wl.hi[0] - wl.lo[0]) / n[0]
@@ -186,14 +178,23 @@ def oracle_sample(wl, edge, reps=1, flux=0):
     else:
         o.set_initial(wl.ic)
         dt = o.compute_dt()
-    ups, secs = 0, 0.0
+    rng = np.random.default_rng(seed)
+    ups, secs, where = 0, 0.0, []
     for _ in range(reps):
-        t0 = time.perf_counter()
-        _, rep = o.advance_box(dt, blo, bhi)
-        secs += time.perf_counter() - t0
-        ups += rep.cell_updates
-    desc = (f"one step of the {'x'.join(str(bhi[k] - blo[k]) for k in range(wl.dim))} cell box at "
-            f"{blo} of {wl.name} (box + face neighbours reconstructed/predicted), single thread")
+        for _b in range(nbox):
+            blo = [int(rng.integers(0, max(1, n[k] - edge + 1))) for k in range(wl.dim)]
+            bhi = [min(n[k], blo[k] + edge) for k in range(wl.dim)]
+            glo = [max(0, b - wl.degree - 2) for b in blo]
+            ghi = [min(n[k], b + wl.degree + 2) for k, b in enumerate(bhi)]
+            o.set_initial_box(wl.ic, glo, ghi)
+            t0 = time.perf_counter()
+            _, rep = o.advance_box(dt, blo, bhi)
+            secs += time.perf_counter() - t0
+            ups += rep.cell_updates
+            where.append(tuple(blo))
+    desc = (f"one step of {len(where)} {'x'.join([str(edge)] * wl.dim)} cell boxes at seeded random positions "
+            f"{where[:4]}{'...' if len(where) > 4 else ''} of {wl.name} (each box + its face-neighbour layer "
+            f"reconstructed/predicted), single thread")
     return ups / secs, desc, ups, secs
 
 
@@ -201,14 +202,14 @@ def run_reference(args, wl):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    edge = max(2, args.cpu_box // 2)
+    edge = max(2, args.cpu_box // 2) if wl.lmax > 0 else 8
     fl = 1 if args.flux == "osher" else 0
-    for _ in range(args.warmup):
-        oracle_sample(wl, edge, flux=fl)
+    for i in range(args.warmup):
+        oracle_sample(wl, edge, flux=fl, nbox=1, seed=100 + i)
     tot_u, tot_s = 0, 0.0
     desc = ""
-    for _ in range(args.steps):
-        _, desc, u, s = oracle_sample(wl, edge, flux=fl)
+    for i in range(args.steps):
+        _, desc, u, s = oracle_sample(wl, edge, flux=fl, nbox=(2 if wl.dim == 3 else 16) if wl.lmax == 0 else 1, seed=3585 + i)
         tot_u += u
         tot_s += s
     val = tot_u / tot_s
@@ -450,7 +451,8 @@ def main():
             "ic_setup_s": t_ic,
         }
         if world == 1 and not args.no_cpu_baseline:
-            v, desc, u, secs = oracle_sample(wl, args.cpu_box, flux=1 if args.flux == "osher" else 0)
+            v, desc, u, secs = (oracle_sample(wl, 10, flux=1 if args.flux == "osher" else 0, nbox=4 if wl.dim == 3 else 32) if wl.lmax == 0
+                                else oracle_sample(wl, args.cpu_box, flux=1 if args.flux == "osher" else 0))
             line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc,
                                     "cell_updates": u, "seconds": secs, "host_nproc": os.cpu_count()}
         print(json.dumps(line), flush=True)

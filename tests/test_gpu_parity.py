@@ -18,13 +18,18 @@ pytestmark = pytest.mark.gpu
 
 def rel_err(a, b, axis=None):
     """Reading R8: max |a-b| / scale_v per trailing variable v, then max over v,
-    with scale_v = max(max_c |b_v|, max_c |b_0|): a variable that is zero in
-    exact arithmetic (v_y of a 1D tube, psi of Orszag-Tang at t=0) is measured
-    against the density scale."""
+    with scale_v = max_c |b_v| (SURVEY §8(c)'s per-variable relative error); only
+    a variable that is zero in exact arithmetic (max_c |b_v| <= 1e-9 max_c |b_0|:
+    v_y of a 1D tube, psi of Orszag-Tang at t=0) is measured against the
+    density scale."""
+    return (np.abs(a.reshape(-1, a.shape[-1]) - b.reshape(-1, b.shape[-1])).max(axis=0) / var_scale(b)).max()
+
+
+def var_scale(b):
     b2 = b.reshape(-1, b.shape[-1])
-    a2 = a.reshape(-1, a.shape[-1])
-    scale = np.maximum(np.abs(b2).max(axis=0), np.abs(b2[:, 0]).max())
-    return (np.abs(a2 - b2).max(axis=0) / scale).max()
+    sv = np.abs(b2).max(axis=0)
+    rho = np.abs(b2[:, 0]).max()
+    return np.where(sv > 1e-9 * rho, sv, rho)
 
 
 def pair(dim, degree, n, lo, hi, bc, ic, system=0, gamma=1.4, ch=0.0, cfl=0.9, ic_quad=0, flux=0, flux_quad=3):
@@ -249,7 +254,7 @@ def test_c2_512_sampled_parity():
     for blo, bhi in boxes:
         out, _ = o.advance_box(dt, blo, bhi)
         gg = ug[blo[1]:bhi[1], blo[0]:bhi[0]].reshape(-1, 4)
-        scale = np.maximum(np.abs(ug).reshape(-1, 4).max(0), 1.0)
+        scale = var_scale(ug)   # per-variable scale of the whole 512^2 state (R8)
         assert (np.abs(gg - out).max(axis=0) / scale).max() <= 1e-11, (blo, np.abs(gg - out).max(axis=0))
 
 
@@ -269,7 +274,7 @@ def test_c4_256_sampled_parity(flux):
     assert abs(rep.dt0 - dt) <= 1e-14 * dt
     ug = g.get_state().reshape(256, 256, 256, 5)
     o = O.Oracle(dim=3, degree=2, n=wl.n, lo=wl.lo, hi=wl.hi, bc=wl.bc, cfl=wl.cfl, flux=flux)
-    scale = np.array([1.0, 1.0, 1.0, 1.0, 2.5])
+    scale = var_scale(ug)   # per-variable scale of the whole 256^3 state (R8; max |rho v| ~ 0.08 after one step)
     boxes = [((0, 0, 0), (2, 2, 2)), ((254, 100, 127), (256, 102, 129)),   # corner / face
              ((62, 127, 127), (65, 129, 129)),                              # across r = 0.5
              ((127, 127, 127), (129, 129, 129)), ((200, 40, 90), (202, 42, 92))]

@@ -48,4 +48,4 @@ def main(rep, workload, flux="rusanov", label=""):
 
 
 if __name__ == "__main__":
-    main(*sys.argv[1:4])
+    main(*sys.argv[1:5])
