@@ -173,6 +173,18 @@ ader_status ader_get_state(const ader_ctx* c, double* u_host, int64_t capacity_c
 ader_status ader_get_cells(const ader_ctx* c, ader_cell* out, int64_t capacity, int64_t* n);
 double      ader_time(const ader_ctx* c);
 
+/* One macro step with the state crossing the host boundary (the e2e path):
+ * in_host (optional, [owned cell][nu] like ader_set_cells) is copied in first;
+ * out_host receives the owned state after the step ([owned cell][nu], like
+ * ader_get_state).  The face fluxes and the update run in slabs along the
+ * last axis and each finished slab is copied to out_host on a second stream
+ * while the next slabs' fluxes run, so most of the device-to-host copy
+ * overlaps the step; the result is bitwise that of ader_set_cells +
+ * ader_step(1) + ader_get_state.  in_host may equal out_host.  Host buffers
+ * should be pinned for the copies to overlap.  Uniform grids
+ * (ADER_ERR_UNSUPPORTED on AMR). */
+ader_status ader_step_io(ader_ctx* c, const double* in_host, double* out_host, double t_end, ader_step_report* rep);
+
 /* --- time stepping ---------------------------------------------------------- */
 /* Whole level-0 macro steps until t >= t_end or max_macro_steps were taken:
  * dt0 = cfl / max over active cells of sum_dir s_dir/dx_dir (all ranks),

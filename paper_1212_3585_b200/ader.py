@@ -107,6 +107,7 @@ def lib():
         L.ader_time.argtypes = [vp]
         L.ader_time.restype = C.c_double
         L.ader_step.argtypes = [vp, C.c_double, C.c_int64, C.POINTER(AderStepReport)]
+        L.ader_step_io.argtypes = [vp, dp, dp, C.c_double, C.POINTER(AderStepReport)]
         L.ader_refine.argtypes = [vp, C.POINTER(AderStepReport)]
         L.ader_partition.argtypes = [C.POINTER(AderConfig), C.c_int32, C.POINTER(AderPartitionInfo)]
         L.ader_nccl_unique_id.argtypes = [C.POINTER(C.c_uint8)]
@@ -132,7 +133,7 @@ EXPORTED = ("ader_create", "ader_destroy", "ader_last_error", "ader_set_stream",
             "ader_partition", "ader_halo_plan", "ader_nccl_unique_id", "ader_set_profiling", "ader_kernel_stats",
             "ader_launch_count", "ader_debug_dump", "ader_sizeof", "ader_debug_group_create",
             "ader_debug_group_set_initial", "ader_debug_group_step", "ader_rcb_partition",
-            "ader_create_host_comm")
+            "ader_create_host_comm", "ader_step_io")
 
 
 def _dp(a):
@@ -336,6 +337,20 @@ class Solver:
     def step(self, t_end=1e300, max_steps=1) -> AderStepReport:
         rep = AderStepReport()
         self._chk(lib().ader_step(self.ptr, t_end, max_steps, C.byref(rep)))
+        return rep
+
+    def step_io(self, host_in, host_out, t_end=1e300) -> AderStepReport:
+        """One macro step with the state crossing the host boundary (ader_step_io):
+        host_in / host_out are numpy arrays or raw pointers (int) of
+        [owned cell][nu] doubles; host_in may be None."""
+        def ptr(a):
+            if a is None:
+                return None
+            if isinstance(a, int):
+                return C.cast(C.c_void_p(a), C.POINTER(C.c_double))
+            return _dp(a)
+        rep = AderStepReport()
+        self._chk(lib().ader_step_io(self.ptr, ptr(host_in), ptr(host_out), t_end, C.byref(rep)))
         return rep
 
     def refine(self):

@@ -168,6 +168,8 @@ struct ader_ctx {
   double dx[3] = {1, 1, 1}, inv_dx[3] = {1, 1, 1};
   KCtx k{};
   cudaStream_t own_stream = nullptr;
+  cudaStream_t io_stream = nullptr;            // ader_step_io: device-to-host copies of finished slabs
+  std::vector<cudaEvent_t> io_ev;              // one per slab (created on first use)
   double *u = nullptr, *wx = nullptr, *wxy = nullptr, *w = nullptr, *q = nullptr, *F = nullptr;
   double *stage = nullptr;                     // compact staging buffer (set/get)
   double *sendb[6] = {}, *recvb[6] = {};       // halo buffers per side
@@ -739,6 +741,8 @@ void free_ctx(ader_ctx* c) {
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   if (c->comm) g_nccl.CommDestroy(c->comm);
   delete c->hostcomm;
+  for (cudaEvent_t e : c->io_ev) cudaEventDestroy(e);
+  if (c->io_stream) cudaStreamDestroy(c->io_stream);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
   delete c;
 }
@@ -1241,10 +1245,70 @@ void advance_dt(ader_ctx* c, double dt, const double* dtdx_dev = nullptr) {
   c->t += dt;
 }
 
+// Tail of a macro step for ader_step_io: face fluxes and the update in K slabs
+// along the last axis, each finished slab of the owned state gathered and
+// copied to the host on a second stream while the next slabs' fluxes run.
+// The update of slab i needs the lower faces of slab i+1's first level, so
+// the order is flux(0), flux(1), update(0), copy(0), flux(2), update(1), ...
+// Same kernels and arithmetic as run_flux + run_update: bitwise the same state.
+ader_status tail_to_host(ader_ctx* c, const double* dtdx_dev, double* out_host) {
+  const int W = c->d - 1, H = c->H, zH = c->d == 3 ? H : 0;
+  const int lo = (W == 2) ? zH : H, nW = c->n[W];
+  const int K = std::max(1, std::min(8, nW / 8));
+  if (!c->io_stream) CK(cudaStreamCreateWithFlags(&c->io_stream, cudaStreamNonBlocking));
+  while ((int)c->io_ev.size() < K + 1) {
+    cudaEvent_t e;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c->io_ev.push_back(e);
+  }
+  auto cut = [&](int i) { return lo + (int)((long long)nW * i / K); };
+  Box fb[3];
+  face_boxes(c, fb);
+  long long nf = 0;
+  for (int k = 0; k < c->d; ++k) nf += fb[k].count();
+  const double fl_per_face = face_flops(c);
+  const long long plane = (long long)c->n[0] * (c->d == 3 ? c->n[1] : 1);   // owned cells per level of W
+  auto flux = [&](int i) {
+    Box e = make_box(H, H + c->n[0] + 1, H, H + c->n[1] + 1, zH, zH + c->n[2] + (c->d == 3 ? 1 : 0));
+    e.lo[W] = cut(i);
+    e.ext[W] = cut(i + 1) - cut(i) + (i + 1 == K ? 1 : 0);
+    Scope s(c, ADER_K_FLUX, fl_per_face * (double)nf * e.ext[W] / (nW + 1));
+    launch_face_flux_cells(c->k, c->q, c->F, e, H, c->n, transmissive_mask(c), reflective_mask(c), c->cnt, c->qs);
+  };
+  auto update_copy = [&](int i) -> ader_status {
+    Box r = owned(c);
+    r.lo[W] = cut(i);
+    r.ext[W] = cut(i + 1) - cut(i);
+    {
+      Scope s(c, ADER_K_UPDATE, (double)r.count() * c->nv * 3.0 * c->d);
+      double dtdx[3] = {0, 0, 0};
+      launch_update(c->k, c->u, c->F, r, dtdx, c->inv_dx, c->cnt, dtdx_dev);
+    }
+    const long long off = (long long)(cut(i) - lo) * plane * c->nv;
+    launch_gather(c->k, c->u, c->nv, r, c->stage + off);
+    CK(cudaEventRecord(c->io_ev[i], c->k.stream));
+    CK(cudaStreamWaitEvent(c->io_stream, c->io_ev[i], 0));
+    CK(cudaMemcpyAsync(out_host + off, c->stage + off, (size_t)r.count() * c->nv * sizeof(double),
+                       cudaMemcpyDeviceToHost, c->io_stream));
+    return ADER_OK;
+  };
+  flux(0);
+  for (int i = 0; i < K; ++i) {
+    if (i + 1 < K) flux(i + 1);
+    ader_status st = update_copy(i);
+    if (st != ADER_OK) return st;
+  }
+  // later work on the compute stream (and its syncs) also covers the copies
+  CK(cudaEventRecord(c->io_ev[K], c->io_stream));
+  CK(cudaStreamWaitEvent(c->k.stream, c->io_ev[K], 0));
+  c->speed_valid = true;
+  return ADER_OK;
+}
+
 // One macro step enqueued without a host round trip: ghost layers, WENO, the
 // CFL speed (from the previous update, or a CFL kernel), NCCL max over ranks,
 // dt on the device (k_step_dt), predictor, fluxes, update.
-ader_status enqueue_step(ader_ctx* c, double t_end) {
+ader_status enqueue_step(ader_ctx* c, double t_end, double* out_host = nullptr) {
   ader_status st = fill_halo(c, c->u);
   if (st != ADER_OK) return st;
   const bool fused = fused_weno_pred(c);
@@ -1259,15 +1323,23 @@ ader_status enqueue_step(ader_ctx* c, double t_end) {
       return fail(c, ADER_ERR_NCCL, "allreduce(max) of the CFL speed failed");
     launch_step_dt(c->k, c->cnt, c->st, c->cfg.cfl, t_end, c->dx);
   }
+  const bool chunked = out_host && !fused_pred_flux(c);
   if (fused_pred_flux(c)) run_pred_flux(c, 0.0, c->st->dtdx);
   else {
     if (fused) run_weno_predictor(c, 0.0, c->st->dtdx);
     else run_predictor(c, 0.0, c->st->dtdx, true);
-    run_flux(c);
+    if (!chunked) run_flux(c);
   }
   CK(cudaMemsetAsync(&c->cnt->speed_bits, 0, sizeof(unsigned long long), c->k.stream));
+  if (chunked) return tail_to_host(c, c->st->dtdx, out_host);
   run_update(c, 0.0, c->st->dtdx);
   c->speed_valid = true;
+  if (out_host) {   // fused walk: the whole state after the update
+    const Box b = owned(c);
+    launch_gather(c->k, c->u, c->nv, b, c->stage);
+    CK(cudaMemcpyAsync(out_host, c->stage, (size_t)b.count() * c->nv * sizeof(double), cudaMemcpyDeviceToHost,
+                       c->k.stream));
+  }
   return ADER_OK;
 }
 
@@ -1336,6 +1408,45 @@ ader_status dt_from_speed(ader_ctx* c, double speed, double t_end, double* dt) {
   return ADER_OK;
 }
 }  // namespace
+
+ader_status ader_step_io(ader_ctx* c, const double* in_host, double* out_host, double t_end, ader_step_report* rep) {
+  if (!c || !out_host) return ADER_ERR_ARG;
+  const auto w0 = std::chrono::steady_clock::now();
+  if (c->loopback) return fail(c, ADER_ERR_ARG, "group contexts step through ader_debug_group_step");
+  if (c->amr) return fail(c, ADER_ERR_UNSUPPORTED, "ader_step_io: uniform grids only (use ader_step + ader_get_cells)");
+  const Box b = owned(c);
+  if (in_host) {
+    CK(cudaMemcpyAsync(c->stage, in_host, (size_t)b.count() * c->nv * sizeof(double), cudaMemcpyHostToDevice,
+                       c->k.stream));
+    launch_scatter(c->k, c->u, c->nv, b, c->stage);
+    c->speed_valid = false;
+    c->guess_ready = false;
+  }
+  ader_step_report r;
+  std::memset(&r, 0, sizeof(r));
+  unsigned long long sw0 = 0, pc0 = 0;
+  ader_status st = step_begin(c, &sw0, &pc0);
+  if (st != ADER_OK) return st;
+  st = read_state(c);
+  if (st != ADER_OK) return st;
+  const long long steps0 = c->hst->steps;
+  if (c->t < t_end) {
+    if (c->has_exact) st = refresh_exact(c);
+    if (st == ADER_OK) st = enqueue_step(c, t_end, out_host);
+  } else {
+    launch_gather(c->k, c->u, c->nv, b, c->stage);
+    CK(cudaMemcpyAsync(out_host, c->stage, (size_t)b.count() * c->nv * sizeof(double), cudaMemcpyDeviceToHost,
+                       c->k.stream));
+  }
+  if (st == ADER_OK) st = read_state(c);
+  r.macro_steps = c->hst->steps - steps0;
+  r.dt0 = c->hst->last_dt;
+  r.min_threshold_margin = 1e300;
+  st = step_finish(c, st, &r, sw0, pc0);
+  r.wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - w0).count();
+  if (rep) *rep = r;
+  return st;
+}
 
 ader_status ader_step(ader_ctx* c, double t_end, int64_t max_macro_steps, ader_step_report* rep) {
   if (!c) return ADER_ERR_ARG;
