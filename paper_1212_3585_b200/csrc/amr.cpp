@@ -72,6 +72,12 @@ struct AmrState {
   int band = 0;                                       // compute-set margin in level-0 cells
   bool band_sets = false;                             // ADER_AMR_BAND=1: the uniform band instead of R28 sets
   std::vector<int> lpres[kAmrMaxLevels];              // active cells whose averages this rank holds (multi-rank)
+  // multi-rank: rows of w / q only for the cells this rank computes (R28);
+  // a cell keeps its row while it stays computed, rows of cells that leave
+  // are released one list rebuild later (the adapt's new-cell initialisation
+  // still reads the refined mothers' w / q); row 0 is scratch for the rest
+  std::vector<int> slot_of, slot_defer, free_slots;
+  int nslots = 1, slot_cap = 0;
   std::vector<char> own, comp;                        // per id
   long long nlev[kAmrMaxLevels]{};                    // alive cells per level (whole tree)
   std::vector<int> lown[kAmrMaxLevels];               // owned active cells (multi-rank)
@@ -521,8 +527,12 @@ ader_status ensure_capacity(AmrState* A, std::string& err) {
   AmrDevView& V = A->V;
   ACK(grow((void**)&V.u, sizeof(double) * A->nv));
   ACK(grow((void**)&V.mem, sizeof(double) * 6 * A->nv));
-  ACK(grow((void**)&V.w, sizeof(double) * A->nv * A->NS));
-  ACK(grow((void**)&V.q, sizeof(double) * A->nv * A->NST));
+  if (A->ranks.world == 1) {
+    ACK(grow((void**)&V.w, sizeof(double) * A->nv * A->NS));
+    ACK(grow((void**)&V.q, sizeof(double) * A->nv * A->NST));
+  } else {
+    ACK(grow((void**)&V.slot, sizeof(int)));
+  }
   ACK(grow((void**)&V.chi, sizeof(double)));
   ACK(grow((void**)&V.level, sizeof(int)));
   ACK(grow((void**)&V.status, sizeof(int)));
@@ -570,6 +580,50 @@ struct Uploader {
     return ADER_OK;
   }
 };
+
+// Multi-rank rows of w / q (see slot_of): release the rows deferred at the
+// previous rebuild whose cells are still not computed, defer the rows of cells
+// that left the compute lists, give new computed cells a row, grow w / q
+// (rows kept) and return the per-id row array for the device (0 = scratch).
+ader_status assign_slots(AmrState* A, std::vector<int>& dev_slot, std::string& err) {
+  const int nu = (int)A->cells.size();
+  if ((int)A->slot_of.size() < nu) A->slot_of.resize(nu, -1);
+  std::vector<char> need(nu, 0);
+  for (int l = 0; l <= A->lmax; ++l)
+    for (int i : A->lact[l]) need[i] = 1;
+  for (int i : A->slot_defer)
+    if (i < nu && A->slot_of[i] >= 0 && !need[i]) { A->free_slots.push_back(A->slot_of[i]); A->slot_of[i] = -1; }
+  A->slot_defer.clear();
+  for (int i = 0; i < nu; ++i) {
+    if (A->slot_of[i] >= 0 && !need[i]) A->slot_defer.push_back(i);
+    if (need[i] && A->slot_of[i] < 0) {
+      if (!A->free_slots.empty()) { A->slot_of[i] = A->free_slots.back(); A->free_slots.pop_back(); }
+      else A->slot_of[i] = A->nslots++;
+    }
+  }
+  if (A->nslots > A->slot_cap) {
+    const int nc = std::max(A->nslots + A->nslots / 2, 1024);
+    AmrDevView& V = A->V;
+    auto grow = [&](double** p, size_t row) -> cudaError_t {
+      double* np = nullptr;
+      cudaError_t e = cudaMalloc(&np, (size_t)nc * row * sizeof(double));
+      if (e != cudaSuccess) return e;
+      if (*p) {
+        cudaMemcpyAsync(np, *p, (size_t)A->slot_cap * row * sizeof(double), cudaMemcpyDeviceToDevice, A->k->stream);
+        cudaStreamSynchronize(A->k->stream);
+        cudaFree(*p);
+      }
+      *p = np;
+      return cudaSuccess;
+    };
+    ACK(grow(&V.w, (size_t)A->nv * A->NS));
+    ACK(grow(&V.q, (size_t)A->nv * A->NST));
+    A->slot_cap = nc;
+  }
+  dev_slot.resize(nu);
+  for (int i = 0; i < nu; ++i) dev_slot[i] = A->slot_of[i] >= 0 ? A->slot_of[i] : 0;
+  return ADER_OK;
+}
 
 // Push the host tree to the device: only the ids whose links or status changed
 // since the last upload (plus the map entries they occupy), and the per-level
@@ -764,9 +818,17 @@ ader_status upload_topology(AmrState* A, std::string& err) {
   const size_t os = up.add(sets.data(), sets.size() * sizeof(long long));
   const size_t ol = up.add(all.data(), all.size() * sizeof(int));
   const size_t oo = W > 1 ? up.add(A->own.data(), A->own.size()) : 0;
+  std::vector<int> dslot;
+  if (W > 1) {
+    s = assign_slots(A, dslot, err);
+    if (s != ADER_OK) return s;
+  }
+  const size_t osl = W > 1 ? up.add(dslot.data(), sizeof(int) * dslot.size()) : 0;
   s = up.run(err);
   if (s != ADER_OK) return s;
   if (W > 1) ACK(cudaMemcpyAsync(A->V.own, A->dscratch + oo, A->own.size(), cudaMemcpyDeviceToDevice, sm));
+  if (W > 1)
+    ACK(cudaMemcpyAsync(A->V.slot, A->dscratch + osl, sizeof(int) * dslot.size(), cudaMemcpyDeviceToDevice, sm));
   A->tm_u[2] += now_s() - w0; w0 = now_s();
   amr_launch_meta_scatter(*A->k, A->V, (const long long*)(A->dscratch + om), (int)(meta.size() / 8));
   amr_launch_map_set(*A->k, A->V, (const long long*)(A->dscratch + oc), (int)(clears.size() / 3));
@@ -1450,7 +1512,13 @@ void amr_destroy(AmrState* A) {
                  1e3 * A->tm_u[0] / A->tm_steps, 1e3 * A->tm_u[1] / A->tm_steps, 1e3 * A->tm_u[3] / A->tm_steps,
                  1e3 * A->tm_u[2] / A->tm_steps);
   cudaStreamSynchronize(A->k->stream);
-  void* ps[] = {A->V.u, A->V.mem, A->V.w, A->V.q, A->V.chi, A->V.level, A->V.status, A->V.mother, A->V.child, A->V.idx,
+  if (std::getenv("ADER_AMR_MEM"))
+    std::fprintf(stderr, "amr memory rank %d/%d: ids %zu (capacity %d), w/q rows %d (capacity %d): w/q %.3f GB, "
+                         "per-id w/q would be %.3f GB\n", A->ranks.rank, A->ranks.world, A->cells.size(), A->cap,
+                 A->ranks.world > 1 ? A->nslots : (int)A->cells.size(), A->ranks.world > 1 ? A->slot_cap : A->cap,
+                 8e-9 * A->nv * (A->NS + A->NST) * (A->ranks.world > 1 ? A->slot_cap : A->cap),
+                 8e-9 * A->nv * (A->NS + A->NST) * A->cap);
+  void* ps[] = {A->V.u, A->V.mem, A->V.w, A->V.q, A->V.chi, A->V.level, A->V.status, A->V.mother, A->V.child, A->V.idx, A->V.slot,
                 A->V.own, A->dlist, A->xsend, A->xrecv, A->rb_buf, A->rb_tmp};
   for (void* p : ps)
     if (p) cudaFree(p);

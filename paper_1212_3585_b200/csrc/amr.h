@@ -41,6 +41,8 @@ struct AmrDevView {            // raw device pointers handed to kernels
   int* level; int* status; int* mother; int* child;
   long long* idx;              // [cap][3]
   unsigned char* own;          // [cap] multi-rank: 1 = this rank's cell (errors count); nullptr for one rank
+  int* slot;                   // [cap] multi-rank: row of the cell in w / q (rows only for the cells this
+                               // rank computes, R28; row 0 is scratch); nullptr for one rank (row = id)
   const int* map[kAmrMaxLevels];
   long long n[kAmrMaxLevels][3];
   int bc[6];

@@ -50,6 +50,9 @@ __device__ __forceinline__ double amr_u_at(const AmrDevView& V, int l, long long
   return (v >= 1 && v <= V.D && ((fl >> (v - 1)) & 1)) ? -a : a;
 }
 
+// row of a cell in w / q: its slot on a multi-rank context (R28), else its id
+__device__ __forceinline__ long long wq_row(const AmrDevView& V, int id) { return V.slot ? (long long)V.slot[id] : id; }
+
 __device__ __forceinline__ void amr_error(DevCounters* c, int code, int stage, long long cell) {
   if (atomicCAS(&c->err_code, 0, code) == 0) {
     c->err_stage = stage;
@@ -78,7 +81,7 @@ __device__ __forceinline__ double subbox(const AmrDevView& V, const SubTables& S
   for (int k = 0; k < D; ++k) off[k] = (int)(V.idx[(long long)cell * 3 + k] - V.idx[(long long)mom * 3 + k] * V.r);
   double acc = 0.0;
   if (mode == 0) {
-    const double* w = V.w + ((long long)mom * V.NV + v) * NS;
+    const double* w = V.w + (wq_row(V, mom) * V.NV + v) * NS;
 #pragma unroll
     for (int p = 0; p < NS; ++p) {
       double c = S.Psub[off[0]][p % N] * S.Psub[off[1]][(p / N) % N];
@@ -86,7 +89,7 @@ __device__ __forceinline__ double subbox(const AmrDevView& V, const SubTables& S
       acc += c * w[p];
     }
   } else {
-    const double* q = V.q + ((long long)mom * V.NV + v) * NST;
+    const double* q = V.q + (wq_row(V, mom) * V.NV + v) * NST;
     for (int p = 0; p < NST; ++p) {
       const int sp = p % NS, s = p / NS;
       double c = S.Psub[off[0]][sp % N] * S.Psub[off[1]][(sp / N) % N];
@@ -129,7 +132,7 @@ __global__ void __launch_bounds__(128) k_amr_weno(AmrDevView V, const int* __res
   const int c = list[i / NV], v = i % NV;
   const int l = V.level[c];
   const long long x0 = V.idx[(long long)c * 3], y0 = V.idx[(long long)c * 3 + 1], z0 = V.idx[(long long)c * 3 + 2];
-  double* wo = V.w + ((long long)c * NV + v) * NS;
+  double* wo = V.w + (wq_row(V, c) * NV + v) * NS;
   if (D == 2) {
     double wx[W][N];
     for (int jy = 0; jy < W; ++jy) {
@@ -287,7 +290,7 @@ __device__ __forceinline__ bool amr_cell_face_w(const AmrDevView& V, int c, bool
   const int l = V.level[c];
   long long ix[3] = {V.idx[(long long)c * 3], V.idx[(long long)c * 3 + 1], V.idx[(long long)c * 3 + 2]};
   ix[DIR] += side ? 1 : -1;
-  const double* qc = V.q + (long long)c * NV * NST;
+  const double* qc = V.q + wq_row(V, c) * NV * NST;
   const bool out = ix[DIR] < 0 || ix[DIR] >= V.n[l][DIR];
   // kind as listed above, -1 error.  Every lane group of the warp runs the
   // same two __syncwarp()s whatever its kind (2D: several cells per warp).
@@ -299,13 +302,13 @@ __device__ __forceinline__ bool amr_cell_face_w(const AmrDevView& V, int c, bool
     nb = amr_lookup(V, l, ix[0], ix[1], ix[2]);
     const int st = nb >= 0 ? V.status[nb] : 9;
     if (st == 0) {
-      const double* qn = V.q + (long long)nb * NV * NST;
+      const double* qn = V.q + wq_row(V, nb) * NV * NST;
       kind = 0;
       qL = side ? qc : qn;
       qR = side ? qn : qc;
     } else if (st == 1) {
       // coarse-fine: the virtual neighbour scales its mother's q_h down
-      const double* qK = V.q + (long long)V.mother[nb] * NV * NST;
+      const double* qK = V.q + wq_row(V, V.mother[nb]) * NV * NST;
       constexpr int ax0 = (DIR == 0) ? 1 : 0, ax1 = (DIR == 2) ? 1 : 2;
       o1 = (int)(V.idx[(long long)c * 3 + ax0] % V.r);
       o2 = (D == 3) ? (int)(V.idx[(long long)c * 3 + ax1] % V.r) : 0;
@@ -625,7 +628,8 @@ void amr_launch_predictor(const KCtx& k, const AmrDevView& v, const int* list, i
                           double tol, int max_sweeps, DevCounters* cnt) {
   if (n <= 0) return;
   Box none{{0, 0, 0}, {0, 0, 0}};
-  launch_predictor_list(k, v.w, v.q, none, list, n, dtdx, tol, max_sweeps, cnt, v.own);
+  launch_predictor_list(k, v.w, v.q, none, list, n, dtdx, tol, max_sweeps, cnt, v.own, nullptr, 0, false, nullptr,
+                        0.0, v.slot);
 }
 
 void amr_launch_flux_update(const KCtx& k, const AmrDevView& v, const SubTables& st, const int* list, int n, int m,

@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? 4 : 2) k_predictor(
     const double tol, const int max_sweeps, DevCounters* __restrict__ cnt, const int* __restrict__ list,
     const long long nlist, const unsigned char* __restrict__ emask, const double* __restrict__ dtdx_dev,
     const long long qs, const int guess, const StepState* __restrict__ gst, const double guess_r,
-    const __grid_constant__ DevTables T) {
+    const int* __restrict__ rows, const __grid_constant__ DevTables T) {
   using C = PredCfg<D, M, SYS>;
   constexpr int NV = C::NV, N = C::N, NS = C::NS, NST = C::NST, G = C::G, CPW = C::CPW, FSZ = C::FSZ;
   extern __shared__ double smem[];
@@ -160,8 +160,9 @@ __global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? 4 : 2) k_predictor(
   {
     const long long r0 = wb * CPW + slot;
     const long long c0 = r0 < count ? cell_of(r0) : 0;
+    const long long d0 = rows ? (long long)rows[c0] : c0;   // row of w / q
 #pragma unroll
-    for (int v = 0; v < NV; ++v) wn[v] = r0 < count ? __ldg(&w[c0 * (NV * NS) + v * NS + node]) : 1.0;
+    for (int v = 0; v < NV; ++v) wn[v] = r0 < count ? __ldg(&w[d0 * (NV * NS) + v * NS + node]) : 1.0;
   }
   unsigned long long acc_sweeps = 0, acc_cells = 0;
   int acc_max = 0;
@@ -170,20 +171,22 @@ __global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? 4 : 2) k_predictor(
   const bool cell_ok = rc < count;
   const bool active = cell_ok && lane_ok;
   const long long cell = cell_ok ? cell_of(rc) : 0;
+  const long long drow = rows ? (long long)rows[cell] : cell;   // row of w / q
   double wv[NV], qv[NV][N];
 #pragma unroll
   for (int v = 0; v < NV; ++v) wv[v] = wn[v];
   {
     const long long rn = (wb + wstride) * CPW + slot;
     const long long cn = rn < count ? cell_of(rn) : 0;
+    const long long dn = rows ? (long long)rows[cn] : cn;
 #pragma unroll
-    for (int v = 0; v < NV; ++v) wn[v] = rn < count ? __ldg(&w[cn * (NV * NS) + v * NS + node]) : 1.0;
+    for (int v = 0; v < NV; ++v) wn[v] = rn < count ? __ldg(&w[dn * (NV * NS) + v * NS + node]) : 1.0;
   }
   bool conv, bad;
   int nsw;
   if (use_guess && cell_ok && lane_ok) {
     // q0 = w + sum_a c[s][a] q_prev[a] (the cell's previous q, read in place)
-    const double* qp = q + cell * qs + node;
+    const double* qp = q + drow * qs + node;
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
       double old[N];
@@ -204,7 +207,7 @@ __global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? 4 : 2) k_predictor(
     else if (!conv) record_error(cnt, 2, 1, cell);
   }
   if (active) {
-    double* qo = q + cell * qs + node;   // qs: block stride (>= NV * NST)
+    double* qo = q + drow * qs + node;   // qs: block stride (>= NV * NST)
 #pragma unroll
     for (int v = 0; v < NV; ++v)
 #pragma unroll
@@ -585,7 +588,7 @@ void launch_predictor(const KCtx& k, const double* w, double* q, const Box& regi
 void launch_predictor_list(const KCtx& k, const double* w, double* q, const Box& region, const int* list,
                            long long nlist, const double dtdx[3], double tol, int max_sweeps, DevCounters* cnt,
                            const unsigned char* emask, const double* dtdx_dev, long long qs, bool guess,
-                           const StepState* gst, double guess_r) {
+                           const StepState* gst, double guess_r, const int* slot) {
   const long long count = list ? nlist : region.count();
   if (count == 0) return;
   ADER_DISPATCH(k.D, k.M, k.SYS, {
@@ -608,7 +611,7 @@ void launch_predictor_list(const KCtx& k, const double* w, double* q, const Box&
     count_launch(k);
     kern<<<g, kPredWarps * 32, sm, k.stream>>>(w, q, region, k.sy, k.sz, dtdx[0], dtdx[1], dtdx[2], k.gamma,
                                                 k.ch, tol, max_sweeps, cnt, list, nlist, emask, dtdx_dev, qstride, guess ? 1 : 0,
-                                                gst, guess_r, k.tab);
+                                                gst, guess_r, slot, k.tab);
   });
 }
 

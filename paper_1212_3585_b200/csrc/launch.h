@@ -76,13 +76,14 @@ void launch_weno_sweep(const KCtx& k, int sweep, const double* src, double* dst,
 void launch_predictor(const KCtx& k, const double* w, double* q, const Box& region, const double dtdx[3],
                       double tol, int max_sweeps, DevCounters* cnt, const double* dtdx_dev = nullptr,
                       long long qs = 0, bool guess = false, const StepState* gst = nullptr, double guess_r = 0.0);
-// Predictor on the cells of an id list (AMR levels): w, q indexed by id.  If
-// emask is given only cells with emask[id] != 0 report solver errors.
+// Predictor on the cells of an id list (AMR levels): w, q indexed by id (or by
+// slot[id] if given).  If emask is given only cells with emask[id] != 0 report
+// solver errors.
 void launch_predictor_list(const KCtx& k, const double* w, double* q, const Box& region, const int* list,
                            long long nlist, const double dtdx[3], double tol, int max_sweeps, DevCounters* cnt,
                            const unsigned char* emask = nullptr, const double* dtdx_dev = nullptr,
                            long long qs = 0, bool guess = false, const StepState* gst = nullptr,
-                           double guess_r = 0.0);
+                           double guess_r = 0.0, const int* slot = nullptr);
 // Face fluxes on the lower face of every cell of `ext` (owned block + 1 on each
 // active axis), one lane group per cell computing all its lower faces
 // (L2-friendly traversal).  bmask bit 2*dir (2*dir+1): the first (last) face

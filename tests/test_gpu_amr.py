@@ -42,7 +42,7 @@ def compare(g, o, tol):
     assert np.array_equal(lg, lo_) and np.array_equal(ig, io) and np.array_equal(sg, so)
     act = so == 0
     sv, rho = np.abs(uo[act]).max(axis=0), np.abs(uo[act, 0]).max()
-    scale = np.where(sv > 1e-9 * rho, sv, rho)   # R8: per-variable scale
+    scale = np.where(sv > 1e-6 * rho, sv, rho)   # R8: per-variable scale
     err = (np.abs(ug[act] - uo[act]).max(axis=0) / scale).max()
     assert err <= tol, err
     return err

@@ -19,8 +19,8 @@ pytestmark = pytest.mark.gpu
 def rel_err(a, b, axis=None):
     """Reading R8: max |a-b| / scale_v per trailing variable v, then max over v,
     with scale_v = max_c |b_v| (SURVEY §8(c)'s per-variable relative error); only
-    a variable that is zero in exact arithmetic (max_c |b_v| <= 1e-9 max_c |b_0|:
-    v_y of a 1D tube, psi of Orszag-Tang at t=0) is measured against the
+    a variable at the noise level of the scheme (max_c |b_v| <= 1e-6 max_c |b_0|:
+    v_y of a 1D tube, the GLM psi of Orszag-Tang) is measured against the
     density scale."""
     return (np.abs(a.reshape(-1, a.shape[-1]) - b.reshape(-1, b.shape[-1])).max(axis=0) / var_scale(b)).max()
 
@@ -29,7 +29,7 @@ def var_scale(b):
     b2 = b.reshape(-1, b.shape[-1])
     sv = np.abs(b2).max(axis=0)
     rho = np.abs(b2[:, 0]).max()
-    return np.where(sv > 1e-9 * rho, sv, rho)
+    return np.where(sv > 1e-6 * rho, sv, rho)
 
 
 def pair(dim, degree, n, lo, hi, bc, ic, system=0, gamma=1.4, ch=0.0, cfl=0.9, ic_quad=0, flux=0, flux_quad=3):

@@ -24,7 +24,7 @@ def rel_err_v(a, b):
     a2 = a.reshape(-1, a.shape[-1])
     sv = np.abs(b2).max(axis=0)
     rho = np.abs(b2[:, 0]).max()
-    scale = np.where(sv > 1e-9 * rho, sv, rho)
+    scale = np.where(sv > 1e-6 * rho, sv, rho)
     return (np.abs(a2 - b2).max(axis=0) / scale).max()
 
 
