@@ -1308,11 +1308,13 @@ ader_status tail_to_host(ader_ctx* c, const double* dtdx_dev, double* out_host) 
 // One macro step enqueued without a host round trip: ghost layers, WENO, the
 // CFL speed (from the previous update, or a CFL kernel), NCCL max over ranks,
 // dt on the device (k_step_dt), predictor, fluxes, update.
-ader_status enqueue_step(ader_ctx* c, double t_end, double* out_host = nullptr) {
-  ader_status st = fill_halo(c, c->u);
-  if (st != ADER_OK) return st;
+ader_status enqueue_step(ader_ctx* c, double t_end, double* out_host = nullptr, bool head_done = false) {
   const bool fused = fused_weno_pred(c);
-  if (!fused) run_weno(c);
+  if (!head_done) {
+    ader_status st = fill_halo(c, c->u);
+    if (st != ADER_OK) return st;
+    if (!fused) run_weno(c);
+  }
   {
     Scope sc(c, ADER_K_OTHER, 0.0);
     if (!c->speed_valid) {
@@ -1409,13 +1411,145 @@ ader_status dt_from_speed(ader_ctx* c, double speed, double t_end, double* dt) {
 }
 }  // namespace
 
+// Head of an ader_step_io step with a new host state (one rank, periodic /
+// transmissive / reflective sides): the state arrives in K slabs along the last
+// axis W on the copy stream, and as each slab lands the compute stream
+// scatters it, fills its ghost cells along the other axes, runs the WENO
+// sweeps along those axes on its levels and takes its CFL speed; after the
+// last slab the ghost levels along W are filled, swept, and the sweep along W
+// runs on all levels.  The same kernels on the same cells as fill_halo +
+// run_weno + the CFL kernel, so the step is bitwise unchanged; the copy-in
+// overlaps all but the last slab's sweeps.
+bool pipelined_head_ok(const ader_ctx* c) {
+  if (c->cfg.world_size > 1 || fused_weno_pred(c) || c->has_exact) return false;
+  for (int k = 0; k < 2 * c->d; ++k)
+    if (c->cfg.bc[k] == ADER_BC_INFLOW || c->cfg.bc[k] == ADER_BC_EXACT) return false;
+  // worth it for states the copy takes milliseconds on (the slab launches cost ~0.1 ms)
+  // (ADER_STEP_IO_PIPELINE=1 forces it for small states: tests)
+  const char* e = std::getenv("ADER_STEP_IO_PIPELINE");
+  return c->n[c->d - 1] >= 16 && (owned(c).count() * c->nv * 8 >= (64LL << 20) || (e && e[0] == '1'));
+}
+
+ader_status head_from_host(ader_ctx* c, const double* in_host) {
+  const int d = c->d, W = d - 1, H = c->H, M = c->M, zH = d == 3 ? H : 0;
+  const int lo = (W == 2) ? zH : H, nW = c->n[W];
+  const int K = std::max(1, std::min(8, nW / 8));
+  if (!c->io_stream) CK(cudaStreamCreateWithFlags(&c->io_stream, cudaStreamNonBlocking));
+  while ((int)c->io_ev.size() < 2 * K + 2) {
+    cudaEvent_t e;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c->io_ev.push_back(e);
+  }
+  auto cut = [&](int i) { return lo + (int)((long long)nW * i / K); };
+  const long long plane = (long long)c->n[0] * (d == 3 ? c->n[1] : 1);
+  const int nx = c->n[0], ny = c->n[1], nz = c->n[2];
+  // the sweeps' boxes (run_weno); per slab restricted to its owned levels of W
+  Box rx, ry;
+  if (d == 2) rx = make_box(H - 1, H + nx + 1, H - 1 - M, H + ny + 1 + M, 0, 1);
+  else {
+    rx = make_box(H - 1, H + nx + 1, H - 1 - M, H + ny + 1 + M, zH - 1 - M, zH + nz + 1 + M);
+    ry = make_box(H - 1, H + nx + 1, H - 1, H + ny + 1, zH - 1 - M, zH + nz + 1 + M);
+  }
+  auto restrict_w = [&](Box b, int a, int e) { b.lo[W] = a; b.ext[W] = e - a; return b; };
+  const double pf = weno_problem_flops(M) * c->nv;
+  // the ordering of run_weno's sweeps is kept per level: x before y on a level
+  // (3D); the copy-in of slab i+1 overlaps the work on slab i
+  auto enqueue_copy = [&](int i) -> ader_status {
+    Box r = owned(c);
+    r.lo[W] = cut(i);
+    r.ext[W] = cut(i + 1) - cut(i);
+    const long long off = (long long)(cut(i) - lo) * plane * c->nv;
+    if (i == 0) CK(cudaEventRecord(c->io_ev[2 * K], c->k.stream));   // stage free (previous users done)
+    CK(cudaStreamWaitEvent(c->io_stream, c->io_ev[2 * K], 0));
+    CK(cudaMemcpyAsync(c->stage + off, in_host + off, (size_t)r.count() * c->nv * sizeof(double),
+                       cudaMemcpyHostToDevice, c->io_stream));
+    CK(cudaEventRecord(c->io_ev[i], c->io_stream));
+    return ADER_OK;
+  };
+  for (int i = 0; i < K; ++i) {
+    ader_status st = enqueue_copy(i);
+    if (st != ADER_OK) return st;
+  }
+  CK(cudaMemsetAsync(&c->cnt->speed_bits, 0, sizeof(unsigned long long), c->k.stream));
+  int wdone = lo + M;   // levels [lo + M, wdone) of the sweep along W are done
+  for (int i = 0; i < K; ++i) {
+    Box r = owned(c);
+    r.lo[W] = cut(i);
+    r.ext[W] = cut(i + 1) - cut(i);
+    const long long off = (long long)(cut(i) - lo) * plane * c->nv;
+    CK(cudaStreamWaitEvent(c->k.stream, c->io_ev[i], 0));
+    launch_scatter(c->k, c->u, c->nv, r, c->stage + off);
+    {
+      Scope s(c, ADER_K_HALO, 0.0);
+      for (int a = 0; a < W; ++a) {   // local ghost fills of the other axes on these levels
+        ader_halo_desc dl, dh;
+        axis_plans(c, a, &dl, &dh);
+        auto mode = [](int kind) { return kind == 2 ? 0 : (kind == 4 ? 2 : 1); };
+        Box rl = restrict_w(desc_box(dl.recv_lo, dl.recv_hi), cut(i), cut(i + 1));
+        Box rh = restrict_w(desc_box(dh.recv_lo, dh.recv_hi), cut(i), cut(i + 1));
+        launch_fill_axis(c->k, c->u, rl, a, mode(dl.kind), H, c->n[a]);
+        launch_fill_axis(c->k, c->u, rh, a, mode(dh.kind), H, c->n[a]);
+      }
+    }
+    {
+      const Box bx = restrict_w(rx, cut(i), cut(i + 1));
+      Scope s(c, ADER_K_WENO, pf * (bx.count() + (d == 3 ? (double)restrict_w(ry, cut(i), cut(i + 1)).count() * c->N : 0.0)));
+      launch_weno_sweep(c->k, 0, c->u, c->wx, bx);
+      if (d == 3) launch_weno_sweep(c->k, 1, c->wx, c->wxy, restrict_w(ry, cut(i), cut(i + 1)));
+    }
+    {
+      Scope s(c, ADER_K_OTHER, 0.0);
+      launch_cfl_speed(c->k, c->u, r, c->inv_dx, c->cnt);
+    }
+    // the sweep along W on the levels whose 2M+1 window is in (no ghost levels)
+    const int wb = cut(i + 1) - M;
+    if (wb > wdone) {
+      const Box bz = restrict_w(grown(c, 1), wdone, wb);
+      Scope s(c, ADER_K_WENO, pf * bz.count() * (d == 3 ? c->N * c->N : c->N));
+      launch_weno_sweep(c->k, W, d == 3 ? c->wxy : c->wx, c->w, bz);
+      wdone = wb;
+    }
+  }
+  c->speed_valid = true;
+  // ghost levels along W, their sweeps, then the sweep along W on all levels
+  {
+    Scope s(c, ADER_K_HALO, 0.0);
+    ader_halo_desc dl, dh;
+    axis_plans(c, W, &dl, &dh);
+    auto mode = [](int kind) { return kind == 2 ? 0 : (kind == 4 ? 2 : 1); };
+    launch_fill_axis(c->k, c->u, desc_box(dl.recv_lo, dl.recv_hi), W, mode(dl.kind), H, c->n[W]);
+    launch_fill_axis(c->k, c->u, desc_box(dh.recv_lo, dh.recv_hi), W, mode(dh.kind), H, c->n[W]);
+  }
+  {
+    const int glo = (d == 3 ? zH : H) - 1 - M, ghi = lo + nW + 1 + M;
+    const Box b0 = restrict_w(rx, glo, lo), b1 = restrict_w(rx, lo + nW, ghi);
+    // the sweep along W on the levels left: [lo - 1, lo + M) and [wdone, lo + nW + 1)
+    const Box z0 = restrict_w(grown(c, 1), lo - 1, lo + M), z1 = restrict_w(grown(c, 1), wdone, lo + nW + 1);
+    const double per = d == 3 ? c->N * c->N : c->N;
+    double fl = pf * (b0.count() + b1.count()) + pf * per * (z0.count() + z1.count());
+    if (d == 3) fl += pf * c->N * (restrict_w(ry, glo, lo).count() + restrict_w(ry, lo + nW, ghi).count());
+    Scope s(c, ADER_K_WENO, fl);
+    launch_weno_sweep(c->k, 0, c->u, c->wx, b0);
+    launch_weno_sweep(c->k, 0, c->u, c->wx, b1);
+    if (d == 3) {
+      launch_weno_sweep(c->k, 1, c->wx, c->wxy, restrict_w(ry, glo, lo));
+      launch_weno_sweep(c->k, 1, c->wx, c->wxy, restrict_w(ry, lo + nW, ghi));
+    }
+    launch_weno_sweep(c->k, W, d == 3 ? c->wxy : c->wx, c->w, z0);
+    launch_weno_sweep(c->k, W, d == 3 ? c->wxy : c->wx, c->w, z1);
+  }
+  c->guess_ready = false;
+  return ADER_OK;
+}
+
 ader_status ader_step_io(ader_ctx* c, const double* in_host, double* out_host, double t_end, ader_step_report* rep) {
   if (!c || !out_host) return ADER_ERR_ARG;
   const auto w0 = std::chrono::steady_clock::now();
   if (c->loopback) return fail(c, ADER_ERR_ARG, "group contexts step through ader_debug_group_step");
   if (c->amr) return fail(c, ADER_ERR_UNSUPPORTED, "ader_step_io: uniform grids only (use ader_step + ader_get_cells)");
   const Box b = owned(c);
-  if (in_host) {
+  const bool pipe = in_host && pipelined_head_ok(c);
+  if (in_host && !pipe) {
     CK(cudaMemcpyAsync(c->stage, in_host, (size_t)b.count() * c->nv * sizeof(double), cudaMemcpyHostToDevice,
                        c->k.stream));
     launch_scatter(c->k, c->u, c->nv, b, c->stage);
@@ -1430,7 +1564,15 @@ ader_status ader_step_io(ader_ctx* c, const double* in_host, double* out_host, d
   st = read_state(c);
   if (st != ADER_OK) return st;
   const long long steps0 = c->hst->steps;
-  if (c->t < t_end) {
+  if (pipe) {   // the copy-in overlaps the ghost fill and sweeps of the slabs already in
+    st = head_from_host(c, in_host);
+    if (st == ADER_OK && c->t < t_end) st = enqueue_step(c, t_end, out_host, true);
+    else if (st == ADER_OK) {
+      launch_gather(c->k, c->u, c->nv, b, c->stage);
+      CK(cudaMemcpyAsync(out_host, c->stage, (size_t)b.count() * c->nv * sizeof(double), cudaMemcpyDeviceToHost,
+                         c->k.stream));
+    }
+  } else if (c->t < t_end) {
     if (c->has_exact) st = refresh_exact(c);
     if (st == ADER_OK) st = enqueue_step(c, t_end, out_host);
   } else {

@@ -1,6 +1,8 @@
-"""ader_step_io (the e2e path: state in from the host, one macro step, state out
-with the copy-out overlapped by the slab-wise face fluxes / update) gives
-bitwise the state of ader_set_cells + ader_step(1) + ader_get_state."""
+"""ader_step_io (the e2e path: state in from the host — in slabs along the last
+axis overlapped with the ghost fill / WENO sweeps of the slabs already in —
+one macro step, state out with the copy-out overlapped by the slab-wise face
+fluxes / update) gives bitwise the state of ader_set_cells + ader_step(1) +
+ader_get_state."""
 import numpy as np
 import pytest
 import torch
@@ -19,12 +21,19 @@ CASES = {
                                cfl=0.3), W.explosion(3)),
     "ot_mhd_M3": (dict(dim=2, degree=3, n0=(40, 17), lo=(0, 0), hi=(2 * np.pi, 2 * np.pi), bc=(0,) * 6, system=1,
                        gamma=5 / 3, ch=2.0, cfl=0.5), W.orszag_tang()),
+    # slab-pipelined copy-in (n along the last axis >= 16): walls and periodic in 3D
+    "explosion3d_walls_tall": (dict(dim=3, degree=2, n0=(10, 9, 33), lo=(0,) * 3, hi=(1,) * 3, bc=(2, 1, 2, 1, 2, 1),
+                                    cfl=0.3), W.explosion(3)),
+    "random3d_periodic": (dict(dim=3, degree=2, n0=(12, 11, 24), lo=(0,) * 3, hi=(1,) * 3, bc=(0,) * 6, cfl=0.3),
+                          W.random_smooth(3)),
 }
 
 
 @pytest.mark.parametrize("name", list(CASES))
 @pytest.mark.parametrize("fuse", [0, 1])
-def test_step_io_equals_set_step_get(name, fuse):
+@pytest.mark.parametrize("pipeline", ["0", "1"])
+def test_step_io_equals_set_step_get(name, fuse, pipeline, monkeypatch):
+    monkeypatch.setenv("ADER_STEP_IO_PIPELINE", pipeline)
     kw, ic = CASES[name]
     a = ader.Solver(ader.make_config(device=0, fuse_pred_flux=fuse, **kw))
     b = ader.Solver(ader.make_config(device=0, fuse_pred_flux=fuse, **kw))
