@@ -14,6 +14,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
 #include <thread>
 #include <vector>
 
@@ -121,21 +124,92 @@ namespace {
 
 double now_s() { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); }
 
-// host threads for the O(cells) scans of the tree mirror (one below 256k ids)
+// Persistent host worker threads for the O(cells) scans of the tree mirror
+// (spawning std::threads per scan cost more than the scans below 256k ids).
+class HostPool {
+ public:
+  static HostPool& get() {
+    static HostPool p;
+    return p;
+  }
+  int size() const { return (int)workers_.size() + 1; }
+  // fn(t) for t in [0, T), t = 0 on the calling thread; returns when all are done
+  void run(int T, const std::function<void(int)>& fn) {
+    T = std::max(1, std::min(T, size()));
+    if (T == 1) { fn(0); return; }
+    {
+      std::lock_guard<std::mutex> g(m_);
+      job_ = &fn;
+      njob_ = T;
+      pending_ = T - 1;
+      ++gen_;
+    }
+    cv_.notify_all();
+    fn(0);
+    std::unique_lock<std::mutex> g(m_);
+    done_.wait(g, [&] { return pending_ == 0; });
+    job_ = nullptr;
+  }
+  ~HostPool() {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      stop_ = true;
+      ++gen_;
+    }
+    cv_.notify_all();
+    for (auto& t : workers_) t.join();
+  }
+
+ private:
+  HostPool() {
+    const unsigned hc = std::thread::hardware_concurrency();
+    const int n = (int)std::max(1u, std::min(8u, hc ? hc : 1u)) - 1;
+    for (int w = 0; w < n; ++w) workers_.emplace_back([this, w] { loop(w + 1); });
+  }
+  void loop(int id) {
+    long seen = 0;
+    for (;;) {
+      const std::function<void(int)>* job;
+      int nj;
+      {
+        std::unique_lock<std::mutex> g(m_);
+        cv_.wait(g, [&] { return gen_ != seen; });
+        seen = gen_;
+        if (stop_) return;
+        job = job_;
+        nj = njob_;
+      }
+      if (job && id < nj) {
+        (*job)(id);
+        std::lock_guard<std::mutex> g(m_);
+        if (--pending_ == 0) done_.notify_all();
+      }
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex m_;
+  std::condition_variable cv_, done_;
+  const std::function<void(int)>* job_ = nullptr;
+  int njob_ = 0, pending_ = 0;
+  long gen_ = 0;
+  bool stop_ = false;
+};
+
+// host threads for a scan of n ids (one below 16k ids; ADER_HOST_THREADS caps it, A/B)
 int host_threads(int n) {
-  if (n < (1 << 18)) return 1;
-  const unsigned hc = std::thread::hardware_concurrency();
-  return (int)std::max(1u, std::min(8u, hc ? hc : 1u));
+  static const int cap = [] {
+    const char* e = std::getenv("ADER_HOST_THREADS");
+    return e ? std::max(1, std::atoi(e)) : 64;
+  }();
+  if (n < (1 << 14) || cap == 1) return 1;
+  return std::min(cap, HostPool::get().size());
 }
 
 // fn(t, i0, i1) on T contiguous chunks of [0, n), chunk 0 on the calling thread
 template <class F>
 void parallel_chunks(int n, int T, F fn) {
-  std::vector<std::thread> th;
-  for (int t = 1; t < T; ++t)
-    th.emplace_back(fn, t, (int)((long long)n * t / T), (int)((long long)n * (t + 1) / T));
-  fn(0, 0, (int)((long long)n / T));
-  for (auto& x : th) x.join();
+  if (T <= 1) { fn(0, 0, n); return; }
+  HostPool::get().run(T, [&](int t) { fn(t, (int)((long long)n * t / T), (int)((long long)n * (t + 1) / T)); });
 }
 
 double lagrange(const DevTables& T, int N, int p, double x) {
@@ -460,19 +534,35 @@ void virtually_refine(AmrState* A, int v, bool t0) {
 }
 
 void closure(AmrState* A, bool t0) {
+  // the virtual mothers (found by a threaded scan in id order; the ones the
+  // closure creates are appended and visited in the same pass): rules 4-5 act
+  // only around them.  Passes repeat until none acts (least fixed point, R17).
   int nb[26];
+  const int nu = (int)A->cells.size(), T = host_threads(nu);
+  std::vector<std::vector<int>> part(T);
+  parallel_chunks(nu, T, [&](int t, int i0, int i1) {
+    for (int i = i0; i < i1; ++i)
+      if (A->cells[i].alive && A->cells[i].status == -1) part[t].push_back(i);
+  });
+  std::vector<int> vm;
+  for (const auto& P : part) vm.insert(vm.end(), P.begin(), P.end());
   bool changed = true;
   while (changed) {
     changed = false;
-    const int nu = (int)A->cells.size();
-    for (int i = 0; i < nu; ++i) {
+    for (size_t j = 0; j < vm.size(); ++j) {
+      const int i = vm[j];
       if (!A->cells[i].alive || A->cells[i].status != -1) continue;
       const int k = voronoi(A, i, nb);
-      for (int j = 0; j < k; ++j) {
-        const int v = nb[j];
+      for (int q = 0; q < k; ++q) {
+        const int v = nb[q];
         if (v < 0 || A->cells[v].child >= 0) continue;
         if (A->cells[v].status == 0) { virtually_refine(A, v, t0); changed = true; }
-        else if (A->cells[v].status == 1) { refine_cell(A, A->cells[v].mother, t0); changed = true; }
+        else if (A->cells[v].status == 1) {
+          const int m = A->cells[v].mother;
+          refine_cell(A, m, t0);
+          vm.push_back(m);
+          changed = true;
+        }
       }
     }
   }
@@ -652,20 +742,37 @@ ader_status upload_topology(AmrState* A, std::string& err) {
   A->dirty.clear();
   A->all_dirty = false;
   const int ncand = full ? nu : (int)cand.size();
-  for (int ci = 0; ci < ncand; ++ci) {
-    const int i = full ? ci : cand[ci];
-    if (i >= nu) continue;
-    const HCell& C = A->cells[i];
-    HCell& P = A->mirror[i];
-    const bool same_pos = C.alive == P.alive && C.level == P.level && C.idx[0] == P.idx[0] && C.idx[1] == P.idx[1] &&
-                          C.idx[2] == P.idx[2];
-    const bool same = same_pos && C.status == P.status && C.mother == P.mother && C.child == P.child;
-    if (same && (C.alive || !P.alive)) continue;
-    const long long m[8] = {i, C.level, C.alive ? C.status : 9, C.mother, C.child, C.idx[0], C.idx[1], C.idx[2]};
-    meta.insert(meta.end(), m, m + 8);
-    if (P.alive && (!C.alive || !same_pos)) { clears.push_back(P.level); clears.push_back(lin(A, P.level, P.idx)); clears.push_back(-1); }
-    if (C.alive && (!P.alive || !same_pos)) { sets.push_back(C.level); sets.push_back(lin(A, C.level, C.idx)); sets.push_back(i); }
-    P = C;
+  // compare the candidates with the device mirror (threaded; per-chunk records
+  // concatenated in chunk order = the serial order)
+  struct Diff { std::vector<long long> meta, clears, sets; };
+  const int TD = host_threads(ncand);
+  std::vector<Diff> dp(TD);
+  parallel_chunks(ncand, TD, [&](int t, int c0, int c1) {
+    Diff& D = dp[t];
+    for (int ci = c0; ci < c1; ++ci) {
+      const int i = full ? ci : cand[ci];
+      if (i >= nu) continue;
+      const HCell& C = A->cells[i];
+      HCell& P = A->mirror[i];
+      const bool same_pos = C.alive == P.alive && C.level == P.level && C.idx[0] == P.idx[0] &&
+                            C.idx[1] == P.idx[1] && C.idx[2] == P.idx[2];
+      const bool same = same_pos && C.status == P.status && C.mother == P.mother && C.child == P.child;
+      if (same && (C.alive || !P.alive)) continue;
+      const long long m[8] = {i, C.level, C.alive ? C.status : 9, C.mother, C.child, C.idx[0], C.idx[1], C.idx[2]};
+      D.meta.insert(D.meta.end(), m, m + 8);
+      if (P.alive && (!C.alive || !same_pos)) {
+        D.clears.push_back(P.level); D.clears.push_back(lin(A, P.level, P.idx)); D.clears.push_back(-1);
+      }
+      if (C.alive && (!P.alive || !same_pos)) {
+        D.sets.push_back(C.level); D.sets.push_back(lin(A, C.level, C.idx)); D.sets.push_back(i);
+      }
+      P = C;
+    }
+  });
+  for (const Diff& D : dp) {
+    meta.insert(meta.end(), D.meta.begin(), D.meta.end());
+    clears.insert(clears.end(), D.clears.begin(), D.clears.end());
+    sets.insert(sets.end(), D.sets.begin(), D.sets.end());
   }
   A->tm_u[3] += now_s() - w0;
   for (int l = 0; l <= A->lmax; ++l) {
@@ -1108,19 +1215,25 @@ ader_status adapt_apply(AmrState* A, bool t0, const std::vector<double>& chi, st
   for (auto& c : A->cells) c.isnew = false;
   const int nu = (int)A->cells.size();
   std::vector<char> mark(nu, 0);
-  parallel_chunks(nu, host_threads(nu), [&](int, int i0, int i1) {
-    for (int i = i0; i < i1; ++i)
-      mark[i] = A->cells[i].alive && A->cells[i].status == 0 && A->cells[i].level < A->lmax && chi[i] > A->cfg.chi_ref;
+  // refinement marks, and how close any strict comparison of P:622-624 came to
+  // flipping: min over the active cells of the relative distance of chi to
+  // chi_ref and chi_rec (ader_step_report.min_threshold_margin; the oracle
+  // computes the same; a min is exact in any order)
+  const int TM = host_threads(nu);
+  std::vector<double> mpart(TM, 1e300);
+  parallel_chunks(nu, TM, [&](int t, int i0, int i1) {
+    double mm = 1e300;
+    for (int i = i0; i < i1; ++i) {
+      const HCell& C = A->cells[i];
+      if (!C.alive || C.status != 0) continue;
+      mark[i] = C.level < A->lmax && chi[i] > A->cfg.chi_ref;
+      const double m1 = std::fabs(chi[i] - A->cfg.chi_ref) / A->cfg.chi_ref;
+      const double m2 = std::fabs(chi[i] - A->cfg.chi_rec) / A->cfg.chi_rec;
+      mm = std::min(mm, std::min(m1, m2));
+    }
+    mpart[t] = mm;
   });
-  // how close any strict comparison of P:622-624 came to flipping: min over the
-  // active cells of the relative distance of chi to chi_ref and chi_rec
-  // (ader_step_report.min_threshold_margin; the oracle computes the same)
-  for (int i = 0; i < nu; ++i) {
-    if (!A->cells[i].alive || A->cells[i].status != 0) continue;
-    const double m1 = std::fabs(chi[i] - A->cfg.chi_ref) / A->cfg.chi_ref;
-    const double m2 = std::fabs(chi[i] - A->cfg.chi_rec) / A->cfg.chi_rec;
-    A->margin = std::min(A->margin, std::min(m1, m2));
-  }
+  for (double m : mpart) A->margin = std::min(A->margin, m);
   for (int i = 0; i < nu; ++i)
     if (mark[i]) refine_cell(A, i, t0);
   A->tm_a[0] += now_s() - w0; w0 = now_s();
@@ -1146,8 +1259,10 @@ ader_status adapt_apply(AmrState* A, bool t0, const std::vector<double>& chi, st
         cand[i] = ok;
       }
     });
-    bool any_cand = false;
-    for (int i = 0; i < nu2 && !any_cand; ++i) any_cand = cand[i];
+    std::vector<int> cl;   // candidate ids, ascending
+    for (int i = 0; i < nu2; ++i)
+      if (cand[i]) cl.push_back(i);
+    bool any_cand = !cl.empty();
     while (any_cand) {
       // tentative simultaneous rule 7, then closure; reverted candidates retry
       // (the changes are journaled and undone in reverse order on a revert)
@@ -1157,18 +1272,17 @@ ader_status adapt_apply(AmrState* A, bool t0, const std::vector<double>& chi, st
       A->jon = true;
       A->jcells.clear();
       A->jmap.clear();
-      std::vector<char> destroy(nu2, 0);
-      for (int i = 0; i < nu2; ++i) {
-        if (!cand[i]) continue;
-        const int k = voronoi(A, i, nb);
+      std::vector<char> destroy(cl.size(), 0);
+      for (size_t j = 0; j < cl.size(); ++j) {
+        const int k = voronoi(A, cl[j], nb);
         bool busy = false;
-        for (int j = 0; j < k && !busy; ++j) busy = nb[j] >= 0 && A->cells[nb[j]].status == -1;
-        destroy[i] = !busy;
+        for (int q = 0; q < k && !busy; ++q) busy = nb[q] >= 0 && A->cells[nb[q]].status == -1;
+        destroy[j] = !busy;
       }
       std::vector<int> fr;
-      for (int i = 0; i < nu2; ++i) {
-        if (!cand[i]) continue;
-        if (destroy[i]) destroy_children(A, i, &fr);
+      for (size_t j = 0; j < cl.size(); ++j) {
+        const int i = cl[j];
+        if (destroy[j]) destroy_children(A, i, &fr);
         else
           for (int q = 0; q < A->rd; ++q) wcell(A, A->cells[i].child + q).status = 1;
         wcell(A, i).status = 0;
@@ -1176,12 +1290,14 @@ ader_status adapt_apply(AmrState* A, bool t0, const std::vector<double>& chi, st
       closure(A, false);
       A->jon = false;
       bool reverted = false;
-      for (int i = 0; i < nu2; ++i)
-        if (cand[i] && A->cells[i].status == -1) { cand[i] = 0; reverted = true; }
+      std::vector<int> kept;
+      for (int i : cl) {
+        if (A->cells[i].status == -1) { cand[i] = 0; reverted = true; }
+        else kept.push_back(i);
+      }
       if (!reverted) {
         freed.insert(freed.end(), fr.begin(), fr.end());
-        for (int i = 0; i < nu2; ++i)
-          if (cand[i]) coarsened.push_back(i);
+        coarsened.insert(coarsened.end(), cl.begin(), cl.end());
         break;
       }
       for (size_t j = A->jmap.size(); j-- > 0;) A->hmap[A->jmap[j].first.first][A->jmap[j].first.second] = A->jmap[j].second;
@@ -1190,6 +1306,7 @@ ader_status adapt_apply(AmrState* A, bool t0, const std::vector<double>& chi, st
       A->cells.resize(snap_size);
       A->free_blocks = snap_free;
       A->inits.resize(snap_inits);
+      cl.swap(kept);   // reverted candidates retry no more
     }
   }
   A->tm_a[2] += now_s() - w0; w0 = now_s();
