@@ -3,7 +3,7 @@
 //   k_amr_project   projection of the mother's q_h into virtual children
 //   k_amr_weno      dimension-by-dimension WENO of a listed active cell
 //   k_predictor     (kernels.cu, list mode) space-time predictor
-//   k_amr_flux_update_w face fluxes incl. coarse-fine faces with flux memory
+//   k_amr_flux_w + k_amr_update_w face fluxes incl. coarse-fine faces with flux memory, update
 //                   (eqn.memory.sum) + one-step update (eq:finite_vol)
 //   k_amr_indicator refinement indicator, reading R14 of eqn.indicator,
 //                   evaluated without FMA contraction (bit-exact flags, H2)
@@ -301,11 +301,13 @@ __device__ __forceinline__ bool amr_cell_face_w(const AmrDevView& V, int c, bool
   else {
     nb = amr_lookup(V, l, ix[0], ix[1], ix[2]);
     const int st = nb >= 0 ? V.status[nb] : 9;
-    if (st == 0) {
+    if (st == 0 && side) {
+      kind = 8;   // computed once, as the lower face of the neighbour (k_amr_update_w reads it there)
+    } else if (st == 0) {
       const double* qn = V.q + wq_row(V, nb) * NV * NST;
       kind = 0;
-      qL = side ? qc : qn;
-      qR = side ? qn : qc;
+      qL = qn;
+      qR = qc;
     } else if (st == 1) {
       // coarse-fine: the virtual neighbour scales its mother's q_h down
       const double* qK = V.q + wq_row(V, V.mother[nb]) * NV * NST;
@@ -343,7 +345,7 @@ __device__ __forceinline__ bool amr_cell_face_w(const AmrDevView& V, int c, bool
         mm[p] = 0.0;
       }
       Fout[p] = acc / (double)V.rd;
-    } else if (kind >= 0) {
+    } else if (kind >= 0 && kind < 8) {
       double acc = rb[p][0];
 #pragma unroll
       for (int j = 1; j < NS; ++j) acc += rb[p][j];
@@ -355,24 +357,28 @@ __device__ __forceinline__ bool amr_cell_face_w(const AmrDevView& V, int c, bool
   return ok;
 }
 
+// Face fluxes of the listed (active) cells: every lower face and the upper
+// faces no active same-level neighbour computes (boundaries, walls,
+// coarse-fine faces, faces against virtual mothers), each into the cell's own
+// row of the flux-memory array (unused by active cells: memory lives on
+// virtual children); a face between two active cells of a level is computed
+// once, by its upper cell, with the same (lower, upper) traces either way.
 template <int D, int M, int SYS, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32) k_amr_flux_update_w(AmrDevView V, const __grid_constant__ SubTables S,
-                                                                   const int* __restrict__ list, int n, int m,
-                                                                   double dtdx0, double dtdx1, double dtdx2,
-                                                                   double gamma, double ch, DevCounters* cnt,
-                                                                   const __grid_constant__ DevTables T) {
+__global__ void __launch_bounds__(WARPS * 32) k_amr_flux_w(AmrDevView V, const __grid_constant__ SubTables S,
+                                                            const int* __restrict__ list, int n, int m,
+                                                            double gamma, double ch, DevCounters* cnt,
+                                                            const __grid_constant__ DevTables T) {
   constexpr int NV = Phys<SYS, D>::NV, NS = ipow_a(M + 1, D);
   constexpr int G = (NS <= 8) ? 8 : (NS <= 16 ? 16 : 32);
   constexpr int CPW = 32 / G;
   __shared__ double red[WARPS * CPW][NV][G + 1];
-  __shared__ double Fs[WARPS * CPW][6][NV];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int p = lane & (G - 1), grp = warp * CPW + lane / G;
   const int i = (blockIdx.x * WARPS + warp) * CPW + lane / G;
   const bool valid = i < n;
   const int c = list[valid ? i : 0];
   double(*rb)[G + 1] = red[grp];
-  double* F = &Fs[grp][0][0];
+  double* F = V.mem + (long long)c * 6 * NV;
   bool ok = true;
   ok &= amr_cell_face_w<D, M, SYS, 0, G>(V, c, valid, 0, m, p, gamma, ch, T, S, rb, F + 0 * NV);
   ok &= amr_cell_face_w<D, M, SYS, 0, G>(V, c, valid, 1, m, p, gamma, ch, T, S, rb, F + 1 * NV);
@@ -383,14 +389,36 @@ __global__ void __launch_bounds__(WARPS * 32) k_amr_flux_update_w(AmrDevView V, 
     ok &= amr_cell_face_w<D, M, SYS, 2, G>(V, c, valid, 1, m, p, gamma, ch, T, S, rb, F + 5 * NV);
   }
   if (valid && !ok && (!V.own || V.own[c])) amr_error(cnt, 1, 2, c);   // multi-rank: band cells' errors do not count
-  __syncwarp();
-  if (valid && p < NV) {
-    const double dtdx[3] = {dtdx0, dtdx1, dtdx2};
-    double uu = V.u[(long long)c * NV + p];
+}
+
+// FV update (eq:finite_vol @ P:147-152) of the listed cells from the face
+// fluxes k_amr_flux_w left in the flux-memory rows: the lower face of each
+// direction from the cell's row, the upper face from the row of the active
+// same-level neighbour (its lower face) or else from the cell's own row.
+template <int D, int SYS>
+__global__ void __launch_bounds__(256) k_amr_update_w(AmrDevView V, const int* __restrict__ list, int n,
+                                                      double dtdx0, double dtdx1, double dtdx2) {
+  constexpr int NV = Phys<SYS, D>::NV;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n * NV) return;
+  const int c = list[i / NV], p = i % NV;
+  const int l = V.level[c];
+  const double dtdx[3] = {dtdx0, dtdx1, dtdx2};
+  double uu = V.u[(long long)c * NV + p];
 #pragma unroll
-    for (int d = 0; d < D; ++d) uu = uu - dtdx[d] * (F[(2 * d + 1) * NV + p] - F[(2 * d) * NV + p]);
-    V.u[(long long)c * NV + p] = uu;
+  for (int d = 0; d < D; ++d) {
+    long long ix[3] = {V.idx[(long long)c * 3], V.idx[(long long)c * 3 + 1], V.idx[(long long)c * 3 + 2]};
+    ix[d] += 1;
+    const bool out = ix[d] >= V.n[l][d];
+    long long hi = (long long)c * 6 + 2 * d + 1;
+    if (!(out && (V.bc[2 * d + 1] == ADER_BC_TRANSMISSIVE || V.bc[2 * d + 1] == ADER_BC_REFLECTIVE))) {
+      const int nb = amr_lookup(V, l, ix[0], ix[1], ix[2]);
+      if (nb >= 0 && V.status[nb] == 0) hi = (long long)nb * 6 + 2 * d;
+    }
+    const double fhi = V.mem[hi * NV + p], flo = V.mem[((long long)c * 6 + 2 * d) * NV + p];
+    uu = uu - dtdx[d] * (fhi - flo);
   }
+  V.u[(long long)c * NV + p] = uu;
 }
 
 // ---------------------------------------------------------------------------
@@ -640,8 +668,11 @@ void amr_launch_flux_update(const KCtx& k, const AmrDevView& v, const SubTables&
     constexpr int NS = ipow_a(M + 1, D);
     constexpr int CPW = 32 / ((NS <= 8) ? 8 : (NS <= 16 ? 16 : 32));
     constexpr int WARPS = 4;
-    k_amr_flux_update_w<D, M, SYS, WARPS><<<gsz(n, WARPS * CPW), WARPS * 32, 0, k.stream>>>(
-        v, st, list, n, m, dtdx[0], dtdx[1], dtdx[2], k.gamma, k.ch, cnt, k.tab);
+    k_amr_flux_w<D, M, SYS, WARPS><<<gsz(n, WARPS * CPW), WARPS * 32, 0, k.stream>>>(v, st, list, n, m, k.gamma,
+                                                                                      k.ch, cnt, k.tab);
+    cl(k);
+    k_amr_update_w<D, SYS><<<gsz((long long)n * Phys<SYS, D>::NV, 256), 256, 0, k.stream>>>(v, list, n, dtdx[0],
+                                                                                           dtdx[1], dtdx[2]);
   });
 }
 
