@@ -169,6 +169,10 @@ struct ader_ctx {
   KCtx k{};
   cudaStream_t own_stream = nullptr;
   cudaStream_t io_stream = nullptr;            // ader_step_io: device-to-host copies of finished slabs
+  cudaGraphExec_t step_graph = nullptr;        // one uniform macro step captured as a CUDA graph
+  bool use_graphs = true;                      // ADER_NO_GRAPHS=1 at ader_create: direct launches (A/B)
+  double graph_t_end = 0.0;                    // the t_end baked into it (k_step_dt's clip)
+  long long graph_launches = 0;                // kernels per replay (launch accounting)
   std::vector<cudaEvent_t> io_ev;              // one per slab (created on first use)
   double *u = nullptr, *wx = nullptr, *wxy = nullptr, *w = nullptr, *q = nullptr, *F = nullptr;
   double *stage = nullptr;                     // compact staging buffer (set/get)
@@ -741,6 +745,7 @@ void free_ctx(ader_ctx* c) {
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   if (c->comm) g_nccl.CommDestroy(c->comm);
   delete c->hostcomm;
+  if (c->step_graph) cudaGraphExecDestroy(c->step_graph);
   for (cudaEvent_t e : c->io_ev) cudaEventDestroy(e);
   if (c->io_stream) cudaStreamDestroy(c->io_stream);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
@@ -1031,6 +1036,10 @@ static ader_status create_impl(const ader_config* cfg, ader_ctx** out, bool loop
   }
   c->halo_cap = cap * c->nv;
   c->loopback = loopback;
+  {
+    const char* e = std::getenv("ADER_NO_GRAPHS");
+    c->use_graphs = !(e && e[0] == '1');
+  }
   if (cfg->world_size > 1) {
     for (int i = 0; i < 2 * c->d; ++i) {
       CK(alloc(&c->sendb[i], (size_t)c->halo_cap));
@@ -1411,6 +1420,43 @@ ader_status dt_from_speed(ader_ctx* c, double speed, double t_end, double* dt) {
 }
 }  // namespace
 
+// One uniform macro step as a CUDA graph (the steady state: CFL speed from the
+// previous update, no host work between steps), replayed for every step of a
+// chunk: the ~20 kernels of a step (ghost fills, WENO sweeps, dt, predictor,
+// fluxes, update) launch as one graph, which removes the per-launch host cost
+// that bounds small grids.  Used when nothing needs the host per step: one
+// rank, no exact-solution sides, profiling off, not the fused WENO+predictor
+// experiment.  Re-captured when t_end changes (k_step_dt clips against it).
+bool graphs_ok(const ader_ctx* c) {
+  return c->use_graphs && !c->prof && c->cfg.world_size == 1 && !c->loopback && !c->has_exact && !fused_weno_pred(c) &&
+         c->cfg.pred_guess == 0 && c->speed_valid;
+}
+
+ader_status enqueue_step_graph(ader_ctx* c, double t_end) {
+  if (c->step_graph && c->graph_t_end != t_end) {
+    cudaGraphExecDestroy(c->step_graph);
+    c->step_graph = nullptr;
+  }
+  if (!c->step_graph) {
+    const long long l0 = c->launches;
+    cudaGraph_t g = nullptr;
+    CK(cudaStreamBeginCapture(c->k.stream, cudaStreamCaptureModeThreadLocal));
+    ader_status st = enqueue_step(c, t_end);
+    cudaError_t e = cudaStreamEndCapture(c->k.stream, &g);
+    if (st != ADER_OK) { if (g) cudaGraphDestroy(g); return st; }
+    CK(e);
+    e = cudaGraphInstantiate(&c->step_graph, g, 0);
+    cudaGraphDestroy(g);
+    CK(e);
+    c->graph_t_end = t_end;
+    c->graph_launches = c->launches - l0;
+    c->launches = l0;
+  }
+  CK(cudaGraphLaunch(c->step_graph, c->k.stream));
+  c->launches += c->graph_launches;
+  return ADER_OK;
+}
+
 // Head of an ader_step_io step with a new host state (one rank, periodic /
 // transmissive / reflective sides): the state arrives in K slabs along the last
 // axis W on the copy stream, and as each slab lands the compute stream
@@ -1619,7 +1665,8 @@ ader_status ader_step(ader_ctx* c, double t_end, int64_t max_macro_steps, ader_s
     const int64_t nstep = std::min<int64_t>(chunk, max_macro_steps - enq);
     const auto h0 = std::chrono::steady_clock::now();
     if (c->has_exact) st = refresh_exact(c);
-    for (int64_t i = 0; i < nstep && st == ADER_OK; ++i) st = enqueue_step(c, t_end);
+    for (int64_t i = 0; i < nstep && st == ADER_OK; ++i)
+      st = graphs_ok(c) ? enqueue_step_graph(c, t_end) : enqueue_step(c, t_end);
     if (st != ADER_OK) break;
     enq += nstep;
     const auto h1 = std::chrono::steady_clock::now();

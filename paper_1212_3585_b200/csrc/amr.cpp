@@ -1385,25 +1385,53 @@ ader_status rebalance(const Group& G, std::string& err) {
   if (!rcb_partition(A0->d, A0->n[0], w.data(), W, nr.lo, nr.hi)) return ADER_OK;
   const double cur = imbalance(A0, A0->ranks, w), nxt = imbalance(A0, nr, w);
   if (!(cur > 1.05 && nxt * 1.02 < cur)) return ADER_OK;
+  // The cells whose level-0 ancestor changes owner move from the old to the
+  // new owner (one grouped point-to-point of their averages, ids ascending
+  // on both sides); then every rank's new compute and present sets are built
+  // and one exchange of every level brings the present copies up to date.  At
+  // synchronized time a cell's only state is its average (the flux memory is
+  // cleared, the WENO / predictor dofs are recomputed every step).
   const size_t nu = A0->cells.size(), nv = (size_t)A0->nv;
-  std::vector<double*> buf(G.size(), nullptr), tmp(G.size(), nullptr);
   ader_status s = ADER_OK;
-  auto cleanup = [&]() {
-    for (AmrState* A : G) cudaStreamSynchronize(A->k->stream);
+  auto owner_in = [&](const AmrState* A, const AmrRanks& R, const HCell& C) {
+    long long a[3];
+    ancestor0(A, C, a);
+    for (int p = 0; p < R.world; ++p) {
+      bool in = true;
+      for (int k = 0; k < A->d && in; ++k) in = a[k] >= R.lo[p][k] && a[k] < R.hi[p][k];
+      if (in) return p;
+    }
+    return -1;
   };
-  auto ids_of = [&](const AmrState* A, const std::vector<char>& mask) {
-    std::vector<int> ids;
-    for (size_t i = 0; i < nu; ++i)
-      if (A->cells[i].alive && mask[i]) ids.push_back((int)i);
-    return ids;
-  };
-  // 1. owners' rows (old blocks) into zeroed per-id arrays
+  struct Move { std::vector<int> sids, rids; std::vector<long long> soff, roff; };
+  std::vector<Move> mv(G.size());
   for (size_t g = 0; g < G.size() && s == ADER_OK; ++g) {
     AmrState* A = G[g];
-    cudaStream_t sm = A->k->stream;
-    if (A->rb_cap < nu * nv) {   // persistent, grown 2x (no allocation per rebalance)
-      const size_t cap = std::max(nu * nv, 2 * A->rb_cap);
-      cudaStreamSynchronize(sm);
+    const int me = A->ranks.rank;
+    std::vector<std::vector<int>> snd(W), rcv(W);
+    for (size_t i = 0; i < nu; ++i) {
+      const HCell& C = A->cells[i];
+      if (!C.alive) continue;   // virtual cells too: the new owner exports them (ader_get_cells)
+      const int po = owner_in(A, A->ranks, C), pn = owner_in(A, nr, C);
+      if (po == pn) continue;
+      if (po == me) snd[pn].push_back((int)i);
+      if (pn == me) rcv[po].push_back((int)i);
+    }
+    Move& M = mv[g];
+    M.soff.assign(W + 1, 0);
+    M.roff.assign(W + 1, 0);
+    for (int p = 0; p < W; ++p) {
+      M.soff[p] = (long long)M.sids.size();
+      M.sids.insert(M.sids.end(), snd[p].begin(), snd[p].end());
+      M.roff[p] = (long long)M.rids.size();
+      M.rids.insert(M.rids.end(), rcv[p].begin(), rcv[p].end());
+    }
+    M.soff[W] = (long long)M.sids.size();
+    M.roff[W] = (long long)M.rids.size();
+    const size_t need = std::max(M.sids.size(), M.rids.size()) * nv + 1;
+    if (A->rb_cap < need) {   // persistent, grown 2x
+      const size_t cap = std::max(need, 2 * A->rb_cap);
+      cudaStreamSynchronize(A->k->stream);
       if (A->rb_buf) cudaFree(A->rb_buf);
       if (A->rb_tmp) cudaFree(A->rb_tmp);
       A->rb_buf = A->rb_tmp = nullptr;
@@ -1412,38 +1440,60 @@ ader_status rebalance(const Group& G, std::string& err) {
           cudaMalloc(&A->rb_tmp, sizeof(double) * cap) != cudaSuccess) { err = "cudaMalloc (rebalance)"; s = ADER_ERR_CUDA; break; }
       A->rb_cap = cap;
     }
-    buf[g] = A->rb_buf;
-    tmp[g] = A->rb_tmp;
-    cudaMemsetAsync(buf[g], 0, sizeof(double) * nu * nv, sm);
-    const std::vector<int> ids = ids_of(A, A->own);
+  }
+  // device id lists of the moves (one upload per rank), then gather the sent rows
+  std::vector<const int*> dsids(G.size(), nullptr), drids(G.size(), nullptr);
+  for (size_t g = 0; g < G.size() && s == ADER_OK; ++g) {
+    AmrState* A = G[g];
     Uploader up{A, {}};
-    const size_t oi = up.add(ids.data(), sizeof(int) * ids.size());
+    const size_t os = up.add(mv[g].sids.data(), sizeof(int) * mv[g].sids.size());
+    const size_t orr = up.add(mv[g].rids.data(), sizeof(int) * mv[g].rids.size());
     s = up.run(err);
     if (s != ADER_OK) break;
-    const int* dids = (const int*)(A->dscratch + oi);
-    amr_launch_rows_gather(*A->k, A->V.u, dids, (int)ids.size(), A->nv, tmp[g]);
-    amr_launch_rows_scatter(*A->k, buf[g], dids, (int)ids.size(), A->nv, tmp[g]);
+    dsids[g] = (const int*)(A->dscratch + os);
+    drids[g] = (const int*)(A->dscratch + orr);
+    amr_launch_rows_gather(*A->k, A->V.u, dsids[g], (int)mv[g].sids.size(), A->nv, A->rb_buf);
   }
-  // 2. sum over the ranks
-  if (s == ADER_OK && G.size() == 1) {
-    s = A0->comm.sum(A0->comm.ctx, buf[0], nu * nv, A0->k->stream);
-    if (s != ADER_OK) err = "allreduce(sum) of the migrated averages failed";
+  if (s == ADER_OK && G.size() > 1) {
+    for (AmrState* A : G) cudaStreamSynchronize(A->k->stream);
+    for (size_t g = 0; g < G.size() && s == ADER_OK; ++g) {
+      AmrState* A = G[g];
+      const int me = A->ranks.rank;
+      for (int p = 0; p < W; ++p) {
+        if (p == me) continue;
+        const long long n = mv[g].roff[p + 1] - mv[g].roff[p];
+        if (n != mv[p].soff[me + 1] - mv[p].soff[me]) { err = "rebalance plans disagree"; s = ADER_ERR_SOLVER; break; }
+        if (n && cudaMemcpyAsync(A->rb_tmp + mv[g].roff[p] * nv, G[p]->rb_buf + mv[p].soff[me] * nv,
+                                 sizeof(double) * n * nv, cudaMemcpyDeviceToDevice, A->k->stream) != cudaSuccess) {
+          err = "rebalance copy"; s = ADER_ERR_CUDA; break;
+        }
+      }
+    }
+    for (AmrState* A : G) cudaStreamSynchronize(A->k->stream);
   } else if (s == ADER_OK) {
-    std::vector<double> tot(nu * nv, 0.0), part(nu * nv);
-    for (size_t g = 0; g < G.size() && s == ADER_OK; ++g) {
-      cudaStream_t sm = G[g]->k->stream;
-      if (cudaMemcpyAsync(part.data(), buf[g], sizeof(double) * nu * nv, cudaMemcpyDeviceToHost, sm) != cudaSuccess ||
-          cudaStreamSynchronize(sm) != cudaSuccess) { err = "rebalance download"; s = ADER_ERR_CUDA; break; }
-      for (size_t i = 0; i < tot.size(); ++i) tot[i] += part[i];
+    const Move& M = mv[0];
+    std::vector<int> peers;
+    std::vector<double*> sp, rp;
+    std::vector<size_t> sc, rc;
+    for (int p = 0; p < W; ++p) {
+      const size_t ns = (size_t)(M.soff[p + 1] - M.soff[p]), nr2 = (size_t)(M.roff[p + 1] - M.roff[p]);
+      if (p == A0->ranks.rank || (!ns && !nr2)) continue;
+      peers.push_back(p);
+      sp.push_back(A0->rb_buf + M.soff[p] * nv); sc.push_back(ns * nv);
+      rp.push_back(A0->rb_tmp + M.roff[p] * nv); rc.push_back(nr2 * nv);
     }
-    for (size_t g = 0; g < G.size() && s == ADER_OK; ++g) {
-      cudaStream_t sm = G[g]->k->stream;
-      if (cudaMemcpyAsync(buf[g], tot.data(), sizeof(double) * nu * nv, cudaMemcpyHostToDevice, sm) != cudaSuccess ||
-          cudaStreamSynchronize(sm) != cudaSuccess) { err = "rebalance upload"; s = ADER_ERR_CUDA; break; }
+    if (!peers.empty()) {
+      s = A0->comm.p2p(A0->comm.ctx, (int)peers.size(), peers.data(), sp.data(), sc.data(), rp.data(), rc.data(),
+                       A0->k->stream);
+      if (s != ADER_OK) err = "rebalance point-to-point failed";
     }
   }
-  // 3. new blocks: ownership, compute sets, lists, exchange plans; then the
-  //    rows of the new compute set
+  for (size_t g = 0; g < G.size() && s == ADER_OK; ++g) {
+    AmrState* A = G[g];
+    amr_launch_rows_scatter(*A->k, A->V.u, drids[g], (int)mv[g].rids.size(), A->nv, A->rb_tmp);
+    cudaStreamSynchronize(A->k->stream);   // the id lists live in the upload scratch
+  }
+  // new blocks: ownership, compute / present sets, lists, exchange plans
   for (size_t g = 0; g < G.size() && s == ADER_OK; ++g) {
     AmrState* A = G[g];
     for (int p = 0; p < W; ++p)
@@ -1452,16 +1502,13 @@ ader_status rebalance(const Group& G, std::string& err) {
     if (s != ADER_OK) break;
     // virtual children that entered this rank's lists: no flux memory from before
     for (int l = 1; l <= A->lmax; ++l) amr_launch_zero_mem(*A->k, A->V, L_vch(A, l), (int)A->lvch[l].size());
-    const std::vector<int> ids = ids_of(A, A->comp);
-    Uploader up{A, {}};
-    const size_t oi = up.add(ids.data(), sizeof(int) * ids.size());
-    s = up.run(err);
-    if (s != ADER_OK) break;
-    const int* dids = (const int*)(A->dscratch + oi);
-    amr_launch_rows_gather(*A->k, buf[g], dids, (int)ids.size(), A->nv, tmp[g]);
-    amr_launch_rows_scatter(*A->k, A->V.u, dids, (int)ids.size(), A->nv, tmp[g]);
     A->nrebal++;
   }
+  // the owners' averages to every rank's new present copies
+  for (int l = 0; l <= A0->lmax && s == ADER_OK; ++l) s = exchange(G, l, err);
+  auto cleanup = [&]() {
+    for (AmrState* A : G) cudaStreamSynchronize(A->k->stream);
+  };
   cleanup();
   return s;
 }

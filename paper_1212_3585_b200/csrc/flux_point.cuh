@@ -61,14 +61,14 @@ __device__ __forceinline__ void face_trace(const double* q0, int p, const double
       for (int k = 1; k < N; ++k) a += psi[k] * x[k];
       out[v] = a;
     }
-    return;
-  }
+  } else {
 #pragma unroll
-  for (int v = 0; v < NV; ++v) {
-    double a = psi[0] * ldq<GL>(&q[v * NST]);
+    for (int v = 0; v < NV; ++v) {
+      double a = psi[0] * ldq<GL>(&q[v * NST]);
 #pragma unroll
-    for (int k = 1; k < N; ++k) a += psi[k] * ldq<GL>(&q[v * NST + k * sn]);
-    out[v] = a;
+      for (int k = 1; k < N; ++k) a += psi[k] * ldq<GL>(&q[v * NST + k * sn]);
+      out[v] = a;
+    }
   }
 }
 

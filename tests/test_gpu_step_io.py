@@ -56,3 +56,24 @@ def test_step_io_equals_set_step_get(name, fuse, pipeline, monkeypatch):
     assert np.array_equal(host.numpy(), b.get_state())
     a.close()
     b.close()
+
+
+# Uniform steps replay as one CUDA graph per macro step (profiling off, one
+# rank): bitwise the same states and the same launch accounting as the
+# directly enqueued kernels (ADER_NO_GRAPHS=1), also across a change of t_end
+# (the graph is re-captured: k_step_dt clips against it).
+@pytest.mark.parametrize("name", ["vortex2d_M3_periodic", "explosion3d_walls"])
+def test_graph_replay_equals_direct_launches(name, monkeypatch):
+    kw, ic = CASES[name]
+    out = {}
+    for off in ("0", "1"):
+        monkeypatch.setenv("ADER_NO_GRAPHS", off)
+        s = ader.Solver(ader.make_config(device=0, **kw))
+        s.set_initial(ic)
+        l0 = s.launch_count()
+        r1 = s.step(1e300, 7)
+        r2 = s.step(r1.t + 2.5 * r1.dt0, 10)   # ends inside the third step: dt clipped
+        out[off] = (s.get_state(), s.launch_count() - l0, r1.t, r2.t, r2.macro_steps)
+        s.close()
+    assert np.array_equal(out["0"][0], out["1"][0])
+    assert out["0"][1:] == out["1"][1:]
