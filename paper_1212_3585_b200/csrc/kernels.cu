@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <type_traits>
 
 #include "device.cuh"
@@ -100,7 +101,7 @@ __global__ void __launch_bounds__(256) k_weno(const double* __restrict__ src, do
 // carry the same flux, so it is evaluated once and q^1_s = w - (sum_s' T_ss') G.
 // ===========================================================================
 
-template <int D, int M, int SYS, int WARPS>
+template <int D, int M, int SYS, int WARPS, bool XM = false>
 __global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? 4 : 2) k_predictor(
     const double* __restrict__ w, double* __restrict__ q, const Box R, const long long sy, const long long sz,
     const double dtdx0, const double dtdx1, const double dtdx2, const double gamma, const double ch,
@@ -201,7 +202,8 @@ __global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? 4 : 2) k_predictor(
       }
     }
   }
-  predictor_cell<D, M, SYS>(wv, qv, Fs, L, dtdx, cell_ok, gamma, ch, tol, max_sweeps, T, nsw, conv, bad, use_guess);
+  predictor_cell<D, M, SYS, false, XM>(wv, qv, Fs, L, dtdx, cell_ok, gamma, ch, tol, max_sweeps, T, nsw, conv, bad,
+                                        use_guess);
   if (active && (!emask || emask[cell])) {   // emask: cells whose errors count (multi-rank AMR: owned)
     if (bad) record_error(cnt, 1, 1, cell);
     else if (!conv) record_error(cnt, 2, 1, cell);
@@ -538,6 +540,11 @@ size_t pred_smem() {
   constexpr int LP = (N == 4) ? 4 : N;
   return sizeof(double) * ((size_t)kPredWarps * CPW * (D * NV * N * (NS / N) * LP + 8) + N * N);   // + R25 coefficients
 }
+
+bool pred_dmma_enabled() {
+  static const bool on = !(std::getenv("ADER_PRED_DMMA") && std::getenv("ADER_PRED_DMMA")[0] == '0');
+  return on;
+}
 }  // namespace
 
 bool supported(int D, int M, int SYS) {
@@ -596,13 +603,17 @@ void launch_predictor_list(const KCtx& k, const double* w, double* q, const Box&
     constexpr int NS = ipow_c(N, D);
     constexpr int CPW = 32 / ((NS <= 8) ? 8 : (NS <= 16 ? 16 : 32));
     const size_t sm = pred_smem<D, M, SYS>();
-    auto kern = k_predictor<D, M, SYS, kPredWarps>;
+    // 2D M = 3: the x contraction on the FP64 tensor cores (dmma_x); ADER_PRED_DMMA=0 selects the
+    // shared-memory contraction (A/B)
+    constexpr bool XMC = (D == 2 && M == 3);
+    auto kern = (XMC && pred_dmma_enabled()) ? k_predictor<D, M, SYS, kPredWarps, XMC> : k_predictor<D, M, SYS, kPredWarps>;
     int dev = 0;
     cudaGetDevice(&dev);
-    static int attr_dev_mask = 0;   // the attribute is per device
-    if (!(attr_dev_mask & (1 << (dev & 31)))) {
+    static int attr_dev_mask = 0;   // the attribute is per device (and kernel variant)
+    const int abit = 1 << ((dev & 15) * 2 + (kern == k_predictor<D, M, SYS, kPredWarps> ? 0 : 1));
+    if (!(attr_dev_mask & abit)) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      attr_dev_mask |= 1 << (dev & 31);
+      attr_dev_mask |= abit;
     }
     const long long qstride = qs > 0 ? qs : (long long)Phys<SYS, D>::NV * NS * N;
     // persistent grid: enough CTAs for every SM at full occupancy, a few times over

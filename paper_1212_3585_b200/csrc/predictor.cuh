@@ -65,7 +65,25 @@ struct PredLane {
 // sweeps, conv the convergence flag (reading R2), bad an inadmissible state.
 // Sweep 1 starts from the time-constant guess q^0 = w (R3): all N time levels
 // carry the same flux, so it is evaluated once and q^1_s = w - (sum_s' T_ss') G.
-template <int D, int M, int SYS, bool PERS = false>
+// x contraction of one (variable, time level) by the FP64 tensor-core MMA
+// (mma.sync m8n8k4 f64, 2D M = 3): with the node-per-lane layout lane L =
+// ix + 4 iy of a 16-lane cell group is exactly A[row L/4][col L%4] of the
+// 8x4 A fragment, row = the x line (iy; the warp's second cell holds rows
+// 4-7), col = the node along it; B[k][n] = D[n/2][k] (each row of D twice),
+// so C[line][n] = sum_j D[n/2][j] f*_x[j] and the lane's first accumulator
+// register c0 = C[iy][2 ix] is its own G_x = sum_j D[ix][j] f*_x[line, j].
+// The f*_x values never touch shared memory; the rows of a cell are
+// independent, so a converged cell's stale values do not reach the other.
+__device__ __forceinline__ double dmma_x(double a, double b) {
+  double c0, c1;
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%4, %5};"
+               : "=d"(c0), "=d"(c1)
+               : "d"(a), "d"(b), "d"(0.0), "d"(0.0));
+  (void)c1;
+  return c0;
+}
+
+template <int D, int M, int SYS, bool PERS = false, bool XMMA = false>
 __device__ __forceinline__ void predictor_cell(const double (&wv)[Phys<SYS, D>::NV],
                                                double (&qv)[Phys<SYS, D>::NV][M + 1], double* Fs,
                                                const PredLane<D, M, SYS>& L, const double (&dtdx)[3], bool cell_ok,
@@ -79,6 +97,10 @@ __device__ __forceinline__ void predictor_cell(const double (&wv)[Phys<SYS, D>::
   constexpr int LP = C::LP, NL = C::NL;
   const int node = L.node;
   const bool lane_ok = L.lane_ok;
+  static_assert(!XMMA || (D == 2 && N == 4 && G == 16 && LINES), "DMMA x contraction: 2D, M = 3");
+  // B fragment of dmma_x: B[k = lane % 4][n = lane / 4] = D[n / 2][k]
+  const int lane32 = threadIdx.x & 31;
+  const double bD = XMMA ? T.D[(lane32 >> 3) & 3][lane32 & 3] : 0.0;
   conv = !cell_ok;
   bad = false;
   nsw = 0;
@@ -104,11 +126,10 @@ __device__ __forceinline__ void predictor_cell(const double (&wv)[Phys<SYS, D>::
         }
     };
     // G = sum_dir D_dir f*_dir of variable v, level s
-    auto contract = [&](int v, int s) -> double {
+    auto contract = [&](int v, int s, double g) -> double {
       const int sl = PERS ? 0 : s;
-      double g = 0.0;
 #pragma unroll
-      for (int d = 0; d < D; ++d) {
+      for (int d = XMMA ? 1 : 0; d < D; ++d) {
         if constexpr (LINES) {
           const double2* fb = reinterpret_cast<const double2*>(Fs + (((d * NV + v) * SL + sl) * NL + L.line[d]) * LP);
           const double2 f01 = fb[0], f23 = fb[1];
@@ -126,14 +147,58 @@ __device__ __forceinline__ void predictor_cell(const double (&wv)[Phys<SYS, D>::
       return g;
     };
     double Gs[NV][NT];
-    if constexpr (PERS) {
+    // XMMA: the fluxes of level s with f*_y stored and G_x = D_x f*_x formed
+    // by dmma_x in registers (all 32 lanes execute the MMA)
+    auto xmma_level = [&](int s) {
+      const int sl = PERS ? 0 : s;
+      double fx[NV];
+      if (live && lane_ok) {
+        double uu[NV], f[D][NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) uu[v] = FIRST ? wv[v] : qv[v][s];
+        bad |= !PH::fluxes(uu, gamma, ch, f);
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          fx[v] = dtdx[0] * f[0][v];
+          Fs[(((1 * NV + v) * SL + sl) * NL + L.line[1]) * LP + L.ia[1]] = dtdx[1] * f[1][v];
+        }
+      } else {
+#pragma unroll
+        for (int v = 0; v < NV; ++v) fx[v] = 0.0;
+      }
+#pragma unroll
+      for (int v = 0; v < NV; ++v) Gs[v][s] = dmma_x(fx[v], bD);
+    };
+    if constexpr (XMMA) {
+#pragma unroll
+      for (int s = 0; s < NT; ++s) {
+        xmma_level(s);
+        if constexpr (PERS) {
+          __syncwarp();
+          if (live && lane_ok) {
+#pragma unroll
+            for (int v = 0; v < NV; ++v) Gs[v][s] = contract(v, s, Gs[v][s]);
+          }
+          __syncwarp();
+        }
+      }
+      if constexpr (!PERS) {
+        __syncwarp();
+        if (live && lane_ok) {
+#pragma unroll
+          for (int v = 0; v < NV; ++v)
+#pragma unroll
+            for (int s = 0; s < NT; ++s) Gs[v][s] = contract(v, s, Gs[v][s]);
+        }
+      }
+    } else if constexpr (PERS) {
 #pragma unroll
       for (int s = 0; s < NT; ++s) {
         if (live && lane_ok) store_fluxes(s);
         __syncwarp();
         if (live && lane_ok) {
 #pragma unroll
-          for (int v = 0; v < NV; ++v) Gs[v][s] = contract(v, s);
+          for (int v = 0; v < NV; ++v) Gs[v][s] = contract(v, s, 0.0);
         }
         __syncwarp();
       }
@@ -147,7 +212,7 @@ __device__ __forceinline__ void predictor_cell(const double (&wv)[Phys<SYS, D>::
 #pragma unroll
         for (int v = 0; v < NV; ++v)
 #pragma unroll
-          for (int s = 0; s < NT; ++s) Gs[v][s] = contract(v, s);
+          for (int s = 0; s < NT; ++s) Gs[v][s] = contract(v, s, 0.0);
       }
     }
     // convergence bookkeeping on the high words of |dq| and |q| (monotone in

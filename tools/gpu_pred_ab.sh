@@ -1,19 +1,15 @@
 #!/bin/bash
-# predictor contractions: warp shuffles (default build) vs shared memory (-DADER_PRED_SMEM), same box
+# A/B of a predictor variant selected by an env var (arg 2, e.g. ADER_PRED_DMMA): q/state/cells and
+# sweeps vs the variant switched off, then C2 and C5 bench lines both ways
 mkdir -p gpurun_out
-TAG=${1:-pab}
-bench2() {
-  for c in c4 c2; do
-    if [ $c = c4 ]; then A=""; else A="--config c2 --n 512"; fi
-    timeout 900 python bench.py $A --no-cpu-baseline --e2e-steps 1 > gpurun_out/bench_${TAG}_$1_$c.log 2>&1
-    tail -1 gpurun_out/bench_${TAG}_$1_$c.log | python -c "
-import json,sys; d=json.loads(sys.stdin.read()); print('$1 $c', round(d['ms_per_step'],3), [(e['kernel'], round(e['frac'],3), round(e['ms_per_launch'],3)) for e in d['roofline_kernels']], 'pw', round(d['pred_weno_fp64']['frac'],3))"
-  done
-}
+TAG=${1:-ab}; VAR=${2:-ADER_PRED_DMMA}
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build_$TAG.log 2>&1 || { echo build failed; tail gpurun_out/build_$TAG.log; exit 1; }
-timeout 900 python -m pytest tests/test_gpu_parity.py -q -x > gpurun_out/pytest_$TAG.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/pytest_$TAG.log; grep -E "^E  " gpurun_out/pytest_$TAG.log | head -5
-timeout 600 python tools/pf_ab.py > gpurun_out/pf_ab_$TAG.log 2>&1; echo "pf_ab (walk uses smem contractions) rc=$?"; grep -c "bitwise=True" gpurun_out/pf_ab_$TAG.log
-bench2 shfl
-touch paper_1212_3585_b200/csrc/kernels.cu
-make -s -C paper_1212_3585_b200/csrc NVCC="/usr/local/cuda/bin/nvcc -DADER_PRED_SMEM" > /dev/null 2>&1 || { echo smem build failed; exit 1; }
-bench2 smem
+env $VAR=0 timeout 600 python tools/pred_ab.py save gpurun_out/ab_off_$TAG.npz 2>&1 | tail -3
+timeout 600 python tools/pred_ab.py save gpurun_out/ab_on_$TAG.npz 2>&1 | tail -3
+python tools/pred_ab.py cmp gpurun_out/ab_off_$TAG.npz gpurun_out/ab_on_$TAG.npz
+for x in 0 1 0 1; do
+for c in "c2 --n 512" "c5"; do
+env $VAR=$x timeout 600 python bench.py --config $c --no-cpu-baseline --e2e-steps 1 > gpurun_out/bench_${TAG}_$x.log 2>&1; tail -1 gpurun_out/bench_${TAG}_$x.log | python -c "
+import json,sys; d=json.loads(sys.stdin.read()); print('$VAR=$x', '$c', round(d['ms_per_step'],4), [(k['kernel'], round(k.get('ms_per_launch',0),4), round(k['frac'],3)) for k in d['roofline_kernels']], round(d['pred_weno_fp64']['frac'],3), d['pred_sweeps_mean'])"
+done
+done
