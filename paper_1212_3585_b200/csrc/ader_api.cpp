@@ -640,7 +640,11 @@ void run_flux(ader_ctx* c) {
   const Box ext = make_box(H, H + c->n[0] + 1, H, H + c->n[1] + 1, zH, zH + c->n[2] + (c->d == 3 ? 1 : 0));
   // ADER_FLUX_LEGACY=1: the round-1 kernel (direct global loads), for A/B checks
   static const bool legacy = !(std::getenv("ADER_FLUX_TMA") && std::getenv("ADER_FLUX_TMA")[0] == '1');
-  if (legacy)
+  // ADER_FLUX_ROT=1: coalesced block loads + warp-shuffle line sums (flux_rot.cu)
+  static const bool rot = std::getenv("ADER_FLUX_ROT") && std::getenv("ADER_FLUX_ROT")[0] == '1';
+  if (rot)
+    launch_face_flux_rot(c->k, c->q, c->F, ext, H, c->n, transmissive_mask(c), reflective_mask(c), c->cnt, c->qs);
+  else if (legacy)
     launch_face_flux_cells(c->k, c->q, c->F, ext, H, c->n, transmissive_mask(c), reflective_mask(c), c->cnt, c->qs);
   else
     launch_face_flux_tma(c->k, c->q, c->F, ext, H, c->n, transmissive_mask(c), reflective_mask(c), c->cnt);

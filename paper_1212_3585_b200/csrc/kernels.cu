@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? 4 : 2) k_predictor(
     const double tol, const int max_sweeps, DevCounters* __restrict__ cnt, const int* __restrict__ list,
     const long long nlist, const unsigned char* __restrict__ emask, const double* __restrict__ dtdx_dev,
     const long long qs, const int guess, const StepState* __restrict__ gst, const double guess_r,
-    const int* __restrict__ rows, const __grid_constant__ DevTables T) {
+    const int* __restrict__ rows, const int flat, const __grid_constant__ DevTables T) {
   using C = PredCfg<D, M, SYS>;
   constexpr int NV = C::NV, N = C::N, NS = C::NS, NST = C::NST, G = C::G, CPW = C::CPW, FSZ = C::FSZ;
   extern __shared__ double smem[];
@@ -144,26 +144,44 @@ __global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? 4 : 2) k_predictor(
   const long long count = list ? nlist : R.count();
   // (32-bit index decomposition: a rank's box holds < 2^31 cells)
   const unsigned bx = (unsigned)R.ext[0], by = (unsigned)R.ext[1];
-  auto cell_of = [&](long long r) -> long long {
-    if (list) return (long long)list[r];
-    const unsigned ur = (unsigned)r, t = ur / bx, z = t / by;
-    return (long long)(R.lo[0] + (int)(ur - t * bx)) + (long long)(R.lo[1] + (int)(t - z * by)) * sy +
-           (long long)(R.lo[2] + (int)z) * sz;
-  };
   const double dtdx[3] = {dtdx_dev ? dtdx_dev[0] : dtdx0, dtdx_dev ? dtdx_dev[1] : dtdx1,
                           dtdx_dev ? dtdx_dev[2] : dtdx2};
 
   // persistent warps: the warp walks cell groups with a stride of the whole
-  // grid and prefetches the next group's w while it iterates on the current one
+  // grid and prefetches the next group's w while it iterates on the current one.
+  // Box mode advances the group's box coordinates by the decomposed stride
+  // (add with carry) instead of dividing the linear index in every iteration
+  // (two 32-bit divisions were 11 % of the kernel's stall samples at 256^3).
   const long long wstride = (long long)gridDim.x * WARPS;
   long long wb = (long long)blockIdx.x * WARPS + warp;        // warp-uniform iteration index
+  unsigned px, py, pz, sx_, sy_, sz_;                         // next cell's box coordinates, stride
+  {
+    const unsigned r0 = (unsigned)(wb * CPW + slot), t0 = r0 / bx;
+    px = r0 - t0 * bx; pz = t0 / by; py = t0 - pz * by;
+    const unsigned dr = (unsigned)(wstride * CPW), t1 = dr / bx;
+    sx_ = dr - t1 * bx; sz_ = t1 / by; sy_ = t1 - sz_ * by;
+  }
+  auto cell_at = [&](long long r) -> long long {   // cell of index r, whose box coordinates are (px, py, pz)
+    if (list) return (long long)list[r];
+    return (long long)(R.lo[0] + (int)px) + (long long)(R.lo[1] + (int)py) * sy + (long long)(R.lo[2] + (int)pz) * sz;
+  };
+  auto advance = [&]() {
+    px += sx_;
+    const unsigned cx = px >= bx ? 1u : 0u;
+    px -= cx * bx;
+    py += sy_ + cx;
+    const unsigned cy = py >= by ? 1u : 0u;
+    py -= cy * by;
+    pz += sz_ + cy;
+  };
   double wn[NV];
+  long long celln, drown;
   {
     const long long r0 = wb * CPW + slot;
-    const long long c0 = r0 < count ? cell_of(r0) : 0;
-    const long long d0 = rows ? (long long)rows[c0] : c0;   // row of w / q
+    celln = r0 < count ? cell_at(r0) : 0;
+    drown = rows ? (long long)rows[celln] : celln;   // row of w / q
 #pragma unroll
-    for (int v = 0; v < NV; ++v) wn[v] = r0 < count ? __ldg(&w[d0 * (NV * NS) + v * NS + node]) : 1.0;
+    for (int v = 0; v < NV; ++v) wn[v] = r0 < count ? __ldg(&w[drown * (NV * NS) + v * NS + node]) : 1.0;
   }
   unsigned long long acc_sweeps = 0, acc_cells = 0;
   int acc_max = 0;
@@ -171,17 +189,18 @@ __global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? 4 : 2) k_predictor(
   const long long rc = wb * CPW + slot;
   const bool cell_ok = rc < count;
   const bool active = cell_ok && lane_ok;
-  const long long cell = cell_ok ? cell_of(rc) : 0;
-  const long long drow = rows ? (long long)rows[cell] : cell;   // row of w / q
+  const long long cell = celln;
+  const long long drow = drown;
   double wv[NV], qv[NV][N];
 #pragma unroll
   for (int v = 0; v < NV; ++v) wv[v] = wn[v];
   {
     const long long rn = (wb + wstride) * CPW + slot;
-    const long long cn = rn < count ? cell_of(rn) : 0;
-    const long long dn = rows ? (long long)rows[cn] : cn;
+    advance();
+    celln = rn < count ? cell_at(rn) : 0;
+    drown = rows ? (long long)rows[celln] : celln;
 #pragma unroll
-    for (int v = 0; v < NV; ++v) wn[v] = rn < count ? __ldg(&w[dn * (NV * NS) + v * NS + node]) : 1.0;
+    for (int v = 0; v < NV; ++v) wn[v] = rn < count ? __ldg(&w[drown * (NV * NS) + v * NS + node]) : 1.0;
   }
   bool conv, bad;
   int nsw;
@@ -203,7 +222,7 @@ __global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? 4 : 2) k_predictor(
     }
   }
   predictor_cell<D, M, SYS, false, XM>(wv, qv, Fs, L, dtdx, cell_ok, gamma, ch, tol, max_sweeps, T, nsw, conv, bad,
-                                        use_guess);
+                                        use_guess, flat != 0);
   if (active && (!emask || emask[cell])) {   // emask: cells whose errors count (multi-rank AMR: owned)
     if (bad) record_error(cnt, 1, 1, cell);
     else if (!conv) record_error(cnt, 2, 1, cell);
@@ -541,6 +560,12 @@ size_t pred_smem() {
   return sizeof(double) * ((size_t)kPredWarps * CPW * (D * NV * N * (NS / N) * LP + 8) + N * N);   // + R25 coefficients
 }
 
+// ADER_PRED_FLAT=0: no flat-cell first sweep (A/B; bitwise the same q either way)
+bool pred_flat_enabled() {
+  static const bool on = !(std::getenv("ADER_PRED_FLAT") && std::getenv("ADER_PRED_FLAT")[0] == '0');
+  return on;
+}
+
 bool pred_dmma_enabled() {
   static const bool on = !(std::getenv("ADER_PRED_DMMA") && std::getenv("ADER_PRED_DMMA")[0] == '0');
   return on;
@@ -622,7 +647,7 @@ void launch_predictor_list(const KCtx& k, const double* w, double* q, const Box&
     count_launch(k);
     kern<<<g, kPredWarps * 32, sm, k.stream>>>(w, q, region, k.sy, k.sz, dtdx[0], dtdx[1], dtdx[2], k.gamma,
                                                 k.ch, tol, max_sweeps, cnt, list, nlist, emask, dtdx_dev, qstride, guess ? 1 : 0,
-                                                gst, guess_r, slot, k.tab);
+                                                gst, guess_r, slot, pred_flat_enabled() ? 1 : 0, k.tab);
   });
 }
 

@@ -96,6 +96,10 @@ void launch_face_flux_cells(const KCtx& k, const double* q, double* F, const Box
 // bulk copies (flux_tma.cu); q blocks at stride q_block_stride(D, M, SYS).
 void launch_face_flux_tma(const KCtx& k, const double* q, double* F, const Box& ext, int H, const int n[3],
                           int bmask, int rmask, DevCounters* cnt);
+// The same fluxes up to the rounding of the trace sums, from coalesced block
+// loads and warp-shuffle line sums (flux_rot.cu); q blocks at stride qs.
+void launch_face_flux_rot(const KCtx& k, const double* q, double* F, const Box& ext, int H, const int n[3],
+                          int bmask, int rmask, DevCounters* cnt, long long qs);
 // nu N^(d+1) rounded up to an even number of doubles (16-byte aligned blocks)
 long long q_block_stride(int D, int M, int SYS);
 // a1 + a2 fused (weno_pred.cu): WENO sweeps of the cell averages u and the

@@ -89,7 +89,7 @@ __device__ __forceinline__ void predictor_cell(const double (&wv)[Phys<SYS, D>::
                                                const PredLane<D, M, SYS>& L, const double (&dtdx)[3], bool cell_ok,
                                                double gamma, double ch, double tol, int max_sweeps,
                                                const DevTables& T, int& nsw, bool& conv, bool& bad,
-                                               bool from_guess = false) {
+                                               bool from_guess = false, bool flat_en = false) {
   using PH = Phys<SYS, D>;
   using C = PredCfg<D, M, SYS, PERS>;
   constexpr int NV = C::NV, N = C::N, NS = C::NS, G = C::G;
@@ -104,6 +104,25 @@ __device__ __forceinline__ void predictor_cell(const double (&wv)[Phys<SYS, D>::
   conv = !cell_ok;
   bad = false;
   nsw = 0;
+  // Flat cells (flat_en): if every node of every cell of the warp carries the
+  // same w (bit for bit; the WENO flat-window shortcut makes constant regions
+  // exactly so), the first sweep's f*_dir is one value per variable and
+  // direction, identical on every lane, so each lane contracts its own copy
+  // in the order of the general path — the same numbers in the same order
+  // (bitwise the same G) without the shared-memory round trip.
+  // (M = 2 only: at M = 3 the extra live state spills registers, and the 2D M = 3 workloads
+  // have no constant regions to gain from)
+  bool flat_warp = false;
+  if (M == 2 && flat_en && !from_guess) {
+    const int lead = (threadIdx.x & 31) & ~(G - 1);
+    bool same = true;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const long long mine = __double_as_longlong(wv[v]);
+      same &= mine == __shfl_sync(0xffffffffu, mine, lead);
+    }
+    flat_warp = __all_sync(0xffffffffu, same || !(cell_ok && lane_ok));
+  }
   // one Picard sweep; FIRST: the iterate is the time-constant guess (one flux level)
   auto sweep_once = [&](auto first_tag) {
     constexpr bool FIRST = decltype(first_tag)::value;
@@ -169,7 +188,23 @@ __device__ __forceinline__ void predictor_cell(const double (&wv)[Phys<SYS, D>::
 #pragma unroll
       for (int v = 0; v < NV; ++v) Gs[v][s] = dmma_x(fx[v], bD);
     };
-    if constexpr (XMMA) {
+    if (M == 2 && FIRST && flat_warp) {
+      if (live && lane_ok) {
+        double f[D][NV];
+        bad |= !PH::fluxes(wv, gamma, ch, f);
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          double g = 0.0;
+#pragma unroll
+          for (int d = 0; d < D; ++d) {
+            const double fs = dtdx[d] * f[d][v];
+#pragma unroll
+            for (int j = 0; j < N; ++j) g += L.Drow[d][j] * fs;
+          }
+          Gs[v][0] = g;
+        }
+      }
+    } else if constexpr (XMMA) {
 #pragma unroll
       for (int s = 0; s < NT; ++s) {
         xmma_level(s);
