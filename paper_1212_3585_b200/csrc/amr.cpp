@@ -54,6 +54,10 @@ struct AmrState {
   // is the all-levels active list at oall = 0; one rank: owned = active)
   std::vector<int> lact[kAmrMaxLevels], lvch[kAmrMaxLevels], lvmo[kAmrMaxLevels];
   long long oact[kAmrMaxLevels]{}, ovch[kAmrMaxLevels]{}, ovmo[kAmrMaxLevels]{}, oall = 0, nall = 0;
+  // reconstruction work lists: the active cells of a level split into sibling patches (mother ids,
+  // amr_launch_weno_patches) and the cells reconstructed from their own box (amr_launch_weno)
+  std::vector<int> lwc[kAmrMaxLevels], lwp[kAmrMaxLevels], wcount;
+  long long owc[kAmrMaxLevels]{}, owp[kAmrMaxLevels]{};
   SubTables st{};
   double t = 0.0;
   ader_ic_fn ic = nullptr;
@@ -877,7 +881,33 @@ ader_status upload_topology(AmrState* A, std::string& err) {
       X.roff[W] = (long long)X.rids.size();
       xneed = std::max(xneed, std::max(X.sids.size(), X.rids.size()) * (size_t)A->nv);
     }
+  // reconstruction lists: a mother with at least `thr` listed active children is reconstructed as
+  // one sibling patch (thr: where the patch's 1D problems undercut the per-cell boxes'), the other
+  // cells from their own box; ADER_AMR_WENO_PATCH=0 keeps every cell on its own box
+  {
+    static const bool patch_on = !(std::getenv("ADER_AMR_WENO_PATCH") && std::getenv("ADER_AMR_WENO_PATCH")[0] == '0');
+    const int N = A->N, WW = 2 * A->M + 1, Wp = A->r + 2 * A->M, R = A->r;
+    const double pc = A->d == 2 ? WW + N : WW * WW + WW * N + N * N;
+    const double pp = A->d == 2 ? R * Wp + R * R * N : R * Wp * Wp + R * R * N * Wp + R * R * R * N * N;
+    const int thr = (int)std::ceil(pp / pc);
+    for (int l = 0; l <= A->lmax; ++l) { A->lwc[l].clear(); A->lwp[l].clear(); }
+    A->lwc[0] = A->lact[0];
+    if (patch_on && A->r == 3 && A->lmax >= 1) {
+      A->wcount.assign(nu, 0);
+      for (int l = 1; l <= A->lmax; ++l)
+        for (int i : A->lact[l]) A->wcount[A->cells[i].mother]++;
+      for (int l = 1; l <= A->lmax; ++l)
+        for (int i : A->lact[l]) {
+          int& c = A->wcount[A->cells[i].mother];
+          if (c >= thr) { A->lwp[l].push_back(A->cells[i].mother); c = -1; }   // first listed child: the patch
+          else if (c >= 0) A->lwc[l].push_back(i);
+        }
+    } else {
+      for (int l = 1; l <= A->lmax; ++l) A->lwc[l] = A->lact[l];
+    }
+  }
   size_t tot = 0;
+  for (int l = 0; l <= A->lmax; ++l) tot += A->lwc[l].size() + A->lwp[l].size();
   for (int l = 0; l <= A->lmax; ++l)
     tot += A->lact[l].size() + A->lvch[l].size() + A->lvmo[l].size() + A->lown[l].size() + A->xp[l].sids.size() +
            A->xp[l].rids.size();
@@ -905,6 +935,8 @@ ader_status upload_topology(AmrState* A, std::string& err) {
     A->ovmo[l] = (long long)all.size(); all.insert(all.end(), A->lvmo[l].begin(), A->lvmo[l].end());
     A->xp[l].dso = (long long)all.size(); all.insert(all.end(), A->xp[l].sids.begin(), A->xp[l].sids.end());
     A->xp[l].dro = (long long)all.size(); all.insert(all.end(), A->xp[l].rids.begin(), A->xp[l].rids.end());
+    A->owc[l] = (long long)all.size(); all.insert(all.end(), A->lwc[l].begin(), A->lwc[l].end());
+    A->owp[l] = (long long)all.size(); all.insert(all.end(), A->lwp[l].begin(), A->lwp[l].end());
   }
   if (xneed > A->xcap) {
     if (A->xsend) { cudaStreamSynchronize(A->k->stream); cudaFree(A->xsend); cudaFree(A->xrecv); }
@@ -947,6 +979,11 @@ ader_status upload_topology(AmrState* A, std::string& err) {
 const int* L_act(const AmrState* A, int l) { return A->dlist + A->oact[l]; }
 const int* L_vch(const AmrState* A, int l) { return A->dlist + A->ovch[l]; }
 const int* L_vmo(const AmrState* A, int l) { return A->dlist + A->ovmo[l]; }
+// WENO of the listed active cells of level l: sibling patches + the remaining cells' own boxes
+void launch_weno_level(AmrState* A, int l) {
+  amr_launch_weno(*A->k, A->V, A->dlist + A->owc[l], (int)A->lwc[l].size());
+  amr_launch_weno_patches(*A->k, A->V, A->dlist + A->owp[l], (int)A->lwp[l].size(), l);
+}
 
 void psi_at(const AmrState* A, double tau, double out[4]) {
   for (int s = 0; s < 4; ++s) out[s] = s < A->N ? lagrange(A->k->tab, A->N, s, tau) : 0.0;
@@ -1162,7 +1199,7 @@ ader_status advance(const Group& G, int l, int m, double dt0, std::string& err) 
       const int N = A->N, nS = (A->M % 2 == 0) ? 3 : 4;
       wfl = (double)na * A->nv * per * (nS * (4.0 * N * N + 2.0 * N + 6.0) + 1.0 + 3.0 * N * nS);
     }
-    { AScope sc(A, ADER_K_WENO, wfl); amr_launch_weno(*A->k, A->V, L_act(A, l), na); }
+    { AScope sc(A, ADER_K_WENO, wfl); launch_weno_level(A, l); }
     { AScope sc(A, ADER_K_PRED, 0.0);
       amr_launch_predictor(*A->k, A->V, L_act(A, l), na, dtdx, A->cfg.pred_tol, A->cfg.pred_max_sweeps, A->cnt); }
   }
@@ -1196,7 +1233,7 @@ ader_status adapt_indicator(AmrState* A, bool t0, std::vector<double>& chi, std:
   const int na = (int)A->nall;
   amr_launch_indicator(*A->k, A->V, A->dlist + A->oall, na, A->cfg.chi_eps);
   if (!t0)
-    for (int l = 0; l <= A->lmax; ++l) amr_launch_weno(*A->k, A->V, L_act(A, l), (int)A->lact[l].size());
+    for (int l = 0; l <= A->lmax; ++l) launch_weno_level(A, l);
   chi.assign(A->cells.size(), 0.0);
   ACK(cudaMemcpyAsync(chi.data(), A->V.chi, sizeof(double) * A->cells.size(), cudaMemcpyDeviceToHost, sm));
   ACK(cudaStreamSynchronize(sm));

@@ -104,6 +104,9 @@ void amr_launch_average(const KCtx& k, const AmrDevView& v, const int* list, int
 void amr_launch_project(const KCtx& k, const AmrDevView& v, const SubTables& st, const int* list, int n,
                         const double* psi_tau);
 void amr_launch_weno(const KCtx& k, const AmrDevView& v, const int* list, int n);
+// WENO of the active children (level `level`, refinement factor 3) of the listed mothers, one
+// sibling patch per CTA; bitwise the w of amr_launch_weno on those children
+void amr_launch_weno_patches(const KCtx& k, const AmrDevView& v, const int* moms, int n, int level);
 void amr_launch_predictor(const KCtx& k, const AmrDevView& v, const int* list, int n, const double dtdx[3],
                           double tol, int max_sweeps, DevCounters* cnt);
 void amr_launch_flux_update(const KCtx& k, const AmrDevView& v, const SubTables& st, const int* list, int n,

@@ -191,6 +191,117 @@ __global__ void __launch_bounds__(128) k_amr_weno(AmrDevView V, const int* __res
 }
 
 // ---------------------------------------------------------------------------
+// WENO of the active children of one mother together (sibling patch): the
+// R^D children's (2M+1)^D boxes overlap in a window of W = R + 2M cells per
+// axis, so the dimension-by-dimension sweeps run once over the window in
+// shared memory — NV * (R W^(D-1) + R^2 N W^(D-2) + R^3 N^2) 1D problems per
+// patch, 21 per (cell, variable) at D = 3, R = 3, M = 2 against the 49 of the
+// per-cell box.  Every 1D problem has the inputs of the corresponding problem
+// of k_amr_weno, so w is bitwise the same.  One CTA per listed mother
+// (level l - 1); children that are not active at level l, or have no w row on
+// this rank, are skipped; window cells that do not exist (possible only
+// beyond the box of every written child) read 0.  Variables in batches of VB
+// so the three stage buffers fit 48 KB.
+template <int D, int M, int NV, int R>
+__global__ void __launch_bounds__(128) k_amr_weno_patch(AmrDevView V, const int* __restrict__ moms, int n, int l,
+                                                        const __grid_constant__ DevTables T) {
+  constexpr int N = M + 1, WW = 2 * M + 1, W = R + 2 * M, NS = ipow_a(N, D), RD = ipow_a(R, D);
+  constexpr int VB = NV < 5 ? NV : 5;
+  constexpr int NU = ipow_a(W, D);                                        // window cells
+  constexpr int NX = ipow_a(W, D - 1) * R * N;                            // x-sweep outputs per variable
+  constexpr int NY = (D == 3) ? W * R * R * N * N : 0;                    // y-sweep outputs per variable (3D)
+  constexpr int SA = VB * (NU > NY ? NU : NY), SB = VB * NX;
+  __shared__ double bufA[SA];   // window averages, then the y-sweep outputs
+  __shared__ double bufB[SB];   // x-sweep outputs
+  __shared__ int cid[RD];
+  const int mom = moms[blockIdx.x];
+  const int tid = threadIdx.x;
+  const long long X0 = V.idx[(long long)mom * 3] * R, Y0 = V.idx[(long long)mom * 3 + 1] * R,
+                  Z0 = (D == 3) ? V.idx[(long long)mom * 3 + 2] * R : 0;
+  if (tid < RD) {
+    const int cx = tid % R, cy = (tid / R) % R, cz = tid / (R * R);
+    const int id = amr_lookup(V, l, X0 + cx, Y0 + cy, Z0 + cz);
+    const bool wr = id >= 0 && V.status[id] == 0 && V.level[id] == l && (!V.slot || V.slot[id] != 0);
+    cid[tid] = wr ? id : -1;
+  }
+  for (int v0 = 0; v0 < NV; v0 += VB) {
+    const int nvb = (NV - v0 < VB) ? NV - v0 : VB;
+    __syncthreads();
+    // window averages U[v][z][y][x]
+    for (int e = tid; e < nvb * NU; e += blockDim.x) {
+      const int v = e / NU, c = e - v * NU;
+      const int wx = c % W, wy = (c / W) % W, wz = c / (W * W);
+      int fl = 0;
+      const int id = amr_lookup_flip(V, l, X0 - M + wx, Y0 - M + wy, (D == 3) ? Z0 - M + wz : 0, &fl);
+      double a = 0.0;
+      if (id >= 0) {
+        a = V.u[(long long)id * NV + v0 + v];
+        const int gv = v0 + v;
+        if (gv >= 1 && gv <= D && ((fl >> (gv - 1)) & 1)) a = -a;
+      }
+      bufA[v * NU + c] = a;
+    }
+    __syncthreads();
+    // x sweep: (v, rest = (y[, z]) of the window, child column cx) -> B[v][rest][cx][a]
+    constexpr int NR = ipow_a(W, D - 1);
+    for (int e = tid; e < nvb * NR * R; e += blockDim.x) {
+      const int v = e / (NR * R), t = e - v * (NR * R), rest = t / R, cx = t - rest * R;
+      double win[WW], out[N];
+#pragma unroll
+      for (int o = 0; o < WW; ++o) win[o] = bufA[v * NU + rest * W + cx + o];
+      weno1d<M>(T, win, out);
+#pragma unroll
+      for (int a = 0; a < N; ++a) bufB[v * NX + (rest * R + cx) * N + a] = out[a];
+    }
+    __syncthreads();
+    if constexpr (D == 2) {
+      // y sweep: (v, cy, cx, a) -> w[child][v][a + N b]
+      for (int e = tid; e < nvb * R * R * N; e += blockDim.x) {
+        const int v = e / (R * R * N), t = e - v * (R * R * N), cy = t / (R * N), t2 = t - cy * (R * N),
+                  cx = t2 / N, a = t2 - cx * N;
+        const int id = cid[cy * R + cx];
+        if (id < 0) continue;
+        double win[WW], out[N];
+#pragma unroll
+        for (int j = 0; j < WW; ++j) win[j] = bufB[v * NX + ((cy + j) * R + cx) * N + a];
+        weno1d<M>(T, win, out);
+        double* wo = V.w + (wq_row(V, id) * NV + v0 + v) * NS;
+#pragma unroll
+        for (int b = 0; b < N; ++b) wo[a + N * b] = out[b];
+      }
+    } else {
+      // y sweep: (v, z of the window, cy, cx, a) -> A[v][z][cy][cx][a][b]
+      for (int e = tid; e < nvb * W * R * R * N; e += blockDim.x) {
+        const int v = e / (W * R * R * N), t = e - v * (W * R * R * N), wz = t / (R * R * N),
+                  t2 = t - wz * (R * R * N), cy = t2 / (R * N), t3 = t2 - cy * (R * N), cx = t3 / N, a = t3 - cx * N;
+        double win[WW], out[N];
+#pragma unroll
+        for (int j = 0; j < WW; ++j) win[j] = bufB[v * NX + (((wz * W) + cy + j) * R + cx) * N + a];
+        weno1d<M>(T, win, out);
+#pragma unroll
+        for (int b = 0; b < N; ++b) bufA[v * NY + (((wz * R + cy) * R + cx) * N + a) * N + b] = out[b];
+      }
+      __syncthreads();
+      // z sweep: (v, cz, cy, cx, a, b) -> w[child][v][a + N b + N^2 c]
+      for (int e = tid; e < nvb * RD * N * N; e += blockDim.x) {
+        const int v = e / (RD * N * N), t = e - v * (RD * N * N), ch = t / (N * N), ab = t - ch * (N * N);
+        const int id = cid[ch];
+        if (id < 0) continue;
+        const int cx = ch % R, cy = (ch / R) % R, cz = ch / (R * R);
+        const int a = ab / N, b = ab - a * N;
+        double win[WW], out[N];
+#pragma unroll
+        for (int k = 0; k < WW; ++k) win[k] = bufA[v * NY + ((((cz + k) * R + cy) * R + cx) * N + a) * N + b];
+        weno1d<M>(T, win, out);
+        double* wo = V.w + (wq_row(V, id) * NV + v0 + v) * NS;
+#pragma unroll
+        for (int cc = 0; cc < N; ++cc) wo[a + N * b + N * N * cc] = out[cc];
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // face flux / update.  Trace of a same-level cell X on its face (DIR, at_one)
 // at tangential nodes (t1, t2) and time node s; coarse trace of K at the fine
 // face points via the sub-interval tables.
@@ -649,6 +760,15 @@ void amr_launch_weno(const KCtx& k, const AmrDevView& v, const int* list, int n)
   AMR_DISPATCH(k.D, k.M, k.SYS, {
     constexpr int NV = Phys<SYS, D>::NV;
     k_amr_weno<D, M, NV><<<gsz((long long)n * NV, 128), 128, 0, k.stream>>>(v, list, n, k.tab);
+  });
+}
+
+void amr_launch_weno_patches(const KCtx& k, const AmrDevView& v, const int* moms, int n, int level) {
+  if (n <= 0) return;
+  cl(k);
+  AMR_DISPATCH(k.D, k.M, k.SYS, {
+    constexpr int NV = Phys<SYS, D>::NV;
+    k_amr_weno_patch<D, M, NV, 3><<<n, 128, 0, k.stream>>>(v, moms, n, level, k.tab);
   });
 }
 
