@@ -56,7 +56,7 @@ struct AmrState {
   long long oact[kAmrMaxLevels]{}, ovch[kAmrMaxLevels]{}, ovmo[kAmrMaxLevels]{}, oall = 0, nall = 0;
   // reconstruction work lists: the active cells of a level split into sibling patches (mother ids,
   // amr_launch_weno_patches) and the cells reconstructed from their own box (amr_launch_weno)
-  std::vector<int> lwc[kAmrMaxLevels], lwp[kAmrMaxLevels], wcount;
+  std::vector<int> lwc[kAmrMaxLevels], lwp[kAmrMaxLevels];
   long long owc[kAmrMaxLevels]{}, owp[kAmrMaxLevels]{};
   SubTables st{};
   double t = 0.0;
@@ -893,15 +893,31 @@ ader_status upload_topology(AmrState* A, std::string& err) {
     for (int l = 0; l <= A->lmax; ++l) { A->lwc[l].clear(); A->lwp[l].clear(); }
     A->lwc[0] = A->lact[0];
     if (patch_on && A->r == 3 && A->lmax >= 1) {
-      A->wcount.assign(nu, 0);
-      for (int l = 1; l <= A->lmax; ++l)
-        for (int i : A->lact[l]) A->wcount[A->cells[i].mother]++;
-      for (int l = 1; l <= A->lmax; ++l)
-        for (int i : A->lact[l]) {
-          int& c = A->wcount[A->cells[i].mother];
-          if (c >= thr) { A->lwp[l].push_back(A->cells[i].mother); c = -1; }   // first listed child: the patch
-          else if (c >= 0) A->lwc[l].push_back(i);
+      // siblings occupy one block of r^d consecutive ids and the lists are in id order, so the
+      // listed children of a mother are adjacent: one pass per level, chunked over host threads
+      // (a chunk starts at the first group that begins inside it and finishes its last group)
+      for (int l = 1; l <= A->lmax; ++l) {
+        const std::vector<int>& L = A->lact[l];
+        const int nl = (int)L.size(), T = host_threads(nl);
+        std::vector<std::vector<int>> pc_(T), pp_(T);
+        parallel_chunks(nl, T, [&](int t, int i0, int i1) {
+          int j = i0;
+          if (j > 0)
+            while (j < i1 && A->cells[L[j]].mother == A->cells[L[j - 1]].mother) ++j;
+          while (j < i1) {
+            const int mo = A->cells[L[j]].mother;
+            int e = j + 1;
+            while (e < nl && A->cells[L[e]].mother == mo) ++e;
+            if (e - j >= thr) pp_[t].push_back(mo);
+            else pc_[t].insert(pc_[t].end(), L.begin() + j, L.begin() + e);
+            j = e;
+          }
+        });
+        for (int t = 0; t < T; ++t) {
+          A->lwc[l].insert(A->lwc[l].end(), pc_[t].begin(), pc_[t].end());
+          A->lwp[l].insert(A->lwp[l].end(), pp_[t].begin(), pp_[t].end());
         }
+      }
     } else {
       for (int l = 1; l <= A->lmax; ++l) A->lwc[l] = A->lact[l];
     }

@@ -393,45 +393,70 @@ __device__ __forceinline__ bool amr_face_point(int kind, const double* qL, const
   return numflux_pt<SYS, D, DIR>(um, up, gamma, ch, T, ft);
 }
 
-template <int D, int M, int SYS, int DIR, int G>
-__device__ __forceinline__ bool amr_cell_face_w(const AmrDevView& V, int c, bool valid, int side, int m, int p,
-                                                double gamma, double ch, const DevTables& T, const SubTables& S,
-                                                double (*rb)[G + 1], double* Fout) {
-  constexpr int NV = Phys<SYS, D>::NV, N = M + 1, NS = ipow_a(N, D), NST = NS * N, NT = NS / N;
+// What lies across face (dir, side) of cell c: the face kind (above; 8 = the
+// active same-level neighbour computes it as its lower face; -1 error), the
+// neighbour id, the cell's sub-face offsets inside a coarse neighbour and the
+// w / q rows of the lower and upper side.  Evaluated by ONE lane per face
+// (lane f of the cell's lane group takes face f = 2 dir + side) and broadcast,
+// so the 2D chains of dependent loads (idx -> id map -> status -> mother ->
+// row) of a cell run side by side instead of one after the other.
+struct AmrFace {
+  int kind, nb, o1, o2;
+  long long rowL, rowR;
+};
+__device__ __forceinline__ AmrFace amr_face_info(const AmrDevView& V, int c, int dir, int side) {
+  AmrFace f;
   const int l = V.level[c];
   long long ix[3] = {V.idx[(long long)c * 3], V.idx[(long long)c * 3 + 1], V.idx[(long long)c * 3 + 2]};
-  ix[DIR] += side ? 1 : -1;
-  const double* qc = V.q + wq_row(V, c) * NV * NST;
-  const bool out = ix[DIR] < 0 || ix[DIR] >= V.n[l][DIR];
-  // kind as listed above, -1 error.  Every lane group of the warp runs the
-  // same two __syncwarp()s whatever its kind (2D: several cells per warp).
-  int kind = -1, nb = -1, o1 = 0, o2 = 0;
-  const double *qL = qc, *qR = qc;
-  if (out && V.bc[2 * DIR + side] == ADER_BC_TRANSMISSIVE) kind = side ? 2 : 1;
-  else if (out && V.bc[2 * DIR + side] == ADER_BC_REFLECTIVE) kind = side ? 6 : 5;
+  const long long own[3] = {ix[0], ix[1], ix[2]};
+  ix[dir] += side ? 1 : -1;
+  const long long rowc = wq_row(V, c);
+  const bool out = ix[dir] < 0 || ix[dir] >= V.n[l][dir];
+  f.kind = -1; f.nb = -1; f.o1 = 0; f.o2 = 0; f.rowL = rowc; f.rowR = rowc;
+  if (out && V.bc[2 * dir + side] == ADER_BC_TRANSMISSIVE) f.kind = side ? 2 : 1;
+  else if (out && V.bc[2 * dir + side] == ADER_BC_REFLECTIVE) f.kind = side ? 6 : 5;
   else {
-    nb = amr_lookup(V, l, ix[0], ix[1], ix[2]);
-    const int st = nb >= 0 ? V.status[nb] : 9;
+    f.nb = amr_lookup(V, l, ix[0], ix[1], ix[2]);
+    const int st = f.nb >= 0 ? V.status[f.nb] : 9;
     if (st == 0 && side) {
-      kind = 8;   // computed once, as the lower face of the neighbour (k_amr_update_w reads it there)
+      f.kind = 8;   // computed once, as the lower face of the neighbour (k_amr_update_w reads it there)
     } else if (st == 0) {
-      const double* qn = V.q + wq_row(V, nb) * NV * NST;
-      kind = 0;
-      qL = qn;
-      qR = qc;
+      f.kind = 0;
+      f.rowL = wq_row(V, f.nb);
     } else if (st == 1) {
       // coarse-fine: the virtual neighbour scales its mother's q_h down
-      const double* qK = V.q + wq_row(V, V.mother[nb]) * NV * NST;
-      constexpr int ax0 = (DIR == 0) ? 1 : 0, ax1 = (DIR == 2) ? 1 : 2;
-      o1 = (int)(V.idx[(long long)c * 3 + ax0] % V.r);
-      o2 = (D == 3) ? (int)(V.idx[(long long)c * 3 + ax1] % V.r) : 0;
-      kind = side ? 4 : 3;
-      qL = side ? qc : qK;
-      qR = side ? qK : qc;
+      const long long rowK = wq_row(V, V.mother[f.nb]);
+      const int ax0 = (dir == 0) ? 1 : 0, ax1 = (dir == 2) ? 1 : 2;
+      f.o1 = (int)(own[ax0] % V.r);
+      f.o2 = (V.D == 3) ? (int)(own[ax1] % V.r) : 0;
+      f.kind = side ? 4 : 3;
+      if (side) f.rowR = rowK; else f.rowL = rowK;
     } else if (st == -1) {
-      kind = V.child[c] >= 0 ? 7 : -1;
+      f.kind = V.child[c] >= 0 ? 7 : -1;
     }
   }
+  return f;
+}
+__device__ __forceinline__ AmrFace amr_face_bcast(const AmrFace& f, int src) {
+  AmrFace g;
+  g.kind = __shfl_sync(0xffffffffu, f.kind, src);
+  g.nb = __shfl_sync(0xffffffffu, f.nb, src);
+  g.o1 = __shfl_sync(0xffffffffu, f.o1, src);
+  g.o2 = __shfl_sync(0xffffffffu, f.o2, src);
+  g.rowL = __shfl_sync(0xffffffffu, f.rowL, src);
+  g.rowR = __shfl_sync(0xffffffffu, f.rowR, src);
+  return g;
+}
+
+template <int D, int M, int SYS, int DIR, int G>
+__device__ __forceinline__ bool amr_cell_face_w(const AmrDevView& V, int c, bool valid, int side, int m, int p,
+                                                const AmrFace& fi, double gamma, double ch, const DevTables& T,
+                                                const SubTables& S, double (*rb)[G + 1], double* Fout) {
+  constexpr int NV = Phys<SYS, D>::NV, N = M + 1, NS = ipow_a(N, D), NST = NS * N, NT = NS / N;
+  // Every lane group of the warp runs the same two __syncwarp()s whatever its
+  // kind (2D: several cells per warp).
+  const int kind = fi.kind, nb = fi.nb, o1 = fi.o1, o2 = fi.o2;
+  const double *qL = V.q + fi.rowL * NV * NST, *qR = V.q + fi.rowR * NV * NST;
   bool ok = kind >= 0;
   if (valid && kind >= 0 && kind < 7 && p < NS) {
     const int s = p / NT, t = p - s * NT, t1 = t % N, t2 = t / N;
@@ -490,14 +515,17 @@ __global__ void __launch_bounds__(WARPS * 32) k_amr_flux_w(AmrDevView V, const _
   const int c = list[valid ? i : 0];
   double(*rb)[G + 1] = red[grp];
   double* F = V.mem + (long long)c * 6 * NV;
+  // lane f < 2D of the lane group looks across face f; the others receive it
+  AmrFace mine = amr_face_info(V, c, (p < 2 * D) ? (p >> 1) : 0, p & 1);
+  const int base = lane & ~(G - 1);
   bool ok = true;
-  ok &= amr_cell_face_w<D, M, SYS, 0, G>(V, c, valid, 0, m, p, gamma, ch, T, S, rb, F + 0 * NV);
-  ok &= amr_cell_face_w<D, M, SYS, 0, G>(V, c, valid, 1, m, p, gamma, ch, T, S, rb, F + 1 * NV);
-  ok &= amr_cell_face_w<D, M, SYS, 1, G>(V, c, valid, 0, m, p, gamma, ch, T, S, rb, F + 2 * NV);
-  ok &= amr_cell_face_w<D, M, SYS, 1, G>(V, c, valid, 1, m, p, gamma, ch, T, S, rb, F + 3 * NV);
+  ok &= amr_cell_face_w<D, M, SYS, 0, G>(V, c, valid, 0, m, p, amr_face_bcast(mine, base + 0), gamma, ch, T, S, rb, F + 0 * NV);
+  ok &= amr_cell_face_w<D, M, SYS, 0, G>(V, c, valid, 1, m, p, amr_face_bcast(mine, base + 1), gamma, ch, T, S, rb, F + 1 * NV);
+  ok &= amr_cell_face_w<D, M, SYS, 1, G>(V, c, valid, 0, m, p, amr_face_bcast(mine, base + 2), gamma, ch, T, S, rb, F + 2 * NV);
+  ok &= amr_cell_face_w<D, M, SYS, 1, G>(V, c, valid, 1, m, p, amr_face_bcast(mine, base + 3), gamma, ch, T, S, rb, F + 3 * NV);
   if constexpr (D == 3) {
-    ok &= amr_cell_face_w<D, M, SYS, 2, G>(V, c, valid, 0, m, p, gamma, ch, T, S, rb, F + 4 * NV);
-    ok &= amr_cell_face_w<D, M, SYS, 2, G>(V, c, valid, 1, m, p, gamma, ch, T, S, rb, F + 5 * NV);
+    ok &= amr_cell_face_w<D, M, SYS, 2, G>(V, c, valid, 0, m, p, amr_face_bcast(mine, base + 4), gamma, ch, T, S, rb, F + 4 * NV);
+    ok &= amr_cell_face_w<D, M, SYS, 2, G>(V, c, valid, 1, m, p, amr_face_bcast(mine, base + 5), gamma, ch, T, S, rb, F + 5 * NV);
   }
   if (valid && !ok && (!V.own || V.own[c])) amr_error(cnt, 1, 2, c);   // multi-rank: band cells' errors do not count
 }

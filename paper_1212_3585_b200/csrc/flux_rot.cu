@@ -274,19 +274,12 @@ int env_int(const char* name, int dflt) {
 template <int D, int M, int SYS, int FLUX>
 void rot_variant(const KCtx& k, const double* q, double* F, const Box& E, int H, const int n[3], int bmask, int rmask,
                  DevCounters* cnt, long long qs) {
-  // A/B knobs: run length along x, rows per y chunk, CTAs per SM the register budget is set for
-  static const int rl = env_int("ADER_FLUX_RL", 8);
+  // A/B knobs: rows per y chunk, CTAs per SM the register budget is set for (3: 168 registers,
+  // no spills at D = 3; 4: 128 registers)
   static const int yc = env_int("ADER_FLUX_YC", 16) > 0 ? env_int("ADER_FLUX_YC", 16) : 16;
-  static const int mb = env_int("ADER_FLUX_MINB", 4);
-#define ADER_ROT_GO(RL_)                                                                          \
-  {                                                                                               \
-    if (mb >= 5) launch_rot<D, M, SYS, FLUX, RL_, 5>(k, q, F, E, H, n, bmask, rmask, cnt, qs, yc);      \
-    else if (mb == 4) launch_rot<D, M, SYS, FLUX, RL_, 4>(k, q, F, E, H, n, bmask, rmask, cnt, qs, yc); \
-    else launch_rot<D, M, SYS, FLUX, RL_, 3>(k, q, F, E, H, n, bmask, rmask, cnt, qs, yc);              \
-  }
-  if (rl <= 4) ADER_ROT_GO(4)
-  else ADER_ROT_GO(8)
-#undef ADER_ROT_GO
+  static const int mb = env_int("ADER_FLUX_MINB", D == 3 ? 3 : 4);
+  if (mb >= 4) launch_rot<D, M, SYS, FLUX, 8, 4>(k, q, F, E, H, n, bmask, rmask, cnt, qs, yc);
+  else launch_rot<D, M, SYS, FLUX, 8, 3>(k, q, F, E, H, n, bmask, rmask, cnt, qs, yc);
 }
 
 }  // namespace
