@@ -402,16 +402,24 @@ def main():
         if kl[ader.K_PRED]:
             # algorithmic bytes of one predictor launch: read w, write q of every predicted cell
             cells_per_launch = rep.pred_cells / max(1, args.steps) / max(1e-9, kl[ader.K_PRED] / nprof)
+            # flat cells (ader_step_report.pred_flat_cells) get a one-byte flag instead of a q block
+            flat_frac = rep.pred_flat_cells / max(1, rep.pred_cells)
             entries.append(entry("stdg_predictor", kms[ader.K_PRED] / kl[ader.K_PRED],
                                  kfl[ader.K_PRED] / kl[ader.K_PRED],
-                                 cells_per_launch * nvv * (N ** wl.dim + N ** (wl.dim + 1)) * 8,
-                                 "algorithmic bytes (w read + q written per predicted cell) / CUDA-event time",
+                                 cells_per_launch * (nvv * N ** wl.dim * 8
+                                                     + (1.0 - flat_frac) * nvv * N ** (wl.dim + 1) * 8 + flat_frac),
+                                 "algorithmic bytes (w read per predicted cell + q written per cell that is not "
+                                 f"flat: {1.0 - flat_frac:.4f} of them) / CUDA-event time",
                                  sweeps_note + " / CUDA-event time"))
         if wl.lmax == 0 and kl[ader.K_FLUX] and not kl[ader.K_PRED_FLUX]:
             # face flux: algorithmic bytes = every q read once + F written
+            flat_frac = rep.pred_flat_cells / max(1, rep.pred_cells)
             entries.append(entry(f"face_flux_{args.flux}", kms[ader.K_FLUX] / kl[ader.K_FLUX],
-                                 kfl[ader.K_FLUX] / kl[ader.K_FLUX], ext * nvv * (N ** (wl.dim + 1) + wl.dim) * 8,
-                                 "algorithmic bytes (each q read once, F written) / CUDA-event time",
+                                 kfl[ader.K_FLUX] / kl[ader.K_FLUX],
+                                 ext * ((1.0 - flat_frac) * nvv * N ** (wl.dim + 1) * 8 + flat_frac * (nvv * 8 + 1)
+                                        + nvv * wl.dim * 8),
+                                 "algorithmic bytes (the q block of each cell that is not flat read once, w and "
+                                 f"the flag of a flat cell ({flat_frac:.4f} of them), F written) / CUDA-event time",
                                  "algorithmic FP64 flops of the face quadrature / CUDA-event time"))
         if kl[ader.K_PRED_FLUX]:
             # fused a2 + a3 walk (+ its tile-face kernel): w read, F written; q never leaves the SM
@@ -455,6 +463,7 @@ def main():
             "pred_weno_fp64": pred_weno,
             "kernel_share_of_step": share,
             "pred_sweeps_mean": rep.pred_sweeps_total / max(1, rep.pred_cells),
+            "pred_flat_frac": rep.pred_flat_cells / max(1, rep.pred_cells),
             "clocks": clocks,
             "e2e": e2e,
             "gpu_launches": int(launches),

@@ -15,7 +15,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libader_b200.so")
 _LIB = None
 
-ABI_VERSION = 5
+ABI_VERSION = 6
 EULER, MHD_GLM = 0, 1
 PERIODIC, TRANSMISSIVE, REFLECTIVE, INFLOW = 0, 1, 2, 3
 RUSANOV, OSHER = 0, 1
@@ -51,7 +51,7 @@ class AderStepReport(C.Structure):
         ("macro_steps", C.c_int64), ("cell_updates", C.c_int64), ("updates_per_level", C.c_int64 * 8),
         ("pred_sweeps_total", C.c_int64), ("pred_sweeps_max", C.c_int32), ("rebalances", C.c_int32),
         ("pred_cells", C.c_int64), ("cons_total", C.c_double * 9), ("wall_s", C.c_double),
-        ("min_threshold_margin", C.c_double),
+        ("min_threshold_margin", C.c_double), ("pred_flat_cells", C.c_int64),
     ]
 
 

@@ -188,6 +188,13 @@ struct ader_ctx {
   double t = 0.0;
   bool speed_valid = false;
   bool guess_ready = false;                    // R25: q holds the previous step's predictor of this state
+  // flat cells (D = 3, M = 2): flags of the cells whose q block the predictor did not write
+  // (q_h rebuilt from w by the face-flux kernel), valid while qflat_on; the dt/dx it used
+  unsigned char* qflat = nullptr;
+  bool qflat_on = false;
+  unsigned long long flat0 = 0;                // flat_cells counter at the start of the call
+  double pf_dtdx[3] = {0, 0, 0};
+  const double* pf_dtdx_dev = nullptr;
   ader_ic_fn ic = nullptr;                     // the problem's IC (ADER_BC_EXACT sides, R26)
   void* ic_user = nullptr;
   bool has_exact = false;                      // a side of this rank is ADER_BC_EXACT
@@ -562,7 +569,17 @@ int boundary_mask(const ader_ctx* c, int bc) {
 int transmissive_mask(const ader_ctx* c) { return boundary_mask(c, ADER_BC_TRANSMISSIVE); }
 int reflective_mask(const ader_ctx* c) { return boundary_mask(c, ADER_BC_REFLECTIVE); }
 
-void run_predictor(ader_ctx* c, double dt, const double* dtdx_dev = nullptr, bool guess = false) {
+// ADER_PRED_FLAT_SKIP=0: every predicted cell gets its q block (A/B; bitwise the same F and state)
+bool flat_skip_env() {
+  static const bool on = !(std::getenv("ADER_PRED_FLAT_SKIP") && std::getenv("ADER_PRED_FLAT_SKIP")[0] == '0') &&
+                         !(std::getenv("ADER_PRED_FLAT") && std::getenv("ADER_PRED_FLAT")[0] == '0') &&
+                         !(std::getenv("ADER_FLUX_TMA") && std::getenv("ADER_FLUX_TMA")[0] == '1') &&
+                         !(std::getenv("ADER_FLUX_ROT") && std::getenv("ADER_FLUX_ROT")[0] == '1');
+  return on;
+}
+
+void run_predictor(ader_ctx* c, double dt, const double* dtdx_dev = nullptr, bool guess = false,
+                   bool allow_skip = true) {
   // owned block + the face-neighbour layer, except beyond transmissive sides (R5)
   Box r = grown(c, 1);
   const int tm = transmissive_mask(c) | reflective_mask(c);   // no predictor beyond walls either (R22)
@@ -577,8 +594,13 @@ void run_predictor(ader_ctx* c, double dt, const double* dtdx_dev = nullptr, boo
   // loop, else from the host's dt ratio (loopback groups)
   const bool g = guess && c->cfg.pred_guess == 1 && c->guess_ready;
   const double gr = (!dtdx_dev && c->prev_dt_host > 0.0 && dt > 0.0) ? dt / c->prev_dt_host : 0.0;
+  // flat cells without a q block: not with the R25 guess (it reads the previous q blocks)
+  const bool skip = allow_skip && c->qflat && c->cfg.pred_guess == 0 && flat_skip_env();
   launch_predictor(c->k, c->w, c->q, r, dtdx, c->cfg.pred_tol, c->cfg.pred_max_sweeps, c->cnt, dtdx_dev, c->qs, g,
-                   dtdx_dev ? c->st : nullptr, gr);
+                   dtdx_dev ? c->st : nullptr, gr, skip ? c->qflat : nullptr);
+  c->qflat_on = skip;
+  for (int k = 0; k < 3; ++k) c->pf_dtdx[k] = dtdx[k];
+  c->pf_dtdx_dev = dtdx_dev;
   if (guess) { c->guess_ready = true; c->prev_dt_host = dt; }
 }
 
@@ -595,6 +617,7 @@ bool fused_weno_pred_env() {
 bool fused_weno_pred(const ader_ctx* c) { return fused_weno_pred_env() && c->cfg.pred_guess == 0; }
 
 void run_weno_predictor(ader_ctx* c, double dt, const double* dtdx_dev = nullptr) {
+  c->qflat_on = false;   // the fused walk writes every q block
   Box r = grown(c, 1);
   const int tm = transmissive_mask(c) | reflective_mask(c);   // as run_predictor (R5, R22)
   for (int a = 0; a < c->d; ++a) {
@@ -645,7 +668,8 @@ void run_flux(ader_ctx* c) {
   if (rot)
     launch_face_flux_rot(c->k, c->q, c->F, ext, H, c->n, transmissive_mask(c), reflective_mask(c), c->cnt, c->qs);
   else if (legacy)
-    launch_face_flux_cells(c->k, c->q, c->F, ext, H, c->n, transmissive_mask(c), reflective_mask(c), c->cnt, c->qs);
+    launch_face_flux_cells(c->k, c->q, c->F, ext, H, c->n, transmissive_mask(c), reflective_mask(c), c->cnt, c->qs,
+                           c->qflat_on ? c->qflat : nullptr, c->w, c->pf_dtdx, c->pf_dtdx_dev);
   else
     launch_face_flux_tma(c->k, c->q, c->F, ext, H, c->n, transmissive_mask(c), reflective_mask(c), c->cnt);
 }
@@ -735,6 +759,7 @@ void free_ctx(ader_ctx* c) {
   double* bufs[] = {c->u, c->wx, c->wxy, c->w, c->q, c->F, c->stage, c->pfb};
   for (double* b : bufs)
     if (b) cudaFree(b);
+  if (c->qflat) cudaFree(c->qflat);
   if (c->st) cudaFree(c->st);
   if (c->hst) cudaFreeHost(c->hst);
   if (c->cons_part) cudaFree(c->cons_part);
@@ -1011,6 +1036,10 @@ static ader_status create_impl(const ader_config* cfg, ader_ctx** out, bool loop
   c->qs = q_block_stride(c->d, c->M, c->cfg.system);
   CK(alloc(&c->q, nc * c->qs));
   CK(alloc(&c->F, nc * c->nv * c->d));
+  if (c->d == 3 && c->M == 2) {   // flat-cell flags (cells outside the predictor's region stay 0)
+    CK(cudaMalloc(&c->qflat, nc));
+    CK(cudaMemset(c->qflat, 0, nc));
+  }
   if (cfg->fuse_pred_flux == 1 && cfg->pred_guess == 0) {
     const long long nb = pred_flux_buffer_doubles(c->d, c->M, cfg->system, predictor_region(c), c->H, c->n);
     if (nb < 0) return fail(c, ADER_ERR_CUDA, "pred_flux: unsupported (d, M, system)");
@@ -1286,7 +1315,8 @@ ader_status tail_to_host(ader_ctx* c, const double* dtdx_dev, double* out_host) 
     e.lo[W] = cut(i);
     e.ext[W] = cut(i + 1) - cut(i) + (i + 1 == K ? 1 : 0);
     Scope s(c, ADER_K_FLUX, fl_per_face * (double)nf * e.ext[W] / (nW + 1));
-    launch_face_flux_cells(c->k, c->q, c->F, e, H, c->n, transmissive_mask(c), reflective_mask(c), c->cnt, c->qs);
+    launch_face_flux_cells(c->k, c->q, c->F, e, H, c->n, transmissive_mask(c), reflective_mask(c), c->cnt, c->qs,
+                           c->qflat_on ? c->qflat : nullptr, c->w, c->pf_dtdx, c->pf_dtdx_dev);
   };
   auto update_copy = [&](int i) -> ader_status {
     Box r = owned(c);
@@ -1382,6 +1412,7 @@ ader_status step_begin(ader_ctx* c, unsigned long long* sw0, unsigned long long*
   CK(cudaStreamSynchronize(c->k.stream));
   *sw0 = c->hcnt->sweeps;
   *pc0 = c->hcnt->cells;
+  c->flat0 = c->hcnt->flat_cells;
   return ADER_OK;
 }
 
@@ -1395,6 +1426,7 @@ ader_status step_finish(ader_ctx* c, ader_status st, ader_step_report* r, unsign
   r->updates_per_level[0] = r->cell_updates;
   r->pred_sweeps_total = (int64_t)(c->hcnt->sweeps - sw0);
   r->pred_cells = (int64_t)(c->hcnt->cells - pc0);
+  r->pred_flat_cells = (int64_t)(c->hcnt->flat_cells - c->flat0);
   r->pred_sweeps_max = c->hcnt->sweeps_max;
   // conserved totals (diagnostic): block partials on device, summed in order here
   const Box b = owned(c);
@@ -1930,7 +1962,7 @@ ader_status ader_debug_dump(ader_ctx* c, int32_t what, double dt, double* out, i
     CK(cudaMemsetAsync(c->F, 0, (size_t)c->ncell * c->nv * c->d * sizeof(double), c->k.stream));
     run_pred_flux(c, dt);
   } else if (fused_weno_pred(c)) run_weno_predictor(c, dt);
-  else run_predictor(c, dt);
+  else run_predictor(c, dt, nullptr, false, what != 1);   // the PRED dump needs every q block
   c->guess_ready = false;   // q no longer holds the last step's predictor
   if (what == 1) {
     if (capacity < b.count() * c->nv * c->NST) return fail(c, ADER_ERR_ARG, "capacity too small");

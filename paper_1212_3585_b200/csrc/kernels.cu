@@ -108,7 +108,8 @@ __global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? 4 : 2) k_predictor(
     const double tol, const int max_sweeps, DevCounters* __restrict__ cnt, const int* __restrict__ list,
     const long long nlist, const unsigned char* __restrict__ emask, const double* __restrict__ dtdx_dev,
     const long long qs, const int guess, const StepState* __restrict__ gst, const double guess_r,
-    const int* __restrict__ rows, const int flat, const __grid_constant__ DevTables T) {
+    const int* __restrict__ rows, const int flat, unsigned char* __restrict__ qflat,
+    const __grid_constant__ DevTables T) {
   using C = PredCfg<D, M, SYS>;
   constexpr int NV = C::NV, N = C::N, NS = C::NS, NST = C::NST, G = C::G, CPW = C::CPW, FSZ = C::FSZ;
   extern __shared__ double smem[];
@@ -183,7 +184,7 @@ __global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? 4 : 2) k_predictor(
 #pragma unroll
     for (int v = 0; v < NV; ++v) wn[v] = r0 < count ? __ldg(&w[drown * (NV * NS) + v * NS + node]) : 1.0;
   }
-  unsigned long long acc_sweeps = 0, acc_cells = 0;
+  unsigned long long acc_sweeps = 0, acc_cells = 0, acc_flat = 0;
   int acc_max = 0;
   for (; wb * CPW < count; wb += wstride) {
   const long long rc = wb * CPW + slot;
@@ -221,21 +222,31 @@ __global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? 4 : 2) k_predictor(
       }
     }
   }
+  bool was_flat = false;
   predictor_cell<D, M, SYS, false, XM>(wv, qv, Fs, L, dtdx, cell_ok, gamma, ch, tol, max_sweeps, T, nsw, conv, bad,
-                                        use_guess, flat != 0);
+                                        use_guess, flat != 0, &was_flat);
+  // qflat (uniform boxes): a flat cell that converged in its first sweep is fully described
+  // by its w — q_h[v][s][node] = w_v - Tsum[s] G_v(node) — so only a flag is stored and the
+  // face-flux kernel rebuilds the traces from w (flat_cell_G): no 3.2 KB q_h block written
+  // here and read there for the constant regions
+  const bool skipq = qflat && was_flat && conv && !bad && nsw == 1;
+  if (qflat && active && node == 0) qflat[cell] = skipq ? 1 : 0;
   if (active && (!emask || emask[cell])) {   // emask: cells whose errors count (multi-rank AMR: owned)
     if (bad) record_error(cnt, 1, 1, cell);
     else if (!conv) record_error(cnt, 2, 1, cell);
   }
   if (active) {
-    double* qo = q + drow * qs + node;   // qs: block stride (>= NV * NST)
+    if (!skipq) {
+      double* qo = q + drow * qs + node;   // qs: block stride (>= NV * NST)
 #pragma unroll
-    for (int v = 0; v < NV; ++v)
+      for (int v = 0; v < NV; ++v)
 #pragma unroll
-      for (int s = 0; s < N; ++s) qo[v * NST + s * NS] = qv[v][s];
+        for (int s = 0; s < N; ++s) qo[v * NST + s * NS] = qv[v][s];
+    }
     if (node == 0) {
       acc_sweeps += (unsigned long long)nsw;
       acc_cells += 1ull;
+      acc_flat += skipq ? 1ull : 0ull;
       acc_max = nsw > acc_max ? nsw : acc_max;
     }
   }
@@ -246,11 +257,13 @@ __global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? 4 : 2) k_predictor(
   for (int o = 16; o > 0; o >>= 1) {
     acc_sweeps += __shfl_xor_sync(0xffffffffu, acc_sweeps, o);
     acc_cells += __shfl_xor_sync(0xffffffffu, acc_cells, o);
+    acc_flat += __shfl_xor_sync(0xffffffffu, acc_flat, o);
     acc_max = max(acc_max, __shfl_xor_sync(0xffffffffu, acc_max, o));
   }
   if (lane == 0 && acc_cells) {
     atomicAdd(&cnt->sweeps, acc_sweeps);
     atomicAdd(&cnt->cells, acc_cells);
+    if (acc_flat) atomicAdd(&cnt->flat_cells, acc_flat);
     atomicMax(&cnt->sweeps_max, acc_max);
   }
 }
@@ -336,6 +349,161 @@ __global__ void __launch_bounds__(WARPS * 32, (FLUX == 1) ? 5 : (SYS == 1 ? 4 : 
   // order (rows padded to G+1 doubles: conflict-free column writes and row reads)
   __shared__ double red[WARPS * CPW][K][G + 1];
   double(*rb)[G + 1] = red[warp * CPW + lane / G];
+  if (pok) {
+#pragma unroll
+    for (int i = 0; i < K; ++i) rb[i][p] = v[i];
+  }
+  __syncwarp();
+  for (int i = p; i < K; i += G) {
+    double acc = rb[i][0];
+#pragma unroll
+    for (int j = 1; j < NS; ++j) acc += rb[i][j];
+    const int dir = i / NV, var = i - dir * NV;
+    const bool face_ok = dir == 0 ? (ok && iny && inz) : (dir == 1 ? (ok && inx && inz) : (ok && inx && iny));
+    if (face_ok) F[((long long)dir * ncell + cR) * NV + var] = acc;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// a3 with flat cells rebuilt from w (D = 3, M = 2; one cell per warp).  A cell
+// flagged by the predictor (qflat) has no q block: its q_h[v][s][node] =
+// w_v - Tsum[s] G_v(node) with G the predictor's flat first sweep
+// (flat_cell_G, the same code, so bitwise the value the predictor would have
+// stored).  Lane p builds G of node p into a shared table per cell (own; a
+// flat lower neighbour with the same w bit for bit — the rule inside a
+// constant region — shares it, another flat neighbour gets a second table),
+// and the trace contractions of flagged cells read the table instead of
+// gathering from a q block.  Unflagged cells go through face_trace as in
+// k_face_flux_cells; same trace arithmetic, point flux and point-sum order.
+template <int D, int M, int NV, int DIR>
+__device__ __forceinline__ void flat_trace(const double* __restrict__ tab, const double (&w)[NV], int p,
+                                           const double (&psi)[kMaxN], const DevTables& T, double (&out)[NV]) {
+  constexpr int N = M + 1, NS = ipow_c(N, D), NT = NS / N;
+  const int s = p / NT, t = p - s * NT;
+  const int t1 = t % N, t2 = t / N;
+  constexpr int ax0 = (DIR == 0) ? 1 : 0;
+  constexpr int ax1 = (DIR == 2) ? 1 : 2;
+  constexpr int sn = ipow_c(N, DIR);
+  const int base = t1 * ipow_c(N, ax0) + (D == 3 ? t2 * ipow_c(N, ax1) : 0);
+  const double ts = T.Tsum[s];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    double a = psi[0] * flat_cell_q(w[v], ts, tab[v * NS + base]);
+#pragma unroll
+    for (int k = 1; k < N; ++k) a += psi[k] * flat_cell_q(w[v], ts, tab[v * NS + base + k * sn]);
+    out[v] = a;
+  }
+}
+
+template <int D, int M, int SYS, int WARPS, int YC, int FLUX>
+__global__ void __launch_bounds__(WARPS * 32, (FLUX == 1) ? 4 : (SYS == 1 ? 3 : 6)) k_face_flux_cells_flat(
+    const double* __restrict__ q, double* __restrict__ F, const Box E, const int H, const int n0, const int n1,
+    const int n2, const long long sy, const long long sz, const long long ncell, const double gamma, const double ch,
+    const int bmask, const int rmask, DevCounters* __restrict__ cnt, const long long QSB,
+    const unsigned char* __restrict__ qflat, const double* __restrict__ w, const double dtdx0, const double dtdx1,
+    const double dtdx2, const double* __restrict__ dtdx_dev, const __grid_constant__ DevTables T) {
+  using PH = Phys<SYS, D>;
+  constexpr int NV = PH::NV, N = M + 1, NS = ipow_c(N, D), NT = NS / N;
+  static_assert(D == 3 && NS <= 32 && NS > 16, "one cell per warp");
+  constexpr int G = 32;
+  constexpr int KP = pow2_at_least(D * NV);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int p = lane;
+  const unsigned r = blockIdx.x * WARPS + warp;
+  const unsigned ex = (unsigned)E.ext[0], ez = (unsigned)E.ext[2];
+  const unsigned t = r / ex;
+  const int x = (int)(r - t * ex);
+  const int yi = (int)(t % YC);
+  const unsigned t2 = t / YC;
+  const unsigned yb = t2 / ez;
+  const int z = (int)(t2 - yb * ez);
+  const int y = (int)(yb * YC + yi);
+  const bool ok = y < E.ext[1];
+  const int cx = E.lo[0] + x, cy = E.lo[1] + y, cz = E.lo[2] + z;
+  const long long cR = ok ? cx + cy * sy + cz * sz : 0;
+  const int zH = H;
+  const bool inx = cx < H + n0, iny = cy < H + n1, inz = cz < zH + n2;
+  const bool pok = p < NS;
+  const bool fok[3] = {ok && iny && inz && pok, ok && inx && inz && pok, ok && inx && iny && pok};
+  const int ps = pok ? p : 0;
+  const int s = ps / NT, tt = ps - (ps / NT) * NT;
+  double wt = T.w[s] * T.w[tt % N];
+  wt *= T.w[tt / N];
+  constexpr int K = D * NV;
+  const long long BLK = QSB;
+  __shared__ double red[WARPS][K][G + 1];
+  __shared__ double tabs[WARPS][2][NV * NS];
+  double(*rb)[G + 1] = red[warp];
+  double* tab0 = tabs[warp][0];
+  double* tab1 = tabs[warp][1];
+  const double dtdx[3] = {dtdx_dev ? dtdx_dev[0] : dtdx0, dtdx_dev ? dtdx_dev[1] : dtdx1,
+                          dtdx_dev ? dtdx_dev[2] : dtdx2};
+  const long long nstr[3] = {1, sy, sz};
+  // flags of the cell and its three lower neighbours (warp-uniform)
+  const bool fo = ok && qflat[cR] != 0;
+  bool fnb[3];
+#pragma unroll
+  for (int d = 0; d < D; ++d) fnb[d] = ok && qflat[cR - nstr[d]] != 0;
+  // G of node p of a flat cell with state ws into a table
+  auto build = [&](double* tab, const double (&ws)[NV]) -> bool {
+    bool okb = true;
+    if (pok) {
+      const int ia[3] = {p % N, (p / N) % N, p / (N * N)};
+      double Drow[D][N], g[NV];
+#pragma unroll
+      for (int d = 0; d < D; ++d)
+#pragma unroll
+        for (int j = 0; j < N; ++j) Drow[d][j] = T.D[ia[d]][j];
+      okb = flat_cell_G<D, M, SYS>(ws, Drow, dtdx, gamma, ch, g);
+#pragma unroll
+      for (int v = 0; v < NV; ++v) tab[v * NS + p] = g[v];
+    }
+    return okb;
+  };
+  double wo[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) wo[v] = fo ? __ldg(w + cR * (NV * NS) + v * NS) : 0.0;
+  if (fo) (void)build(tab0, wo);   // (an inadmissible w was already reported by the predictor)
+  __syncwarp();
+  double v[KP];
+  bool good = true;
+  const double* qown = q + cR * BLK;
+  auto face = [&](auto dirc, bool tlo, bool thi, bool rlo, bool rhi, double* val) {
+    constexpr int DIR = decltype(dirc)::value;
+    const long long cN = cR - nstr[DIR];
+    double wn[NV];
+    bool shared_tab = false;
+    if (fnb[DIR]) {
+      bool same = fo;
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        wn[i] = __ldg(w + cN * (NV * NS) + i * NS);
+        same &= __double_as_longlong(wn[i]) == __double_as_longlong(wo[i]);
+      }
+      shared_tab = same;
+      if (!same) {
+        __syncwarp();            // the previous face's reads of tab1 are done
+        (void)build(tab1, wn);
+        __syncwarp();
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < NV; ++i) val[i] = 0.0;
+    if (!fok[DIR]) return;
+    double a[NV], b[NV];
+    if (fnb[DIR]) flat_trace<D, M, NV, DIR>(shared_tab ? tab0 : tab1, wn, ps, T.psi1, T, a);
+    else face_trace<D, M, NV, DIR, true>(q + cN * BLK, ps, T.psi1, a);
+    if (fo) flat_trace<D, M, NV, DIR>(tab0, wo, ps, T.psi0, T, b);
+    else face_trace<D, M, NV, DIR, true>(qown, ps, T.psi0, b);
+    good &= point_flux_states<D, SYS, DIR, FLUX>(a, b, tlo, thi, rlo, rhi, wt, gamma, ch, T, val);
+  };
+  face(std::integral_constant<int, 0>{}, (bmask & 1) && cx == H, (bmask & 2) && cx == H + n0, (rmask & 1) && cx == H,
+       (rmask & 2) && cx == H + n0, v);
+  face(std::integral_constant<int, 1>{}, (bmask & 4) && cy == H, (bmask & 8) && cy == H + n1, (rmask & 4) && cy == H,
+       (rmask & 8) && cy == H + n1, v + NV);
+  face(std::integral_constant<int, 2>{}, (bmask & 16) && cz == zH, (bmask & 32) && cz == zH + n2,
+       (rmask & 16) && cz == zH, (rmask & 32) && cz == zH + n2, v + 2 * NV);
+  if (!good) record_error(cnt, 1, 2, cR);
   if (pok) {
 #pragma unroll
     for (int i = 0; i < K; ++i) rb[i][p] = v[i];
@@ -612,15 +780,15 @@ void launch_weno_sweep(const KCtx& k, int sweep, const double* src, double* dst,
 
 void launch_predictor(const KCtx& k, const double* w, double* q, const Box& region, const double dtdx[3],
                       double tol, int max_sweeps, DevCounters* cnt, const double* dtdx_dev, long long qs, bool guess,
-                      const StepState* gst, double guess_r) {
+                      const StepState* gst, double guess_r, unsigned char* qflat) {
   launch_predictor_list(k, w, q, region, nullptr, 0, dtdx, tol, max_sweeps, cnt, nullptr, dtdx_dev, qs, guess, gst,
-                        guess_r);
+                        guess_r, nullptr, qflat);
 }
 
 void launch_predictor_list(const KCtx& k, const double* w, double* q, const Box& region, const int* list,
                            long long nlist, const double dtdx[3], double tol, int max_sweeps, DevCounters* cnt,
                            const unsigned char* emask, const double* dtdx_dev, long long qs, bool guess,
-                           const StepState* gst, double guess_r, const int* slot) {
+                           const StepState* gst, double guess_r, const int* slot, unsigned char* qflat) {
   const long long count = list ? nlist : region.count();
   if (count == 0) return;
   ADER_DISPATCH(k.D, k.M, k.SYS, {
@@ -647,15 +815,38 @@ void launch_predictor_list(const KCtx& k, const double* w, double* q, const Box&
     count_launch(k);
     kern<<<g, kPredWarps * 32, sm, k.stream>>>(w, q, region, k.sy, k.sz, dtdx[0], dtdx[1], dtdx[2], k.gamma,
                                                 k.ch, tol, max_sweeps, cnt, list, nlist, emask, dtdx_dev, qstride, guess ? 1 : 0,
-                                                gst, guess_r, slot, pred_flat_enabled() ? 1 : 0, k.tab);
+                                                gst, guess_r, slot, pred_flat_enabled() ? 1 : 0, (pred_flat_enabled() && !guess) ? qflat : nullptr,
+                                                k.tab);
   });
 }
 
 namespace {
 template <int D, int M, int SYS>
 void flux_cells_for(const KCtx& k, const double* q, double* F, const Box& ext, int H, const int n[3], int bmask,
-                    int rmask, DevCounters* cnt, long long qs) {
+                    int rmask, DevCounters* cnt, long long qs, const unsigned char* qflat, const double* w,
+                    const double* dtdx, const double* dtdx_dev) {
   constexpr int YC = 16;
+  if constexpr (D == 3 && M == 2) {
+    if (qflat) {   // flat cells rebuilt from w (one cell per warp)
+      const long long ychf = (ext.ext[1] + YC - 1) / YC;
+      const long long groupsf = (long long)ext.ext[0] * ychf * YC * ext.ext[2];
+      count_launch(k);
+      const unsigned gf = grid_for(groupsf, kFluxWarps);
+      const double d0 = dtdx ? dtdx[0] : 0.0, d1 = dtdx ? dtdx[1] : 0.0, d2 = dtdx ? dtdx[2] : 0.0;
+      if constexpr (SYS == 0) {
+        if (k.tab.flux == 1) {
+          k_face_flux_cells_flat<D, M, SYS, kFluxWarps, YC, 1><<<gf, kFluxWarps * 32, 0, k.stream>>>(
+              q, F, ext, H, n[0], n[1], n[2], k.sy, k.sz, k.ncell, k.gamma, k.ch, bmask, rmask, cnt, qs, qflat, w, d0,
+              d1, d2, dtdx_dev, k.tab);
+          return;
+        }
+      }
+      k_face_flux_cells_flat<D, M, SYS, kFluxWarps, YC, 0><<<gf, kFluxWarps * 32, 0, k.stream>>>(
+          q, F, ext, H, n[0], n[1], n[2], k.sy, k.sz, k.ncell, k.gamma, k.ch, bmask, rmask, cnt, qs, qflat, w, d0, d1,
+          d2, dtdx_dev, k.tab);
+      return;
+    }
+  }
   constexpr int NS = ipow_c(M + 1, D);
   constexpr int CPW = 32 / ((NS <= 8) ? 8 : (NS <= 16 ? 16 : 32));
   const long long ych = (ext.ext[1] + YC - 1) / YC;
@@ -675,9 +866,11 @@ void flux_cells_for(const KCtx& k, const double* q, double* F, const Box& ext, i
 }  // namespace
 
 void launch_face_flux_cells(const KCtx& k, const double* q, double* F, const Box& ext, int H, const int n[3],
-                            int bmask, int rmask, DevCounters* cnt, long long qs) {
+                            int bmask, int rmask, DevCounters* cnt, long long qs, const unsigned char* qflat,
+                            const double* w, const double* dtdx, const double* dtdx_dev) {
   if (ext.count() == 0) return;
-  ADER_DISPATCH(k.D, k.M, k.SYS, (flux_cells_for<D, M, SYS>(k, q, F, ext, H, n, bmask, rmask, cnt, qs)));
+  ADER_DISPATCH(k.D, k.M, k.SYS,
+                (flux_cells_for<D, M, SYS>(k, q, F, ext, H, n, bmask, rmask, cnt, qs, qflat, w, dtdx, dtdx_dev)));
 }
 
 void launch_update(const KCtx& k, double* u, const double* F, const Box& R, const double dtdx[3],

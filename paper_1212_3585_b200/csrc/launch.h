@@ -31,6 +31,7 @@ struct DevCounters {              // device-resident, zeroed by the host
   int pad;
   unsigned long long err_any;     // multi-rank: max over the ranks of err_code (set before every
                                   // host check, so all ranks stop at the same step)
+  unsigned long long flat_cells;  // predicted cells flagged flat (no q block written)
 };
 
 // Device-resident step control of the uniform path: the time step is formed
@@ -70,12 +71,16 @@ void launch_weno_sweep(const KCtx& k, int sweep, const double* src, double* dst,
 // device (StepState::dtdx) instead of dtdx.
 // qs: stride of a cell's q block in doubles (0 = nu N^(d+1); the uniform path
 // uses q_block_stride, the block size rounded up to even).
+// qflat (optional, [padded cell], M = 2, no guess): cells whose nodes all carry the same w and
+// that converge in the first sweep get qflat[cell] = 1 and NO q block (q_h = w - Tsum[s] G(node),
+// rebuilt from w by launch_face_flux_cells); every other predicted cell gets 0 and its block.
 // guess (reading R25): start the Picard iteration from the cell's previous q
 // (read in place from q) extrapolated by r = dt_n / dt_{n-1}: r from gst
 // (device StepState: dt / prev_dt) if given, else guess_r; r <= 0 = R3.
 void launch_predictor(const KCtx& k, const double* w, double* q, const Box& region, const double dtdx[3],
                       double tol, int max_sweeps, DevCounters* cnt, const double* dtdx_dev = nullptr,
-                      long long qs = 0, bool guess = false, const StepState* gst = nullptr, double guess_r = 0.0);
+                      long long qs = 0, bool guess = false, const StepState* gst = nullptr, double guess_r = 0.0,
+                      unsigned char* qflat = nullptr);
 // Predictor on the cells of an id list (AMR levels): w, q indexed by id (or by
 // slot[id] if given).  If emask is given only cells with emask[id] != 0 report
 // solver errors.
@@ -83,15 +88,19 @@ void launch_predictor_list(const KCtx& k, const double* w, double* q, const Box&
                            long long nlist, const double dtdx[3], double tol, int max_sweeps, DevCounters* cnt,
                            const unsigned char* emask = nullptr, const double* dtdx_dev = nullptr,
                            long long qs = 0, bool guess = false, const StepState* gst = nullptr,
-                           double guess_r = 0.0, const int* slot = nullptr);
+                           double guess_r = 0.0, const int* slot = nullptr, unsigned char* qflat = nullptr);
 // Face fluxes on the lower face of every cell of `ext` (owned block + 1 on each
 // active axis), one lane group per cell computing all its lower faces
 // (L2-friendly traversal).  bmask bit 2*dir (2*dir+1): the first (last) face
 // along dir is a physical transmissive boundary and takes the interior trace
 // on both sides; rmask, same bits: a reflective wall (R22), the exterior state
 // is the interior trace with the normal momentum negated.
+// qflat / w / dtdx (optional, D = 3, M = 2): the flags launch_predictor left, its w array and the
+// dt/dx it used (dtdx_dev: read from the device instead) — flat cells' traces come from w.
 void launch_face_flux_cells(const KCtx& k, const double* q, double* F, const Box& ext, int H, const int n[3],
-                            int bmask, int rmask, DevCounters* cnt, long long qs);
+                            int bmask, int rmask, DevCounters* cnt, long long qs,
+                            const unsigned char* qflat = nullptr, const double* w = nullptr,
+                            const double* dtdx = nullptr, const double* dtdx_dev = nullptr);
 // The same fluxes (bitwise) with the q blocks streamed into shared memory by
 // bulk copies (flux_tma.cu); q blocks at stride q_block_stride(D, M, SYS).
 void launch_face_flux_tma(const KCtx& k, const double* q, double* F, const Box& ext, int H, const int n[3],

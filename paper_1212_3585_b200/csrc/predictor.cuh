@@ -59,6 +59,35 @@ struct PredLane {
   }
 };
 
+// Flat cell (every node carries the same w): G = sum_dir D_dir f*_dir at the node
+// whose rows of the differentiation matrix are Drow — f*_dir is one value per
+// variable and direction, contracted in the order of the general path.  The
+// predictor's flat first sweep and the face-flux kernel (which rebuilds a flat
+// cell's q_h = w - Tsum[s] G from w instead of reading it) both call this.
+template <int D, int M, int SYS>
+__device__ __forceinline__ bool flat_cell_G(const double (&w)[Phys<SYS, D>::NV], const double (&Drow)[D][M + 1],
+                                            const double (&dtdx)[3], double gamma, double ch,
+                                            double (&G)[Phys<SYS, D>::NV]) {
+  using PH = Phys<SYS, D>;
+  constexpr int NV = PH::NV, N = M + 1;
+  double f[D][NV];
+  const bool ok = PH::fluxes(w, gamma, ch, f);
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    double g = 0.0;
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const double fs = dtdx[d] * f[d][v];
+#pragma unroll
+      for (int j = 0; j < N; ++j) g = fma(Drow[d][j], fs, g);
+    }
+    G[v] = g;
+  }
+  return ok;
+}
+// time level s of a flat cell's first-sweep iterate: q^1_s = w - Tsum[s] G
+__device__ __forceinline__ double flat_cell_q(double w, double tsum, double G) { return fma(-tsum, G, w); }
+
 // Picard iteration of one cell per lane group (all 32 lanes of the warp call
 // it together, with the same from_guess; cell_ok false for a lane group without a cell).  wv: this
 // node's w (eqn.weno.z); on return qv holds the node's time pencil, nsw the
@@ -89,7 +118,8 @@ __device__ __forceinline__ void predictor_cell(const double (&wv)[Phys<SYS, D>::
                                                const PredLane<D, M, SYS>& L, const double (&dtdx)[3], bool cell_ok,
                                                double gamma, double ch, double tol, int max_sweeps,
                                                const DevTables& T, int& nsw, bool& conv, bool& bad,
-                                               bool from_guess = false, bool flat_en = false) {
+                                               bool from_guess = false, bool flat_en = false,
+                                               bool* was_flat = nullptr) {
   using PH = Phys<SYS, D>;
   using C = PredCfg<D, M, SYS, PERS>;
   constexpr int NV = C::NV, N = C::N, NS = C::NS, G = C::G;
@@ -123,6 +153,7 @@ __device__ __forceinline__ void predictor_cell(const double (&wv)[Phys<SYS, D>::
     }
     flat_warp = __all_sync(0xffffffffu, same || !(cell_ok && lane_ok));
   }
+  if (was_flat) *was_flat = flat_warp && max_sweeps >= 1;
   // one Picard sweep; FIRST: the iterate is the time-constant guess (one flux level)
   auto sweep_once = [&](auto first_tag) {
     constexpr bool FIRST = decltype(first_tag)::value;
@@ -190,19 +221,10 @@ __device__ __forceinline__ void predictor_cell(const double (&wv)[Phys<SYS, D>::
     };
     if (M == 2 && FIRST && flat_warp) {
       if (live && lane_ok) {
-        double f[D][NV];
-        bad |= !PH::fluxes(wv, gamma, ch, f);
+        double g[NV];
+        bad |= !flat_cell_G<D, M, SYS>(wv, L.Drow, dtdx, gamma, ch, g);
 #pragma unroll
-        for (int v = 0; v < NV; ++v) {
-          double g = 0.0;
-#pragma unroll
-          for (int d = 0; d < D; ++d) {
-            const double fs = dtdx[d] * f[d][v];
-#pragma unroll
-            for (int j = 0; j < N; ++j) g += L.Drow[d][j] * fs;
-          }
-          Gs[v][0] = g;
-        }
+        for (int v = 0; v < NV; ++v) Gs[v][0] = g[v];
       }
     } else if constexpr (XMMA) {
 #pragma unroll
@@ -263,7 +285,7 @@ __device__ __forceinline__ void predictor_cell(const double (&wv)[Phys<SYS, D>::
         for (int s = 0; s < N; ++s) {
           double acc;
           if (FIRST) {
-            acc = wv[v] - T.Tsum[s] * Gs[v][0];
+            acc = flat_cell_q(wv[v], T.Tsum[s], Gs[v][0]);   // = w - Tsum[s] G, one rounding
           } else {
             acc = wv[v];
 #pragma unroll
