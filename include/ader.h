@@ -127,11 +127,10 @@ typedef struct {
                                    * threshold comparison came to flipping
                                    * a refinement decision; 1e300 if no adapt ran     */
   int64_t pred_flat_cells;        /* of pred_cells: cells whose nodes all carried the same
-                                   * reconstruction w and that converged in the first
-                                   * Picard sweep (eqn.stdg.final P:463-474 with the
-                                   * time-constant guess, R3) — the uniform 3D M = 2 path
-                                   * stores a flag instead of their q_h block and the face
-                                   * flux rebuilds q_h = w - Tsum G from w (ABI 6)      */
+                                   * reconstruction w bit for bit and that converged in the
+                                   * first Picard sweep (eqn.stdg.final P:463-474 with the
+                                   * time-constant guess, R3; counted at M = 2) — how much
+                                   * of the workload is constant-state streaming (ABI 6)  */
 } ader_step_report;
 
 /* One cell as exported by ader_get_cells: parity key (level, idx, status). */

@@ -569,9 +569,11 @@ int boundary_mask(const ader_ctx* c, int bc) {
 int transmissive_mask(const ader_ctx* c) { return boundary_mask(c, ADER_BC_TRANSMISSIVE); }
 int reflective_mask(const ader_ctx* c) { return boundary_mask(c, ADER_BC_REFLECTIVE); }
 
-// ADER_PRED_FLAT_SKIP=0: every predicted cell gets its q block (A/B; bitwise the same F and state)
+// ADER_PRED_FLAT_SKIP=1 (3D M = 2, opt-in): flat cells get a flag instead of their q block and the
+// face-flux kernel rebuilds their q_h from w — bitwise the same F and state, but measured slower at
+// C4 (the flux turns FP64-bound: 36 vs 29 ms), so every block is written by default
 bool flat_skip_env() {
-  static const bool on = !(std::getenv("ADER_PRED_FLAT_SKIP") && std::getenv("ADER_PRED_FLAT_SKIP")[0] == '0') &&
+  static const bool on = (std::getenv("ADER_PRED_FLAT_SKIP") && std::getenv("ADER_PRED_FLAT_SKIP")[0] == '1') &&
                          !(std::getenv("ADER_PRED_FLAT") && std::getenv("ADER_PRED_FLAT")[0] == '0') &&
                          !(std::getenv("ADER_FLUX_TMA") && std::getenv("ADER_FLUX_TMA")[0] == '1') &&
                          !(std::getenv("ADER_FLUX_ROT") && std::getenv("ADER_FLUX_ROT")[0] == '1');
@@ -1036,7 +1038,7 @@ static ader_status create_impl(const ader_config* cfg, ader_ctx** out, bool loop
   c->qs = q_block_stride(c->d, c->M, c->cfg.system);
   CK(alloc(&c->q, nc * c->qs));
   CK(alloc(&c->F, nc * c->nv * c->d));
-  if (c->d == 3 && c->M == 2) {   // flat-cell flags (cells outside the predictor's region stay 0)
+  if (c->d == 3 && c->M == 2 && flat_skip_env()) {   // flat-cell flags (cells outside the predictor's region stay 0)
     CK(cudaMalloc(&c->qflat, nc));
     CK(cudaMemset(c->qflat, 0, nc));
   }

@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(WARPS * 32, (SYS == 0) ? 4 : 2) k_predictor(
     if (node == 0) {
       acc_sweeps += (unsigned long long)nsw;
       acc_cells += 1ull;
-      acc_flat += skipq ? 1ull : 0ull;
+      acc_flat += (was_flat && conv && !bad && nsw == 1) ? 1ull : 0ull;
       acc_max = nsw > acc_max ? nsw : acc_max;
     }
   }
