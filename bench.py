@@ -402,24 +402,28 @@ def main():
         if kl[ader.K_PRED]:
             # algorithmic bytes of one predictor launch: read w, write q of every predicted cell
             cells_per_launch = rep.pred_cells / max(1, args.steps) / max(1e-9, kl[ader.K_PRED] / nprof)
-            # flat cells (ader_step_report.pred_flat_cells) get a one-byte flag instead of a q block
-            flat_frac = rep.pred_flat_cells / max(1, rep.pred_cells)
+            # opt-in ADER_PRED_FLAT_SKIP=1 (3D M = 2): flat cells get a one-byte flag instead of a q block
+            skip_on = os.environ.get("ADER_PRED_FLAT_SKIP") == "1" and wl.dim == 3 and wl.degree == 2
+            flat_frac = rep.pred_flat_cells / max(1, rep.pred_cells) if skip_on else 0.0
             entries.append(entry("stdg_predictor", kms[ader.K_PRED] / kl[ader.K_PRED],
                                  kfl[ader.K_PRED] / kl[ader.K_PRED],
                                  cells_per_launch * (nvv * N ** wl.dim * 8
                                                      + (1.0 - flat_frac) * nvv * N ** (wl.dim + 1) * 8 + flat_frac),
-                                 "algorithmic bytes (w read per predicted cell + q written per cell that is not "
-                                 f"flat: {1.0 - flat_frac:.4f} of them) / CUDA-event time",
+                                 "algorithmic bytes (w read per predicted cell + q written per cell"
+                                 + (f" that is not flat: {1.0 - flat_frac:.4f} of them" if skip_on else "")
+                                 + ") / CUDA-event time",
                                  sweeps_note + " / CUDA-event time"))
         if wl.lmax == 0 and kl[ader.K_FLUX] and not kl[ader.K_PRED_FLUX]:
             # face flux: algorithmic bytes = every q read once + F written
-            flat_frac = rep.pred_flat_cells / max(1, rep.pred_cells)
+            skip_on = os.environ.get("ADER_PRED_FLAT_SKIP") == "1" and wl.dim == 3 and wl.degree == 2
+            flat_frac = rep.pred_flat_cells / max(1, rep.pred_cells) if skip_on else 0.0
             entries.append(entry(f"face_flux_{args.flux}", kms[ader.K_FLUX] / kl[ader.K_FLUX],
                                  kfl[ader.K_FLUX] / kl[ader.K_FLUX],
                                  ext * ((1.0 - flat_frac) * nvv * N ** (wl.dim + 1) * 8 + flat_frac * (nvv * 8 + 1)
                                         + nvv * wl.dim * 8),
-                                 "algorithmic bytes (the q block of each cell that is not flat read once, w and "
-                                 f"the flag of a flat cell ({flat_frac:.4f} of them), F written) / CUDA-event time",
+                                 ("algorithmic bytes (the q block of each cell that is not flat read once, w and "
+                                  f"the flag of a flat cell ({flat_frac:.4f} of them), F written) / CUDA-event time")
+                                 if skip_on else "algorithmic bytes (each q read once, F written) / CUDA-event time",
                                  "algorithmic FP64 flops of the face quadrature / CUDA-event time"))
         if kl[ader.K_PRED_FLUX]:
             # fused a2 + a3 walk (+ its tile-face kernel): w read, F written; q never leaves the SM
