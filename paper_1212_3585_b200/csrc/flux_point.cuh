@@ -72,6 +72,44 @@ __device__ __forceinline__ void face_trace(const double* q0, int p, const double
   }
 }
 
+// Both x traces of a block at the face point p: out0 = sum_a psi0[a] q[..a..]
+// (xi = 0) and out1 = sum_a psi1[a] q[..a..] (xi = 1) from ONE set of loads —
+// the same loads, products and order as face_trace<.., 0, true> gives for each.
+template <int D, int M, int NV>
+__device__ __forceinline__ void face_trace_x_both(const double* q0, int p, const double (&psi0)[kMaxN],
+                                                  const double (&psi1)[kMaxN], double (&out0)[NV],
+                                                  double (&out1)[NV]) {
+  constexpr int N = M + 1, NS = ipow_c(N, D), NST = NS * N, NT = NS / N;
+  const int s = p / NT, t = p - s * NT;
+  const int t1 = t % N, t2 = t / N;
+  const double* q = q0 + s * NS + t1 * N + (D == 3 ? t2 * N * N : 0);
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    const double* pc = q + v * NST;
+    double x[N];
+    if constexpr (N == 4) {
+      const double2 lo = __ldg(reinterpret_cast<const double2*>(pc));
+      const double2 hi = __ldg(reinterpret_cast<const double2*>(pc + 2));
+      x[0] = lo.x; x[1] = lo.y; x[2] = hi.x; x[3] = hi.y;
+    } else if constexpr (N == 3) {
+      const bool odd = (reinterpret_cast<uintptr_t>(pc) & 8) != 0;
+      const double2 pr = __ldg(reinterpret_cast<const double2*>(pc + (odd ? 1 : 0)));
+      const double sg = __ldg(pc + (odd ? 0 : 2));
+      x[0] = odd ? sg : pr.x;
+      x[1] = odd ? pr.x : pr.y;
+      x[2] = odd ? pr.y : sg;
+    } else {
+#pragma unroll
+      for (int k = 0; k < N; ++k) x[k] = __ldg(pc + k);
+    }
+    double a = psi0[0] * x[0], b = psi1[0] * x[0];
+#pragma unroll
+    for (int k = 1; k < N; ++k) { a += psi0[k] * x[k]; b += psi1[k] * x[k]; }
+    out0[v] = a;
+    out1[v] = b;
+  }
+}
+
 // The two-point flux of one face point from the raw traces a (q_h^-, xi = 1 of
 // the lower cell) and b (q_h^+, xi = 0 of the upper cell), with the boundary
 // flags of the face, times the quadrature weight wt.

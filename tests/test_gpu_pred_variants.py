@@ -89,3 +89,12 @@ def test_rotation_shuffle_flux_matches_gather_flux(tmp_path):
             continue
         d = np.abs(a[k] - b[k]).max()
         assert d <= 1e-13 * max(np.abs(a[k]).max(), 1e-300), (k, d)
+
+
+def test_x_run_flux_bitwise_equals_cell_flux(tmp_path):
+    """3D M = 2 Euler/Rusanov default: the face-flux kernel that walks runs of 8 cells along x and carries the
+    xi = 1 trace (flux:F/G/H P:158-172, eqn.rusanov) gives bitwise the F, q and states of
+    k_face_flux_cells (ADER_FLUX_RUNS=0), on explosions with transmissive sides and walls."""
+    a, b = _ab("flux_ab.py", tmp_path, "ADER_FLUX_RUNS", ("0", "5"))
+    for k in a.files:
+        assert np.array_equal(a[k], b[k]), k
