@@ -936,18 +936,24 @@ void flux_cells_for(const KCtx& k, const double* q, double* F, const Box& ext, i
     }();
     // x runs of 8 cells (default; ADER_FLUX_RUNS=0: k_face_flux_cells, 5..7: CTAs/SM of the register budget)
     if (runs > 0 && !qflat && k.tab.flux == 0) {
-      constexpr int RL = 8;
-      const unsigned nrx = (unsigned)((ext.ext[0] + RL - 1) / RL);
+      static const int rl = [] {
+        const char* e = std::getenv("ADER_FLUX_RL");
+        return (e && e[0]) ? std::atoi(e) : 8;
+      }();
+      const int RLv = rl >= 16 ? 16 : 8;
+      const unsigned nrx = (unsigned)((ext.ext[0] + RLv - 1) / RLv);
       const long long ychr = (ext.ext[1] + YC - 1) / YC;
       const long long groupsr = (long long)nrx * ychr * YC * ext.ext[2];
       count_launch(k);
       const unsigned gr = grid_for(groupsr, kFluxWarps);
-#define ADER_RUNS(MB_)                                                                                          \
-  k_face_flux_runs<D, M, SYS, kFluxWarps, YC, 0, RL, MB_><<<gr, kFluxWarps * 32, 0, k.stream>>>(                \
+#define ADER_RUNS(RL_, MB_)                                                                                     \
+  k_face_flux_runs<D, M, SYS, kFluxWarps, YC, 0, RL_, MB_><<<gr, kFluxWarps * 32, 0, k.stream>>>(               \
       q, F, ext, H, n[0], n[1], n[2], k.sy, k.sz, k.ncell, k.gamma, k.ch, bmask, rmask, cnt, qs, nrx, k.tab)
-      if (runs >= 7) ADER_RUNS(7);
-      else if (runs == 6) ADER_RUNS(6);
-      else ADER_RUNS(5);
+      if (RLv == 16) { if (runs <= 4) ADER_RUNS(16, 4); else ADER_RUNS(16, 5); }
+      else if (runs >= 7) ADER_RUNS(8, 7);
+      else if (runs == 6) ADER_RUNS(8, 6);
+      else if (runs == 5) ADER_RUNS(8, 5);
+      else ADER_RUNS(8, 4);
 #undef ADER_RUNS
       return;
     }
