@@ -326,33 +326,41 @@ __global__ void __launch_bounds__(WARPS * 32, (FLUX == 1) ? 5 : (SYS == 1 ? 4 : 
   const int s = ps / NT, tt = ps - (ps / NT) * NT;
   double wt = T.w[s] * T.w[tt % N];
   if (D == 3) wt *= T.w[tt / N];
-  double v[KP];
+  double v[NV];
   bool good = true;
   constexpr int K = D * NV;
   const long long BLK = QSB;   // block stride
+  // point sums through shared memory: lane p stores its K = D*NV weighted
+  // point fluxes in column p — each direction's as soon as they are formed, so
+  // no K-value accumulator stays live across the faces — then lane i sums row
+  // i over the NS points in order (rows padded to G+1 doubles: conflict-free
+  // column writes and row reads)
+  __shared__ double red[WARPS * CPW][K][G + 1];
+  double(*rb)[G + 1] = red[warp * CPW + lane / G];
+  auto put = [&](int row0) {
+    if (pok) {
+#pragma unroll
+      for (int i = 0; i < NV; ++i) rb[row0 + i][p] = v[i];
+    }
+  };
   // (tried and removed: staging the cell's own block in shared memory (1.6x
   // slower, bank conflicts) and an L1 prefetch of the D+1 blocks (8 % slower))
   const double* qown = q + cR * BLK;
   good &= point_flux_blocks<D, M, SYS, 0, FLUX, true>(
       q + (cR - 1) * BLK, qown, ps, fok[0], (bmask & 1) && cx == H, (bmask & 2) && cx == H + n0,
       (rmask & 1) && cx == H, (rmask & 2) && cx == H + n0, wt, gamma, ch, T, v);
+  put(0);
   good &= point_flux_blocks<D, M, SYS, 1, FLUX, true>(
       q + (cR - sy) * BLK, qown, ps, fok[1], (bmask & 4) && cy == H, (bmask & 8) && cy == H + n1,
-      (rmask & 4) && cy == H, (rmask & 8) && cy == H + n1, wt, gamma, ch, T, v + NV);
-  if constexpr (D == 3)
+      (rmask & 4) && cy == H, (rmask & 8) && cy == H + n1, wt, gamma, ch, T, v);
+  put(NV);
+  if constexpr (D == 3) {
     good &= point_flux_blocks<D, M, SYS, 2, FLUX, true>(
         q + (cR - sz) * BLK, qown, ps, fok[2], (bmask & 16) && cz == zH, (bmask & 32) && cz == zH + n2,
-        (rmask & 16) && cz == zH, (rmask & 32) && cz == zH + n2, wt, gamma, ch, T, v + 2 * NV);
-  if (!good) record_error(cnt, 1, 2, cR);
-  // point sums through shared memory: lane p stores its K = D*NV weighted
-  // point fluxes in column p, then lane i sums row i over the NS points in
-  // order (rows padded to G+1 doubles: conflict-free column writes and row reads)
-  __shared__ double red[WARPS * CPW][K][G + 1];
-  double(*rb)[G + 1] = red[warp * CPW + lane / G];
-  if (pok) {
-#pragma unroll
-    for (int i = 0; i < K; ++i) rb[i][p] = v[i];
+        (rmask & 16) && cz == zH, (rmask & 32) && cz == zH + n2, wt, gamma, ch, T, v);
+    put(2 * NV);
   }
+  if (!good) record_error(cnt, 1, 2, cR);
   __syncwarp();
   for (int i = p; i < K; i += G) {
     double acc = rb[i][0];

@@ -13,6 +13,9 @@ sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(_
 from paper_1212_3585_b200 import ader  # noqa: E402
 from paper_1212_3585_b200 import workloads as W  # noqa: E402
 
+if __import__("os").environ.get("ADER_AB_LIB"):   # A/B against another build of the library
+    ader.LIB_PATH = __import__("os").environ["ADER_AB_LIB"]
+
 CASES = {
     "c4_expl3d_24": dict(cfg=dict(dim=3, degree=2, n0=(24, 20, 22), lo=(-1,) * 3, hi=(1,) * 3, bc=(1,) * 6, cfl=0.3),
                          ic=lambda: W.explosion(3), steps=3),
