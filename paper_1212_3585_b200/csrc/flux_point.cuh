@@ -113,7 +113,8 @@ __device__ __forceinline__ void face_trace_x_both(const double* q0, int p, const
 // The two-point flux of one face point from the raw traces a (q_h^-, xi = 1 of
 // the lower cell) and b (q_h^+, xi = 0 of the upper cell), with the boundary
 // flags of the face, times the quadrature weight wt.
-template <int D, int SYS, int DIR, int FLUX>
+// (INTERIOR: the caller knows that none of the four boundary flags is set — no selects)
+template <int D, int SYS, int DIR, int FLUX, bool INTERIOR = false>
 __device__ __forceinline__ bool point_flux_states(const double (&a)[Phys<SYS, D>::NV], const double (&b)[Phys<SYS, D>::NV],
                                                   bool tlo, bool thi, bool rlo, bool rhi, double wt, double gamma,
                                                   double ch, const DevTables& T, double* val) {
@@ -122,13 +123,13 @@ __device__ __forceinline__ bool point_flux_states(const double (&a)[Phys<SYS, D>
   double um[NV], up[NV];
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
-    um[v] = (tlo || rlo) ? b[v] : a[v];   // transmissive boundary: interior trace on both sides (R5)
-    up[v] = (thi || rhi) ? a[v] : b[v];
+    um[v] = (!INTERIOR && (tlo || rlo)) ? b[v] : a[v];   // transmissive boundary: interior trace on both sides (R5)
+    up[v] = (!INTERIOR && (thi || rhi)) ? a[v] : b[v];
   }
   // reflective wall (R22): the exterior state is the interior trace with the
   // normal momentum negated
-  if (rlo) um[1 + DIR] = -um[1 + DIR];
-  if (rhi) up[1 + DIR] = -up[1 + DIR];
+  if (!INTERIOR && rlo) um[1 + DIR] = -um[1 + DIR];
+  if (!INTERIOR && rhi) up[1 + DIR] = -up[1 + DIR];
   // equal traces (e.g. inside a constant region): eqn.rusanov and eqn.osher
   // reduce exactly to f(q) — 0.5 (f + f) = f and the dissipation term is 0 — so one flux
   // evaluation gives the bitwise-identical result
@@ -162,7 +163,7 @@ __device__ __forceinline__ bool point_flux_states(const double (&a)[Phys<SYS, D>
 // One space-time quadrature point of the face between the cell blocks qL0
 // (lower side) and qR0 (upper side), [NV][N^(D+1)] each, in global (GL_L,
 // GL_R) or shared memory.
-template <int D, int M, int SYS, int DIR, int FLUX, bool GL_L, bool GL_R = GL_L>
+template <int D, int M, int SYS, int DIR, int FLUX, bool GL_L, bool GL_R = GL_L, bool INTERIOR = false>
 __device__ __forceinline__ bool point_flux_blocks(const double* qL0, const double* qR0, int p, bool fok, bool tlo,
                                                   bool thi, bool rlo, bool rhi, double wt, double gamma, double ch,
                                                   const DevTables& T, double* val) {
@@ -176,7 +177,7 @@ __device__ __forceinline__ bool point_flux_blocks(const double* qL0, const doubl
   double a[NV], b[NV];
   face_trace<D, M, NV, DIR, GL_L>(qL0, p, T.psi1, a);   // q_h^- (xi = 1 of the left cell)
   face_trace<D, M, NV, DIR, GL_R>(qR0, p, T.psi0, b);   // q_h^+ (xi = 0 of the right cell)
-  return point_flux_states<D, SYS, DIR, FLUX>(a, b, tlo, thi, rlo, rhi, wt, gamma, ch, T, val);
+  return point_flux_states<D, SYS, DIR, FLUX, INTERIOR>(a, b, tlo, thi, rlo, rhi, wt, gamma, ch, T, val);
 }
 
 }  // namespace ader

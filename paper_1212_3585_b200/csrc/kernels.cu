@@ -346,18 +346,32 @@ __global__ void __launch_bounds__(WARPS * 32, (FLUX == 1) ? 5 : (SYS == 1 ? 4 : 
   // (tried and removed: staging the cell's own block in shared memory (1.6x
   // slower, bank conflicts) and an L1 prefetch of the D+1 blocks (8 % slower))
   const double* qown = q + cR * BLK;
-  good &= point_flux_blocks<D, M, SYS, 0, FLUX, true>(
-      q + (cR - 1) * BLK, qown, ps, fok[0], (bmask & 1) && cx == H, (bmask & 2) && cx == H + n0,
-      (rmask & 1) && cx == H, (rmask & 2) && cx == H + n0, wt, gamma, ch, T, v);
+  // (a face none of whose boundary flags is set takes the point flux without the boundary selects)
+  const int bm = bmask | rmask;
+  if (!(((bm & 1) && cx == H) || ((bm & 2) && cx == H + n0)))
+    good &= point_flux_blocks<D, M, SYS, 0, FLUX, true, true, true>(q + (cR - 1) * BLK, qown, ps, fok[0], false, false,
+                                                                    false, false, wt, gamma, ch, T, v);
+  else
+    good &= point_flux_blocks<D, M, SYS, 0, FLUX, true>(
+        q + (cR - 1) * BLK, qown, ps, fok[0], (bmask & 1) && cx == H, (bmask & 2) && cx == H + n0,
+        (rmask & 1) && cx == H, (rmask & 2) && cx == H + n0, wt, gamma, ch, T, v);
   put(0);
-  good &= point_flux_blocks<D, M, SYS, 1, FLUX, true>(
-      q + (cR - sy) * BLK, qown, ps, fok[1], (bmask & 4) && cy == H, (bmask & 8) && cy == H + n1,
-      (rmask & 4) && cy == H, (rmask & 8) && cy == H + n1, wt, gamma, ch, T, v);
+  if (!(((bm & 4) && cy == H) || ((bm & 8) && cy == H + n1)))
+    good &= point_flux_blocks<D, M, SYS, 1, FLUX, true, true, true>(q + (cR - sy) * BLK, qown, ps, fok[1], false, false,
+                                                                    false, false, wt, gamma, ch, T, v);
+  else
+    good &= point_flux_blocks<D, M, SYS, 1, FLUX, true>(
+        q + (cR - sy) * BLK, qown, ps, fok[1], (bmask & 4) && cy == H, (bmask & 8) && cy == H + n1,
+        (rmask & 4) && cy == H, (rmask & 8) && cy == H + n1, wt, gamma, ch, T, v);
   put(NV);
   if constexpr (D == 3) {
-    good &= point_flux_blocks<D, M, SYS, 2, FLUX, true>(
-        q + (cR - sz) * BLK, qown, ps, fok[2], (bmask & 16) && cz == zH, (bmask & 32) && cz == zH + n2,
-        (rmask & 16) && cz == zH, (rmask & 32) && cz == zH + n2, wt, gamma, ch, T, v);
+    if (!(((bm & 16) && cz == zH) || ((bm & 32) && cz == zH + n2)))
+      good &= point_flux_blocks<D, M, SYS, 2, FLUX, true, true, true>(q + (cR - sz) * BLK, qown, ps, fok[2], false,
+                                                                      false, false, false, wt, gamma, ch, T, v);
+    else
+      good &= point_flux_blocks<D, M, SYS, 2, FLUX, true>(
+          q + (cR - sz) * BLK, qown, ps, fok[2], (bmask & 16) && cz == zH, (bmask & 32) && cz == zH + n2,
+          (rmask & 16) && cz == zH, (rmask & 32) && cz == zH + n2, wt, gamma, ch, T, v);
     put(2 * NV);
   }
   if (!good) record_error(cnt, 1, 2, cR);
@@ -418,6 +432,9 @@ __global__ void __launch_bounds__(WARPS * 32, MB) k_face_flux_runs(
 #pragma unroll
   for (int i = 0; i < NV; ++i) ax[i] = 0.0;
   const long long row = cy * sy + cz * sz;
+  // a boundary flag applies on the y / z faces of this row (uniform over the run)
+  const bool ybnd = (((bmask | rmask) & 4) && cy == H) || (((bmask | rmask) & 8) && cy == H + n1);
+  const bool zbnd = (((bmask | rmask) & 16) && cz == zH) || (((bmask | rmask) & 32) && cz == zH + n2);
 #pragma unroll 1
   for (int c = 0; c < RL; ++c) {
     const int x = x0 + c;
@@ -436,9 +453,12 @@ __global__ void __launch_bounds__(WARPS * 32, MB) k_face_flux_runs(
         double b[NV], an[NV];
         if (c == 0) face_trace<D, M, NV, 0, true>(q + (cR - 1) * BLK, ps, T.psi1, ax);
         face_trace_x_both<D, M, NV>(qown, ps, T.psi0, T.psi1, b, an);
-        good &= point_flux_states<D, SYS, 0, FLUX>(ax, b, (bmask & 1) && cx == H, (bmask & 2) && cx == H + n0,
-                                                   (rmask & 1) && cx == H, (rmask & 2) && cx == H + n0, wt, gamma,
-                                                   ch, T, val);
+        const bool xlo = cx == H, xhi = cx == H + n0;
+        if (!(((bmask | rmask) & 1) && xlo) && !(((bmask | rmask) & 2) && xhi))   // interior face: no selects
+          good &= point_flux_states<D, SYS, 0, FLUX, true>(ax, b, false, false, false, false, wt, gamma, ch, T, val);
+        else
+          good &= point_flux_states<D, SYS, 0, FLUX>(ax, b, (bmask & 1) && xlo, (bmask & 2) && xhi, (rmask & 1) && xlo,
+                                                     (rmask & 2) && xhi, wt, gamma, ch, T, val);
 #pragma unroll
         for (int i = 0; i < NV; ++i) ax[i] = an[i];
       }
@@ -447,16 +467,24 @@ __global__ void __launch_bounds__(WARPS * 32, MB) k_face_flux_runs(
         for (int i = 0; i < NV; ++i) rb[i][p] = val[i];
       }
     }
-    good &= point_flux_blocks<D, M, SYS, 1, FLUX, true>(
-        q + (cR - sy) * BLK, qown, ps, ok && inx && inz && pok, (bmask & 4) && cy == H, (bmask & 8) && cy == H + n1,
-        (rmask & 4) && cy == H, (rmask & 8) && cy == H + n1, wt, gamma, ch, T, val);
+    if (!ybnd)
+      good &= point_flux_blocks<D, M, SYS, 1, FLUX, true, true, true>(q + (cR - sy) * BLK, qown, ps, ok && inx && inz && pok,
+                                                                      false, false, false, false, wt, gamma, ch, T, val);
+    else
+      good &= point_flux_blocks<D, M, SYS, 1, FLUX, true>(
+          q + (cR - sy) * BLK, qown, ps, ok && inx && inz && pok, (bmask & 4) && cy == H, (bmask & 8) && cy == H + n1,
+          (rmask & 4) && cy == H, (rmask & 8) && cy == H + n1, wt, gamma, ch, T, val);
     if (pok) {
 #pragma unroll
       for (int i = 0; i < NV; ++i) rb[NV + i][p] = val[i];
     }
-    good &= point_flux_blocks<D, M, SYS, 2, FLUX, true>(
-        q + (cR - sz) * BLK, qown, ps, ok && inx && iny && pok, (bmask & 16) && cz == zH,
-        (bmask & 32) && cz == zH + n2, (rmask & 16) && cz == zH, (rmask & 32) && cz == zH + n2, wt, gamma, ch, T, val);
+    if (!zbnd)
+      good &= point_flux_blocks<D, M, SYS, 2, FLUX, true, true, true>(q + (cR - sz) * BLK, qown, ps, ok && inx && iny && pok,
+                                                                      false, false, false, false, wt, gamma, ch, T, val);
+    else
+      good &= point_flux_blocks<D, M, SYS, 2, FLUX, true>(
+          q + (cR - sz) * BLK, qown, ps, ok && inx && iny && pok, (bmask & 16) && cz == zH,
+          (bmask & 32) && cz == zH + n2, (rmask & 16) && cz == zH, (rmask & 32) && cz == zH + n2, wt, gamma, ch, T, val);
     if (pok) {
 #pragma unroll
       for (int i = 0; i < NV; ++i) rb[2 * NV + i][p] = val[i];
