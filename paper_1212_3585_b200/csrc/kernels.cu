@@ -52,21 +52,40 @@ __device__ __forceinline__ void record_error(DevCounters* c, int code, int stage
 // The z sweep (K = 2) visits cells x fastest, then y inside chunks of YC rows,
 // then z, then the chunk: the 2M+1 source planes it reads then span a few MB
 // of L2 instead of 5 full planes (~120 MB at 256^3, re-read from HBM).
-template <int M, int K, int NV, int YC>
+// G3: the (y, z) row comes from blockIdx.y / .z (y inside the chunk and z in
+// blockIdx.y, the chunk in blockIdx.z: the same traversal) and only x and the
+// dof from the thread index, so no thread divides by a run-time extent (the
+// index arithmetic was more than half of the z sweep's instructions).
+template <int M, int K, int NV, int YC, bool G3 = false>
 __global__ void __launch_bounds__(256) k_weno(const double* __restrict__ src, double* __restrict__ dst,
                                               const Box R, const long long sy, const long long sz,
                                               const long long astride, const __grid_constant__ DevTables T) {
   constexpr int N = M + 1;
   constexpr int NT = ipow_c(N, K);
   constexpr int NIN = NV * NT;
+  const unsigned ex = (unsigned)R.ext[0], ey = (unsigned)R.ext[1], ez = (unsigned)R.ext[2];
+  unsigned x, y, z;
+  int inner;
+  if constexpr (G3) {
+    const unsigned gx = blockIdx.x * blockDim.x + threadIdx.x;
+    x = gx / NIN;
+    inner = (int)(gx - x * NIN);
+    if (x >= ex) return;
+    if constexpr (YC > 1) {
+      z = blockIdx.y / YC;
+      y = blockIdx.z * YC + (blockIdx.y - z * YC);
+      if (y >= ey) return;
+    } else {
+      y = blockIdx.y;
+      z = blockIdx.z;
+    }
+  } else {
   // 32-bit index decomposition (the launcher guarantees < 2^32 threads)
   const unsigned gid = blockIdx.x * blockDim.x + threadIdx.x;
   const unsigned r = gid / NIN;
-  const int inner = (int)(gid - r * NIN);
-  const unsigned ex = (unsigned)R.ext[0], ey = (unsigned)R.ext[1], ez = (unsigned)R.ext[2];
+  inner = (int)(gid - r * NIN);
   const unsigned ty = r / ex;
-  const unsigned x = r - ty * ex;
-  unsigned y, z;
+  x = r - ty * ex;
   if constexpr (YC > 1) {
     const unsigned t2 = ty / YC;
     const unsigned yb = t2 / ez;
@@ -77,6 +96,7 @@ __global__ void __launch_bounds__(256) k_weno(const double* __restrict__ src, do
     z = ty / ey;
     y = ty - z * ey;
     if (z >= ez) return;
+  }
   }
   const long long cell = (long long)(R.lo[0] + (int)x) + (long long)(R.lo[1] + (int)y) * sy +
                          (long long)(R.lo[2] + (int)z) * sz;
@@ -896,6 +916,20 @@ static void weno_sweep_nv(const KCtx& k, const double* src, double* dst, const B
   if (threads >= (1LL << 32) - 256) return;   // guarded at ader_create (32-bit thread indexing)
   const unsigned g = grid_for(threads, 256);
   count_launch(k);
+  // ADER_WENO_G3=0: linear thread index decomposed by division (A/B; the same dofs)
+  static const bool g3 = !(std::getenv("ADER_WENO_G3") && std::getenv("ADER_WENO_G3")[0] == '0');
+  const long long gy = (YC > 1) ? (long long)YC * R.ext[2] : R.ext[1];
+  const long long gz = (YC > 1) ? (R.ext[1] + YC - 1) / YC : R.ext[2];
+  if (g3 && gy <= 65535 && gz <= 65535) {
+    const dim3 grid(grid_for((long long)R.ext[0] * k.NV * per, 256), (unsigned)gy, (unsigned)gz);
+    switch (k.NV) {
+      case 4: k_weno<M, K, 4, YC, true><<<grid, 256, 0, k.stream>>>(src, dst, R, k.sy, k.sz, astride, k.tab); break;
+      case 5: k_weno<M, K, 5, YC, true><<<grid, 256, 0, k.stream>>>(src, dst, R, k.sy, k.sz, astride, k.tab); break;
+      case 9: k_weno<M, K, 9, YC, true><<<grid, 256, 0, k.stream>>>(src, dst, R, k.sy, k.sz, astride, k.tab); break;
+      default: break;
+    }
+    return;
+  }
   switch (k.NV) {
     case 4: k_weno<M, K, 4, YC><<<g, 256, 0, k.stream>>>(src, dst, R, k.sy, k.sz, astride, k.tab); break;
     case 5: k_weno<M, K, 5, YC><<<g, 256, 0, k.stream>>>(src, dst, R, k.sy, k.sz, astride, k.tab); break;
